@@ -1,0 +1,343 @@
+#!/usr/bin/env python
+"""Throughput benchmark of the cDMD hot path on B200 (BASELINE.json metric).
+
+metric : "1080p frames/sec (sketch+modes+fg mask) at 1/2/4/8 B200; % of HBM roofline"
+step   : one pass of the whole hot path over one batch:
+         cdmd_sketch -> all_reduce(Y) -> cdmd_fit -> cdmd_modes -> cdmd_foreground
+workload (N=1): c4_1080p_sparse = 1920x1080, m = 500 frames, sparse C (s = n/ln n),
+         p = 2000, k = 50, K = 10, tau = 25, dynamic background (north_star (3)).
+value  : frames of the batch / device time per step (max over ranks), inputs resident
+         in HBM; X (1.04 GB) is larger than L2, so no flush is needed between steps.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config NAME] [--bg dynamic|static]
+    python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N
+    python bench.py --impl reference     # the CPU oracle (test infrastructure) as the baseline arm
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FALLBACK_HBM_GBS = 6650.0   # B200_PROFILING.md fallback, used only without MEASURED_PEAKS.json
+METRIC = "1080p frames/sec (sketch+modes+fg mask) at 1/2/4/8 B200; % of HBM roofline"
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured"
+    return FALLBACK_HBM_GBS, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi samples of SM clock and throttle reasons during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu):
+        self.gpu, self.rows, self.proc = gpu, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        rows = [r for r in self.rows if len(r) == 6 and r[0].isdigit()]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[2 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(float(r[0]) for r in rows),
+                "sm_max_mhz": max(float(r[1]) for r in rows), "reasons": reasons, "samples": len(rows)}
+
+
+def sector_bytes_sparse(n_local, pix0, n_total, p, seed, m):
+    """Algorithmic bytes of the sparse sketch: distinct 32-B sectors of X gathered per
+    frame x m frames (the sector is the HBM access granule) + the p x m int32 Y."""
+    from oracle.sensing import default_s, sparse_rows   # counting only; not on the timed path
+    rows = sparse_rows(n_total, p, default_s(n_total), seed)
+    pos = np.concatenate([r[0] for r in rows])
+    pos = pos[(pos >= pix0) & (pos < pix0 + n_local)] - pix0
+    return int(np.unique(pos // 32).size) * 32 * m + 4 * p * m
+
+
+def run_reference(args):
+    """The oracle (test infrastructure) timed as it stands on this host's cores, on a
+    bounded sample of the same workload: the full sketch + fit, then modes + dynamic
+    background + mask on 1/`frac` of the pixels, extrapolated to the whole frame."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import cdmd as OD
+    from oracle import sensing as OS
+    from synth.scene import config_by_name, video_for
+    cfg = config_by_name(args.config)
+    X = video_for(cfg)
+    m, n = X.shape
+    kind = {"spixel": 0, "sparse": 1, "rademacher": 2, "gaussian": 3}[cfg.kind]
+    frac = args.ref_frac
+    rng = np.random.default_rng(0)
+    pix = np.sort(rng.choice(n, n // frac, replace=False))
+    times = []
+    for _ in range(max(1, args.steps if args.steps <= 3 else 1)):
+        t0 = time.perf_counter()
+        if kind in (0, 1):
+            Y = OS.sketch(X, kind, cfg.p, cfg.sensing_seed)
+            t_sk = time.perf_counter() - t0
+        else:  # dense sketches: a sample of rows, extrapolated
+            rows = np.arange(0, cfg.p, max(1, cfg.p // 16))
+            OS.sketch(X, kind, cfg.p, cfg.sensing_seed, rows=rows)
+            t_sk = (time.perf_counter() - t0) * cfg.p / len(rows)
+            Y = None
+        t1 = time.perf_counter()
+        if Y is None:
+            raise SystemExit("reference arm: dense-C configs need the full oracle sketch (not sampled here)")
+        model = OD.fit(Y, cfg.k, cfg.K)
+        t_fit = time.perf_counter() - t1
+        t2 = time.perf_counter()
+        Xs = X[:, pix]
+        Phi = OD.modes(Xs, model["M"])
+        L = OD.background_dynamic(Phi, model) if args.bg == "dynamic" else OD.background_static(Phi, model)
+        OD.mask(Xs, L, cfg.tau)
+        t_px = (time.perf_counter() - t2) * frac
+        times.append(t_sk + t_fit + t_px)
+    t = min(times)
+    cores = len(os.sched_getaffinity(0))
+    val = m / t
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": "frames/s", "n_gpus": args.gpus,
+        "steps": len(times), "warmup": 0, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg.name, "video": f"{cfg.width}x{cfg.height}x{cfg.m}", "sensing": cfg.kind,
+                   "p": cfg.p, "k": cfg.k, "K": cfg.K, "tau": cfg.tau, "background": args.bg},
+        "cpu_baseline": {"value": val, "unit": "frames/s", "cores": cores, "kind": "oracle",
+                         "sample": f"full sketch+fit; modes+background+mask on 1/{frac} of the pixels "
+                                   f"({len(pix)} px), extrapolated x{frac}"},
+        "e2e": {"value": val, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="cdmd", choices=["cdmd", "reference"])
+    ap.add_argument("--config", default="c4_1080p_sparse")
+    ap.add_argument("--bg", default="dynamic", choices=["dynamic", "static"])
+    ap.add_argument("--ref-frac", type=int, default=32)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1512_04205_b200 import cdmd as C
+    from paper_1512_04205_b200.dist import slab
+    from synth.scene import config_by_name, video_for
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = config_by_name(args.config)
+    n, m = cfg.n, cfg.m
+    pix0, nl = slab(n, world, rank)
+    X_host = video_for(cfg, pix0=pix0, n_local=nl)
+    ld = ((nl + 15) // 16) * 16
+    Xd = torch.zeros((m, ld), dtype=torch.uint8, device="cuda")
+    Xd[:, :nl] = torch.from_numpy(X_host).cuda()
+    H = C.Handle(local)
+    P = C.Pipeline(H, n, nl, m, cfg.kind, cfg.p, cfg.k, cfg.K, seed=cfg.sensing_seed, pix0=pix0)
+    mode = C.BG_DYNAMIC if args.bg == "dynamic" else C.BG_STATIC
+    stream = torch.cuda.current_stream()
+    ev = {s: [] for s in ("sketch", "allreduce", "fit", "modes", "foreground")}
+
+    def step(record=False):
+        marks = [torch.cuda.Event(enable_timing=True) for _ in range(6)] if record else None
+        if record:
+            marks[0].record(stream)
+        P.sketch(Xd)
+        if record:
+            marks[1].record(stream)
+        if world > 1:
+            dist.all_reduce(P.Y, op=dist.ReduceOp.SUM)
+        if record:
+            marks[2].record(stream)
+        P.fit()
+        if record:
+            marks[3].record(stream)
+        P.modes(Xd)
+        if record:
+            marks[4].record(stream)
+        P.foreground(Xd, cfg.tau, mode)
+        if record:
+            marks[5].record(stream)
+            for i, s in enumerate(ev):
+                ev[s].append((marks[i], marks[i + 1]))
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        start.record(stream)
+        for _ in range(args.steps):
+            step(record=True)
+        stop.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = start.elapsed_time(stop) / args.steps
+    stage_ms = {s: sum(a.elapsed_time(b) for a, b in v) / len(v) for s, v in ev.items()}
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = m / (ms_max * 1e-3)
+
+    # roofline of the dominant kernel (HBM-bound passes; algorithmic bytes per launch)
+    hbm, hbm_src = peaks()
+    ke, nc = P.model.k_eff, P.model.n_coef
+    algo = {
+        "modes": nl * (m - 1) + 4 * nl * ke,
+        "foreground": nl * m + 4 * m * ((nl + 31) // 32) + 4 * nl * nc,
+    }
+    if cfg.kind in ("sparse", "spixel"):
+        algo["sketch"] = (sector_bytes_sparse(nl, pix0, n, cfg.p, cfg.sensing_seed, m)
+                          if cfg.kind == "sparse" else 32 * cfg.p * m + 4 * cfg.p * m)
+    cand = {s: stage_ms[s] for s in algo}
+    dom = max(cand, key=cand.get)
+    achieved = algo[dom] / (stage_ms[dom] * 1e-3) / 1e9
+    roof = {"kernel": {"sketch": "sketch_sparse_kernel", "modes": "cdmd_modes",
+                       "foreground": "foreground_dynamic_kernel" if mode else "foreground_static_kernel"}[dom],
+            "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
+            "frac": round(achieved / hbm, 4), "traffic": None, "peak_source": hbm_src,
+            "algorithmic_bytes_per_launch": algo[dom], "launch_ms": round(stage_ms[dom], 4)}
+
+    # e2e: host (pinned) video in, mask out, through the same public calls
+    e2e = None
+    if not args.no_e2e:
+        Xh = torch.from_numpy(np.ascontiguousarray(np.pad(X_host, ((0, 0), (0, ld - nl))))).pin_memory()
+        mh = torch.empty(P.mask.shape, dtype=P.mask.dtype).pin_memory()
+        e_steps = max(3, min(10, args.steps))
+
+        def e2e_step():
+            Xd.copy_(Xh, non_blocking=True)
+            step()
+            mh.copy_(P.mask, non_blocking=True)
+        e2e_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(e_steps):
+            e2e_step()
+        b.record(stream)
+        torch.cuda.synchronize()
+        te = torch.tensor([a.elapsed_time(b) / e_steps], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": m / (float(te.item()) * 1e-3), "unit": "frames/s",
+               "h2d_bytes_per_step": int(Xh.numel()) * world, "d2h_bytes_per_step": int(mh.numel() * 4) * world}
+
+    if rank == 0:
+        cpu = None
+        if not args.no_cpu_baseline and world == 1:
+            cpu = cpu_baseline(cfg, X_host, args)
+        launches_per_step = {"sparse": 2, "spixel": 2}.get(cfg.kind, 1) + 6 + 1 + 1
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": "frames/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max, 4),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic",
+            "config": {"workload": cfg.name, "video": f"{cfg.width}x{cfg.height}x{m}", "sensing": cfg.kind,
+                       "p": cfg.p, "k": cfg.k, "K": cfg.K, "tau": cfg.tau, "background": args.bg,
+                       "parallelism": f"pixel-rows x{world}", "l2": "inputs larger than L2 (X = %.2f GB)" % (n * m / 1e9),
+                       "k_eff": ke, "K_eff": P.model.K_eff, "n_coef": nc},
+            "stage_ms": {s: round(v, 4) for s, v in stage_ms.items()},
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches_per_step * args.steps,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def cpu_baseline(cfg, X, args):
+    """The oracle as it stands, on a bounded sample (about 10-30 s of CPU work)."""
+    from oracle import cdmd as OD
+    from oracle import sensing as OS
+    m, n = X.shape
+    frac = args.ref_frac
+    rng = np.random.default_rng(0)
+    pix = np.sort(rng.choice(n, n // frac, replace=False))
+    kind = {"spixel": 0, "sparse": 1, "rademacher": 2, "gaussian": 3}[cfg.kind]
+    t0 = time.perf_counter()
+    Y = OS.sketch(X, kind, cfg.p, cfg.sensing_seed)
+    t_sk = time.perf_counter() - t0
+    t1 = time.perf_counter()
+    model = OD.fit(Y, cfg.k, cfg.K)
+    t_fit = time.perf_counter() - t1
+    t2 = time.perf_counter()
+    Xs = X[:, pix]
+    Phi = OD.modes(Xs, model["M"])
+    L = OD.background_dynamic(Phi, model) if args.bg == "dynamic" else OD.background_static(Phi, model)
+    OD.mask(Xs, L, cfg.tau)
+    t_px = (time.perf_counter() - t2) * frac
+    total = t_sk + t_fit + t_px
+    return {"value": round(m / total, 3), "unit": "frames/s", "cores": len(os.sched_getaffinity(0)),
+            "kind": "oracle",
+            "sample": f"{cfg.name}: full sketch ({t_sk:.1f}s) + fit ({t_fit:.1f}s); modes+background+mask "
+                      f"on 1/{frac} of the pixels ({len(pix)} px, {t_px / frac:.1f}s) extrapolated x{frac}"}
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,208 @@
+/*
+ * cdmd.h — C ABI of libcdmd, the B200 (sm_100a) hot path of compressed dynamic
+ * mode decomposition (cDMD, Erichson, Brunton & Kutz, arXiv 1512.04205).
+ *
+ * Citations "P:n" are lines of the paper's LaTeX source; "Alg. 1" is
+ * its Algorithm 1.  Readings of silent/garbled passages: DESIGN.md §4.
+ *
+ * Conventions shared by every entry point
+ *  - Pointers are DEVICE pointers unless the argument says "host".
+ *  - The CALLER owns every buffer (video, sketch, model, modes, mask, workspace);
+ *    the library keeps only immutable per-handle state (cuBLAS/cuSOLVER handles,
+ *    the Gaussian table) and never allocates on the hot path.
+ *  - Calls are asynchronous on the given stream, except cdmd_fit (it reads the
+ *    solver status and the model sizes back to the host once) and cdmd_create.
+ *  - Validation happens on the host before any launch; an invalid call returns a
+ *    status other than CDMD_OK and launches nothing.
+ *  - One handle per device per host thread.  Entry points are reentrant.
+ *
+ * Data layouts
+ *  - Video X (D of Alg. 1): uint8, FRAME-MAJOR, X[t*ld + j] is pixel
+ *    (pix0 + j) of frame t+1 (a frame is the paper's column x_t).  A rank
+ *    of a pixel-sharded run holds the slab of global pixels [pix0, pix0+n_local).
+ *    X must be 16-byte aligned, ld >= n_local and ld % 16 == 0, pix0 % 128 == 0.
+ *  - Sketch Y_full = C D: p x m, column-major, Y[r + t*ldy]; int32 for
+ *    CDMD_SPIXEL / CDMD_SPARSE / CDMD_RADEMACHER (exact), float for CDMD_GAUSSIAN.
+ *    Y = first m-1 columns, Y' = last m-1 columns (Eq. FullData, reading R2).
+ *  - Modes Phi (Eq. cDMDModes): complex n x k with columns in conjugate
+ *    pairs, stored FOLDED as k_eff real float columns, Phi[j + c*ldphi]:
+ *    real eigenvalue  -> column c = phi_c;
+ *    pair (c, c+1)    -> columns c, c+1 = Re phi_c, Im phi_c  (phi_{c+1} = conj phi_c).
+ *  - Mask (Eq. thres): bit (j % 32) of uint32 word mask[t*ldw + j/32]
+ *    is 1 iff |x_jt - L_jt| > tau.
+ */
+#ifndef CDMD_H
+#define CDMD_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define CDMD_API __attribute__((visibility("default")))
+#else
+#define CDMD_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* cdmd_stream;       /* == cudaStream_t; NULL = legacy default stream */
+typedef struct cdmd_handle_s* cdmd_handle;
+
+typedef enum {
+  CDMD_OK = 0,
+  CDMD_ERR_ARG = 1,        /* null / misaligned pointer, bad layout or enum      */
+  CDMD_ERR_RANGE = 2,      /* p, s, m, k, K, tau out of range                    */
+  CDMD_ERR_NUMERIC = 3,    /* solver non-convergence, every sigma dropped, ...   */
+  CDMD_ERR_CUDA = 4,       /* CUDA runtime / cuBLAS / cuSOLVER error             */
+  CDMD_ERR_WORKSPACE = 5,  /* workspace or model buffer too small                */
+  CDMD_ERR_UNSUPPORTED = 6 /* not built for this device (needs sm_100a)          */
+} cdmd_status;
+
+/* Measurement matrix C in R^{p x n} (Alg. 1 step 2, P:334 read as p x n). */
+typedef enum {
+  CDMD_SPIXEL = 0,     /* C = R, p rows of I_n without replacement            */
+  CDMD_SPARSE = 1,     /* +-1 w.p. 1/(2s) each, 0 otherwise                    */
+  CDMD_RADEMACHER = 2, /* +-1 (Bernoulli; the s = 1 case of P:386-393)              */
+  CDMD_GAUSSIAN = 3    /* N(0,1) rounded to bf16 (reading R7)                       */
+} cdmd_measure;
+
+typedef enum {
+  CDMD_BG_STATIC = 0,  /* x_BG = Re(Phi beta), one value per pixel            */
+  CDMD_BG_DYNAMIC = 1  /* L_jt = Re sum_{p in S} beta_p phi_jp lambda_p^{t-1} */
+} cdmd_bg_mode;
+
+typedef struct {
+  const uint8_t* X;   /* device, frame-major, see "Data layouts"                  */
+  int64_t n_total;    /* n: pixels per frame of the whole video            */
+  int64_t pix0;       /* first global pixel of this slab (multiple of 128)        */
+  int64_t n_local;    /* pixels in this slab                                      */
+  int64_t m;          /* frames, m >= 2                                    */
+  int64_t ld;         /* bytes between frames, >= n_local, multiple of 16         */
+} cdmd_video;
+
+typedef struct {
+  int32_t kind;       /* cdmd_measure                                             */
+  int64_t p;          /* measurements, 1 <= p <= n_total                  */
+  double s;           /* sparse rate, > 1; <= 0 selects n_total / ln(n_total)     */
+  uint64_t seed;      /* Philox4x32-10 key = (seed & 0xffffffff, seed >> 32)       */
+} cdmd_sensing;
+
+/* The fitted model (Alg. 1 outputs Phi, b, V of P:331 in factored form).
+ * Bind it to ONE caller-allocated device buffer with cdmd_model_bind(); the
+ * pointers below then point into that buffer.  Host fields are written by
+ * cdmd_fit before it returns. */
+typedef struct {
+  /* capacities, set by cdmd_model_bind */
+  int32_t k, K;        /* target rank and OMP sparsity             */
+  int32_t limbs;       /* int8 limbs of the fixed-point M used by cdmd_modes       */
+  int32_t kpad;        /* k rounded up to the MMA column block                     */
+  int64_t m, mpad;     /* frames; m - 1 rounded up to 128                          */
+  /* device arrays */
+  double* lambda;      /* [2k]   eigenvalues lambda_j (re, im)         */
+  double* omega;       /* [2k]   omega_j = log(lambda_j)/dt                */
+  int32_t* pair;       /* [k]    0 real, +1 first / -1 second member of a pair     */
+  double* sigma;       /* [k]    singular values of Y                  */
+  double* Mfold;       /* [(m-1) k] folded M = V S^-1 W, column-major, ld m-1      */
+  double* beta;        /* [2K]   OMP amplitudes (re, im) on the support    */
+  int32_t* support;    /* [K]    selected modes, in selection order                */
+  int8_t* Mq;          /* [kpad*limbs][mpad] fixed-point limbs of Mfold            */
+  double* Mq_scale;    /* [kpad] per-column dequantisation scales                  */
+  float* coef;         /* [2K][m] background coefficients per used Phi column      */
+  int32_t* coef_col;   /* [2K]   which folded Phi column each coef row multiplies  */
+  int32_t* dev_info;   /* [8]    device-side status words                           */
+  /* host outputs of cdmd_fit */
+  int32_t k_eff;       /* singular values kept (sigma_j > 1e-6 sigma_1; reading R10) */
+  int32_t K_eff;       /* OMP atoms selected (<= K)                                 */
+  int32_t n_coef;      /* rows of coef in use (<= 2K)                               */
+  int32_t info;        /* 0, or the failing solver's info                           */
+  double dt;           /* frame interval used for omega (reading R15: 1)            */
+} cdmd_model;
+
+/* ---------------------------------------------------------------- lifecycle */
+CDMD_API cdmd_status cdmd_create(int device, cdmd_handle* out);
+CDMD_API void cdmd_destroy(cdmd_handle h);
+CDMD_API const char* cdmd_status_str(cdmd_status s);
+CDMD_API const char* cdmd_version(void);
+
+/* ------------------------------------------------------------------- sketch
+ * Y_full = C D (Alg. 1 step 3; Eq. P:286-288), C generated on the fly from
+ * Philox4x32-10 and never materialised (single pixel = Feistel
+ * permutation rows; sparse = geometric-gap rows; Rademacher = bits; Gaussian =
+ * bf16 inverse-CDF table).  Columns of C are indexed by the GLOBAL pixel, so the
+ * per-slab partial sketches of a pixel-sharded run SUM to the full sketch
+ * (integer kinds bit-exactly).  Y (p x m, ldy >= p) is overwritten.
+ * ws: device workspace of at least cdmd_sketch_workspace_bytes() bytes, 256-B
+ * aligned (index lists of C).  Errors: CDMD_ERR_RANGE if p < 1 or p > n_total,
+ * s <= 1 (sparse), m < 2; CDMD_ERR_ARG on layout violations; CDMD_ERR_WORKSPACE. */
+CDMD_API size_t cdmd_sketch_workspace_bytes(const cdmd_video* v, const cdmd_sensing* c);
+CDMD_API cdmd_status cdmd_sketch(cdmd_handle h, const cdmd_video* v, const cdmd_sensing* c,
+                        void* Y, int64_t ldy, void* ws, size_t ws_bytes, cdmd_stream st);
+
+/* ---------------------------------------------------------------------- fit
+ * The small solve on Y_full (replicated on every rank after the all-reduce):
+ * Alg. 1 step 4 truncated SVD (computed from the Gram matrix Y^T Y, the
+ * method of snapshots), step 6 A~ = U* Y' V S^-1, step 7 eig (
+ * cuSOLVER), M = V S^-1 W (P:346 without X'), Remark 3 OMP on Phi_Y = Y' M
+ * against y_1 (Gram form of Rubinstein et al.), omega =
+ * log(lambda)/dt, the background coefficient table, and the
+ * fixed-point limbs of M for cdmd_modes.  BLOCKING: returns after the model is
+ * complete.  Errors: CDMD_ERR_RANGE if k < 1, k > min(p, m-1), K < 1 or
+ * K > k; CDMD_ERR_NUMERIC if the eigensolvers fail or every sigma is dropped
+ * (model->info holds the solver info). */
+CDMD_API size_t cdmd_model_bytes(int k, int K, int64_t m);
+CDMD_API cdmd_status cdmd_model_bind(cdmd_model* model, void* dev_buf, size_t bytes, int k, int K, int64_t m);
+CDMD_API size_t cdmd_fit_workspace_bytes(cdmd_handle h, int64_t p, int64_t m, int k);
+CDMD_API cdmd_status cdmd_fit(cdmd_handle h, const void* Y, int64_t ldy, int32_t kind, int64_t p, int64_t m,
+                     int k, int K, double dt, cdmd_model* model, void* ws, size_t ws_bytes,
+                     cdmd_stream st);
+
+/* -------------------------------------------------------------------- modes
+ * Phi = X' V S^-1 W = X' M (Alg. 1 step 8, Eq. cDMDModes), X' = frames
+ * 2..m of the slab; written folded (see "Data layouts"), n_local x
+ * k_eff, ldphi >= n_local.  tcgen05 int8 tensor cores on sm_100a: uint8 pixels
+ * times int8 limbs of M, exact int32 accumulation, fp32 output. */
+CDMD_API cdmd_status cdmd_modes(cdmd_handle h, const cdmd_video* v, const cdmd_model* model,
+                       float* Phi, int64_t ldphi, cdmd_stream st);
+
+/* --------------------------------------------------------------- background
+ * Background frames t0+1 .. t0+nt of the slab, frame-major L[t*ldl + j]:
+ * STATIC  L_j  = Re sum_{p in S} beta_p phi_jp              (every t)
+ * DYNAMIC L_jt = Re sum_{p in S} beta_p phi_jp lambda_p^(t-1) (Eq. DMDTerms)
+ * Phi as written by cdmd_modes.  Only for inspection: cdmd_foreground fuses it. */
+CDMD_API cdmd_status cdmd_background(cdmd_handle h, const float* Phi, int64_t ldphi, int64_t n_local,
+                            const cdmd_model* model, int32_t mode, int64_t t0, int64_t nt,
+                            float* L, int64_t ldl, cdmd_stream st);
+
+/* --------------------------------------------------------------- foreground
+ * One pass over X: background (as cdmd_background), residual |x_jt - L_jt| and
+ * threshold tau (Eq. thres, strict >) for all m frames, bit-packed.
+ * mask: ldw >= ceil(n_local/32) uint32 words per frame.  Errors: CDMD_ERR_RANGE
+ * if tau <= 0. */
+CDMD_API cdmd_status cdmd_foreground(cdmd_handle h, const cdmd_video* v, const cdmd_model* model,
+                            const float* Phi, int64_t ldphi, int32_t mode, float tau,
+                            uint32_t* mask, int64_t ldw, cdmd_stream st);
+
+/* ------------------------------------------------ test hooks (same contract)
+ * Export what the device generates so tests can compare it bit for bit with the
+ * oracle's definitions. */
+/* out: device uint32 [4*count]; ctr: device uint32 [4*count]. */
+CDMD_API cdmd_status cdmd_philox(const uint32_t* ctr, uint32_t k0, uint32_t k1, uint32_t* out,
+                        int64_t count, cdmd_stream st);
+/* out: device uint16 [65536] bf16 bit patterns of the Gaussian table. */
+CDMD_API cdmd_status cdmd_gaussian_table(cdmd_handle h, uint16_t* out, cdmd_stream st);
+/* Single pixel: rows (device int32 [p]).  Sparse: device int32 [p*cap] ELL of
+ * (pos << 1 | negative) and int32 counts [p]; cap from cdmd_sparse_cap(). */
+CDMD_API int64_t cdmd_sparse_cap(int64_t n_total, int64_t p, double s);
+CDMD_API cdmd_status cdmd_sensing_rows(cdmd_handle h, int64_t n_total, const cdmd_sensing* c,
+                              int32_t* rows_or_ell, int32_t* counts, cdmd_stream st);
+/* Modes through the CUDA-core (dp4a) reference kernel: bit-identical to
+ * cdmd_modes (both accumulate exactly in int32). */
+CDMD_API cdmd_status cdmd_modes_simt(cdmd_handle h, const cdmd_video* v, const cdmd_model* model,
+                            float* Phi, int64_t ldphi, cdmd_stream st);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CDMD_H */

@@ -1,0 +1,305 @@
+"""Thin Python binding of libcdmd (include/cdmd.h) — argument marshalling only.
+
+Every step of the hot path runs in libcdmd's CUDA kernels (and cuSOLVER for the
+small eigen-solves of cdmd_fit).  PyTorch provides device memory and streams.
+There is no CPU fallback: importing this module on a machine without the built
+library raises, and every call checks the returned status.
+
+Names follow the C ABI: cdmd_sketch, cdmd_fit, cdmd_modes, cdmd_background,
+cdmd_foreground (+ test hooks).  ``Pipeline`` strings them together with
+caller-owned torch buffers (the same calls bench.py times).
+"""
+
+import ctypes
+import math
+import os
+
+import torch
+
+from .build import LIB
+
+SPIXEL, SPARSE, RADEMACHER, GAUSSIAN = 0, 1, 2, 3
+KINDS = {"spixel": SPIXEL, "sparse": SPARSE, "rademacher": RADEMACHER, "gaussian": GAUSSIAN}
+BG_STATIC, BG_DYNAMIC = 0, 1
+STATUS = {0: "ok", 1: "invalid argument", 2: "argument out of range", 3: "numerical failure",
+          4: "CUDA error", 5: "workspace too small", 6: "unsupported device (needs sm_100a)"}
+
+
+class CdmdError(RuntimeError):
+    def __init__(self, where, code):
+        super().__init__(f"{where}: {STATUS.get(code, code)} (status {code})")
+        self.code = code
+
+
+class Video(ctypes.Structure):
+    _fields_ = [("X", ctypes.c_void_p), ("n_total", ctypes.c_int64), ("pix0", ctypes.c_int64),
+                ("n_local", ctypes.c_int64), ("m", ctypes.c_int64), ("ld", ctypes.c_int64)]
+
+
+class Sensing(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("p", ctypes.c_int64), ("s", ctypes.c_double),
+                ("seed", ctypes.c_uint64)]
+
+
+_P = ctypes.c_void_p
+
+
+class Model(ctypes.Structure):
+    _fields_ = [("k", ctypes.c_int32), ("K", ctypes.c_int32), ("limbs", ctypes.c_int32),
+                ("kpad", ctypes.c_int32), ("m", ctypes.c_int64), ("mpad", ctypes.c_int64),
+                ("lambda_", _P), ("omega", _P), ("pair", _P), ("sigma", _P), ("Mfold", _P),
+                ("beta", _P), ("support", _P), ("Mq", _P), ("Mq_scale", _P), ("coef", _P),
+                ("coef_col", _P), ("dev_info", _P),
+                ("k_eff", ctypes.c_int32), ("K_eff", ctypes.c_int32), ("n_coef", ctypes.c_int32),
+                ("info", ctypes.c_int32), ("dt", ctypes.c_double)]
+
+
+SYMBOLS = ["cdmd_create", "cdmd_destroy", "cdmd_status_str", "cdmd_version",
+           "cdmd_sketch_workspace_bytes", "cdmd_sketch", "cdmd_model_bytes", "cdmd_model_bind",
+           "cdmd_fit_workspace_bytes", "cdmd_fit", "cdmd_modes", "cdmd_background",
+           "cdmd_foreground", "cdmd_philox", "cdmd_gaussian_table", "cdmd_sparse_cap",
+           "cdmd_sensing_rows", "cdmd_modes_simt"]
+
+
+def _load():
+    if not os.path.exists(LIB):
+        raise ImportError(f"libcdmd.so not built ({LIB}); run python -m paper_1512_04205_b200.build")
+    lib = ctypes.CDLL(LIB)
+    V, S, M = ctypes.POINTER(Video), ctypes.POINTER(Sensing), ctypes.POINTER(Model)
+    i32, i64, sz, dbl, vp = ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t, ctypes.c_double, ctypes.c_void_p
+    sig = {
+        "cdmd_create": (i32, [ctypes.c_int, ctypes.POINTER(vp)]),
+        "cdmd_destroy": (None, [vp]),
+        "cdmd_status_str": (ctypes.c_char_p, [i32]),
+        "cdmd_version": (ctypes.c_char_p, []),
+        "cdmd_sketch_workspace_bytes": (sz, [V, S]),
+        "cdmd_sketch": (i32, [vp, V, S, vp, i64, vp, sz, vp]),
+        "cdmd_model_bytes": (sz, [ctypes.c_int, ctypes.c_int, i64]),
+        "cdmd_model_bind": (i32, [M, vp, sz, ctypes.c_int, ctypes.c_int, i64]),
+        "cdmd_fit_workspace_bytes": (sz, [vp, i64, i64, ctypes.c_int]),
+        "cdmd_fit": (i32, [vp, vp, i64, i32, i64, i64, ctypes.c_int, ctypes.c_int, dbl, M, vp, sz, vp]),
+        "cdmd_modes": (i32, [vp, V, M, vp, i64, vp]),
+        "cdmd_modes_simt": (i32, [vp, V, M, vp, i64, vp]),
+        "cdmd_background": (i32, [vp, vp, i64, i64, M, i32, i64, i64, vp, i64, vp]),
+        "cdmd_foreground": (i32, [vp, V, M, vp, i64, i32, ctypes.c_float, vp, i64, vp]),
+        "cdmd_philox": (i32, [vp, ctypes.c_uint32, ctypes.c_uint32, vp, i64, vp]),
+        "cdmd_gaussian_table": (i32, [vp, vp, vp]),
+        "cdmd_sparse_cap": (i64, [i64, i64, dbl]),
+        "cdmd_sensing_rows": (i32, [vp, i64, S, vp, vp, vp]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    return lib
+
+
+_lib = _load()
+
+
+def lib():
+    return _lib
+
+
+def _check(where, code):
+    if code != 0:
+        raise CdmdError(where, code)
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)
+
+
+class Handle:
+    """cdmd_create / cdmd_destroy."""
+
+    def __init__(self, device=0):
+        h = ctypes.c_void_p()
+        _check("cdmd_create", _lib.cdmd_create(int(device), ctypes.byref(h)))
+        self.h = h
+        self.device = device
+
+    def __del__(self):
+        if getattr(self, "h", None) is not None and _lib is not None:
+            _lib.cdmd_destroy(self.h)
+            self.h = None
+
+
+def video(X, n_total=None, pix0=0, n_local=None):
+    """cdmd_video over a uint8 CUDA tensor X of shape (m, ld) (frame-major)."""
+    assert X.dtype == torch.uint8 and X.is_cuda and X.dim() == 2 and X.stride(1) == 1
+    m = X.shape[0]
+    n_local = X.shape[1] if n_local is None else n_local
+    n_total = n_local if n_total is None else n_total
+    return Video(X.data_ptr(), n_total, pix0, n_local, m, X.stride(0))
+
+
+def sensing(kind, p, s=0.0, seed=0):
+    return Sensing(KINDS[kind] if isinstance(kind, str) else int(kind), int(p), float(s or 0.0), int(seed))
+
+
+def _empty_bytes(n, device):
+    return torch.empty(max(int(n), 256), dtype=torch.uint8, device=device)
+
+
+# ------------------------------------------------------------------ entry points
+def cdmd_sketch_workspace_bytes(v, c):
+    return _lib.cdmd_sketch_workspace_bytes(ctypes.byref(v), ctypes.byref(c))
+
+
+def cdmd_sketch(h, v, c, Y, ws, stream=None):
+    """Y: (m, ldy) CUDA tensor viewed column-major p x m (Y[t, r] = Y_full[r, t])."""
+    _check("cdmd_sketch", _lib.cdmd_sketch(h.h, ctypes.byref(v), ctypes.byref(c), _ptr(Y), Y.stride(0),
+                                           _ptr(ws), ws.numel() * ws.element_size(), _stream(stream)))
+
+
+def cdmd_model_bytes(k, K, m):
+    return _lib.cdmd_model_bytes(k, K, m)
+
+
+def cdmd_model_bind(buf, k, K, m):
+    M = Model()
+    _check("cdmd_model_bind", _lib.cdmd_model_bind(ctypes.byref(M), _ptr(buf), buf.numel(), k, K, m))
+    M._buf = buf
+    return M
+
+
+def cdmd_fit_workspace_bytes(h, p, m, k):
+    return _lib.cdmd_fit_workspace_bytes(h.h, p, m, k)
+
+
+def cdmd_fit(h, Y, kind, p, m, k, K, model, ws, dt=1.0, stream=None):
+    kind = KINDS[kind] if isinstance(kind, str) else int(kind)
+    _check("cdmd_fit", _lib.cdmd_fit(h.h, _ptr(Y), Y.stride(0), kind, p, m, k, K, dt, ctypes.byref(model),
+                                     _ptr(ws), ws.numel(), _stream(stream)))
+
+
+def cdmd_modes(h, v, model, Phi, stream=None, simt=False):
+    """Phi: (k_cols, ldphi) float32 CUDA tensor (column c of the folded modes is Phi[c])."""
+    f = _lib.cdmd_modes_simt if simt else _lib.cdmd_modes
+    _check("cdmd_modes", f(h.h, ctypes.byref(v), ctypes.byref(model), _ptr(Phi), Phi.stride(0), _stream(stream)))
+
+
+def cdmd_background(h, Phi, n_local, model, mode, t0, nt, L, stream=None):
+    _check("cdmd_background", _lib.cdmd_background(h.h, _ptr(Phi), Phi.stride(0), n_local, ctypes.byref(model),
+                                                   mode, t0, nt, _ptr(L), L.stride(0), _stream(stream)))
+
+
+def cdmd_foreground(h, v, model, Phi, mode, tau, mask, stream=None):
+    """mask: (m, ldw) int32/uint32-sized CUDA tensor of packed words."""
+    _check("cdmd_foreground", _lib.cdmd_foreground(h.h, ctypes.byref(v), ctypes.byref(model), _ptr(Phi),
+                                                   Phi.stride(0), mode, float(tau), _ptr(mask), mask.stride(0),
+                                                   _stream(stream)))
+
+
+def cdmd_philox(ctr, k0, k1, out, stream=None):
+    _check("cdmd_philox", _lib.cdmd_philox(_ptr(ctr), k0, k1, _ptr(out), ctr.numel() // 4, _stream(stream)))
+
+
+def cdmd_gaussian_table(h, out, stream=None):
+    _check("cdmd_gaussian_table", _lib.cdmd_gaussian_table(h.h, _ptr(out), _stream(stream)))
+
+
+def cdmd_sparse_cap(n_total, p, s=0.0):
+    return _lib.cdmd_sparse_cap(n_total, p, float(s or 0.0))
+
+
+def cdmd_sensing_rows(h, n_total, c, out, counts=None, stream=None):
+    _check("cdmd_sensing_rows", _lib.cdmd_sensing_rows(h.h, n_total, ctypes.byref(c), _ptr(out), _ptr(counts),
+                                                       _stream(stream)))
+
+
+# --------------------------------------------------------------- model read-back
+def model_to_host(M):
+    """Copy the model's device arrays into CPU tensors (for tests / reports)."""
+    buf = M._buf
+    base = buf.data_ptr()
+
+    def arr(ptr, count, dtype):
+        es = torch.tensor([], dtype=dtype).element_size()
+        off = ptr - base
+        return buf[off:off + count * es].view(dtype).cpu()
+
+    k, K, m, ke, Ke = M.k, M.K, M.m, M.k_eff, M.K_eff
+    lam = arr(M.lambda_, 2 * k, torch.float64).view(k, 2)[:ke]
+    om = arr(M.omega, 2 * k, torch.float64).view(k, 2)[:ke]
+    beta = arr(M.beta, 2 * K, torch.float64).view(K, 2)[:Ke]
+    return dict(
+        k_eff=ke, K_eff=Ke, n_coef=M.n_coef, info=M.info,
+        lam=torch.complex(lam[:, 0], lam[:, 1]).numpy(),
+        omega=torch.complex(om[:, 0], om[:, 1]).numpy(),
+        pair=arr(M.pair, k, torch.int32)[:ke].numpy(),
+        sigma=arr(M.sigma, k, torch.float64)[:ke].numpy(),
+        Mfold=arr(M.Mfold, (m - 1) * k, torch.float64)[:(m - 1) * ke].view(ke, m - 1).T.numpy(),
+        support=arr(M.support, K, torch.int32)[:Ke].numpy().tolist(),
+        beta=torch.complex(beta[:, 0], beta[:, 1]).numpy(),
+        coef=arr(M.coef, 2 * K * m, torch.float32)[:M.n_coef * m].view(M.n_coef, m).numpy(),
+        coef_col=arr(M.coef_col, 2 * K, torch.int32)[:M.n_coef].numpy(),
+        dev_info=arr(M.dev_info, 8, torch.int32).numpy(),
+    )
+
+
+# ---------------------------------------------------------------------- pipeline
+class Pipeline:
+    """Caller-owned buffers for one (video shape, sensing, k, K) problem, and the
+    five-call hot path sketch -> [all-reduce] -> fit -> modes -> foreground."""
+
+    def __init__(self, handle, n_total, n_local, m, kind, p, k, K, s=0.0, seed=0, pix0=0,
+                 device="cuda", dt=1.0):
+        self.h = handle
+        self.kind = KINDS[kind] if isinstance(kind, str) else int(kind)
+        self.n_total, self.n_local, self.m, self.p, self.k, self.K = n_total, n_local, m, p, k, K
+        self.pix0, self.dt = pix0, dt
+        self.c = sensing(self.kind, p, s, seed)
+        ydt = torch.float32 if self.kind == GAUSSIAN else torch.int32
+        self.Y = torch.empty((m, p), dtype=ydt, device=device)          # column-major p x m
+        probe = Video(0, n_total, pix0, n_local, m, ((n_local + 15) // 16) * 16)
+        self.ws_sketch = _empty_bytes(cdmd_sketch_workspace_bytes(probe, self.c), device)
+        self.ws_fit = _empty_bytes(cdmd_fit_workspace_bytes(handle, p, m, k), device)
+        self.model_buf = _empty_bytes(cdmd_model_bytes(k, K, m), device)
+        self.model = cdmd_model_bind(self.model_buf, k, K, m)
+        self.Phi = torch.empty((k, n_local), dtype=torch.float32, device=device)
+        self.ldw = (n_local + 31) // 32
+        self.mask = torch.empty((m, self.ldw), dtype=torch.int32, device=device)
+
+    def sketch(self, X, stream=None):
+        v = video(X, self.n_total, self.pix0, self.n_local)
+        cdmd_sketch(self.h, v, self.c, self.Y, self.ws_sketch, stream)
+        return self.Y
+
+    def fit(self, stream=None):
+        cdmd_fit(self.h, self.Y, self.kind, self.p, self.m, self.k, self.K, self.model, self.ws_fit,
+                 self.dt, stream)
+        return self.model
+
+    def modes(self, X, stream=None, simt=False):
+        v = video(X, self.n_total, self.pix0, self.n_local)
+        cdmd_modes(self.h, v, self.model, self.Phi, stream, simt=simt)
+        return self.Phi[:self.model.k_eff]
+
+    def foreground(self, X, tau, mode=BG_DYNAMIC, stream=None):
+        v = video(X, self.n_total, self.pix0, self.n_local)
+        cdmd_foreground(self.h, v, self.model, self.Phi, mode, tau, self.mask, stream)
+        return self.mask
+
+    def background(self, mode=BG_DYNAMIC, t0=0, nt=None, stream=None):
+        nt = self.m - t0 if nt is None else nt
+        L = torch.empty((nt, self.n_local), dtype=torch.float32, device=self.Phi.device)
+        cdmd_background(self.h, self.Phi, self.n_local, self.model, mode, t0, nt, L, stream)
+        return L
+
+    def run(self, X, tau, mode=BG_DYNAMIC, allreduce=None, stream=None):
+        self.sketch(X, stream)
+        if allreduce is not None:
+            allreduce(self.Y)
+        self.fit(stream)
+        self.modes(X, stream)
+        return self.foreground(X, tau, mode, stream)
+
+
+from .dist import slab  # noqa: E402,F401  (re-export)

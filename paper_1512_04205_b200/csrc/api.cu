@@ -1,0 +1,324 @@
+// api.cu — the C ABI of libcdmd (include/cdmd.h): host-side validation, handle
+// state, workspace carving and kernel launches.  No torch types cross this
+// boundary; the Python binding (paper_1512_04205_b200/cdmd.py) only marshals
+// pointers and sizes.
+#include <cublas_v2.h>
+#include <cusolverDn.h>
+#include <math.h>
+#include <string.h>
+
+#include "handle.h"
+
+using namespace cdmd;
+
+namespace {
+
+size_t al256(size_t b) { return (b + 255) & ~(size_t)255; }
+
+cdmd_status cuda_status(cudaError_t e) { return e == cudaSuccess ? CDMD_OK : CDMD_ERR_CUDA; }
+
+cdmd_status check_video(const cdmd_video* v) {
+  if (!v || !v->X) return CDMD_ERR_ARG;
+  if (v->m < 2) return CDMD_ERR_RANGE;
+  if (v->n_total < 1 || v->n_local < 1 || v->pix0 < 0 || v->pix0 + v->n_local > v->n_total)
+    return CDMD_ERR_RANGE;
+  if ((reinterpret_cast<uintptr_t>(v->X) & 15) != 0) return CDMD_ERR_ARG;
+  if (v->ld < v->n_local || (v->ld & 15) != 0) return CDMD_ERR_ARG;
+  if (v->pix0 % 128 != 0) return CDMD_ERR_ARG;
+  if (v->n_total > (int64_t)8421504) return CDMD_ERR_RANGE;  // 255 n < 2^31 (exact int32 sums)
+  return CDMD_OK;
+}
+
+cdmd_status check_sensing(int64_t n_total, const cdmd_sensing* c) {
+  if (!c) return CDMD_ERR_ARG;
+  if (c->kind < CDMD_SPIXEL || c->kind > CDMD_GAUSSIAN) return CDMD_ERR_ARG;
+  if (c->p < 1 || c->p > n_total) return CDMD_ERR_RANGE;
+  if (c->kind == CDMD_SPARSE && c->s > 0 && c->s <= 1.0) return CDMD_ERR_RANGE;
+  if (c->kind == CDMD_SPARSE && c->s <= 0 && n_total < 3) return CDMD_ERR_RANGE;  // n/ln n > 1
+  return CDMD_OK;
+}
+
+int64_t kpad_of(int k) { return round_up(k, CDMD_NBLK); }
+int64_t mpad_of(int64_t m) { return round_up(m - 1, CDMD_KBLK); }
+
+struct ModelLayout {
+  size_t lambda, omega, pair, sigma, Mfold, beta, support, Mq, Mq_scale, coef, coef_col, dev_info, total;
+};
+
+ModelLayout model_layout(int k, int K, int64_t m) {
+  ModelLayout L{};
+  size_t off = 0;
+  auto take = [&](size_t b) { size_t o = off; off += al256(b); return o; };
+  const int64_t kp = kpad_of(k), mp = mpad_of(m);
+  L.lambda = take(sizeof(double) * 2 * k);
+  L.omega = take(sizeof(double) * 2 * k);
+  L.pair = take(sizeof(int32_t) * k);
+  L.sigma = take(sizeof(double) * k);
+  L.Mfold = take(sizeof(double) * (m - 1) * k);
+  L.beta = take(sizeof(double) * 2 * K);
+  L.support = take(sizeof(int32_t) * K);
+  L.Mq = take((size_t)kp * CDMD_LIMBS * mp);
+  L.Mq_scale = take(sizeof(double) * kp);
+  L.coef = take(sizeof(float) * 2 * K * m);
+  L.coef_col = take(sizeof(int32_t) * 2 * K);
+  L.dev_info = take(sizeof(int32_t) * 8);
+  L.total = off;
+  return L;
+}
+
+cdmd_status check_model(const cdmd_model* M, int64_t m) {
+  if (!M || !M->lambda || !M->Mq || !M->coef) return CDMD_ERR_ARG;
+  if (M->m != m) return CDMD_ERR_ARG;
+  if (M->k_eff < 1 || M->k_eff > M->k) return CDMD_ERR_ARG;  // cdmd_fit not run
+  return CDMD_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* cdmd_version(void) { return "cdmd-b200 0.1 (sm_100a)"; }
+
+const char* cdmd_status_str(cdmd_status s) {
+  switch (s) {
+    case CDMD_OK: return "ok";
+    case CDMD_ERR_ARG: return "invalid argument";
+    case CDMD_ERR_RANGE: return "argument out of range";
+    case CDMD_ERR_NUMERIC: return "numerical failure";
+    case CDMD_ERR_CUDA: return "CUDA error";
+    case CDMD_ERR_WORKSPACE: return "workspace too small";
+    case CDMD_ERR_UNSUPPORTED: return "unsupported device (needs sm_100a)";
+  }
+  return "unknown status";
+}
+
+cdmd_status cdmd_create(int device, cdmd_handle* out) {
+  if (!out) return CDMD_ERR_ARG;
+  *out = nullptr;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) return CDMD_ERR_CUDA;
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return CDMD_ERR_CUDA;
+  if (prop.major != 10 || prop.minor != 0) return CDMD_ERR_UNSUPPORTED;  // built for sm_100a only
+  if (cudaSetDevice(device) != cudaSuccess) return CDMD_ERR_CUDA;
+  cdmd_handle h = new cdmd_handle_s();
+  h->device = device;
+  h->sm_count = prop.multiProcessorCount;
+  cdmd_status st = CDMD_OK;
+  if (cublasCreate(&h->blas) != CUBLAS_STATUS_SUCCESS) st = CDMD_ERR_CUDA;
+  if (st == CDMD_OK) cublasSetMathMode(h->blas, CUBLAS_DEFAULT_MATH);  // fp64, no emulation
+  if (st == CDMD_OK && cusolverDnCreate(&h->solver) != CUSOLVER_STATUS_SUCCESS) st = CDMD_ERR_CUDA;
+  if (st == CDMD_OK && cusolverDnCreateParams(&h->params) != CUSOLVER_STATUS_SUCCESS) st = CDMD_ERR_CUDA;
+  if (st == CDMD_OK && cudaMalloc(&h->gauss_table, 65536 * sizeof(uint16_t)) != cudaSuccess) st = CDMD_ERR_CUDA;
+  if (st == CDMD_OK && cudaMallocHost(&h->host_info, 16 * sizeof(int32_t)) != cudaSuccess) st = CDMD_ERR_CUDA;
+  if (st == CDMD_OK && launch_gaussian_table(h->gauss_table, 0) != cudaSuccess) st = CDMD_ERR_CUDA;
+  if (st == CDMD_OK && cudaDeviceSynchronize() != cudaSuccess) st = CDMD_ERR_CUDA;
+  if (st != CDMD_OK) {
+    cdmd_destroy(h);
+    return st;
+  }
+  *out = h;
+  return CDMD_OK;
+}
+
+void cdmd_destroy(cdmd_handle h) {
+  if (!h) return;
+  if (h->params) cusolverDnDestroyParams(h->params);
+  if (h->solver) cusolverDnDestroy(h->solver);
+  if (h->blas) cublasDestroy(h->blas);
+  if (h->gauss_table) cudaFree(h->gauss_table);
+  if (h->host_info) cudaFreeHost(h->host_info);
+  delete h;
+}
+
+// ------------------------------------------------------------------- sketch
+size_t cdmd_sketch_workspace_bytes(const cdmd_video* v, const cdmd_sensing* c) {
+  if (!v || !c || check_sensing(v->n_total, c) != CDMD_OK) return 0;
+  return sensing_ws_bytes(make_plan(v->n_total, c));
+}
+
+cdmd_status cdmd_sketch(cdmd_handle h, const cdmd_video* v, const cdmd_sensing* c, void* Y,
+                        int64_t ldy, void* ws, size_t ws_bytes, cdmd_stream st_) {
+  cudaStream_t st = (cudaStream_t)st_;
+  if (!h || !Y) return CDMD_ERR_ARG;
+  cdmd_status s = check_video(v);
+  if (s != CDMD_OK) return s;
+  if ((s = check_sensing(v->n_total, c)) != CDMD_OK) return s;
+  if (ldy < c->p) return CDMD_ERR_ARG;
+  const SensingPlan P = make_plan(v->n_total, c);
+  const size_t need = sensing_ws_bytes(P);
+  if (ws_bytes < need || (need > 256 && !ws)) return CDMD_ERR_WORKSPACE;
+  if (ws && (reinterpret_cast<uintptr_t>(ws) & 255) != 0) return CDMD_ERR_ARG;
+  cudaError_t e = cudaSuccess;
+  switch (P.kind) {
+    case CDMD_SPIXEL: {
+      int32_t* rows = (int32_t*)ws;
+      e = launch_spixel_rows(P, rows, st);
+      if (e == cudaSuccess) e = launch_sketch_spixel(*v, P, rows, (int32_t*)Y, ldy, st);
+      break;
+    }
+    case CDMD_SPARSE: {
+      int32_t* ell = (int32_t*)ws;
+      int32_t* counts = (int32_t*)((char*)ws + al256(sizeof(int32_t) * P.p * P.cap));
+      int32_t* flags = (int32_t*)((char*)counts + al256(sizeof(int32_t) * P.p));
+      e = cudaMemsetAsync(flags, 0, 16, st);
+      if (e == cudaSuccess) e = launch_sparse_rows(P, ell, counts, flags, st);
+      if (e == cudaSuccess) e = launch_sketch_sparse(*v, P, ell, counts, (int32_t*)Y, ldy, st);
+      break;
+    }
+    case CDMD_RADEMACHER:
+      e = launch_sketch_rademacher(*v, P, (int32_t*)Y, ldy, st);
+      break;
+    case CDMD_GAUSSIAN:
+      e = launch_sketch_gaussian(*v, P, h->gauss_table, (float*)Y, ldy, st);
+      break;
+  }
+  return cuda_status(e);
+}
+
+// ---------------------------------------------------------------------- fit
+size_t cdmd_model_bytes(int k, int K, int64_t m) {
+  if (k < 1 || K < 1 || m < 2) return 0;
+  return model_layout(k, K, m).total;
+}
+
+cdmd_status cdmd_model_bind(cdmd_model* M, void* buf, size_t bytes, int k, int K, int64_t m) {
+  if (!M || !buf) return CDMD_ERR_ARG;
+  if (k < 1 || k > 256 || K < 1 || K > 32 || K > k || m < 2) return CDMD_ERR_RANGE;
+  if ((reinterpret_cast<uintptr_t>(buf) & 255) != 0) return CDMD_ERR_ARG;
+  const ModelLayout L = model_layout(k, K, m);
+  if (bytes < L.total) return CDMD_ERR_WORKSPACE;
+  char* b = (char*)buf;
+  memset(M, 0, sizeof(*M));
+  M->k = k;
+  M->K = K;
+  M->limbs = CDMD_LIMBS;
+  M->kpad = (int32_t)kpad_of(k);
+  M->m = m;
+  M->mpad = mpad_of(m);
+  M->lambda = (double*)(b + L.lambda);
+  M->omega = (double*)(b + L.omega);
+  M->pair = (int32_t*)(b + L.pair);
+  M->sigma = (double*)(b + L.sigma);
+  M->Mfold = (double*)(b + L.Mfold);
+  M->beta = (double*)(b + L.beta);
+  M->support = (int32_t*)(b + L.support);
+  M->Mq = (int8_t*)(b + L.Mq);
+  M->Mq_scale = (double*)(b + L.Mq_scale);
+  M->coef = (float*)(b + L.coef);
+  M->coef_col = (int32_t*)(b + L.coef_col);
+  M->dev_info = (int32_t*)(b + L.dev_info);
+  M->dt = 1.0;
+  return CDMD_OK;
+}
+
+size_t cdmd_fit_workspace_bytes(cdmd_handle h, int64_t p, int64_t m, int k) {
+  if (!h || p < 1 || m < 2 || k < 1) return 0;
+  return fit_ws_bytes(h, p, m, k);
+}
+
+cdmd_status cdmd_fit(cdmd_handle h, const void* Y, int64_t ldy, int32_t kind, int64_t p, int64_t m,
+                     int k, int K, double dt, cdmd_model* model, void* ws, size_t ws_bytes,
+                     cdmd_stream st) {
+  if (!h || !Y || !model || !ws) return CDMD_ERR_ARG;
+  if (kind < CDMD_SPIXEL || kind > CDMD_GAUSSIAN) return CDMD_ERR_ARG;
+  if (m < 2 || p < 1) return CDMD_ERR_RANGE;
+  if (k < 1 || k > p || k > m - 1 || k > model->k) return CDMD_ERR_RANGE;  // P:355 "p >= k"
+  if (K < 1 || K > k || K > model->K) return CDMD_ERR_RANGE;
+  if (ldy < p || !(dt > 0.0)) return CDMD_ERR_ARG;
+  if (model->m != m) return CDMD_ERR_ARG;
+  if ((reinterpret_cast<uintptr_t>(ws) & 255) != 0) return CDMD_ERR_ARG;
+  model->k_eff = model->K_eff = model->n_coef = model->info = 0;
+  return fit_impl(h, Y, ldy, kind, p, m, k, K, dt, model, ws, ws_bytes, (cudaStream_t)st);
+}
+
+// -------------------------------------------------------------------- modes
+static cdmd_status modes_common(cdmd_handle h, const cdmd_video* v, const cdmd_model* M, float* Phi,
+                                int64_t ldphi) {
+  if (!h || !Phi) return CDMD_ERR_ARG;
+  cdmd_status s = check_video(v);
+  if (s != CDMD_OK) return s;
+  if ((s = check_model(M, v->m)) != CDMD_OK) return s;
+  if (ldphi < v->n_local) return CDMD_ERR_ARG;
+  return CDMD_OK;
+}
+
+cdmd_status cdmd_modes(cdmd_handle h, const cdmd_video* v, const cdmd_model* M, float* Phi,
+                       int64_t ldphi, cdmd_stream st) {
+  cdmd_status s = modes_common(h, v, M, Phi, ldphi);
+  if (s != CDMD_OK) return s;
+  return cuda_status(launch_modes_tc(*v, *M, Phi, ldphi, (cudaStream_t)st));
+}
+
+cdmd_status cdmd_modes_simt(cdmd_handle h, const cdmd_video* v, const cdmd_model* M, float* Phi,
+                            int64_t ldphi, cdmd_stream st) {
+  cdmd_status s = modes_common(h, v, M, Phi, ldphi);
+  if (s != CDMD_OK) return s;
+  return cuda_status(launch_modes_simt(*v, *M, Phi, ldphi, (cudaStream_t)st));
+}
+
+// ---------------------------------------------------------- background / mask
+cdmd_status cdmd_background(cdmd_handle h, const float* Phi, int64_t ldphi, int64_t n_local,
+                            const cdmd_model* M, int32_t mode, int64_t t0, int64_t nt, float* L,
+                            int64_t ldl, cdmd_stream st) {
+  if (!h || !Phi || !L || !M) return CDMD_ERR_ARG;
+  if (mode != CDMD_BG_STATIC && mode != CDMD_BG_DYNAMIC) return CDMD_ERR_ARG;
+  if (n_local < 1 || ldphi < n_local || ldl < n_local) return CDMD_ERR_ARG;
+  cdmd_status s = check_model(M, M->m);
+  if (s != CDMD_OK) return s;
+  if (t0 < 0 || nt < 1 || t0 + nt > M->m || nt > 65535) return CDMD_ERR_RANGE;
+  return cuda_status(launch_background(Phi, ldphi, n_local, *M, mode, t0, nt, L, ldl, (cudaStream_t)st));
+}
+
+cdmd_status cdmd_foreground(cdmd_handle h, const cdmd_video* v, const cdmd_model* M,
+                            const float* Phi, int64_t ldphi, int32_t mode, float tau,
+                            uint32_t* mask, int64_t ldw, cdmd_stream st) {
+  if (!h || !mask || !Phi) return CDMD_ERR_ARG;
+  if (mode != CDMD_BG_STATIC && mode != CDMD_BG_DYNAMIC) return CDMD_ERR_ARG;
+  cdmd_status s = check_video(v);
+  if (s != CDMD_OK) return s;
+  if ((s = check_model(M, v->m)) != CDMD_OK) return s;
+  if (!(tau > 0.0f)) return CDMD_ERR_RANGE;
+  if (ldphi < v->n_local || ldw < ceil_div(v->n_local, 32)) return CDMD_ERR_ARG;
+  return cuda_status(launch_foreground(*v, *M, Phi, ldphi, mode, tau, mask, ldw, (cudaStream_t)st));
+}
+
+// --------------------------------------------------------------- test hooks
+cdmd_status cdmd_philox(const uint32_t* ctr, uint32_t k0, uint32_t k1, uint32_t* out, int64_t count,
+                        cdmd_stream st) {
+  if (count < 0 || (count > 0 && (!ctr || !out))) return CDMD_ERR_ARG;
+  return cuda_status(launch_philox_test(ctr, k0, k1, out, count, (cudaStream_t)st));
+}
+
+cdmd_status cdmd_gaussian_table(cdmd_handle h, uint16_t* out, cdmd_stream st) {
+  if (!h || !out) return CDMD_ERR_ARG;
+  return cuda_status(cudaMemcpyAsync(out, h->gauss_table, 65536 * sizeof(uint16_t),
+                                     cudaMemcpyDeviceToDevice, (cudaStream_t)st));
+}
+
+int64_t cdmd_sparse_cap(int64_t n_total, int64_t p, double s) {
+  cdmd_sensing c{CDMD_SPARSE, p, s, 0};
+  return make_plan(n_total, &c).cap;
+}
+
+cdmd_status cdmd_sensing_rows(cdmd_handle h, int64_t n_total, const cdmd_sensing* c,
+                              int32_t* rows_or_ell, int32_t* counts, cdmd_stream st_) {
+  cudaStream_t st = (cudaStream_t)st_;
+  if (!h || !rows_or_ell) return CDMD_ERR_ARG;
+  cdmd_status s = check_sensing(n_total, c);
+  if (s != CDMD_OK) return s;
+  const SensingPlan P = make_plan(n_total, c);
+  if (P.kind == CDMD_SPIXEL) return cuda_status(launch_spixel_rows(P, rows_or_ell, st));
+  if (P.kind == CDMD_SPARSE) {
+    if (!counts) return CDMD_ERR_ARG;
+    int32_t* flags = nullptr;
+    if (cudaMallocAsync((void**)&flags, 16, st) != cudaSuccess) return CDMD_ERR_CUDA;
+    cudaMemsetAsync(flags, 0, 16, st);
+    cudaError_t e = launch_sparse_rows(P, rows_or_ell, counts, flags, st);
+    cudaFreeAsync(flags, st);
+    return cuda_status(e);
+  }
+  return CDMD_ERR_ARG;
+}
+
+}  // extern "C"

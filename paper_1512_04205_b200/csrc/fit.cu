@@ -1,0 +1,565 @@
+// fit.cu — the small cDMD solve on the sketch (not HBM-bound; O(p m^2 + m^3)).
+//
+// Alg. 1 on Y_full = C D (p x m), Y = Y_full[:, :m-1], Y' = Y_full[:, 1:]:
+//   G = Y_full^T Y_full (m x m, fp64; one cuBLAS DGEMM) holds every inner
+//   product the solve needs: Y^T Y = G[0:m-1, 0:m-1], Y^T Y' = G[0:m-1, 1:m],
+//   Y'^T Y' = G[1:m, 1:m], Y'^T y1 = G[1:m, 0], ||y1||^2 = G[0, 0].
+//   step 4  truncated SVD of Y (Eq. svd) by the method of
+//           snapshots: Y^T Y = V S^2 V^T (cuSOLVER syevd), top k, sigma_j kept iff
+//           sigma_j > 1e-6 sigma_1 (reading R10)
+//   step 6  A~ = U^T Y' V S^-1 = S^-1 V^T (Y^T Y') V S^-1
+//   step 7  A~ W = W Lambda (cuSOLVER geev), canonical order/phase
+//   step 8' M = V S^-1 W (P:346 without X'), kept conjugate-folded (real columns)
+//   Rem. 3  beta = omp(Phi_Y, y1) with Phi_Y = Y' M, in the Gram form of
+//           Rubinstein et al.: Phi_Y^H Phi_Y = M^H (Y'^T Y') M, Phi_Y^H y1 =
+//           M^H (Y'^T y1) -- identical selections, residual norms from the Gram
+//           omega = log(lambda)/dt; coefficient table of the background
+//           L_jt = Re sum_{p in S} beta_p phi_jp lambda_p^(t-1)
+//   modes   int8 fixed-point limbs of M for cdmd_modes
+#include <cublas_v2.h>
+#include <cusolverDn.h>
+#include <math.h>
+#include <stdio.h>
+
+#include "handle.h"
+
+namespace cdmd {
+
+static constexpr double RANK_RTOL = 1e-6;  // reading R10
+static constexpr double OMP_STOP = 1e-6;   // reading R12: stop when ||r|| <= 1e-6 ||y1||
+static constexpr double TIE_RTOL = 1e-9;   // reading R13
+
+struct FitWs {
+  double *Yd, *G, *A, *w, *V, *T, *B, *VR, *Wc, *SW, *T2, *Gf, *cf;
+  int* dinfo;
+  void* sy_dev;
+  size_t sy_dev_bytes, sy_host_bytes;
+  void* ge_dev;
+  size_t ge_dev_bytes, ge_host_bytes;
+  size_t total;
+};
+
+static size_t al(size_t b) { return (b + 255) & ~(size_t)255; }
+
+static cdmd_status layout_ws(cdmd_handle h, int64_t p, int64_t m, int k, char* base, FitWs* W) {
+  const int64_t n1 = m - 1;
+  size_t off = 0;
+  auto take = [&](size_t bytes) -> char* {
+    char* ptr = base ? base + off : nullptr;
+    off += al(bytes);
+    return ptr;
+  };
+  W->Yd = (double*)take(sizeof(double) * p * m);
+  W->G = (double*)take(sizeof(double) * m * m);
+  W->A = (double*)take(sizeof(double) * n1 * n1);
+  W->w = (double*)take(sizeof(double) * n1);
+  W->V = (double*)take(sizeof(double) * n1 * k);
+  W->T = (double*)take(sizeof(double) * n1 * k);
+  W->B = (double*)take(sizeof(double) * k * k);
+  W->VR = (double*)take(sizeof(double) * k * k);
+  W->Wc = (double*)take(sizeof(double) * 2 * k);
+  W->SW = (double*)take(sizeof(double) * k * k);
+  W->T2 = (double*)take(sizeof(double) * n1 * k);
+  W->Gf = (double*)take(sizeof(double) * k * k);
+  W->cf = (double*)take(sizeof(double) * k);
+  W->dinfo = (int*)take(sizeof(int) * 16);
+  // solver workspaces (queried with the final dimensions)
+  size_t d = 0, hb = 0;
+  if (cusolverDnXsyevd_bufferSize(h->solver, h->params, CUSOLVER_EIG_MODE_VECTOR,
+                                  CUBLAS_FILL_MODE_LOWER, n1, CUDA_R_64F, W->A, n1, CUDA_R_64F,
+                                  W->w, CUDA_R_64F, &d, &hb) != CUSOLVER_STATUS_SUCCESS)
+    return CDMD_ERR_CUDA;
+  W->sy_dev_bytes = d;
+  W->sy_host_bytes = hb;
+  W->sy_dev = take(d + 16);
+  d = 0;
+  hb = 0;
+  if (cusolverDnXgeev_bufferSize(h->solver, h->params, CUSOLVER_EIG_MODE_NOVECTOR,
+                                 CUSOLVER_EIG_MODE_VECTOR, k, CUDA_R_64F, W->B, k, CUDA_C_64F,
+                                 W->Wc, CUDA_R_64F, nullptr, k, CUDA_R_64F, W->VR, k, CUDA_R_64F,
+                                 &d, &hb) != CUSOLVER_STATUS_SUCCESS)
+    return CDMD_ERR_CUDA;
+  W->ge_dev_bytes = d;
+  W->ge_host_bytes = hb;
+  W->ge_dev = take(d + 16);
+  W->total = off;
+  return CDMD_OK;
+}
+
+size_t fit_ws_bytes(cdmd_handle h, int64_t p, int64_t m, int k) {
+  FitWs W{};
+  if (layout_ws(h, p, m, k, nullptr, &W) != CDMD_OK) return 0;
+  return W.total;
+}
+
+// ------------------------------------------------------------------ kernels
+template <typename T>
+__global__ void to_f64_kernel(const T* __restrict__ Y, int64_t ldy, int64_t p, int64_t m,
+                              double* __restrict__ Yd) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= p * m) return;
+  const int64_t r = i % p, t = i / p;
+  Yd[i] = (double)Y[r + t * ldy];
+}
+
+// sigma_j = sqrt(w), descending; V = matching eigenvectors; k_eff
+__global__ void select_topk_kernel(const double* __restrict__ A, const double* __restrict__ w,
+                                   int64_t n1, int k, double* __restrict__ V,
+                                   double* __restrict__ sigma, int* __restrict__ dinfo) {
+  const int c = blockIdx.x;  // output column
+  const int64_t src = n1 - 1 - c;
+  const double s0 = sqrt(fmax(w[n1 - 1], 0.0));
+  for (int64_t i = threadIdx.x; i < n1; i += blockDim.x) V[i + c * n1] = A[i + src * n1];
+  if (threadIdx.x == 0) {
+    const double s = sqrt(fmax(w[src], 0.0));
+    sigma[c] = s;
+    if (c == 0) {
+      int ke = 0;
+      for (int j = 0; j < k; ++j)
+        if (sqrt(fmax(w[n1 - 1 - j], 0.0)) > RANK_RTOL * s0) ++ke; else break;
+      dinfo[INFO_K_EFF] = ke;
+    }
+  }
+}
+
+__global__ void scale_atilde_kernel(double* __restrict__ B, const double* __restrict__ sigma, int k) {
+  const int i = threadIdx.x, j = blockIdx.x;
+  if (i < k) B[i + j * k] /= sigma[i] * sigma[j];
+}
+
+// canonical eigen-order and phase (reading R11) + folded S^-1 W + lambda/omega/pair
+__global__ void canonicalize_kernel(int k, const double* __restrict__ Wc, const double* __restrict__ VR,
+                                    const double* __restrict__ sigma, double dt,
+                                    double* __restrict__ lam_out, double* __restrict__ om_out,
+                                    int32_t* __restrict__ pair_out, double* __restrict__ SW,
+                                    int* __restrict__ dinfo) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  // units: (first index, is_pair); LAPACK layout of real geev output
+  int ufirst[512];
+  int upair[512];
+  int nu = 0;
+  int flags = 0;
+  for (int j = 0; j < k && nu < 512;) {
+    const double re = Wc[2 * j], im = Wc[2 * j + 1];
+    if (im == 0.0) {
+      ufirst[nu] = j; upair[nu] = 0; ++nu; ++j;
+    } else if (im > 0.0 && j + 1 < k && Wc[2 * j + 2] == re && Wc[2 * j + 3] == -im) {
+      ufirst[nu] = j; upair[nu] = 1; ++nu; j += 2;
+    } else {
+      flags |= FLAG_EIG_PAIRING;  // treat as real part only (should not happen)
+      ufirst[nu] = j; upair[nu] = 0; ++nu; ++j;
+    }
+  }
+  // stable insertion sort by (|lambda| desc, real before pair)
+  for (int a = 1; a < nu; ++a) {
+    const int f = ufirst[a], pr = upair[a];
+    const double ka = hypot(Wc[2 * f], Wc[2 * f + 1]);
+    int b = a - 1;
+    while (b >= 0) {
+      const int fb = ufirst[b];
+      const double kb = hypot(Wc[2 * fb], Wc[2 * fb + 1]);
+      const bool after = (kb > ka) || (kb == ka && upair[b] <= pr);
+      if (after) break;
+      ufirst[b + 1] = ufirst[b]; upair[b + 1] = upair[b];
+      --b;
+    }
+    ufirst[b + 1] = f; upair[b + 1] = pr;
+  }
+  int c = 0;
+  for (int u = 0; u < nu; ++u) {
+    const int j = ufirst[u];
+    const double re = Wc[2 * j], im = upair[u] ? Wc[2 * j + 1] : 0.0;
+    // normalise the eigenvector: unit 2-norm, largest |component| real positive
+    double nrm = 0.0;
+    for (int i = 0; i < k; ++i) {
+      const double a = VR[i + j * k], b = upair[u] ? VR[i + (j + 1) * k] : 0.0;
+      nrm += a * a + b * b;
+    }
+    nrm = sqrt(nrm);
+    int imax = 0;
+    double amax = -1.0;
+    for (int i = 0; i < k; ++i) {
+      const double a = VR[i + j * k] / nrm, b = upair[u] ? VR[i + (j + 1) * k] / nrm : 0.0;
+      const double mag = hypot(a, b);
+      if (mag > amax) { amax = mag; imax = i; }
+    }
+    const double pa = VR[imax + j * k] / nrm, pb = upair[u] ? VR[imax + (j + 1) * k] / nrm : 0.0;
+    const double pm = hypot(pa, pb);
+    const double cr = pa / pm, ci = -pb / pm;  // conj(phase)
+    for (int i = 0; i < k; ++i) {
+      const double a = VR[i + j * k] / nrm, b = upair[u] ? VR[i + (j + 1) * k] / nrm : 0.0;
+      const double nr = a * cr - b * ci, ni = a * ci + b * cr;
+      SW[i + c * k] = nr / sigma[i];
+      if (upair[u]) SW[i + (c + 1) * k] = ni / sigma[i];
+    }
+    const double lr = re, li = im;
+    const double lmod = hypot(lr, li), larg = atan2(li, lr);
+    lam_out[2 * c] = lr; lam_out[2 * c + 1] = li;
+    om_out[2 * c] = log(lmod) / dt; om_out[2 * c + 1] = larg / dt;
+    pair_out[c] = upair[u] ? 1 : 0;
+    if (upair[u]) {
+      lam_out[2 * c + 2] = lr; lam_out[2 * c + 3] = -li;
+      om_out[2 * c + 2] = log(lmod) / dt; om_out[2 * c + 3] = -larg / dt;
+      pair_out[c + 1] = -1;
+      c += 2;
+    } else {
+      c += 1;
+    }
+  }
+  if (flags) atomicOr(&dinfo[INFO_FLAGS], flags);
+}
+
+// complex helpers
+struct cplx { double r, i; };
+__device__ __forceinline__ cplx cmul(cplx a, cplx b) { return {a.r * b.r - a.i * b.i, a.r * b.i + a.i * b.r}; }
+__device__ __forceinline__ cplx cconjmul(cplx a, cplx b) { return {a.r * b.r + a.i * b.i, a.r * b.i - a.i * b.r}; }  // conj(a) b
+
+__device__ __forceinline__ void mode_rep(const int32_t* pair, int j, int& ra, int& rb, double& sg) {
+  const int pj = pair[j];
+  if (pj == 0) { ra = j; rb = j; sg = 0.0; }
+  else if (pj > 0) { ra = j; rb = j + 1; sg = 1.0; }
+  else { ra = j - 1; rb = j; sg = -1.0; }
+}
+
+// <phi_i, phi_j> = phi_i^H phi_j from the fold Gram Gf = F^T F (phi = f_ra + i sg f_rb)
+__device__ __forceinline__ cplx gram_c(const double* Gf, int k, const int32_t* pair, int i, int j) {
+  int ai, bi, aj, bj;
+  double si, sj;
+  mode_rep(pair, i, ai, bi, si);
+  mode_rep(pair, j, aj, bj, sj);
+  const double re = Gf[ai + aj * k] + si * sj * Gf[bi + bj * k];
+  const double im = sj * Gf[ai + bj * k] - si * Gf[bi + aj * k];
+  return {re, im};
+}
+
+// OMP (Remark 3 P:363-369) in Gram form + background coefficient table.
+// One block.  corr_j = phi_j^H r = alpha_j - sum_{s in S} <phi_j, phi_s> beta_s.
+__global__ void __launch_bounds__(256) omp_kernel(
+    int k, int K, int64_t m, const double* __restrict__ Gf, const double* __restrict__ cf,
+    const double* __restrict__ G, const int32_t* __restrict__ pair, const double* __restrict__ lam,
+    double* __restrict__ beta_out, int32_t* __restrict__ support_out, float* __restrict__ coef,
+    int32_t* __restrict__ coef_col, int* __restrict__ dinfo) {
+  __shared__ double sc[512];
+  __shared__ double red[256];
+  __shared__ int redi[256];
+  __shared__ int S[32];
+  __shared__ cplx alpha[512];
+  __shared__ cplx beta[32];
+  __shared__ cplx Lc[32 * 32];  // Cholesky factor of Gc[S,S]
+  __shared__ int nS_sh, stop_sh;
+  __shared__ int F[128];
+  __shared__ int nF_sh;
+  const int tid = threadIdx.x;
+  const double y1n2 = G[0];
+  for (int j = tid; j < k; j += blockDim.x) {
+    int ra, rb;
+    double sg;
+    mode_rep(pair, j, ra, rb, sg);
+    alpha[j] = {cf[ra], -sg * cf[rb]};
+  }
+  if (tid == 0) { nS_sh = 0; stop_sh = 0; }
+  __syncthreads();
+  const int Kmax = K < k ? K : k;
+  for (int it = 0; it < Kmax; ++it) {
+    const int nS = nS_sh;
+    if (tid == 0) {
+      double rn2 = y1n2;
+      for (int s = 0; s < nS; ++s) {
+        const cplx t = cconjmul(alpha[S[s]], beta[s]);
+        rn2 -= t.r;
+      }
+      if (!(y1n2 > 0.0) || rn2 <= OMP_STOP * OMP_STOP * y1n2) stop_sh = 1;
+    }
+    __syncthreads();
+    if (stop_sh) break;
+    double best = -1.0;
+    for (int j = tid; j < k; j += blockDim.x) {
+      bool in = false;
+      for (int s = 0; s < nS; ++s) in |= (S[s] == j);
+      const cplx gjj = gram_c(Gf, k, pair, j, j);
+      double score = -1.0;
+      if (!in && gjj.r > 0.0) {
+        cplx c = alpha[j];
+        for (int s = 0; s < nS; ++s) {
+          const cplx g = gram_c(Gf, k, pair, j, S[s]);
+          const cplx t = cmul(g, beta[s]);
+          c.r -= t.r; c.i -= t.i;
+        }
+        score = hypot(c.r, c.i) / sqrt(gjj.r);
+      }
+      sc[j] = score;
+      best = fmax(best, score);
+    }
+    red[tid] = best;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+      if (tid < o) red[tid] = fmax(red[tid], red[tid + o]);
+      __syncthreads();
+    }
+    const double bmax = red[0];
+    __syncthreads();
+    int cand = 1 << 30;
+    for (int j = tid; j < k; j += blockDim.x)
+      if (sc[j] >= bmax * (1.0 - TIE_RTOL) && j < cand) cand = j;
+    redi[tid] = cand;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+      if (tid < o) redi[tid] = min(redi[tid], redi[tid + o]);
+      __syncthreads();
+    }
+    if (tid == 0) {
+      const int js = redi[0];
+      if (!(bmax > 0.0) || !isfinite(bmax) || js >= k || nS >= 32) {
+        stop_sh = 1;
+      } else {
+        S[nS] = js;
+        const int n = nS + 1;
+        // complex Cholesky of Gc[S,S] (Hermitian positive definite), from scratch
+        bool ok = true;
+        for (int a = 0; a < n && ok; ++a) {
+          for (int b = 0; b <= a; ++b) {
+            cplx s = gram_c(Gf, k, pair, S[a], S[b]);  // <phi_a, phi_b>: row a, col b
+            for (int q = 0; q < b; ++q) {
+              const cplx t = cmul(Lc[a * 32 + q], cplx{Lc[b * 32 + q].r, -Lc[b * 32 + q].i});
+              s.r -= t.r; s.i -= t.i;
+            }
+            if (a == b) {
+              if (!(s.r > 0.0)) { ok = false; break; }
+              Lc[a * 32 + a] = {sqrt(s.r), 0.0};
+            } else {
+              const double d = Lc[b * 32 + b].r;
+              Lc[a * 32 + b] = {s.r / d, s.i / d};
+            }
+          }
+        }
+        if (!ok) {
+          stop_sh = 1;
+          atomicOr(&dinfo[INFO_FLAGS], 8);
+        } else {
+          // Normal equations: Gc beta = alpha with Gc[a][b] = <phi_a, phi_b>.
+          // L computed above satisfies L L^H = H with H[a][b] = <phi_a, phi_b>.
+          cplx z[32];
+          for (int a = 0; a < n; ++a) {  // L z = alpha_S
+            cplx s = alpha[S[a]];
+            for (int q = 0; q < a; ++q) {
+              const cplx t = cmul(Lc[a * 32 + q], z[q]);
+              s.r -= t.r; s.i -= t.i;
+            }
+            z[a] = {s.r / Lc[a * 32 + a].r, s.i / Lc[a * 32 + a].r};
+          }
+          for (int a = n - 1; a >= 0; --a) {  // L^H beta = z
+            cplx s = z[a];
+            for (int q = a + 1; q < n; ++q) {
+              const cplx lq = {Lc[q * 32 + a].r, -Lc[q * 32 + a].i};
+              const cplx t = cmul(lq, beta[q]);
+              s.r -= t.r; s.i -= t.i;
+            }
+            beta[a] = {s.r / Lc[a * 32 + a].r, s.i / Lc[a * 32 + a].r};
+          }
+          nS_sh = n;
+        }
+      }
+    }
+    __syncthreads();
+    if (stop_sh) break;
+  }
+  __syncthreads();
+  const int nS = nS_sh;
+  // outputs + used fold columns (sorted, unique)
+  if (tid == 0) {
+    int nF = 0;
+    for (int s = 0; s < nS; ++s) {
+      support_out[s] = S[s];
+      beta_out[2 * s] = beta[s].r;
+      beta_out[2 * s + 1] = beta[s].i;
+      int ra, rb;
+      double sg;
+      mode_rep(pair, S[s], ra, rb, sg);
+      const int cols[2] = {ra, rb};
+      for (int q = 0; q < (sg != 0.0 ? 2 : 1); ++q) {
+        bool have = false;
+        for (int f = 0; f < nF; ++f) have |= (F[f] == cols[q]);
+        if (!have && nF < 128) F[nF++] = cols[q];
+      }
+    }
+    for (int a = 1; a < nF; ++a) {
+      const int v = F[a];
+      int b = a - 1;
+      while (b >= 0 && F[b] > v) { F[b + 1] = F[b]; --b; }
+      F[b + 1] = v;
+    }
+    for (int f = 0; f < nF; ++f) coef_col[f] = F[f];
+    nF_sh = nF;
+    dinfo[INFO_K_SEL] = nS;
+    dinfo[INFO_N_COEF] = nF;
+  }
+  __syncthreads();
+  const int nF = nF_sh;
+  // coef[f][t] = sum over support modes touching fold column F[f] of
+  //   Re(beta lambda^t) (the f_ra part) or -sg Im(beta lambda^t) (the f_rb part)
+  for (int64_t idx = tid; idx < (int64_t)nF * m; idx += blockDim.x) {
+    const int f = (int)(idx / m);
+    const int64_t t = idx % m;
+    double acc = 0.0;
+    for (int s = 0; s < nS; ++s) {
+      int ra, rb;
+      double sg;
+      mode_rep(pair, S[s], ra, rb, sg);
+      if (ra != F[f] && !(sg != 0.0 && rb == F[f])) continue;
+      const double lr = lam[2 * S[s]], li = lam[2 * S[s] + 1];
+      const double lmod = hypot(lr, li), larg = atan2(li, lr);
+      const double mag = exp((double)t * log(lmod));
+      double sn, cs;
+      sincos((double)t * larg, &sn, &cs);
+      const cplx c = cmul(beta[s], cplx{mag * cs, mag * sn});
+      if (ra == F[f]) acc += c.r;
+      if (sg != 0.0 && rb == F[f]) acc += -sg * c.i;
+    }
+    coef[f * m + t] = (float)acc;
+  }
+}
+
+// int8 limbs of M: Q = rint(M / s_c * 126 * 128^(L-1)),
+// balanced base-128 digits, Mq[(l*kpad + c) * mpad + t]; scale = s_c / (126 128^(L-1)).
+__global__ void quantize_kernel(const double* __restrict__ Mf, int64_t n1, int k_eff, int kpad,
+                                int64_t mpad, int8_t* __restrict__ Mq, double* __restrict__ scale) {
+  const int c = blockIdx.x;
+  __shared__ double red[256];
+  double mx = 0.0;
+  if (c < k_eff)
+    for (int64_t t = threadIdx.x; t < n1; t += blockDim.x) mx = fmax(mx, fabs(Mf[t + c * n1]));
+  red[threadIdx.x] = mx;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + o]);
+    __syncthreads();
+  }
+  const double sc = red[0];
+  const double full = 126.0 * 2097152.0;  // 126 * 128^(L-1), L = 4
+  const double mul = sc > 0.0 ? full / sc : 0.0;
+  if (threadIdx.x == 0) scale[c] = sc > 0.0 ? sc / full : 0.0;
+  for (int64_t t = threadIdx.x; t < mpad; t += blockDim.x) {
+    long long Q = (c < k_eff && t < n1) ? llrint(Mf[t + c * n1] * mul) : 0;
+    int8_t d[CDMD_LIMBS];
+#pragma unroll
+    for (int l = CDMD_LIMBS - 1; l >= 1; --l) {
+      const long long q = (Q + 64) >> 7;  // floor((Q + 64) / 128)
+      d[l] = (int8_t)(Q - (q << 7));
+      Q = q;
+    }
+    d[0] = (int8_t)Q;
+#pragma unroll
+    for (int l = 0; l < CDMD_LIMBS; ++l) Mq[((int64_t)l * kpad + c) * mpad + t] = d[l];
+  }
+}
+
+#define BL(x)                                             \
+  do {                                                    \
+    if ((x) != CUBLAS_STATUS_SUCCESS) return CDMD_ERR_CUDA; \
+  } while (0)
+#define CU(x)                                 \
+  do {                                        \
+    if ((x) != cudaSuccess) return CDMD_ERR_CUDA; \
+  } while (0)
+
+cdmd_status fit_impl(cdmd_handle h, const void* Y, int64_t ldy, int kind, int64_t p, int64_t m,
+                     int k, int K, double dt, cdmd_model* model, void* ws, size_t ws_bytes,
+                     cudaStream_t st) {
+  FitWs W{};
+  cdmd_status s0 = layout_ws(h, p, m, k, (char*)ws, &W);
+  if (s0 != CDMD_OK) return s0;
+  if (ws_bytes < W.total) return CDMD_ERR_WORKSPACE;
+  const int64_t n1 = m - 1;
+  BL(cublasSetStream(h->blas, st));
+  if (cusolverDnSetStream(h->solver, st) != CUSOLVER_STATUS_SUCCESS) return CDMD_ERR_CUDA;
+  CU(cudaMemsetAsync(W.dinfo, 0, sizeof(int) * 16, st));
+  CU(cudaMemsetAsync(model->dev_info, 0, sizeof(int32_t) * 8, st));
+  // Y -> fp64
+  {
+    const int64_t N = p * m;
+    if (kind == CDMD_GAUSSIAN)
+      to_f64_kernel<float><<<(unsigned)ceil_div(N, 256), 256, 0, st>>>((const float*)Y, ldy, p, m, W.Yd);
+    else
+      to_f64_kernel<int32_t><<<(unsigned)ceil_div(N, 256), 256, 0, st>>>((const int32_t*)Y, ldy, p, m, W.Yd);
+    CU(cudaGetLastError());
+  }
+  const double one = 1.0, zero = 0.0;
+  // G = Y_full^T Y_full
+  BL(cublasDgemm(h->blas, CUBLAS_OP_T, CUBLAS_OP_N, (int)m, (int)m, (int)p, &one, W.Yd, (int)p,
+                 W.Yd, (int)p, &zero, W.G, (int)m));
+  // A = Y^T Y = G[0:m-1, 0:m-1]
+  CU(cudaMemcpy2DAsync(W.A, sizeof(double) * n1, W.G, sizeof(double) * m, sizeof(double) * n1, n1,
+                       cudaMemcpyDeviceToDevice, st));
+  size_t hneed = W.sy_host_bytes > W.ge_host_bytes ? W.sy_host_bytes : W.ge_host_bytes;
+  if (h->host_ws.size() < hneed + 16) h->host_ws.resize(hneed + 16);
+  if (cusolverDnXsyevd(h->solver, h->params, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n1,
+                       CUDA_R_64F, W.A, n1, CUDA_R_64F, W.w, CUDA_R_64F, W.sy_dev, W.sy_dev_bytes,
+                       W.sy_host_bytes ? h->host_ws.data() : nullptr, W.sy_host_bytes,
+                       W.dinfo + 8) != CUSOLVER_STATUS_SUCCESS)
+    return CDMD_ERR_CUDA;
+  select_topk_kernel<<<k, 128, 0, st>>>(W.A, W.w, n1, k, W.V, model->sigma, W.dinfo);
+  CU(cudaGetLastError());
+  CU(cudaMemcpyAsync(h->host_info, W.dinfo, sizeof(int) * 16, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  if (h->host_info[8] != 0) {
+    model->info = h->host_info[8];
+    return CDMD_ERR_NUMERIC;
+  }
+  const int ke = h->host_info[INFO_K_EFF];
+  model->k_eff = ke;
+  if (ke < 1) return CDMD_ERR_NUMERIC;
+  // A~ = S^-1 V^T (Y^T Y') V S^-1, Y^T Y' = G[0:m-1, 1:m] = G + m (ld m)
+  BL(cublasDgemm(h->blas, CUBLAS_OP_N, CUBLAS_OP_N, (int)n1, ke, (int)n1, &one, W.G + m, (int)m,
+                 W.V, (int)n1, &zero, W.T, (int)n1));
+  BL(cublasDgemm(h->blas, CUBLAS_OP_T, CUBLAS_OP_N, ke, ke, (int)n1, &one, W.V, (int)n1, W.T,
+                 (int)n1, &zero, W.B, ke));
+  scale_atilde_kernel<<<ke, ke <= 1024 ? ((ke + 31) / 32) * 32 : 1024, 0, st>>>(W.B, model->sigma, ke);
+  CU(cudaGetLastError());
+  // eig(A~): real nonsymmetric, LAPACK-style output (pairs as Re/Im columns)
+  {
+    size_t d = 0, hb = 0;
+    if (cusolverDnXgeev_bufferSize(h->solver, h->params, CUSOLVER_EIG_MODE_NOVECTOR,
+                                   CUSOLVER_EIG_MODE_VECTOR, ke, CUDA_R_64F, W.B, ke, CUDA_C_64F,
+                                   W.Wc, CUDA_R_64F, nullptr, ke, CUDA_R_64F, W.VR, ke,
+                                   CUDA_R_64F, &d, &hb) != CUSOLVER_STATUS_SUCCESS)
+      return CDMD_ERR_CUDA;
+    if (d > W.ge_dev_bytes) return CDMD_ERR_WORKSPACE;
+    if (h->host_ws.size() < hb + 16) h->host_ws.resize(hb + 16);
+    if (cusolverDnXgeev(h->solver, h->params, CUSOLVER_EIG_MODE_NOVECTOR, CUSOLVER_EIG_MODE_VECTOR,
+                        ke, CUDA_R_64F, W.B, ke, CUDA_C_64F, W.Wc, CUDA_R_64F, nullptr, ke,
+                        CUDA_R_64F, W.VR, ke, CUDA_R_64F, W.ge_dev, d,
+                        hb ? h->host_ws.data() : nullptr, hb, W.dinfo + 9) != CUSOLVER_STATUS_SUCCESS)
+      return CDMD_ERR_CUDA;
+  }
+  canonicalize_kernel<<<1, 32, 0, st>>>(ke, W.Wc, W.VR, model->sigma, dt, model->lambda,
+                                        model->omega, model->pair, W.SW, W.dinfo);
+  CU(cudaGetLastError());
+  // M (folded) = V S^-1 W
+  BL(cublasDgemm(h->blas, CUBLAS_OP_N, CUBLAS_OP_N, (int)n1, ke, ke, &one, W.V, (int)n1, W.SW, ke,
+                 &zero, model->Mfold, (int)n1));
+  // Gf = M^T (Y'^T Y') M, cf = M^T (Y'^T y1): Y'^T Y' = G + m + 1, Y'^T y1 = G + 1
+  BL(cublasDgemm(h->blas, CUBLAS_OP_N, CUBLAS_OP_N, (int)n1, ke, (int)n1, &one, W.G + m + 1, (int)m,
+                 model->Mfold, (int)n1, &zero, W.T2, (int)n1));
+  BL(cublasDgemm(h->blas, CUBLAS_OP_T, CUBLAS_OP_N, ke, ke, (int)n1, &one, model->Mfold, (int)n1,
+                 W.T2, (int)n1, &zero, W.Gf, ke));
+  BL(cublasDgemv(h->blas, CUBLAS_OP_T, (int)n1, ke, &one, model->Mfold, (int)n1, W.G + 1, 1, &zero,
+                 W.cf, 1));
+  omp_kernel<<<1, 256, 0, st>>>(ke, K, m, W.Gf, W.cf, W.G, model->pair, model->lambda, model->beta,
+                                model->support, model->coef, model->coef_col, W.dinfo);
+  CU(cudaGetLastError());
+  quantize_kernel<<<model->kpad, 256, 0, st>>>(model->Mfold, n1, ke, model->kpad, model->mpad,
+                                               model->Mq, model->Mq_scale);
+  CU(cudaGetLastError());
+  CU(cudaMemcpyAsync(model->dev_info, W.dinfo, sizeof(int32_t) * 8, cudaMemcpyDeviceToDevice, st));
+  CU(cudaMemcpyAsync(h->host_info, W.dinfo, sizeof(int) * 16, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  model->K_eff = h->host_info[INFO_K_SEL];
+  model->n_coef = h->host_info[INFO_N_COEF];
+  model->dt = dt;
+  model->info = h->host_info[9];
+  if (h->host_info[9] != 0) return CDMD_ERR_NUMERIC;
+  if (h->host_info[INFO_FLAGS] & FLAG_EIG_PAIRING) return CDMD_ERR_NUMERIC;
+  return CDMD_OK;
+}
+
+}  // namespace cdmd

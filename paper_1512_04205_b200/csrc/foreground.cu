@@ -1,0 +1,155 @@
+// foreground.cu — background reconstruction + residual + threshold + bit-pack
+// (Eq. DMDTerms, x_BG = Phi beta P:206-208, Eq. thres).
+//
+// The background of pixel j at frame t is a short real dot product over the
+// folded Phi columns the OMP support touches (cdmd_fit's coefficient table):
+//   L_jt = sum_f Phi[j, F_f] h_f(t),  h_f(t) = sum of Re / -sg Im of beta_p lambda_p^(t-1)
+// STATIC uses h_f(1) for every t.  mask_jt = [ |x_jt - L_jt| > tau ].
+// Layout: each lane owns pixels base + lane + 32 i (i < 4), so a warp ballot per
+// slot i yields one mask word (32 consecutive pixels) directly; X reads are
+// 32-B coalesced per slot.  One pass over X, mask written once.
+#include "common.cuh"
+
+namespace cdmd {
+
+constexpr int FG_FRAMES = 64;   // frames per block (grid y)
+
+template <int NC>
+__global__ void __launch_bounds__(256) foreground_dynamic_kernel(
+    const uint8_t* __restrict__ X, int64_t ld, int64_t n_local, int64_t m,
+    const float* __restrict__ Phi, int64_t ldphi, const float* __restrict__ coef,
+    const int32_t* __restrict__ coef_col, int n_coef, float tau, uint32_t* __restrict__ mask,
+    int64_t ldw) {
+  __shared__ float h[FG_FRAMES][NC];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t base = ((int64_t)blockIdx.x * 8 + warp) * 128;
+  const int64_t t0 = (int64_t)blockIdx.y * FG_FRAMES;
+  const int nt = (int)(m - t0 < FG_FRAMES ? m - t0 : FG_FRAMES);
+  for (int i = threadIdx.x; i < FG_FRAMES * NC; i += blockDim.x) {
+    const int tt = i / NC, f = i % NC;
+    h[tt][f] = (f < n_coef && tt < nt) ? coef[(int64_t)f * m + t0 + tt] : 0.f;
+  }
+  float ph[4][NC];
+#pragma unroll
+  for (int s = 0; s < 4; ++s) {
+    const int64_t j = base + lane + 32 * s;
+#pragma unroll
+    for (int f = 0; f < NC; ++f)
+      ph[s][f] = (f < n_coef && j < n_local) ? __ldg(Phi + j + (int64_t)coef_col[f] * ldphi) : 0.f;
+  }
+  __syncthreads();
+  if (base >= n_local) return;
+  for (int tt = 0; tt < nt; ++tt) {
+    const int64_t t = t0 + tt;
+    const uint8_t* __restrict__ xt = X + t * ld;
+    float xv[4];
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      const int64_t j = base + lane + 32 * s;
+      xv[s] = j < n_local ? (float)__ldg(xt + j) : 0.f;
+    }
+    float L[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int f = 0; f < NC; ++f) {
+      const float hf = h[tt][f];
+#pragma unroll
+      for (int s = 0; s < 4; ++s) L[s] = fmaf(ph[s][f], hf, L[s]);
+    }
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      const unsigned word = __ballot_sync(0xffffffffu, fabsf(xv[s] - L[s]) > tau);
+      const int64_t wi = (base >> 5) + s;
+      if (lane == s && 32 * wi < n_local) mask[t * ldw + wi] = word;
+    }
+  }
+}
+
+// STATIC: per pixel integer thresholds lo/hi with x > L + tau <=> x >= hi and
+// x < L - tau <=> x <= lo (x integer), then one pass over all m frames.
+__global__ void __launch_bounds__(256) foreground_static_kernel(
+    const uint8_t* __restrict__ X, int64_t ld, int64_t n_local, int64_t m,
+    const float* __restrict__ Phi, int64_t ldphi, const float* __restrict__ coef,
+    const int32_t* __restrict__ coef_col, int n_coef, float tau, uint32_t* __restrict__ mask,
+    int64_t ldw) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t base = ((int64_t)blockIdx.x * 8 + warp) * 128;
+  if (base >= n_local) return;
+  const int64_t t0 = (int64_t)blockIdx.y * FG_FRAMES;
+  const int64_t t1 = t0 + FG_FRAMES < m ? t0 + FG_FRAMES : m;
+  int lo[4], hi[4];
+#pragma unroll
+  for (int s = 0; s < 4; ++s) {
+    const int64_t j = base + lane + 32 * s;
+    float L = 0.f;
+    if (j < n_local)
+      for (int f = 0; f < n_coef; ++f) L = fmaf(__ldg(Phi + j + (int64_t)coef_col[f] * ldphi), coef[(int64_t)f * m], L);
+    const float a = floorf(L + tau) + 1.f, b = ceilf(L - tau) - 1.f;
+    hi[s] = (int)fminf(fmaxf(a, -1.f), 256.f);
+    lo[s] = (int)fminf(fmaxf(b, -1.f), 256.f);
+  }
+  for (int64_t t = t0; t < t1; ++t) {
+    const uint8_t* __restrict__ xt = X + t * ld;
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      const int64_t j = base + lane + 32 * s;
+      const int x = j < n_local ? (int)__ldg(xt + j) : 0;
+      const bool fg = j < n_local && (x >= hi[s] || x <= lo[s]);
+      const unsigned word = __ballot_sync(0xffffffffu, fg);
+      const int64_t wi = (base >> 5) + s;
+      if (lane == s && 32 * wi < n_local) mask[t * ldw + wi] = word;
+    }
+  }
+}
+
+template <int NC>
+static cudaError_t launch_dyn(const cdmd_video& v, const cdmd_model& M, const float* Phi,
+                              int64_t ldphi, float tau, uint32_t* mask, int64_t ldw, cudaStream_t st) {
+  dim3 grid((unsigned)ceil_div(v.n_local, 1024), (unsigned)ceil_div(v.m, FG_FRAMES));
+  foreground_dynamic_kernel<NC><<<grid, 256, 0, st>>>(v.X, v.ld, v.n_local, v.m, Phi, ldphi, M.coef,
+                                                      M.coef_col, M.n_coef, tau, mask, ldw);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_foreground(const cdmd_video& v, const cdmd_model& M, const float* Phi,
+                              int64_t ldphi, int mode, float tau, uint32_t* mask, int64_t ldw,
+                              cudaStream_t st) {
+  if (mode == CDMD_BG_STATIC) {
+    dim3 grid((unsigned)ceil_div(v.n_local, 1024), (unsigned)ceil_div(v.m, FG_FRAMES));
+    foreground_static_kernel<<<grid, 256, 0, st>>>(v.X, v.ld, v.n_local, v.m, Phi, ldphi, M.coef,
+                                                   M.coef_col, M.n_coef, tau, mask, ldw);
+    return cudaGetLastError();
+  }
+  const int nc = M.n_coef;
+  if (nc <= 4) return launch_dyn<4>(v, M, Phi, ldphi, tau, mask, ldw, st);
+  if (nc <= 8) return launch_dyn<8>(v, M, Phi, ldphi, tau, mask, ldw, st);
+  if (nc <= 12) return launch_dyn<12>(v, M, Phi, ldphi, tau, mask, ldw, st);
+  if (nc <= 16) return launch_dyn<16>(v, M, Phi, ldphi, tau, mask, ldw, st);
+  if (nc <= 24) return launch_dyn<24>(v, M, Phi, ldphi, tau, mask, ldw, st);
+  if (nc <= 32) return launch_dyn<32>(v, M, Phi, ldphi, tau, mask, ldw, st);
+  return launch_dyn<64>(v, M, Phi, ldphi, tau, mask, ldw, st);
+}
+
+// Background frames t0+1 .. t0+nt (inspection path of cdmd_background).
+__global__ void background_kernel(const float* __restrict__ Phi, int64_t ldphi, int64_t n_local,
+                                  int64_t m, const float* __restrict__ coef,
+                                  const int32_t* __restrict__ coef_col, int n_coef, int dynamic,
+                                  int64_t t0, int64_t nt, float* __restrict__ L, int64_t ldl) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t tt = blockIdx.y;
+  if (j >= n_local || tt >= nt) return;
+  const int64_t t = dynamic ? t0 + tt : 0;
+  float acc = 0.f;
+  for (int f = 0; f < n_coef; ++f) acc = fmaf(Phi[j + (int64_t)coef_col[f] * ldphi], coef[(int64_t)f * m + t], acc);
+  L[tt * ldl + j] = acc;
+}
+
+cudaError_t launch_background(const float* Phi, int64_t ldphi, int64_t n_local, const cdmd_model& M,
+                              int mode, int64_t t0, int64_t nt, float* L, int64_t ldl,
+                              cudaStream_t st) {
+  dim3 grid((unsigned)ceil_div(n_local, 256), (unsigned)nt);
+  background_kernel<<<grid, 256, 0, st>>>(Phi, ldphi, n_local, M.m, M.coef, M.coef_col, M.n_coef,
+                                          mode == CDMD_BG_DYNAMIC, t0, nt, L, ldl);
+  return cudaGetLastError();
+}
+
+}  // namespace cdmd

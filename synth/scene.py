@@ -123,8 +123,11 @@ def _scene(cfg_w, cfg_h, m, seed, n_rects, flicker):
 
 
 def make_video(width, height, m, seed, noise=2.0, n_rects=2, flicker=False,
-               pix0=0, n_local=None, periodic=True):
+               pix0=0, n_local=None, periodic=True, threads=None):
     """Return uint8 array (m, n_local): frame t holds global pixels [pix0, pix0+n_local)."""
+    from concurrent.futures import ThreadPoolExecutor
+    import os
+
     n = width * height
     n_local = n - pix0 if n_local is None else n_local
     sc = _scene(width, height, m, seed, n_rects, flicker)
@@ -134,32 +137,45 @@ def make_video(width, height, m, seed, noise=2.0, n_rects=2, flicker=False,
     b1_ = (r1 + ROWBLK - 1) // ROWBLK
     R0, R1 = b0 * ROWBLK, min(height, b1_ * ROWBLK)
     a = sc.a[R0:R1]
-    pb1 = sc.b1[R0:R1] if periodic else 0 * a
-    pb2 = sc.b2[R0:R1] if periodic else 0 * a
+    z = np.zeros_like(a)
+    pb1 = sc.b1[R0:R1] if periodic else z
+    pb2 = sc.b2[R0:R1] if periodic else z
     ff = sc.f[R0:R1]
-    ys = np.arange(R0, R1)[:, None]
-    xs = np.arange(width)[None, :]
-    out = np.empty((m, n_local), dtype=np.uint8)
-    off = pix0 - R0 * width
     cos4 = [1, 0, -1, 0]
     sin4 = [0, 1, 0, -1]
-    for t in range(m):
-        fr = a + cos4[t % 4] * pb1 + sin4[t % 4] * pb2 + (1 - 2 * (t % 2)) * ff
+    # the four (eight with flicker) distinct noiseless background frames
+    base = {}
+    for ph in range(4):
+        for fl in (0, 1):
+            base[(ph, fl)] = (a + cos4[ph] * pb1 + sin4[ph] * pb2 + (1 - 2 * fl) * ff).astype(np.float32)
+    out = np.empty((m, n_local), dtype=np.uint8)
+    off = pix0 - R0 * width
+
+    def frame(t):
+        fr = base[(t % 4, t % 2)].copy()
         if noise > 0:
-            nz = np.empty_like(fr)
             for b in range(b0, b1_):
                 lo, hi = b * ROWBLK - R0, min(R1, (b + 1) * ROWBLK) - R0
                 g = np.random.default_rng([seed, 7, t, b])
-                nz[lo:hi] = g.standard_normal((hi - lo, width), dtype=np.float32) * noise
-            fr = fr + nz
+                fr[lo:hi] += g.standard_normal((hi - lo, width), dtype=np.float32) * np.float32(noise)
         for (cx, cy, vx, vy, w, h) in sc.rects:
             x0 = int(round(cx + vx * t - w / 2))
             y0 = int(round(cy + vy * t - h / 2))
-            ins = (xs >= x0) & (xs < x0 + w) & (ys >= y0) & (ys < y0 + h)
-            if ins.any():
-                fr = np.where(ins, 250.0, fr)
-        fr = np.clip(np.rint(fr), 0, 255).astype(np.uint8).reshape(-1)
-        out[t] = fr[off:off + n_local]
+            xa, xb = max(0, x0), min(width, x0 + w)
+            ya, yb = max(R0, y0), min(R1, y0 + h)
+            if xa < xb and ya < yb:
+                fr[ya - R0:yb - R0, xa:xb] = 250.0
+        np.rint(fr, out=fr)
+        np.clip(fr, 0, 255, out=fr)
+        out[t] = fr.reshape(-1)[off:off + n_local].astype(np.uint8)
+
+    nthreads = threads or min(16, os.cpu_count() or 1)
+    if m * n_local < (1 << 20) or nthreads == 1:
+        for t in range(m):
+            frame(t)
+    else:
+        with ThreadPoolExecutor(nthreads) as ex:
+            list(ex.map(frame, range(m)))
     return out
 
 

@@ -1,0 +1,87 @@
+"""Multi-process (gloo, world_size 2, CPU) coverage of the pixel-sharded path's
+host logic: slab partition + the one all-reduce of the partial sketches.  The
+per-slab partial sketches come from the oracle here (no GPU); the GPU ranks run
+the same partition with libcdmd."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_1512_04205_b200.dist import allreduce_sum, slab
+
+
+def test_slab_partition_properties():
+    for n in [768, 76800, 345600, 2073600, 8294400, 1000, 129]:
+        for world in [1, 2, 3, 4, 8]:
+            parts = [slab(n, world, r) for r in range(world)]
+            assert parts[0][0] == 0
+            for (a, na), (b, _) in zip(parts, parts[1:]):
+                assert a + na == b
+            assert parts[-1][0] + parts[-1][1] == n
+            assert all(p0 % 128 == 0 for p0, _ in parts)
+            sizes = [na for _, na in parts]
+            assert max(sizes) - min(sizes) <= 128
+    assert slab(2073600, 8, 3) == (3 * 259200, 259200)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, kind, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import sensing as S
+        from synth.scene import make_video
+        W, H, m, p = 48, 40, 12, 30
+        n = W * H
+        pix0, nl = slab(n, world, rank)
+        Xs = make_video(W, H, m, seed=3, noise=2.0, n_rects=1, pix0=pix0, n_local=nl)
+        Y = S.sketch(Xs, kind, p, seed=7, n_total=n, pix0=pix0)
+        t = torch.from_numpy(np.ascontiguousarray(Y))
+        allreduce_sum(t)
+        if rank == 0:
+            out.put(t.numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("kind", [0, 1, 2])
+def test_two_rank_allreduce_equals_single_rank(kind):
+    from oracle import sensing as S
+    from synth.scene import make_video
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_worker, args=(r, 2, port, kind, q)) for r in range(2)]
+    for p_ in ps:
+        p_.start()
+    got = q.get(timeout=120)
+    for p_ in ps:
+        p_.join(timeout=60)
+        assert p_.exitcode == 0
+    X = make_video(48, 40, 12, seed=3, noise=2.0, n_rects=1)
+    want = S.sketch(X, kind, 30, seed=7)
+    assert np.array_equal(got, want)   # integer sketches: bit-identical across world sizes
+
+
+def test_slab_generation_is_consistent():
+    # each rank generates exactly its own bytes of the same global video
+    from synth.scene import make_video
+    X = make_video(200, 70, 6, seed=5, noise=2.0, n_rects=2)
+    n = X.shape[1]
+    for world in (2, 3):
+        parts = [make_video(200, 70, 6, seed=5, noise=2.0, n_rects=2, pix0=p0, n_local=nl)
+                 for p0, nl in (slab(n, world, r) for r in range(world))]
+        assert np.array_equal(np.concatenate(parts, axis=1), X)

@@ -1,0 +1,307 @@
+"""GPU (libcdmd, sm_100a) vs CPU oracle parity on identical seeded inputs.
+
+Every call goes through the C ABI (paper_1512_04205_b200.cdmd is ctypes only).
+Tolerances: tests/parity.py (north_star).  Sizes: small cases the oracle runs in
+seconds that still span several tiles and ragged tails, plus the bench's full
+1080p configuration checked exactly (integer sketch) or on sampled outputs.
+"""
+
+import zlib
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import cdmd as OD
+from oracle import sensing as OS
+from synth.scene import config_by_name, make_video, video_for
+import parity as PT  # tests/parity.py (tests/ is on sys.path under pytest)
+
+pytestmark = pytest.mark.gpu
+
+KIND = {"spixel": 0, "sparse": 1, "rademacher": 2, "gaussian": 3}
+
+
+@pytest.fixture(scope="module")
+def C():
+    from paper_1512_04205_b200 import cdmd
+    return cdmd
+
+
+@pytest.fixture(scope="module")
+def H(C):
+    return C.Handle(0)
+
+
+def to_dev(X, ld=None):
+    m, n = X.shape
+    ld = ((n + 15) // 16) * 16 if ld is None else ld
+    buf = torch.zeros((m, ld), dtype=torch.uint8, device="cuda")
+    buf[:, :n] = torch.from_numpy(X).cuda()
+    return buf
+
+
+def gpu_run(C, H, X, kind, p, k, K, tau, s=0.0, seed=0, modes_simt=False, ld=None):
+    m, n = X.shape
+    Xd = to_dev(X, ld)
+    P = C.Pipeline(H, n, n, m, kind, p, k, K, s=s, seed=seed)
+    Y = P.sketch(Xd).cpu().numpy().T.copy()          # p x m
+    P.fit()
+    mh = C.model_to_host(P.model)
+    Phi = P.modes(Xd, simt=modes_simt).cpu().numpy()  # k_eff x n folded
+    out = dict(Y=Y, model=mh, Phi=Phi)
+    for mode, name in ((C.BG_DYNAMIC, "dyn"), (C.BG_STATIC, "sta")):
+        Wd = P.foreground(Xd, tau, mode).cpu().numpy().view(np.uint32)
+        out["mask_" + name] = OD.unpack_mask(Wd, n)
+        out["L_" + name] = P.background(mode).cpu().numpy()   # (m, n) frame-major
+    torch.cuda.synchronize()
+    out["P"], out["Xd"] = P, Xd
+    return out
+
+
+def oracle_run(X, kind, p, k, K, tau, s=None, seed=0):
+    Y = OS.sketch(X, KIND[kind], p, seed, s=s)
+    model = OD.fit(Y, k, K)
+    Phi = OD.modes(X, model["M"])
+    Ld = OD.background_dynamic(Phi, model)          # n x m
+    Ls = OD.background_static(Phi, model)           # n
+    Xf = X.astype(np.float64)
+    return dict(Y=Y, model=model, Phi=Phi, L_dyn=Ld.T, L_sta=Ls,
+                res_dyn=np.abs(Xf - Ld.T), res_sta=np.abs(Xf - Ls[None, :]),
+                mask_dyn=OD.mask(X, Ld, tau), mask_sta=OD.mask(X, Ls, tau))
+
+
+def check_all(g, o, kind, tau):
+    # sketch
+    if kind == "gaussian":
+        d = np.linalg.norm(g["Y"] - o["Y"], axis=0) / np.linalg.norm(o["Y"], axis=0)
+        assert d.max() <= PT.RTOL_Y_GAUSS, d.max()
+    else:
+        assert g["Y"].dtype == np.int32 or g["Y"].dtype == np.int64
+        assert np.array_equal(g["Y"].astype(np.int64), o["Y"])
+    gm, om = g["model"], o["model"]
+    assert gm["k_eff"] == om["k_eff"]
+    perm, err = PT.match_eigs(gm["lam"], om["lam"])
+    assert err <= PT.RTOL_EIG, err
+    s_rel = np.abs(gm["sigma"] - om["sigma"]) / om["sigma"]
+    assert s_rel.max() <= 1e-6, s_rel.max()
+    assert list(gm["pair"]) == list(om["pair"]) or sorted(gm["pair"]) == sorted(om["pair"])
+    # modes, per column after phase alignment, well-separated eigenvalues only
+    Pg = PT.unfold(g["Phi"], gm["pair"])
+    for i in range(gm["k_eff"]):
+        j = perm[i]
+        if not PT.well_separated(om["lam"], j):
+            continue
+        r = PT.phase_aligned_rel(Pg[:, i], o["Phi"][:, j])
+        assert r <= PT.RTOL_PHI, (i, j, r)
+    # OMP support (modulo conjugation)
+    assert gm["K_eff"] == len(om["support"])
+    assert PT.supports_equal_mod_conj(gm["support"], gm["lam"], om["support"], om["lam"])
+    # backgrounds
+    scale = max(1.0, np.abs(o["L_dyn"]).max())
+    assert np.abs(g["L_dyn"] - o["L_dyn"]).max() <= 1e-4 * scale
+    assert np.abs(g["L_sta"][0] - o["L_sta"]).max() <= 1e-4 * scale
+    # masks
+    for name in ("dyn", "sta"):
+        frac, band, nd = PT.mask_agreement(g["mask_" + name], o["mask_" + name], o["res_" + name], tau)
+        assert frac >= PT.MASK_AGREE and band, (name, frac, nd)
+
+
+# ------------------------------------------------------------- generator pins
+def test_philox_known_answers(C):
+    ctr32 = torch.tensor(np.array([[0, 0, 0, 0], [0xffffffff] * 4,
+                                   [0x243f6a88, 0x85a308d3, 0x13198a2e, 0x03707344]], dtype=np.uint32).view(np.int32),
+                         device="cuda")
+    keys = [(0, 0), (0xffffffff, 0xffffffff), (0xa4093822, 0x299f31d0)]
+    want = [[0x6627e8d5, 0xe169c58d, 0xbc57ac4c, 0x9b00dbd8], [0x408f276d, 0x41c83b0e, 0xa20bc7c6, 0x6d5451fd],
+            [0xd16cfe09, 0x94fdcceb, 0x5001e420, 0x24126ea1]]
+    for i, (k0, k1) in enumerate(keys):
+        out = torch.zeros(4, dtype=torch.int32, device="cuda")
+        C.cdmd_philox(ctr32[i].contiguous(), k0, k1, out)
+        assert out.cpu().numpy().view(np.uint32).tolist() == want[i]
+
+
+def test_philox_random_counters_match_oracle(C):
+    from oracle.philox import philox4x32_10
+    rng = np.random.default_rng(0)
+    c = rng.integers(0, 2 ** 32, size=(4096, 4), dtype=np.uint64)
+    out = torch.zeros(4096 * 4, dtype=torch.int32, device="cuda")
+    C.cdmd_philox(torch.from_numpy(c.astype(np.uint32).view(np.int32)).cuda().reshape(-1), 123, 456, out)
+    got = out.cpu().numpy().view(np.uint32).reshape(4096, 4)
+    w = philox4x32_10(c[:, 0], c[:, 1], c[:, 2], c[:, 3], 123, 456)
+    assert np.array_equal(got, np.stack(w, 1).astype(np.uint32))
+
+
+def test_gaussian_table_bit_exact(C, H):
+    out = torch.zeros(65536, dtype=torch.int16, device="cuda")
+    C.cdmd_gaussian_table(H, out)
+    bits = out.cpu().numpy().view(np.uint16).astype(np.uint32) << 16
+    got = bits.view(np.float32).astype(np.float64)
+    assert np.array_equal(got, OS.gaussian_table())
+
+
+@pytest.mark.parametrize("n,p,seed", [(1, 1, 0), (768, 768, 3), (76800, 1000, 0), (2073600, 2000, 0),
+                                      (8294400, 4000, 9), (1000, 999, 5)])
+def test_spixel_rows_bit_exact(C, H, n, p, seed):
+    out = torch.zeros(p, dtype=torch.int32, device="cuda")
+    C.cdmd_sensing_rows(H, n, C.sensing("spixel", p, 0, seed), out)
+    assert np.array_equal(out.cpu().numpy().astype(np.int64), OS.spixel_rows(n, p, seed))
+
+
+@pytest.mark.parametrize("n,p,s,seed", [(768, 50, 0.0, 0), (3700, 120, 0.0, 1), (2073600, 2000, 0.0, 0),
+                                        (5000, 64, 3.5, 2), (8294400, 400, 0.0, 0)])
+def test_sparse_rows_bit_exact(C, H, n, p, s, seed):
+    cap = C.cdmd_sparse_cap(n, p, s)
+    ell = torch.zeros(p * cap, dtype=torch.int32, device="cuda")
+    cnt = torch.zeros(p, dtype=torch.int32, device="cuda")
+    C.cdmd_sensing_rows(H, n, C.sensing("sparse", p, s, seed), ell, cnt)
+    ell = ell.cpu().numpy().reshape(p, cap)
+    cnt = cnt.cpu().numpy()
+    rows = OS.sparse_rows(n, p, s if s > 0 else OS.default_s(n), seed)
+    for r in range(p):
+        pos, sg = rows[r]
+        assert cnt[r] == len(pos)
+        e = ell[r, :cnt[r]].astype(np.int64)
+        assert np.array_equal(e >> 1, pos)
+        assert np.array_equal(np.where(e & 1, -1, 1), sg)
+
+
+# ------------------------------------------------------- whole-path parity
+CASES = [
+    # name, (W, H, m, noise, rects), kind, p, k, K, tau
+    ("c1", None, "sparse", 50, 10, 2, 25.0),
+    ("ragged_sparse", (100, 37, 33, 2.0, 1), "sparse", 120, 12, 5, 20.0),
+    ("ragged_spixel", (97, 61, 45, 2.0, 2), "spixel", 400, 15, 6, 25.0),
+    ("rademacher_small", (180, 120, 60, 2.0, 2), "rademacher", 300, 20, 6, 25.0),
+    ("gaussian_small", (160, 100, 50, 2.0, 1), "gaussian", 256, 16, 6, 25.0),
+]
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
+def test_pipeline_parity_small(C, H, case):
+    name, shape, kind, p, k, K, tau = case
+    if shape is None:
+        cfg = config_by_name("c1_32x24_sparse")
+        X = video_for(cfg)
+    else:
+        W, Hh, m, noise, rects = shape
+        X = make_video(W, Hh, m, seed=zlib.crc32(name.encode()) % 1000, noise=noise, n_rects=rects)
+    g = gpu_run(C, H, X, kind, p, k, K, tau)
+    o = oracle_run(X, kind, p, k, K, tau)
+    check_all(g, o, kind, tau)
+
+
+def test_c2_full_parity(C, H):
+    cfg = config_by_name("c2_320x240_spixel")
+    X = video_for(cfg)
+    g = gpu_run(C, H, X, cfg.kind, cfg.p, cfg.k, cfg.K, cfg.tau)
+    o = oracle_run(X, cfg.kind, cfg.p, cfg.k, cfg.K, cfg.tau)
+    check_all(g, o, cfg.kind, cfg.tau)
+
+
+def test_modes_tensor_core_equals_simt(C, H):
+    X = make_video(333, 200, 77, seed=4, noise=2.0, n_rects=2)   # ragged n, ragged m
+    m, n = X.shape
+    Xd = to_dev(X)
+    P = C.Pipeline(H, n, n, m, "sparse", 200, 24, 6)
+    P.sketch(Xd)
+    P.fit()
+    a = P.modes(Xd).clone()
+    b = P.modes(Xd, simt=True).clone()
+    assert torch.equal(a, b)
+
+
+def test_sketch_slabs_sum_to_full(C, H):
+    X = make_video(256, 90, 20, seed=8, noise=2.0, n_rects=1)
+    m, n = X.shape
+    for kind in ("spixel", "sparse", "rademacher"):
+        full = C.Pipeline(H, n, n, m, kind, 64, 8, 2)
+        full.sketch(to_dev(X))
+        acc = torch.zeros_like(full.Y)
+        for p0, nl in [(0, 128 * 60), (128 * 60, n - 128 * 60)]:
+            P = C.Pipeline(H, n, nl, m, kind, 64, 8, 2, pix0=p0)
+            acc += P.sketch(to_dev(X[:, p0:p0 + nl])).clone()
+        assert torch.equal(acc, full.Y)
+
+
+def test_c3_rademacher_full_size_sampled_rows(C, H):
+    cfg = config_by_name("c3_720x480_rademacher")
+    X = video_for(cfg)
+    m, n = X.shape
+    P = C.Pipeline(H, n, n, m, "rademacher", cfg.p, cfg.k, cfg.K)
+    Y = P.sketch(to_dev(X)).cpu().numpy().T
+    rows = [0, 1, 777, cfg.p - 1]
+    want = OS.sketch(X, OS.RADEMACHER, cfg.p, 0, rows=rows)
+    assert np.array_equal(Y[rows].astype(np.int64), want)
+
+
+def test_c4_gaussian_full_size_sampled_rows(C, H):
+    cfg = config_by_name("c4_1080p_gaussian")
+    X = video_for(cfg)
+    m, n = X.shape
+    P = C.Pipeline(H, n, n, m, "gaussian", cfg.p, cfg.k, cfg.K)
+    Y = P.sketch(to_dev(X)).cpu().numpy().T.astype(np.float64)
+    rows = [0, 1999]
+    want = OS.sketch(X, OS.GAUSSIAN, cfg.p, 0, rows=rows, chunk=1 << 18)
+    d = np.linalg.norm(Y[rows] - want, axis=1) / np.linalg.norm(want, axis=1)
+    assert d.max() <= PT.RTOL_Y_GAUSS
+
+
+def test_c4_sparse_full_size(C, H):
+    """The bench configuration, in the bench's launch configuration."""
+    cfg = config_by_name("c4_1080p_sparse")
+    X = video_for(cfg)
+    m, n = X.shape
+    Xd = to_dev(X)
+    P = C.Pipeline(H, n, n, m, "sparse", cfg.p, cfg.k, cfg.K)
+    Yg = P.sketch(Xd).cpu().numpy().T.astype(np.int64)
+    Yo = OS.sketch(X, OS.SPARSE, cfg.p, 0)
+    assert np.array_equal(Yg, Yo)
+    P.fit()
+    gm = C.model_to_host(P.model)
+    om = OD.fit(Yo, cfg.k, cfg.K)
+    assert gm["k_eff"] == om["k_eff"]
+    perm, err = PT.match_eigs(gm["lam"], om["lam"])
+    assert err <= PT.RTOL_EIG
+    assert PT.supports_equal_mod_conj(gm["support"], gm["lam"], om["support"], om["lam"])
+    Phi = P.modes(Xd)
+    mask = P.foreground(Xd, cfg.tau, C.BG_DYNAMIC).cpu().numpy().view(np.uint32)
+    torch.cuda.synchronize()
+    # sampled pixels: oracle Phi rows and background for 4096 random pixels + a ragged tail
+    rng = np.random.default_rng(0)
+    pix = np.unique(np.concatenate([rng.choice(n, 4096, replace=False), np.arange(n - 40, n)]))
+    Po = X[1:, pix].T.astype(np.float64) @ om["M"]                    # |pix| x k
+    Pg = PT.unfold(Phi.cpu().numpy()[:, pix], gm["pair"])
+    for i in range(gm["k_eff"]):
+        j = perm[i]
+        if PT.well_separated(om["lam"], j):
+            assert PT.phase_aligned_rel(Pg[:, i], Po[:, j]) <= PT.RTOL_PHI
+    Ld = OD.background_dynamic(Po, om)                                # |pix| x m
+    res = np.abs(X[:, pix].astype(np.float64) - Ld.T)
+    mo = res > cfg.tau
+    mg = OD.unpack_mask(mask, n)[:, pix]
+    frac, band, nd = PT.mask_agreement(mg, mo, res, cfg.tau)
+    assert frac >= PT.MASK_AGREE and band, (frac, nd)
+
+
+def test_errors_are_reported_not_launched(C, H):
+    X = to_dev(make_video(64, 32, 10, seed=1, noise=1.0, n_rects=0))
+    v = C.video(X)
+    Y = torch.zeros((10, 100), dtype=torch.int32, device="cuda")
+    ws = torch.zeros(1 << 20, dtype=torch.uint8, device="cuda")
+    with pytest.raises(C.CdmdError) as e:
+        C.cdmd_sketch(H, v, C.sensing("sparse", 5000), Y, ws)     # p > n
+    assert e.value.code == 2
+    with pytest.raises(C.CdmdError) as e:
+        C.cdmd_sketch(H, v, C.sensing("sparse", 50, 0.5), Y, ws)  # s <= 1
+    assert e.value.code == 2
+    P = C.Pipeline(H, 2048, 2048, 10, "sparse", 50, 8, 2)
+    P.sketch(X)
+    with pytest.raises(C.CdmdError) as e:
+        C.cdmd_fit(H, P.Y, "sparse", 50, 10, 10, 2, P.model, P.ws_fit)   # k > m - 1
+    assert e.value.code == 2
+    P.fit()
+    P.modes(X)
+    with pytest.raises(C.CdmdError) as e:
+        C.cdmd_foreground(H, v, P.model, P.Phi, C.BG_DYNAMIC, 0.0, P.mask)  # tau <= 0
+    assert e.value.code == 2
