@@ -20,6 +20,7 @@
 #include <cusolverDn.h>
 #include <math.h>
 #include <stdio.h>
+#include <stdlib.h>
 
 #include "handle.h"
 
@@ -453,6 +454,32 @@ __global__ void quantize_kernel(const double* __restrict__ Mf, int64_t n1, int k
   }
 }
 
+// Optional substep timing (env CDMD_PROFILE_FIT=1): CUDA events, printed to stderr.
+struct FitProf {
+  bool on = false;
+  cudaStream_t st = nullptr;
+  cudaEvent_t ev[16];
+  const char* name[16];
+  int n = 0;
+  void mark(const char* nm) {
+    if (!on || n >= 16) return;
+    cudaEventCreate(&ev[n]);
+    cudaEventRecord(ev[n], st);
+    name[n++] = nm;
+  }
+  void report() {
+    if (!on || n < 2) return;
+    cudaEventSynchronize(ev[n - 1]);
+    for (int i = 1; i < n; ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ev[i - 1], ev[i]);
+      fprintf(stderr, "[cdmd_fit] %-12s %8.3f ms\n", name[i], ms);
+    }
+    for (int i = 0; i < n; ++i) cudaEventDestroy(ev[i]);
+    n = 0;
+  }
+};
+
 #define BL(x)                                             \
   do {                                                    \
     if ((x) != CUBLAS_STATUS_SUCCESS) return CDMD_ERR_CUDA; \
@@ -470,6 +497,10 @@ cdmd_status fit_impl(cdmd_handle h, const void* Y, int64_t ldy, int kind, int64_
   if (s0 != CDMD_OK) return s0;
   if (ws_bytes < W.total) return CDMD_ERR_WORKSPACE;
   const int64_t n1 = m - 1;
+  FitProf prof;
+  prof.on = getenv("CDMD_PROFILE_FIT") != nullptr;
+  prof.st = st;
+  prof.mark("start");
   BL(cublasSetStream(h->blas, st));
   if (cusolverDnSetStream(h->solver, st) != CUSOLVER_STATUS_SUCCESS) return CDMD_ERR_CUDA;
   CU(cudaMemsetAsync(W.dinfo, 0, sizeof(int) * 16, st));
@@ -484,12 +515,14 @@ cdmd_status fit_impl(cdmd_handle h, const void* Y, int64_t ldy, int kind, int64_
     CU(cudaGetLastError());
   }
   const double one = 1.0, zero = 0.0;
+  prof.mark("to_f64");
   // G = Y_full^T Y_full
   BL(cublasDgemm(h->blas, CUBLAS_OP_T, CUBLAS_OP_N, (int)m, (int)m, (int)p, &one, W.Yd, (int)p,
                  W.Yd, (int)p, &zero, W.G, (int)m));
   // A = Y^T Y = G[0:m-1, 0:m-1]
   CU(cudaMemcpy2DAsync(W.A, sizeof(double) * n1, W.G, sizeof(double) * m, sizeof(double) * n1, n1,
                        cudaMemcpyDeviceToDevice, st));
+  prof.mark("gram");
   size_t hneed = W.sy_host_bytes > W.ge_host_bytes ? W.sy_host_bytes : W.ge_host_bytes;
   if (h->host_ws.size() < hneed + 16) h->host_ws.resize(hneed + 16);
   if (cusolverDnXsyevd(h->solver, h->params, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n1,
@@ -497,10 +530,12 @@ cdmd_status fit_impl(cdmd_handle h, const void* Y, int64_t ldy, int kind, int64_
                        W.sy_host_bytes ? h->host_ws.data() : nullptr, W.sy_host_bytes,
                        W.dinfo + 8) != CUSOLVER_STATUS_SUCCESS)
     return CDMD_ERR_CUDA;
+  prof.mark("syevd");
   select_topk_kernel<<<k, 128, 0, st>>>(W.A, W.w, n1, k, W.V, model->sigma, W.dinfo);
   CU(cudaGetLastError());
   CU(cudaMemcpyAsync(h->host_info, W.dinfo, sizeof(int) * 16, cudaMemcpyDeviceToHost, st));
   CU(cudaStreamSynchronize(st));
+  prof.mark("select+sync");
   if (h->host_info[8] != 0) {
     model->info = h->host_info[8];
     return CDMD_ERR_NUMERIC;
@@ -515,6 +550,7 @@ cdmd_status fit_impl(cdmd_handle h, const void* Y, int64_t ldy, int kind, int64_
                  (int)n1, &zero, W.B, ke));
   scale_atilde_kernel<<<ke, ke <= 1024 ? ((ke + 31) / 32) * 32 : 1024, 0, st>>>(W.B, model->sigma, ke);
   CU(cudaGetLastError());
+  prof.mark("atilde");
   // eig(A~): real nonsymmetric, LAPACK-style output (pairs as Re/Im columns)
   {
     size_t d = 0, hb = 0;
@@ -531,6 +567,7 @@ cdmd_status fit_impl(cdmd_handle h, const void* Y, int64_t ldy, int kind, int64_
                         hb ? h->host_ws.data() : nullptr, hb, W.dinfo + 9) != CUSOLVER_STATUS_SUCCESS)
       return CDMD_ERR_CUDA;
   }
+  prof.mark("geev");
   canonicalize_kernel<<<1, 32, 0, st>>>(ke, W.Wc, W.VR, model->sigma, dt, model->lambda,
                                         model->omega, model->pair, W.SW, W.dinfo);
   CU(cudaGetLastError());
@@ -544,15 +581,19 @@ cdmd_status fit_impl(cdmd_handle h, const void* Y, int64_t ldy, int kind, int64_
                  W.T2, (int)n1, &zero, W.Gf, ke));
   BL(cublasDgemv(h->blas, CUBLAS_OP_T, (int)n1, ke, &one, model->Mfold, (int)n1, W.G + 1, 1, &zero,
                  W.cf, 1));
+  prof.mark("canon+M+gram");
   omp_kernel<<<1, 256, 0, st>>>(ke, K, m, W.Gf, W.cf, W.G, model->pair, model->lambda, model->beta,
                                 model->support, model->coef, model->coef_col, W.dinfo);
   CU(cudaGetLastError());
+  prof.mark("omp+coef");
   quantize_kernel<<<model->kpad, 256, 0, st>>>(model->Mfold, n1, ke, model->kpad, model->mpad,
                                                model->Mq, model->Mq_scale);
   CU(cudaGetLastError());
   CU(cudaMemcpyAsync(model->dev_info, W.dinfo, sizeof(int32_t) * 8, cudaMemcpyDeviceToDevice, st));
   CU(cudaMemcpyAsync(h->host_info, W.dinfo, sizeof(int) * 16, cudaMemcpyDeviceToHost, st));
   CU(cudaStreamSynchronize(st));
+  prof.mark("quant+sync");
+  prof.report();
   model->K_eff = h->host_info[INFO_K_SEL];
   model->n_coef = h->host_info[INFO_N_COEF];
   model->dt = dt;

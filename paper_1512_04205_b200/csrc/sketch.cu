@@ -6,7 +6,8 @@
 // Single pixel / sparse: HBM sector-gather bound (one 32-B sector per (entry,
 // frame)); integer sums are exact in int32 (|Y| <= 255 n < 2^31 for n <= 8.4e6).
 // Rademacher: int8 x uint8 dot products (dp4a here; tcgen05 kind::i8 in
-// sketch_tc.cu).  Gaussian: fp32 accumulation of exact bf16 x uint8 products.
+// sketch_tc.cu).  Gaussian: exact bf16 x uint8 products, fp32 partial sums over
+// short pixel chunks accumulated in fp64, one rounding to fp32 Y at the end.
 #include "common.cuh"
 
 namespace cdmd {
@@ -176,8 +177,9 @@ __global__ void __launch_bounds__(256) sketch_gaussian_simt_kernel(
   const int tid = threadIdx.x;
   const int tx = tid & 15, ty = tid >> 4;
   const int64_t r0 = (int64_t)blockIdx.x * 64, f0 = (int64_t)blockIdx.y * 64;
-  float acc[4][4] = {};
+  double acc64[4][4] = {};
   for (int64_t c0 = 0; c0 < n_local; c0 += 32) {
+    float acc[4][4] = {};
     __syncthreads();
     {  // 64 rows x 4 groups of 8 pixels: one Philox call per thread
       const int rr = tid >> 2, g = tid & 3;
@@ -211,13 +213,18 @@ __global__ void __launch_bounds__(256) sketch_gaussian_simt_kernel(
 #pragma unroll
         for (int w2 = 0; w2 < 4; ++w2) acc[u][w2] = fmaf(a[u], b[w2], acc[u][w2]);
     }
+    // fp32 partial sums of 32 exact products, accumulated across chunks in fp64
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int w2 = 0; w2 < 4; ++w2) acc64[u][w2] += (double)acc[u][w2];
   }
 #pragma unroll
   for (int a = 0; a < 4; ++a)
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
       const int64_t r = r0 + ty * 4 + a, t = f0 + tx * 4 + b;
-      if (r < p && t < m) Y[r + t * ldy] = acc[a][b];
+      if (r < p && t < m) Y[r + t * ldy] = (float)acc64[a][b];
     }
 }
 

@@ -54,11 +54,14 @@ def well_separated(lam, i, tol=1e-8):
     return all(abs(lam[i] - lam[j]) > tol * max(1.0, abs(lam[i])) for j in range(len(lam)) if j != i)
 
 
-def supports_equal_mod_conj(sup_gpu, lam_gpu, sup_ref, lam_ref, tol=1e-6):
-    """Supports as eigenvalue sets, a mode and its conjugate counted as one unit."""
-    def units(sup, lam):
-        return sorted((round(abs(lam[s]), 9), round(abs(lam[s].imag), 9)) for s in sup)
-    return units(sup_gpu, lam_gpu) == units(sup_ref, lam_ref)
+def supports_equal_mod_conj(sup_gpu, pair_gpu, perm, sup_ref, pair_ref):
+    """Supports compared as sets of eigen-units (a mode and its conjugate partner
+    are one unit), GPU indices mapped to oracle indices by eigenvalue matching."""
+    def unit(i, pair):
+        return i - 1 if pair[i] < 0 else i
+    g = sorted(unit(perm[i], pair_ref) for i in sup_gpu)
+    o = sorted(unit(i, pair_ref) for i in sup_ref)
+    return g == o
 
 
 def mask_agreement(mask_gpu, mask_ref, resid_ref, tau):

@@ -96,7 +96,7 @@ def check_all(g, o, kind, tau):
         assert r <= PT.RTOL_PHI, (i, j, r)
     # OMP support (modulo conjugation)
     assert gm["K_eff"] == len(om["support"])
-    assert PT.supports_equal_mod_conj(gm["support"], gm["lam"], om["support"], om["lam"])
+    assert PT.supports_equal_mod_conj(gm["support"], gm["pair"], perm, om["support"], om["pair"])
     # backgrounds
     scale = max(1.0, np.abs(o["L_dyn"]).max())
     assert np.abs(g["L_dyn"] - o["L_dyn"]).max() <= 1e-4 * scale
@@ -263,7 +263,7 @@ def test_c4_sparse_full_size(C, H):
     assert gm["k_eff"] == om["k_eff"]
     perm, err = PT.match_eigs(gm["lam"], om["lam"])
     assert err <= PT.RTOL_EIG
-    assert PT.supports_equal_mod_conj(gm["support"], gm["lam"], om["support"], om["lam"])
+    assert PT.supports_equal_mod_conj(gm["support"], gm["pair"], perm, om["support"], om["pair"])
     Phi = P.modes(Xd)
     mask = P.foreground(Xd, cfg.tau, C.BG_DYNAMIC).cpu().numpy().view(np.uint32)
     torch.cuda.synchronize()
