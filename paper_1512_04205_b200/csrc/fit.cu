@@ -40,6 +40,12 @@ struct FitWs {
   size_t total;
 };
 
+// truncated symmetric eigensolver: syevdx (k largest only, default) or syevd
+static bool use_syevdx() {
+  const char* e = getenv("CDMD_SYEV");
+  return !(e && e[0] == 'd' && e[1] == 0);
+}
+
 static size_t al(size_t b) { return (b + 255) & ~(size_t)255; }
 
 static cdmd_status layout_ws(cdmd_handle h, int64_t p, int64_t m, int k, char* base, FitWs* W) {
@@ -70,6 +76,18 @@ static cdmd_status layout_ws(cdmd_handle h, int64_t p, int64_t m, int k, char* b
                                   CUBLAS_FILL_MODE_LOWER, n1, CUDA_R_64F, W->A, n1, CUDA_R_64F,
                                   W->w, CUDA_R_64F, &d, &hb) != CUSOLVER_STATUS_SUCCESS)
     return CDMD_ERR_CUDA;
+  {
+    size_t d2 = 0, hb2 = 0;
+    int64_t meig = 0;
+    double vl = 0.0, vu = 0.0;
+    if (cusolverDnXsyevdx_bufferSize(h->solver, h->params, CUSOLVER_EIG_MODE_VECTOR, CUSOLVER_EIG_RANGE_I,
+                                     CUBLAS_FILL_MODE_LOWER, n1, CUDA_R_64F, W->A, n1, &vl, &vu,
+                                     n1 - k + 1, n1, &meig, CUDA_R_64F, W->w, CUDA_R_64F, &d2,
+                                     &hb2) != CUSOLVER_STATUS_SUCCESS)
+      return CDMD_ERR_CUDA;
+    if (d2 > d) d = d2;
+    if (hb2 > hb) hb = hb2;
+  }
   W->sy_dev_bytes = d;
   W->sy_host_bytes = hb;
   W->sy_dev = take(d + 16);
@@ -103,13 +121,14 @@ __global__ void to_f64_kernel(const T* __restrict__ Y, int64_t ldy, int64_t p, i
   Yd[i] = (double)Y[r + t * ldy];
 }
 
-// sigma_j = sqrt(w), descending; V = matching eigenvectors; k_eff
+// sigma_j = sqrt(w), descending; V = matching eigenvectors; k_eff.  Eigen-pairs
+// are ascending in (w, A); the largest sits at index `top`.
 __global__ void select_topk_kernel(const double* __restrict__ A, const double* __restrict__ w,
-                                   int64_t n1, int k, double* __restrict__ V,
+                                   int64_t n1, int64_t top, int k, double* __restrict__ V,
                                    double* __restrict__ sigma, int* __restrict__ dinfo) {
   const int c = blockIdx.x;  // output column
-  const int64_t src = n1 - 1 - c;
-  const double s0 = sqrt(fmax(w[n1 - 1], 0.0));
+  const int64_t src = top - c;
+  const double s0 = sqrt(fmax(w[top], 0.0));
   for (int64_t i = threadIdx.x; i < n1; i += blockDim.x) V[i + c * n1] = A[i + src * n1];
   if (threadIdx.x == 0) {
     const double s = sqrt(fmax(w[src], 0.0));
@@ -117,7 +136,7 @@ __global__ void select_topk_kernel(const double* __restrict__ A, const double* _
     if (c == 0) {
       int ke = 0;
       for (int j = 0; j < k; ++j)
-        if (sqrt(fmax(w[n1 - 1 - j], 0.0)) > RANK_RTOL * s0) ++ke; else break;
+        if (sqrt(fmax(w[top - j], 0.0)) > RANK_RTOL * s0) ++ke; else break;
       dinfo[INFO_K_EFF] = ke;
     }
   }
@@ -128,86 +147,93 @@ __global__ void scale_atilde_kernel(double* __restrict__ B, const double* __rest
   if (i < k) B[i + j * k] /= sigma[i] * sigma[j];
 }
 
-// canonical eigen-order and phase (reading R11) + folded S^-1 W + lambda/omega/pair
-__global__ void canonicalize_kernel(int k, const double* __restrict__ Wc, const double* __restrict__ VR,
-                                    const double* __restrict__ sigma, double dt,
-                                    double* __restrict__ lam_out, double* __restrict__ om_out,
-                                    int32_t* __restrict__ pair_out, double* __restrict__ SW,
-                                    int* __restrict__ dinfo) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  // units: (first index, is_pair); LAPACK layout of real geev output
-  int ufirst[512];
-  int upair[512];
-  int nu = 0;
-  int flags = 0;
-  for (int j = 0; j < k && nu < 512;) {
-    const double re = Wc[2 * j], im = Wc[2 * j + 1];
-    if (im == 0.0) {
-      ufirst[nu] = j; upair[nu] = 0; ++nu; ++j;
-    } else if (im > 0.0 && j + 1 < k && Wc[2 * j + 2] == re && Wc[2 * j + 3] == -im) {
-      ufirst[nu] = j; upair[nu] = 1; ++nu; j += 2;
-    } else {
-      flags |= FLAG_EIG_PAIRING;  // treat as real part only (should not happen)
-      ufirst[nu] = j; upair[nu] = 0; ++nu; ++j;
+// canonical eigen-order and phase (reading R11) + folded S^-1 W + lambda/omega/pair.
+// One block: thread 0 forms and sorts the units (real eigenvalue / conjugate pair,
+// LAPACK layout of real geev output); one warp per unit normalises its vector.
+__global__ void __launch_bounds__(256) canonicalize_kernel(
+    int k, const double* __restrict__ Wc, const double* __restrict__ VR, const double* __restrict__ sigma,
+    double dt, double* __restrict__ lam_out, double* __restrict__ om_out, int32_t* __restrict__ pair_out,
+    double* __restrict__ SW, int* __restrict__ dinfo) {
+  __shared__ int ufirst[256], upair[256], ucol[256];
+  __shared__ double umod[256];
+  __shared__ int nu_sh;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    int nu = 0, flags = 0;
+    for (int j = 0; j < k && nu < 256;) {
+      const double re = Wc[2 * j], im = Wc[2 * j + 1];
+      int pr = 0;
+      if (im != 0.0) {
+        if (im > 0.0 && j + 1 < k && Wc[2 * j + 2] == re && Wc[2 * j + 3] == -im) pr = 1;
+        else flags |= FLAG_EIG_PAIRING;
+      }
+      ufirst[nu] = j; upair[nu] = pr; umod[nu] = hypot(re, pr ? im : 0.0); ++nu;
+      j += pr ? 2 : 1;
     }
-  }
-  // stable insertion sort by (|lambda| desc, real before pair)
-  for (int a = 1; a < nu; ++a) {
-    const int f = ufirst[a], pr = upair[a];
-    const double ka = hypot(Wc[2 * f], Wc[2 * f + 1]);
-    int b = a - 1;
-    while (b >= 0) {
-      const int fb = ufirst[b];
-      const double kb = hypot(Wc[2 * fb], Wc[2 * fb + 1]);
-      const bool after = (kb > ka) || (kb == ka && upair[b] <= pr);
-      if (after) break;
-      ufirst[b + 1] = ufirst[b]; upair[b + 1] = upair[b];
-      --b;
+    // stable insertion sort by (|lambda| desc, real before pair)
+    for (int a = 1; a < nu; ++a) {
+      const int f = ufirst[a], pr = upair[a];
+      const double ka = umod[a];
+      int b = a - 1;
+      while (b >= 0 && !((umod[b] > ka) || (umod[b] == ka && upair[b] <= pr))) {
+        ufirst[b + 1] = ufirst[b]; upair[b + 1] = upair[b]; umod[b + 1] = umod[b];
+        --b;
+      }
+      ufirst[b + 1] = f; upair[b + 1] = pr; umod[b + 1] = ka;
     }
-    ufirst[b + 1] = f; upair[b + 1] = pr;
+    int c = 0;
+    for (int u = 0; u < nu; ++u) { ucol[u] = c; c += upair[u] ? 2 : 1; }
+    nu_sh = nu;
+    if (flags) atomicOr(&dinfo[INFO_FLAGS], flags);
   }
-  int c = 0;
-  for (int u = 0; u < nu; ++u) {
-    const int j = ufirst[u];
-    const double re = Wc[2 * j], im = upair[u] ? Wc[2 * j + 1] : 0.0;
-    // normalise the eigenvector: unit 2-norm, largest |component| real positive
+  __syncthreads();
+  const int nu = nu_sh;
+  for (int u = warp; u < nu; u += blockDim.x / 32) {
+    const int j = ufirst[u], pr = upair[u], c = ucol[u];
+    const double* va = VR + (int64_t)j * k;
+    const double* vb = VR + (int64_t)(j + 1) * k;
+    // unit 2-norm
     double nrm = 0.0;
-    for (int i = 0; i < k; ++i) {
-      const double a = VR[i + j * k], b = upair[u] ? VR[i + (j + 1) * k] : 0.0;
+    for (int i = lane; i < k; i += 32) {
+      const double a = va[i], b = pr ? vb[i] : 0.0;
       nrm += a * a + b * b;
     }
+    for (int o = 16; o > 0; o >>= 1) nrm += __shfl_xor_sync(0xffffffffu, nrm, o);
     nrm = sqrt(nrm);
-    int imax = 0;
+    // largest |component| (first index on ties)
     double amax = -1.0;
-    for (int i = 0; i < k; ++i) {
-      const double a = VR[i + j * k] / nrm, b = upair[u] ? VR[i + (j + 1) * k] / nrm : 0.0;
-      const double mag = hypot(a, b);
-      if (mag > amax) { amax = mag; imax = i; }
+    int imax = 0x7fffffff;
+    for (int i = lane; i < k; i += 32) {
+      const double a = va[i] / nrm, b = pr ? vb[i] / nrm : 0.0;
+      const double mg = hypot(a, b);
+      if (mg > amax) { amax = mg; imax = i; }
     }
-    const double pa = VR[imax + j * k] / nrm, pb = upair[u] ? VR[imax + (j + 1) * k] / nrm : 0.0;
+    for (int o = 16; o > 0; o >>= 1) {
+      const double oa = __shfl_xor_sync(0xffffffffu, amax, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, imax, o);
+      if (oa > amax || (oa == amax && oi < imax)) { amax = oa; imax = oi; }
+    }
+    const double pa = va[imax] / nrm, pb = pr ? vb[imax] / nrm : 0.0;
     const double pm = hypot(pa, pb);
     const double cr = pa / pm, ci = -pb / pm;  // conj(phase)
-    for (int i = 0; i < k; ++i) {
-      const double a = VR[i + j * k] / nrm, b = upair[u] ? VR[i + (j + 1) * k] / nrm : 0.0;
-      const double nr = a * cr - b * ci, ni = a * ci + b * cr;
-      SW[i + c * k] = nr / sigma[i];
-      if (upair[u]) SW[i + (c + 1) * k] = ni / sigma[i];
+    for (int i = lane; i < k; i += 32) {
+      const double a = va[i] / nrm, b = pr ? vb[i] / nrm : 0.0;
+      SW[i + (int64_t)c * k] = (a * cr - b * ci) / sigma[i];
+      if (pr) SW[i + (int64_t)(c + 1) * k] = (a * ci + b * cr) / sigma[i];
     }
-    const double lr = re, li = im;
-    const double lmod = hypot(lr, li), larg = atan2(li, lr);
-    lam_out[2 * c] = lr; lam_out[2 * c + 1] = li;
-    om_out[2 * c] = log(lmod) / dt; om_out[2 * c + 1] = larg / dt;
-    pair_out[c] = upair[u] ? 1 : 0;
-    if (upair[u]) {
-      lam_out[2 * c + 2] = lr; lam_out[2 * c + 3] = -li;
-      om_out[2 * c + 2] = log(lmod) / dt; om_out[2 * c + 3] = -larg / dt;
-      pair_out[c + 1] = -1;
-      c += 2;
-    } else {
-      c += 1;
+    if (lane == 0) {
+      const double lr = Wc[2 * j], li = pr ? Wc[2 * j + 1] : 0.0;
+      const double lmod = hypot(lr, li), larg = atan2(li, lr);
+      lam_out[2 * c] = lr; lam_out[2 * c + 1] = li;
+      om_out[2 * c] = log(lmod) / dt; om_out[2 * c + 1] = larg / dt;
+      pair_out[c] = pr ? 1 : 0;
+      if (pr) {
+        lam_out[2 * c + 2] = lr; lam_out[2 * c + 3] = -li;
+        om_out[2 * c + 2] = log(lmod) / dt; om_out[2 * c + 3] = -larg / dt;
+        pair_out[c + 1] = -1;
+      }
     }
   }
-  if (flags) atomicOr(&dinfo[INFO_FLAGS], flags);
 }
 
 // complex helpers
@@ -525,13 +551,27 @@ cdmd_status fit_impl(cdmd_handle h, const void* Y, int64_t ldy, int kind, int64_
   prof.mark("gram");
   size_t hneed = W.sy_host_bytes > W.ge_host_bytes ? W.sy_host_bytes : W.ge_host_bytes;
   if (h->host_ws.size() < hneed + 16) h->host_ws.resize(hneed + 16);
-  if (cusolverDnXsyevd(h->solver, h->params, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n1,
-                       CUDA_R_64F, W.A, n1, CUDA_R_64F, W.w, CUDA_R_64F, W.sy_dev, W.sy_dev_bytes,
-                       W.sy_host_bytes ? h->host_ws.data() : nullptr, W.sy_host_bytes,
-                       W.dinfo + 8) != CUSOLVER_STATUS_SUCCESS)
-    return CDMD_ERR_CUDA;
+  int64_t top = n1 - 1;
+  if (use_syevdx()) {
+    // only the k largest eigenpairs (1-based indices n1-k+1 .. n1, ascending)
+    int64_t meig = 0;
+    double vl = 0.0, vu = 0.0;
+    if (cusolverDnXsyevdx(h->solver, h->params, CUSOLVER_EIG_MODE_VECTOR, CUSOLVER_EIG_RANGE_I,
+                          CUBLAS_FILL_MODE_LOWER, n1, CUDA_R_64F, W.A, n1, &vl, &vu, n1 - k + 1, n1, &meig,
+                          CUDA_R_64F, W.w, CUDA_R_64F, W.sy_dev, W.sy_dev_bytes,
+                          W.sy_host_bytes ? h->host_ws.data() : nullptr, W.sy_host_bytes,
+                          W.dinfo + 8) != CUSOLVER_STATUS_SUCCESS)
+      return CDMD_ERR_CUDA;
+    top = k - 1;
+  } else {
+    if (cusolverDnXsyevd(h->solver, h->params, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n1,
+                         CUDA_R_64F, W.A, n1, CUDA_R_64F, W.w, CUDA_R_64F, W.sy_dev, W.sy_dev_bytes,
+                         W.sy_host_bytes ? h->host_ws.data() : nullptr, W.sy_host_bytes,
+                         W.dinfo + 8) != CUSOLVER_STATUS_SUCCESS)
+      return CDMD_ERR_CUDA;
+  }
   prof.mark("syevd");
-  select_topk_kernel<<<k, 128, 0, st>>>(W.A, W.w, n1, k, W.V, model->sigma, W.dinfo);
+  select_topk_kernel<<<k, 128, 0, st>>>(W.A, W.w, n1, top, k, W.V, model->sigma, W.dinfo);
   CU(cudaGetLastError());
   CU(cudaMemcpyAsync(h->host_info, W.dinfo, sizeof(int) * 16, cudaMemcpyDeviceToHost, st));
   CU(cudaStreamSynchronize(st));
@@ -568,7 +608,7 @@ cdmd_status fit_impl(cdmd_handle h, const void* Y, int64_t ldy, int kind, int64_
       return CDMD_ERR_CUDA;
   }
   prof.mark("geev");
-  canonicalize_kernel<<<1, 32, 0, st>>>(ke, W.Wc, W.VR, model->sigma, dt, model->lambda,
+  canonicalize_kernel<<<1, 256, 0, st>>>(ke, W.Wc, W.VR, model->sigma, dt, model->lambda,
                                         model->omega, model->pair, W.SW, W.dinfo);
   CU(cudaGetLastError());
   // M (folded) = V S^-1 W

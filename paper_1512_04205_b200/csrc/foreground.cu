@@ -64,40 +64,68 @@ __global__ void __launch_bounds__(256) foreground_dynamic_kernel(
   }
 }
 
-// STATIC: per pixel integer thresholds lo/hi with x > L + tau <=> x >= hi and
-// x < L - tau <=> x <= lo (x integer), then one pass over all m frames.
+// STATIC: the background is one value per pixel, so the threshold
+// test reduces to integer bounds: with integer x,
+//   x > L + tau  <=>  x > floor(L + tau)      x < L - tau  <=>  x < ceil(L - tau).
+// Each thread owns one mask word (32 consecutive pixels): per frame it loads 32
+// bytes (2 x 16 B, the warp reads 1 KB contiguous), compares four pixels per
+// byte-SIMD instruction and stores one coalesced word.  HBM-bound.
+__device__ __forceinline__ uint32_t movemask4(uint32_t v) {  // bytes 0x00/0xFF -> 4 bits
+  return ((v & 0x01010101u) * 0x10204080u) >> 28;
+}
+
 __global__ void __launch_bounds__(256) foreground_static_kernel(
     const uint8_t* __restrict__ X, int64_t ld, int64_t n_local, int64_t m,
     const float* __restrict__ Phi, int64_t ldphi, const float* __restrict__ coef,
     const int32_t* __restrict__ coef_col, int n_coef, float tau, uint32_t* __restrict__ mask,
-    int64_t ldw) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t base = ((int64_t)blockIdx.x * 8 + warp) * 128;
-  if (base >= n_local) return;
-  const int64_t t0 = (int64_t)blockIdx.y * FG_FRAMES;
-  const int64_t t1 = t0 + FG_FRAMES < m ? t0 + FG_FRAMES : m;
-  int lo[4], hi[4];
+    int64_t ldw, int64_t frames_per_block) {
+  const int64_t wi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t j0 = wi * 32;
+  if (j0 >= n_local) return;
+  const int64_t t0 = (int64_t)blockIdx.y * frames_per_block;
+  const int64_t t1 = t0 + frames_per_block < m ? t0 + frames_per_block : m;
+  uint32_t hiw[8], low[8], always = 0;
 #pragma unroll
-  for (int s = 0; s < 4; ++s) {
-    const int64_t j = base + lane + 32 * s;
-    float L = 0.f;
-    if (j < n_local)
-      for (int f = 0; f < n_coef; ++f) L = fmaf(__ldg(Phi + j + (int64_t)coef_col[f] * ldphi), coef[(int64_t)f * m], L);
-    const float a = floorf(L + tau) + 1.f, b = ceilf(L - tau) - 1.f;
-    hi[s] = (int)fminf(fmaxf(a, -1.f), 256.f);
-    lo[s] = (int)fminf(fmaxf(b, -1.f), 256.f);
-  }
-  for (int64_t t = t0; t < t1; ++t) {
-    const uint8_t* __restrict__ xt = X + t * ld;
+  for (int w = 0; w < 8; ++w) {
+    uint32_t hw = 0, lw = 0;
 #pragma unroll
-    for (int s = 0; s < 4; ++s) {
-      const int64_t j = base + lane + 32 * s;
-      const int x = j < n_local ? (int)__ldg(xt + j) : 0;
-      const bool fg = j < n_local && (x >= hi[s] || x <= lo[s]);
-      const unsigned word = __ballot_sync(0xffffffffu, fg);
-      const int64_t wi = (base >> 5) + s;
-      if (lane == s && 32 * wi < n_local) mask[t * ldw + wi] = word;
+    for (int b = 0; b < 4; ++b) {
+      const int64_t j = j0 + 4 * w + b;
+      float L = 0.f;
+      if (j < n_local)
+        for (int f = 0; f < n_coef; ++f) L = fmaf(__ldg(Phi + j + (int64_t)coef_col[f] * ldphi), coef[(int64_t)f * m], L);
+      const float fh = floorf(L + tau), fl = ceilf(L - tau);
+      if (j < n_local && (fh < 0.f || fl > 255.f)) always |= 1u << (4 * w + b);
+      hw |= (uint32_t)fminf(fmaxf(fh, 0.f), 255.f) << (8 * b);
+      lw |= (uint32_t)fminf(fmaxf(fl, 0.f), 255.f) << (8 * b);
     }
+    hiw[w] = hw;
+    low[w] = lw;
+  }
+  const uint32_t valid = (j0 + 32 <= n_local) ? 0xffffffffu : ((1u << (n_local - j0)) - 1u);
+  const bool full = j0 + 32 <= n_local;
+  const uint8_t* __restrict__ xp = X + j0;
+  for (int64_t t = t0; t < t1; ++t) {
+    uint32_t xw[8];
+    if (full) {
+      const uint4 a = __ldg(reinterpret_cast<const uint4*>(xp + t * ld));
+      const uint4 b = __ldg(reinterpret_cast<const uint4*>(xp + t * ld + 16));
+      xw[0] = a.x; xw[1] = a.y; xw[2] = a.z; xw[3] = a.w;
+      xw[4] = b.x; xw[5] = b.y; xw[6] = b.z; xw[7] = b.w;
+    } else {
+#pragma unroll
+      for (int w = 0; w < 8; ++w) {
+        uint32_t v = 0;
+        for (int b = 0; b < 4; ++b)
+          if (j0 + 4 * w + b < n_local) v |= (uint32_t)xp[t * ld + 4 * w + b] << (8 * b);
+        xw[w] = v;
+      }
+    }
+    uint32_t word = always;
+#pragma unroll
+    for (int w = 0; w < 8; ++w)
+      word |= movemask4(__vcmpgtu4(xw[w], hiw[w]) | __vcmpltu4(xw[w], low[w])) << (4 * w);
+    mask[t * ldw + wi] = word & valid;
   }
 }
 
@@ -110,15 +138,25 @@ static cudaError_t launch_dyn(const cdmd_video& v, const cdmd_model& M, const fl
   return cudaGetLastError();
 }
 
+bool foreground_tc_supported(const cdmd_video& v, const cdmd_model& M);
+cudaError_t launch_foreground_tc(const cdmd_video& v, const cdmd_model& M, const float* Phi, int64_t ldphi,
+                                 float tau, uint32_t* mask, int64_t ldw, cudaStream_t st);
+
 cudaError_t launch_foreground(const cdmd_video& v, const cdmd_model& M, const float* Phi,
                               int64_t ldphi, int mode, float tau, uint32_t* mask, int64_t ldw,
                               cudaStream_t st) {
   if (mode == CDMD_BG_STATIC) {
-    dim3 grid((unsigned)ceil_div(v.n_local, 1024), (unsigned)ceil_div(v.m, FG_FRAMES));
+    // one thread per mask word; frames split so the grid covers >= 4 waves
+    const int64_t words = ceil_div(v.n_local, 32);
+    const int64_t bx = ceil_div(words, 256);
+    int64_t fpb = v.m;
+    while (fpb > 16 && bx * ceil_div(v.m, fpb) < 4 * 148) fpb = (fpb + 1) / 2;
+    dim3 grid((unsigned)bx, (unsigned)ceil_div(v.m, fpb));
     foreground_static_kernel<<<grid, 256, 0, st>>>(v.X, v.ld, v.n_local, v.m, Phi, ldphi, M.coef,
-                                                   M.coef_col, M.n_coef, tau, mask, ldw);
+                                                   M.coef_col, M.n_coef, tau, mask, ldw, fpb);
     return cudaGetLastError();
   }
+  if (foreground_tc_supported(v, M)) return launch_foreground_tc(v, M, Phi, ldphi, tau, mask, ldw, st);
   const int nc = M.n_coef;
   if (nc <= 4) return launch_dyn<4>(v, M, Phi, ldphi, tau, mask, ldw, st);
   if (nc <= 8) return launch_dyn<8>(v, M, Phi, ldphi, tau, mask, ldw, st);
