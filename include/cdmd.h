@@ -202,6 +202,13 @@ CDMD_API cdmd_status cdmd_sensing_rows(cdmd_handle h, int64_t n_total, const cdm
 CDMD_API cdmd_status cdmd_modes_simt(cdmd_handle h, const cdmd_video* v, const cdmd_model* model,
                             float* Phi, int64_t ldphi, cdmd_stream st);
 
+/* The on-device small nonsymmetric eigensolver cdmd_fit uses for A~ (k <= 118):
+ * A: device k x k column-major (not modified); W: device 2k (re, im), complex
+ * pairs consecutive (+im first); VR: device k x k column-major, LAPACK real-geev
+ * layout (pair j, j+1 -> Re, Im columns); info: device int, 0 on success. */
+CDMD_API cdmd_status cdmd_eig(const double* A, int k, double* W, double* VR, int32_t* info,
+                              cdmd_stream st);
+
 #ifdef __cplusplus
 }
 #endif

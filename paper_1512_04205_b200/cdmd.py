@@ -58,7 +58,7 @@ SYMBOLS = ["cdmd_create", "cdmd_destroy", "cdmd_status_str", "cdmd_version",
            "cdmd_sketch_workspace_bytes", "cdmd_sketch", "cdmd_model_bytes", "cdmd_model_bind",
            "cdmd_fit_workspace_bytes", "cdmd_fit", "cdmd_modes", "cdmd_background",
            "cdmd_foreground", "cdmd_philox", "cdmd_gaussian_table", "cdmd_sparse_cap",
-           "cdmd_sensing_rows", "cdmd_modes_simt"]
+           "cdmd_sensing_rows", "cdmd_modes_simt", "cdmd_eig"]
 
 
 def _load():
@@ -86,6 +86,7 @@ def _load():
         "cdmd_gaussian_table": (i32, [vp, vp, vp]),
         "cdmd_sparse_cap": (i64, [i64, i64, dbl]),
         "cdmd_sensing_rows": (i32, [vp, i64, S, vp, vp, vp]),
+        "cdmd_eig": (i32, [vp, ctypes.c_int, vp, vp, vp, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -212,6 +213,11 @@ def cdmd_sparse_cap(n_total, p, s=0.0):
 def cdmd_sensing_rows(h, n_total, c, out, counts=None, stream=None):
     _check("cdmd_sensing_rows", _lib.cdmd_sensing_rows(h.h, n_total, ctypes.byref(c), _ptr(out), _ptr(counts),
                                                        _stream(stream)))
+
+
+def cdmd_eig(A, W, VR, info, stream=None):
+    """A: (k, k) float64 CUDA tensor holding A^T row-major == A column-major."""
+    _check("cdmd_eig", _lib.cdmd_eig(_ptr(A), A.shape[0], _ptr(W), _ptr(VR), _ptr(info), _stream(stream)))
 
 
 # --------------------------------------------------------------- model read-back

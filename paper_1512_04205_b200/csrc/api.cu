@@ -11,6 +11,11 @@
 
 using namespace cdmd;
 
+namespace cdmd {
+size_t hqr_smem_bytes(int k);
+cudaError_t launch_hqr_eig(int k, const double* A, double* W, double* VR, int* info, cudaStream_t st);
+}  // namespace cdmd
+
 namespace {
 
 size_t al256(size_t b) { return (b + 255) & ~(size_t)255; }
@@ -319,6 +324,12 @@ cdmd_status cdmd_sensing_rows(cdmd_handle h, int64_t n_total, const cdmd_sensing
     return cuda_status(e);
   }
   return CDMD_ERR_ARG;
+}
+
+cdmd_status cdmd_eig(const double* A, int k, double* W, double* VR, int32_t* info, cdmd_stream st) {
+  if (!A || !W || !VR || !info) return CDMD_ERR_ARG;
+  if (k < 1 || hqr_smem_bytes(k) > 227 * 1024) return CDMD_ERR_RANGE;
+  return cuda_status(launch_hqr_eig(k, A, W, VR, info, (cudaStream_t)st));
 }
 
 }  // extern "C"

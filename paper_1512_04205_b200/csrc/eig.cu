@@ -1,0 +1,505 @@
+// eig.cu — eigen-decomposition of the small real nonsymmetric A~ (Alg. 1 step 7,
+// P:344) on the device, replacing cuSOLVER's hybrid geev for k <= 118.
+//
+// One warp, the matrix and the Schur vectors resident in shared memory (fp64):
+//   1. Householder reduction to upper Hessenberg form, accumulating Q
+//      (EISPACK orthes / ortran);
+//   2. Francis double-shift QR iteration with Wilkinson / exceptional shifts,
+//      accumulating the Schur vectors (EISPACK hqr2);
+//   3. back substitution for the eigenvectors of the quasi-triangular Schur form
+//      and back transformation with the Schur vectors (hqr2).
+// The scalar control flow runs redundantly (uniformly) on all 32 lanes; every row /
+// column / Schur-vector update loop and every dot product is split across lanes.
+// Output follows the LAPACK real-geev convention the canonicalisation expects:
+// lambda_j = (wr, wi) with each complex pair listed (+im, -im) consecutively and
+// exactly conjugate, VR column j = Re v, column j+1 = Im v for the pair.
+#include <math.h>
+
+#include "common.cuh"
+
+namespace cdmd {
+
+namespace {
+
+struct Warp {
+  int lane;
+  __device__ __forceinline__ void sync() const { __syncwarp(); }
+  __device__ __forceinline__ double sum(double v) const {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+  }
+};
+
+// complex division (a + ib) / (c + id) (Smith's algorithm)
+__device__ __forceinline__ void cdiv(double xr, double xi, double yr, double yi, double& cr, double& ci) {
+  double r, d;
+  if (fabs(yr) > fabs(yi)) {
+    r = yi / yr;
+    d = yr + r * yi;
+    cr = (xr + r * xi) / d;
+    ci = (xi - r * xr) / d;
+  } else {
+    r = yr / yi;
+    d = yi + r * yr;
+    cr = (r * xr + xi) / d;
+    ci = (r * xi - xr) / d;
+  }
+}
+
+}  // namespace
+
+// A: k x k column-major (device); outputs W (2k: re, im), VR (k x k column-major).
+__global__ void __launch_bounds__(32) hqr_eig_kernel(int nn, const double* __restrict__ A,
+                                                    double* __restrict__ W, double* __restrict__ VR,
+                                                    int* __restrict__ info) {
+  extern __shared__ double sm[];
+  const int ld = nn + 1;
+  double* H = sm;                 // nn x ld, row-major: H[i * ld + j]
+  double* V = H + nn * ld;        // Schur vectors, row-major
+  double* ort = V + nn * ld;      // nn
+  double* d = ort + nn;           // nn real parts
+  double* e = d + nn;             // nn imaginary parts
+  const Warp wp{(int)(threadIdx.x & 31)};
+  const int lane = wp.lane;
+#define Hx(i, j) H[(i) * ld + (j)]
+#define Vx(i, j) V[(i) * ld + (j)]
+  for (int idx = lane; idx < nn * nn; idx += 32) {
+    const int i = idx % nn, j = idx / nn;  // A column-major
+    Hx(i, j) = A[idx];
+    Vx(i, j) = (i == j) ? 1.0 : 0.0;
+  }
+  wp.sync();
+  const int low = 0, high = nn - 1;
+  // ------------------------------------------------ 1. orthes (Hessenberg)
+  for (int m = low + 1; m <= high - 1; ++m) {
+    double scale = 0.0;
+    for (int i = m + lane; i <= high; i += 32) scale += fabs(Hx(i, m - 1));
+    scale = wp.sum(scale);
+    if (scale != 0.0) {
+      double h = 0.0;
+      for (int i = m + lane; i <= high; i += 32) {
+        const double o = Hx(i, m - 1) / scale;
+        ort[i] = o;
+        h += o * o;
+      }
+      h = wp.sum(h);
+      wp.sync();
+      const double om = ort[m];
+      const double g = om > 0 ? -sqrt(h) : sqrt(h);
+      h = h - om * g;
+      wp.sync();
+      if (lane == 0) ort[m] = om - g;
+      wp.sync();
+      // H = (I - u u'/h) H: columns j = m .. nn-1
+      for (int j = m + lane; j < nn; j += 32) {
+        double f = 0.0;
+        for (int i = high; i >= m; --i) f += ort[i] * Hx(i, j);
+        f = f / h;
+        for (int i = m; i <= high; ++i) Hx(i, j) -= f * ort[i];
+      }
+      wp.sync();
+      // H = H (I - u u'/h): rows i = 0 .. high
+      for (int i = lane; i <= high; i += 32) {
+        double f = 0.0;
+        for (int j = high; j >= m; --j) f += ort[j] * Hx(i, j);
+        f = f / h;
+        for (int j = m; j <= high; ++j) Hx(i, j) -= f * ort[j];
+      }
+      wp.sync();
+      if (lane == 0) {
+        ort[m] = scale * ort[m];
+        Hx(m, m - 1) = scale * g;
+      }
+      wp.sync();
+    }
+  }
+  // ortran: accumulate the transformations into V
+  for (int m = high - 1; m >= low + 1; --m) {
+    if (Hx(m, m - 1) != 0.0) {
+      for (int i = m + 1 + lane; i <= high; i += 32) ort[i] = Hx(i, m - 1);
+      wp.sync();
+      for (int j = m + lane; j <= high; j += 32) {
+        double g = 0.0;
+        for (int i = m; i <= high; ++i) g += ort[i] * Vx(i, j);
+        g = (g / ort[m]) / Hx(m, m - 1);  // double division avoids underflow
+        for (int i = m; i <= high; ++i) Vx(i, j) += g * ort[i];
+      }
+      wp.sync();
+    }
+  }
+  // ------------------------------------------------------- 2. hqr2 (Schur)
+  int n = nn - 1;
+  const double eps = 0x1p-52;
+  double exshift = 0.0;
+  double p = 0, q = 0, r = 0, s = 0, z = 0, t, w, x, y;
+  double norm = 0.0;
+  for (int i = lane; i < nn; i += 32)
+    for (int j = (i > 0 ? i - 1 : 0); j < nn; ++j) norm += fabs(Hx(i, j));
+  norm = wp.sum(norm);
+  int iter = 0, total_iter = 0, fail = 0;
+  while (n >= low) {
+    int l = n;
+    while (l > low) {
+      s = fabs(Hx(l - 1, l - 1)) + fabs(Hx(l, l));
+      if (s == 0.0) s = norm;
+      if (fabs(Hx(l, l - 1)) < eps * s) break;
+      l--;
+    }
+    if (l == n) {  // one root found
+      const double hn = Hx(n, n) + exshift;
+      wp.sync();
+      if (lane == 0) {
+        Hx(n, n) = hn;
+        d[n] = hn;
+        e[n] = 0.0;
+      }
+      wp.sync();
+      n--;
+      iter = 0;
+    } else if (l == n - 1) {  // two roots found
+      w = Hx(n, n - 1) * Hx(n - 1, n);
+      p = (Hx(n - 1, n - 1) - Hx(n, n)) / 2.0;
+      q = p * p + w;
+      z = sqrt(fabs(q));
+      const double hnn = Hx(n, n) + exshift, hn1 = Hx(n - 1, n - 1) + exshift;
+      wp.sync();
+      if (lane == 0) {
+        Hx(n, n) = hnn;
+        Hx(n - 1, n - 1) = hn1;
+      }
+      wp.sync();
+      x = hnn;
+      if (q >= 0) {  // real pair
+        z = (p >= 0) ? p + z : p - z;
+        double dn1 = x + z, dn = dn1;
+        if (z != 0.0) dn = x - w / z;
+        x = Hx(n, n - 1);
+        s = fabs(x) + fabs(z);
+        p = x / s;
+        q = z / s;
+        r = sqrt(p * p + q * q);
+        p = p / r;
+        q = q / r;
+        wp.sync();
+        if (lane == 0) {
+          d[n - 1] = dn1;
+          d[n] = dn;
+          e[n - 1] = 0.0;
+          e[n] = 0.0;
+        }
+        for (int j = n - 1 + lane; j < nn; j += 32) {  // row modification
+          const double zz = Hx(n - 1, j);
+          Hx(n - 1, j) = q * zz + p * Hx(n, j);
+          Hx(n, j) = q * Hx(n, j) - p * zz;
+        }
+        wp.sync();
+        for (int i = lane; i <= n; i += 32) {  // column modification
+          const double zz = Hx(i, n - 1);
+          Hx(i, n - 1) = q * zz + p * Hx(i, n);
+          Hx(i, n) = q * Hx(i, n) - p * zz;
+        }
+        for (int i = low + lane; i <= high; i += 32) {  // accumulate
+          const double zz = Vx(i, n - 1);
+          Vx(i, n - 1) = q * zz + p * Vx(i, n);
+          Vx(i, n) = q * Vx(i, n) - p * zz;
+        }
+        wp.sync();
+      } else {  // complex pair
+        wp.sync();
+        if (lane == 0) {
+          d[n - 1] = x + p;
+          d[n] = x + p;
+          e[n - 1] = z;
+          e[n] = -z;
+        }
+        wp.sync();
+      }
+      n = n - 2;
+      iter = 0;
+    } else {  // no convergence yet: form shift
+      x = Hx(n, n);
+      y = 0.0;
+      w = 0.0;
+      if (l < n) {
+        y = Hx(n - 1, n - 1);
+        w = Hx(n, n - 1) * Hx(n - 1, n);
+      }
+      if (iter == 10) {  // Wilkinson's original ad hoc shift
+        exshift += x;
+        wp.sync();
+        for (int i = low + lane; i <= n; i += 32) Hx(i, i) -= x;
+        wp.sync();
+        s = fabs(Hx(n, n - 1)) + fabs(Hx(n - 1, n - 2));
+        x = y = 0.75 * s;
+        w = -0.4375 * s * s;
+      }
+      if (iter == 30) {  // MATLAB's ad hoc shift
+        s = (y - x) / 2.0;
+        s = s * s + w;
+        if (s > 0) {
+          s = sqrt(s);
+          if (y < x) s = -s;
+          s = x - w / ((y - x) / 2.0 + s);
+          wp.sync();
+          for (int i = low + lane; i <= n; i += 32) Hx(i, i) -= s;
+          wp.sync();
+          exshift += s;
+          x = y = w = 0.964;
+        }
+      }
+      iter++;
+      if (++total_iter > 60 * nn) {
+        fail = 1;
+        break;
+      }
+      int m = n - 2;  // look for two consecutive small sub-diagonal elements
+      while (m >= l) {
+        z = Hx(m, m);
+        r = x - z;
+        s = y - z;
+        p = (r * s - w) / Hx(m + 1, m) + Hx(m, m + 1);
+        q = Hx(m + 1, m + 1) - z - r - s;
+        r = Hx(m + 2, m + 1);
+        s = fabs(p) + fabs(q) + fabs(r);
+        p = p / s;
+        q = q / s;
+        r = r / s;
+        if (m == l) break;
+        if (fabs(Hx(m, m - 1)) * (fabs(q) + fabs(r)) <
+            eps * (fabs(p) * (fabs(Hx(m - 1, m - 1)) + fabs(z) + fabs(Hx(m + 1, m + 1)))))
+          break;
+        m--;
+      }
+      wp.sync();
+      for (int i = m + 2 + lane; i <= n; i += 32) {
+        Hx(i, i - 2) = 0.0;
+        if (i > m + 2) Hx(i, i - 3) = 0.0;
+      }
+      wp.sync();
+      for (int kk = m; kk <= n - 1; ++kk) {  // double QR step, rows l:n, columns m:n
+        const bool notlast = (kk != n - 1);
+        if (kk != m) {
+          p = Hx(kk, kk - 1);
+          q = Hx(kk + 1, kk - 1);
+          r = notlast ? Hx(kk + 2, kk - 1) : 0.0;
+          x = fabs(p) + fabs(q) + fabs(r);
+          if (x == 0.0) continue;
+          p = p / x;
+          q = q / x;
+          r = r / x;
+        }
+        s = sqrt(p * p + q * q + r * r);
+        if (p < 0) s = -s;
+        if (s != 0) {
+          double newsub = 0.0;
+          bool setsub = false;
+          if (kk != m) {
+            newsub = -s * x;
+            setsub = true;
+          } else if (l != m) {
+            newsub = -Hx(kk, kk - 1);
+            setsub = true;
+          }
+          wp.sync();
+          if (setsub && lane == 0) Hx(kk, kk - 1) = newsub;
+          wp.sync();
+          p = p + s;
+          x = p / s;
+          y = q / s;
+          z = r / s;
+          q = q / p;
+          r = r / p;
+          for (int j = kk + lane; j < nn; j += 32) {  // row modification
+            double pp = Hx(kk, j) + q * Hx(kk + 1, j);
+            if (notlast) {
+              pp = pp + r * Hx(kk + 2, j);
+              Hx(kk + 2, j) = Hx(kk + 2, j) - pp * z;
+            }
+            Hx(kk, j) = Hx(kk, j) - pp * x;
+            Hx(kk + 1, j) = Hx(kk + 1, j) - pp * y;
+          }
+          wp.sync();
+          const int imax = n < kk + 3 ? n : kk + 3;
+          for (int i = lane; i <= imax; i += 32) {  // column modification
+            double pp = x * Hx(i, kk) + y * Hx(i, kk + 1);
+            if (notlast) {
+              pp = pp + z * Hx(i, kk + 2);
+              Hx(i, kk + 2) = Hx(i, kk + 2) - pp * r;
+            }
+            Hx(i, kk) = Hx(i, kk) - pp;
+            Hx(i, kk + 1) = Hx(i, kk + 1) - pp * q;
+          }
+          for (int i = low + lane; i <= high; i += 32) {  // accumulate transformations
+            double pp = x * Vx(i, kk) + y * Vx(i, kk + 1);
+            if (notlast) {
+              pp = pp + z * Vx(i, kk + 2);
+              Vx(i, kk + 2) = Vx(i, kk + 2) - pp * r;
+            }
+            Vx(i, kk) = Vx(i, kk) - pp;
+            Vx(i, kk + 1) = Vx(i, kk + 1) - pp * q;
+          }
+          wp.sync();
+        }
+      }
+    }
+  }
+  if (fail) {
+    if (lane == 0) *info = 1;
+    return;
+  }
+  // ------------------------------------- 3. eigenvectors of the Schur form
+  if (norm != 0.0) {
+    for (n = nn - 1; n >= 0; n--) {
+      p = d[n];
+      q = e[n];
+      if (q == 0) {  // real vector
+        int l = n;
+        wp.sync();
+        if (lane == 0) Hx(n, n) = 1.0;
+        wp.sync();
+        for (int i = n - 1; i >= 0; i--) {
+          w = Hx(i, i) - p;
+          double rr = 0.0;
+          for (int j = l + lane; j <= n; j += 32) rr += Hx(i, j) * Hx(j, n);
+          r = wp.sum(rr);
+          if (e[i] < 0.0) {
+            z = w;
+            s = r;
+          } else {
+            l = i;
+            double v0, v1 = 0.0;
+            bool two = false;
+            if (e[i] == 0.0) {
+              v0 = (w != 0.0) ? -r / w : -r / (eps * norm);
+            } else {  // solve real equations
+              x = Hx(i, i + 1);
+              y = Hx(i + 1, i);
+              q = (d[i] - p) * (d[i] - p) + e[i] * e[i];
+              t = (x * s - z * r) / q;
+              v0 = t;
+              v1 = (fabs(x) > fabs(z)) ? (-r - w * t) / x : (-s - y * t) / z;
+              two = true;
+            }
+            wp.sync();
+            if (lane == 0) {
+              Hx(i, n) = v0;
+              if (two) Hx(i + 1, n) = v1;
+            }
+            wp.sync();
+            t = fabs(Hx(i, n));  // overflow control
+            if ((eps * t) * t > 1) {
+              for (int j = i + lane; j <= n; j += 32) Hx(j, n) = Hx(j, n) / t;
+              wp.sync();
+            }
+          }
+        }
+      } else if (q < 0) {  // complex vector (columns n-1 = Re, n = Im)
+        int l = n - 1;
+        double a0, a1;
+        if (fabs(Hx(n, n - 1)) > fabs(Hx(n - 1, n))) {
+          a0 = q / Hx(n, n - 1);
+          a1 = -(Hx(n, n) - p) / Hx(n, n - 1);
+        } else {
+          cdiv(0.0, -Hx(n - 1, n), Hx(n - 1, n - 1) - p, q, a0, a1);
+        }
+        wp.sync();
+        if (lane == 0) {
+          Hx(n - 1, n - 1) = a0;
+          Hx(n - 1, n) = a1;
+          Hx(n, n - 1) = 0.0;
+          Hx(n, n) = 1.0;
+        }
+        wp.sync();
+        for (int i = n - 2; i >= 0; i--) {
+          double ra = 0.0, sa = 0.0;
+          for (int j = l + lane; j <= n; j += 32) {
+            ra += Hx(i, j) * Hx(j, n - 1);
+            sa += Hx(i, j) * Hx(j, n);
+          }
+          ra = wp.sum(ra);
+          sa = wp.sum(sa);
+          w = Hx(i, i) - p;
+          if (e[i] < 0.0) {
+            z = w;
+            r = ra;
+            s = sa;
+          } else {
+            l = i;
+            double c0, c1, c2 = 0.0, c3 = 0.0;
+            bool two = false;
+            if (e[i] == 0) {
+              cdiv(-ra, -sa, w, q, c0, c1);
+            } else {  // solve complex equations
+              x = Hx(i, i + 1);
+              y = Hx(i + 1, i);
+              double vr = (d[i] - p) * (d[i] - p) + e[i] * e[i] - q * q;
+              const double vi = (d[i] - p) * 2.0 * q;
+              if (vr == 0.0 && vi == 0.0)
+                vr = eps * norm * (fabs(w) + fabs(q) + fabs(x) + fabs(y) + fabs(z));
+              cdiv(x * r - z * ra + q * sa, x * s - z * sa - q * ra, vr, vi, c0, c1);
+              if (fabs(x) > (fabs(z) + fabs(q))) {
+                c2 = (-ra - w * c0 + q * c1) / x;
+                c3 = (-sa - w * c1 - q * c0) / x;
+              } else {
+                cdiv(-r - y * c0, -s - y * c1, z, q, c2, c3);
+              }
+              two = true;
+            }
+            wp.sync();
+            if (lane == 0) {
+              Hx(i, n - 1) = c0;
+              Hx(i, n) = c1;
+              if (two) {
+                Hx(i + 1, n - 1) = c2;
+                Hx(i + 1, n) = c3;
+              }
+            }
+            wp.sync();
+            t = fmax(fabs(Hx(i, n - 1)), fabs(Hx(i, n)));  // overflow control
+            if ((eps * t) * t > 1) {
+              for (int j = i + lane; j <= n; j += 32) {
+                Hx(j, n - 1) = Hx(j, n - 1) / t;
+                Hx(j, n) = Hx(j, n) / t;
+              }
+              wp.sync();
+            }
+          }
+        }
+      }
+    }
+    // back transformation: V = V * (upper triangular part of H)
+    for (int j = nn - 1; j >= low; j--) {
+      for (int i = low + lane; i <= high; i += 32) {
+        double zz = 0.0;
+        const int kmax = j < high ? j : high;
+        for (int kx = low; kx <= kmax; ++kx) zz += Vx(i, kx) * Hx(kx, j);
+        Vx(i, j) = zz;
+      }
+      wp.sync();
+    }
+  }
+  for (int j = lane; j < nn; j += 32) {
+    W[2 * j] = d[j];
+    W[2 * j + 1] = e[j];
+  }
+  for (int idx = lane; idx < nn * nn; idx += 32) {
+    const int i = idx % nn, j = idx / nn;
+    VR[idx] = Vx(i, j);
+  }
+  if (lane == 0) *info = 0;
+#undef Hx
+#undef Vx
+}
+
+size_t hqr_smem_bytes(int k) { return sizeof(double) * ((size_t)2 * k * (k + 1) + 3 * (size_t)k); }
+
+cudaError_t launch_hqr_eig(int k, const double* A, double* W, double* VR, int* info, cudaStream_t st) {
+  const size_t smem = hqr_smem_bytes(k);
+  cudaError_t e = cudaFuncSetAttribute(hqr_eig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  hqr_eig_kernel<<<1, 32, smem, st>>>(k, A, W, VR, info);
+  return cudaGetLastError();
+}
+
+}  // namespace cdmd

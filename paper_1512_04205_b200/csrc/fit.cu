@@ -40,6 +40,15 @@ struct FitWs {
   size_t total;
 };
 
+size_t hqr_smem_bytes(int k);
+cudaError_t launch_hqr_eig(int k, const double* A, double* W, double* VR, int* info, cudaStream_t st);
+
+static bool use_device_eig(int k) {
+  const char* e = getenv("CDMD_GEEV");
+  if (e && e[0] == 'c') return false;
+  return hqr_smem_bytes(k) <= 227 * 1024;
+}
+
 // truncated symmetric eigensolver: syevdx (k largest only, default) or syevd
 static bool use_syevdx() {
   const char* e = getenv("CDMD_SYEV");
@@ -591,8 +600,12 @@ cdmd_status fit_impl(cdmd_handle h, const void* Y, int64_t ldy, int kind, int64_
   scale_atilde_kernel<<<ke, ke <= 1024 ? ((ke + 31) / 32) * 32 : 1024, 0, st>>>(W.B, model->sigma, ke);
   CU(cudaGetLastError());
   prof.mark("atilde");
-  // eig(A~): real nonsymmetric, LAPACK-style output (pairs as Re/Im columns)
-  {
+  // eig(A~): real nonsymmetric, LAPACK-style output (pairs as Re/Im columns).
+  // Default: the single-warp on-device Hessenberg + Francis QR solver (eig.cu);
+  // cuSOLVER's hybrid geev for k > 118 or with CDMD_GEEV=cusolver.
+  if (use_device_eig(ke)) {
+    CU(launch_hqr_eig(ke, W.B, W.Wc, W.VR, W.dinfo + 9, st));
+  } else {
     size_t d = 0, hb = 0;
     if (cusolverDnXgeev_bufferSize(h->solver, h->params, CUSOLVER_EIG_MODE_NOVECTOR,
                                    CUSOLVER_EIG_MODE_VECTOR, ke, CUDA_R_64F, W.B, ke, CUDA_C_64F,

@@ -79,6 +79,19 @@ __global__ void __launch_bounds__(256) foreground_static_kernel(
     const float* __restrict__ Phi, int64_t ldphi, const float* __restrict__ coef,
     const int32_t* __restrict__ coef_col, int n_coef, float tau, uint32_t* __restrict__ mask,
     int64_t ldw, int64_t frames_per_block) {
+  // static background of the block's 8192 pixels, computed with coalesced Phi
+  // reads into shared memory (stored [b][thread] so the per-thread reads below
+  // are conflict-free), then converted to per-pixel integer bounds
+  __shared__ float Ls[32][257];
+  const int64_t jb = (int64_t)blockIdx.x * blockDim.x * 32;
+  for (int i = threadIdx.x; i < 32 * 256; i += blockDim.x) {
+    const int64_t j = jb + i;
+    float L = 0.f;
+    if (j < n_local)
+      for (int f = 0; f < n_coef; ++f) L = fmaf(__ldg(Phi + j + (int64_t)coef_col[f] * ldphi), coef[(int64_t)f * m], L);
+    Ls[i & 31][i >> 5] = L;
+  }
+  __syncthreads();
   const int64_t wi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t j0 = wi * 32;
   if (j0 >= n_local) return;
@@ -91,9 +104,7 @@ __global__ void __launch_bounds__(256) foreground_static_kernel(
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
       const int64_t j = j0 + 4 * w + b;
-      float L = 0.f;
-      if (j < n_local)
-        for (int f = 0; f < n_coef; ++f) L = fmaf(__ldg(Phi + j + (int64_t)coef_col[f] * ldphi), coef[(int64_t)f * m], L);
+      const float L = Ls[4 * w + b][threadIdx.x];
       const float fh = floorf(L + tau), fl = ceilf(L - tau);
       if (j < n_local && (fh < 0.f || fl > 255.f)) always |= 1u << (4 * w + b);
       hw |= (uint32_t)fminf(fmaxf(fh, 0.f), 255.f) << (8 * b);
@@ -105,6 +116,7 @@ __global__ void __launch_bounds__(256) foreground_static_kernel(
   const uint32_t valid = (j0 + 32 <= n_local) ? 0xffffffffu : ((1u << (n_local - j0)) - 1u);
   const bool full = j0 + 32 <= n_local;
   const uint8_t* __restrict__ xp = X + j0;
+#pragma unroll 2
   for (int64_t t = t0; t < t1; ++t) {
     uint32_t xw[8];
     if (full) {

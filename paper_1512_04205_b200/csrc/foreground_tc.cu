@@ -156,27 +156,46 @@ __global__ void __launch_bounds__(32 * (2 + FG_EPI_WARPS), 1) foreground_tc_kern
     int stage = 0;
     uint32_t phase = 0;
     int it = 0, ti = 0;
+    // A = Phi_F of a tile, prefetched into registers one tile ahead (coalesced:
+    // consecutive lanes own consecutive pixels) and split into smem when its
+    // buffer is free, so the MMA of tile i+1 never waits for the epilogue.
+    const int ar = etid & (FG_BM - 1);
+    const int afh = etid >> 7;
+    constexpr int AH = KP / 2;
+    float pv[AH];
+    auto load_phi = [&](int tile) {
+      const int64_t j = (int64_t)tile * FG_BM + ar;
+#pragma unroll
+      for (int u = 0; u < AH; ++u) {
+        const int f = afh * AH + u;
+        pv[u] = (tile < num_tiles && f < n_coef && j < n_local) ? __ldg(Phi + j + (int64_t)coef_col[f] * ldphi) : 0.f;
+      }
+    };
+    auto build_a = [&](int tix) {
+      const int ab = tix & 1;
+      tc::mbar_wait(&aempty[ab], ((uint32_t)(tix >> 1) & 1u) ^ 1u);
+      uint8_t* pa = sA + (size_t)ab * 3 * PART_A;
+#pragma unroll
+      for (int u = 0; u < AH; ++u) {
+        const int f = afh * AH + u;
+        __nv_bfloat16 a0, a1, a2;
+        split3(pv[u], a0, a1, a2);
+        const uint32_t off = km_off(ar, f >> 3, KP) + (f & 7) * 2;
+        *reinterpret_cast<__nv_bfloat16*>(pa + off) = a0;
+        *reinterpret_cast<__nv_bfloat16*>(pa + PART_A + off) = a1;
+        *reinterpret_cast<__nv_bfloat16*>(pa + 2 * PART_A + off) = a2;
+      }
+      tc::fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&afull[ab]);
+    };
+    load_phi(blockIdx.x);
+    if ((int)blockIdx.x < num_tiles) build_a(0);
+    load_phi(blockIdx.x + gridDim.x);
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++ti) {
-      // build the three bf16 parts of A = Phi_F for this tile
-      {
-        const int ab = ti & 1;
-        tc::mbar_wait(&aempty[ab], ((uint32_t)(ti >> 1) & 1u) ^ 1u);
-        const int r = etid & (FG_BM - 1);
-        const int fh = etid >> 7;  // which half of the KP columns
-        const int64_t j = (int64_t)tile * FG_BM + r;
-        uint8_t* pa = sA + (size_t)ab * 3 * PART_A;
-        for (int f = fh * (KP / 2); f < (fh + 1) * (KP / 2); ++f) {
-          const float v = (f < n_coef && j < n_local) ? __ldg(Phi + j + (int64_t)coef_col[f] * ldphi) : 0.f;
-          __nv_bfloat16 a0, a1, a2;
-          split3(v, a0, a1, a2);
-          const uint32_t off = km_off(r, f >> 3, KP) + (f & 7) * 2;
-          *reinterpret_cast<__nv_bfloat16*>(pa + off) = a0;
-          *reinterpret_cast<__nv_bfloat16*>(pa + PART_A + off) = a1;
-          *reinterpret_cast<__nv_bfloat16*>(pa + 2 * PART_A + off) = a2;
-        }
-        tc::fence_proxy_async();
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(&afull[ab]);
+      if (tile + (int)gridDim.x < num_tiles) {
+        build_a(ti + 1);
+        load_phi(tile + 2 * gridDim.x);
       }
       const int64_t wi = (int64_t)tile * (FG_BM / 32) + q;  // mask word of this warp's 32 pixels
       const bool wvalid = 32 * wi < n_local;

@@ -305,3 +305,41 @@ def test_errors_are_reported_not_launched(C, H):
     with pytest.raises(C.CdmdError) as e:
         C.cdmd_foreground(H, v, P.model, P.Phi, C.BG_DYNAMIC, 0.0, P.mask)  # tau <= 0
     assert e.value.code == 2
+
+
+@pytest.mark.parametrize("k,seed", [(1, 0), (2, 1), (5, 2), (17, 3), (50, 4), (64, 5), (100, 6), (118, 7)])
+def test_device_eig_matches_lapack(C, k, seed):
+    """The on-device Hessenberg/Francis-QR eigensolver (cdmd_eig) vs LAPACK (numpy)."""
+    rng = np.random.default_rng(seed)
+    A = rng.standard_normal((k, k))
+    if k >= 5:  # plant a few conjugate pairs on the unit circle and a repeated-modulus set
+        Q, _ = np.linalg.qr(rng.standard_normal((k, k)))
+        D = np.diag(rng.uniform(0.2, 1.0, k))
+        for b in range(0, min(k - 1, 8), 2):
+            c, s_ = np.cos(0.3 * (b + 1)), np.sin(0.3 * (b + 1))
+            D[b:b + 2, b:b + 2] = [[c, -s_], [s_, c]]
+        A = Q @ D @ Q.T
+    Ad = torch.from_numpy(A.T.copy()).cuda()     # column-major A
+    W = torch.zeros(2 * k, dtype=torch.float64, device="cuda")
+    VR = torch.zeros(k * k, dtype=torch.float64, device="cuda")
+    info = torch.full((1,), -1, dtype=torch.int32, device="cuda")
+    C.cdmd_eig(Ad, W, VR, info)
+    assert int(info.item()) == 0
+    w = W.cpu().numpy().reshape(k, 2)
+    lam = w[:, 0] + 1j * w[:, 1]
+    V = VR.cpu().numpy().reshape(k, k).T          # column j = VR[:, j]
+    ref = np.linalg.eigvals(A)
+    perm, err = PT.match_eigs(lam, ref)
+    assert err < 1e-10
+    j = 0
+    while j < k:   # A v = lambda v for every (complex) eigenvector
+        if w[j, 1] == 0:
+            v = V[:, j]
+            jn = 1
+        else:
+            assert w[j, 1] > 0 and w[j + 1, 1] == -w[j, 1] and w[j + 1, 0] == w[j, 0]
+            v = V[:, j] + 1j * V[:, j + 1]
+            jn = 2
+        res = np.linalg.norm(A @ v - lam[j] * v) / (np.linalg.norm(A) * np.linalg.norm(v))
+        assert res < 1e-12, (j, res)
+        j += jn
