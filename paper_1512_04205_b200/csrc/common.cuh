@@ -28,6 +28,17 @@ __device__ __forceinline__ uint4 philox(uint4 c, uint32_t k0, uint32_t k1) {
   return c;
 }
 
+// Exact recombination of the int8-limb partial sums of the modes GEMM
+// (DESIGN.md §5.3): tot = sum_l acc_l 128^(3-l) in int64 (exact), then one
+// conversion to fp32 and one fp32 multiply by the column scale.  Shared by the
+// dp4a and tcgen05 kernels so their outputs are bit-identical.
+__device__ __forceinline__ float combine_limbs(uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                               float scale) {
+  const long long tot = ((long long)(int32_t)a0 << 21) + ((long long)(int32_t)a1 << 14) +
+                        ((long long)(int32_t)a2 << 7) + (long long)(int32_t)a3;
+  return (float)tot * scale;
+}
+
 // Philox counter word c3 tags the use of the stream.
 enum : uint32_t { TAG_SPIXEL = 1, TAG_SPARSE = 2, TAG_RADEMACHER = 3, TAG_GAUSSIAN = 4 };
 

@@ -206,20 +206,24 @@ __global__ void __launch_bounds__(32 * (2 + FG_EPI_WARPS), 1) foreground_tc_kern
         tc::fence_after();
         const uint8_t* xs = sX + (size_t)stage * FG_XSTAGE;
         const uint32_t tb_addr = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(tb * FG_BN + half * 128);
-        for (int c16 = 0; c16 < 128; c16 += 16) {
-          uint32_t Lr[16];
-          tc::tmem_ld16(tb_addr + c16, Lr);
+        // 32 frames per group: one ballot per frame gives the warp's mask word;
+        // lane i keeps frame i's word and the group is stored with one instruction
+        uint32_t* mrow = mask + ((int64_t)fb * FG_BN + half * 128) * ldw + wi;
+        for (int c32 = 0; c32 < 128; c32 += 32) {
+          uint32_t Lr[32];
+          tc::tmem_ld16(tb_addr + c32, *reinterpret_cast<uint32_t(*)[16]>(&Lr[0]));
+          tc::tmem_ld16(tb_addr + c32 + 16, *reinterpret_cast<uint32_t(*)[16]>(&Lr[16]));
           tc::tmem_ld_wait();
+          const uint8_t* xr = xs + (half * 128 + c32) * FG_BM + row;
+          uint32_t myword = 0;
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const int fl = half * 128 + c16 + i;            // frame within the unit
-            const int64_t t = (int64_t)fb * FG_BN + fl;
-            const uint32_t xb = xs[fl * FG_BM + row];
-            const float x = __uint_as_float(0x4B000000u | xb) - 8388608.0f;
-            const bool fg = fabsf(x - __uint_as_float(Lr[i])) > tau;
-            const uint32_t word = __ballot_sync(0xffffffffu, fg);
-            if (lane == 0 && wvalid && t < m) mask[t * ldw + wi] = word;
+          for (int i = 0; i < 32; ++i) {
+            const float x = __uint_as_float(0x4B000000u | (uint32_t)xr[i * FG_BM]) - 8388608.0f;
+            const uint32_t word = __ballot_sync(0xffffffffu, fabsf(x - __uint_as_float(Lr[i])) > tau);
+            myword = (lane == i) ? word : myword;
           }
+          const int64_t t = (int64_t)fb * FG_BN + half * 128 + c32 + lane;
+          if (wvalid && t < m) mrow[(int64_t)(c32 + lane) * ldw] = myword;
         }
         tc::fence_before();
         __syncwarp();

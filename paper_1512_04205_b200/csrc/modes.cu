@@ -3,7 +3,7 @@
 // Numerics: X' is uint8 (exact), M is represented by CDMD_LIMBS
 // balanced base-128 int8 limbs per column (cdmd_fit writes them), so every
 // partial product sum_t X'[t,j] d_l[t,c] is an EXACT int32 (|.| <= (m-1) 255 127);
-// the limbs are recombined exactly in int64 and scaled once to fp32.  The only
+// the limbs are recombined exactly in int64, converted once to fp32 and scaled.  The only
 // error is the quantisation of M (2^-28 of the column maximum for 4 limbs).
 // This file holds the CUDA-core (dp4a) kernel; modes_tc.cu holds the tcgen05
 // kernel, which produces bit-identical output.
@@ -65,15 +65,13 @@ __global__ void __launch_bounds__(256) modes_simt_kernel(
   }
   const int c = c0 + ty;
   if (c >= k_eff) return;
-  const double sc = scale[c];
+  const float sc = (float)scale[c];
 #pragma unroll
   for (int a = 0; a < 4; ++a) {
     const int64_t j = px0 + tx * 4 + a;
     if (j >= n_local) continue;
-    long long tot = 0;
-#pragma unroll
-    for (int l = 0; l < CDMD_LIMBS; ++l) tot = tot * 128 + (long long)acc[l][a];
-    Phi[j + (int64_t)c * ldphi] = (float)((double)tot * sc);
+    Phi[j + (int64_t)c * ldphi] =
+        combine_limbs((uint32_t)acc[0][a], (uint32_t)acc[1][a], (uint32_t)acc[2][a], (uint32_t)acc[3][a], sc);
   }
 }
 

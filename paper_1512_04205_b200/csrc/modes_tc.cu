@@ -9,7 +9,7 @@
 //       buffers so the epilogue of tile i overlaps the MMAs of tile i+1.
 // Persistent CTAs (one per SM), warp roles: warp 0 TMA producer, warp 1 TMEM
 // allocator + single-thread MMA issuer, warps 2-5 epilogue (TMEM -> registers ->
-// exact limb recombination in fp64 -> fp32 Phi, coalesced stores).
+// exact limb recombination in int64 -> fp32 Phi, coalesced stores).
 // The result is bit-identical to modes.cu's dp4a kernel (both accumulate exactly).
 #include <cudaTypedefs.h>
 
@@ -121,6 +121,9 @@ __global__ void __launch_bounds__(192, 1) modes_tc_kernel(
       const uint32_t tb = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * NT);
       for (int c0 = 0; c0 < k_eff; c0 += 16) {
         uint32_t r0[16], r1[16], r2[16], r3[16];
+        float sc[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) sc[i] = (float)__ldg(scale + (c0 + i < kpad ? c0 + i : 0));
         tc::tmem_ld16(tb + 0 * kpad + c0, r0);
         tc::tmem_ld16(tb + 1 * kpad + c0, r1);
         tc::tmem_ld16(tb + 2 * kpad + c0, r2);
@@ -130,13 +133,7 @@ __global__ void __launch_bounds__(192, 1) modes_tc_kernel(
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
             const int c = c0 + i;
-            if (c < k_eff) {
-              double v = (double)(int32_t)r0[i];
-              v = fma(v, 128.0, (double)(int32_t)r1[i]);
-              v = fma(v, 128.0, (double)(int32_t)r2[i]);
-              v = fma(v, 128.0, (double)(int32_t)r3[i]);
-              Phi[j + (int64_t)c * ldphi] = (float)(v * __ldg(scale + c));
-            }
+            if (c < k_eff) Phi[j + (int64_t)c * ldphi] = combine_limbs(r0[i], r1[i], r2[i], r3[i], sc[i]);
           }
         }
       }
