@@ -84,12 +84,24 @@ __global__ void __launch_bounds__(256) foreground_static_kernel(
   // are conflict-free), then converted to per-pixel integer bounds
   __shared__ float Ls[32][257];
   const int64_t jb = (int64_t)blockIdx.x * blockDim.x * 32;
-  for (int i = threadIdx.x; i < 32 * 256; i += blockDim.x) {
-    const int64_t j = jb + i;
-    float L = 0.f;
-    if (j < n_local)
-      for (int f = 0; f < n_coef; ++f) L = fmaf(__ldg(Phi + j + (int64_t)coef_col[f] * ldphi), coef[(int64_t)f * m], L);
-    Ls[i & 31][i >> 5] = L;
+  {
+    float Lacc[32];
+#pragma unroll
+    for (int u = 0; u < 32; ++u) Lacc[u] = 0.f;
+    for (int f = 0; f < n_coef; ++f) {  // 32 independent coalesced loads in flight per column
+      const float* col = Phi + (int64_t)coef_col[f] * ldphi + jb + threadIdx.x;
+      const float c = coef[(int64_t)f * m];
+#pragma unroll
+      for (int u = 0; u < 32; ++u) {
+        const int64_t j = jb + threadIdx.x + 256 * u;
+        Lacc[u] = fmaf(j < n_local ? __ldg(col + 256 * u) : 0.f, c, Lacc[u]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 32; ++u) {
+      const int i = threadIdx.x + 256 * u;
+      Ls[i & 31][i >> 5] = Lacc[u];
+    }
   }
   __syncthreads();
   const int64_t wi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -162,7 +174,7 @@ cudaError_t launch_foreground(const cdmd_video& v, const cdmd_model& M, const fl
     const int64_t words = ceil_div(v.n_local, 32);
     const int64_t bx = ceil_div(words, 256);
     int64_t fpb = v.m;
-    while (fpb > 16 && bx * ceil_div(v.m, fpb) < 4 * 148) fpb = (fpb + 1) / 2;
+    while (fpb > 64 && bx * ceil_div(v.m, fpb) < 2 * 148) fpb = (fpb + 1) / 2;
     dim3 grid((unsigned)bx, (unsigned)ceil_div(v.m, fpb));
     foreground_static_kernel<<<grid, 256, 0, st>>>(v.X, v.ld, v.n_local, v.m, Phi, ldphi, M.coef,
                                                    M.coef_col, M.n_coef, tau, mask, ldw, fpb);
