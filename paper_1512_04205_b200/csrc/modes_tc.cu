@@ -8,7 +8,7 @@
 //   D = int32 in TMEM (exact: |D| <= (m-1) 255 127 < 2^31), two accumulator
 //       buffers so the epilogue of tile i overlaps the MMAs of tile i+1.
 // Persistent CTAs (one per SM), warp roles: warp 0 TMA producer, warp 1 TMEM
-// allocator + single-thread MMA issuer, warps 2-5 epilogue (TMEM -> registers ->
+// allocator + single-thread MMA issuer, warps 2-9 epilogue (TMEM -> registers ->
 // exact limb recombination in int64 -> fp32 Phi, coalesced stores).
 // The result is bit-identical to modes.cu's dp4a kernel (both accumulate exactly).
 #include <cudaTypedefs.h>
@@ -23,7 +23,7 @@ constexpr int TC_BK = 128;      // frames per TMA stage
 constexpr int TC_STAGE = TC_BM * TC_BK;  // bytes per A stage
 
 template <int NT>
-__global__ void __launch_bounds__(192, 1) modes_tc_kernel(
+__global__ void __launch_bounds__(320, 1) modes_tc_kernel(
     const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, int64_t n_local,
     int nkb, int stages, int kpad, int k_eff, const double* __restrict__ scale, float* __restrict__ Phi,
     int64_t ldphi, int num_tiles, uint32_t tmem_cols) {
@@ -37,8 +37,10 @@ __global__ void __launch_bounds__(192, 1) modes_tc_kernel(
   uint64_t* tempty = tfull + 2;
   uint64_t* bfull = tempty + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bfull + 1);
+  __shared__ float sScale[256];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int c = threadIdx.x; c < kpad; c += blockDim.x) sScale[c] = (float)scale[c];
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < stages; ++s) {
       tc::mbar_init(&full[s], 1);
@@ -46,8 +48,8 @@ __global__ void __launch_bounds__(192, 1) modes_tc_kernel(
     }
     tc::mbar_init(&tfull[0], 1);
     tc::mbar_init(&tfull[1], 1);
-    tc::mbar_init(&tempty[0], 4);
-    tc::mbar_init(&tempty[1], 4);
+    tc::mbar_init(&tempty[0], 8);
+    tc::mbar_init(&tempty[1], 8);
     tc::mbar_init(bfull, 1);
     tc::fence_mbar_init();
     tc::tma_prefetch(&mapA);
@@ -109,8 +111,10 @@ __global__ void __launch_bounds__(192, 1) modes_tc_kernel(
       }
     }
   } else {  // ------------------------------------------------------ epilogue
-    const int q = warp & 3;         // TMEM lane quarter this warp may access
-    const int row = q * 32 + lane;  // pixel within the tile
+    // 8 warps: warp w reads TMEM lane quarter (w % 4) and every other 16-column chunk
+    const int q = warp & 3;                // TMEM lane quarter this warp may access
+    const int cpar = (warp - 2) >> 2;      // which 16-column chunks (0: even, 1: odd)
+    const int row = q * 32 + lane;         // pixel within the tile
     int it = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
       const int acc = it & 1;
@@ -119,22 +123,19 @@ __global__ void __launch_bounds__(192, 1) modes_tc_kernel(
       tc::fence_after();
       const int64_t j = (int64_t)tile * TC_BM + row;
       const uint32_t tb = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * NT);
-      for (int c0 = 0; c0 < k_eff; c0 += 16) {
+      float* __restrict__ out = Phi + j;
+      for (int c0 = 16 * cpar; c0 < k_eff; c0 += 32) {
         uint32_t r0[16], r1[16], r2[16], r3[16];
-        float sc[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) sc[i] = (float)__ldg(scale + (c0 + i < kpad ? c0 + i : 0));
         tc::tmem_ld16(tb + 0 * kpad + c0, r0);
         tc::tmem_ld16(tb + 1 * kpad + c0, r1);
         tc::tmem_ld16(tb + 2 * kpad + c0, r2);
         tc::tmem_ld16(tb + 3 * kpad + c0, r3);
         tc::tmem_ld_wait();
+        const int nc = k_eff - c0 < 16 ? k_eff - c0 : 16;
         if (j < n_local) {
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const int c = c0 + i;
-            if (c < k_eff) Phi[j + (int64_t)c * ldphi] = combine_limbs(r0[i], r1[i], r2[i], r3[i], sc[i]);
-          }
+          for (int i = 0; i < 16; ++i)
+            if (i < nc) out[(int64_t)(c0 + i) * ldphi] = combine_limbs(r0[i], r1[i], r2[i], r3[i], sScale[c0 + i]);
         }
       }
       tc::fence_before();
@@ -200,7 +201,7 @@ static cudaError_t launch_nt(const cdmd_video& v, const cdmd_model& M, float* Ph
   const int grid = num_tiles < sms ? num_tiles : sms;
   uint32_t cols = 32;
   while (cols < 2u * NT) cols <<= 1;
-  modes_tc_kernel<NT><<<grid, 192, smem, st>>>(mapA, mapB, v.n_local, nkb, stages, M.kpad, M.k_eff,
+  modes_tc_kernel<NT><<<grid, 320, smem, st>>>(mapA, mapB, v.n_local, nkb, stages, M.kpad, M.k_eff,
                                                 M.Mq_scale, Phi, ldphi, num_tiles, cols);
   return cudaGetLastError();
 }
