@@ -24,7 +24,9 @@ namespace cdmd {
 constexpr int FG_BM = 128;         // pixels per tile (UMMA M, TMEM lanes)
 constexpr int FG_BN = 256;         // frames per unit (UMMA N, TMEM columns per buffer)
 constexpr int FG_XSTAGE = FG_BM * FG_BN;  // bytes of X per unit
-constexpr int FG_EPI_WARPS = 8;
+constexpr int FG_FSPLIT = 4;                 // frame slices per unit (per TMEM lane quarter)
+constexpr int FG_EPI_WARPS = 4 * FG_FSPLIT;   // epilogue warps
+constexpr int FG_FW = FG_BN / FG_FSPLIT;      // frames per epilogue warp per unit
 
 // no-swizzle K-major core-matrix layout: row r, 16-B chunk c at
 // (r / 8) * SBO + c * 128 + (r % 8) * 16, SBO = 16 * KP
@@ -150,9 +152,9 @@ __global__ void __launch_bounds__(32 * (2 + FG_EPI_WARPS), 1) foreground_tc_kern
   } else {  // ---------------------------------------------------------- epilogue
     const int ew = warp - 2;          // 0..7
     const int q = warp & 3;           // TMEM lane quarter
-    const int half = ew >> 2;         // frames [half*128, half*128+128) of a unit
+    const int half = ew >> 2;         // frame slice [half*FG_FW, (half+1)*FG_FW) of a unit
     const int row = q * 32 + lane;    // pixel within the tile
-    const int etid = ew * 32 + lane;  // 0..255
+    const int etid = ew * 32 + lane;  // 0 .. 32*FG_EPI_WARPS-1
     int stage = 0;
     uint32_t phase = 0;
     int it = 0, ti = 0;
@@ -160,8 +162,8 @@ __global__ void __launch_bounds__(32 * (2 + FG_EPI_WARPS), 1) foreground_tc_kern
     // consecutive lanes own consecutive pixels) and split into smem when its
     // buffer is free, so the MMA of tile i+1 never waits for the epilogue.
     const int ar = etid & (FG_BM - 1);
-    const int afh = etid >> 7;
-    constexpr int AH = KP / 2;
+    const int afh = etid >> 7;                   // which KP/FG_FSPLIT columns of A
+    constexpr int AH = KP / FG_FSPLIT;
     float pv[AH];
     auto load_phi = [&](int tile) {
       const int64_t j = (int64_t)tile * FG_BM + ar;
@@ -205,16 +207,16 @@ __global__ void __launch_bounds__(32 * (2 + FG_EPI_WARPS), 1) foreground_tc_kern
         tc::mbar_wait(&xfull[stage], phase);
         tc::fence_after();
         const uint8_t* xs = sX + (size_t)stage * FG_XSTAGE;
-        const uint32_t tb_addr = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(tb * FG_BN + half * 128);
+        const uint32_t tb_addr = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(tb * FG_BN + half * FG_FW);
         // 32 frames per group: one ballot per frame gives the warp's mask word;
         // lane i keeps frame i's word and the group is stored with one instruction
-        uint32_t* mrow = mask + ((int64_t)fb * FG_BN + half * 128) * ldw + wi;
-        for (int c32 = 0; c32 < 128; c32 += 32) {
+        uint32_t* mrow = mask + ((int64_t)fb * FG_BN + half * FG_FW) * ldw + wi;
+        for (int c32 = 0; c32 < FG_FW; c32 += 32) {
           uint32_t Lr[32];
           tc::tmem_ld16(tb_addr + c32, *reinterpret_cast<uint32_t(*)[16]>(&Lr[0]));
           tc::tmem_ld16(tb_addr + c32 + 16, *reinterpret_cast<uint32_t(*)[16]>(&Lr[16]));
           tc::tmem_ld_wait();
-          const uint8_t* xr = xs + (half * 128 + c32) * FG_BM + row;
+          const uint8_t* xr = xs + (half * FG_FW + c32) * FG_BM + row;
           uint32_t myword = 0;
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
@@ -222,7 +224,7 @@ __global__ void __launch_bounds__(32 * (2 + FG_EPI_WARPS), 1) foreground_tc_kern
             const uint32_t word = __ballot_sync(0xffffffffu, fabsf(x - __uint_as_float(Lr[i])) > tau);
             myword = (lane == i) ? word : myword;
           }
-          const int64_t t = (int64_t)fb * FG_BN + half * 128 + c32 + lane;
+          const int64_t t = (int64_t)fb * FG_BN + half * FG_FW + c32 + lane;
           if (wvalid && t < m) mrow[(int64_t)(c32 + lane) * ldw] = myword;
         }
         tc::fence_before();
