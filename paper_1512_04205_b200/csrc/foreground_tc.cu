@@ -1,32 +1,34 @@
 // foreground_tc.cu — fused dynamic background + residual + threshold + bit-pack on
 // tcgen05 tensor cores (Eq. DMDTerms P:185-193 with Eq. thres).
 //
-// The dynamic background of a 128-pixel tile over 256 frames is the rank-NC
-// product L = Phi_F (128 x NC) . H^T (NC x 256) of the folded support modes and the
-// coefficient table h_f(t) = Re/Im of beta_p lambda_p^(t-1).  On CUDA cores that is
-// NC FMAs per pixel-frame (ALU-bound above HBM speed); here it is six
-// kind::f16 MMAs per (tile, frame block) on bf16 three-term splits of both factors
-//   Phi_F = A0 + A1 + A2,  H = B0 + B1 + B2  (24 significant bits each),
-//   L ~= sum_{i + j <= 2} A_i B_j^T  accumulated in fp32 in TMEM,
-// followed by an epilogue that reads L from TMEM (lane = pixel), compares with the
-// uint8 pixels of the TMA-staged X tile and ballots 32 pixels into one mask word.
-// Persistent CTAs; warp 0 TMA producer, warp 1 TMEM owner + MMA issuer, warps 2..9
-// epilogue (also build the A splits of each tile from Phi).  One read of X, one
-// write of the mask, Phi_F read once.
+// The dynamic background of a 256-pixel tile over a 128-frame unit is the rank-NC
+// product L^T = H (128 frames x NC) . Phi_F^T (NC x 256 pixels) of the coefficient
+// table h_f(t) = Re/Im of beta_p lambda_p^(t-1) and the folded support modes.  On
+// CUDA cores that is NC FMAs per pixel-frame (ALU-bound above HBM speed); here it is
+// six kind::f16 MMAs (M = 128 frames, N = 256 pixels) on bf16 three-term splits
+//   H = A0 + A1 + A2,  Phi_F = B0 + B1 + B2  (24 significant bits each),
+//   L^T ~= sum_{i + j <= 2} A_i B_j^T  accumulated in fp32 in TMEM,
+// followed by an epilogue in which each thread owns one frame (TMEM lane) and reads
+// 32 consecutive pixels' backgrounds (TMEM columns) and bytes (two 16-B loads from
+// the SWIZZLE_128B TMA tile), builds the 32-bit mask word in registers (f32x2 packed
+// subtractions) and stores whole words.  Persistent CTAs; warp 0 TMA producer,
+// warp 1 TMEM owner + MMA issuer, warps 2..17 epilogue (they also split Phi_F of the
+// next tile into the B operand).  One read of X, one write of the mask.
 #include <cuda_bf16.h>
 #include <cudaTypedefs.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "tc.cuh"
 
 namespace cdmd {
 
-constexpr int FG_BM = 128;         // pixels per tile (UMMA M, TMEM lanes)
-constexpr int FG_BN = 256;         // frames per unit (UMMA N, TMEM columns per buffer)
-constexpr int FG_XSTAGE = FG_BM * FG_BN;  // bytes of X per unit
-constexpr int FG_FSPLIT = 4;                 // frame slices per unit (per TMEM lane quarter)
-constexpr int FG_EPI_WARPS = 4 * FG_FSPLIT;   // epilogue warps
-constexpr int FG_FW = FG_BN / FG_FSPLIT;      // frames per epilogue warp per unit
+constexpr int FG_BN = 256;          // pixels per tile (UMMA N, TMEM columns per buffer)
+constexpr int FG_BM = 128;          // frames per unit (UMMA M, TMEM lanes)
+constexpr int FG_XSTAGE = FG_BM * FG_BN;   // bytes of X per unit (two 128x128 SW128 boxes)
+constexpr int FG_FSPLIT = 4;        // pixel slices per unit (per TMEM lane quarter)
+constexpr int FG_EPI_WARPS = 4 * FG_FSPLIT;
+constexpr int FG_PW = FG_BN / FG_FSPLIT;   // pixels per epilogue warp per unit
 
 // no-swizzle K-major core-matrix layout: row r, 16-B chunk c at
 // (r / 8) * SBO + c * 128 + (r % 8) * 16, SBO = 16 * KP
@@ -50,39 +52,74 @@ __device__ __forceinline__ uint64_t desc_nosw(uint32_t saddr, uint32_t lbo, uint
   return d;
 }
 
+__device__ __forceinline__ unsigned long long f2pack(float lo, float hi) {
+  return (unsigned long long)__float_as_uint(lo) | ((unsigned long long)__float_as_uint(hi) << 32);
+}
+__device__ __forceinline__ unsigned long long fadd2(unsigned long long a, unsigned long long b) {
+  unsigned long long d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ unsigned long long fsub2(unsigned long long a, unsigned long long b) {
+  unsigned long long d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+
+// 32 mask bits of one frame: pixels of 8 byte-words xw (4 pixels each) against 32
+// background values L; bit i = |x_i - L_i| > tau.  The uint8 pixel becomes an exact
+// float through 2^23 + x (byte permute into the mantissa), subtractions run as
+// packed f32x2 pairs.
+__device__ __forceinline__ uint32_t mask32(const uint32_t (&xw)[8], const uint32_t (&L)[32], float tau) {
+  const unsigned long long bias = f2pack(-8388608.0f, -8388608.0f);
+  uint32_t word = 0;
+#pragma unroll
+  for (int i = 0; i < 32; i += 2) {
+    const uint32_t a = __byte_perm(xw[i >> 2], 0x4B000000u, 0x7540u + (i & 3));
+    const uint32_t b = __byte_perm(xw[i >> 2], 0x4B000000u, 0x7540u + ((i + 1) & 3));
+    unsigned long long x2 = fadd2(((unsigned long long)b << 32) | a, bias);                  // exact x
+    const unsigned long long l2 = (unsigned long long)L[i] | ((unsigned long long)L[i + 1] << 32);
+    const unsigned long long d2 = fsub2(x2, l2);
+    const float d0 = __uint_as_float((uint32_t)d2), d1 = __uint_as_float((uint32_t)(d2 >> 32));
+    if (fabsf(d0) > tau) word |= 1u << i;
+    if (fabsf(d1) > tau) word |= 2u << i;
+  }
+  return word;
+}
+
 template <int KP>
 __global__ void __launch_bounds__(32 * (2 + FG_EPI_WARPS), 1) foreground_tc_kernel(
     const __grid_constant__ CUtensorMap mapX, int64_t n_local, int64_t m, int nfb,
     const float* __restrict__ Phi, int64_t ldphi, const float* __restrict__ coef,
     const int32_t* __restrict__ coef_col, int n_coef, float tau, uint32_t* __restrict__ mask,
-    int64_t ldw, int num_tiles, int stages) {
-  constexpr int PART_A = FG_BM * KP * 2;  // bytes of one split part of A
+    int64_t ldw, int num_tiles, int stages, int dbg) {
+  constexpr int PART_B = FG_BN * KP * 2;  // bytes of one split part of Phi_F (B)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const int mB = nfb * FG_BN;
-  const int PART_B = mB * KP * 2;
-  uint8_t* sX = smem;                                          // stages x 32 KB
-  uint8_t* sB = sX + (size_t)stages * FG_XSTAGE;               // 3 parts x mB rows x KP
-  uint8_t* sA = sB + 3 * (size_t)PART_B;                       // 2 buffers x 3 parts
-  uint64_t* xfull = reinterpret_cast<uint64_t*>(sA + 2 * 3 * PART_A);
+  const int mA = nfb * FG_BM;
+  const int PART_A = mA * KP * 2;
+  uint8_t* sX = smem;                                          // stages x 32 KB (SW128 boxes)
+  uint8_t* sA = sX + (size_t)stages * FG_XSTAGE;               // H: 3 parts x mA frames x KP
+  uint8_t* sB = sA + 3 * (size_t)PART_A;                       // Phi_F: 2 buffers x 3 parts
+  uint64_t* xfull = reinterpret_cast<uint64_t*>(sB + 2 * 3 * PART_B);
   uint64_t* xempty = xfull + stages;
-  uint64_t* afull = xempty + stages;
-  uint64_t* aempty = afull + 2;
-  uint64_t* tfull = aempty + 2;
+  uint64_t* bfull = xempty + stages;
+  uint64_t* bempty = bfull + 2;
+  uint64_t* tfull = bempty + 2;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // ---- coefficient table H (frames x KP), split in three bf16 parts, resident
-  for (int idx = threadIdx.x; idx < mB * KP; idx += blockDim.x) {
+  for (int idx = threadIdx.x; idx < mA * KP; idx += blockDim.x) {
     const int t = idx / KP, f = idx % KP;
     const float v = (t < m && f < n_coef) ? coef[(int64_t)f * m + t] : 0.f;
     __nv_bfloat16 b0, b1, b2;
     split3(v, b0, b1, b2);
     const uint32_t off = km_off(t, f >> 3, KP) + (f & 7) * 2;
-    *reinterpret_cast<__nv_bfloat16*>(sB + off) = b0;
-    *reinterpret_cast<__nv_bfloat16*>(sB + PART_B + off) = b1;
-    *reinterpret_cast<__nv_bfloat16*>(sB + 2 * PART_B + off) = b2;
+    *reinterpret_cast<__nv_bfloat16*>(sA + off) = b0;
+    *reinterpret_cast<__nv_bfloat16*>(sA + PART_A + off) = b1;
+    *reinterpret_cast<__nv_bfloat16*>(sA + 2 * PART_A + off) = b2;
   }
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < stages; ++s) {
@@ -90,8 +127,8 @@ __global__ void __launch_bounds__(32 * (2 + FG_EPI_WARPS), 1) foreground_tc_kern
       tc::mbar_init(&xempty[s], FG_EPI_WARPS);
     }
     for (int b = 0; b < 2; ++b) {
-      tc::mbar_init(&afull[b], FG_EPI_WARPS);
-      tc::mbar_init(&aempty[b], 1);
+      tc::mbar_init(&bfull[b], FG_EPI_WARPS);
+      tc::mbar_init(&bempty[b], 1);
       tc::mbar_init(&tfull[b], 1);
       tc::mbar_init(&tempty[b], FG_EPI_WARPS);
     }
@@ -113,7 +150,9 @@ __global__ void __launch_bounds__(32 * (2 + FG_EPI_WARPS), 1) foreground_tc_kern
         for (int fb = 0; fb < nfb; ++fb) {
           tc::mbar_wait(&xempty[stage], phase ^ 1u);
           tc::mbar_arrive_expect_tx(&xfull[stage], FG_XSTAGE);
-          tc::tma_load_2d(sX + (size_t)stage * FG_XSTAGE, &mapX, &xfull[stage], tile * FG_BM, fb * FG_BN);
+          uint8_t* dst = sX + (size_t)stage * FG_XSTAGE;
+          tc::tma_load_2d(dst, &mapX, &xfull[stage], tile * FG_BN, fb * FG_BM);
+          tc::tma_load_2d(dst + FG_XSTAGE / 2, &mapX, &xfull[stage], tile * FG_BN + 128, fb * FG_BM);
           if (++stage == stages) { stage = 0; phase ^= 1u; }
         }
     }
@@ -123,8 +162,8 @@ __global__ void __launch_bounds__(32 * (2 + FG_EPI_WARPS), 1) foreground_tc_kern
       const uint32_t aBase = tc::smem_u32(sA), bBase = tc::smem_u32(sB);
       int it = 0, ti = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++ti) {
-        const int ab = ti & 1;
-        tc::mbar_wait(&afull[ab], (uint32_t)(ti >> 1) & 1u);
+        const int bb = ti & 1;
+        tc::mbar_wait(&bfull[bb], (uint32_t)(ti >> 1) & 1u);
         tc::fence_after();
         for (int fb = 0; fb < nfb; ++fb, ++it) {
           const int tb = it & 1;
@@ -138,94 +177,90 @@ __global__ void __launch_bounds__(32 * (2 + FG_EPI_WARPS), 1) foreground_tc_kern
             for (int pj = 0; pj < 3 - pi; ++pj)
 #pragma unroll
               for (int kk = 0; kk < KP / 16; ++kk) {
-                const uint64_t ad = desc_nosw(aBase + (ab * 3 + pi) * PART_A + kk * 256, 128, 16 * KP);
-                const uint64_t bd =
-                    desc_nosw(bBase + pj * PART_B + fb * (FG_BN / 8) * (16 * KP) + kk * 256, 128, 16 * KP);
-                tc::mma_f16(d, ad, bd, IDESC, first ? 0u : 1u);
+                const uint64_t ad =
+                    desc_nosw(aBase + pi * PART_A + fb * (FG_BM / 8) * (16 * KP) + kk * 256, 128, 16 * KP);
+                const uint64_t bd = desc_nosw(bBase + (bb * 3 + pj) * PART_B + kk * 256, 128, 16 * KP);
+                if (!(dbg & 2)) tc::mma_f16(d, ad, bd, IDESC, first ? 0u : 1u);
                 first = 0;
               }
           tc::mma_commit(&tfull[tb]);
         }
-        tc::mma_commit(&aempty[ab]);
+        tc::mma_commit(&bempty[bb]);
       }
     }
   } else {  // ---------------------------------------------------------- epilogue
-    const int ew = warp - 2;          // 0..7
-    const int q = warp & 3;           // TMEM lane quarter
-    const int half = ew >> 2;         // frame slice [half*FG_FW, (half+1)*FG_FW) of a unit
-    const int row = q * 32 + lane;    // pixel within the tile
-    const int etid = ew * 32 + lane;  // 0 .. 32*FG_EPI_WARPS-1
+    const int ew = warp - 2;          // 0 .. FG_EPI_WARPS-1
+    const int q = warp & 3;           // TMEM lane quarter: frames 32q .. 32q+31 of a unit
+    const int sl = ew >> 2;           // pixel slice [sl*FG_PW, (sl+1)*FG_PW) of a tile
+    const int r = q * 32 + lane;      // frame within the unit (= TMEM lane)
+    const int etid = ew * 32 + lane;
     int stage = 0;
     uint32_t phase = 0;
     int it = 0, ti = 0;
-    // A = Phi_F of a tile, prefetched into registers one tile ahead (coalesced:
-    // consecutive lanes own consecutive pixels) and split into smem when its
-    // buffer is free, so the MMA of tile i+1 never waits for the epilogue.
-    const int ar = etid & (FG_BM - 1);
-    const int afh = etid >> 7;                   // which KP/FG_FSPLIT columns of A
-    constexpr int AH = KP / FG_FSPLIT;
-    float pv[AH];
+    // Phi_F of a tile (B operand), prefetched into registers one tile ahead
+    // (consecutive threads own consecutive pixels: coalesced) and split into smem
+    // when its buffer is free.
+    const int br = etid & (FG_BN - 1);
+    const int bfh = etid >> 8;                    // which half of the KP columns
+    constexpr int BH = KP / 2;
+    float pv[BH];
     auto load_phi = [&](int tile) {
-      const int64_t j = (int64_t)tile * FG_BM + ar;
+      const int64_t j = (int64_t)tile * FG_BN + br;
 #pragma unroll
-      for (int u = 0; u < AH; ++u) {
-        const int f = afh * AH + u;
+      for (int u = 0; u < BH; ++u) {
+        const int f = bfh * BH + u;
         pv[u] = (tile < num_tiles && f < n_coef && j < n_local) ? __ldg(Phi + j + (int64_t)coef_col[f] * ldphi) : 0.f;
       }
     };
-    auto build_a = [&](int tix) {
-      const int ab = tix & 1;
-      tc::mbar_wait(&aempty[ab], ((uint32_t)(tix >> 1) & 1u) ^ 1u);
-      uint8_t* pa = sA + (size_t)ab * 3 * PART_A;
+    auto build_b = [&](int tix) {
+      const int bb = tix & 1;
+      tc::mbar_wait(&bempty[bb], ((uint32_t)(tix >> 1) & 1u) ^ 1u);
+      uint8_t* pb = sB + (size_t)bb * 3 * PART_B;
 #pragma unroll
-      for (int u = 0; u < AH; ++u) {
-        const int f = afh * AH + u;
+      for (int u = 0; u < BH; ++u) {
+        const int f = bfh * BH + u;
         __nv_bfloat16 a0, a1, a2;
         split3(pv[u], a0, a1, a2);
-        const uint32_t off = km_off(ar, f >> 3, KP) + (f & 7) * 2;
-        *reinterpret_cast<__nv_bfloat16*>(pa + off) = a0;
-        *reinterpret_cast<__nv_bfloat16*>(pa + PART_A + off) = a1;
-        *reinterpret_cast<__nv_bfloat16*>(pa + 2 * PART_A + off) = a2;
+        const uint32_t off = km_off(br, f >> 3, KP) + (f & 7) * 2;
+        *reinterpret_cast<__nv_bfloat16*>(pb + off) = a0;
+        *reinterpret_cast<__nv_bfloat16*>(pb + PART_B + off) = a1;
+        *reinterpret_cast<__nv_bfloat16*>(pb + 2 * PART_B + off) = a2;
       }
       tc::fence_proxy_async();
       __syncwarp();
-      if (lane == 0) tc::mbar_arrive(&afull[ab]);
+      if (lane == 0) tc::mbar_arrive(&bfull[bb]);
     };
     load_phi(blockIdx.x);
-    if ((int)blockIdx.x < num_tiles) build_a(0);
+    if ((int)blockIdx.x < num_tiles) build_b(0);
     load_phi(blockIdx.x + gridDim.x);
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++ti) {
       if (tile + (int)gridDim.x < num_tiles) {
-        build_a(ti + 1);
+        build_b(ti + 1);
         load_phi(tile + 2 * gridDim.x);
       }
-      const int64_t wi = (int64_t)tile * (FG_BM / 32) + q;  // mask word of this warp's 32 pixels
-      const bool wvalid = 32 * wi < n_local;
       for (int fb = 0; fb < nfb; ++fb, ++it) {
         const int tb = it & 1;
         tc::mbar_wait(&tfull[tb], (uint32_t)(it >> 1) & 1u);
         tc::mbar_wait(&xfull[stage], phase);
         tc::fence_after();
         const uint8_t* xs = sX + (size_t)stage * FG_XSTAGE;
-        const uint32_t tb_addr = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(tb * FG_BN + half * FG_FW);
-        // 32 frames per group: one ballot per frame gives the warp's mask word;
-        // lane i keeps frame i's word and the group is stored with one instruction
-        uint32_t* mrow = mask + ((int64_t)fb * FG_BN + half * FG_FW) * ldw + wi;
-        for (int c32 = 0; c32 < FG_FW; c32 += 32) {
-          uint32_t Lr[32];
-          tc::tmem_ld16(tb_addr + c32, *reinterpret_cast<uint32_t(*)[16]>(&Lr[0]));
-          tc::tmem_ld16(tb_addr + c32 + 16, *reinterpret_cast<uint32_t(*)[16]>(&Lr[16]));
-          tc::tmem_ld_wait();
-          const uint8_t* xr = xs + (half * FG_FW + c32) * FG_BM + row;
-          uint32_t myword = 0;
+        const uint32_t ta = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(tb * FG_BN);
+        const int64_t t = (int64_t)fb * FG_BM + r;
+        uint32_t words[FG_PW / 32];
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const float x = __uint_as_float(0x4B000000u | (uint32_t)xr[i * FG_BM]) - 8388608.0f;
-            const uint32_t word = __ballot_sync(0xffffffffu, fabsf(x - __uint_as_float(Lr[i])) > tau);
-            myword = (lane == i) ? word : myword;
-          }
-          const int64_t t = (int64_t)fb * FG_BN + half * FG_FW + c32 + lane;
-          if (wvalid && t < m) mrow[(int64_t)(c32 + lane) * ldw] = myword;
+        for (int w = 0; w < FG_PW / 32; ++w) {
+          const int j0 = sl * FG_PW + 32 * w;       // pixel offset in the tile
+          uint32_t L[32];
+          tc::tmem_ld16(ta + j0, *reinterpret_cast<uint32_t(*)[16]>(&L[0]));
+          tc::tmem_ld16(ta + j0 + 16, *reinterpret_cast<uint32_t(*)[16]>(&L[16]));
+          // pixels j0..j0+31 of frame r: box j0/128, 16-B chunks c, c+1 XOR-swizzled by r%8
+          const uint8_t* row = xs + (j0 >> 7) * (FG_XSTAGE / 2) + r * 128;
+          const int c = (j0 & 127) >> 4;
+          const uint4 a = *reinterpret_cast<const uint4*>(row + (((c) ^ (r & 7)) << 4));
+          const uint4 b = *reinterpret_cast<const uint4*>(row + (((c + 1) ^ (r & 7)) << 4));
+          const uint32_t xw[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+          tc::tmem_ld_wait();
+          words[w] = (dbg & 1) ? 0u : mask32(xw, L, tau);
         }
         tc::fence_before();
         __syncwarp();
@@ -234,6 +269,15 @@ __global__ void __launch_bounds__(32 * (2 + FG_EPI_WARPS), 1) foreground_tc_kern
           tc::mbar_arrive(&xempty[stage]);
         }
         if (++stage == stages) { stage = 0; phase ^= 1u; }
+        const int64_t w0 = ((int64_t)tile * FG_BN + sl * FG_PW) >> 5;   // first mask word
+        if (t < m) {
+          uint32_t* dst = mask + t * ldw + w0;
+          if (32 * (w0 + 1) < n_local) {          // both words hold pixels of the slab
+            *reinterpret_cast<uint2*>(dst) = make_uint2(words[0], words[1]);
+          } else if (32 * w0 < n_local) {
+            dst[0] = words[0];
+          }
+        }
       }
     }
   }
@@ -258,8 +302,13 @@ static PFN_cuTensorMapEncodeTiled_v12000 fg_encode_fn() {
 }
 
 static size_t fg_smem_bytes(int KP, int nfb, int stages) {
-  return 1024 + (size_t)stages * FG_XSTAGE + 3 * (size_t)nfb * FG_BN * KP * 2 + 2 * 3 * (size_t)FG_BM * KP * 2 +
+  return 1024 + (size_t)stages * FG_XSTAGE + 3 * (size_t)nfb * FG_BM * KP * 2 + 2 * 3 * (size_t)FG_BN * KP * 2 +
          512;
+}
+
+static int dbg_mode() {
+  const char* e = getenv("CDMD_FG_DBG");
+  return e ? atoi(e) : 0;
 }
 
 static int fg_kp(int n_coef) { return n_coef <= 16 ? 16 : (n_coef <= 32 ? 32 : 0); }
@@ -267,21 +316,21 @@ static int fg_kp(int n_coef) { return n_coef <= 16 ? 16 : (n_coef <= 32 ? 32 : 0
 bool foreground_tc_supported(const cdmd_video& v, const cdmd_model& M) {
   const int KP = fg_kp(M.n_coef);
   if (!KP || !fg_encode_fn()) return false;
-  const int nfb = (int)ceil_div(v.m, FG_BN);
-  return fg_smem_bytes(KP, nfb, 2) <= 227 * 1024;
+  const int nfb = (int)ceil_div(v.m, FG_BM);
+  return fg_smem_bytes(KP, nfb, 2) <= 227 * 1024 && (v.ld % 16) == 0;
 }
 
 template <int KP>
 static cudaError_t launch_kp(const cdmd_video& v, const cdmd_model& M, const float* Phi, int64_t ldphi,
                              float tau, uint32_t* mask, int64_t ldw, cudaStream_t st) {
-  const int nfb = (int)ceil_div(v.m, FG_BN);
+  const int nfb = (int)ceil_div(v.m, FG_BM);
   CUtensorMap mapX;
   cuuint64_t dims[2] = {(cuuint64_t)v.n_local, (cuuint64_t)v.m};
   cuuint64_t strides[1] = {(cuuint64_t)v.ld};
-  cuuint32_t box[2] = {FG_BM, FG_BN};
+  cuuint32_t box[2] = {128, FG_BM};
   cuuint32_t estr[2] = {1, 1};
   if (fg_encode_fn()(&mapX, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(v.X), dims, strides, box, estr,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return cudaErrorInvalidValue;
   int stages = 4;
@@ -292,10 +341,10 @@ static cudaError_t launch_kp(const cdmd_video& v, const cdmd_model& M, const flo
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int num_tiles = (int)ceil_div(v.n_local, FG_BM);
+  const int num_tiles = (int)ceil_div(v.n_local, FG_BN);
   const int grid = num_tiles < sms ? num_tiles : sms;
   foreground_tc_kernel<KP><<<grid, 32 * (2 + FG_EPI_WARPS), smem, st>>>(
-      mapX, v.n_local, v.m, nfb, Phi, ldphi, M.coef, M.coef_col, M.n_coef, tau, mask, ldw, num_tiles, stages);
+      mapX, v.n_local, v.m, nfb, Phi, ldphi, M.coef, M.coef_col, M.n_coef, tau, mask, ldw, num_tiles, stages, dbg_mode());
   return cudaGetLastError();
 }
 
