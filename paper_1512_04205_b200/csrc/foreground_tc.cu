@@ -273,7 +273,12 @@ __global__ void __launch_bounds__(32 * (2 + FG_EPI_WARPS), 1) foreground_tc_kern
         if (t < m) {
           uint32_t* dst = mask + t * ldw + w0;
           if (32 * (w0 + 1) < n_local) {          // both words hold pixels of the slab
-            *reinterpret_cast<uint2*>(dst) = make_uint2(words[0], words[1]);
+            if ((ldw & 1) == 0) {
+              *reinterpret_cast<uint2*>(dst) = make_uint2(words[0], words[1]);
+            } else {
+              dst[0] = words[0];
+              dst[1] = words[1];
+            }
           } else if (32 * w0 < n_local) {
             dst[0] = words[0];
           }
