@@ -285,9 +285,10 @@ __global__ void __launch_bounds__(32) hqr_eig_kernel(int nn, const double* __res
           r = notlast ? Hx(kk + 2, kk - 1) : 0.0;
           x = fabs(p) + fabs(q) + fabs(r);
           if (x == 0.0) continue;
-          p = p / x;
-          q = q / x;
-          r = r / x;
+          const double ix = 1.0 / x;  // one division, three multiplies
+          p = p * ix;
+          q = q * ix;
+          r = r * ix;
         }
         s = sqrt(p * p + q * q + r * r);
         if (p < 0) s = -s;
@@ -305,11 +306,12 @@ __global__ void __launch_bounds__(32) hqr_eig_kernel(int nn, const double* __res
           if (setsub && lane == 0) Hx(kk, kk - 1) = newsub;
           wp.sync();
           p = p + s;
-          x = p / s;
-          y = q / s;
-          z = r / s;
-          q = q / p;
-          r = r / p;
+          const double is = 1.0 / s, ip = 1.0 / p;
+          x = p * is;
+          y = q * is;
+          z = r * is;
+          q = q * ip;
+          r = r * ip;
           for (int j = kk + lane; j < nn; j += 32) {  // row modification
             double pp = Hx(kk, j) + q * Hx(kk + 1, j);
             if (notlast) {
