@@ -252,11 +252,16 @@ def main():
     cand = {s: stage_ms[s] for s in algo}
     dom = max(cand, key=cand.get)
     achieved = algo[dom] / (stage_ms[dom] * 1e-3) / 1e9
-    roof = {"kernel": {"sketch": "sketch_sparse_kernel", "modes": "cdmd_modes",
-                       "foreground": "foreground_dynamic_kernel" if mode else "foreground_static_kernel"}[dom],
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp) and cfg.name == "c4_1080p_sparse" and world == 1 and mode:
+        traffic = json.load(open(tp)).get(dom)
+    roof = {"kernel": {"sketch": "sketch_sparse_kernel", "modes": "modes_tc_kernel",
+                       "foreground": "foreground_tc_kernel" if mode else "foreground_static_kernel"}[dom],
             "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
-            "frac": round(achieved / hbm, 4), "traffic": None, "peak_source": hbm_src,
-            "algorithmic_bytes_per_launch": algo[dom], "launch_ms": round(stage_ms[dom], 4)}
+            "frac": round(achieved / hbm, 4), "traffic": traffic, "peak_source": hbm_src,
+            "algorithmic_bytes_per_launch": algo[dom], "launch_ms": round(stage_ms[dom], 4),
+            "stage_roofline": {s: round(algo[s] / (stage_ms[s] * 1e-3) / 1e9 / hbm, 4) for s in algo}}
 
     # e2e: host (pinned) video in, mask out, through the same public calls
     e2e = None
