@@ -8,6 +8,8 @@
 // Rademacher: int8 x uint8 dot products (dp4a here; tcgen05 kind::i8 in
 // sketch_tc.cu).  Gaussian: exact bf16 x uint8 products, fp32 partial sums over
 // short pixel chunks accumulated in fp64, one rounding to fp32 Y at the end.
+#include <stdlib.h>
+
 #include "common.cuh"
 
 namespace cdmd {
@@ -157,8 +159,14 @@ __global__ void __launch_bounds__(256) sketch_rademacher_simt_kernel(
     }
 }
 
+bool sketch_rademacher_tc_supported(const cdmd_video& v);
+cudaError_t launch_sketch_rademacher_tc(const cdmd_video& v, const SensingPlan& P, int32_t* Y, int64_t ldy,
+                                        cudaStream_t st);
+
 cudaError_t launch_sketch_rademacher(const cdmd_video& v, const SensingPlan& P, int32_t* Y,
                                      int64_t ldy, cudaStream_t st) {
+  if (sketch_rademacher_tc_supported(v) && !getenv("CDMD_SIMT_SKETCH"))
+    return launch_sketch_rademacher_tc(v, P, Y, ldy, st);
   dim3 grid((unsigned)ceil_div(P.p, 64), (unsigned)ceil_div(v.m, 64));
   sketch_rademacher_simt_kernel<<<grid, 256, 0, st>>>(v.X, v.ld, v.pix0, v.n_local, v.m, P.p, P.k0,
                                                       P.k1, Y, ldy);

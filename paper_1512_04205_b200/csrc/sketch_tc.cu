@@ -1,0 +1,210 @@
+// sketch_tc.cu — dense sketches on tcgen05 tensor cores (Alg. 1 step 3, P:336;
+// "computing Y = CX using unstructured dense matrices has a time complexity of
+// O(pnm)").
+//
+// Rademacher: Y[r, t] = sum_i c_ri X[t, i] with c_ri = +-1 as one
+// split-K int8 GEMM, D[rows x frames] = C[rows x pixels] . X[frames x pixels]^T:
+//   A = C tile, 128 rows x 128 pixels of s8, regenerated from Philox in SMEM by four
+//       generator warps (one Philox call = the 128 sign bits of (row, 128-px chunk))
+//       in the SWIZZLE_128B K-major layout;
+//   B = X tile, <= 256 frames x 128 pixels of u8 -- the stored frame-major layout is
+//       already K-major -- TMA-staged with SWIZZLE_128B;
+//   D = int32 accumulators in TMEM for the CTA's (row block, frame block), summed
+//       over its pixel range.  kind::i8 takes u8 x s8 directly, so no -128 shift is
+//       needed; every product and sum is exact (|Y| <= 255 n < 2^31).
+// Pixel ranges are split across CTAs and the partial sums meet in Y through int32
+// atomics (exact and order-independent).  Warp roles: 0 TMA producer, 1 TMEM owner +
+// MMA issuer, 2..5 C generators and then the epilogue.
+#include <cudaTypedefs.h>
+
+#include "common.cuh"
+#include "tc.cuh"
+
+namespace cdmd {
+
+constexpr int SK_BM = 128;   // rows of C per CTA (UMMA M)
+constexpr int SK_BK = 128;   // pixels per stage (one Philox call per row)
+constexpr int SK_CST = SK_BM * SK_BK;  // bytes of a C stage
+
+__global__ void __launch_bounds__(192, 1) sketch_rademacher_tc_kernel(
+    const __grid_constant__ CUtensorMap mapX, int64_t pix0, int64_t n_local, int64_t m, int64_t p,
+    uint32_t k0, uint32_t k1, int fbn, int nchunks_total, int chunks_per_split, int stages,
+    int32_t* __restrict__ Y, int64_t ldy) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int xst = fbn * SK_BK;                    // bytes of an X stage
+  uint8_t* sX = smem;
+  uint8_t* sC = sX + (size_t)stages * xst;
+  uint64_t* xfull = reinterpret_cast<uint64_t*>(sC + (size_t)stages * SK_CST);
+  uint64_t* xempty = xfull + stages;
+  uint64_t* cfull = xempty + stages;
+  uint64_t* cempty = cfull + stages;
+  uint64_t* tfull = cempty + stages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t r0 = (int64_t)blockIdx.x * SK_BM;     // first row of C
+  const int64_t f0 = (int64_t)blockIdx.y * fbn;       // first frame
+  const int c_begin = blockIdx.z * chunks_per_split;  // 128-pixel chunks of this split
+  const int c_end = min(nchunks_total, c_begin + chunks_per_split);
+  const int nch = c_end - c_begin;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < stages; ++s) {
+      tc::mbar_init(&xfull[s], 1);
+      tc::mbar_init(&xempty[s], 1);
+      tc::mbar_init(&cfull[s], 4);
+      tc::mbar_init(&cempty[s], 1);
+    }
+    tc::mbar_init(tfull, 1);
+    tc::fence_mbar_init();
+    tc::tma_prefetch(&mapX);
+  }
+  if (warp == 1) tc::tmem_alloc(tmem_slot, 256);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ------------------------------------------ TMA producer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int c = c_begin; c < c_end; ++c) {
+        tc::mbar_wait(&xempty[stage], phase ^ 1u);
+        tc::mbar_arrive_expect_tx(&xfull[stage], (uint32_t)xst);
+        tc::tma_load_2d(sX + (size_t)stage * xst, &mapX, &xfull[stage], c * SK_BK, (int32_t)f0);
+        if (++stage == stages) { stage = 0; phase ^= 1u; }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ------------------------------------------- MMA issuer
+      const uint32_t idesc = tc::idesc_i8(SK_BM, fbn, /*a_signed=*/true, /*b_signed=*/false, false, false);
+      const uint32_t xBase = tc::smem_u32(sX), cBase = tc::smem_u32(sC);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int i = 0; i < nch; ++i) {
+        tc::mbar_wait(&xfull[stage], phase);
+        tc::mbar_wait(&cfull[stage], phase);
+        tc::fence_after();
+#pragma unroll
+        for (int kk = 0; kk < SK_BK / 32; ++kk) {
+          const uint64_t ad = tc::smem_desc_sw128(cBase + stage * SK_CST + kk * 32, 0, 1024);
+          const uint64_t bd = tc::smem_desc_sw128(xBase + stage * xst + kk * 32, 0, 1024);
+          tc::mma_i8(tmem_base, ad, bd, idesc, (i | kk) != 0);
+        }
+        tc::mma_commit(&xempty[stage]);
+        tc::mma_commit(&cempty[stage]);
+        if (++stage == stages) { stage = 0; phase ^= 1u; }
+      }
+      tc::mma_commit(tfull);
+    }
+  } else {  // ------------------------------------------ C generators + epilogue
+    const int g = threadIdx.x - 64;             // 0..127: the row of C this thread generates
+    const int64_t row = r0 + g;
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int i = 0; i < nch; ++i) {
+      const int c = c_begin + i;
+      uint4 w = make_uint4(0, 0, 0, 0);
+      if (row < p) w = philox(make_uint4((uint32_t)((pix0 >> 7) + c), (uint32_t)row, 0u, TAG_RADEMACHER), k0, k1);
+      const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+      tc::mbar_wait(&cempty[stage], phase ^ 1u);
+      uint8_t* dst = sC + (size_t)stage * SK_CST + g * 128;
+#pragma unroll
+      for (int ch = 0; ch < 8; ++ch) {           // 16 pixels per 16-B chunk
+        uint32_t v[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const uint32_t nib = (ws[ch >> 1] >> (16 * (ch & 1) + 4 * q)) & 0xFu;
+          const uint32_t spread = (nib * 0x00204081u) & 0x01010101u;  // bit b -> byte b
+          v[q] = 0x01010101u + spread * 0xFEu;                        // bit 1 -> -1, 0 -> +1
+        }
+        *reinterpret_cast<uint4*>(dst + ((ch ^ (g & 7)) << 4)) = make_uint4(v[0], v[1], v[2], v[3]);
+      }
+      tc::fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&cfull[stage]);
+      if (++stage == stages) { stage = 0; phase ^= 1u; }
+    }
+    // epilogue: TMEM lane = row of C, columns = frames; int32 atomics into Y
+    tc::mbar_wait(tfull, 0);
+    tc::fence_after();
+    const int q = warp & 3;
+    const int64_t rr = r0 + q * 32 + lane;
+    const uint32_t ta = tmem_base + ((uint32_t)(q * 32) << 16);
+    const int fvalid = (int)min((int64_t)fbn, m - f0);
+    for (int c0 = 0; c0 < fbn; c0 += 16) {
+      uint32_t v[16];
+      tc::tmem_ld16(ta + c0, v);
+      tc::tmem_ld_wait();
+      if (rr < p && nch > 0) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          if (c0 + i < fvalid) atomicAdd(Y + rr + (f0 + c0 + i) * ldy, (int32_t)v[i]);
+      }
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc::fence_after();
+    tc::tmem_dealloc(tmem_base, 256);
+  }
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 sk_encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+bool sketch_rademacher_tc_supported(const cdmd_video& v) { return sk_encode_fn() != nullptr && (v.ld % 16) == 0; }
+
+cudaError_t launch_sketch_rademacher_tc(const cdmd_video& v, const SensingPlan& P, int32_t* Y, int64_t ldy,
+                                        cudaStream_t st) {
+  // frame blocks of at most 256 (UMMA N), multiple of 16
+  const int nfb = (int)ceil_div(v.m, 256);
+  const int fbn = (int)round_up(ceil_div(v.m, nfb), 16);
+  const int nrb = (int)ceil_div(P.p, SK_BM);
+  const int nchunks = (int)ceil_div(v.n_local, SK_BK);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  // split the pixel range so the grid covers ~2 waves of 148 SMs
+  int splits = (int)ceil_div(2 * sms, (int64_t)nrb * nfb);
+  if (splits > nchunks) splits = nchunks;
+  if (splits < 1) splits = 1;
+  const int cps = (int)ceil_div(nchunks, splits);
+  splits = (int)ceil_div(nchunks, cps);
+  CUtensorMap mapX;
+  cuuint64_t dims[2] = {(cuuint64_t)v.n_local, (cuuint64_t)v.m};
+  cuuint64_t strides[1] = {(cuuint64_t)v.ld};
+  cuuint32_t box[2] = {SK_BK, (cuuint32_t)fbn};
+  cuuint32_t estr[2] = {1, 1};
+  if (sk_encode_fn()(&mapX, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(v.X), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return cudaErrorInvalidValue;
+  const int xst = fbn * SK_BK;
+  int stages = 4;
+  auto smem_of = [&](int s) { return (size_t)1024 + (size_t)s * (xst + SK_CST) + 512; };
+  while (stages > 2 && smem_of(stages) > 110 * 1024) --stages;  // two CTAs per SM
+  const size_t smem = smem_of(stages);
+  cudaError_t e = cudaFuncSetAttribute(sketch_rademacher_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  e = cudaMemsetAsync(Y, 0, sizeof(int32_t) * (size_t)ldy * v.m, st);
+  if (e != cudaSuccess) return e;
+  dim3 grid((unsigned)nrb, (unsigned)nfb, (unsigned)splits);
+  sketch_rademacher_tc_kernel<<<grid, 192, smem, st>>>(mapX, v.pix0, v.n_local, v.m, P.p, P.k0, P.k1, fbn,
+                                                       nchunks, cps, stages, Y, ldy);
+  return cudaGetLastError();
+}
+
+}  // namespace cdmd

@@ -343,3 +343,19 @@ def test_device_eig_matches_lapack(C, k, seed):
         res = np.linalg.norm(A @ v - lam[j] * v) / (np.linalg.norm(A) * np.linalg.norm(v))
         assert res < 1e-12, (j, res)
         j += jn
+
+
+@pytest.mark.parametrize("W,Hh,m,p", [(720, 480, 300, 1500), (333, 101, 77, 200), (128, 8, 600, 130)])
+def test_rademacher_tensor_core_sketch_equals_simt(C, H, W, Hh, m, p, monkeypatch):
+    """tcgen05 kind::i8 split-K sketch vs the dp4a kernel: both exact int32 -> identical."""
+    X = make_video(W, Hh, m, seed=W + m, noise=2.0, n_rects=1)
+    n = X.shape[1]
+    Xd = to_dev(X)
+    P = C.Pipeline(H, n, n, m, "rademacher", p, 8, 2)
+    a = P.sketch(Xd).clone()
+    monkeypatch.setenv("CDMD_SIMT_SKETCH", "1")
+    b = P.sketch(Xd).clone()
+    assert torch.equal(a, b)
+    rows = [0, p // 2, p - 1]
+    want = OS.sketch(X, OS.RADEMACHER, p, 0, rows=rows)
+    assert np.array_equal(a.cpu().numpy().T[rows].astype(np.int64), want)
