@@ -308,4 +308,64 @@ class Pipeline:
         return self.foreground(X, tau, mode, stream)
 
 
+class Streaming:
+    """Multi-batch streaming driver (a long video is decomposed in independent
+    consecutive batches).  `lanes` independent (handle, CUDA stream, buffers, host
+    thread) sets run batches round-robin, so the latency-bound small solve of one
+    batch (cdmd_fit, which blocks its own host thread) overlaps the HBM-bound passes
+    and solves of the others.  Each batch runs the same five calls as Pipeline.run.
+    With torch.distributed initialised, the per-batch all-reduces are issued in batch
+    order on every rank (a ticket lock), so collectives match across ranks."""
+
+    def __init__(self, device, n_total, n_local, m, kind, p, k, K, lanes=4, s=0.0, seed=0, pix0=0, dt=1.0):
+        import threading
+        self.lanes = []
+        for _ in range(lanes):
+            h = Handle(device)
+            st = torch.cuda.Stream(device=device)
+            with torch.cuda.stream(st):
+                pipe = Pipeline(h, n_total, n_local, m, kind, p, k, K, s=s, seed=seed, pix0=pix0,
+                                device=f"cuda:{device}", dt=dt)
+            self.lanes.append((h, st, pipe))
+        self._cv = threading.Condition()
+        self._next_ar = 0
+
+    def _ordered_allreduce(self, b, fn, Y):
+        with self._cv:
+            self._cv.wait_for(lambda: self._next_ar == b)
+            fn(Y)
+            self._next_ar += 1
+            self._cv.notify_all()
+
+    def run(self, videos, tau, mode=BG_DYNAMIC, allreduce=None, start_event=None):
+        """videos: list of uint8 CUDA tensors (m, ld), one per batch.  Returns the
+        per-lane end events (record them into the caller's stream to join)."""
+        import concurrent.futures as cf
+        self._next_ar = 0
+        L = len(self.lanes)
+        ends = [None] * L
+
+        def lane_work(li):
+            h, st, pipe = self.lanes[li]
+            with torch.cuda.stream(st):
+                if start_event is not None:
+                    st.wait_event(start_event)
+                for b in range(li, len(videos), L):
+                    X = videos[b]
+                    pipe.sketch(X, st)
+                    if allreduce is not None:
+                        self._ordered_allreduce(b, allreduce, pipe.Y)
+                    pipe.fit(st)
+                    pipe.modes(X, st)
+                    pipe.foreground(X, tau, mode, st)
+                ev = torch.cuda.Event(enable_timing=True)
+                ev.record(st)
+                ends[li] = ev
+
+        with cf.ThreadPoolExecutor(L) as ex:
+            for f in [ex.submit(lane_work, i) for i in range(L)]:
+                f.result()
+        return ends
+
+
 from .dist import slab  # noqa: E402,F401  (re-export)
