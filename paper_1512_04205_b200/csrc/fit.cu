@@ -31,7 +31,7 @@ static constexpr double OMP_STOP = 1e-6;   // reading R12: stop when ||r|| <= 1e
 static constexpr double TIE_RTOL = 1e-9;   // reading R13
 
 struct FitWs {
-  double *Yd, *G, *A, *w, *V, *T, *B, *VR, *Wc, *SW, *T2, *Gf, *cf;
+  double *Yd, *G, *A, *w, *V, *T, *B, *VR, *Wc, *SW, *T2, *Gf, *cf, *ehw;
   int* dinfo;
   void* sy_dev;
   size_t sy_dev_bytes, sy_host_bytes;
@@ -41,18 +41,25 @@ struct FitWs {
 };
 
 size_t hqr_smem_bytes(int k);
+bool eh_supported(int n, int k);
+size_t eh_work_doubles(int n, int k);
+cudaError_t launch_eh(int n, int k, const double* G, int64_t ldg, double* lam, double* Zout, double* work,
+                      int* info, cudaStream_t st);
+
+// symmetric eigensolver: the 8-CTA cluster solver (eigh.cu, default for n1 <= 510),
+// CDMD_SYEV=d -> cuSOLVER syevd, CDMD_SYEV=dx -> cuSOLVER syevdx
+static int syev_mode(int n1, int k) {
+  const char* e = getenv("CDMD_SYEV");
+  if (e && e[0] == 'd' && e[1] == 0) return 1;
+  if (e && e[0] == 'd' && e[1] == 'x') return 2;
+  return eh_supported(n1, k) ? 0 : 2;
+}
 cudaError_t launch_hqr_eig(int k, const double* A, double* W, double* VR, int* info, cudaStream_t st);
 
 static bool use_device_eig(int k) {
   const char* e = getenv("CDMD_GEEV");
   if (e && e[0] == 'c') return false;
   return hqr_smem_bytes(k) <= 227 * 1024;
-}
-
-// truncated symmetric eigensolver: syevdx (k largest only, default) or syevd
-static bool use_syevdx() {
-  const char* e = getenv("CDMD_SYEV");
-  return !(e && e[0] == 'd' && e[1] == 0);
 }
 
 static size_t al(size_t b) { return (b + 255) & ~(size_t)255; }
@@ -79,6 +86,7 @@ static cdmd_status layout_ws(cdmd_handle h, int64_t p, int64_t m, int k, char* b
   W->Gf = (double*)take(sizeof(double) * k * k);
   W->cf = (double*)take(sizeof(double) * k);
   W->dinfo = (int*)take(sizeof(int) * 16);
+  W->ehw = (double*)take(sizeof(double) * eh_work_doubles((int)n1, k));
   // solver workspaces (queried with the final dimensions)
   size_t d = 0, hb = 0;
   if (cusolverDnXsyevd_bufferSize(h->solver, h->params, CUSOLVER_EIG_MODE_VECTOR,
@@ -561,7 +569,13 @@ cdmd_status fit_impl(cdmd_handle h, const void* Y, int64_t ldy, int kind, int64_
   size_t hneed = W.sy_host_bytes > W.ge_host_bytes ? W.sy_host_bytes : W.ge_host_bytes;
   if (h->host_ws.size() < hneed + 16) h->host_ws.resize(hneed + 16);
   int64_t top = n1 - 1;
-  if (use_syevdx()) {
+  const int smode = syev_mode((int)n1, k);
+  if (smode == 0) {
+    // cluster tridiagonalisation + bisection + inverse iteration; k largest pairs
+    // written ascending into (W.w, W.A) like syevdx
+    CU(launch_eh((int)n1, k, W.G, m, W.w, W.A, W.ehw, W.dinfo + 8, st));
+    top = k - 1;
+  } else if (smode == 2) {
     // only the k largest eigenpairs (1-based indices n1-k+1 .. n1, ascending)
     int64_t meig = 0;
     double vl = 0.0, vu = 0.0;
