@@ -55,9 +55,14 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
 
 // G: n x n column-major (ld = ldg), symmetric.  Outputs d[n], e[n-1], tau[n],
 // V: n x n column-major holding reflector j in column j (entries j+1 .. n-1, v[j+1] = 1).
+__device__ unsigned long long g_eh_prof[8];
+
 __global__ void __cluster_dims__(EH_CL, 1, 1) __launch_bounds__(EH_T, 1)
     eh_tridiag_kernel(int n, const double* __restrict__ G, int64_t ldg, double* __restrict__ d,
                       double* __restrict__ e, double* __restrict__ tau_out, double* __restrict__ V) {
+  unsigned long long tp[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  unsigned long long tq = clock64();
+#define EH_TICK(k) do { if (threadIdx.x == 0) { const unsigned long long t_ = clock64(); tp[k] += t_ - tq; tq = t_; } } while (0)
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = (int)cluster.block_rank();
   extern __shared__ double sm[];
@@ -65,13 +70,14 @@ __global__ void __cluster_dims__(EH_CL, 1, 1) __launch_bounds__(EH_T, 1)
   const int64_t stride = (n + EH_CL - 1) / EH_CL + 1;  // cbuf row stride (max rows per CTA + 1)
   double* Aloc = sm;                                   // lower-triangle rows of this CTA
   double* xbuf = Aloc + eh_asz_max(n);                 // [n] column below the diagonal
-  double* pbuf = xbuf + n;                             // [n] p = tau A v
-  double* cbuf = pbuf + n;                             // [8][stride] column contributions
+  double* pbuf2 = xbuf + n;                            // [2][n] p = tau A v (double-buffered)
+  double* cbuf = pbuf2 + 2 * n;                        // [8][stride] column contributions
   double* nrm = cbuf + EH_CL * stride;                 // [8] partial squared norms
-  double* kpart = nrm + EH_CL;                         // [8] partial p.v
-  double* v = kpart + EH_CL;                           // [n]
+  double* kpart2 = nrm + EH_CL;                        // [2][8] partial p.v (double-buffered)
+  double* v = kpart2 + 2 * EH_CL;                      // [n]
   double* w = v + n;                                   // [n]
-  double* red = w + n;                                 // [33]
+  double* red = w + n;                                 // [40]
+  double* cpart = red + 40;                            // [16 warps][n] column partial sums
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   // load own rows (lower part) from G
   for (int64_t s = 0; s < nr; ++s) {
@@ -79,9 +85,13 @@ __global__ void __cluster_dims__(EH_CL, 1, 1) __launch_bounds__(EH_T, 1)
     double* row = Aloc + eh_off(rank, s);
     for (int64_t c = tid; c <= i; c += EH_T) row[c] = G[i + c * ldg];
   }
+  for (int i = tid; i < (EH_T / 32) * n; i += EH_T) cpart[i] = 0.0;
   __syncthreads();
   cluster.sync();
+  EH_TICK(0);
   for (int j = 0; j < n - 1; ++j) {
+    double* pbuf = pbuf2 + (j & 1) * n;
+    double* kpart = kpart2 + (j & 1) * EH_CL;
     // (a) push own entries of column j (rows i > j) and the partial norm of x[1:]
     double part = 0.0;
     for (int64_t s = tid; s < nr; s += EH_T) {
@@ -95,7 +105,9 @@ __global__ void __cluster_dims__(EH_CL, 1, 1) __launch_bounds__(EH_T, 1)
     part = block_sum(part, red);
     if (tid == 0)
       for (int r = 0; r < EH_CL; ++r) cluster.map_shared_rank(nrm, r)[rank] = part;
+    EH_TICK(1);
     cluster.sync();
+    EH_TICK(2);
     // (b) Householder reflector (redundantly on every CTA): H = I - tau v v^T
     double xn2 = 0.0;
     for (int r = 0; r < EH_CL; ++r) xn2 += nrm[r];
@@ -117,29 +129,39 @@ __global__ void __cluster_dims__(EH_CL, 1, 1) __launch_bounds__(EH_T, 1)
     if (tau != 0.0) {
       for (int i = j + 1 + tid; i < n; i += EH_T)
         if ((i % EH_CL) == rank) V[i + (int64_t)j * n] = v[i];   // reflector for the back transform
-      // (c) p = tau A v on the trailing block: own-row part (warp per row) and
-      //     column contributions to every row (thread per column), reduce-scattered
+      // (c) p = tau A v on the trailing block, one sweep over the own rows (warp per
+      //     row): the row part s_l = sum_{i<=l} A[l][i] v_i and the column part
+      //     c_i += A[l][i] v_l (per-warp partials), then the column sums are
+      //     reduce-scattered to the rows' owners
+      double* cw = cpart + warp * n;
       for (int64_t s = warp; s < nr; s += EH_T / 32) {
         const int64_t l = rank + EH_CL * s;
         if (l <= j) continue;
         const double* row = Aloc + eh_off(rank, s);
+        const double vl = v[l];
         double acc = 0.0;
-        for (int64_t i = j + 1 + lane; i <= l; i += 32) acc += row[i] * v[i];
+        for (int64_t i = j + 1 + lane; i < l; i += 32) {
+          const double a = row[i];
+          acc += a * v[i];
+          cw[i] += a * vl;
+        }
         for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (lane == 0) pbuf[l] = acc;   // own-row partial (only own rows are read)
+        if (lane == 0) pbuf[l] = acc + row[l] * vl;   // own-row partial incl. the diagonal
       }
+      __syncthreads();
       for (int i = j + 1 + tid; i < n; i += EH_T) {
         double acc = 0.0;
-        int64_t s0 = (i - rank) / EH_CL + 1;   // first own row l > i
-        if (i < rank) s0 = 0;
-        for (int64_t s = s0; s < nr; ++s) {
-          const int64_t l = rank + EH_CL * s;
-          if (l > i) acc += Aloc[eh_off(rank, s) + i] * v[l];
+#pragma unroll
+        for (int q = 0; q < EH_T / 32; ++q) {
+          acc += cpart[q * n + i];
+          cpart[q * n + i] = 0.0;
         }
         // to the owner of row i, slot (source rank, local row i / 8)
         cluster.map_shared_rank(cbuf, i % EH_CL)[(int64_t)rank * stride + i / EH_CL] = acc;
       }
+      EH_TICK(3);
       cluster.sync();
+      EH_TICK(2);
       // (d) owners complete p for their rows and push it; partial p.v
       double kp = 0.0;
       for (int64_t s = tid; s < nr; s += EH_T) {
@@ -154,7 +176,9 @@ __global__ void __cluster_dims__(EH_CL, 1, 1) __launch_bounds__(EH_T, 1)
       kp = block_sum(kp, red);
       if (tid == 0)
         for (int r = 0; r < EH_CL; ++r) cluster.map_shared_rank(kpart, r)[rank] = kp;
+      EH_TICK(4);
       cluster.sync();
+      EH_TICK(2);
       // (e) w = p - (tau/2)(p.v) v; rank-2 update of own rows: A -= v w^T + w v^T
       double pv = 0.0;
       for (int r = 0; r < EH_CL; ++r) pv += kpart[r];
@@ -169,14 +193,20 @@ __global__ void __cluster_dims__(EH_CL, 1, 1) __launch_bounds__(EH_T, 1)
         for (int64_t i = j + 1 + lane; i <= l; i += 32) row[i] -= vl * w[i] + wl * v[i];
       }
       __syncthreads();
+      EH_TICK(5);
     }
-    cluster.sync();   // buffers (xbuf, nrm, v) are rewritten by the next column
+    // no trailing cluster barrier: p and p.v are double-buffered, and every other
+    // remote write of the next column happens after a barrier its readers passed
   }
+  cluster.sync();
+  if (rank == 0 && threadIdx.x == 0)
+    for (int k = 0; k < 8; ++k) g_eh_prof[k] = tp[k];
   if (rank == ((n - 1) % EH_CL) && tid == 0) d[n - 1] = Aloc[eh_off(rank, (n - 1) / EH_CL) + (n - 1)];
 }
 
 // Sturm count: number of eigenvalues of T(d, e) smaller than x
-__device__ int eh_sturm(int n, const double* d, const double* e2, double x, double pivmin) {
+__device__ int eh_sturm(int n, const double* __restrict__ d, const double* __restrict__ e2, double x,
+                        double pivmin) {
   int cnt = 0;
   double q = d[0] - x;
   if (fabs(q) < pivmin) q = -pivmin;
@@ -189,87 +219,92 @@ __device__ int eh_sturm(int n, const double* d, const double* e2, double x, doub
   return cnt;
 }
 
-// One block.  The (r+1)-th largest eigenvalue of T goes to lam[k-1-r] (ascending
-// output, as syevd) and its eigenvector to Z[:, k-1-r]
-// eigenvector of T (unit norm).  Clusters (relative gap <= 1e-3 of ||T||) are
-// handled by one thread with modified Gram-Schmidt between inverse iterations.
-__global__ void __launch_bounds__(256) eh_tridiag_eig_kernel(int n, int k, const double* __restrict__ d,
-                                                             const double* __restrict__ e, double* __restrict__ lam,
-                                                             double* __restrict__ Z, double* __restrict__ work,
-                                                             int* __restrict__ info) {
-  extern __shared__ double sh[];
-  double* sd = sh;            // n
-  double* se = sd + n;        // n
-  double* se2 = se + n;       // n
-  double* slam = se2 + n;     // k
-  __shared__ double tnorm_s, pivmin_s, gl_s, gu_s;
-  __shared__ int cstart[256];
-  const int tid = threadIdx.x;
-  for (int i = tid; i < n; i += blockDim.x) {
-    sd[i] = d[i];
-    se[i] = i < n - 1 ? e[i] : 0.0;
-    se2[i] = se[i] * se[i];
-  }
-  __syncthreads();
-  if (tid == 0) {
-    double gl = sd[0], gu = sd[0], tn = 0.0, emax2 = 0.0;
+// Gershgorin bounds, ||T||, pivmin and e^2 (one block)
+__global__ void eh_prep_kernel(int n, const double* __restrict__ d, const double* __restrict__ e,
+                               double* __restrict__ e2, double* __restrict__ bounds) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) e2[i] = i < n - 1 ? e[i] * e[i] : 0.0;
+  if (threadIdx.x == 0) {
+    double gl = d[0], gu = d[0], tn = 0.0, emax2 = 0.0;
     for (int i = 0; i < n; ++i) {
-      const double r = (i > 0 ? fabs(se[i - 1]) : 0.0) + (i < n - 1 ? fabs(se[i]) : 0.0);
-      gl = fmin(gl, sd[i] - r);
-      gu = fmax(gu, sd[i] + r);
-      tn = fmax(tn, fabs(sd[i]) + r);
-      emax2 = fmax(emax2, se2[i]);
+      const double r = (i > 0 ? fabs(e[i - 1]) : 0.0) + (i < n - 1 ? fabs(e[i]) : 0.0);
+      gl = fmin(gl, d[i] - r);
+      gu = fmax(gu, d[i] + r);
+      tn = fmax(tn, fabs(d[i]) + r);
+      if (i < n - 1) emax2 = fmax(emax2, e[i] * e[i]);
     }
-    tnorm_s = tn;
-    pivmin_s = fmax(2.2250738585072014e-308 * fmax(emax2, 1.0), 1e-300);
-    const double pad = 2.0 * 2.220446049250313e-16 * tn * n + 2.0 * pivmin_s;
-    gl_s = gl - pad;
-    gu_s = gu + pad;
+    const double pivmin = fmax(2.2250738585072014e-308 * fmax(emax2, 1.0), 1e-300);
+    const double pad = 2.0 * 2.220446049250313e-16 * tn * n + 2.0 * pivmin;
+    bounds[0] = gl - pad;
+    bounds[1] = gu + pad;
+    bounds[2] = tn;
+    bounds[3] = pivmin;
   }
-  __syncthreads();
+}
+
+// One warp per wanted eigenvalue: 32-point multisection (5 bits per round) on Sturm
+// counts.  The (r+1)-th largest eigenvalue (ascending index n-1-r) goes to lam[k-1-r].
+__global__ void __launch_bounds__(32) eh_bisect_kernel(int n, int k, const double* __restrict__ d,
+                                                       const double* __restrict__ e2,
+                                                       const double* __restrict__ bounds,
+                                                       double* __restrict__ lam) {
+  const int r = blockIdx.x, lane = threadIdx.x;
+  if (r >= k) return;
+  const int idx = n - 1 - r;
+  double lo = bounds[0], hi = bounds[1];
+  const double pivmin = bounds[3];
   const double eps = 2.220446049250313e-16;
-  // ---- bisection: eigenvalue with ascending index n-1-r
-  for (int r = tid; r < k; r += blockDim.x) {
-    const int idx = n - 1 - r;  // want count(< x) = idx at the lower end
-    double lo = gl_s, hi = gu_s;
-    for (int it = 0; it < 200; ++it) {
-      const double mid = 0.5 * (lo + hi);
-      if (hi - lo <= 2.0 * eps * fmax(fabs(lo), fabs(hi)) + pivmin_s) break;
-      if (eh_sturm(n, sd, se2, mid, pivmin_s) > idx) hi = mid;
-      else lo = mid;
-    }
-    slam[r] = 0.5 * (lo + hi);
+  for (int round = 0; round < 40; ++round) {
+    if (hi - lo <= 2.0 * eps * fmax(fabs(lo), fabs(hi)) + pivmin) break;
+    const double x = lo + (hi - lo) * (double)(lane + 1) / 33.0;
+    const int c = eh_sturm(n, d, e2, x, pivmin);
+    // points with count <= idx lie below the eigenvalue
+    const unsigned below = __ballot_sync(0xffffffffu, c <= idx);
+    const int nb = __popc(below);   // counts are monotone: the first nb points are below
+    const double nlo = nb > 0 ? lo + (hi - lo) * (double)nb / 33.0 : lo;
+    const double nhi = nb < 32 ? lo + (hi - lo) * (double)(nb + 1) / 33.0 : hi;
+    lo = nlo;
+    hi = nhi;
   }
-  __syncthreads();
-  // ---- clusters (descending order): start indices
-  if (tid == 0) {
-    int nc = 0;
+  if (lane == 0) lam[k - 1 - r] = 0.5 * (lo + hi);
+}
+
+// Inverse iteration on T - lambda I (LU with partial pivoting), one thread per group
+// of eigenvalues closer than 1e-7 ||T|| (re-orthogonalised with modified Gram-Schmidt,
+// as LAPACK dstein does for clusters).  lam ascending (k largest); Z[:, q] <-> lam[q].
+__global__ void __launch_bounds__(128) eh_invit_kernel(int n, int k, const double* __restrict__ d,
+                                                       const double* __restrict__ e,
+                                                       const double* __restrict__ bounds,
+                                                       const double* __restrict__ lam, double* __restrict__ Z,
+                                                       double* __restrict__ work, int* __restrict__ info) {
+  __shared__ int cstart[258];
+  const double tnorm = bounds[2];
+  const double eps = 2.220446049250313e-16;
+  if (threadIdx.x == 0) {
+    int nc = 0;   // groups in descending order r = 0 .. k-1 (q = k-1-r)
     for (int r = 0; r < k; ++r)
-      if (r == 0 || fabs(slam[r - 1] - slam[r]) > 1e-3 * tnorm_s) cstart[nc++] = r;
+      if (r == 0 || fabs(lam[k - r] - lam[k - 1 - r]) > 1e-7 * tnorm) cstart[nc++] = r;
     cstart[nc] = k;
-    cstart[255] = nc;
+    cstart[257] = nc;
   }
   __syncthreads();
-  const int ncl = cstart[255];
-  // ---- inverse iteration, one thread per cluster; work: 6 n doubles per thread
-  for (int c = tid; c < ncl; c += blockDim.x) {
-    double* wk = work + (int64_t)c * 6 * n;
-    double* u = wk;            // U diagonal
-    double* u1 = u + n;        // first superdiagonal
-    double* u2 = u1 + n;       // second superdiagonal
-    double* lm = u2 + n;       // multipliers
-    double* z = lm + n;        // iterate
-    double* piv = z + n;       // row interchange flags
+  const int ncl = cstart[257];
+  for (int c = threadIdx.x; c < ncl; c += blockDim.x) {
+    double* u = work + (int64_t)c * 6 * n;
+    double* u1 = u + n;
+    double* u2 = u1 + n;
+    double* lm = u2 + n;
+    double* z = lm + n;
+    double* piv = z + n;
     for (int r = cstart[c]; r < cstart[c + 1]; ++r) {
-      const double lambda = slam[r];
-      // LU with partial pivoting of T - lambda I (rows i, i+1 may swap)
-      const double tiny = eps * tnorm_s;
-      double a = sd[0] - lambda, b = n > 1 ? se[0] : 0.0;
+      const int q = k - 1 - r;
+      const double lambda = lam[q];
+      const double tiny = eps * tnorm;
+      double a = d[0] - lambda, b = n > 1 ? e[0] : 0.0;
       for (int i = 0; i < n - 1; ++i) {
-        const double sub = se[i];            // T[i+1][i]
-        const double dnext = sd[i + 1] - lambda;
-        const double enext = (i + 1 < n - 1) ? se[i + 1] : 0.0;
-        if (fabs(a) >= fabs(sub)) {          // no interchange
+        const double sub = e[i];
+        const double dnext = d[i + 1] - lambda;
+        const double enext = (i + 1 < n - 1) ? e[i + 1] : 0.0;
+        if (fabs(a) >= fabs(sub)) {
           piv[i] = 0.0;
           const double mult = (a != 0.0) ? sub / a : 0.0;
           lm[i] = mult;
@@ -278,7 +313,7 @@ __global__ void __launch_bounds__(256) eh_tridiag_eig_kernel(int n, int k, const
           u2[i] = 0.0;
           a = dnext - mult * b;
           b = enext;
-        } else {                             // interchange rows i and i+1
+        } else {
           piv[i] = 1.0;
           const double mult = a / sub;
           lm[i] = mult;
@@ -290,10 +325,8 @@ __global__ void __launch_bounds__(256) eh_tridiag_eig_kernel(int n, int k, const
         }
       }
       u[n - 1] = (fabs(a) > tiny) ? a : (a >= 0 ? tiny : -tiny);
-      // start vector (deterministic, non-degenerate)
       for (int i = 0; i < n; ++i) z[i] = 1.0 + 0.5 * sin(1.0 + 0.713 * i + 0.37 * r);
-      for (int it = 0; it < 6; ++it) {
-        // forward: apply the row interchanges and multipliers (L^-1 P)
+      for (int it = 0; it < 3; ++it) {
         for (int i = 0; i < n - 1; ++i) {
           if (piv[i] != 0.0) {
             const double t = z[i];
@@ -303,17 +336,15 @@ __global__ void __launch_bounds__(256) eh_tridiag_eig_kernel(int n, int k, const
             z[i + 1] -= lm[i] * z[i];
           }
         }
-        // back substitution with U (diag u, super u1, u2)
         for (int i = n - 1; i >= 0; --i) {
-          double s = z[i];
-          if (i + 1 < n) s -= u1[i] * z[i + 1];
-          if (i + 2 < n) s -= u2[i] * z[i + 2];
-          z[i] = s / u[i];
+          double s2 = z[i];
+          if (i + 1 < n) s2 -= u1[i] * z[i + 1];
+          if (i + 2 < n) s2 -= u2[i] * z[i + 2];
+          z[i] = s2 / u[i];
         }
-        // re-orthogonalise against the earlier members of the cluster
-        for (int q = cstart[c]; q < r; ++q) {
+        for (int rr = cstart[c]; rr < r; ++rr) {
+          const double* zq = Z + (int64_t)(k - 1 - rr) * n;
           double dot = 0.0;
-          const double* zq = Z + (int64_t)(k - 1 - q) * n;
           for (int i = 0; i < n; ++i) dot += zq[i] * z[i];
           for (int i = 0; i < n; ++i) z[i] -= dot * zq[i];
         }
@@ -322,42 +353,67 @@ __global__ void __launch_bounds__(256) eh_tridiag_eig_kernel(int n, int k, const
         const double inv = 1.0 / sqrt(nn);
         for (int i = 0; i < n; ++i) z[i] *= inv;
       }
-      // sign convention: largest component positive
       int im = 0;
       for (int i = 1; i < n; ++i)
         if (fabs(z[i]) > fabs(z[im])) im = i;
       const double sg = z[im] < 0 ? -1.0 : 1.0;
-      for (int i = 0; i < n; ++i) Z[i + (int64_t)(k - 1 - r) * n] = sg * z[i];
-      lam[k - 1 - r] = slam[r];
+      for (int i = 0; i < n; ++i) Z[i + (int64_t)q * n] = sg * z[i];
     }
   }
-  if (tid == 0) *info = 0;
+  if (threadIdx.x == 0) *info = 0;
 }
 
-// Z <- Q Z, Q = H_0 H_1 ... H_{n-2}; one warp per column of Z (k columns).
+// Z <- Q Z, Q = H_0 H_1 ... H_{n-2}: blocks of 16 columns (one warp each, the column in
+// shared memory); reflectors staged through shared memory 16 at a time.
+constexpr int EH_RB = 16;
 __global__ void __launch_bounds__(512) eh_backtransform_kernel(int n, int k, const double* __restrict__ V,
                                                                const double* __restrict__ tau,
                                                                double* __restrict__ Z) {
-  const int col = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (col >= k) return;
-  double* z = Z + (int64_t)col * n;
-  for (int j = n - 2; j >= 0; --j) {
-    const double tj = tau[j];
-    if (tj == 0.0) continue;
-    const double* vj = V + (int64_t)j * n;
-    double s = 0.0;
-    for (int i = j + 1 + lane; i < n; i += 32) s += vj[i] * z[i];
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    s *= tj;
-    for (int i = j + 1 + lane; i < n; i += 32) z[i] -= s * vj[i];
-    __syncwarp();
+  extern __shared__ double bsm[];
+  double* zs = bsm;                       // [16][n]
+  double* vs = zs + 16 * (size_t)n;       // [EH_RB][n]
+  __shared__ double ts[EH_RB];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int col = blockIdx.x * 16 + warp;
+  for (int i = threadIdx.x; i < 16 * n; i += blockDim.x) {
+    const int cc = blockIdx.x * 16 + i / n;
+    zs[i] = cc < k ? Z[(int64_t)cc * n + i % n] : 0.0;
+  }
+  for (int jb = n - 2; jb >= 0; jb -= EH_RB) {
+    const int j0 = jb - EH_RB + 1 > 0 ? jb - EH_RB + 1 : 0;
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < (jb - j0 + 1) * n; idx += blockDim.x) {
+      const int jj = j0 + idx / n, i = idx % n;
+      vs[(jj - j0) * n + i] = i > jj ? V[(int64_t)jj * n + i] : 0.0;
+    }
+    if (threadIdx.x < jb - j0 + 1) ts[threadIdx.x] = tau[j0 + threadIdx.x];
+    __syncthreads();
+    if (col < k) {
+      double* z = zs + warp * n;
+      for (int j = jb; j >= j0; --j) {
+        const double tj = ts[j - j0];
+        if (tj == 0.0) continue;
+        const double* vj = vs + (j - j0) * n;
+        double sacc = 0.0;
+        for (int i = j + 1 + lane; i < n; i += 32) sacc += vj[i] * z[i];
+        for (int o = 16; o > 0; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
+        sacc *= tj;
+        for (int i = j + 1 + lane; i < n; i += 32) z[i] -= sacc * vj[i];
+        __syncwarp();
+      }
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 16 * n; i += blockDim.x) {
+    const int cc = blockIdx.x * 16 + i / n;
+    if (cc < k) Z[(int64_t)cc * n + i % n] = zs[i];
   }
 }
 
 size_t eh_tridiag_smem(int n) {
   const int64_t stride = (n + EH_CL - 1) / EH_CL + 1;
-  return sizeof(double) * ((size_t)eh_asz_max(n) + 4 * (size_t)n + EH_CL * stride + 2 * EH_CL + 40);
+  return sizeof(double) * ((size_t)eh_asz_max(n) + 5 * (size_t)n + EH_CL * stride + 3 * EH_CL + 40 +
+                           (size_t)(EH_T / 32) * n);
 }
 
 bool eh_supported(int n, int k) { return n >= 3 && n <= EH_NMAX && k <= 256 && eh_tridiag_smem(n) <= 227 * 1024; }
@@ -367,6 +423,8 @@ size_t eh_work_doubles(int n, int k) {
 }
 
 // G (n x n, ld ldg) -> lam[k] (ascending: the k largest), Zout (n x k column-major, ld n).
+void eh_prof_read(unsigned long long* out) { cudaMemcpyFromSymbol(out, g_eh_prof, sizeof(unsigned long long) * 8); }
+
 cudaError_t launch_eh(int n, int k, const double* G, int64_t ldg, double* lam, double* Zout, double* work,
                       int* info, cudaStream_t st) {
   double* V = work;
@@ -379,12 +437,16 @@ cudaError_t launch_eh(int n, int k, const double* G, int64_t ldg, double* lam, d
   if (err != cudaSuccess) return err;
   eh_tridiag_kernel<<<EH_CL, EH_T, smem, st>>>(n, G, ldg, d, e, tau, V);
   if ((err = cudaGetLastError()) != cudaSuccess) return err;
-  const size_t smem2 = sizeof(double) * (3 * (size_t)n + k);
-  err = cudaFuncSetAttribute(eh_tridiag_eig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
+  double* e2 = wk;
+  double* bounds = e2 + n;
+  double* ivw = bounds + 8;
+  eh_prep_kernel<<<1, 256, 0, st>>>(n, d, e, e2, bounds);
+  eh_bisect_kernel<<<k, 32, 0, st>>>(n, k, d, e2, bounds, lam);
+  eh_invit_kernel<<<1, 128, 0, st>>>(n, k, d, e, bounds, lam, Zout, ivw, info);
+  const size_t smem3 = sizeof(double) * (16 + EH_RB) * (size_t)n;
+  err = cudaFuncSetAttribute(eh_backtransform_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3);
   if (err != cudaSuccess) return err;
-  eh_tridiag_eig_kernel<<<1, 256, smem2, st>>>(n, k, d, e, lam, Zout, wk, info);
-  if ((err = cudaGetLastError()) != cudaSuccess) return err;
-  eh_backtransform_kernel<<<(unsigned)ceil_div(k, 16), 512, 0, st>>>(n, k, V, tau, Zout);
+  eh_backtransform_kernel<<<(unsigned)ceil_div(k, 16), 512, smem3, st>>>(n, k, V, tau, Zout);
   return cudaGetLastError();
 }
 

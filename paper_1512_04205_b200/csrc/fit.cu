@@ -42,6 +42,7 @@ struct FitWs {
 
 size_t hqr_smem_bytes(int k);
 bool eh_supported(int n, int k);
+void eh_prof_read(unsigned long long* out);
 size_t eh_work_doubles(int n, int k);
 cudaError_t launch_eh(int n, int k, const double* G, int64_t ldg, double* lam, double* Zout, double* work,
                       int* info, cudaStream_t st);
@@ -661,6 +662,12 @@ cdmd_status fit_impl(cdmd_handle h, const void* Y, int64_t ldy, int kind, int64_
   CU(cudaStreamSynchronize(st));
   prof.mark("quant+sync");
   prof.report();
+  if (prof.on && syev_mode((int)n1, k) == 0) {
+    unsigned long long t[8];
+    eh_prof_read(t);
+    fprintf(stderr, "[cdmd_eh] load %llu  a %llu  sync %llu  c %llu  d %llu  e %llu (cycles, CTA 0)\n", t[0], t[1],
+            t[2], t[3], t[4], t[5]);
+  }
   model->K_eff = h->host_info[INFO_K_SEL];
   model->n_coef = h->host_info[INFO_N_COEF];
   model->dt = dt;
