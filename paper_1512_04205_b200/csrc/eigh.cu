@@ -62,7 +62,11 @@ __global__ void __cluster_dims__(EH_CL, 1, 1) __launch_bounds__(EH_T, 1)
                       double* __restrict__ e, double* __restrict__ tau_out, double* __restrict__ V) {
   unsigned long long tp[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   unsigned long long tq = clock64();
+#ifdef CDMD_EH_PROF
 #define EH_TICK(k) do { if (threadIdx.x == 0) { const unsigned long long t_ = clock64(); tp[k] += t_ - tq; tq = t_; } } while (0)
+#else
+#define EH_TICK(k) do { (void)tq; } while (0)
+#endif
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = (int)cluster.block_rank();
   extern __shared__ double sm[];
