@@ -236,8 +236,14 @@ __global__ void __launch_bounds__(256) sketch_gaussian_simt_kernel(
     }
 }
 
+bool sketch_gaussian_tc_supported(const cdmd_video& v);
+cudaError_t launch_sketch_gaussian_tc(const cdmd_video& v, const SensingPlan& P, const uint16_t* table, float* Y,
+                                      int64_t ldy, cudaStream_t st);
+
 cudaError_t launch_sketch_gaussian(const cdmd_video& v, const SensingPlan& P, const uint16_t* table,
                                    float* Y, int64_t ldy, cudaStream_t st) {
+  if (sketch_gaussian_tc_supported(v) && !getenv("CDMD_SIMT_SKETCH"))
+    return launch_sketch_gaussian_tc(v, P, table, Y, ldy, st);
   dim3 grid((unsigned)ceil_div(P.p, 64), (unsigned)ceil_div(v.m, 64));
   sketch_gaussian_simt_kernel<<<grid, 256, 0, st>>>(v.X, v.ld, v.pix0, v.n_local, v.m, P.p, P.k0,
                                                     P.k1, table, Y, ldy);

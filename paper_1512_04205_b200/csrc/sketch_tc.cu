@@ -15,6 +15,7 @@
 // Pixel ranges are split across CTAs and the partial sums meet in Y through int32
 // atomics (exact and order-independent).  Warp roles: 0 TMA producer, 1 TMEM owner +
 // MMA issuer, 2..5 C generators and then the epilogue.
+#include <cuda_fp16.h>
 #include <cudaTypedefs.h>
 
 #include "common.cuh"
@@ -204,6 +205,233 @@ cudaError_t launch_sketch_rademacher_tc(const cdmd_video& v, const SensingPlan& 
   dim3 grid((unsigned)nrb, (unsigned)nfb, (unsigned)splits);
   sketch_rademacher_tc_kernel<<<grid, 192, smem, st>>>(mapX, v.pix0, v.n_local, v.m, P.p, P.k0, P.k1, fbn,
                                                        nchunks, cps, stages, Y, ldy);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------ Gaussian
+// Y = C D with c_ri = T[u16] (bf16-valued N(0,1)) as one split-K
+// kind::f16 GEMM with fp32 accumulation in TMEM (north_star: "bf16 x uint8-exact
+// operands accumulate in fp32 on tensor cores"):
+//   A = C tile, 128 rows x 64 pixels of fp16 (every table value is exact in fp16),
+//       regenerated in SMEM by eight generator warps: one Philox call -> eight 16-bit
+//       table indices -> one 16-B chunk; the table's positive half (32768 fp16) is
+//       resident in SMEM (T is odd-symmetric);
+//   B = X tile, <= 512 frames x 64 pixels, converted by four warps from uint8 to the
+//       exact fp16 value x - 128 (centred: 4x smaller partial sums); one spare frame row
+//       of ones yields sum_i c_ri, and the epilogue adds back 128 * sum_i c_ri;
+//   D = fp32 in TMEM (M = 128, N <= 512 over two MMAs), split-K partial sums meet in Y
+//       through fp32 atomics.
+constexpr int GS_BM = 128;            // rows of C per CTA
+constexpr int GS_BK = 64;             // pixels per stage (128-B fp16 rows)
+constexpr int GS_A = GS_BM * GS_BK * 2;   // bytes of an A stage
+constexpr int GS_GEN_WARPS = 8;
+constexpr int GS_CVT_WARPS = 4;
+constexpr int GS_THREADS = 32 * (1 + GS_GEN_WARPS + GS_CVT_WARPS);
+
+__global__ void __launch_bounds__(GS_THREADS, 1) sketch_gaussian_tc_kernel(
+    const uint8_t* __restrict__ X, int64_t ld, int64_t pix0, int64_t n_local, int64_t m, int64_t p,
+    uint32_t k0, uint32_t k1, const uint16_t* __restrict__ table_bf16, int npad, int nchunks_total,
+    int chunks_per_split, float* __restrict__ Y, int64_t ldy) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int BST = npad * GS_BK * 2;                     // bytes of a B stage
+  uint8_t* sA = smem;                                   // 2 x 16 KB
+  uint8_t* sB = sA + 2 * GS_A;                          // 2 x BST
+  uint16_t* htab = reinterpret_cast<uint16_t*>(sB + 2 * (size_t)BST);   // 32768 fp16 bits
+  uint64_t* afull = reinterpret_cast<uint64_t*>(htab + 32768);
+  uint64_t* bfull = afull + 2;
+  uint64_t* sempty = bfull + 2;
+  uint64_t* tfull = sempty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t r0 = (int64_t)blockIdx.x * GS_BM;
+  const int c_begin = blockIdx.y * chunks_per_split;
+  const int c_end = min(nchunks_total, c_begin + chunks_per_split);
+  const int nch = c_end - c_begin;
+  // positive half of the table as fp16 bits: T[32768 + j], j < 32768
+  for (int j = threadIdx.x; j < 32768; j += blockDim.x) {
+    const float v = __uint_as_float((uint32_t)table_bf16[32768 + j] << 16);
+    htab[j] = __half_as_ushort(__float2half_rn(v));   // exact: 8 significant bits
+  }
+  if (warp == 0 && lane == 0) {
+    for (int b = 0; b < 2; ++b) {
+      tc::mbar_init(&afull[b], GS_GEN_WARPS);
+      tc::mbar_init(&bfull[b], GS_CVT_WARPS);
+      tc::mbar_init(&sempty[b], 1);
+    }
+    tc::mbar_init(tfull, 1);
+    tc::fence_mbar_init();
+  }
+  if (warp == 0) tc::tmem_alloc(tmem_slot, 512);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ------------------------------------------- MMA issuer
+      const uint32_t aBase = tc::smem_u32(sA), bBase = tc::smem_u32(sB);
+      for (int i = 0; i < nch; ++i) {
+        const int st = i & 1;
+        const uint32_t ph = (uint32_t)(i >> 1) & 1u;
+        tc::mbar_wait(&afull[st], ph);
+        tc::mbar_wait(&bfull[st], ph);
+        tc::fence_after();
+        for (int nb = 0; nb < npad; nb += 256) {
+          const int nn = npad - nb < 256 ? npad - nb : 256;
+          const uint32_t idesc = tc::idesc_f16(GS_BM, nn, false, false, false, false);
+#pragma unroll
+          for (int kk = 0; kk < GS_BK / 16; ++kk) {
+            const uint64_t ad = tc::smem_desc_sw128(aBase + st * GS_A + kk * 32, 0, 1024);
+            const uint64_t bd = tc::smem_desc_sw128(bBase + st * BST + nb * 128 + kk * 32, 0, 1024);
+            tc::mma_f16(tmem_base + (uint32_t)nb, ad, bd, idesc, (i | kk) != 0);
+          }
+        }
+        tc::mma_commit(&sempty[st]);
+      }
+      tc::mma_commit(tfull);
+    }
+  } else if (warp <= GS_GEN_WARPS) {  // ---------------- C generators, then epilogue
+    const int g = threadIdx.x - 32;            // 0..255
+    const int rr = g & (GS_BM - 1);            // row of the tile
+    const int half = g >> 7;                   // pixels [32 half, 32 half + 32) of a stage
+    const int64_t row = r0 + rr;
+    for (int i = 0; i < nch; ++i) {
+      const int st = i & 1;
+      const uint32_t ph = (uint32_t)(i >> 1) & 1u;
+      tc::mbar_wait(&sempty[st], ph ^ 1u);
+      uint8_t* dst = sA + st * GS_A + rr * 128;
+      const int64_t gpx = pix0 + (int64_t)(c_begin + i) * GS_BK + 32 * half;   // global pixel of the first value
+#pragma unroll
+      for (int cq = 0; cq < 4; ++cq) {          // 8 pixels per Philox call and per 16-B chunk
+        uint4 w = make_uint4(0, 0, 0, 0);
+        if (row < p) w = philox(make_uint4((uint32_t)((gpx >> 3) + cq), (uint32_t)row, 0u, TAG_GAUSSIAN), k0, k1);
+        const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+        uint32_t h2[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint32_t hv[2];
+#pragma unroll
+          for (int b = 0; b < 2; ++b) {
+            const uint32_t u = (ws[q] >> (16 * b)) & 0xFFFFu;
+            hv[b] = (u & 0x8000u) ? htab[u & 0x7FFFu] : (uint32_t)(htab[0x7FFFu - u] ^ 0x8000u);
+          }
+          h2[q] = hv[0] | (hv[1] << 16);
+        }
+        const int chunk = 4 * half + cq;
+        *reinterpret_cast<uint4*>(dst + ((chunk ^ (rr & 7)) << 4)) = make_uint4(h2[0], h2[1], h2[2], h2[3]);
+      }
+      tc::fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&afull[st]);
+    }
+    if (warp <= 4) {  // epilogue: TMEM lane = row of C, column t = frame, column m = sum_i c_ri
+      tc::mbar_wait(tfull, 0);
+      tc::fence_after();
+      const int q = warp & 3;
+      const int64_t ry = r0 + q * 32 + lane;
+      const uint32_t ta = tmem_base + ((uint32_t)(q * 32) << 16);
+      uint32_t rs[16];
+      tc::tmem_ld16(ta + (uint32_t)(m & ~15), rs);
+      tc::tmem_ld_wait();
+      const float rowsum = __uint_as_float(rs[m & 15]);
+      for (int c0 = 0; c0 < (int)m; c0 += 16) {
+        uint32_t v[16];
+        tc::tmem_ld16(ta + c0, v);
+        tc::tmem_ld_wait();
+        if (ry < p && nch > 0) {
+#pragma unroll
+          for (int t = 0; t < 16; ++t)
+            if (c0 + t < m) atomicAdd(Y + ry + (int64_t)(c0 + t) * ldy, fmaf(128.0f, rowsum, __uint_as_float(v[t])));
+        }
+      }
+    }
+  } else {  // ------------------------------------ X converters: uint8 -> fp16 (x - 128)
+    const int cthr = threadIdx.x - 32 * (1 + GS_GEN_WARPS);   // 0..127
+    for (int i = 0; i < nch; ++i) {
+      const int st = i & 1;
+      const uint32_t ph = (uint32_t)(i >> 1) & 1u;
+      tc::mbar_wait(&sempty[st], ph ^ 1u);
+      uint8_t* bst = sB + (size_t)st * BST;
+      const int64_t jx = (int64_t)(c_begin + i) * GS_BK;   // local pixel of the stage
+      for (int task = cthr; task < npad * 4; task += 32 * GS_CVT_WARPS) {
+        const int f = task >> 2, qd = task & 3;            // frame row, 16-pixel quarter
+        const int64_t j = jx + 16 * qd;
+        uint4 o0, o1;
+        if (f < m) {
+          uint32_t xw[4] = {0, 0, 0, 0};
+          if (j + 16 <= n_local) {
+            const uint4 xv = __ldg(reinterpret_cast<const uint4*>(X + (int64_t)f * ld + j));
+            xw[0] = xv.x; xw[1] = xv.y; xw[2] = xv.z; xw[3] = xv.w;
+          } else {
+            for (int b = 0; b < 16; ++b)
+              if (j + b < n_local) xw[b >> 2] |= (uint32_t)X[(int64_t)f * ld + j + b] << (8 * (b & 3));
+          }
+          uint32_t hw[8];
+#pragma unroll
+          for (int b = 0; b < 8; ++b) {   // two pixels -> half2 (1024 + x) - 1152 = x - 128, exact
+            const uint32_t pr = __byte_perm(xw[b >> 1], 0x64646464u, (b & 1) ? 0x7372u : 0x5150u);
+            __half2 h = __hsub2(*reinterpret_cast<const __half2*>(&pr), __halves2half2(__ushort_as_half(0x6480), __ushort_as_half(0x6480)));
+            hw[b] = *reinterpret_cast<uint32_t*>(&h);
+          }
+          // pixels beyond the slab contribute nothing
+          if (j + 16 > n_local)
+            for (int b = 0; b < 16; ++b)
+              if (j + b >= n_local) hw[b >> 1] &= (b & 1) ? 0x0000FFFFu : 0xFFFF0000u;
+          o0 = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+          o1 = make_uint4(hw[4], hw[5], hw[6], hw[7]);
+        } else if (f == m) {                 // the row of ones: D[:, m] = sum_i c_ri
+          uint32_t hw[8];
+#pragma unroll
+          for (int b = 0; b < 8; ++b) {
+            const uint32_t lo = (j + 2 * b < n_local) ? 0x3C00u : 0u, hi = (j + 2 * b + 1 < n_local) ? 0x3C00u : 0u;
+            hw[b] = lo | (hi << 16);
+          }
+          o0 = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+          o1 = make_uint4(hw[4], hw[5], hw[6], hw[7]);
+        } else {
+          o0 = o1 = make_uint4(0, 0, 0, 0);
+        }
+        uint8_t* rowp = bst + (size_t)f * 128;
+        *reinterpret_cast<uint4*>(rowp + (((2 * qd) ^ (f & 7)) << 4)) = o0;
+        *reinterpret_cast<uint4*>(rowp + (((2 * qd + 1) ^ (f & 7)) << 4)) = o1;
+      }
+      tc::fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&bfull[st]);
+    }
+  }
+  __syncthreads();
+  if (warp == 0) {
+    tc::fence_after();
+    tc::tmem_dealloc(tmem_base, 512);
+  }
+}
+
+bool sketch_gaussian_tc_supported(const cdmd_video& v) { return v.m + 1 <= 512 && (v.ld % 16) == 0; }
+
+cudaError_t launch_sketch_gaussian_tc(const cdmd_video& v, const SensingPlan& P, const uint16_t* table, float* Y,
+                                      int64_t ldy, cudaStream_t st) {
+  const int npad = (int)round_up(v.m + 1, 16);     // frames + the row of ones
+  const int nrb = (int)ceil_div(P.p, GS_BM);
+  const int nchunks = (int)ceil_div(v.n_local, GS_BK);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int splits = sms / nrb;   // one CTA per SM (225 KB SMEM): a single wave
+  if (splits > nchunks) splits = nchunks;
+  if (splits < 1) splits = 1;
+  const int cps = (int)ceil_div(nchunks, splits);
+  splits = (int)ceil_div(nchunks, cps);
+  const size_t smem = 1024 + 2 * (size_t)GS_A + 2 * (size_t)npad * GS_BK * 2 + 65536 + 256;
+  cudaError_t e = cudaFuncSetAttribute(sketch_gaussian_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  e = cudaMemsetAsync(Y, 0, sizeof(float) * (size_t)ldy * v.m, st);
+  if (e != cudaSuccess) return e;
+  dim3 grid((unsigned)nrb, (unsigned)splits);
+  sketch_gaussian_tc_kernel<<<grid, GS_THREADS, smem, st>>>(v.X, v.ld, v.pix0, v.n_local, v.m, P.p, P.k0, P.k1, table,
+                                                            npad, nchunks, cps, Y, ldy);
   return cudaGetLastError();
 }
 

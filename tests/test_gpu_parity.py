@@ -359,3 +359,23 @@ def test_rademacher_tensor_core_sketch_equals_simt(C, H, W, Hh, m, p, monkeypatc
     rows = [0, p // 2, p - 1]
     want = OS.sketch(X, OS.RADEMACHER, p, 0, rows=rows)
     assert np.array_equal(a.cpu().numpy().T[rows].astype(np.int64), want)
+
+
+@pytest.mark.parametrize("W,Hh,m,p", [(160, 100, 50, 256), (333, 101, 77, 200), (720, 480, 300, 500)])
+def test_gaussian_tensor_core_sketch(C, H, W, Hh, m, p, monkeypatch):
+    """tcgen05 kind::f16 sketch (fp32 accumulation) vs the fp64-chunked SIMT kernel and
+    the oracle: per-column normwise <= 1e-4 (north_star), in practice ~1e-6."""
+    X = make_video(W, Hh, m, seed=W + 3 * m, noise=2.0, n_rects=1)
+    n = X.shape[1]
+    Xd = to_dev(X)
+    P = C.Pipeline(H, n, n, m, "gaussian", p, 8, 2)
+    a = P.sketch(Xd).clone().cpu().numpy().T.astype(np.float64)
+    monkeypatch.setenv("CDMD_SIMT_SKETCH", "1")
+    b = P.sketch(Xd).clone().cpu().numpy().T.astype(np.float64)
+    rows = [0, p // 3, p - 1]
+    want = OS.sketch(X, OS.GAUSSIAN, p, 0, rows=rows)
+    for got in (a, b):
+        d = np.linalg.norm(got[rows] - want, axis=1) / np.linalg.norm(want, axis=1)
+        assert d.max() <= PT.RTOL_Y_GAUSS, d.max()
+    col = np.linalg.norm(a - b, axis=0) / np.linalg.norm(b, axis=0)
+    assert col.max() <= 1e-5, col.max()
