@@ -216,7 +216,7 @@ cudaError_t launch_sketch_rademacher_tc(const cdmd_video& v, const SensingPlan& 
 //       regenerated in SMEM by eight generator warps: one Philox call -> eight 16-bit
 //       table indices -> one 16-B chunk; the table's positive half (32768 fp16) is
 //       resident in SMEM (T is odd-symmetric);
-//   B = X tile, <= 512 frames x 64 pixels, converted by four warps from uint8 to the
+//   B = X tile, <= 512 frames x 64 pixels, converted by eight warps from uint8 to the
 //       exact fp16 value x - 128 (centred: 4x smaller partial sums); one spare frame row
 //       of ones yields sum_i c_ri, and the epilogue adds back 128 * sum_i c_ri;
 //   D = fp32 in TMEM (M = 128, N <= 512 over two MMAs), split-K partial sums meet in Y
@@ -225,7 +225,8 @@ constexpr int GS_BM = 128;            // rows of C per CTA
 constexpr int GS_BK = 64;             // pixels per stage (128-B fp16 rows)
 constexpr int GS_A = GS_BM * GS_BK * 2;   // bytes of an A stage
 constexpr int GS_GEN_WARPS = 8;
-constexpr int GS_CVT_WARPS = 4;
+constexpr int GS_CVT_WARPS = 8;
+constexpr int GS_TASKS = 8;         // (frame, 16-px) slots per converter thread: 512 frames x 4 / 256
 constexpr int GS_THREADS = 32 * (1 + GS_GEN_WARPS + GS_CVT_WARPS);
 
 __global__ void __launch_bounds__(GS_THREADS, 1) sketch_gaussian_tc_kernel(
@@ -348,58 +349,78 @@ __global__ void __launch_bounds__(GS_THREADS, 1) sketch_gaussian_tc_kernel(
       }
     }
   } else {  // ------------------------------------ X converters: uint8 -> fp16 (x - 128)
-    const int cthr = threadIdx.x - 32 * (1 + GS_GEN_WARPS);   // 0..127
+    // each thread owns GS_TASKS (frame, 16-pixel quarter) slots of a stage; the bytes of
+    // the next stage are loaded into registers while the current one is converted
+    const int cthr = threadIdx.x - 32 * (1 + GS_GEN_WARPS);
+    constexpr int NT = 32 * GS_CVT_WARPS;
+    uint4 cur[GS_TASKS], nxt[GS_TASKS];
+    auto load_stage = [&](int i, uint4 (&buf)[GS_TASKS]) {
+      const int64_t jx = (int64_t)(c_begin + i) * GS_BK;
+#pragma unroll
+      for (int u = 0; u < GS_TASKS; ++u) {
+        const int task = cthr + NT * u;
+        const int f = task >> 2, qd = task & 3;
+        const int64_t j = jx + 16 * qd;
+        uint4 xv = make_uint4(0, 0, 0, 0);
+        if (f < m && task < npad * 4) {
+          if (j + 16 <= n_local) {
+            xv = __ldg(reinterpret_cast<const uint4*>(X + (int64_t)f * ld + j));
+          } else {
+            uint32_t xw[4] = {0, 0, 0, 0};
+            for (int b = 0; b < 16; ++b)
+              if (j + b < n_local) xw[b >> 2] |= (uint32_t)X[(int64_t)f * ld + j + b] << (8 * (b & 3));
+            xv = make_uint4(xw[0], xw[1], xw[2], xw[3]);
+          }
+        }
+        buf[u] = xv;
+      }
+    };
+    if (nch > 0) load_stage(0, cur);
     for (int i = 0; i < nch; ++i) {
       const int st = i & 1;
       const uint32_t ph = (uint32_t)(i >> 1) & 1u;
+      if (i + 1 < nch) load_stage(i + 1, nxt);
       tc::mbar_wait(&sempty[st], ph ^ 1u);
       uint8_t* bst = sB + (size_t)st * BST;
-      const int64_t jx = (int64_t)(c_begin + i) * GS_BK;   // local pixel of the stage
-      for (int task = cthr; task < npad * 4; task += 32 * GS_CVT_WARPS) {
-        const int f = task >> 2, qd = task & 3;            // frame row, 16-pixel quarter
+      const int64_t jx = (int64_t)(c_begin + i) * GS_BK;
+#pragma unroll
+      for (int u = 0; u < GS_TASKS; ++u) {
+        const int task = cthr + NT * u;
+        if (task >= npad * 4) break;
+        const int f = task >> 2, qd = task & 3;
         const int64_t j = jx + 16 * qd;
-        uint4 o0, o1;
+        uint32_t hw[8];
         if (f < m) {
-          uint32_t xw[4] = {0, 0, 0, 0};
-          if (j + 16 <= n_local) {
-            const uint4 xv = __ldg(reinterpret_cast<const uint4*>(X + (int64_t)f * ld + j));
-            xw[0] = xv.x; xw[1] = xv.y; xw[2] = xv.z; xw[3] = xv.w;
-          } else {
-            for (int b = 0; b < 16; ++b)
-              if (j + b < n_local) xw[b >> 2] |= (uint32_t)X[(int64_t)f * ld + j + b] << (8 * (b & 3));
-          }
-          uint32_t hw[8];
+          const uint32_t xw[4] = {cur[u].x, cur[u].y, cur[u].z, cur[u].w};
 #pragma unroll
           for (int b = 0; b < 8; ++b) {   // two pixels -> half2 (1024 + x) - 1152 = x - 128, exact
             const uint32_t pr = __byte_perm(xw[b >> 1], 0x64646464u, (b & 1) ? 0x7372u : 0x5150u);
-            __half2 h = __hsub2(*reinterpret_cast<const __half2*>(&pr), __halves2half2(__ushort_as_half(0x6480), __ushort_as_half(0x6480)));
+            __half2 h = __hsub2(*reinterpret_cast<const __half2*>(&pr),
+                                __halves2half2(__ushort_as_half(0x6480), __ushort_as_half(0x6480)));
             hw[b] = *reinterpret_cast<uint32_t*>(&h);
           }
-          // pixels beyond the slab contribute nothing
-          if (j + 16 > n_local)
+          if (j + 16 > n_local)   // pixels beyond the slab contribute nothing
             for (int b = 0; b < 16; ++b)
               if (j + b >= n_local) hw[b >> 1] &= (b & 1) ? 0x0000FFFFu : 0xFFFF0000u;
-          o0 = make_uint4(hw[0], hw[1], hw[2], hw[3]);
-          o1 = make_uint4(hw[4], hw[5], hw[6], hw[7]);
-        } else if (f == m) {                 // the row of ones: D[:, m] = sum_i c_ri
-          uint32_t hw[8];
+        } else if (f == m) {      // the row of ones: D[:, m] = sum_i c_ri
 #pragma unroll
           for (int b = 0; b < 8; ++b) {
             const uint32_t lo = (j + 2 * b < n_local) ? 0x3C00u : 0u, hi = (j + 2 * b + 1 < n_local) ? 0x3C00u : 0u;
             hw[b] = lo | (hi << 16);
           }
-          o0 = make_uint4(hw[0], hw[1], hw[2], hw[3]);
-          o1 = make_uint4(hw[4], hw[5], hw[6], hw[7]);
         } else {
-          o0 = o1 = make_uint4(0, 0, 0, 0);
+#pragma unroll
+          for (int b = 0; b < 8; ++b) hw[b] = 0u;
         }
         uint8_t* rowp = bst + (size_t)f * 128;
-        *reinterpret_cast<uint4*>(rowp + (((2 * qd) ^ (f & 7)) << 4)) = o0;
-        *reinterpret_cast<uint4*>(rowp + (((2 * qd + 1) ^ (f & 7)) << 4)) = o1;
+        *reinterpret_cast<uint4*>(rowp + (((2 * qd) ^ (f & 7)) << 4)) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+        *reinterpret_cast<uint4*>(rowp + (((2 * qd + 1) ^ (f & 7)) << 4)) = make_uint4(hw[4], hw[5], hw[6], hw[7]);
       }
       tc::fence_proxy_async();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&bfull[st]);
+#pragma unroll
+      for (int u = 0; u < GS_TASKS; ++u) cur[u] = nxt[u];
     }
   }
   __syncthreads();
