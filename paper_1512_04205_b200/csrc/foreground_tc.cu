@@ -94,8 +94,8 @@ __global__ void __launch_bounds__(32 * (2 + FG_EPI_WARPS), 1) foreground_tc_kern
     const int32_t* __restrict__ coef_col, int n_coef, float tau, uint32_t* __restrict__ mask,
     int64_t ldw, int num_tiles, int stages, int dbg) {
   constexpr int PART_B = FG_BN * KP * 2;  // bytes of one split part of Phi_F (B)
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem_raw[];   // 1024-B aligned: SWIZZLE_128B atoms
+  uint8_t* smem = smem_raw;                                  // (keeps the shared address space visible)
   const int mA = nfb * FG_BM;
   const int PART_A = mA * KP * 2;
   uint8_t* sX = smem;                                          // stages x 32 KB (SW128 boxes)

@@ -27,8 +27,8 @@ __global__ void __launch_bounds__(320, 1) modes_tc_kernel(
     const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, int64_t n_local,
     int nkb, int stages, int kpad, int k_eff, const double* __restrict__ scale, float* __restrict__ Phi,
     int64_t ldphi, int num_tiles, uint32_t tmem_cols) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem_raw[];   // 1024-B aligned: SWIZZLE_128B atoms
+  uint8_t* smem = smem_raw;                                  // (keeps the shared address space visible)
   uint8_t* sB = smem;                                   // NT x (nkb * 128) bytes, panel-major
   uint8_t* sA = sB + (size_t)NT * nkb * TC_BK;          // stages x 16 KB
   uint64_t* full = reinterpret_cast<uint64_t*>(sA + (size_t)stages * TC_STAGE);

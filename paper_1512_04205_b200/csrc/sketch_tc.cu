@@ -31,8 +31,8 @@ __global__ void __launch_bounds__(192, 1) sketch_rademacher_tc_kernel(
     const __grid_constant__ CUtensorMap mapX, int64_t pix0, int64_t n_local, int64_t m, int64_t p,
     uint32_t k0, uint32_t k1, int fbn, int nchunks_total, int chunks_per_split, int stages,
     int32_t* __restrict__ Y, int64_t ldy) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem_raw[];   // 1024-B aligned: SWIZZLE_128B atoms
+  uint8_t* smem = smem_raw;                                  // (keeps the shared address space visible)
   const int xst = fbn * SK_BK;                    // bytes of an X stage
   uint8_t* sX = smem;
   uint8_t* sC = sX + (size_t)stages * xst;
@@ -233,8 +233,8 @@ __global__ void __launch_bounds__(GS_THREADS, 1) sketch_gaussian_tc_kernel(
     const uint8_t* __restrict__ X, int64_t ld, int64_t pix0, int64_t n_local, int64_t m, int64_t p,
     uint32_t k0, uint32_t k1, const uint16_t* __restrict__ table_bf16, int npad, int nchunks_total,
     int chunks_per_split, float* __restrict__ Y, int64_t ldy) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem_raw[];   // 1024-B aligned: SWIZZLE_128B atoms
+  uint8_t* smem = smem_raw;                                  // (keeps the shared address space visible)
   const int BST = npad * GS_BK * 2;                     // bytes of a B stage
   uint8_t* sA = smem;                                   // 2 x 16 KB
   uint8_t* sB = sA + 2 * GS_A;                          // 2 x BST
