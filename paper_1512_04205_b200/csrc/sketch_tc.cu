@@ -312,13 +312,13 @@ __global__ void __launch_bounds__(GS_THREADS, 1) sketch_gaussian_tc_kernel(
         uint32_t h2[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          uint32_t hv[2];
-#pragma unroll
-          for (int b = 0; b < 2; ++b) {
-            const uint32_t u = (ws[q] >> (16 * b)) & 0xFFFFu;
-            hv[b] = (u & 0x8000u) ? htab[u & 0x7FFFu] : (uint32_t)(htab[0x7FFFu - u] ^ 0x8000u);
-          }
-          h2[q] = hv[0] | (hv[1] << 16);
+          // both 16-bit indices of the word at once: T[u] = +H[u - 32768] for u >= 32768,
+          // -H[32767 - u] = -H[u ^ 0x7FFF] otherwise (T is odd-symmetric)
+          const uint32_t wq = ws[q];
+          const uint32_t sg = ~wq & 0x80008000u;            // 0x8000 in each negative half
+          const uint32_t idx = (wq ^ (sg - (sg >> 15))) & 0x7FFF7FFFu;
+          const uint32_t h0 = htab[idx & 0xFFFFu], h1 = htab[idx >> 16];
+          h2[q] = (h0 | (h1 << 16)) ^ sg;
         }
         const int chunk = 4 * half + cq;
         *reinterpret_cast<uint4*>(dst + ((chunk ^ (rr & 7)) << 4)) = make_uint4(h2[0], h2[1], h2[2], h2[3]);
