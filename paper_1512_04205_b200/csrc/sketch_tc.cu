@@ -212,37 +212,42 @@ cudaError_t launch_sketch_rademacher_tc(const cdmd_video& v, const SensingPlan& 
 // Y = C D with c_ri = T[u16] (bf16-valued N(0,1)) as one split-K
 // kind::f16 GEMM with fp32 accumulation in TMEM (north_star: "bf16 x uint8-exact
 // operands accumulate in fp32 on tensor cores"):
-//   A = C tile, 128 rows x 64 pixels of fp16 (every table value is exact in fp16),
+//   A = C tile, 128 rows x 32 pixels of fp16 (every table value is exact in fp16),
 //       regenerated in SMEM by eight generator warps: one Philox call -> eight 16-bit
 //       table indices -> one 16-B chunk; the table's positive half (32768 fp16) is
 //       resident in SMEM (T is odd-symmetric);
-//   B = X tile, <= 512 frames x 64 pixels, converted by eight warps from uint8 to the
+//   B = X tile, <= 512 frames x 32 pixels (TMA-staged uint8, 4 stages deep), converted
+//       in SMEM by eight warps from uint8 to the
 //       exact fp16 value x - 128 (centred: 4x smaller partial sums); one spare frame row
 //       of ones yields sum_i c_ri, and the epilogue adds back 128 * sum_i c_ri;
 //   D = fp32 in TMEM (M = 128, N <= 512 over two MMAs), split-K partial sums meet in Y
 //       through fp32 atomics.
 constexpr int GS_BM = 128;            // rows of C per CTA
-constexpr int GS_BK = 64;             // pixels per stage (128-B fp16 rows)
-constexpr int GS_A = GS_BM * GS_BK * 2;   // bytes of an A stage
+constexpr int GS_BK = 32;             // pixels per stage (64-B fp16 rows, SWIZZLE_64B)
+constexpr int GS_A = GS_BM * GS_BK * 2;   // bytes of an A stage (8 KB)
+constexpr int GS_XS = 4;              // uint8 X stages (TMA)
 constexpr int GS_GEN_WARPS = 8;
 constexpr int GS_CVT_WARPS = 8;
-constexpr int GS_TASKS = 8;         // (frame, 16-px) slots per converter thread: 512 frames x 4 / 256
-constexpr int GS_THREADS = 32 * (1 + GS_GEN_WARPS + GS_CVT_WARPS);
+constexpr int GS_THREADS = 32 * (2 + GS_GEN_WARPS + GS_CVT_WARPS);
 
 __global__ void __launch_bounds__(GS_THREADS, 1) sketch_gaussian_tc_kernel(
-    const uint8_t* __restrict__ X, int64_t ld, int64_t pix0, int64_t n_local, int64_t m, int64_t p,
+    const __grid_constant__ CUtensorMap mapX, int64_t pix0, int64_t n_local, int64_t m, int64_t p,
     uint32_t k0, uint32_t k1, const uint16_t* __restrict__ table_bf16, int npad, int nchunks_total,
     int chunks_per_split, float* __restrict__ Y, int64_t ldy) {
-  extern __shared__ __align__(1024) uint8_t smem_raw[];   // 1024-B aligned: SWIZZLE_128B atoms
-  uint8_t* smem = smem_raw;                                  // (keeps the shared address space visible)
-  const int BST = npad * GS_BK * 2;                     // bytes of a B stage
-  uint8_t* sA = smem;                                   // 2 x 16 KB
+  extern __shared__ __align__(1024) uint8_t smem_raw[];   // 1024-B aligned: swizzle atoms
+  uint8_t* smem = smem_raw;
+  const int BST = npad * GS_BK * 2;                     // bytes of a B stage (fp16)
+  const int XST = npad * GS_BK;                         // bytes of an X stage (uint8)
+  uint8_t* sA = smem;                                   // 2 x 8 KB
   uint8_t* sB = sA + 2 * GS_A;                          // 2 x BST
-  uint16_t* htab = reinterpret_cast<uint16_t*>(sB + 2 * (size_t)BST);   // 32768 fp16 bits
+  uint8_t* sX = sB + 2 * (size_t)BST;                   // GS_XS x XST
+  uint16_t* htab = reinterpret_cast<uint16_t*>(sX + (size_t)GS_XS * XST);   // 32768 fp16 bits
   uint64_t* afull = reinterpret_cast<uint64_t*>(htab + 32768);
   uint64_t* bfull = afull + 2;
   uint64_t* sempty = bfull + 2;
-  uint64_t* tfull = sempty + 2;
+  uint64_t* xfull = sempty + 2;
+  uint64_t* xempty = xfull + GS_XS;
+  uint64_t* tfull = xempty + GS_XS;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -250,10 +255,9 @@ __global__ void __launch_bounds__(GS_THREADS, 1) sketch_gaussian_tc_kernel(
   const int c_begin = blockIdx.y * chunks_per_split;
   const int c_end = min(nchunks_total, c_begin + chunks_per_split);
   const int nch = c_end - c_begin;
-  // positive half of the table as fp16 bits: T[32768 + j], j < 32768
-  for (int j = threadIdx.x; j < 32768; j += blockDim.x) {
+  for (int j = threadIdx.x; j < 32768; j += blockDim.x) {   // positive half of T as fp16 bits
     const float v = __uint_as_float((uint32_t)table_bf16[32768 + j] << 16);
-    htab[j] = __half_as_ushort(__float2half_rn(v));   // exact: 8 significant bits
+    htab[j] = __half_as_ushort(__float2half_rn(v));         // exact: 8 significant bits
   }
   if (warp == 0 && lane == 0) {
     for (int b = 0; b < 2; ++b) {
@@ -261,14 +265,21 @@ __global__ void __launch_bounds__(GS_THREADS, 1) sketch_gaussian_tc_kernel(
       tc::mbar_init(&bfull[b], GS_CVT_WARPS);
       tc::mbar_init(&sempty[b], 1);
     }
+    for (int b = 0; b < GS_XS; ++b) {
+      tc::mbar_init(&xfull[b], 1);
+      tc::mbar_init(&xempty[b], GS_CVT_WARPS);
+    }
     tc::mbar_init(tfull, 1);
     tc::fence_mbar_init();
+    tc::tma_prefetch(&mapX);
   }
   if (warp == 0) tc::tmem_alloc(tmem_slot, 512);
+  tc::fence_proxy_async();
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  const int wtma = 1 + GS_GEN_WARPS + GS_CVT_WARPS;       // the TMA warp
 
   if (warp == 0) {
     if (lane == 0) {  // ------------------------------------------- MMA issuer
@@ -284,8 +295,8 @@ __global__ void __launch_bounds__(GS_THREADS, 1) sketch_gaussian_tc_kernel(
           const uint32_t idesc = tc::idesc_f16(GS_BM, nn, false, false, false, false);
 #pragma unroll
           for (int kk = 0; kk < GS_BK / 16; ++kk) {
-            const uint64_t ad = tc::smem_desc_sw128(aBase + st * GS_A + kk * 32, 0, 1024);
-            const uint64_t bd = tc::smem_desc_sw128(bBase + st * BST + nb * 128 + kk * 32, 0, 1024);
+            const uint64_t ad = tc::smem_desc(aBase + st * GS_A + kk * 32, 0, 512, 4);
+            const uint64_t bd = tc::smem_desc(bBase + st * BST + nb * 64 + kk * 32, 0, 512, 4);
             tc::mma_f16(tmem_base + (uint32_t)nb, ad, bd, idesc, (i | kk) != 0);
           }
         }
@@ -293,35 +304,50 @@ __global__ void __launch_bounds__(GS_THREADS, 1) sketch_gaussian_tc_kernel(
       }
       tc::mma_commit(tfull);
     }
+  } else if (warp == wtma) {
+    if (lane == 0) {  // ---------------------------------------- TMA producer (X uint8)
+      for (int i = 0; i < nch; ++i) {
+        const int xs = i % GS_XS;
+        const uint32_t ph = (uint32_t)(i / GS_XS) & 1u;
+        tc::mbar_wait(&xempty[xs], ph ^ 1u);
+        tc::mbar_arrive_expect_tx(&xfull[xs], (uint32_t)XST);
+        const int px = (c_begin + i) * GS_BK;
+        for (int fb = 0; fb < npad; fb += 256)
+          tc::tma_load_2d(sX + (size_t)xs * XST + (size_t)fb * GS_BK, &mapX, &xfull[xs], px, fb);
+      }
+    }
   } else if (warp <= GS_GEN_WARPS) {  // ---------------- C generators, then epilogue
     const int g = threadIdx.x - 32;            // 0..255
     const int rr = g & (GS_BM - 1);            // row of the tile
-    const int half = g >> 7;                   // pixels [32 half, 32 half + 32) of a stage
+    const int half = g >> 7;                   // pixels [16 half, 16 half + 16) of a stage
     const int64_t row = r0 + rr;
+    const int swz = (rr >> 1) & 3;             // SWIZZLE_64B chunk permutation of this row
     for (int i = 0; i < nch; ++i) {
       const int st = i & 1;
       const uint32_t ph = (uint32_t)(i >> 1) & 1u;
-      tc::mbar_wait(&sempty[st], ph ^ 1u);
-      uint8_t* dst = sA + st * GS_A + rr * 128;
-      const int64_t gpx = pix0 + (int64_t)(c_begin + i) * GS_BK + 32 * half;   // global pixel of the first value
+      uint32_t h2[2][4];
+      const int64_t gpx = pix0 + (int64_t)(c_begin + i) * GS_BK + 16 * half;
 #pragma unroll
-      for (int cq = 0; cq < 4; ++cq) {          // 8 pixels per Philox call and per 16-B chunk
+      for (int cq = 0; cq < 2; ++cq) {          // 8 pixels per Philox call and per 16-B chunk
         uint4 w = make_uint4(0, 0, 0, 0);
         if (row < p) w = philox(make_uint4((uint32_t)((gpx >> 3) + cq), (uint32_t)row, 0u, TAG_GAUSSIAN), k0, k1);
         const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
-        uint32_t h2[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          // both 16-bit indices of the word at once: T[u] = +H[u - 32768] for u >= 32768,
-          // -H[32767 - u] = -H[u ^ 0x7FFF] otherwise (T is odd-symmetric)
+          // both 16-bit indices at once: T[u] = +H[u - 32768] (u >= 32768), -H[u ^ 0x7FFF] otherwise
           const uint32_t wq = ws[q];
-          const uint32_t sg = ~wq & 0x80008000u;            // 0x8000 in each negative half
+          const uint32_t sg = ~wq & 0x80008000u;
           const uint32_t idx = (wq ^ (sg - (sg >> 15))) & 0x7FFF7FFFu;
           const uint32_t h0 = htab[idx & 0xFFFFu], h1 = htab[idx >> 16];
-          h2[q] = (h0 | (h1 << 16)) ^ sg;
+          h2[cq][q] = (h0 | (h1 << 16)) ^ sg;
         }
-        const int chunk = 4 * half + cq;
-        *reinterpret_cast<uint4*>(dst + ((chunk ^ (rr & 7)) << 4)) = make_uint4(h2[0], h2[1], h2[2], h2[3]);
+      }
+      tc::mbar_wait(&sempty[st], ph ^ 1u);
+      uint8_t* dst = sA + st * GS_A + rr * 64;
+#pragma unroll
+      for (int cq = 0; cq < 2; ++cq) {
+        const int chunk = 2 * half + cq;
+        *reinterpret_cast<uint4*>(dst + ((chunk ^ swz) << 4)) = make_uint4(h2[cq][0], h2[cq][1], h2[cq][2], h2[cq][3]);
       }
       tc::fence_proxy_async();
       __syncwarp();
@@ -348,58 +374,34 @@ __global__ void __launch_bounds__(GS_THREADS, 1) sketch_gaussian_tc_kernel(
         }
       }
     }
-  } else {  // ------------------------------------ X converters: uint8 -> fp16 (x - 128)
-    // each thread owns GS_TASKS (frame, 16-pixel quarter) slots of a stage; the bytes of
-    // the next stage are loaded into registers while the current one is converted
-    const int cthr = threadIdx.x - 32 * (1 + GS_GEN_WARPS);
+  } else {  // --------------------------- X converters: uint8 (SMEM) -> fp16 x - 128
+    const int cthr = threadIdx.x - 32 * (1 + GS_GEN_WARPS);   // 0..255
     constexpr int NT = 32 * GS_CVT_WARPS;
-    uint4 cur[GS_TASKS], nxt[GS_TASKS];
-    auto load_stage = [&](int i, uint4 (&buf)[GS_TASKS]) {
-      const int64_t jx = (int64_t)(c_begin + i) * GS_BK;
-#pragma unroll
-      for (int u = 0; u < GS_TASKS; ++u) {
-        const int task = cthr + NT * u;
-        const int f = task >> 2, qd = task & 3;
-        const int64_t j = jx + 16 * qd;
-        uint4 xv = make_uint4(0, 0, 0, 0);
-        if (f < m && task < npad * 4) {
-          if (j + 16 <= n_local) {
-            xv = __ldg(reinterpret_cast<const uint4*>(X + (int64_t)f * ld + j));
-          } else {
-            uint32_t xw[4] = {0, 0, 0, 0};
-            for (int b = 0; b < 16; ++b)
-              if (j + b < n_local) xw[b >> 2] |= (uint32_t)X[(int64_t)f * ld + j + b] << (8 * (b & 3));
-            xv = make_uint4(xw[0], xw[1], xw[2], xw[3]);
-          }
-        }
-        buf[u] = xv;
-      }
-    };
-    if (nch > 0) load_stage(0, cur);
+    const __half2 c1152 = __halves2half2(__ushort_as_half(0x6480), __ushort_as_half(0x6480));
     for (int i = 0; i < nch; ++i) {
       const int st = i & 1;
       const uint32_t ph = (uint32_t)(i >> 1) & 1u;
-      if (i + 1 < nch) load_stage(i + 1, nxt);
+      const int xs = i % GS_XS;
+      tc::mbar_wait(&xfull[xs], (uint32_t)(i / GS_XS) & 1u);
       tc::mbar_wait(&sempty[st], ph ^ 1u);
+      const uint8_t* xt = sX + (size_t)xs * XST;
       uint8_t* bst = sB + (size_t)st * BST;
-      const int64_t jx = (int64_t)(c_begin + i) * GS_BK;
-#pragma unroll
-      for (int u = 0; u < GS_TASKS; ++u) {
-        const int task = cthr + NT * u;
-        if (task >= npad * 4) break;
-        const int f = task >> 2, qd = task & 3;
-        const int64_t j = jx + 16 * qd;
+      const int64_t jx = (int64_t)(c_begin + i) * GS_BK;       // first local pixel of the stage
+      const bool tail = jx + GS_BK > n_local;
+      for (int task = cthr; task < npad * 2; task += NT) {
+        const int f = task >> 1, hf = task & 1;                // frame row, 16-pixel half
+        const int64_t j = jx + 16 * hf;
         uint32_t hw[8];
         if (f < m) {
-          const uint32_t xw[4] = {cur[u].x, cur[u].y, cur[u].z, cur[u].w};
+          const uint4 xv = *reinterpret_cast<const uint4*>(xt + f * GS_BK + 16 * hf);
+          const uint32_t xw[4] = {xv.x, xv.y, xv.z, xv.w};
 #pragma unroll
           for (int b = 0; b < 8; ++b) {   // two pixels -> half2 (1024 + x) - 1152 = x - 128, exact
             const uint32_t pr = __byte_perm(xw[b >> 1], 0x64646464u, (b & 1) ? 0x7372u : 0x5150u);
-            __half2 h = __hsub2(*reinterpret_cast<const __half2*>(&pr),
-                                __halves2half2(__ushort_as_half(0x6480), __ushort_as_half(0x6480)));
-            hw[b] = *reinterpret_cast<uint32_t*>(&h);
+            __half2 hh = __hsub2(*reinterpret_cast<const __half2*>(&pr), c1152);
+            hw[b] = *reinterpret_cast<uint32_t*>(&hh);
           }
-          if (j + 16 > n_local)   // pixels beyond the slab contribute nothing
+          if (tail)   // pixels beyond the slab contribute nothing
             for (int b = 0; b < 16; ++b)
               if (j + b >= n_local) hw[b >> 1] &= (b & 1) ? 0x0000FFFFu : 0xFFFF0000u;
         } else if (f == m) {      // the row of ones: D[:, m] = sum_i c_ri
@@ -412,15 +414,17 @@ __global__ void __launch_bounds__(GS_THREADS, 1) sketch_gaussian_tc_kernel(
 #pragma unroll
           for (int b = 0; b < 8; ++b) hw[b] = 0u;
         }
-        uint8_t* rowp = bst + (size_t)f * 128;
-        *reinterpret_cast<uint4*>(rowp + (((2 * qd) ^ (f & 7)) << 4)) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
-        *reinterpret_cast<uint4*>(rowp + (((2 * qd + 1) ^ (f & 7)) << 4)) = make_uint4(hw[4], hw[5], hw[6], hw[7]);
+        uint8_t* rowp = bst + (size_t)f * 64;
+        const int swz = (f >> 1) & 3;
+        *reinterpret_cast<uint4*>(rowp + (((2 * hf) ^ swz) << 4)) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+        *reinterpret_cast<uint4*>(rowp + (((2 * hf + 1) ^ swz) << 4)) = make_uint4(hw[4], hw[5], hw[6], hw[7]);
       }
       tc::fence_proxy_async();
       __syncwarp();
-      if (lane == 0) tc::mbar_arrive(&bfull[st]);
-#pragma unroll
-      for (int u = 0; u < GS_TASKS; ++u) cur[u] = nxt[u];
+      if (lane == 0) {
+        tc::mbar_arrive(&xempty[xs]);
+        tc::mbar_arrive(&bfull[st]);
+      }
     }
   }
   __syncthreads();
@@ -430,7 +434,7 @@ __global__ void __launch_bounds__(GS_THREADS, 1) sketch_gaussian_tc_kernel(
   }
 }
 
-bool sketch_gaussian_tc_supported(const cdmd_video& v) { return v.m + 1 <= 512 && (v.ld % 16) == 0; }
+bool sketch_gaussian_tc_supported(const cdmd_video& v) { return v.m + 1 <= 512 && (v.ld % 16) == 0 && sk_encode_fn() != nullptr; }
 
 cudaError_t launch_sketch_gaussian_tc(const cdmd_video& v, const SensingPlan& P, const uint16_t* table, float* Y,
                                       int64_t ldy, cudaStream_t st) {
@@ -440,19 +444,28 @@ cudaError_t launch_sketch_gaussian_tc(const cdmd_video& v, const SensingPlan& P,
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  int splits = sms / nrb;   // one CTA per SM (225 KB SMEM): a single wave
+  int splits = sms / nrb;   // one CTA per SM: a single wave
   if (splits > nchunks) splits = nchunks;
   if (splits < 1) splits = 1;
   const int cps = (int)ceil_div(nchunks, splits);
   splits = (int)ceil_div(nchunks, cps);
-  const size_t smem = 1024 + 2 * (size_t)GS_A + 2 * (size_t)npad * GS_BK * 2 + 65536 + 256;
+  CUtensorMap mapX;
+  cuuint64_t dims[2] = {(cuuint64_t)v.n_local, (cuuint64_t)v.m};
+  cuuint64_t strides[1] = {(cuuint64_t)v.ld};
+  cuuint32_t box[2] = {GS_BK, 256};
+  cuuint32_t estr[2] = {1, 1};
+  if (sk_encode_fn()(&mapX, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(v.X), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return cudaErrorInvalidValue;
+  const size_t smem = 1024 + 2 * (size_t)GS_A + 2 * (size_t)npad * GS_BK * 2 + (size_t)GS_XS * npad * GS_BK + 65536 + 256;
   cudaError_t e = cudaFuncSetAttribute(sketch_gaussian_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   e = cudaMemsetAsync(Y, 0, sizeof(float) * (size_t)ldy * v.m, st);
   if (e != cudaSuccess) return e;
   dim3 grid((unsigned)nrb, (unsigned)splits);
-  sketch_gaussian_tc_kernel<<<grid, GS_THREADS, smem, st>>>(v.X, v.ld, v.pix0, v.n_local, v.m, P.p, P.k0, P.k1, table,
-                                                            npad, nchunks, cps, Y, ldy);
+  sketch_gaussian_tc_kernel<<<grid, GS_THREADS, smem, st>>>(mapX, v.pix0, v.n_local, v.m, P.p, P.k0, P.k1, table, npad,
+                                                            nchunks, cps, Y, ldy);
   return cudaGetLastError();
 }
 
