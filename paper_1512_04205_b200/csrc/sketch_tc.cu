@@ -233,7 +233,7 @@ constexpr int GS_THREADS = 32 * (2 + GS_GEN_WARPS + GS_CVT_WARPS);
 __global__ void __launch_bounds__(GS_THREADS, 1) sketch_gaussian_tc_kernel(
     const __grid_constant__ CUtensorMap mapX, int64_t pix0, int64_t n_local, int64_t m, int64_t p,
     uint32_t k0, uint32_t k1, const uint16_t* __restrict__ table_bf16, int npad, int nchunks_total,
-    int chunks_per_split, float* __restrict__ Y, int64_t ldy) {
+    int chunks_per_split, int xbox, float* __restrict__ Y, int64_t ldy) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];   // 1024-B aligned: swizzle atoms
   uint8_t* smem = smem_raw;
   const int BST = npad * GS_BK * 2;                     // bytes of a B stage (fp16)
@@ -312,7 +312,7 @@ __global__ void __launch_bounds__(GS_THREADS, 1) sketch_gaussian_tc_kernel(
         tc::mbar_wait(&xempty[xs], ph ^ 1u);
         tc::mbar_arrive_expect_tx(&xfull[xs], (uint32_t)XST);
         const int px = (c_begin + i) * GS_BK;
-        for (int fb = 0; fb < npad; fb += 256)
+        for (int fb = 0; fb < npad; fb += xbox)   // boxes of xbox frame rows tile npad exactly
           tc::tma_load_2d(sX + (size_t)xs * XST + (size_t)fb * GS_BK, &mapX, &xfull[xs], px, fb);
       }
     }
@@ -452,7 +452,14 @@ cudaError_t launch_sketch_gaussian_tc(const cdmd_video& v, const SensingPlan& P,
   CUtensorMap mapX;
   cuuint64_t dims[2] = {(cuuint64_t)v.n_local, (cuuint64_t)v.m};
   cuuint64_t strides[1] = {(cuuint64_t)v.ld};
-  cuuint32_t box[2] = {GS_BK, 256};
+  // frame rows per TMA box: a multiple of 16 that divides npad, at most 256
+  int xbox = npad;
+  if (xbox > 256) {
+    int q = npad / 16, kk = 16;
+    while (q % kk) --kk;
+    xbox = 16 * kk;
+  }
+  cuuint32_t box[2] = {GS_BK, (cuuint32_t)xbox};
   cuuint32_t estr[2] = {1, 1};
   if (sk_encode_fn()(&mapX, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(v.X), dims, strides, box, estr,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -465,7 +472,7 @@ cudaError_t launch_sketch_gaussian_tc(const cdmd_video& v, const SensingPlan& P,
   if (e != cudaSuccess) return e;
   dim3 grid((unsigned)nrb, (unsigned)splits);
   sketch_gaussian_tc_kernel<<<grid, GS_THREADS, smem, st>>>(mapX, v.pix0, v.n_local, v.m, P.p, P.k0, P.k1, table, npad,
-                                                            nchunks, cps, Y, ldy);
+                                                            nchunks, cps, xbox, Y, ldy);
   return cudaGetLastError();
 }
 
