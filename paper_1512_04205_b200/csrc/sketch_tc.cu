@@ -375,25 +375,26 @@ __global__ void __launch_bounds__(GS_THREADS, 1) sketch_gaussian_tc_kernel(
       }
     }
   } else {  // --------------------------- X converters: uint8 (SMEM) -> fp16 x - 128
+    // thread = (16-pixel half hf, frames f0 + 128 u): fixed half and swizzle pattern,
+    // 32-bit indexing; the slab's last (ragged) chunk and the rows >= m take a slow path
     const int cthr = threadIdx.x - 32 * (1 + GS_GEN_WARPS);   // 0..255
-    constexpr int NT = 32 * GS_CVT_WARPS;
+    const int hf = cthr & 1, fr0 = cthr >> 1;                   // half, first frame (0..127)
     const __half2 c1152 = __halves2half2(__ushort_as_half(0x6480), __ushort_as_half(0x6480));
+    const int nfull = (int)m;                                   // rows that hold pixels
     for (int i = 0; i < nch; ++i) {
       const int st = i & 1;
       const uint32_t ph = (uint32_t)(i >> 1) & 1u;
       const int xs = i % GS_XS;
       tc::mbar_wait(&xfull[xs], (uint32_t)(i / GS_XS) & 1u);
       tc::mbar_wait(&sempty[st], ph ^ 1u);
-      const uint8_t* xt = sX + (size_t)xs * XST;
+      const uint8_t* xt = sX + (size_t)xs * XST + 16 * hf;
       uint8_t* bst = sB + (size_t)st * BST;
-      const int64_t jx = (int64_t)(c_begin + i) * GS_BK;       // first local pixel of the stage
-      const bool tail = jx + GS_BK > n_local;
-      for (int task = cthr; task < npad * 2; task += NT) {
-        const int f = task >> 1, hf = task & 1;                // frame row, 16-pixel half
-        const int64_t j = jx + 16 * hf;
+      const int64_t jx = (int64_t)(c_begin + i) * GS_BK + 16 * hf;   // first local pixel of the half
+      const bool tail = jx + 16 > n_local;
+      for (int f = fr0; f < npad; f += 128) {
         uint32_t hw[8];
-        if (f < m) {
-          const uint4 xv = *reinterpret_cast<const uint4*>(xt + f * GS_BK + 16 * hf);
+        if (f < nfull) {
+          const uint4 xv = *reinterpret_cast<const uint4*>(xt + f * GS_BK);
           const uint32_t xw[4] = {xv.x, xv.y, xv.z, xv.w};
 #pragma unroll
           for (int b = 0; b < 8; ++b) {   // two pixels -> half2 (1024 + x) - 1152 = x - 128, exact
@@ -401,20 +402,21 @@ __global__ void __launch_bounds__(GS_THREADS, 1) sketch_gaussian_tc_kernel(
             __half2 hh = __hsub2(*reinterpret_cast<const __half2*>(&pr), c1152);
             hw[b] = *reinterpret_cast<uint32_t*>(&hh);
           }
-          if (tail)   // pixels beyond the slab contribute nothing
+          if (tail) {   // pixels beyond the slab contribute nothing
             for (int b = 0; b < 16; ++b)
-              if (j + b >= n_local) hw[b >> 1] &= (b & 1) ? 0x0000FFFFu : 0xFFFF0000u;
-        } else if (f == m) {      // the row of ones: D[:, m] = sum_i c_ri
+              if (jx + b >= n_local) hw[b >> 1] &= (b & 1) ? 0x0000FFFFu : 0xFFFF0000u;
+          }
+        } else if (f == nfull) {   // the row of ones: D[:, m] = sum_i c_ri
 #pragma unroll
           for (int b = 0; b < 8; ++b) {
-            const uint32_t lo = (j + 2 * b < n_local) ? 0x3C00u : 0u, hi = (j + 2 * b + 1 < n_local) ? 0x3C00u : 0u;
+            const uint32_t lo = (jx + 2 * b < n_local) ? 0x3C00u : 0u, hi = (jx + 2 * b + 1 < n_local) ? 0x3C00u : 0u;
             hw[b] = lo | (hi << 16);
           }
         } else {
 #pragma unroll
           for (int b = 0; b < 8; ++b) hw[b] = 0u;
         }
-        uint8_t* rowp = bst + (size_t)f * 64;
+        uint8_t* rowp = bst + f * 64;
         const int swz = (f >> 1) & 3;
         *reinterpret_cast<uint4*>(rowp + (((2 * hf) ^ swz) << 4)) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
         *reinterpret_cast<uint4*>(rowp + (((2 * hf + 1) ^ swz) << 4)) = make_uint4(hw[4], hw[5], hw[6], hw[7]);
