@@ -45,7 +45,8 @@ def build(force=False, verbose=True):
            "-I", os.path.join(ROOT, "include"), "-o", LIB + ".tmp",
            *[os.path.join(CSRC, s) for s in SOURCES],
            "-L", os.path.join(cuda, "lib64"), "-lcusolver", "-lcublas",
-           "-Xlinker", "-rpath=" + os.path.join(cuda, "lib64")]
+           "-Xlinker", "-rpath=" + os.path.join(cuda, "lib64"),
+           *os.environ.get("CDMD_EXTRA_NVCC", "").split()]   # e.g. -DCDMD_GS_PROF (instrumented builds)
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True)

@@ -15,6 +15,7 @@
 // Pixel ranges are split across CTAs and the partial sums meet in Y through int32
 // atomics (exact and order-independent).  Warp roles: 0 TMA producer, 1 TMEM owner +
 // MMA issuer, 2..5 C generators and then the epilogue.
+#include <cstdio>
 #include <cuda_fp16.h>
 #include <cudaTypedefs.h>
 
@@ -222,11 +223,24 @@ cudaError_t launch_sketch_rademacher_tc(const cdmd_video& v, const SensingPlan& 
 //       of ones yields sum_i c_ri, and the epilogue adds back 128 * sum_i c_ri;
 //   D = fp32 in TMEM (M = 128, N <= 512 over two MMAs), split-K partial sums meet in Y
 //       through fp32 atomics.
+#ifdef CDMD_GS_PROF
+__device__ long long gs_prof[8 * 16];
+#define GS_T(ii, slot)                                                                               \
+  if (blockIdx.x == 0 && blockIdx.y == 0 && (threadIdx.x & 31) == 0 && (ii) >= 100 && (ii) < 108 && \
+      (warp <= 1 || warp == 1 + GS_GEN_WARPS || warp == GS_GEN_WARPS + GS_CVT_WARPS || warp == 1 + GS_GEN_WARPS + GS_CVT_WARPS)) \
+    gs_prof[((ii) - 100) * 16 + (slot)] = clock64();
+#else
+#define GS_T(ii, slot)
+#endif
 constexpr int GS_BM = 128;            // rows of C per CTA
 constexpr int GS_BK = 32;             // pixels per stage (64-B fp16 rows, SWIZZLE_64B)
 constexpr int GS_A = GS_BM * GS_BK * 2;   // bytes of an A stage (8 KB)
-constexpr int GS_XS = 4;              // uint8 X stages (TMA)
-constexpr int GS_GEN_WARPS = 8;
+constexpr int GS_XK = 64;             // pixels per uint8 X stage (64-B TMA rows)
+constexpr int GS_XS = 2;              // uint8 X stages (TMA)
+#ifndef GS_GEN_WARPS_DEF
+#define GS_GEN_WARPS_DEF 8
+#endif
+constexpr int GS_GEN_WARPS = GS_GEN_WARPS_DEF;   // 4, 8 or 16: thread = (row, 8-pixel chunks) of the A stage
 constexpr int GS_CVT_WARPS = 8;
 constexpr int GS_THREADS = 32 * (2 + GS_GEN_WARPS + GS_CVT_WARPS);
 
@@ -237,7 +251,7 @@ __global__ void __launch_bounds__(GS_THREADS, 1) sketch_gaussian_tc_kernel(
   extern __shared__ __align__(1024) uint8_t smem_raw[];   // 1024-B aligned: swizzle atoms
   uint8_t* smem = smem_raw;
   const int BST = npad * GS_BK * 2;                     // bytes of a B stage (fp16)
-  const int XST = npad * GS_BK;                         // bytes of an X stage (uint8)
+  const int XST = npad * GS_XK;                         // bytes of an X stage (uint8)
   uint8_t* sA = smem;                                   // 2 x 8 KB
   uint8_t* sB = sA + 2 * GS_A;                          // 2 x BST
   uint8_t* sX = sB + 2 * (size_t)BST;                   // GS_XS x XST
@@ -288,7 +302,9 @@ __global__ void __launch_bounds__(GS_THREADS, 1) sketch_gaussian_tc_kernel(
         const int st = i & 1;
         const uint32_t ph = (uint32_t)(i >> 1) & 1u;
         tc::mbar_wait(&afull[st], ph);
+        GS_T(i, 0)
         tc::mbar_wait(&bfull[st], ph);
+        GS_T(i, 1)
         tc::fence_after();
         for (int nb = 0; nb < npad; nb += 256) {
           const int nn = npad - nb < 256 ? npad - nb : 256;
@@ -301,36 +317,42 @@ __global__ void __launch_bounds__(GS_THREADS, 1) sketch_gaussian_tc_kernel(
           }
         }
         tc::mma_commit(&sempty[st]);
+        GS_T(i, 2)
       }
       tc::mma_commit(tfull);
     }
   } else if (warp == wtma) {
     if (lane == 0) {  // ---------------------------------------- TMA producer (X uint8)
-      for (int i = 0; i < nch; ++i) {
+      const int nx = (nch + 1) >> 1;   // X stages of GS_XK = 2 GS_BK pixels (64-B rows)
+      for (int i = 0; i < nx; ++i) {
         const int xs = i % GS_XS;
         const uint32_t ph = (uint32_t)(i / GS_XS) & 1u;
         tc::mbar_wait(&xempty[xs], ph ^ 1u);
         tc::mbar_arrive_expect_tx(&xfull[xs], (uint32_t)XST);
-        const int px = (c_begin + i) * GS_BK;
+        GS_T(2 * i, 15)
+        const int px = (c_begin + 2 * i) * GS_BK;
         for (int fb = 0; fb < npad; fb += xbox)   // boxes of xbox frame rows tile npad exactly
-          tc::tma_load_2d(sX + (size_t)xs * XST + (size_t)fb * GS_BK, &mapX, &xfull[xs], px, fb);
+          tc::tma_load_2d(sX + (size_t)xs * XST + (size_t)fb * GS_XK, &mapX, &xfull[xs], px, fb);
       }
     }
   } else if (warp <= GS_GEN_WARPS) {  // ---------------- C generators, then epilogue
-    const int g = threadIdx.x - 32;            // 0..255
+    constexpr int GS_NQ = 16 / GS_GEN_WARPS;    // 16-B chunks (8 pixels, one Philox call) per thread and stage
+    const int g = threadIdx.x - 32;            // 0..32 GS_GEN_WARPS - 1
     const int rr = g & (GS_BM - 1);            // row of the tile
-    const int half = g >> 7;                   // pixels [16 half, 16 half + 16) of a stage
+    const int q0 = g >> 7;                     // chunks q0 + (GS_GEN_WARPS / 4) c of the stage's four
     const int64_t row = r0 + rr;
     const int swz = (rr >> 1) & 3;             // SWIZZLE_64B chunk permutation of this row
+    const uint32_t ctr0 = (uint32_t)(pix0 >> 3) + (uint32_t)(c_begin * (GS_BK / 8) + q0);
     for (int i = 0; i < nch; ++i) {
       const int st = i & 1;
       const uint32_t ph = (uint32_t)(i >> 1) & 1u;
-      uint32_t h2[2][4];
-      const int64_t gpx = pix0 + (int64_t)(c_begin + i) * GS_BK + 16 * half;
+      uint32_t h2[GS_NQ][4];
 #pragma unroll
-      for (int cq = 0; cq < 2; ++cq) {          // 8 pixels per Philox call and per 16-B chunk
-        uint4 w = make_uint4(0, 0, 0, 0);
-        if (row < p) w = philox(make_uint4((uint32_t)((gpx >> 3) + cq), (uint32_t)row, 0u, TAG_GAUSSIAN), k0, k1);
+      for (int c = 0; c < GS_NQ; ++c) {
+        uint4 w = make_uint4(0, 0, 0, 0);   // one Philox call = eight 16-bit table indices
+        if (row < p)
+          w = philox(make_uint4(ctr0 + (uint32_t)(i * (GS_BK / 8) + c * (GS_GEN_WARPS / 4)), (uint32_t)row, 0u, TAG_GAUSSIAN),
+                     k0, k1);
         const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
@@ -339,19 +361,21 @@ __global__ void __launch_bounds__(GS_THREADS, 1) sketch_gaussian_tc_kernel(
           const uint32_t sg = ~wq & 0x80008000u;
           const uint32_t idx = (wq ^ (sg - (sg >> 15))) & 0x7FFF7FFFu;
           const uint32_t h0 = htab[idx & 0xFFFFu], h1 = htab[idx >> 16];
-          h2[cq][q] = (h0 | (h1 << 16)) ^ sg;
+          h2[c][q] = (h0 | (h1 << 16)) ^ sg;
         }
       }
+      GS_T(i, 3)
       tc::mbar_wait(&sempty[st], ph ^ 1u);
-      uint8_t* dst = sA + st * GS_A + rr * 64;
+      GS_T(i, 4)
 #pragma unroll
-      for (int cq = 0; cq < 2; ++cq) {
-        const int chunk = 2 * half + cq;
-        *reinterpret_cast<uint4*>(dst + ((chunk ^ swz) << 4)) = make_uint4(h2[cq][0], h2[cq][1], h2[cq][2], h2[cq][3]);
+      for (int c = 0; c < GS_NQ; ++c) {
+        const int q8 = q0 + c * (GS_GEN_WARPS / 4);
+        *reinterpret_cast<uint4*>(sA + st * GS_A + rr * 64 + ((q8 ^ swz) << 4)) = make_uint4(h2[c][0], h2[c][1], h2[c][2], h2[c][3]);
       }
       tc::fence_proxy_async();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&afull[st]);
+      GS_T(i, 5)
     }
     if (warp <= 4) {  // epilogue: TMEM lane = row of C, column t = frame, column m = sum_i c_ri
       tc::mbar_wait(tfull, 0);
@@ -375,61 +399,98 @@ __global__ void __launch_bounds__(GS_THREADS, 1) sketch_gaussian_tc_kernel(
       }
     }
   } else {  // --------------------------- X converters: uint8 (SMEM) -> fp16 x - 128
-    // thread = (16-pixel half hf, frames f0 + 128 u): fixed half and swizzle pattern,
-    // 32-bit indexing; the slab's last (ragged) chunk and the rows >= m take a slow path
+    // thread = (16-pixel half hf, frames fr0 + 128 u): all four frame rows are read and
+    // converted into registers before the B slot is awaited, so the conversion overlaps
+    // the MMA that still reads the slot; the ragged last chunk of the slab and the row
+    // of ones take a per-element path
     const int cthr = threadIdx.x - 32 * (1 + GS_GEN_WARPS);   // 0..255
     const int hf = cthr & 1, fr0 = cthr >> 1;                   // half, first frame (0..127)
     const __half2 c1152 = __halves2half2(__ushort_as_half(0x6480), __ushort_as_half(0x6480));
-    const int nfull = (int)m;                                   // rows that hold pixels
+    const int mi = (int)m;
     for (int i = 0; i < nch; ++i) {
       const int st = i & 1;
       const uint32_t ph = (uint32_t)(i >> 1) & 1u;
-      const int xs = i % GS_XS;
-      tc::mbar_wait(&xfull[xs], (uint32_t)(i / GS_XS) & 1u);
-      tc::mbar_wait(&sempty[st], ph ^ 1u);
-      const uint8_t* xt = sX + (size_t)xs * XST + 16 * hf;
-      uint8_t* bst = sB + (size_t)st * BST;
+      const int xi = i >> 1, xs = xi % GS_XS;                   // one X stage = two B stages
+      if ((i & 1) == 0) tc::mbar_wait(&xfull[xs], (uint32_t)(xi / GS_XS) & 1u);
+      const uint8_t* xt = sX + (size_t)xs * XST + GS_BK * (i & 1) + 16 * hf;
       const int64_t jx = (int64_t)(c_begin + i) * GS_BK + 16 * hf;   // first local pixel of the half
-      const bool tail = jx + 16 > n_local;
-      for (int f = fr0; f < npad; f += 128) {
-        uint32_t hw[8];
-        if (f < nfull) {
-          const uint4 xv = *reinterpret_cast<const uint4*>(xt + f * GS_BK);
-          const uint32_t xw[4] = {xv.x, xv.y, xv.z, xv.w};
+      const int64_t rem = n_local - jx;
+      const int valid = rem >= 16 ? 16 : (rem > 0 ? (int)rem : 0);
+      uint32_t hw[4][8];
+      if (valid == 16) {   // branch-free: four predicated 16-B loads in flight, then convert
+        uint4 xv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int f = fr0 + 128 * u;
+          xv[u] = f < mi ? *reinterpret_cast<const uint4*>(xt + f * GS_XK) : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int f = fr0 + 128 * u;
+          const uint32_t xw[4] = {xv[u].x, xv[u].y, xv[u].z, xv[u].w};
+          const uint32_t fill = f == mi ? 0x3C003C00u : 0u;   // the row of ones: D[:, m] = sum_i c_ri
 #pragma unroll
           for (int b = 0; b < 8; ++b) {   // two pixels -> half2 (1024 + x) - 1152 = x - 128, exact
             const uint32_t pr = __byte_perm(xw[b >> 1], 0x64646464u, (b & 1) ? 0x7372u : 0x5150u);
             __half2 hh = __hsub2(*reinterpret_cast<const __half2*>(&pr), c1152);
-            hw[b] = *reinterpret_cast<uint32_t*>(&hh);
+            hw[u][b] = f < mi ? *reinterpret_cast<uint32_t*>(&hh) : fill;
           }
-          if (tail) {   // pixels beyond the slab contribute nothing
-            for (int b = 0; b < 16; ++b)
-              if (jx + b >= n_local) hw[b >> 1] &= (b & 1) ? 0x0000FFFFu : 0xFFFF0000u;
-          }
-        } else if (f == nfull) {   // the row of ones: D[:, m] = sum_i c_ri
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int f = fr0 + 128 * u;
 #pragma unroll
           for (int b = 0; b < 8; ++b) {
-            const uint32_t lo = (jx + 2 * b < n_local) ? 0x3C00u : 0u, hi = (jx + 2 * b + 1 < n_local) ? 0x3C00u : 0u;
-            hw[b] = lo | (hi << 16);
-          }
-        } else {
+            uint32_t w = 0u;
 #pragma unroll
-          for (int b = 0; b < 8; ++b) hw[b] = 0u;
+            for (int e = 0; e < 2; ++e) {
+              const int q = 2 * b + e;
+              uint32_t h = 0u;
+              if (q < valid) {
+                if (f < mi) h = __half_as_ushort(__int2half_rn((int)xt[f * GS_XK + q] - 128));
+                else if (f == mi) h = 0x3C00u;   // the row of ones: D[:, m] = sum_i c_ri
+              }
+              w |= h << (16 * e);
+            }
+            hw[u][b] = w;
+          }
         }
-        uint8_t* rowp = bst + f * 64;
-        const int swz = (f >> 1) & 3;
-        *reinterpret_cast<uint4*>(rowp + (((2 * hf) ^ swz) << 4)) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
-        *reinterpret_cast<uint4*>(rowp + (((2 * hf + 1) ^ swz) << 4)) = make_uint4(hw[4], hw[5], hw[6], hw[7]);
+      }
+      GS_T(i, 9 + (warp == 1 + GS_GEN_WARPS ? 0 : 3))
+      tc::mbar_wait(&sempty[st], ph ^ 1u);
+      GS_T(i, 10 + (warp == 1 + GS_GEN_WARPS ? 0 : 3))
+      uint8_t* bst = sB + (size_t)st * BST;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int f = fr0 + 128 * u;
+        if (f < npad) {
+          uint8_t* rowp = bst + f * 64;
+          const int swz = (f >> 1) & 3;
+          *reinterpret_cast<uint4*>(rowp + (((2 * hf) ^ swz) << 4)) = make_uint4(hw[u][0], hw[u][1], hw[u][2], hw[u][3]);
+          *reinterpret_cast<uint4*>(rowp + (((2 * hf + 1) ^ swz) << 4)) = make_uint4(hw[u][4], hw[u][5], hw[u][6], hw[u][7]);
+        }
       }
       tc::fence_proxy_async();
       __syncwarp();
       if (lane == 0) {
-        tc::mbar_arrive(&xempty[xs]);
+        if ((i & 1) || i == nch - 1) tc::mbar_arrive(&xempty[xs]);
         tc::mbar_arrive(&bfull[st]);
+      GS_T(i, 11 + (warp == 1 + GS_GEN_WARPS ? 0 : 3))
       }
     }
   }
   __syncthreads();
+#ifdef CDMD_GS_PROF
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
+    const long long t0 = gs_prof[0];
+    for (int r = 0; r < 8; ++r) {
+      printf("GSPROF stage %d:", 100 + r);
+      for (int c = 0; c < 16; ++c) printf(" %lld", gs_prof[r * 16 + c] - t0);
+      printf("\n");
+    }
+  }
+#endif
   if (warp == 0) {
     tc::fence_after();
     tc::tmem_dealloc(tmem_base, 512);
@@ -461,13 +522,13 @@ cudaError_t launch_sketch_gaussian_tc(const cdmd_video& v, const SensingPlan& P,
     while (q % kk) --kk;
     xbox = 16 * kk;
   }
-  cuuint32_t box[2] = {GS_BK, (cuuint32_t)xbox};
+  cuuint32_t box[2] = {GS_XK, (cuuint32_t)xbox};
   cuuint32_t estr[2] = {1, 1};
   if (sk_encode_fn()(&mapX, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(v.X), dims, strides, box, estr,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return cudaErrorInvalidValue;
-  const size_t smem = 1024 + 2 * (size_t)GS_A + 2 * (size_t)npad * GS_BK * 2 + (size_t)GS_XS * npad * GS_BK + 65536 + 256;
+  const size_t smem = 1024 + 2 * (size_t)GS_A + 2 * (size_t)npad * GS_BK * 2 + (size_t)GS_XS * npad * GS_XK + 65536 + 256;
   cudaError_t e = cudaFuncSetAttribute(sketch_gaussian_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   e = cudaMemsetAsync(Y, 0, sizeof(float) * (size_t)ldy * v.m, st);
