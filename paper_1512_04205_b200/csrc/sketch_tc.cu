@@ -262,7 +262,9 @@ __global__ void __launch_bounds__(GS_THREADS, 1) sketch_gaussian_tc_kernel(
   uint64_t* xfull = sempty + 2;
   uint64_t* xempty = xfull + GS_XS;
   uint64_t* tfull = xempty + GS_XS;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+  uint64_t* bhi = tfull + 1;      // B frames [256, npad) of a stage converted
+  uint64_t* slo = bhi + 2;        // the stage's MMAs on frames [0, 256) done
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(slo + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t r0 = (int64_t)blockIdx.x * GS_BM;
@@ -276,8 +278,10 @@ __global__ void __launch_bounds__(GS_THREADS, 1) sketch_gaussian_tc_kernel(
   if (warp == 0 && lane == 0) {
     for (int b = 0; b < 2; ++b) {
       tc::mbar_init(&afull[b], GS_GEN_WARPS);
-      tc::mbar_init(&bfull[b], GS_CVT_WARPS);
+      tc::mbar_init(&bfull[b], GS_CVT_WARPS / 2);
+      tc::mbar_init(&bhi[b], GS_CVT_WARPS / 2);
       tc::mbar_init(&sempty[b], 1);
+      tc::mbar_init(&slo[b], 1);
     }
     for (int b = 0; b < GS_XS; ++b) {
       tc::mbar_init(&xfull[b], 1);
@@ -306,7 +310,13 @@ __global__ void __launch_bounds__(GS_THREADS, 1) sketch_gaussian_tc_kernel(
         tc::mbar_wait(&bfull[st], ph);
         GS_T(i, 1)
         tc::fence_after();
+        // frames [0, 256) as soon as their converter half is done, then [256, npad)
         for (int nb = 0; nb < npad; nb += 256) {
+          if (nb) {
+            tc::mma_commit(&slo[st]);
+            tc::mbar_wait(&bhi[st], ph);
+            tc::fence_after();
+          }
           const int nn = npad - nb < 256 ? npad - nb : 256;
           const uint32_t idesc = tc::idesc_f16(GS_BM, nn, false, false, false, false);
 #pragma unroll
@@ -316,6 +326,7 @@ __global__ void __launch_bounds__(GS_THREADS, 1) sketch_gaussian_tc_kernel(
             tc::mma_f16(tmem_base + (uint32_t)nb, ad, bd, idesc, (i | kk) != 0);
           }
         }
+        if (npad <= 256) tc::mma_commit(&slo[st]);
         tc::mma_commit(&sempty[st]);
         GS_T(i, 2)
       }
@@ -399,12 +410,13 @@ __global__ void __launch_bounds__(GS_THREADS, 1) sketch_gaussian_tc_kernel(
       }
     }
   } else {  // --------------------------- X converters: uint8 (SMEM) -> fp16 x - 128
-    // thread = (16-pixel half hf, frames fr0 + 128 u): all four frame rows are read and
+    // thread = (16-pixel half hf, frames fr0 + 64 u of its 256-frame group): all four frame rows are read and
     // converted into registers before the B slot is awaited, so the conversion overlaps
     // the MMA that still reads the slot; the ragged last chunk of the slab and the row
     // of ones take a per-element path
     const int cthr = threadIdx.x - 32 * (1 + GS_GEN_WARPS);   // 0..255
-    const int hf = cthr & 1, fr0 = cthr >> 1;                   // half, first frame (0..127)
+    const int grp = cthr >> 7;                                  // frames [256 grp, 256 grp + 256)
+    const int hf = cthr & 1, fr0 = 256 * grp + ((cthr & 127) >> 1);   // half, first frame
     const __half2 c1152 = __halves2half2(__ushort_as_half(0x6480), __ushort_as_half(0x6480));
     const int mi = (int)m;
     for (int i = 0; i < nch; ++i) {
@@ -421,12 +433,12 @@ __global__ void __launch_bounds__(GS_THREADS, 1) sketch_gaussian_tc_kernel(
         uint4 xv[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const int f = fr0 + 128 * u;
+          const int f = fr0 + 64 * u;
           xv[u] = f < mi ? *reinterpret_cast<const uint4*>(xt + f * GS_XK) : make_uint4(0, 0, 0, 0);
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const int f = fr0 + 128 * u;
+          const int f = fr0 + 64 * u;
           const uint32_t xw[4] = {xv[u].x, xv[u].y, xv[u].z, xv[u].w};
           const uint32_t fill = f == mi ? 0x3C003C00u : 0u;   // the row of ones: D[:, m] = sum_i c_ri
 #pragma unroll
@@ -439,7 +451,7 @@ __global__ void __launch_bounds__(GS_THREADS, 1) sketch_gaussian_tc_kernel(
       } else {
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const int f = fr0 + 128 * u;
+          const int f = fr0 + 64 * u;
 #pragma unroll
           for (int b = 0; b < 8; ++b) {
             uint32_t w = 0u;
@@ -458,12 +470,12 @@ __global__ void __launch_bounds__(GS_THREADS, 1) sketch_gaussian_tc_kernel(
         }
       }
       GS_T(i, 9 + (warp == 1 + GS_GEN_WARPS ? 0 : 3))
-      tc::mbar_wait(&sempty[st], ph ^ 1u);
+      tc::mbar_wait(grp ? &sempty[st] : &slo[st], ph ^ 1u);
       GS_T(i, 10 + (warp == 1 + GS_GEN_WARPS ? 0 : 3))
       uint8_t* bst = sB + (size_t)st * BST;
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const int f = fr0 + 128 * u;
+        const int f = fr0 + 64 * u;
         if (f < npad) {
           uint8_t* rowp = bst + f * 64;
           const int swz = (f >> 1) & 3;
@@ -475,7 +487,7 @@ __global__ void __launch_bounds__(GS_THREADS, 1) sketch_gaussian_tc_kernel(
       __syncwarp();
       if (lane == 0) {
         if ((i & 1) || i == nch - 1) tc::mbar_arrive(&xempty[xs]);
-        tc::mbar_arrive(&bfull[st]);
+        if (grp == 0 || npad > 256) tc::mbar_arrive(grp ? &bhi[st] : &bfull[st]);
       GS_T(i, 11 + (warp == 1 + GS_GEN_WARPS ? 0 : 3))
       }
     }
@@ -528,7 +540,7 @@ cudaError_t launch_sketch_gaussian_tc(const cdmd_video& v, const SensingPlan& P,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return cudaErrorInvalidValue;
-  const size_t smem = 1024 + 2 * (size_t)GS_A + 2 * (size_t)npad * GS_BK * 2 + (size_t)GS_XS * npad * GS_XK + 65536 + 256;
+  const size_t smem = 1024 + 2 * (size_t)GS_A + 2 * (size_t)npad * GS_BK * 2 + (size_t)GS_XS * npad * GS_XK + 65536 + 512;
   cudaError_t e = cudaFuncSetAttribute(sketch_gaussian_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   e = cudaMemsetAsync(Y, 0, sizeof(float) * (size_t)ldy * v.m, st);
