@@ -33,15 +33,17 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 FALLBACK_HBM_GBS = 6650.0   # B200_PROFILING.md fallback, used only without MEASURED_PEAKS.json
+FALLBACK_BF16_TFLOPS = 1590.0
 METRIC = "1080p frames/sec (sketch+modes+fg mask) at 1/2/4/8 B200; % of HBM roofline"
 
 
 def peaks():
+    """(HBM GB/s, dense bf16 TFLOP/s burst, source): MEASURED_PEAKS.json, else the recipe's fallback."""
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
         d = json.load(open(p))
-        return float(d["hbm_gbs"]), "measured"
-    return FALLBACK_HBM_GBS, "fallback"
+        return float(d["hbm_gbs"]), float(d["bf16_tflops"]), "measured"
+    return FALLBACK_HBM_GBS, FALLBACK_BF16_TFLOPS, "fallback"
 
 
 class ClockSampler:
@@ -230,10 +232,12 @@ def main():
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
+        n0 = C.cdmd_kernel_launches()
         start.record(stream)
         for _ in range(args.steps):
             step(record=True)
         stop.record(stream)
+        launches = C.cdmd_kernel_launches() - n0
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -269,8 +273,10 @@ def main():
         if world > 1:
             dist.barrier()
         with ClockSampler(local) as clk:
+            n0 = C.cdmd_kernel_launches()
             a, b_ = stream_run(args.steps)
             torch.cuda.synchronize()
+            launches = C.cdmd_kernel_launches() - n0
         if world > 1:
             dist.barrier()
         ts = torch.tensor([a.elapsed_time(b_) / args.steps], dtype=torch.float64, device="cuda")
@@ -281,8 +287,9 @@ def main():
         streaming = {"lanes": args.lanes, "ms_per_batch": round(ms_max, 4),
                      "note": "batches pipelined across lanes (own handle, stream, buffers, copy of X)"}
 
-    # roofline of the dominant kernel (HBM-bound passes; algorithmic bytes per launch)
-    hbm, hbm_src = peaks()
+    # roofline of the dominant kernel: HBM-bound passes (algorithmic bytes per launch) and,
+    # for the dense sensings, the tensor-core sketch (algorithmic 2 p n m flops per launch)
+    hbm, bf16, peak_src = peaks()
     ke, nc = P.model.k_eff, P.model.n_coef
     algo = {
         "modes": nl * (m - 1) + 4 * nl * ke,
@@ -291,19 +298,32 @@ def main():
     if cfg.kind in ("sparse", "spixel"):
         algo["sketch"] = (sector_bytes_sparse(nl, pix0, n, cfg.p, cfg.sensing_seed, m)
                           if cfg.kind == "sparse" else 32 * cfg.p * m + 4 * cfg.p * m)
+    elif cfg.kind in ("rademacher", "gaussian"):
+        algo["sketch"] = 2 * cfg.p * nl * m
+    # kind::f16 runs at the bf16 rate; kind::i8 at twice it (the guide's nominal 4.5 / 2.25 ratio)
+    tensor_peak = bf16 * (2.0 if cfg.kind == "rademacher" else 1.0)
+
+    def stage_roof(s):
+        if s == "sketch" and cfg.kind in ("rademacher", "gaussian"):
+            return algo[s] / (stage_ms[s] * 1e-3) / 1e12, tensor_peak, "tensor", "TFLOP/s"
+        return algo[s] / (stage_ms[s] * 1e-3) / 1e9, hbm, "hbm", "GB/s"
+
     cand = {s: stage_ms[s] for s in algo}
     dom = max(cand, key=cand.get)
-    achieved = algo[dom] / (stage_ms[dom] * 1e-3) / 1e9
+    achieved, peak, bound, unit = stage_roof(dom)
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp) and cfg.name == "c4_1080p_sparse" and world == 1 and mode:
         traffic = json.load(open(tp)).get(dom)
-    roof = {"kernel": {"sketch": "sketch_sparse_kernel", "modes": "modes_tc_kernel",
+    sk_kernel = {"sparse": "sketch_sparse_kernel", "spixel": "sketch_spixel_kernel",
+                 "rademacher": "sketch_rademacher_tc_kernel", "gaussian": "sketch_gaussian_tc_kernel"}[cfg.kind]
+    roof = {"kernel": {"sketch": sk_kernel, "modes": "modes_tc_kernel",
                        "foreground": "foreground_tc_kernel" if mode else "foreground_static_kernel"}[dom],
-            "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
-            "frac": round(achieved / hbm, 4), "traffic": traffic, "peak_source": hbm_src,
-            "algorithmic_bytes_per_launch": algo[dom], "launch_ms": round(stage_ms[dom], 4),
-            "stage_roofline": {s: round(algo[s] / (stage_ms[s] * 1e-3) / 1e9 / hbm, 4) for s in algo}}
+            "bound": bound, "achieved": round(achieved, 1), "peak": peak, "unit": unit,
+            "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
+            ("algorithmic_flops_per_launch" if bound == "tensor" else "algorithmic_bytes_per_launch"): algo[dom],
+            "launch_ms": round(stage_ms[dom], 4),
+            "stage_roofline": {s: round(stage_roof(s)[0] / stage_roof(s)[1], 4) for s in algo}}
 
     # e2e: host (pinned) video in, mask out, through the same public calls
     e2e = None
@@ -336,7 +356,6 @@ def main():
         cpu = None
         if not args.no_cpu_baseline and world == 1:
             cpu = cpu_baseline(cfg, X_host, args)
-        launches_per_step = {"sparse": 2, "spixel": 2}.get(cfg.kind, 1) + 6 + 1 + 1
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": "frames/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max, 4),
@@ -352,7 +371,7 @@ def main():
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": launches_per_step * args.steps,
+            "gpu_launches": launches,   # libcdmd kernels launched in the timed region (cdmd_kernel_launches)
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)

@@ -125,6 +125,10 @@ CDMD_API cdmd_status cdmd_create(int device, cdmd_handle* out);
 CDMD_API void cdmd_destroy(cdmd_handle h);
 CDMD_API const char* cdmd_status_str(cdmd_status s);
 CDMD_API const char* cdmd_version(void);
+/* Number of libcdmd kernel launches this process has issued so far (all handles,
+ * all streams; cuBLAS / cuSOLVER launches inside cdmd_fit are not counted).
+ * Diagnostics: bench.py reports the difference across its timed region.          */
+CDMD_API uint64_t cdmd_kernel_launches(void);
 
 /* ------------------------------------------------------------------- sketch
  * Y_full = C D (Alg. 1 step 3; Eq. P:286-288), C generated on the fly from

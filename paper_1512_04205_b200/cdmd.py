@@ -54,7 +54,7 @@ class Model(ctypes.Structure):
                 ("info", ctypes.c_int32), ("dt", ctypes.c_double)]
 
 
-SYMBOLS = ["cdmd_create", "cdmd_destroy", "cdmd_status_str", "cdmd_version",
+SYMBOLS = ["cdmd_create", "cdmd_destroy", "cdmd_status_str", "cdmd_version", "cdmd_kernel_launches",
            "cdmd_sketch_workspace_bytes", "cdmd_sketch", "cdmd_model_bytes", "cdmd_model_bind",
            "cdmd_fit_workspace_bytes", "cdmd_fit", "cdmd_modes", "cdmd_background",
            "cdmd_foreground", "cdmd_philox", "cdmd_gaussian_table", "cdmd_sparse_cap",
@@ -72,6 +72,7 @@ def _load():
         "cdmd_destroy": (None, [vp]),
         "cdmd_status_str": (ctypes.c_char_p, [i32]),
         "cdmd_version": (ctypes.c_char_p, []),
+        "cdmd_kernel_launches": (ctypes.c_uint64, []),
         "cdmd_sketch_workspace_bytes": (sz, [V, S]),
         "cdmd_sketch": (i32, [vp, V, S, vp, i64, vp, sz, vp]),
         "cdmd_model_bytes": (sz, [ctypes.c_int, ctypes.c_int, i64]),
@@ -204,6 +205,11 @@ def cdmd_philox(ctr, k0, k1, out, stream=None):
 
 def cdmd_gaussian_table(h, out, stream=None):
     _check("cdmd_gaussian_table", _lib.cdmd_gaussian_table(h.h, _ptr(out), _stream(stream)))
+
+
+def cdmd_kernel_launches():
+    """libcdmd kernel launches issued by this process so far (cuBLAS/cuSOLVER excluded)."""
+    return int(lib().cdmd_kernel_launches())
 
 
 def cdmd_sparse_cap(n_total, p, s=0.0):

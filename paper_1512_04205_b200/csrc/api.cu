@@ -84,6 +84,8 @@ extern "C" {
 
 const char* cdmd_version(void) { return "cdmd-b200 0.1 (sm_100a)"; }
 
+uint64_t cdmd_kernel_launches(void) { return cdmd::launch_counter().load(std::memory_order_relaxed); }
+
 const char* cdmd_status_str(cdmd_status s) {
   switch (s) {
     case CDMD_OK: return "ok";

@@ -2,6 +2,7 @@
 // oracle code is included or mirrored here.
 #pragma once
 #include <cuda_runtime.h>
+#include <atomic>
 #include <stdint.h>
 
 #include "../../include/cdmd.h"
@@ -11,6 +12,14 @@
 #define CDMD_NBLK 16        // kpad granularity (tcgen05 N step for M=128)
 
 namespace cdmd {
+
+// every libcdmd kernel launch site calls note_launch() (cdmd_kernel_launches)
+inline std::atomic<uint64_t>& launch_counter() {
+  static std::atomic<uint64_t> n{0};
+  return n;
+}
+inline void note_launch() { launch_counter().fetch_add(1, std::memory_order_relaxed); }
+
 
 // ---------------------------------------------------------------- Philox4x32-10
 // Salmon et al. SC'11 (the generator DESIGN.md §3.1 fixes for C): per round

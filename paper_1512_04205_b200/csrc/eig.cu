@@ -500,6 +500,7 @@ cudaError_t launch_hqr_eig(int k, const double* A, double* W, double* VR, int* i
   const size_t smem = hqr_smem_bytes(k);
   cudaError_t e = cudaFuncSetAttribute(hqr_eig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
+  note_launch();
   hqr_eig_kernel<<<1, 32, smem, st>>>(k, A, W, VR, info);
   return cudaGetLastError();
 }

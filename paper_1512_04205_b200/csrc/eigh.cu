@@ -439,17 +439,22 @@ cudaError_t launch_eh(int n, int k, const double* G, int64_t ldg, double* lam, d
   const size_t smem = eh_tridiag_smem(n);
   cudaError_t err = cudaFuncSetAttribute(eh_tridiag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
+  note_launch();
   eh_tridiag_kernel<<<EH_CL, EH_T, smem, st>>>(n, G, ldg, d, e, tau, V);
   if ((err = cudaGetLastError()) != cudaSuccess) return err;
   double* e2 = wk;
   double* bounds = e2 + n;
   double* ivw = bounds + 8;
+  note_launch();
   eh_prep_kernel<<<1, 256, 0, st>>>(n, d, e, e2, bounds);
+  note_launch();
   eh_bisect_kernel<<<k, 32, 0, st>>>(n, k, d, e2, bounds, lam);
+  note_launch();
   eh_invit_kernel<<<1, 128, 0, st>>>(n, k, d, e, bounds, lam, Zout, ivw, info);
   const size_t smem3 = sizeof(double) * (16 + EH_RB) * (size_t)n;
   err = cudaFuncSetAttribute(eh_backtransform_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3);
   if (err != cudaSuccess) return err;
+  note_launch();
   eh_backtransform_kernel<<<(unsigned)ceil_div(k, 16), 512, smem3, st>>>(n, k, V, tau, Zout);
   return cudaGetLastError();
 }

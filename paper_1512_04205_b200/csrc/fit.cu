@@ -552,6 +552,7 @@ cdmd_status fit_impl(cdmd_handle h, const void* Y, int64_t ldy, int kind, int64_
   // Y -> fp64
   {
     const int64_t N = p * m;
+    note_launch();
     if (kind == CDMD_GAUSSIAN)
       to_f64_kernel<float><<<(unsigned)ceil_div(N, 256), 256, 0, st>>>((const float*)Y, ldy, p, m, W.Yd);
     else
@@ -595,6 +596,7 @@ cdmd_status fit_impl(cdmd_handle h, const void* Y, int64_t ldy, int kind, int64_
       return CDMD_ERR_CUDA;
   }
   prof.mark("syevd");
+  note_launch();
   select_topk_kernel<<<k, 128, 0, st>>>(W.A, W.w, n1, top, k, W.V, model->sigma, W.dinfo);
   CU(cudaGetLastError());
   CU(cudaMemcpyAsync(h->host_info, W.dinfo, sizeof(int) * 16, cudaMemcpyDeviceToHost, st));
@@ -612,6 +614,7 @@ cdmd_status fit_impl(cdmd_handle h, const void* Y, int64_t ldy, int kind, int64_
                  W.V, (int)n1, &zero, W.T, (int)n1));
   BL(cublasDgemm(h->blas, CUBLAS_OP_T, CUBLAS_OP_N, ke, ke, (int)n1, &one, W.V, (int)n1, W.T,
                  (int)n1, &zero, W.B, ke));
+  note_launch();
   scale_atilde_kernel<<<ke, ke <= 1024 ? ((ke + 31) / 32) * 32 : 1024, 0, st>>>(W.B, model->sigma, ke);
   CU(cudaGetLastError());
   prof.mark("atilde");
@@ -636,6 +639,7 @@ cdmd_status fit_impl(cdmd_handle h, const void* Y, int64_t ldy, int kind, int64_
       return CDMD_ERR_CUDA;
   }
   prof.mark("geev");
+  note_launch();
   canonicalize_kernel<<<1, 256, 0, st>>>(ke, W.Wc, W.VR, model->sigma, dt, model->lambda,
                                         model->omega, model->pair, W.SW, W.dinfo);
   CU(cudaGetLastError());
@@ -650,10 +654,12 @@ cdmd_status fit_impl(cdmd_handle h, const void* Y, int64_t ldy, int kind, int64_
   BL(cublasDgemv(h->blas, CUBLAS_OP_T, (int)n1, ke, &one, model->Mfold, (int)n1, W.G + 1, 1, &zero,
                  W.cf, 1));
   prof.mark("canon+M+gram");
+  note_launch();
   omp_kernel<<<1, 256, 0, st>>>(ke, K, m, W.Gf, W.cf, W.G, model->pair, model->lambda, model->beta,
                                 model->support, model->coef, model->coef_col, W.dinfo);
   CU(cudaGetLastError());
   prof.mark("omp+coef");
+  note_launch();
   quantize_kernel<<<model->kpad, 256, 0, st>>>(model->Mfold, n1, ke, model->kpad, model->mpad,
                                                model->Mq, model->Mq_scale);
   CU(cudaGetLastError());

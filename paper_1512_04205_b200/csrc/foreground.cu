@@ -157,6 +157,7 @@ template <int NC>
 static cudaError_t launch_dyn(const cdmd_video& v, const cdmd_model& M, const float* Phi,
                               int64_t ldphi, float tau, uint32_t* mask, int64_t ldw, cudaStream_t st) {
   dim3 grid((unsigned)ceil_div(v.n_local, 1024), (unsigned)ceil_div(v.m, FG_FRAMES));
+  note_launch();
   foreground_dynamic_kernel<NC><<<grid, 256, 0, st>>>(v.X, v.ld, v.n_local, v.m, Phi, ldphi, M.coef,
                                                       M.coef_col, M.n_coef, tau, mask, ldw);
   return cudaGetLastError();
@@ -176,6 +177,7 @@ cudaError_t launch_foreground(const cdmd_video& v, const cdmd_model& M, const fl
     int64_t fpb = v.m;
     while (fpb > 64 && bx * ceil_div(v.m, fpb) < 2 * 148) fpb = (fpb + 1) / 2;
     dim3 grid((unsigned)bx, (unsigned)ceil_div(v.m, fpb));
+    note_launch();
     foreground_static_kernel<<<grid, 256, 0, st>>>(v.X, v.ld, v.n_local, v.m, Phi, ldphi, M.coef,
                                                    M.coef_col, M.n_coef, tau, mask, ldw, fpb);
     return cudaGetLastError();
@@ -209,6 +211,7 @@ cudaError_t launch_background(const float* Phi, int64_t ldphi, int64_t n_local, 
                               int mode, int64_t t0, int64_t nt, float* L, int64_t ldl,
                               cudaStream_t st) {
   dim3 grid((unsigned)ceil_div(n_local, 256), (unsigned)nt);
+  note_launch();
   background_kernel<<<grid, 256, 0, st>>>(Phi, ldphi, n_local, M.m, M.coef, M.coef_col, M.n_coef,
                                           mode == CDMD_BG_DYNAMIC, t0, nt, L, ldl);
   return cudaGetLastError();

@@ -348,6 +348,7 @@ static cudaError_t launch_kp(const cdmd_video& v, const cdmd_model& M, const flo
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int num_tiles = (int)ceil_div(v.n_local, FG_BN);
   const int grid = num_tiles < sms ? num_tiles : sms;
+  note_launch();
   foreground_tc_kernel<KP><<<grid, 32 * (2 + FG_EPI_WARPS), smem, st>>>(
       mapX, v.n_local, v.m, nfb, Phi, ldphi, M.coef, M.coef_col, M.n_coef, tau, mask, ldw, num_tiles, stages, dbg_mode());
   return cudaGetLastError();

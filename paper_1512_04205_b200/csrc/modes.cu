@@ -78,6 +78,7 @@ __global__ void __launch_bounds__(256) modes_simt_kernel(
 cudaError_t launch_modes_simt(const cdmd_video& v, const cdmd_model& M, float* Phi, int64_t ldphi,
                               cudaStream_t st) {
   dim3 grid((unsigned)ceil_div(v.n_local, 64), (unsigned)(M.kpad / 16));
+  note_launch();
   modes_simt_kernel<<<grid, 256, 0, st>>>(v.X, v.ld, v.n_local, v.m, M.Mq, M.Mq_scale, M.kpad,
                                           M.mpad, M.k_eff, Phi, ldphi);
   return cudaGetLastError();

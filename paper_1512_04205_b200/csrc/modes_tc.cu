@@ -201,6 +201,7 @@ static cudaError_t launch_nt(const cdmd_video& v, const cdmd_model& M, float* Ph
   const int grid = num_tiles < sms ? num_tiles : sms;
   uint32_t cols = 32;
   while (cols < 2u * NT) cols <<= 1;
+  note_launch();
   modes_tc_kernel<NT><<<grid, 320, smem, st>>>(mapA, mapB, v.n_local, nkb, stages, M.kpad, M.k_eff,
                                                 M.Mq_scale, Phi, ldphi, num_tiles, cols);
   return cudaGetLastError();

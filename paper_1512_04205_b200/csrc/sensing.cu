@@ -63,6 +63,7 @@ __global__ void spixel_rows_kernel(int64_t n, int64_t p, int h, uint32_t k0, uin
 
 cudaError_t launch_spixel_rows(const SensingPlan& P, int32_t* rows, cudaStream_t st) {
   const int T = 128;
+  note_launch();
   spixel_rows_kernel<<<(unsigned)ceil_div(P.p, T), T, 0, st>>>(P.n, P.p, P.h, P.k0, P.k1, rows);
   return cudaGetLastError();
 }
@@ -96,6 +97,7 @@ __global__ void sparse_rows_kernel(int64_t n, int64_t p, double lq, int64_t cap,
 cudaError_t launch_sparse_rows(const SensingPlan& P, int32_t* ell, int32_t* counts, int32_t* flags,
                                cudaStream_t st) {
   const int T = 64;
+  note_launch();
   sparse_rows_kernel<<<(unsigned)ceil_div(P.p, T), T, 0, st>>>(P.n, P.p, P.lq, P.cap, P.k0, P.k1,
                                                                ell, counts, flags);
   return cudaGetLastError();
@@ -116,6 +118,7 @@ __global__ void gaussian_table_kernel(uint16_t* __restrict__ table) {
 }
 
 cudaError_t launch_gaussian_table(uint16_t* table, cudaStream_t st) {
+  note_launch();
   gaussian_table_kernel<<<256, 256, 0, st>>>(table);
   return cudaGetLastError();
 }
@@ -135,6 +138,7 @@ __global__ void philox_test_kernel(const uint32_t* __restrict__ ctr, uint32_t k0
 cudaError_t launch_philox_test(const uint32_t* ctr, uint32_t k0, uint32_t k1, uint32_t* out,
                                int64_t count, cudaStream_t st) {
   if (count <= 0) return cudaSuccess;
+  note_launch();
   philox_test_kernel<<<(unsigned)ceil_div(count, 256), 256, 0, st>>>(ctr, k0, k1, out, count);
   return cudaGetLastError();
 }

@@ -34,6 +34,7 @@ __global__ void sketch_spixel_kernel(const uint8_t* __restrict__ X, int64_t ld, 
 cudaError_t launch_sketch_spixel(const cdmd_video& v, const SensingPlan& P, const int32_t* rows,
                                  int32_t* Y, int64_t ldy, cudaStream_t st) {
   dim3 grid((unsigned)ceil_div(P.p, 128), (unsigned)ceil_div(v.m, 64));
+  note_launch();
   sketch_spixel_kernel<<<grid, 128, 0, st>>>(v.X, v.ld, v.pix0, v.n_local, v.m, P.p, rows, Y, ldy);
   return cudaGetLastError();
 }
@@ -82,6 +83,7 @@ __global__ void __launch_bounds__(256) sketch_sparse_kernel(
 cudaError_t launch_sketch_sparse(const cdmd_video& v, const SensingPlan& P, const int32_t* ell,
                                  const int32_t* counts, int32_t* Y, int64_t ldy, cudaStream_t st) {
   dim3 grid((unsigned)ceil_div(P.p, 8), (unsigned)ceil_div(v.m, 32));
+  note_launch();
   sketch_sparse_kernel<<<grid, 256, 0, st>>>(v.X, v.ld, v.pix0, v.n_local, v.m, P.p, ell, counts,
                                              P.cap, Y, ldy);
   return cudaGetLastError();
@@ -168,6 +170,7 @@ cudaError_t launch_sketch_rademacher(const cdmd_video& v, const SensingPlan& P, 
   if (sketch_rademacher_tc_supported(v) && !getenv("CDMD_SIMT_SKETCH"))
     return launch_sketch_rademacher_tc(v, P, Y, ldy, st);
   dim3 grid((unsigned)ceil_div(P.p, 64), (unsigned)ceil_div(v.m, 64));
+  note_launch();
   sketch_rademacher_simt_kernel<<<grid, 256, 0, st>>>(v.X, v.ld, v.pix0, v.n_local, v.m, P.p, P.k0,
                                                       P.k1, Y, ldy);
   return cudaGetLastError();
@@ -245,6 +248,7 @@ cudaError_t launch_sketch_gaussian(const cdmd_video& v, const SensingPlan& P, co
   if (sketch_gaussian_tc_supported(v) && !getenv("CDMD_SIMT_SKETCH"))
     return launch_sketch_gaussian_tc(v, P, table, Y, ldy, st);
   dim3 grid((unsigned)ceil_div(P.p, 64), (unsigned)ceil_div(v.m, 64));
+  note_launch();
   sketch_gaussian_simt_kernel<<<grid, 256, 0, st>>>(v.X, v.ld, v.pix0, v.n_local, v.m, P.p, P.k0,
                                                     P.k1, table, Y, ldy);
   return cudaGetLastError();

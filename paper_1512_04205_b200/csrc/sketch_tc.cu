@@ -204,6 +204,7 @@ cudaError_t launch_sketch_rademacher_tc(const cdmd_video& v, const SensingPlan& 
   e = cudaMemsetAsync(Y, 0, sizeof(int32_t) * (size_t)ldy * v.m, st);
   if (e != cudaSuccess) return e;
   dim3 grid((unsigned)nrb, (unsigned)nfb, (unsigned)splits);
+  note_launch();
   sketch_rademacher_tc_kernel<<<grid, 192, smem, st>>>(mapX, v.pix0, v.n_local, v.m, P.p, P.k0, P.k1, fbn,
                                                        nchunks, cps, stages, Y, ldy);
   return cudaGetLastError();
@@ -546,6 +547,7 @@ cudaError_t launch_sketch_gaussian_tc(const cdmd_video& v, const SensingPlan& P,
   e = cudaMemsetAsync(Y, 0, sizeof(float) * (size_t)ldy * v.m, st);
   if (e != cudaSuccess) return e;
   dim3 grid((unsigned)nrb, (unsigned)splits);
+  note_launch();
   sketch_gaussian_tc_kernel<<<grid, GS_THREADS, smem, st>>>(mapX, v.pix0, v.n_local, v.m, P.p, P.k0, P.k1, table, npad,
                                                             nchunks, cps, xbox, Y, ldy);
   return cudaGetLastError();
