@@ -118,6 +118,7 @@ cdmd_status cdmd_create(int device, cdmd_handle* out) {
   if (st == CDMD_OK && cusolverDnCreateParams(&h->params) != CUSOLVER_STATUS_SUCCESS) st = CDMD_ERR_CUDA;
   if (st == CDMD_OK && cudaMalloc(&h->gauss_table, 65536 * sizeof(uint16_t)) != cudaSuccess) st = CDMD_ERR_CUDA;
   if (st == CDMD_OK && cudaMallocHost(&h->host_info, 16 * sizeof(int32_t)) != cudaSuccess) st = CDMD_ERR_CUDA;
+  if (st == CDMD_OK && cudaMalloc(&h->sched, 16 * sizeof(int)) != cudaSuccess) st = CDMD_ERR_CUDA;
   if (st == CDMD_OK && launch_gaussian_table(h->gauss_table, 0) != cudaSuccess) st = CDMD_ERR_CUDA;
   if (st == CDMD_OK && cudaDeviceSynchronize() != cudaSuccess) st = CDMD_ERR_CUDA;
   if (st != CDMD_OK) {
@@ -135,6 +136,7 @@ void cdmd_destroy(cdmd_handle h) {
   if (h->blas) cublasDestroy(h->blas);
   if (h->gauss_table) cudaFree(h->gauss_table);
   if (h->host_info) cudaFreeHost(h->host_info);
+  if (h->sched) cudaFree(h->sched);
   delete h;
 }
 
@@ -254,7 +256,7 @@ cdmd_status cdmd_modes(cdmd_handle h, const cdmd_video* v, const cdmd_model* M, 
                        int64_t ldphi, cdmd_stream st) {
   cdmd_status s = modes_common(h, v, M, Phi, ldphi);
   if (s != CDMD_OK) return s;
-  return cuda_status(launch_modes_tc(*v, *M, Phi, ldphi, (cudaStream_t)st));
+  return cuda_status(launch_modes_tc(*v, *M, Phi, ldphi, h->sched + 0, (cudaStream_t)st));
 }
 
 cdmd_status cdmd_modes_simt(cdmd_handle h, const cdmd_video* v, const cdmd_model* M, float* Phi,
@@ -287,7 +289,7 @@ cdmd_status cdmd_foreground(cdmd_handle h, const cdmd_video* v, const cdmd_model
   if ((s = check_model(M, v->m)) != CDMD_OK) return s;
   if (!(tau > 0.0f)) return CDMD_ERR_RANGE;
   if (ldphi < v->n_local || ldw < ceil_div(v->n_local, 32)) return CDMD_ERR_ARG;
-  return cuda_status(launch_foreground(*v, *M, Phi, ldphi, mode, tau, mask, ldw, (cudaStream_t)st));
+  return cuda_status(launch_foreground(*v, *M, Phi, ldphi, mode, tau, mask, ldw, h->sched + 1, (cudaStream_t)st));
 }
 
 // --------------------------------------------------------------- test hooks

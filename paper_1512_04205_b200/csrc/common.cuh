@@ -96,14 +96,15 @@ cudaError_t launch_sketch_gaussian(const cdmd_video& v, const SensingPlan& P, co
 
 cudaError_t launch_modes_simt(const cdmd_video& v, const cdmd_model& M, float* Phi, int64_t ldphi,
                               cudaStream_t st);
+// tile_counter: one device int of the handle (dynamic persistent tile schedule)
 cudaError_t launch_modes_tc(const cdmd_video& v, const cdmd_model& M, float* Phi, int64_t ldphi,
-                            cudaStream_t st);
+                            int* tile_counter, cudaStream_t st);
 
 cudaError_t launch_background(const float* Phi, int64_t ldphi, int64_t n_local, const cdmd_model& M,
                               int mode, int64_t t0, int64_t nt, float* L, int64_t ldl,
                               cudaStream_t st);
 cudaError_t launch_foreground(const cdmd_video& v, const cdmd_model& M, const float* Phi,
                               int64_t ldphi, int mode, float tau, uint32_t* mask, int64_t ldw,
-                              cudaStream_t st);
+                              int* tile_counter, cudaStream_t st);
 
 }  // namespace cdmd

@@ -272,99 +272,135 @@ __global__ void __launch_bounds__(32) eh_bisect_kernel(int n, int k, const doubl
   if (lane == 0) lam[k - 1 - r] = 0.5 * (lo + hi);
 }
 
-// Inverse iteration on T - lambda I (LU with partial pivoting), one thread per group
+// Inverse iteration on T - lambda I (LU with partial pivoting), one warp per group
 // of eigenvalues closer than 1e-7 ||T|| (re-orthogonalised with modified Gram-Schmidt,
 // as LAPACK dstein does for clusters).  lam ascending (k largest); Z[:, q] <-> lam[q].
-__global__ void __launch_bounds__(128) eh_invit_kernel(int n, int k, const double* __restrict__ d,
-                                                       const double* __restrict__ e,
-                                                       const double* __restrict__ bounds,
-                                                       const double* __restrict__ lam, double* __restrict__ Z,
-                                                       double* __restrict__ work, int* __restrict__ info) {
-  __shared__ int cstart[258];
+__global__ void __launch_bounds__(32) eh_invit_kernel(int n, int k, const double* __restrict__ d,
+                                                      const double* __restrict__ e,
+                                                      const double* __restrict__ bounds,
+                                                      const double* __restrict__ lam, double* __restrict__ Z,
+                                                      int* __restrict__ info) {
+  // one warp (CTA) per group of (numerically) equal eigenvalues; the LU factors and
+  // the iterate live in shared memory.  Lane 0 runs the two sequential recurrences
+  // (multiplying by stored reciprocal pivots); the lanes share the vector operations.
+  extern __shared__ double ism[];
+  double* ui = ism;               // 1 / pivot
+  double* u1 = ui + n;
+  double* u2 = u1 + n;
+  double* lm = u2 + n;
+  double* z = lm + n;
+  uint8_t* pv = reinterpret_cast<uint8_t*>(z + n);   // rows i, i+1 swapped
+  const int lane = threadIdx.x;
   const double tnorm = bounds[2];
   const double eps = 2.220446049250313e-16;
-  if (threadIdx.x == 0) {
-    int nc = 0;   // groups in descending order r = 0 .. k-1 (q = k-1-r)
-    for (int r = 0; r < k; ++r)
-      if (r == 0 || fabs(lam[k - r] - lam[k - 1 - r]) > 1e-7 * tnorm) cstart[nc++] = r;
-    cstart[nc] = k;
-    cstart[257] = nc;
+  // group c of the descending order r = 0 .. k-1 (q = k-1-r): [r0, r1)
+  int g = -1, r0 = 0, r1 = 0;
+  for (int r = 0; r < k; ++r) {
+    if (r == 0 || fabs(lam[k - r] - lam[k - 1 - r]) > 1e-7 * tnorm) {
+      if (g == (int)blockIdx.x) break;
+      ++g;
+      r0 = r;
+    }
+    r1 = r + 1;
   }
-  __syncthreads();
-  const int ncl = cstart[257];
-  for (int c = threadIdx.x; c < ncl; c += blockDim.x) {
-    double* u = work + (int64_t)c * 6 * n;
-    double* u1 = u + n;
-    double* u2 = u1 + n;
-    double* lm = u2 + n;
-    double* z = lm + n;
-    double* piv = z + n;
-    for (int r = cstart[c]; r < cstart[c + 1]; ++r) {
-      const int q = k - 1 - r;
-      const double lambda = lam[q];
-      const double tiny = eps * tnorm;
+  if (g != (int)blockIdx.x) return;
+  auto warp_sum = [&](double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+  };
+  for (int r = r0; r < r1; ++r) {
+    const int q = k - 1 - r;
+    const double lambda = lam[q];
+    const double tiny = eps * tnorm;
+    if (lane == 0) {   // LU of T - lambda I with partial pivoting
       double a = d[0] - lambda, b = n > 1 ? e[0] : 0.0;
       for (int i = 0; i < n - 1; ++i) {
         const double sub = e[i];
         const double dnext = d[i + 1] - lambda;
         const double enext = (i + 1 < n - 1) ? e[i + 1] : 0.0;
         if (fabs(a) >= fabs(sub)) {
-          piv[i] = 0.0;
+          const double piv = (a != 0.0) ? a : tiny;
           const double mult = (a != 0.0) ? sub / a : 0.0;
+          pv[i] = 0;
           lm[i] = mult;
-          u[i] = (a != 0.0) ? a : tiny;
+          ui[i] = 1.0 / piv;
           u1[i] = b;
           u2[i] = 0.0;
           a = dnext - mult * b;
           b = enext;
         } else {
-          piv[i] = 1.0;
           const double mult = a / sub;
+          pv[i] = 1;
           lm[i] = mult;
-          u[i] = sub;
+          ui[i] = 1.0 / sub;
           u1[i] = dnext;
           u2[i] = enext;
           a = b - mult * dnext;
           b = -mult * enext;
         }
       }
-      u[n - 1] = (fabs(a) > tiny) ? a : (a >= 0 ? tiny : -tiny);
-      for (int i = 0; i < n; ++i) z[i] = 1.0 + 0.5 * sin(1.0 + 0.713 * i + 0.37 * r);
-      for (int it = 0; it < 3; ++it) {
+      ui[n - 1] = 1.0 / ((fabs(a) > tiny) ? a : (a >= 0 ? tiny : -tiny));
+      u1[n - 1] = 0.0;
+      u2[n - 1] = 0.0;
+    }
+    for (int i = lane; i < n; i += 32) z[i] = 1.0 + 0.5 * sin(1.0 + 0.713 * i + 0.37 * r);
+    __syncwarp();
+    for (int it = 0; it < 3; ++it) {
+      if (lane == 0) {
+        double zc = z[0];                  // forward: row swaps and multipliers
         for (int i = 0; i < n - 1; ++i) {
-          if (piv[i] != 0.0) {
-            const double t = z[i];
-            z[i] = z[i + 1];
-            z[i + 1] = t - lm[i] * z[i];
+          const double zn = z[i + 1];
+          if (pv[i]) {
+            z[i] = zn;
+            zc = zc - lm[i] * zn;
           } else {
-            z[i + 1] -= lm[i] * z[i];
+            z[i] = zc;
+            zc = zn - lm[i] * zc;
           }
         }
+        z[n - 1] = zc;
+        double z1 = 0.0, z2 = 0.0;         // backward: U z = z
         for (int i = n - 1; i >= 0; --i) {
-          double s2 = z[i];
-          if (i + 1 < n) s2 -= u1[i] * z[i + 1];
-          if (i + 2 < n) s2 -= u2[i] * z[i + 2];
-          z[i] = s2 / u[i];
+          const double zi = (z[i] - u1[i] * z1 - u2[i] * z2) * ui[i];
+          z[i] = zi;
+          z2 = z1;
+          z1 = zi;
         }
-        for (int rr = cstart[c]; rr < r; ++rr) {
-          const double* zq = Z + (int64_t)(k - 1 - rr) * n;
-          double dot = 0.0;
-          for (int i = 0; i < n; ++i) dot += zq[i] * z[i];
-          for (int i = 0; i < n; ++i) z[i] -= dot * zq[i];
-        }
-        double nn = 0.0;
-        for (int i = 0; i < n; ++i) nn += z[i] * z[i];
-        const double inv = 1.0 / sqrt(nn);
-        for (int i = 0; i < n; ++i) z[i] *= inv;
       }
-      int im = 0;
-      for (int i = 1; i < n; ++i)
-        if (fabs(z[i]) > fabs(z[im])) im = i;
-      const double sg = z[im] < 0 ? -1.0 : 1.0;
-      for (int i = 0; i < n; ++i) Z[i + (int64_t)q * n] = sg * z[i];
+      __syncwarp();
+      for (int rr = r0; rr < r; ++rr) {   // orthogonalise within the group (MGS)
+        const double* zq = Z + (int64_t)(k - 1 - rr) * n;
+        double dot = 0.0;
+        for (int i = lane; i < n; i += 32) dot += zq[i] * z[i];
+        dot = warp_sum(dot);
+        for (int i = lane; i < n; i += 32) z[i] -= dot * zq[i];
+        __syncwarp();
+      }
+      double nn = 0.0;
+      for (int i = lane; i < n; i += 32) nn += z[i] * z[i];
+      const double inv = 1.0 / sqrt(warp_sum(nn));
+      for (int i = lane; i < n; i += 32) z[i] *= inv;
+      __syncwarp();
     }
+    // sign: the largest-magnitude entry (first on ties) positive
+    double best = -1.0;
+    int im = n;
+    for (int i = lane; i < n; i += 32) {
+      const double v = fabs(z[i]);
+      if (v > best) { best = v; im = i; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, im, o);
+      if (ob > best || (ob == best && oi < im)) { best = ob; im = oi; }
+    }
+    const double sg = z[im] < 0 ? -1.0 : 1.0;
+    for (int i = lane; i < n; i += 32) Z[i + (int64_t)q * n] = sg * z[i];
+    __syncwarp();
   }
-  if (threadIdx.x == 0) *info = 0;
+  if (blockIdx.x == 0 && lane == 0) *info = 0;
 }
 
 // Z <- Q Z, Q = H_0 H_1 ... H_{n-2}: blocks of 16 columns (one warp each, the column in
@@ -423,7 +459,7 @@ size_t eh_tridiag_smem(int n) {
 bool eh_supported(int n, int k) { return n >= 3 && n <= EH_NMAX && k <= 256 && eh_tridiag_smem(n) <= 227 * 1024; }
 
 size_t eh_work_doubles(int n, int k) {
-  return (size_t)n * n + 3 * (size_t)n + (size_t)n * k + 6 * (size_t)n * k + 64;
+  return (size_t)n * n + 3 * (size_t)n + (size_t)n * k + 64;
 }
 
 // G (n x n, ld ldg) -> lam[k] (ascending: the k largest), Zout (n x k column-major, ld n).
@@ -444,13 +480,15 @@ cudaError_t launch_eh(int n, int k, const double* G, int64_t ldg, double* lam, d
   if ((err = cudaGetLastError()) != cudaSuccess) return err;
   double* e2 = wk;
   double* bounds = e2 + n;
-  double* ivw = bounds + 8;
   note_launch();
   eh_prep_kernel<<<1, 256, 0, st>>>(n, d, e, e2, bounds);
   note_launch();
   eh_bisect_kernel<<<k, 32, 0, st>>>(n, k, d, e2, bounds, lam);
   note_launch();
-  eh_invit_kernel<<<1, 128, 0, st>>>(n, k, d, e, bounds, lam, Zout, ivw, info);
+  const size_t smem2 = sizeof(double) * 5 * (size_t)n + (size_t)n + 16;
+  err = cudaFuncSetAttribute(eh_invit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
+  if (err != cudaSuccess) return err;
+  eh_invit_kernel<<<(unsigned)k, 32, smem2, st>>>(n, k, d, e, bounds, lam, Zout, info);
   const size_t smem3 = sizeof(double) * (16 + EH_RB) * (size_t)n;
   err = cudaFuncSetAttribute(eh_backtransform_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3);
   if (err != cudaSuccess) return err;

@@ -165,11 +165,11 @@ static cudaError_t launch_dyn(const cdmd_video& v, const cdmd_model& M, const fl
 
 bool foreground_tc_supported(const cdmd_video& v, const cdmd_model& M);
 cudaError_t launch_foreground_tc(const cdmd_video& v, const cdmd_model& M, const float* Phi, int64_t ldphi,
-                                 float tau, uint32_t* mask, int64_t ldw, cudaStream_t st);
+                                 float tau, uint32_t* mask, int64_t ldw, int* tile_counter, cudaStream_t st);
 
 cudaError_t launch_foreground(const cdmd_video& v, const cdmd_model& M, const float* Phi,
                               int64_t ldphi, int mode, float tau, uint32_t* mask, int64_t ldw,
-                              cudaStream_t st) {
+                              int* tile_counter, cudaStream_t st) {
   if (mode == CDMD_BG_STATIC) {
     // one thread per mask word; frames split so the grid covers >= 4 waves
     const int64_t words = ceil_div(v.n_local, 32);
@@ -182,7 +182,8 @@ cudaError_t launch_foreground(const cdmd_video& v, const cdmd_model& M, const fl
                                                    M.coef_col, M.n_coef, tau, mask, ldw, fpb);
     return cudaGetLastError();
   }
-  if (foreground_tc_supported(v, M)) return launch_foreground_tc(v, M, Phi, ldphi, tau, mask, ldw, st);
+  if (foreground_tc_supported(v, M))
+    return launch_foreground_tc(v, M, Phi, ldphi, tau, mask, ldw, tile_counter, st);
   const int nc = M.n_coef;
   if (nc <= 4) return launch_dyn<4>(v, M, Phi, ldphi, tau, mask, ldw, st);
   if (nc <= 8) return launch_dyn<8>(v, M, Phi, ldphi, tau, mask, ldw, st);

@@ -11,7 +11,8 @@
 // followed by an epilogue in which each thread owns one frame (TMEM lane) and reads
 // 32 consecutive pixels' backgrounds (TMEM columns) and bytes (two 16-B loads from
 // the SWIZZLE_128B TMA tile), builds the 32-bit mask word in registers (f32x2 packed
-// subtractions) and stores whole words.  Persistent CTAs; warp 0 TMA producer,
+// subtractions) and stores whole words.  Persistent CTAs with a dynamic tile schedule
+// (tc::TileQueue: tiles claimed from a counter); warp 0 TMA producer,
 // warp 1 TMEM owner + MMA issuer, warps 2..17 epilogue (they also split Phi_F of the
 // next tile into the B operand).  One read of X, one write of the mask.
 #include <cuda_bf16.h>
@@ -92,7 +93,7 @@ __global__ void __launch_bounds__(32 * (2 + FG_EPI_WARPS), 1) foreground_tc_kern
     const __grid_constant__ CUtensorMap mapX, int64_t n_local, int64_t m, int nfb,
     const float* __restrict__ Phi, int64_t ldphi, const float* __restrict__ coef,
     const int32_t* __restrict__ coef_col, int n_coef, float tau, uint32_t* __restrict__ mask,
-    int64_t ldw, int num_tiles, int stages, int dbg) {
+    int64_t ldw, int num_tiles, int stages, int dbg, int* __restrict__ tile_counter) {
   constexpr int PART_B = FG_BN * KP * 2;  // bytes of one split part of Phi_F (B)
   extern __shared__ __align__(1024) uint8_t smem_raw[];   // 1024-B aligned: SWIZZLE_128B atoms
   uint8_t* smem = smem_raw;                                  // (keeps the shared address space visible)
@@ -108,6 +109,9 @@ __global__ void __launch_bounds__(32 * (2 + FG_EPI_WARPS), 1) foreground_tc_kern
   uint64_t* tfull = bempty + 2;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  __shared__ int tq_id[tc::TQ_N];
+  __shared__ uint64_t tq_bar[2 * tc::TQ_N];
+  const tc::TileQueue tq{tq_id, tq_bar, tq_bar + tc::TQ_N};
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // ---- coefficient table H (frames x KP), split in three bf16 parts, resident
@@ -132,6 +136,7 @@ __global__ void __launch_bounds__(32 * (2 + FG_EPI_WARPS), 1) foreground_tc_kern
       tc::mbar_init(&tfull[b], 1);
       tc::mbar_init(&tempty[b], FG_EPI_WARPS);
     }
+    tc::tq_init(tq, 1 + FG_EPI_WARPS);   // MMA issuer + epilogue warps
     tc::fence_mbar_init();
     tc::tma_prefetch(&mapX);
   }
@@ -146,7 +151,14 @@ __global__ void __launch_bounds__(32 * (2 + FG_EPI_WARPS), 1) foreground_tc_kern
     if (lane == 0) {  // ------------------------------------------ TMA producer
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x)
+      // tiles are published two ahead of this thread's own loads: the epilogue
+      // prefetches Phi_F of tile k + 2 while it works on tile k
+      int pub = 0;
+      bool ended = false;
+      for (int k = 0;; ++k) {
+        while (!ended && pub <= k + 2) ended = tc::tq_publish(tq, pub++, tile_counter, num_tiles) < 0;
+        const int tile = tq_id[k % tc::TQ_N];   // published by this thread, not yet reusable
+        if (tile < 0) break;
         for (int fb = 0; fb < nfb; ++fb) {
           tc::mbar_wait(&xempty[stage], phase ^ 1u);
           tc::mbar_arrive_expect_tx(&xfull[stage], FG_XSTAGE);
@@ -155,13 +167,15 @@ __global__ void __launch_bounds__(32 * (2 + FG_EPI_WARPS), 1) foreground_tc_kern
           tc::tma_load_2d(dst + FG_XSTAGE / 2, &mapX, &xfull[stage], tile * FG_BN + 128, fb * FG_BM);
           if (++stage == stages) { stage = 0; phase ^= 1u; }
         }
+      }
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ------------------------------------------- MMA issuer
       constexpr uint32_t IDESC = tc::idesc_f16(FG_BM, FG_BN, true, true, false, false);
       const uint32_t aBase = tc::smem_u32(sA), bBase = tc::smem_u32(sB);
       int it = 0, ti = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++ti) {
+      for (;; ++ti) {
+        if (tc::tq_take(tq, ti) < 0) break;
         const int bb = ti & 1;
         tc::mbar_wait(&bfull[bb], (uint32_t)(ti >> 1) & 1u);
         tc::fence_after();
@@ -209,7 +223,7 @@ __global__ void __launch_bounds__(32 * (2 + FG_EPI_WARPS), 1) foreground_tc_kern
 #pragma unroll
       for (int u = 0; u < BH; ++u) {
         const int f = bfh * BH + u;
-        pv[u] = (tile < num_tiles && f < n_coef && j < n_local) ? __ldg(Phi + j + (int64_t)coef_col[f] * ldphi) : 0.f;
+        pv[u] = (tile >= 0 && f < n_coef && j < n_local) ? __ldg(Phi + j + (int64_t)coef_col[f] * ldphi) : 0.f;
       }
     };
     auto build_b = [&](int tix) {
@@ -230,13 +244,18 @@ __global__ void __launch_bounds__(32 * (2 + FG_EPI_WARPS), 1) foreground_tc_kern
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&bfull[bb]);
     };
-    load_phi(blockIdx.x);
-    if ((int)blockIdx.x < num_tiles) build_b(0);
-    load_phi(blockIdx.x + gridDim.x);
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++ti) {
-      if (tile + (int)gridDim.x < num_tiles) {
+    // tile ids in order from the queue: this tile, the next (B being built), the one after
+    int tile = tc::tq_take_warp(tq, 0);
+    load_phi(tile);
+    if (tile >= 0) build_b(0);
+    int tnext = tile >= 0 ? tc::tq_take_warp(tq, 1) : -1;
+    load_phi(tnext);
+    for (; tile >= 0; ++ti) {
+      int tafter = -1;
+      if (tnext >= 0) {
         build_b(ti + 1);
-        load_phi(tile + 2 * gridDim.x);
+        tafter = tc::tq_take_warp(tq, ti + 2);
+        load_phi(tafter);
       }
       for (int fb = 0; fb < nfb; ++fb, ++it) {
         const int tb = it & 1;
@@ -284,6 +303,8 @@ __global__ void __launch_bounds__(32 * (2 + FG_EPI_WARPS), 1) foreground_tc_kern
           }
         }
       }
+      tile = tnext;
+      tnext = tafter;
     }
   }
   __syncthreads();
@@ -322,12 +343,12 @@ bool foreground_tc_supported(const cdmd_video& v, const cdmd_model& M) {
   const int KP = fg_kp(M.n_coef);
   if (!KP || !fg_encode_fn()) return false;
   const int nfb = (int)ceil_div(v.m, FG_BM);
-  return fg_smem_bytes(KP, nfb, 2) <= 227 * 1024 && (v.ld % 16) == 0;
+  return fg_smem_bytes(KP, nfb, 2) <= 226 * 1024 && (v.ld % 16) == 0;   // 1 KB: static smem
 }
 
 template <int KP>
 static cudaError_t launch_kp(const cdmd_video& v, const cdmd_model& M, const float* Phi, int64_t ldphi,
-                             float tau, uint32_t* mask, int64_t ldw, cudaStream_t st) {
+                             float tau, uint32_t* mask, int64_t ldw, int* tile_counter, cudaStream_t st) {
   const int nfb = (int)ceil_div(v.m, FG_BM);
   CUtensorMap mapX;
   cuuint64_t dims[2] = {(cuuint64_t)v.n_local, (cuuint64_t)v.m};
@@ -339,7 +360,7 @@ static cudaError_t launch_kp(const cdmd_video& v, const cdmd_model& M, const flo
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return cudaErrorInvalidValue;
   int stages = 4;
-  while (stages > 2 && fg_smem_bytes(KP, nfb, stages) > 227 * 1024) --stages;
+  while (stages > 2 && fg_smem_bytes(KP, nfb, stages) > 226 * 1024) --stages;
   const size_t smem = fg_smem_bytes(KP, nfb, stages);
   cudaError_t e = cudaFuncSetAttribute(foreground_tc_kernel<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -348,16 +369,19 @@ static cudaError_t launch_kp(const cdmd_video& v, const cdmd_model& M, const flo
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int num_tiles = (int)ceil_div(v.n_local, FG_BN);
   const int grid = num_tiles < sms ? num_tiles : sms;
+  e = cudaMemsetAsync(tile_counter, 0, sizeof(int), st);
+  if (e != cudaSuccess) return e;
   note_launch();
   foreground_tc_kernel<KP><<<grid, 32 * (2 + FG_EPI_WARPS), smem, st>>>(
-      mapX, v.n_local, v.m, nfb, Phi, ldphi, M.coef, M.coef_col, M.n_coef, tau, mask, ldw, num_tiles, stages, dbg_mode());
+      mapX, v.n_local, v.m, nfb, Phi, ldphi, M.coef, M.coef_col, M.n_coef, tau, mask, ldw, num_tiles, stages, dbg_mode(),
+      tile_counter);
   return cudaGetLastError();
 }
 
 cudaError_t launch_foreground_tc(const cdmd_video& v, const cdmd_model& M, const float* Phi, int64_t ldphi,
-                                 float tau, uint32_t* mask, int64_t ldw, cudaStream_t st) {
-  if (fg_kp(M.n_coef) == 16) return launch_kp<16>(v, M, Phi, ldphi, tau, mask, ldw, st);
-  return launch_kp<32>(v, M, Phi, ldphi, tau, mask, ldw, st);
+                                 float tau, uint32_t* mask, int64_t ldw, int* tile_counter, cudaStream_t st) {
+  if (fg_kp(M.n_coef) == 16) return launch_kp<16>(v, M, Phi, ldphi, tau, mask, ldw, tile_counter, st);
+  return launch_kp<32>(v, M, Phi, ldphi, tau, mask, ldw, tile_counter, st);
 }
 
 }  // namespace cdmd

@@ -15,6 +15,7 @@ struct cdmd_handle_s {
   cusolverDnParams_t params = nullptr;
   uint16_t* gauss_table = nullptr;   // device, 65536 bf16 bit patterns (immutable)
   int32_t* host_info = nullptr;      // pinned, 16 words for fit read-back
+  int* sched = nullptr;              // device, tile counters of the persistent kernels (0 modes, 1 foreground)
   std::vector<char> host_ws;         // cuSOLVER host workspace (fit only)
 };
 

@@ -7,7 +7,7 @@
 //       by TMA and kept resident in shared memory;
 //   D = int32 in TMEM (exact: |D| <= (m-1) 255 127 < 2^31), two accumulator
 //       buffers so the epilogue of tile i overlaps the MMAs of tile i+1.
-// Persistent CTAs (one per SM), warp roles: warp 0 TMA producer, warp 1 TMEM
+// Persistent CTAs (one per SM) claiming tiles dynamically (tc::TileQueue), warp roles: warp 0 TMA producer, warp 1 TMEM
 // allocator + single-thread MMA issuer, warps 2-9 epilogue (TMEM -> registers ->
 // exact limb recombination in int64 -> fp32 Phi, coalesced stores).
 // The result is bit-identical to modes.cu's dp4a kernel (both accumulate exactly).
@@ -26,7 +26,7 @@ template <int NT>
 __global__ void __launch_bounds__(320, 1) modes_tc_kernel(
     const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, int64_t n_local,
     int nkb, int stages, int kpad, int k_eff, const double* __restrict__ scale, float* __restrict__ Phi,
-    int64_t ldphi, int num_tiles, uint32_t tmem_cols) {
+    int64_t ldphi, int num_tiles, uint32_t tmem_cols, int* __restrict__ tile_counter) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];   // 1024-B aligned: SWIZZLE_128B atoms
   uint8_t* smem = smem_raw;                                  // (keeps the shared address space visible)
   uint8_t* sB = smem;                                   // NT x (nkb * 128) bytes, panel-major
@@ -38,6 +38,9 @@ __global__ void __launch_bounds__(320, 1) modes_tc_kernel(
   uint64_t* bfull = tempty + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bfull + 1);
   __shared__ float sScale[256];
+  __shared__ int tq_id[tc::TQ_N];
+  __shared__ uint64_t tq_bar[2 * tc::TQ_N];
+  const tc::TileQueue tq{tq_id, tq_bar, tq_bar + tc::TQ_N};
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int c = threadIdx.x; c < kpad; c += blockDim.x) sScale[c] = (float)scale[c];
@@ -51,6 +54,7 @@ __global__ void __launch_bounds__(320, 1) modes_tc_kernel(
     tc::mbar_init(&tempty[0], 8);
     tc::mbar_init(&tempty[1], 8);
     tc::mbar_init(bfull, 1);
+    tc::tq_init(tq, 1 + 8);   // MMA issuer + 8 epilogue warps
     tc::fence_mbar_init();
     tc::tma_prefetch(&mapA);
     tc::tma_prefetch(&mapB);
@@ -67,7 +71,9 @@ __global__ void __launch_bounds__(320, 1) modes_tc_kernel(
       for (int kb = 0; kb < nkb; ++kb) tc::tma_load_2d(sB + (size_t)kb * NT * TC_BK, &mapB, bfull, kb * TC_BK, 0);
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      for (int k = 0;; ++k) {
+        const int tile = tc::tq_publish(tq, k, tile_counter, num_tiles);
+        if (tile < 0) break;
         for (int kb = 0; kb < nkb; ++kb) {
           tc::mbar_wait(&empty[stage], phase ^ 1u);
           tc::mbar_arrive_expect_tx(&full[stage], TC_STAGE);
@@ -86,7 +92,8 @@ __global__ void __launch_bounds__(320, 1) modes_tc_kernel(
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+      for (;; ++it) {
+        if (tc::tq_take(tq, it) < 0) break;
         const int acc = it & 1;
         const uint32_t acc_phase = (uint32_t)(it >> 1) & 1u;
         tc::mbar_wait(&tempty[acc], acc_phase ^ 1u);
@@ -116,7 +123,9 @@ __global__ void __launch_bounds__(320, 1) modes_tc_kernel(
     const int cpar = (warp - 2) >> 2;      // which 16-column chunks (0: even, 1: odd)
     const int row = q * 32 + lane;         // pixel within the tile
     int it = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+    for (;; ++it) {
+      const int tile = tc::tq_take_warp(tq, it);
+      if (tile < 0) break;
       const int acc = it & 1;
       const uint32_t acc_phase = (uint32_t)(it >> 1) & 1u;
       tc::mbar_wait(&tfull[acc], acc_phase);
@@ -178,7 +187,7 @@ static bool make_map_u8(CUtensorMap* map, const void* base, uint64_t d0, uint64_
 
 template <int NT>
 static cudaError_t launch_nt(const cdmd_video& v, const cdmd_model& M, float* Phi, int64_t ldphi,
-                             cudaStream_t st) {
+                             int* tile_counter, cudaStream_t st) {
   const int64_t n1 = v.m - 1;
   const int nkb = (int)(M.mpad / TC_BK);
   CUtensorMap mapA, mapB;
@@ -187,7 +196,7 @@ static cudaError_t launch_nt(const cdmd_video& v, const cdmd_model& M, float* Ph
   if (!make_map_u8(&mapB, M.Mq, (uint64_t)M.mpad, (uint64_t)NT, (uint64_t)M.mpad, TC_BK, NT))
     return cudaErrorInvalidValue;
   const size_t bbytes = (size_t)NT * nkb * TC_BK;
-  const size_t max_smem = 227 * 1024;
+  const size_t max_smem = 225 * 1024;   // 227 KB less the static shared arrays (sScale, tile queue)
   const size_t fixed = bbytes + 1024 + 512;
   int stages = (int)((max_smem - fixed) / TC_STAGE);
   if (stages > 8) stages = 8;
@@ -201,26 +210,28 @@ static cudaError_t launch_nt(const cdmd_video& v, const cdmd_model& M, float* Ph
   const int grid = num_tiles < sms ? num_tiles : sms;
   uint32_t cols = 32;
   while (cols < 2u * NT) cols <<= 1;
+  e = cudaMemsetAsync(tile_counter, 0, sizeof(int), st);
+  if (e != cudaSuccess) return e;
   note_launch();
   modes_tc_kernel<NT><<<grid, 320, smem, st>>>(mapA, mapB, v.n_local, nkb, stages, M.kpad, M.k_eff,
-                                                M.Mq_scale, Phi, ldphi, num_tiles, cols);
+                                                M.Mq_scale, Phi, ldphi, num_tiles, cols, tile_counter);
   return cudaGetLastError();
 }
 
 bool modes_tc_supported(const cdmd_model& M) {
   const int NT = M.kpad * CDMD_LIMBS;
   if (NT > 256 || (NT % 64) != 0) return false;
-  return (size_t)NT * M.mpad + 2 * TC_STAGE + 2048 <= 227 * 1024;
+  return (size_t)NT * M.mpad + 2 * TC_STAGE + 2048 <= 225 * 1024;
 }
 
 cudaError_t launch_modes_tc(const cdmd_video& v, const cdmd_model& M, float* Phi, int64_t ldphi,
-                            cudaStream_t st) {
+                            int* tile_counter, cudaStream_t st) {
   if (!modes_tc_supported(M) || !encode_fn()) return launch_modes_simt(v, M, Phi, ldphi, st);
   switch (M.kpad * CDMD_LIMBS) {
-    case 64: return launch_nt<64>(v, M, Phi, ldphi, st);
-    case 128: return launch_nt<128>(v, M, Phi, ldphi, st);
-    case 192: return launch_nt<192>(v, M, Phi, ldphi, st);
-    case 256: return launch_nt<256>(v, M, Phi, ldphi, st);
+    case 64: return launch_nt<64>(v, M, Phi, ldphi, tile_counter, st);
+    case 128: return launch_nt<128>(v, M, Phi, ldphi, tile_counter, st);
+    case 192: return launch_nt<192>(v, M, Phi, ldphi, tile_counter, st);
+    case 256: return launch_nt<256>(v, M, Phi, ldphi, tile_counter, st);
   }
   return launch_modes_simt(v, M, Phi, ldphi, st);
 }

@@ -105,6 +105,52 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
 }
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
+// ------------------------------------------------- dynamic persistent tile schedule
+// A persistent CTA claims tiles from a global counter instead of a fixed stride, so
+// a CTA that starts late (its SM still held by another stream's kernel) just claims
+// fewer tiles.  One producer thread claims and publishes tile ids through a ring in
+// shared memory; every consumer role reads the same sequence and releases each slot
+// once (the last id of the sequence is -1).
+constexpr int TQ_N = 8;
+struct TileQueue {
+  int* id;          // TQ_N ids
+  uint64_t* full;   // TQ_N barriers, count 1
+  uint64_t* empty;  // TQ_N barriers, count = number of consumer arrivals
+};
+__device__ __forceinline__ void tq_init(const TileQueue& q, uint32_t consumers) {
+  for (int s = 0; s < TQ_N; ++s) {
+    mbar_init(&q.full[s], 1);
+    mbar_init(&q.empty[s], consumers);
+  }
+}
+// producer: claim the next tile (-1 once the counter passes num_tiles) and publish it as entry k
+__device__ __forceinline__ int tq_publish(const TileQueue& q, int k, int* counter, int num_tiles) {
+  const int t0 = atomicAdd(counter, 1);
+  const int t = t0 < num_tiles ? t0 : -1;
+  const int s = k % TQ_N;
+  mbar_wait(&q.empty[s], ((uint32_t)(k / TQ_N) & 1u) ^ 1u);
+  q.id[s] = t;
+  mbar_arrive(&q.full[s]);
+  return t;
+}
+// consumer, one thread: read entry k and release it
+__device__ __forceinline__ int tq_take(const TileQueue& q, int k) {
+  const int s = k % TQ_N;
+  mbar_wait(&q.full[s], (uint32_t)(k / TQ_N) & 1u);
+  const int t = q.id[s];
+  mbar_arrive(&q.empty[s]);
+  return t;
+}
+// consumer, whole warp: every lane reads entry k, lane 0 releases it
+__device__ __forceinline__ int tq_take_warp(const TileQueue& q, int k) {
+  const int s = k % TQ_N;
+  mbar_wait(&q.full[s], (uint32_t)(k / TQ_N) & 1u);
+  const int t = q.id[s];
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) mbar_arrive(&q.empty[s]);
+  return t;
+}
+
 // ------------------------------------------------------------- descriptors
 // Shared-memory matrix descriptor (tcgen05): start, leading / stride byte
 // offsets (>> 4), version 1 (sm_100), layout SWIZZLE_128B (= 2 at bits 61-63).
