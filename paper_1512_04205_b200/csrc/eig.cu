@@ -14,6 +14,7 @@
 // lambda_j = (wr, wi) with each complex pair listed (+im, -im) consecutively and
 // exactly conjugate, VR column j = Re v, column j+1 = Im v for the pair.
 #include <math.h>
+#include <cstdio>
 
 #include "common.cuh"
 
@@ -47,12 +48,33 @@ __device__ __forceinline__ void cdiv(double xr, double xi, double yr, double yi,
   }
 }
 
+// reciprocal and reciprocal square root: hardware approximation + two Newton steps
+// (about 1 ulp; the Francis step's scalar chain is latency-bound, IEEE division and
+// sqrt are several times longer)
+__device__ __forceinline__ double rcp_nr(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+__device__ __forceinline__ double rsqrt_nr(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double h = 0.5 * x;
+  y = y * fma(-h * y, y, 1.5);
+  return y * fma(-h * y, y, 1.5);
+}
+
 }  // namespace
 
 // A: k x k column-major (device); outputs W (2k: re, im), VR (k x k column-major).
+// par3: shared memory holds 32 lane-private vector pairs (2 nn doubles each) and the
+// eigenvectors of the Schur form are back-substituted one per lane.
 __global__ void __launch_bounds__(32) hqr_eig_kernel(int nn, const double* __restrict__ A,
                                                     double* __restrict__ W, double* __restrict__ VR,
-                                                    int* __restrict__ info) {
+                                                    int* __restrict__ info, int par3) {
   extern __shared__ double sm[];
   const int ld = nn + 1;
   double* H = sm;                 // nn x ld, row-major: H[i * ld + j]
@@ -60,6 +82,7 @@ __global__ void __launch_bounds__(32) hqr_eig_kernel(int nn, const double* __res
   double* ort = V + nn * ld;      // nn
   double* d = ort + nn;           // nn real parts
   double* e = d + nn;             // nn imaginary parts
+  double* xbuf = e + nn;          // par3: [32][2 nn] lane-private (Re, Im) vectors
   const Warp wp{(int)(threadIdx.x & 31)};
   const int lane = wp.lane;
 #define Hx(i, j) H[(i) * ld + (j)]
@@ -71,6 +94,13 @@ __global__ void __launch_bounds__(32) hqr_eig_kernel(int nn, const double* __res
   }
   wp.sync();
   const int low = 0, high = nn - 1;
+#ifdef CDMD_EIG_PROF
+  long long tp[6];
+  tp[0] = clock64();
+#define EIG_T(i) tp[i] = clock64();
+#else
+#define EIG_T(i)
+#endif
   // ------------------------------------------------ 1. orthes (Hessenberg)
   for (int m = low + 1; m <= high - 1; ++m) {
     double scale = 0.0;
@@ -114,6 +144,7 @@ __global__ void __launch_bounds__(32) hqr_eig_kernel(int nn, const double* __res
       wp.sync();
     }
   }
+  EIG_T(1)
   // ortran: accumulate the transformations into V
   for (int m = high - 1; m >= low + 1; --m) {
     if (Hx(m, m - 1) != 0.0) {
@@ -128,6 +159,7 @@ __global__ void __launch_bounds__(32) hqr_eig_kernel(int nn, const double* __res
       wp.sync();
     }
   }
+  EIG_T(2)
   // ------------------------------------------------------- 2. hqr2 (Schur)
   int n = nn - 1;
   const double eps = 0x1p-52;
@@ -138,7 +170,16 @@ __global__ void __launch_bounds__(32) hqr_eig_kernel(int nn, const double* __res
     for (int j = (i > 0 ? i - 1 : 0); j < nn; ++j) norm += fabs(Hx(i, j));
   norm = wp.sum(norm);
   int iter = 0, total_iter = 0, fail = 0;
+#ifdef CDMD_EIG_PROF
+  long long qa = 0, qb = 0, qc = 0, qsteps = 0, t_a = 0;
+#define QT(acc) { const long long t_ = clock64(); acc += t_ - t_a; t_a = t_; }
+#else
+#define QT(acc)
+#endif
   while (n >= low) {
+#ifdef CDMD_EIG_PROF
+    t_a = clock64();
+#endif
     int l = n;
     while (l > low) {
       s = fabs(Hx(l - 1, l - 1)) + fabs(Hx(l, l));
@@ -218,6 +259,7 @@ __global__ void __launch_bounds__(32) hqr_eig_kernel(int nn, const double* __res
       n = n - 2;
       iter = 0;
     } else {  // no convergence yet: form shift
+      QT(qa)
       x = Hx(n, n);
       y = 0.0;
       w = 0.0;
@@ -254,23 +296,32 @@ __global__ void __launch_bounds__(32) hqr_eig_kernel(int nn, const double* __res
         break;
       }
       int m = n - 2;  // look for two consecutive small sub-diagonal elements
+      // (p, q, r) are carried multiplied by h = H(m+1, m): the test below is homogeneous
+      // in them and the first reflector is scale-invariant, so no divisions in the loop
       while (m >= l) {
         z = Hx(m, m);
         r = x - z;
         s = y - z;
-        p = (r * s - w) / Hx(m + 1, m) + Hx(m, m + 1);
-        q = Hx(m + 1, m + 1) - z - r - s;
-        r = Hx(m + 2, m + 1);
-        s = fabs(p) + fabs(q) + fabs(r);
-        p = p / s;
-        q = q / s;
-        r = r / s;
+        const double h = Hx(m + 1, m);
+        p = (r * s - w) + Hx(m, m + 1) * h;
+        q = (Hx(m + 1, m + 1) - z - r - s) * h;
+        r = Hx(m + 2, m + 1) * h;
         if (m == l) break;
         if (fabs(Hx(m, m - 1)) * (fabs(q) + fabs(r)) <
             eps * (fabs(p) * (fabs(Hx(m - 1, m - 1)) + fabs(z) + fabs(Hx(m + 1, m + 1)))))
           break;
         m--;
       }
+      {
+        const double sc = fabs(p) + fabs(q) + fabs(r);
+        if (sc != 0.0) {
+          const double isc = rcp_nr(sc);
+          p *= isc;
+          q *= isc;
+          r *= isc;
+        }
+      }
+      QT(qb)
       wp.sync();
       for (int i = m + 2 + lane; i <= n; i += 32) {
         Hx(i, i - 2) = 0.0;
@@ -278,6 +329,9 @@ __global__ void __launch_bounds__(32) hqr_eig_kernel(int nn, const double* __res
       }
       wp.sync();
       for (int kk = m; kk <= n - 1; ++kk) {  // double QR step, rows l:n, columns m:n
+#ifdef CDMD_EIG_PROF
+        ++qsteps;
+#endif
         const bool notlast = (kk != n - 1);
         if (kk != m) {
           p = Hx(kk, kk - 1);
@@ -285,12 +339,17 @@ __global__ void __launch_bounds__(32) hqr_eig_kernel(int nn, const double* __res
           r = notlast ? Hx(kk + 2, kk - 1) : 0.0;
           x = fabs(p) + fabs(q) + fabs(r);
           if (x == 0.0) continue;
-          const double ix = 1.0 / x;  // one division, three multiplies
-          p = p * ix;
-          q = q * ix;
-          r = r * ix;
+          if (x < 1e-140 || x > 1e140) {   // EISPACK's scaling, only where squares could under/overflow
+            const double ix = 1.0 / x;
+            p = p * ix;
+            q = q * ix;
+            r = r * ix;
+          } else {
+            x = 1.0;                        // the reflector is scale-invariant; s below is unscaled
+          }
         }
-        s = sqrt(p * p + q * q + r * r);
+        const double ss = p * p + q * q + r * r;
+        s = ss > 0.0 ? ss * rsqrt_nr(ss) : 0.0;
         if (p < 0) s = -s;
         if (s != 0) {
           double newsub = 0.0;
@@ -306,7 +365,7 @@ __global__ void __launch_bounds__(32) hqr_eig_kernel(int nn, const double* __res
           if (setsub && lane == 0) Hx(kk, kk - 1) = newsub;
           wp.sync();
           p = p + s;
-          const double is = 1.0 / s, ip = 1.0 / p;
+          const double is = rcp_nr(s), ip = rcp_nr(p);
           x = p * is;
           y = q * is;
           z = r * is;
@@ -323,35 +382,157 @@ __global__ void __launch_bounds__(32) hqr_eig_kernel(int nn, const double* __res
           }
           wp.sync();
           const int imax = n < kk + 3 ? n : kk + 3;
-          for (int i = lane; i <= imax; i += 32) {  // column modification
-            double pp = x * Hx(i, kk) + y * Hx(i, kk + 1);
-            if (notlast) {
-              pp = pp + z * Hx(i, kk + 2);
-              Hx(i, kk + 2) = Hx(i, kk + 2) - pp * r;
+          const double zn = notlast ? z : 0.0;
+          // column modification of H (rows 0..imax) and accumulation into V (all rows),
+          // as one loop: with r = 0 the third column is left unchanged when last
+          for (int i = lane; i <= high; i += 32) {
+            double* hr = &Hx(i, kk);
+            double* vr = &Vx(i, kk);
+            const double v0 = vr[0], v1 = vr[1], v2 = notlast ? vr[2] : 0.0;
+            const double pv = x * v0 + y * v1 + zn * v2;
+            vr[0] = v0 - pv;
+            vr[1] = v1 - pv * q;
+            if (notlast) vr[2] = v2 - pv * r;
+            if (i <= imax) {
+              const double h0 = hr[0], h1 = hr[1], h2 = notlast ? hr[2] : 0.0;
+              const double ph = x * h0 + y * h1 + zn * h2;
+              hr[0] = h0 - ph;
+              hr[1] = h1 - ph * q;
+              if (notlast) hr[2] = h2 - ph * r;
             }
-            Hx(i, kk) = Hx(i, kk) - pp;
-            Hx(i, kk + 1) = Hx(i, kk + 1) - pp * q;
-          }
-          for (int i = low + lane; i <= high; i += 32) {  // accumulate transformations
-            double pp = x * Vx(i, kk) + y * Vx(i, kk + 1);
-            if (notlast) {
-              pp = pp + z * Vx(i, kk + 2);
-              Vx(i, kk + 2) = Vx(i, kk + 2) - pp * r;
-            }
-            Vx(i, kk) = Vx(i, kk) - pp;
-            Vx(i, kk + 1) = Vx(i, kk + 1) - pp * q;
           }
           wp.sync();
         }
       }
+      QT(qc)
     }
   }
+#ifdef CDMD_EIG_PROF
+  if (lane == 0) printf("EIGQR deflate+1/2-root %lld shift+msearch %lld sweep(+rest) %lld steps %lld\n", qa, qb, qc, qsteps);
+#endif
   if (fail) {
     if (lane == 0) *info = 1;
     return;
   }
+  EIG_T(3)
   // ------------------------------------- 3. eigenvectors of the Schur form
-  if (norm != 0.0) {
+  if (norm != 0.0 && par3) {
+    // One eigenvector (real) or pair (complex) per lane, 32 at a time in decreasing n:
+    // a round reads only columns <= its own n of the Schur form, so the lanes solve
+    // into private buffers and write their columns back after the round.
+    int nitems = 0;
+    for (int c = nn - 1; c >= 0; --c)
+      if (e[c] <= 0.0) ++nitems;
+    double* xr = xbuf + (size_t)lane * 2 * nn;
+    double* xi = xr + nn;
+    for (int r0 = 0; r0 < nitems; r0 += 32) {
+      // this lane's item: the (r0 + lane)-th index c (descending) with e[c] <= 0
+      int my = -1;
+      {
+        int cnt = 0;
+        for (int c = nn - 1; c >= 0; --c)
+          if (e[c] <= 0.0) {
+            if (cnt == r0 + lane) { my = c; break; }
+            ++cnt;
+          }
+      }
+      if (my >= 0) {
+        const int n3 = my;
+        const double p3 = d[n3], q3 = e[n3];
+        double z3 = 0.0, r3 = 0.0, s3 = 0.0;
+        if (q3 == 0.0) {   // real vector
+          int l = n3;
+          xr[n3] = 1.0;
+          for (int i = n3 - 1; i >= 0; i--) {
+            const double w3 = Hx(i, i) - p3;
+            double rr = 0.0;
+            for (int j = l; j <= n3; ++j) rr += Hx(i, j) * xr[j];
+            if (e[i] < 0.0) {
+              z3 = w3;
+              s3 = rr;
+            } else {
+              l = i;
+              if (e[i] == 0.0) {
+                xr[i] = (w3 != 0.0) ? -rr / w3 : -rr / (eps * norm);
+              } else {   // solve real equations
+                const double x3 = Hx(i, i + 1), y3 = Hx(i + 1, i);
+                const double qq = (d[i] - p3) * (d[i] - p3) + e[i] * e[i];
+                const double t3 = (x3 * s3 - z3 * rr) / qq;
+                xr[i] = t3;
+                xr[i + 1] = (fabs(x3) > fabs(z3)) ? (-rr - w3 * t3) / x3 : (-s3 - y3 * t3) / z3;
+              }
+              const double t3 = fabs(xr[i]);   // overflow control
+              if ((eps * t3) * t3 > 1)
+                for (int j = i; j <= n3; ++j) xr[j] /= t3;
+            }
+          }
+        } else {   // complex vector (columns n-1 = Re, n = Im)
+          int l = n3 - 1;
+          if (fabs(Hx(n3, n3 - 1)) > fabs(Hx(n3 - 1, n3))) {
+            xr[n3 - 1] = q3 / Hx(n3, n3 - 1);
+            xi[n3 - 1] = -(Hx(n3, n3) - p3) / Hx(n3, n3 - 1);
+          } else {
+            cdiv(0.0, -Hx(n3 - 1, n3), Hx(n3 - 1, n3 - 1) - p3, q3, xr[n3 - 1], xi[n3 - 1]);
+          }
+          xr[n3] = 0.0;
+          xi[n3] = 1.0;
+          for (int i = n3 - 2; i >= 0; i--) {
+            double ra = 0.0, sa = 0.0;
+            for (int j = l; j <= n3; ++j) {
+              ra += Hx(i, j) * xr[j];
+              sa += Hx(i, j) * xi[j];
+            }
+            const double w3 = Hx(i, i) - p3;
+            if (e[i] < 0.0) {
+              z3 = w3;
+              r3 = ra;
+              s3 = sa;
+            } else {
+              l = i;
+              if (e[i] == 0) {
+                cdiv(-ra, -sa, w3, q3, xr[i], xi[i]);
+              } else {   // solve complex equations
+                const double x3 = Hx(i, i + 1), y3 = Hx(i + 1, i);
+                double vr = (d[i] - p3) * (d[i] - p3) + e[i] * e[i] - q3 * q3;
+                const double vi = (d[i] - p3) * 2.0 * q3;
+                if (vr == 0.0 && vi == 0.0)
+                  vr = eps * norm * (fabs(w3) + fabs(q3) + fabs(x3) + fabs(y3) + fabs(z3));
+                double c0, c1;
+                cdiv(x3 * r3 - z3 * ra + q3 * sa, x3 * s3 - z3 * sa - q3 * ra, vr, vi, c0, c1);
+                xr[i] = c0;
+                xi[i] = c1;
+                if (fabs(x3) > (fabs(z3) + fabs(q3))) {
+                  xr[i + 1] = (-ra - w3 * c0 + q3 * c1) / x3;
+                  xi[i + 1] = (-sa - w3 * c1 - q3 * c0) / x3;
+                } else {
+                  cdiv(-r3 - y3 * c0, -s3 - y3 * c1, z3, q3, xr[i + 1], xi[i + 1]);
+                }
+              }
+              const double t3 = fmax(fabs(xr[i]), fabs(xi[i]));   // overflow control
+              if ((eps * t3) * t3 > 1)
+                for (int j = i; j <= n3; ++j) {
+                  xr[j] /= t3;
+                  xi[j] /= t3;
+                }
+            }
+          }
+        }
+      }
+      wp.sync();   // every lane of the round has read the Schur form: write the columns
+      if (my >= 0) {
+        if (e[my] == 0.0) {
+          for (int j = 0; j <= my; ++j) Hx(j, my) = xr[j];
+        } else {
+          for (int j = 0; j <= my; ++j) {
+            Hx(j, my - 1) = xr[j];
+            Hx(j, my) = xi[j];
+          }
+          Hx(my, my - 1) = 0.0;
+        }
+      }
+      wp.sync();
+    }
+  } else if (norm != 0.0) {
     for (n = nn - 1; n >= 0; n--) {
       p = d[n];
       q = e[n];
@@ -470,6 +651,9 @@ __global__ void __launch_bounds__(32) hqr_eig_kernel(int nn, const double* __res
         }
       }
     }
+  }
+  if (norm != 0.0) {
+    EIG_T(4)
     // back transformation: V = V * (upper triangular part of H)
     for (int j = nn - 1; j >= low; j--) {
       for (int i = low + lane; i <= high; i += 32) {
@@ -490,18 +674,26 @@ __global__ void __launch_bounds__(32) hqr_eig_kernel(int nn, const double* __res
     VR[idx] = Vx(i, j);
   }
   if (lane == 0) *info = 0;
+#ifdef CDMD_EIG_PROF
+  EIG_T(5)
+  if (lane == 0)
+    printf("EIGPROF n=%d orthes %lld ortran %lld qr %lld (iters %d) backsub %lld backtr+out %lld\n", nn, tp[1] - tp[0],
+           tp[2] - tp[1], tp[3] - tp[2], total_iter, tp[4] - tp[3], tp[5] - tp[4]);
+#endif
 #undef Hx
 #undef Vx
 }
 
 size_t hqr_smem_bytes(int k) { return sizeof(double) * ((size_t)2 * k * (k + 1) + 3 * (size_t)k); }
+static size_t hqr_smem_par3(int k) { return hqr_smem_bytes(k) + sizeof(double) * 64 * (size_t)k; }
 
 cudaError_t launch_hqr_eig(int k, const double* A, double* W, double* VR, int* info, cudaStream_t st) {
-  const size_t smem = hqr_smem_bytes(k);
+  const int par3 = hqr_smem_par3(k) <= 226 * 1024;
+  const size_t smem = par3 ? hqr_smem_par3(k) : hqr_smem_bytes(k);
   cudaError_t e = cudaFuncSetAttribute(hqr_eig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   note_launch();
-  hqr_eig_kernel<<<1, 32, smem, st>>>(k, A, W, VR, info);
+  hqr_eig_kernel<<<1, 32, smem, st>>>(k, A, W, VR, info, par3);
   return cudaGetLastError();
 }
 
