@@ -19,12 +19,16 @@ def launches(path):
     # split into steps at each sparse/spixel/dense sketch launch of ours
     starts = [i for i, (k, _) in enumerate(seq) if k.startswith(("cdmd::sparse_rows", "cdmd::spixel_rows",
                                                                  "cdmd::sketch_rademacher", "cdmd::sketch_gaussian"))]
+    # a step also starts at a dense sketch only when no rows kernel precedes it
+    starts = [i for i in starts if not (i > 0 and i - 1 in starts)]
     print(f"# {len(seq)} kernel launches captured (ncu --metrics gpu__time_duration.sum, "
           f"--clock-control none: cold-cache, serialised; compare SHARES)")
-    if len(starts) >= 2:
-        a, b = starts[-2], starts[-1]
+    if len(starts) >= 3:
+        # the second sequential step (bench.py runs its sequential steps before the
+        # streaming lanes, whose launches interleave)
+        a, b = starts[1], starts[2]
         step = seq[a:b]
-        print(f"# last complete step: launches {a}..{b - 1} ({len(step)} launches)")
+        print(f"# second sequential step: launches {a}..{b - 1} ({len(step)} launches)")
     else:
         step = seq[starts[-1]:] if starts else seq
         print(f"# step from the last sketch launch ({len(step)} launches)")
