@@ -208,21 +208,6 @@ __global__ void __cluster_dims__(EH_CL, 1, 1) __launch_bounds__(EH_T, 1)
   if (rank == ((n - 1) % EH_CL) && tid == 0) d[n - 1] = Aloc[eh_off(rank, (n - 1) / EH_CL) + (n - 1)];
 }
 
-// Sturm count: number of eigenvalues of T(d, e) smaller than x
-__device__ int eh_sturm(int n, const double* __restrict__ d, const double* __restrict__ e2, double x,
-                        double pivmin) {
-  int cnt = 0;
-  double q = d[0] - x;
-  if (fabs(q) < pivmin) q = -pivmin;
-  if (q < 0) ++cnt;
-  for (int i = 1; i < n; ++i) {
-    q = d[i] - x - e2[i - 1] / q;
-    if (fabs(q) < pivmin) q = -pivmin;
-    if (q < 0) ++cnt;
-  }
-  return cnt;
-}
-
 // Gershgorin bounds, ||T||, pivmin and e^2 (one block)
 __global__ void eh_prep_kernel(int n, const double* __restrict__ d, const double* __restrict__ e,
                                double* __restrict__ e2, double* __restrict__ bounds) {
@@ -245,8 +230,42 @@ __global__ void eh_prep_kernel(int n, const double* __restrict__ d, const double
   }
 }
 
-// One warp per wanted eigenvalue: 32-point multisection (5 bits per round) on Sturm
-// counts.  The (r+1)-th largest eigenvalue (ascending index n-1-r) goes to lam[k-1-r].
+// reciprocal: hardware approximation + two Newton steps (about 1 ulp; the Sturm
+// recurrence is a chain of dependent divisions, IEEE division is several times longer)
+__device__ __forceinline__ double eh_rcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double t = fma(-x, r, 1.0);
+  r = fma(r, t, r);
+  t = fma(-x, r, 1.0);
+  return fma(r, t, r);
+}
+
+// Sturm counts at EH_NP points at once (independent chains interleave)
+constexpr int EH_NP = 4;
+__device__ __forceinline__ void eh_sturm_multi(int n, const double* __restrict__ d, const double* __restrict__ e2,
+                                               const double (&x)[EH_NP], double pivmin, int (&cnt)[EH_NP]) {
+  double q[EH_NP];
+#pragma unroll
+  for (int u = 0; u < EH_NP; ++u) {
+    q[u] = d[0] - x[u];
+    if (fabs(q[u]) < pivmin) q[u] = -pivmin;
+    cnt[u] = q[u] < 0 ? 1 : 0;
+  }
+  for (int i = 1; i < n; ++i) {
+    const double di = d[i], ei = e2[i - 1];
+#pragma unroll
+    for (int u = 0; u < EH_NP; ++u) {
+      q[u] = (di - x[u]) - ei * eh_rcp(q[u]);
+      if (fabs(q[u]) < pivmin) q[u] = -pivmin;
+      cnt[u] += q[u] < 0 ? 1 : 0;
+    }
+  }
+}
+
+// One warp per wanted eigenvalue: 128-point multisection (7 bits per round; four
+// points per lane) on Sturm counts.  The (r+1)-th largest eigenvalue (ascending
+// index n-1-r) goes to lam[k-1-r].
 __global__ void __launch_bounds__(32) eh_bisect_kernel(int n, int k, const double* __restrict__ d,
                                                        const double* __restrict__ e2,
                                                        const double* __restrict__ bounds,
@@ -257,15 +276,23 @@ __global__ void __launch_bounds__(32) eh_bisect_kernel(int n, int k, const doubl
   double lo = bounds[0], hi = bounds[1];
   const double pivmin = bounds[3];
   const double eps = 2.220446049250313e-16;
+  constexpr int NPT = 32 * EH_NP;   // points per round, at lo + (hi - lo) t / (NPT + 1)
   for (int round = 0; round < 40; ++round) {
     if (hi - lo <= 2.0 * eps * fmax(fabs(lo), fabs(hi)) + pivmin) break;
-    const double x = lo + (hi - lo) * (double)(lane + 1) / 33.0;
-    const int c = eh_sturm(n, d, e2, x, pivmin);
-    // points with count <= idx lie below the eigenvalue
-    const unsigned below = __ballot_sync(0xffffffffu, c <= idx);
-    const int nb = __popc(below);   // counts are monotone: the first nb points are below
-    const double nlo = nb > 0 ? lo + (hi - lo) * (double)nb / 33.0 : lo;
-    const double nhi = nb < 32 ? lo + (hi - lo) * (double)(nb + 1) / 33.0 : hi;
+    double x[EH_NP];
+    int c[EH_NP];
+#pragma unroll
+    for (int u = 0; u < EH_NP; ++u) x[u] = lo + (hi - lo) * (double)(EH_NP * lane + u + 1) / (double)(NPT + 1);
+    eh_sturm_multi(n, d, e2, x, pivmin, c);
+    // points with count <= idx lie below the eigenvalue; counts are monotone in the
+    // point index, so the number below is the total over lanes and chains
+    int nbl = 0;
+#pragma unroll
+    for (int u = 0; u < EH_NP; ++u) nbl += c[u] <= idx ? 1 : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) nbl += __shfl_xor_sync(0xffffffffu, nbl, o);
+    const double nlo = nbl > 0 ? lo + (hi - lo) * (double)nbl / (double)(NPT + 1) : lo;
+    const double nhi = nbl < NPT ? lo + (hi - lo) * (double)(nbl + 1) / (double)(NPT + 1) : hi;
     lo = nlo;
     hi = nhi;
   }
@@ -403,50 +430,60 @@ __global__ void __launch_bounds__(32) eh_invit_kernel(int n, int k, const double
   if (blockIdx.x == 0 && lane == 0) *info = 0;
 }
 
-// Z <- Q Z, Q = H_0 H_1 ... H_{n-2}: blocks of 16 columns (one warp each, the column in
-// shared memory); reflectors staged through shared memory 16 at a time.
-constexpr int EH_RB = 16;
-__global__ void __launch_bounds__(512) eh_backtransform_kernel(int n, int k, const double* __restrict__ V,
+// Z <- Q Z, Q = H_0 H_1 ... H_{n-3} (applied last to first): one warp per column of
+// Z, the column in registers (element i = lane + 32 t), the next reflector's
+// entries loaded while the current one is applied.
+constexpr int EH_ZR = (EH_NMAX + 31) / 32;
+__global__ void __launch_bounds__(128) eh_backtransform_kernel(int n, int k, const double* __restrict__ V,
                                                                const double* __restrict__ tau,
                                                                double* __restrict__ Z) {
-  extern __shared__ double bsm[];
-  double* zs = bsm;                       // [16][n]
-  double* vs = zs + 16 * (size_t)n;       // [EH_RB][n]
-  __shared__ double ts[EH_RB];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int col = blockIdx.x * 16 + warp;
-  for (int i = threadIdx.x; i < 16 * n; i += blockDim.x) {
-    const int cc = blockIdx.x * 16 + i / n;
-    zs[i] = cc < k ? Z[(int64_t)cc * n + i % n] : 0.0;
+  const int lane = threadIdx.x & 31;
+  const int col = blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (col >= k) return;
+  double z[EH_ZR], vn[EH_ZR];
+  double* zc = Z + (int64_t)col * n;
+#pragma unroll
+  for (int t = 0; t < EH_ZR; ++t) {
+    const int i = lane + 32 * t;
+    z[t] = i < n ? zc[i] : 0.0;
   }
-  for (int jb = n - 2; jb >= 0; jb -= EH_RB) {
-    const int j0 = jb - EH_RB + 1 > 0 ? jb - EH_RB + 1 : 0;
-    __syncthreads();
-    for (int idx = threadIdx.x; idx < (jb - j0 + 1) * n; idx += blockDim.x) {
-      const int jj = j0 + idx / n, i = idx % n;
-      vs[(jj - j0) * n + i] = i > jj ? V[(int64_t)jj * n + i] : 0.0;
+  auto load_v = [&](int j) {
+#pragma unroll
+    for (int t = 0; t < EH_ZR; ++t) {
+      const int i = lane + 32 * t;
+      vn[t] = (j >= 0 && i > j && i < n) ? __ldg(V + (int64_t)j * n + i) : 0.0;
     }
-    if (threadIdx.x < jb - j0 + 1) ts[threadIdx.x] = tau[j0 + threadIdx.x];
-    __syncthreads();
-    if (col < k) {
-      double* z = zs + warp * n;
-      for (int j = jb; j >= j0; --j) {
-        const double tj = ts[j - j0];
-        if (tj == 0.0) continue;
-        const double* vj = vs + (j - j0) * n;
-        double sacc = 0.0;
-        for (int i = j + 1 + lane; i < n; i += 32) sacc += vj[i] * z[i];
-        for (int o = 16; o > 0; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
-        sacc *= tj;
-        for (int i = j + 1 + lane; i < n; i += 32) z[i] -= sacc * vj[i];
-        __syncwarp();
-      }
+  };
+  int j = n - 2;
+  load_v(j);
+  for (; j >= 0; --j) {
+    double v[EH_ZR];
+#pragma unroll
+    for (int t = 0; t < EH_ZR; ++t) v[t] = vn[t];
+    const double tj = __ldg(tau + j);
+    load_v(j - 1);
+    if (j >= 4 && 16 * lane < n) {   // reflector j - 4 into L1: one 128-B line per lane
+      const double* pf = V + (int64_t)(j - 4) * n + 16 * lane;
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(pf));
     }
+    if (tj == 0.0) continue;
+    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+    for (int t = 0; t < EH_ZR; t += 2) {
+      s0 = fma(v[t], z[t], s0);
+      if (t + 1 < EH_ZR) s1 = fma(v[t + 1], z[t + 1], s1);
+    }
+    double sacc = s0 + s1;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
+    sacc *= tj;
+#pragma unroll
+    for (int t = 0; t < EH_ZR; ++t) z[t] = fma(-sacc, v[t], z[t]);
   }
-  __syncthreads();
-  for (int i = threadIdx.x; i < 16 * n; i += blockDim.x) {
-    const int cc = blockIdx.x * 16 + i / n;
-    if (cc < k) Z[(int64_t)cc * n + i % n] = zs[i];
+#pragma unroll
+  for (int t = 0; t < EH_ZR; ++t) {
+    const int i = lane + 32 * t;
+    if (i < n) zc[i] = z[t];
   }
 }
 
@@ -489,11 +526,8 @@ cudaError_t launch_eh(int n, int k, const double* G, int64_t ldg, double* lam, d
   err = cudaFuncSetAttribute(eh_invit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
   if (err != cudaSuccess) return err;
   eh_invit_kernel<<<(unsigned)k, 32, smem2, st>>>(n, k, d, e, bounds, lam, Zout, info);
-  const size_t smem3 = sizeof(double) * (16 + EH_RB) * (size_t)n;
-  err = cudaFuncSetAttribute(eh_backtransform_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3);
-  if (err != cudaSuccess) return err;
   note_launch();
-  eh_backtransform_kernel<<<(unsigned)ceil_div(k, 16), 512, smem3, st>>>(n, k, V, tau, Zout);
+  eh_backtransform_kernel<<<(unsigned)ceil_div(k, 4), 128, 0, st>>>(n, k, V, tau, Zout);
   return cudaGetLastError();
 }
 
