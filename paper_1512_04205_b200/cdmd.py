@@ -326,13 +326,18 @@ class Streaming:
     def __init__(self, device, n_total, n_local, m, kind, p, k, K, lanes=4, s=0.0, seed=0, pix0=0, dt=1.0):
         import threading
         self.lanes = []
+        lo, hi = torch.cuda.Stream.priority_range()
         for _ in range(lanes):
             h = Handle(device)
             st = torch.cuda.Stream(device=device)
+            # the small solve runs on a high-priority stream of its own: its kernels (the
+            # 8-CTA tridiagonalisation cluster above all) get SMs ahead of the next
+            # lane's full-resolution pass instead of waiting behind it
+            st_fit = torch.cuda.Stream(device=device, priority=hi)
             with torch.cuda.stream(st):
                 pipe = Pipeline(h, n_total, n_local, m, kind, p, k, K, s=s, seed=seed, pix0=pix0,
                                 device=f"cuda:{device}", dt=dt)
-            self.lanes.append((h, st, pipe))
+            self.lanes.append((h, st, st_fit, pipe))
         self._cv = threading.Condition()
         self._next_ar = 0
 
@@ -352,7 +357,7 @@ class Streaming:
         ends = [None] * L
 
         def lane_work(li):
-            h, st, pipe = self.lanes[li]
+            h, st, st_fit, pipe = self.lanes[li]
             with torch.cuda.stream(st):
                 if start_event is not None:
                     st.wait_event(start_event)
@@ -361,7 +366,9 @@ class Streaming:
                     pipe.sketch(X, st)
                     if allreduce is not None:
                         self._ordered_allreduce(b, allreduce, pipe.Y)
-                    pipe.fit(st)
+                    st_fit.wait_stream(st)
+                    pipe.fit(st_fit)
+                    st.wait_stream(st_fit)
                     pipe.modes(X, st)
                     pipe.foreground(X, tau, mode, st)
                 ev = torch.cuda.Event(enable_timing=True)

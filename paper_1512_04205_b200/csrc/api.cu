@@ -1,3 +1,4 @@
+#include <cstdlib>
 // api.cu — the C ABI of libcdmd (include/cdmd.h): host-side validation, handle
 // state, workspace carving and kernel launches.  No torch types cross this
 // boundary; the Python binding (paper_1512_04205_b200/cdmd.py) only marshals
@@ -12,6 +13,17 @@
 using namespace cdmd;
 
 namespace cdmd {
+int persistent_ctas(int sms) {
+  static int reserve = -1;
+  if (reserve < 0) {
+    const char* e = getenv("CDMD_PERSIST_RESERVE");
+    reserve = e ? atoi(e) : 0;
+    if (reserve < 0) reserve = 0;
+  }
+  const int g = sms - reserve;
+  return g < 1 ? 1 : g;
+}
+
 size_t hqr_smem_bytes(int k);
 cudaError_t launch_hqr_eig(int k, const double* A, double* W, double* VR, int* info, cudaStream_t st);
 }  // namespace cdmd

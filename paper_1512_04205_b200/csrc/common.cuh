@@ -20,6 +20,10 @@ inline std::atomic<uint64_t>& launch_counter() {
 }
 inline void note_launch() { launch_counter().fetch_add(1, std::memory_order_relaxed); }
 
+// CTAs of the persistent full-resolution kernels (modes, foreground): all SMs, or
+// fewer with CDMD_PERSIST_RESERVE=R (R SMs left to other streams' small solves)
+int persistent_ctas(int sms);
+
 
 // ---------------------------------------------------------------- Philox4x32-10
 // Salmon et al. SC'11 (the generator DESIGN.md §3.1 fixes for C): per round

@@ -368,7 +368,8 @@ static cudaError_t launch_kp(const cdmd_video& v, const cdmd_model& M, const flo
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int num_tiles = (int)ceil_div(v.n_local, FG_BN);
-  const int grid = num_tiles < sms ? num_tiles : sms;
+  const int pc = persistent_ctas(sms);
+  const int grid = num_tiles < pc ? num_tiles : pc;
   e = cudaMemsetAsync(tile_counter, 0, sizeof(int), st);
   if (e != cudaSuccess) return e;
   note_launch();

@@ -207,7 +207,8 @@ static cudaError_t launch_nt(const cdmd_video& v, const cdmd_model& M, float* Ph
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int num_tiles = (int)ceil_div(v.n_local, TC_BM);
-  const int grid = num_tiles < sms ? num_tiles : sms;
+  const int pc = persistent_ctas(sms);
+  const int grid = num_tiles < pc ? num_tiles : pc;
   uint32_t cols = 32;
   while (cols < 2u * NT) cols <<= 1;
   e = cudaMemsetAsync(tile_counter, 0, sizeof(int), st);
