@@ -69,21 +69,24 @@ __device__ __forceinline__ unsigned long long fsub2(unsigned long long a, unsign
 
 // 32 mask bits of one frame: pixels of 8 byte-words xw (4 pixels each) against 32
 // background values L; bit i = |x_i - L_i| > tau.  The uint8 pixel becomes an exact
-// float through 2^23 + x (byte permute into the mantissa), subtractions run as
-// packed f32x2 pairs.
+// float through 2^23 + x (byte permute into the mantissa) minus 2^23, one packed
+// f32x2 add per two pixels, and d = x - L is one packed subtraction.  t = tau - |d|
+// is negative exactly when the bit is set (+0 at equality: strict >), and a funnel
+// shift moves its sign bit into the word (pixels taken from 31 down to 0).
 __device__ __forceinline__ uint32_t mask32(const uint32_t (&xw)[8], const uint32_t (&L)[32], float tau) {
   const unsigned long long bias = f2pack(-8388608.0f, -8388608.0f);
   uint32_t word = 0;
 #pragma unroll
-  for (int i = 0; i < 32; i += 2) {
+  for (int i = 30; i >= 0; i -= 2) {
     const uint32_t a = __byte_perm(xw[i >> 2], 0x4B000000u, 0x7540u + (i & 3));
     const uint32_t b = __byte_perm(xw[i >> 2], 0x4B000000u, 0x7540u + ((i + 1) & 3));
-    unsigned long long x2 = fadd2(((unsigned long long)b << 32) | a, bias);                  // exact x
+    const unsigned long long x2 = fadd2(((unsigned long long)b << 32) | a, bias);                  // exact x
     const unsigned long long l2 = (unsigned long long)L[i] | ((unsigned long long)L[i + 1] << 32);
     const unsigned long long d2 = fsub2(x2, l2);
-    const float d0 = __uint_as_float((uint32_t)d2), d1 = __uint_as_float((uint32_t)(d2 >> 32));
-    if (fabsf(d0) > tau) word |= 1u << i;
-    if (fabsf(d1) > tau) word |= 2u << i;
+    const float t1 = tau - fabsf(__uint_as_float((uint32_t)(d2 >> 32)));
+    const float t0 = tau - fabsf(__uint_as_float((uint32_t)d2));
+    word = __funnelshift_l(__float_as_uint(t1), word, 1);   // bit i + 1
+    word = __funnelshift_l(__float_as_uint(t0), word, 1);   // bit i
   }
   return word;
 }
