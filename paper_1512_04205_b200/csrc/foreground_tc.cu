@@ -67,14 +67,24 @@ __device__ __forceinline__ unsigned long long fsub2(unsigned long long a, unsign
   return d;
 }
 
+__device__ __forceinline__ unsigned long long ffma2(unsigned long long a, unsigned long long b,
+                                                    unsigned long long c) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+
 // 32 mask bits of one frame: pixels of 8 byte-words xw (4 pixels each) against 32
 // background values L; bit i = |x_i - L_i| > tau.  The uint8 pixel becomes an exact
 // float through 2^23 + x (byte permute into the mantissa) minus 2^23, one packed
-// f32x2 add per two pixels, and d = x - L is one packed subtraction.  t = tau - |d|
-// is negative exactly when the bit is set (+0 at equality: strict >), and a funnel
-// shift moves its sign bit into the word (pixels taken from 31 down to 0).
+// f32x2 add per two pixels; d = x - L is one packed subtraction and t = d^2 - tau'^2
+// one packed FMA, with tau'^2 the float just above tau^2 so that t >= 0 exactly when
+// d^2 > tau^2 (strict >).  A funnel shift moves the sign bit of t into the word
+// (pixels taken from 31 down to 0); the word is complemented once at the end.
 __device__ __forceinline__ uint32_t mask32(const uint32_t (&xw)[8], const uint32_t (&L)[32], float tau) {
   const unsigned long long bias = f2pack(-8388608.0f, -8388608.0f);
+  const float nt2 = -__uint_as_float(__float_as_uint(tau * tau) + 1u);   // -(next float above tau^2)
+  const unsigned long long ntau2 = f2pack(nt2, nt2);
   uint32_t word = 0;
 #pragma unroll
   for (int i = 30; i >= 0; i -= 2) {
@@ -83,12 +93,11 @@ __device__ __forceinline__ uint32_t mask32(const uint32_t (&xw)[8], const uint32
     const unsigned long long x2 = fadd2(((unsigned long long)b << 32) | a, bias);                  // exact x
     const unsigned long long l2 = (unsigned long long)L[i] | ((unsigned long long)L[i + 1] << 32);
     const unsigned long long d2 = fsub2(x2, l2);
-    const float t1 = tau - fabsf(__uint_as_float((uint32_t)(d2 >> 32)));
-    const float t0 = tau - fabsf(__uint_as_float((uint32_t)d2));
-    word = __funnelshift_l(__float_as_uint(t1), word, 1);   // bit i + 1
-    word = __funnelshift_l(__float_as_uint(t0), word, 1);   // bit i
+    const unsigned long long t2 = ffma2(d2, d2, ntau2);
+    word = __funnelshift_l((uint32_t)(t2 >> 32), word, 1);   // bit i + 1 (complemented)
+    word = __funnelshift_l((uint32_t)t2, word, 1);           // bit i (complemented)
   }
-  return word;
+  return ~word;
 }
 
 template <int KP>
