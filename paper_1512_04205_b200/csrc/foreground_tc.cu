@@ -126,6 +126,8 @@ __global__ void __launch_bounds__(32 * (2 + FG_EPI_WARPS), 1) foreground_tc_kern
   const tc::TileQueue tq{tq_id, tq_bar, tq_bar + tc::TQ_N};
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int idx = threadIdx.x; idx < 2 * 3 * PART_B / 16; idx += blockDim.x)   // B buffers: zero columns stay zero
+    reinterpret_cast<uint4*>(sB)[idx] = make_uint4(0, 0, 0, 0);
   // ---- coefficient table H (frames x KP), split in three bf16 parts, resident
   for (int idx = threadIdx.x; idx < mA * KP; idx += blockDim.x) {
     const int t = idx / KP, f = idx % KP;
@@ -242,15 +244,31 @@ __global__ void __launch_bounds__(32 * (2 + FG_EPI_WARPS), 1) foreground_tc_kern
       const int bb = tix & 1;
       tc::mbar_wait(&bempty[bb], ((uint32_t)(tix >> 1) & 1u) ^ 1u);
       uint8_t* pb = sB + (size_t)bb * 3 * PART_B;
+      if (bfh * BH < n_coef) {   // chunks of columns >= n_coef stay zero (written once)
+        // three-term bf16 split, two columns per conversion; a thread's BH columns of
+        // pixel br are whole 16-B chunks of the K-major layout: one 16-B store per part
+        uint32_t q0[BH / 2], q1[BH / 2], q2[BH / 2];
 #pragma unroll
-      for (int u = 0; u < BH; ++u) {
-        const int f = bfh * BH + u;
-        __nv_bfloat16 a0, a1, a2;
-        split3(pv[u], a0, a1, a2);
-        const uint32_t off = km_off(br, f >> 3, KP) + (f & 7) * 2;
-        *reinterpret_cast<__nv_bfloat16*>(pb + off) = a0;
-        *reinterpret_cast<__nv_bfloat16*>(pb + PART_B + off) = a1;
-        *reinterpret_cast<__nv_bfloat16*>(pb + 2 * PART_B + off) = a2;
+        for (int u = 0; u < BH; u += 2) {
+          const __nv_bfloat162 a = __floats2bfloat162_rn(pv[u], pv[u + 1]);
+          const float2 af = __bfloat1622float2(a);
+          const float r0 = pv[u] - af.x, r1 = pv[u + 1] - af.y;
+          const __nv_bfloat162 b = __floats2bfloat162_rn(r0, r1);
+          const float2 bf = __bfloat1622float2(b);
+          const __nv_bfloat162 c = __floats2bfloat162_rn(r0 - bf.x, r1 - bf.y);
+          q0[u / 2] = *reinterpret_cast<const uint32_t*>(&a);
+          q1[u / 2] = *reinterpret_cast<const uint32_t*>(&b);
+          q2[u / 2] = *reinterpret_cast<const uint32_t*>(&c);
+        }
+#pragma unroll
+        for (int c8 = 0; c8 < BH / 8; ++c8) {
+          const uint32_t off = km_off(br, (bfh * BH) / 8 + c8, KP);
+          *reinterpret_cast<uint4*>(pb + off) = make_uint4(q0[4 * c8], q0[4 * c8 + 1], q0[4 * c8 + 2], q0[4 * c8 + 3]);
+          *reinterpret_cast<uint4*>(pb + PART_B + off) =
+              make_uint4(q1[4 * c8], q1[4 * c8 + 1], q1[4 * c8 + 2], q1[4 * c8 + 3]);
+          *reinterpret_cast<uint4*>(pb + 2 * PART_B + off) =
+              make_uint4(q2[4 * c8], q2[4 * c8 + 1], q2[4 * c8 + 2], q2[4 * c8 + 3]);
+        }
       }
       tc::fence_proxy_async();
       __syncwarp();
