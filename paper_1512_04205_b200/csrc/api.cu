@@ -25,7 +25,8 @@ int persistent_ctas(int sms) {
 }
 
 size_t hqr_smem_bytes(int k);
-cudaError_t launch_hqr_eig(int k, const double* A, double* W, double* VR, int* info, cudaStream_t st);
+cudaError_t launch_hqr_eig(int k, const double* A, double* W, double* VR, int* info, double* scratch,
+                           cudaStream_t st);
 }  // namespace cdmd
 
 namespace {
@@ -345,7 +346,12 @@ cdmd_status cdmd_sensing_rows(cdmd_handle h, int64_t n_total, const cdmd_sensing
 cdmd_status cdmd_eig(const double* A, int k, double* W, double* VR, int32_t* info, cdmd_stream st) {
   if (!A || !W || !VR || !info) return CDMD_ERR_ARG;
   if (k < 1 || hqr_smem_bytes(k) > 227 * 1024) return CDMD_ERR_RANGE;
-  return cuda_status(launch_hqr_eig(k, A, W, VR, info, (cudaStream_t)st));
+  double* scratch = nullptr;
+  if (cudaMallocAsync((void**)&scratch, sizeof(double) * 2 * (size_t)k * k, (cudaStream_t)st) != cudaSuccess)
+    return CDMD_ERR_CUDA;
+  const cudaError_t e = launch_hqr_eig(k, A, W, VR, info, scratch, (cudaStream_t)st);
+  cudaFreeAsync(scratch, (cudaStream_t)st);
+  return cuda_status(e);
 }
 
 }  // extern "C"

@@ -15,6 +15,7 @@
 // exactly conjugate, VR column j = Re v, column j+1 = Im v for the pair.
 #include <math.h>
 #include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -684,10 +685,451 @@ __global__ void __launch_bounds__(32) hqr_eig_kernel(int nn, const double* __res
 #undef Vx
 }
 
+
+// ======================================================================== v2
+// Eigenvalues by the Francis QR without Schur vectors (EISPACK hqr: updates confined
+// to the active block), then every eigenvector at once by inverse iteration on the
+// Hessenberg matrix (one warp per real eigenvalue / conjugate pair) and the back
+// transformation with Q from orthes.  The sequential QR sweep does about half the
+// work of hqr2's, and the eigenvectors leave the serial chain.
+//
+// hqrv_kernel: A (k x k column-major) -> W (wr, wi pairs as hqr2), H0 (the Hessenberg
+// form, row-major k x k) and Q (row-major k x k) for hinvit_kernel.
+__global__ void __launch_bounds__(32) hqrv_kernel(int nn, const double* __restrict__ A, double* __restrict__ W,
+                                                 double* __restrict__ H0, double* __restrict__ Qout,
+                                                 int* __restrict__ info) {
+  extern __shared__ double sm[];
+  const int ld = nn + 1;
+  double* H = sm;                 // nn x ld, row-major
+  double* V = H + nn * ld;        // Q, row-major
+  double* ort = V + nn * ld;      // nn
+  double* d = ort + nn;           // nn real parts
+  double* e = d + nn;             // nn imaginary parts
+  const Warp wp{(int)(threadIdx.x & 31)};
+  const int lane = wp.lane;
+#define Hx(i, j) H[(i) * ld + (j)]
+#define Vx(i, j) V[(i) * ld + (j)]
+  for (int idx = lane; idx < nn * nn; idx += 32) {
+    const int i = idx % nn, j = idx / nn;  // A column-major
+    Hx(i, j) = A[idx];
+    Vx(i, j) = (i == j) ? 1.0 : 0.0;
+  }
+  wp.sync();
+  const int low = 0, high = nn - 1;
+  // ------------------------------------------------ orthes (Hessenberg)
+  for (int m = low + 1; m <= high - 1; ++m) {
+    double scale = 0.0;
+    for (int i = m + lane; i <= high; i += 32) scale += fabs(Hx(i, m - 1));
+    scale = wp.sum(scale);
+    if (scale != 0.0) {
+      double h = 0.0;
+      const double isc = 1.0 / scale;
+      for (int i = m + lane; i <= high; i += 32) {
+        const double o = Hx(i, m - 1) * isc;
+        ort[i] = o;
+        h += o * o;
+      }
+      h = wp.sum(h);
+      wp.sync();
+      const double om = ort[m];
+      const double g = om > 0 ? -sqrt(h) : sqrt(h);
+      h = h - om * g;
+      wp.sync();
+      if (lane == 0) ort[m] = om - g;
+      wp.sync();
+      const double ih = 1.0 / h;
+      for (int j = m + lane; j < nn; j += 32) {   // H = (I - u u'/h) H
+        double f = 0.0;
+        for (int i = high; i >= m; --i) f += ort[i] * Hx(i, j);
+        f *= ih;
+        for (int i = m; i <= high; ++i) Hx(i, j) -= f * ort[i];
+      }
+      wp.sync();
+      for (int i = lane; i <= high; i += 32) {   // H = H (I - u u'/h)
+        double f = 0.0;
+        for (int j = high; j >= m; --j) f += ort[j] * Hx(i, j);
+        f *= ih;
+        for (int j = m; j <= high; ++j) Hx(i, j) -= f * ort[j];
+      }
+      wp.sync();
+      if (lane == 0) {
+        ort[m] = scale * ort[m];
+        Hx(m, m - 1) = scale * g;
+      }
+      wp.sync();
+    }
+  }
+  // ortran: Q explicitly
+  for (int m = high - 1; m >= low + 1; --m) {
+    if (Hx(m, m - 1) != 0.0) {
+      for (int i = m + 1 + lane; i <= high; i += 32) ort[i] = Hx(i, m - 1);
+      wp.sync();
+      for (int j = m + lane; j <= high; j += 32) {
+        double g = 0.0;
+        for (int i = m; i <= high; ++i) g += ort[i] * Vx(i, j);
+        g = (g / ort[m]) / Hx(m, m - 1);
+        for (int i = m; i <= high; ++i) Vx(i, j) += g * ort[i];
+      }
+      wp.sync();
+    }
+  }
+  // the Hessenberg form and Q for the inverse iteration (below-subdiagonal entries are
+  // orthes' workspace: zero them in the copy)
+  for (int idx = lane; idx < nn * nn; idx += 32) {
+    const int i = idx / nn, j = idx % nn;
+    H0[idx] = (i > j + 1) ? 0.0 : Hx(i, j);
+    Qout[idx] = Vx(i, j);
+  }
+  // ------------------------------------------------------- hqr (values only)
+  int n = nn - 1;
+  const double eps = 0x1p-52;
+  double exshift = 0.0;
+  double p = 0, q = 0, r = 0, s = 0, z = 0, w, x, y;
+  double norm = 0.0;
+  for (int i = lane; i < nn; i += 32)
+    for (int j = (i > 0 ? i - 1 : 0); j < nn; ++j) norm += fabs(Hx(i, j));
+  norm = wp.sum(norm);
+  int iter = 0, total_iter = 0, fail = 0;
+  while (n >= low) {
+    int l = n;
+    while (l > low) {
+      s = fabs(Hx(l - 1, l - 1)) + fabs(Hx(l, l));
+      if (s == 0.0) s = norm;
+      if (fabs(Hx(l, l - 1)) < eps * s) break;
+      l--;
+    }
+    if (l == n) {  // one root
+      if (lane == 0) {
+        d[n] = Hx(n, n) + exshift;
+        e[n] = 0.0;
+      }
+      n--;
+      iter = 0;
+    } else if (l == n - 1) {  // two roots
+      w = Hx(n, n - 1) * Hx(n - 1, n);
+      p = (Hx(n - 1, n - 1) - Hx(n, n)) / 2.0;
+      q = p * p + w;
+      z = sqrt(fabs(q));
+      x = Hx(n, n) + exshift;
+      if (q >= 0) {
+        z = (p >= 0) ? p + z : p - z;
+        double dn = x + z;
+        if (z != 0.0) dn = x - w / z;
+        if (lane == 0) {
+          d[n - 1] = x + z;
+          d[n] = dn;
+          e[n - 1] = 0.0;
+          e[n] = 0.0;
+        }
+      } else if (lane == 0) {
+        d[n - 1] = x + p;
+        d[n] = x + p;
+        e[n - 1] = z;
+        e[n] = -z;
+      }
+      n = n - 2;
+      iter = 0;
+    } else {  // shift
+      x = Hx(n, n);
+      y = 0.0;
+      w = 0.0;
+      if (l < n) {
+        y = Hx(n - 1, n - 1);
+        w = Hx(n, n - 1) * Hx(n - 1, n);
+      }
+      if (iter == 10) {
+        exshift += x;
+        wp.sync();
+        for (int i = low + lane; i <= n; i += 32) Hx(i, i) -= x;
+        wp.sync();
+        s = fabs(Hx(n, n - 1)) + fabs(Hx(n - 1, n - 2));
+        x = y = 0.75 * s;
+        w = -0.4375 * s * s;
+      }
+      if (iter == 30) {
+        s = (y - x) / 2.0;
+        s = s * s + w;
+        if (s > 0) {
+          s = sqrt(s);
+          if (y < x) s = -s;
+          s = x - w / ((y - x) / 2.0 + s);
+          wp.sync();
+          for (int i = low + lane; i <= n; i += 32) Hx(i, i) -= s;
+          wp.sync();
+          exshift += s;
+          x = y = w = 0.964;
+        }
+      }
+      iter++;
+      if (++total_iter > 60 * nn) {
+        fail = 1;
+        break;
+      }
+      int m = n - 2;   // (p, q, r) carried multiplied by H(m+1, m): no divisions
+      while (m >= l) {
+        z = Hx(m, m);
+        r = x - z;
+        s = y - z;
+        const double h = Hx(m + 1, m);
+        p = (r * s - w) + Hx(m, m + 1) * h;
+        q = (Hx(m + 1, m + 1) - z - r - s) * h;
+        r = Hx(m + 2, m + 1) * h;
+        if (m == l) break;
+        if (fabs(Hx(m, m - 1)) * (fabs(q) + fabs(r)) <
+            eps * (fabs(p) * (fabs(Hx(m - 1, m - 1)) + fabs(z) + fabs(Hx(m + 1, m + 1)))))
+          break;
+        m--;
+      }
+      {
+        const double sc = fabs(p) + fabs(q) + fabs(r);
+        if (sc != 0.0) {
+          const double isc = rcp_nr(sc);
+          p *= isc;
+          q *= isc;
+          r *= isc;
+        }
+      }
+      wp.sync();
+      for (int i = m + 2 + lane; i <= n; i += 32) {
+        Hx(i, i - 2) = 0.0;
+        if (i > m + 2) Hx(i, i - 3) = 0.0;
+      }
+      wp.sync();
+      for (int kk = m; kk <= n - 1; ++kk) {  // double QR step on the active block l..n
+        const bool notlast = (kk != n - 1);
+        if (kk != m) {
+          p = Hx(kk, kk - 1);
+          q = Hx(kk + 1, kk - 1);
+          r = notlast ? Hx(kk + 2, kk - 1) : 0.0;
+          x = fabs(p) + fabs(q) + fabs(r);
+          if (x == 0.0) continue;
+          if (x < 1e-140 || x > 1e140) {
+            const double ix = 1.0 / x;
+            p = p * ix;
+            q = q * ix;
+            r = r * ix;
+          } else {
+            x = 1.0;
+          }
+        }
+        const double ss = p * p + q * q + r * r;
+        s = ss > 0.0 ? ss * rsqrt_nr(ss) : 0.0;
+        if (p < 0) s = -s;
+        if (s != 0) {
+          double newsub = 0.0;
+          bool setsub = false;
+          if (kk != m) {
+            newsub = -s * x;
+            setsub = true;
+          } else if (l != m) {
+            newsub = -Hx(kk, kk - 1);
+            setsub = true;
+          }
+          wp.sync();
+          if (setsub && lane == 0) Hx(kk, kk - 1) = newsub;
+          wp.sync();
+          p = p + s;
+          const double is = rcp_nr(s), ip = rcp_nr(p);
+          x = p * is;
+          y = q * is;
+          z = r * is;
+          q = q * ip;
+          r = r * ip;
+          for (int j = kk + lane; j <= n; j += 32) {  // rows kk..kk+2, columns kk..n
+            double pp = Hx(kk, j) + q * Hx(kk + 1, j);
+            if (notlast) {
+              pp = pp + r * Hx(kk + 2, j);
+              Hx(kk + 2, j) = Hx(kk + 2, j) - pp * z;
+            }
+            Hx(kk, j) = Hx(kk, j) - pp * x;
+            Hx(kk + 1, j) = Hx(kk + 1, j) - pp * y;
+          }
+          wp.sync();
+          const int imax = n < kk + 3 ? n : kk + 3;
+          for (int i = l + lane; i <= imax; i += 32) {  // columns kk..kk+2, rows l..imax
+            double pp = x * Hx(i, kk) + y * Hx(i, kk + 1);
+            if (notlast) {
+              pp = pp + z * Hx(i, kk + 2);
+              Hx(i, kk + 2) = Hx(i, kk + 2) - pp * r;
+            }
+            Hx(i, kk) = Hx(i, kk) - pp;
+            Hx(i, kk + 1) = Hx(i, kk + 1) - pp * q;
+          }
+          wp.sync();
+        }
+      }
+    }
+  }
+  wp.sync();
+  if (fail) {
+    if (lane == 0) *info = 1;
+    return;
+  }
+  for (int j = lane; j < nn; j += 32) {
+    W[2 * j] = d[j];
+    W[2 * j + 1] = e[j];
+  }
+  if (lane == 0) *info = 0;
+#undef Hx
+#undef Vx
+}
+
+// Inverse iteration on the Hessenberg H0 for eigenvalue j (a warp per CTA; the
+// complex conjugate pair (wi > 0, then wi < 0) is solved once, in complex arithmetic,
+// by the CTA of its first member).  LU of H0 - lambda I with partial pivoting between
+// adjacent rows (Hessenberg), a first solve U x = eps3 (EISPACK invit), one more
+// inverse-iteration step, then v = Q x.  VR column j = Re v (and j+1 = Im v for a
+// pair); canonicalize_kernel normalises and phases it.
+__global__ void __launch_bounds__(32) hinvit_kernel(int nn, const double* __restrict__ W,
+                                                   const double* __restrict__ H0, const double* __restrict__ Q,
+                                                   double* __restrict__ VR) {
+  extern __shared__ double sm[];
+  const int j = blockIdx.x, lane = threadIdx.x;
+  const double wr = W[2 * j], wi = W[2 * j + 1];
+  if (wi < 0.0) return;   // second member of a pair
+  const bool cx = wi != 0.0;
+  const int ld = nn + 1;
+  double* Br = sm;                    // nn x ld (row-major), becomes U
+  double* Bi = Br + nn * ld;          // imaginary part (pairs)
+  double* xr = Bi + nn * ld;          // nn
+  double* xi = xr + nn;               // nn
+  double* mr = xi + nn;               // multipliers (nn)
+  double* mi = mr + nn;
+  uint8_t* sw = reinterpret_cast<uint8_t*>(mi + nn);   // row swap flags
+  double norm = 0.0;
+  for (int idx = lane; idx < nn * nn; idx += 32) {
+    const int i = idx / nn, c = idx % nn;
+    const double h = H0[idx];
+    norm += fabs(h);
+    Br[i * ld + c] = h - (i == c ? wr : 0.0);
+    Bi[i * ld + c] = (i == c) ? -wi : 0.0;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) norm += __shfl_xor_sync(0xffffffffu, norm, o);
+  if (norm == 0.0) norm = 1.0;
+  const double eps3 = norm * 0x1p-52;   // replaces zero pivots, seeds the first solve
+  __syncwarp();
+  // LU with partial pivoting between rows k and k+1
+  for (int k = 0; k < nn - 1; ++k) {
+    const double ar = Br[k * ld + k], ai = Bi[k * ld + k];
+    const double br = Br[(k + 1) * ld + k], bi = Bi[(k + 1) * ld + k];
+    const bool swp = fabs(br) + fabs(bi) > fabs(ar) + fabs(ai);
+    double pr = swp ? br : ar, pi = swp ? bi : ai;   // pivot
+    const double lr = swp ? ar : br, li = swp ? ai : bi;   // eliminated
+    if (pr == 0.0 && pi == 0.0) pr = eps3;
+    double cr, ci;   // multiplier l / p
+    cdiv(lr, li, pr, pi, cr, ci);
+    __syncwarp();
+    for (int c = k + lane; c < nn; c += 32) {
+      double ur = Br[k * ld + c], ui = Bi[k * ld + c];
+      double vr = Br[(k + 1) * ld + c], vi = Bi[(k + 1) * ld + c];
+      if (swp) {
+        const double tr = ur, ti = ui;
+        ur = vr; ui = vi; vr = tr; vi = ti;
+      }
+      if (c == k) { ur = pr; ui = pi; }
+      Br[k * ld + c] = ur;
+      Bi[k * ld + c] = ui;
+      Br[(k + 1) * ld + c] = vr - (cr * ur - ci * ui);
+      Bi[(k + 1) * ld + c] = vi - (cr * ui + ci * ur);
+    }
+    if (lane == 0) {
+      mr[k] = cr;
+      mi[k] = ci;
+      sw[k] = swp ? 1 : 0;
+    }
+    __syncwarp();
+  }
+  if (lane == 0 && Br[(nn - 1) * ld + nn - 1] == 0.0 && Bi[(nn - 1) * ld + nn - 1] == 0.0)
+    Br[(nn - 1) * ld + nn - 1] = eps3;
+  for (int i = lane; i < nn; i += 32) {
+    xr[i] = eps3;
+    xi[i] = 0.0;
+  }
+  __syncwarp();
+  for (int it = 0; it < 2; ++it) {
+    if (it > 0 && lane == 0) {   // apply L^-1 (row swaps and multipliers) to x
+      for (int k = 0; k < nn - 1; ++k) {
+        double ar = xr[k], ai = xi[k], br = xr[k + 1], bi = xi[k + 1];
+        if (sw[k]) {
+          const double tr = ar, ti = ai;
+          ar = br; ai = bi; br = tr; bi = ti;
+        }
+        xr[k] = ar;
+        xi[k] = ai;
+        xr[k + 1] = br - (mr[k] * ar - mi[k] * ai);
+        xi[k + 1] = bi - (mr[k] * ai + mi[k] * ar);
+      }
+    }
+    __syncwarp();
+    // U x = rhs, column-oriented back substitution
+    for (int i = nn - 1; i >= 0; --i) {
+      double ur = Br[i * ld + i], ui = Bi[i * ld + i];
+      if (ur == 0.0 && ui == 0.0) ur = eps3;
+      double vr, vi;
+      cdiv(xr[i], xi[i], ur, ui, vr, vi);
+      __syncwarp();
+      for (int r2 = lane; r2 < i; r2 += 32) {
+        const double cr = Br[r2 * ld + i], ci = Bi[r2 * ld + i];
+        xr[r2] -= cr * vr - ci * vi;
+        xi[r2] -= cr * vi + ci * vr;
+      }
+      if (lane == 0) {
+        xr[i] = vr;
+        xi[i] = vi;
+      }
+      __syncwarp();
+    }
+    // rescale (inverse iteration grows the vector by ~1 / dist(lambda, spectrum))
+    double mx = 0.0;
+    for (int i = lane; i < nn; i += 32) mx = fmax(mx, fabs(xr[i]) + fabs(xi[i]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    const double sc = mx > 0.0 ? 1.0 / mx : 1.0;
+    for (int i = lane; i < nn; i += 32) {
+      xr[i] *= sc;
+      xi[i] *= sc;
+    }
+    __syncwarp();
+  }
+  // v = Q x
+  for (int i = lane; i < nn; i += 32) {
+    double ar = 0.0, ai = 0.0;
+    const double* qrow = Q + (int64_t)i * nn;
+    for (int c = 0; c < nn; ++c) {
+      const double qv = __ldg(qrow + c);
+      ar = fma(qv, xr[c], ar);
+      ai = fma(qv, xi[c], ai);
+    }
+    VR[(int64_t)j * nn + i] = ar;
+    if (cx) VR[(int64_t)(j + 1) * nn + i] = ai;
+  }
+}
+
 size_t hqr_smem_bytes(int k) { return sizeof(double) * ((size_t)2 * k * (k + 1) + 3 * (size_t)k); }
 static size_t hqr_smem_par3(int k) { return hqr_smem_bytes(k) + sizeof(double) * 64 * (size_t)k; }
 
-cudaError_t launch_hqr_eig(int k, const double* A, double* W, double* VR, int* info, cudaStream_t st) {
+static size_t hinvit_smem(int k) { return sizeof(double) * ((size_t)2 * k * (k + 1) + 4 * (size_t)k) + k + 16; }
+
+// scratch: >= 2 k^2 doubles (the Hessenberg form and Q of the v2 path)
+cudaError_t launch_hqr_eig(int k, const double* A, double* W, double* VR, int* info, double* scratch,
+                           cudaStream_t st) {
+  if (scratch && hinvit_smem(k) <= 226 * 1024 && !getenv("CDMD_EIG_V1")) {
+    double* H0 = scratch;
+    double* Q = scratch + (size_t)k * k;
+    const size_t smem = hqr_smem_bytes(k);
+    cudaError_t e = cudaFuncSetAttribute(hqrv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    note_launch();
+    hqrv_kernel<<<1, 32, smem, st>>>(k, A, W, H0, Q, info);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    const size_t smem2 = hinvit_smem(k);
+    e = cudaFuncSetAttribute(hinvit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
+    if (e != cudaSuccess) return e;
+    note_launch();
+    hinvit_kernel<<<(unsigned)k, 32, smem2, st>>>(k, W, H0, Q, VR);
+    return cudaGetLastError();
+  }
   const int par3 = hqr_smem_par3(k) <= 226 * 1024;
   const size_t smem = par3 ? hqr_smem_par3(k) : hqr_smem_bytes(k);
   cudaError_t e = cudaFuncSetAttribute(hqr_eig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -31,7 +31,7 @@ static constexpr double OMP_STOP = 1e-6;   // reading R12: stop when ||r|| <= 1e
 static constexpr double TIE_RTOL = 1e-9;   // reading R13
 
 struct FitWs {
-  double *Yd, *G, *A, *w, *V, *T, *B, *VR, *Wc, *SW, *T2, *Gf, *cf, *ehw;
+  double *Yd, *G, *A, *w, *V, *T, *B, *VR, *Wc, *SW, *T2, *Gf, *cf, *ehw, *Es;
   int* dinfo;
   void* sy_dev;
   size_t sy_dev_bytes, sy_host_bytes;
@@ -55,7 +55,8 @@ static int syev_mode(int n1, int k) {
   if (e && e[0] == 'd' && e[1] == 'x') return 2;
   return eh_supported(n1, k) ? 0 : 2;
 }
-cudaError_t launch_hqr_eig(int k, const double* A, double* W, double* VR, int* info, cudaStream_t st);
+cudaError_t launch_hqr_eig(int k, const double* A, double* W, double* VR, int* info, double* scratch,
+                           cudaStream_t st);
 
 static bool use_device_eig(int k) {
   const char* e = getenv("CDMD_GEEV");
@@ -81,6 +82,7 @@ static cdmd_status layout_ws(cdmd_handle h, int64_t p, int64_t m, int k, char* b
   W->T = (double*)take(sizeof(double) * n1 * k);
   W->B = (double*)take(sizeof(double) * k * k);
   W->VR = (double*)take(sizeof(double) * k * k);
+  W->Es = (double*)take(sizeof(double) * 2 * k * k);   // eig scratch: Hessenberg form and Q
   W->Wc = (double*)take(sizeof(double) * 2 * k);
   W->SW = (double*)take(sizeof(double) * k * k);
   W->T2 = (double*)take(sizeof(double) * n1 * k);
@@ -622,7 +624,7 @@ cdmd_status fit_impl(cdmd_handle h, const void* Y, int64_t ldy, int kind, int64_
   // Default: the single-warp on-device Hessenberg + Francis QR solver (eig.cu);
   // cuSOLVER's hybrid geev for k > 118 or with CDMD_GEEV=cusolver.
   if (use_device_eig(ke)) {
-    CU(launch_hqr_eig(ke, W.B, W.Wc, W.VR, W.dinfo + 9, st));
+    CU(launch_hqr_eig(ke, W.B, W.Wc, W.VR, W.dinfo + 9, W.Es, st));
   } else {
     size_t d = 0, hb = 0;
     if (cusolverDnXgeev_bufferSize(h->solver, h->params, CUSOLVER_EIG_MODE_NOVECTOR,
