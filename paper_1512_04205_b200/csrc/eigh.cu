@@ -35,7 +35,7 @@ __host__ __device__ inline int64_t eh_asz_max(int n) {
   return mx;
 }
 // offset of local row slot s (global row i = rank + 8 s, holding columns 0..i)
-__device__ __forceinline__ int64_t eh_off(int rank, int64_t s) { return s * (rank + 1) + 4 * s * (s - 1); }
+__device__ __forceinline__ int eh_off(int rank, int s) { return s * (rank + 1) + 4 * s * (s - 1); }
 
 __device__ __forceinline__ double block_sum(double v, double* red) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -70,8 +70,8 @@ __global__ void __cluster_dims__(EH_CL, 1, 1) __launch_bounds__(EH_T, 1)
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = (int)cluster.block_rank();
   extern __shared__ double sm[];
-  const int64_t nr = eh_rows(n, rank);
-  const int64_t stride = (n + EH_CL - 1) / EH_CL + 1;  // cbuf row stride (max rows per CTA + 1)
+  const int nr = (int)eh_rows(n, rank);
+  const int stride = (n + EH_CL - 1) / EH_CL + 1;  // cbuf row stride (max rows per CTA + 1)
   double* Aloc = sm;                                   // lower-triangle rows of this CTA
   double* xbuf = Aloc + eh_asz_max(n);                 // [n] column below the diagonal
   double* pbuf2 = xbuf + n;                            // [2][n] p = tau A v (double-buffered)
@@ -84,10 +84,10 @@ __global__ void __cluster_dims__(EH_CL, 1, 1) __launch_bounds__(EH_T, 1)
   double* cpart = red + 40;                            // [16 warps][n] column partial sums
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   // load own rows (lower part) from G
-  for (int64_t s = 0; s < nr; ++s) {
-    const int64_t i = rank + EH_CL * s;
+  for (int s = 0; s < nr; ++s) {
+    const int i = rank + EH_CL * s;
     double* row = Aloc + eh_off(rank, s);
-    for (int64_t c = tid; c <= i; c += EH_T) row[c] = G[i + c * ldg];
+    for (int c = tid; c <= i; c += EH_T) row[c] = G[i + (int64_t)c * ldg];
   }
   for (int i = tid; i < (EH_T / 32) * n; i += EH_T) cpart[i] = 0.0;
   __syncthreads();
@@ -98,8 +98,8 @@ __global__ void __cluster_dims__(EH_CL, 1, 1) __launch_bounds__(EH_T, 1)
     double* kpart = kpart2 + (j & 1) * EH_CL;
     // (a) push own entries of column j (rows i > j) and the partial norm of x[1:]
     double part = 0.0;
-    for (int64_t s = tid; s < nr; s += EH_T) {
-      const int64_t i = rank + EH_CL * s;
+    for (int s = tid; s < nr; s += EH_T) {
+      const int i = rank + EH_CL * s;
       if (i > j) {
         const double xi = Aloc[eh_off(rank, s) + j];
         if (i > j + 1) part += xi * xi;
@@ -138,13 +138,13 @@ __global__ void __cluster_dims__(EH_CL, 1, 1) __launch_bounds__(EH_T, 1)
       //     c_i += A[l][i] v_l (per-warp partials), then the column sums are
       //     reduce-scattered to the rows' owners
       double* cw = cpart + warp * n;
-      for (int64_t s = warp; s < nr; s += EH_T / 32) {
-        const int64_t l = rank + EH_CL * s;
+      for (int s = warp; s < nr; s += EH_T / 32) {
+        const int l = rank + EH_CL * s;
         if (l <= j) continue;
         const double* row = Aloc + eh_off(rank, s);
         const double vl = v[l];
         double acc = 0.0;
-        for (int64_t i = j + 1 + lane; i < l; i += 32) {
+        for (int i = j + 1 + lane; i < l; i += 32) {
           const double a = row[i];
           acc += a * v[i];
           cw[i] += a * vl;
@@ -161,18 +161,18 @@ __global__ void __cluster_dims__(EH_CL, 1, 1) __launch_bounds__(EH_T, 1)
           cpart[q * n + i] = 0.0;
         }
         // to the owner of row i, slot (source rank, local row i / 8)
-        cluster.map_shared_rank(cbuf, i % EH_CL)[(int64_t)rank * stride + i / EH_CL] = acc;
+        cluster.map_shared_rank(cbuf, i % EH_CL)[rank * stride + i / EH_CL] = acc;
       }
       EH_TICK(3);
       cluster.sync();
       EH_TICK(2);
       // (d) owners complete p for their rows and push it; partial p.v
       double kp = 0.0;
-      for (int64_t s = tid; s < nr; s += EH_T) {
-        const int64_t l = rank + EH_CL * s;
+      for (int s = tid; s < nr; s += EH_T) {
+        const int l = rank + EH_CL * s;
         if (l <= j) continue;
         double pl = pbuf[l];
-        for (int r = 0; r < EH_CL; ++r) pl += cbuf[(int64_t)r * stride + s];
+        for (int r = 0; r < EH_CL; ++r) pl += cbuf[r * stride + s];
         pl *= tau;
         kp += pl * v[l];
         for (int r = 0; r < EH_CL; ++r) cluster.map_shared_rank(pbuf, r)[l] = pl;
@@ -189,12 +189,12 @@ __global__ void __cluster_dims__(EH_CL, 1, 1) __launch_bounds__(EH_T, 1)
       const double K = -0.5 * tau * pv;
       for (int i = j + 1 + tid; i < n; i += EH_T) w[i] = pbuf[i] + K * v[i];
       __syncthreads();
-      for (int64_t s = warp; s < nr; s += EH_T / 32) {
-        const int64_t l = rank + EH_CL * s;
+      for (int s = warp; s < nr; s += EH_T / 32) {
+        const int l = rank + EH_CL * s;
         if (l <= j) continue;
         double* row = Aloc + eh_off(rank, s);
         const double vl = v[l], wl = w[l];
-        for (int64_t i = j + 1 + lane; i <= l; i += 32) row[i] -= vl * w[i] + wl * v[i];
+        for (int i = j + 1 + lane; i <= l; i += 32) row[i] -= vl * w[i] + wl * v[i];
       }
       __syncthreads();
       EH_TICK(5);
