@@ -14,6 +14,7 @@
 #include <math.h>
 
 #include "common.cuh"
+#include "tc.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -57,6 +58,20 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
 // V: n x n column-major holding reflector j in column j (entries j+1 .. n-1, v[j+1] = 1).
 __device__ unsigned long long g_eh_prof[8];
 
+// DSMEM exchange primitives: st.async stores into another CTA's shared memory signal
+// that CTA's mbarrier (complete_tx); the receiver arms the barrier with the byte count
+// it expects.  No cluster-wide barrier (and no GPU-scope fence) per exchange.
+__device__ __forceinline__ uint32_t eh_mapa(uint32_t local, int rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void eh_st_async(uint32_t addr, double v, uint32_t mbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(addr),
+               "l"(__double_as_longlong(v)), "r"(mbar)
+               : "memory");
+}
+
 __global__ void __cluster_dims__(EH_CL, 1, 1) __launch_bounds__(EH_T, 1)
     eh_tridiag_kernel(int n, const double* __restrict__ G, int64_t ldg, double* __restrict__ d,
                       double* __restrict__ e, double* __restrict__ tau_out, double* __restrict__ V) {
@@ -71,18 +86,25 @@ __global__ void __cluster_dims__(EH_CL, 1, 1) __launch_bounds__(EH_T, 1)
   const int rank = (int)cluster.block_rank();
   extern __shared__ double sm[];
   const int nr = (int)eh_rows(n, rank);
-  const int stride = (n + EH_CL - 1) / EH_CL + 1;  // cbuf row stride (max rows per CTA + 1)
+  const int stride = (n + EH_CL - 1) / EH_CL + 1;     // cbuf row stride (max rows per CTA + 1)
   double* Aloc = sm;                                   // lower-triangle rows of this CTA
-  double* xbuf = Aloc + eh_asz_max(n);                 // [n] column below the diagonal
-  double* pbuf2 = xbuf + n;                            // [2][n] p = tau A v (double-buffered)
-  double* cbuf = pbuf2 + 2 * n;                        // [8][stride] column contributions
-  double* nrm = cbuf + EH_CL * stride;                 // [8] partial squared norms
-  double* kpart2 = nrm + EH_CL;                        // [2][8] partial p.v (double-buffered)
+  double* xbuf2 = Aloc + eh_asz_max(n);                // [2][n] column below the diagonal (received)
+  double* pbuf2 = xbuf2 + 2 * n;                       // [2][n] p = tau A v (received)
+  double* cbuf2 = pbuf2 + 2 * n;                       // [2][8][stride] column parts (received)
+  double* nrm2 = cbuf2 + 2 * EH_CL * stride;           // [2][8] partial squared norms (received)
+  double* kpart2 = nrm2 + 2 * EH_CL;                   // [2][8] partial p.v (received)
   double* v = kpart2 + 2 * EH_CL;                      // [n]
   double* w = v + n;                                   // [n]
-  double* red = w + n;                                 // [40]
-  double* cpart = red + 40;                            // [16 warps][n] column partial sums
+  double* rowp = w + n;                                // [stride] row parts of own rows
+  double* red = rowp + stride;                         // [40]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(red + 40);   // barX[2], barC[2], barP[2]
+  double* cpart = reinterpret_cast<double*>(bars + 8);      // [16 warps][n] column partial sums
+  uint64_t* barX = bars;
+  uint64_t* barC = bars + 2;
+  uint64_t* barP = bars + 4;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t s_x = tc::smem_u32(xbuf2), s_p = tc::smem_u32(pbuf2), s_c = tc::smem_u32(cbuf2);
+  const uint32_t s_n = tc::smem_u32(nrm2), s_k = tc::smem_u32(kpart2), s_b = tc::smem_u32(bars);
   // load own rows (lower part) from G
   for (int s = 0; s < nr; ++s) {
     const int i = rank + EH_CL * s;
@@ -90,28 +112,45 @@ __global__ void __cluster_dims__(EH_CL, 1, 1) __launch_bounds__(EH_T, 1)
     for (int c = tid; c <= i; c += EH_T) row[c] = G[i + (int64_t)c * ldg];
   }
   for (int i = tid; i < (EH_T / 32) * n; i += EH_T) cpart[i] = 0.0;
+  if (tid == 0) {
+    for (int q = 0; q < 6; ++q) tc::mbar_init(&bars[q], 1);
+    tc::fence_mbar_init();
+  }
   __syncthreads();
-  cluster.sync();
-  EH_TICK(0);
-  for (int j = 0; j < n - 1; ++j) {
-    double* pbuf = pbuf2 + (j & 1) * n;
-    double* kpart = kpart2 + (j & 1) * EH_CL;
-    // (a) push own entries of column j (rows i > j) and the partial norm of x[1:]
+  cluster.sync();   // barriers initialised and every CTA resident before any DSMEM traffic
+  // push own entries of column c (rows l > c) and the partial |x[1:]|^2 to every CTA
+  auto push_column = [&](int c) {
+    const int b = c & 1;
     double part = 0.0;
     for (int s = tid; s < nr; s += EH_T) {
-      const int i = rank + EH_CL * s;
-      if (i > j) {
-        const double xi = Aloc[eh_off(rank, s) + j];
-        if (i > j + 1) part += xi * xi;
-        for (int r = 0; r < EH_CL; ++r) cluster.map_shared_rank(xbuf, r)[i] = xi;
+      const int l = rank + EH_CL * s;
+      if (l > c) {
+        const double xl = Aloc[eh_off(rank, s) + c];
+        if (l > c + 1) part += xl * xl;
+        for (int r = 0; r < EH_CL; ++r)
+          eh_st_async(eh_mapa(s_x + 8u * (uint32_t)(b * n + l), r), xl, eh_mapa(s_b + 8u * (uint32_t)(0 + b), r));
       }
     }
     part = block_sum(part, red);
     if (tid == 0)
-      for (int r = 0; r < EH_CL; ++r) cluster.map_shared_rank(nrm, r)[rank] = part;
-    EH_TICK(1);
-    cluster.sync();
+      for (int r = 0; r < EH_CL; ++r)
+        eh_st_async(eh_mapa(s_n + 8u * (uint32_t)(b * EH_CL + rank), r), part, eh_mapa(s_b + 8u * (uint32_t)b, r));
+  };
+  push_column(0);
+  int own_gt = nr;                 // own rows l > j (updated as j advances)
+  uint32_t phC[2] = {0u, 0u}, phP[2] = {0u, 0u};
+  EH_TICK(0);
+  for (int j = 0; j < n - 1; ++j) {
+    const int b = j & 1;
+    if (own_gt > 0 && rank + EH_CL * (nr - own_gt) <= j) --own_gt;   // own row j left the trailing block
+    if (tid == 0) tc::mbar_arrive_expect_tx(&barX[b], 8u * (uint32_t)(n - j - 1) + 8u * EH_CL);
+    tc::mbar_wait(&barX[b], (uint32_t)(j >> 1) & 1u);
     EH_TICK(2);
+    const double* xbuf = xbuf2 + b * n;
+    const double* nrm = nrm2 + b * EH_CL;
+    double* pbuf = pbuf2 + b * n;
+    const double* kpart = kpart2 + b * EH_CL;
+    const double* cbuf = cbuf2 + b * EH_CL * stride;
     // (b) Householder reflector (redundantly on every CTA): H = I - tau v v^T
     double xn2 = 0.0;
     for (int r = 0; r < EH_CL; ++r) xn2 += nrm[r];
@@ -130,13 +169,18 @@ __global__ void __cluster_dims__(EH_CL, 1, 1) __launch_bounds__(EH_T, 1)
     }
     if (rank == (j % EH_CL) && tid == 0) d[j] = Aloc[eh_off(rank, j / EH_CL) + j];
     __syncthreads();
-    if (tau != 0.0) {
-      for (int i = j + 1 + tid; i < n; i += EH_T)
-        if ((i % EH_CL) == rank) V[i + (int64_t)j * n] = v[i];   // reflector for the back transform
-      // (c) p = tau A v on the trailing block, one sweep over the own rows (warp per
-      //     row): the row part s_l = sum_{i<=l} A[l][i] v_i and the column part
-      //     c_i += A[l][i] v_l (per-warp partials), then the column sums are
-      //     reduce-scattered to the rows' owners
+    EH_TICK(1);
+    if (tau == 0.0) {   // column j + 1 is already final
+      if (j + 1 < n - 1) push_column(j + 1);
+      continue;
+    }
+    for (int i = j + 1 + tid; i < n; i += EH_T)
+      if ((i % EH_CL) == rank) V[i + (int64_t)j * n] = v[i];   // reflector for the back transform
+    // (c) p = tau A v on the trailing block, one sweep over the own rows (warp per
+    //     row): the row part s_l = sum_{i<=l} A[l][i] v_i and the column part
+    //     c_i += A[l][i] v_l (per-warp partials), then the column sums go to the
+    //     rows' owners
+    {
       double* cw = cpart + warp * n;
       for (int s = warp; s < nr; s += EH_T / 32) {
         const int l = rank + EH_CL * s;
@@ -150,57 +194,64 @@ __global__ void __cluster_dims__(EH_CL, 1, 1) __launch_bounds__(EH_T, 1)
           cw[i] += a * vl;
         }
         for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (lane == 0) pbuf[l] = acc + row[l] * vl;   // own-row partial incl. the diagonal
+        if (lane == 0) rowp[s] = acc + row[l] * vl;   // own-row partial incl. the diagonal
       }
-      __syncthreads();
-      for (int i = j + 1 + tid; i < n; i += EH_T) {
-        double acc = 0.0;
-#pragma unroll
-        for (int q = 0; q < EH_T / 32; ++q) {
-          acc += cpart[q * n + i];
-          cpart[q * n + i] = 0.0;
-        }
-        // to the owner of row i, slot (source rank, local row i / 8)
-        cluster.map_shared_rank(cbuf, i % EH_CL)[rank * stride + i / EH_CL] = acc;
-      }
-      EH_TICK(3);
-      cluster.sync();
-      EH_TICK(2);
-      // (d) owners complete p for their rows and push it; partial p.v
-      double kp = 0.0;
-      for (int s = tid; s < nr; s += EH_T) {
-        const int l = rank + EH_CL * s;
-        if (l <= j) continue;
-        double pl = pbuf[l];
-        for (int r = 0; r < EH_CL; ++r) pl += cbuf[r * stride + s];
-        pl *= tau;
-        kp += pl * v[l];
-        for (int r = 0; r < EH_CL; ++r) cluster.map_shared_rank(pbuf, r)[l] = pl;
-      }
-      kp = block_sum(kp, red);
-      if (tid == 0)
-        for (int r = 0; r < EH_CL; ++r) cluster.map_shared_rank(kpart, r)[rank] = kp;
-      EH_TICK(4);
-      cluster.sync();
-      EH_TICK(2);
-      // (e) w = p - (tau/2)(p.v) v; rank-2 update of own rows: A -= v w^T + w v^T
-      double pv = 0.0;
-      for (int r = 0; r < EH_CL; ++r) pv += kpart[r];
-      const double K = -0.5 * tau * pv;
-      for (int i = j + 1 + tid; i < n; i += EH_T) w[i] = pbuf[i] + K * v[i];
-      __syncthreads();
-      for (int s = warp; s < nr; s += EH_T / 32) {
-        const int l = rank + EH_CL * s;
-        if (l <= j) continue;
-        double* row = Aloc + eh_off(rank, s);
-        const double vl = v[l], wl = w[l];
-        for (int i = j + 1 + lane; i <= l; i += 32) row[i] -= vl * w[i] + wl * v[i];
-      }
-      __syncthreads();
-      EH_TICK(5);
     }
-    // no trailing cluster barrier: p and p.v are double-buffered, and every other
-    // remote write of the next column happens after a barrier its readers passed
+    __syncthreads();
+    for (int i = j + 1 + tid; i < n; i += EH_T) {
+      double acc = 0.0;
+#pragma unroll
+      for (int q = 0; q < EH_T / 32; ++q) {
+        acc += cpart[q * n + i];
+        cpart[q * n + i] = 0.0;
+      }
+      const int o = i % EH_CL;   // owner of row i: slot (source rank, local row i / 8)
+      eh_st_async(eh_mapa(s_c + 8u * (uint32_t)((b * EH_CL + rank) * stride + i / EH_CL), o), acc,
+                  eh_mapa(s_b + 8u * (uint32_t)(2 + b), o));
+    }
+    if (tid == 0) tc::mbar_arrive_expect_tx(&barC[b], 8u * EH_CL * (uint32_t)own_gt);
+    EH_TICK(3);
+    tc::mbar_wait(&barC[b], phC[b]);
+    phC[b] ^= 1u;
+    EH_TICK(2);
+    // (d) owners complete p for their rows and send it everywhere; partial p.v
+    double kp = 0.0;
+    for (int s = tid; s < nr; s += EH_T) {
+      const int l = rank + EH_CL * s;
+      if (l <= j) continue;
+      double pl = rowp[s];
+      for (int r = 0; r < EH_CL; ++r) pl += cbuf[r * stride + s];
+      pl *= tau;
+      kp += pl * v[l];
+      for (int r = 0; r < EH_CL; ++r)
+        eh_st_async(eh_mapa(s_p + 8u * (uint32_t)(b * n + l), r), pl, eh_mapa(s_b + 8u * (uint32_t)(4 + b), r));
+    }
+    kp = block_sum(kp, red);
+    if (tid == 0) {
+      for (int r = 0; r < EH_CL; ++r)
+        eh_st_async(eh_mapa(s_k + 8u * (uint32_t)(b * EH_CL + rank), r), kp, eh_mapa(s_b + 8u * (uint32_t)(4 + b), r));
+      tc::mbar_arrive_expect_tx(&barP[b], 8u * (uint32_t)(n - j - 1) + 8u * EH_CL);
+    }
+    EH_TICK(4);
+    tc::mbar_wait(&barP[b], phP[b]);
+    phP[b] ^= 1u;
+    EH_TICK(2);
+    // (e) w = p - (tau/2)(p.v) v; rank-2 update of own rows: A -= v w^T + w v^T
+    double pv = 0.0;
+    for (int r = 0; r < EH_CL; ++r) pv += kpart[r];
+    const double K = -0.5 * tau * pv;
+    for (int i = j + 1 + tid; i < n; i += EH_T) w[i] = pbuf[i] + K * v[i];
+    __syncthreads();
+    for (int s = warp; s < nr; s += EH_T / 32) {
+      const int l = rank + EH_CL * s;
+      if (l <= j) continue;
+      double* row = Aloc + eh_off(rank, s);
+      const double vl = v[l], wl = w[l];
+      for (int i = j + 1 + lane; i <= l; i += 32) row[i] -= vl * w[i] + wl * v[i];
+    }
+    __syncthreads();
+    if (j + 1 < n - 1) push_column(j + 1);
+    EH_TICK(5);
   }
   cluster.sync();
   if (rank == 0 && threadIdx.x == 0)
@@ -489,8 +540,8 @@ __global__ void __launch_bounds__(128) eh_backtransform_kernel(int n, int k, con
 
 size_t eh_tridiag_smem(int n) {
   const int64_t stride = (n + EH_CL - 1) / EH_CL + 1;
-  return sizeof(double) * ((size_t)eh_asz_max(n) + 5 * (size_t)n + EH_CL * stride + 3 * EH_CL + 40 +
-                           (size_t)(EH_T / 32) * n);
+  return sizeof(double) * ((size_t)eh_asz_max(n) + 6 * (size_t)n + 2 * EH_CL * stride + 4 * EH_CL + stride + 40 +
+                           8 + (size_t)(EH_T / 32) * n);
 }
 
 bool eh_supported(int n, int k) { return n >= 3 && n <= EH_NMAX && k <= 256 && eh_tridiag_smem(n) <= 227 * 1024; }
