@@ -8,7 +8,7 @@ workload (N=1): c4_1080p_sparse = 1920x1080, m = 500 frames, sparse C (s = n/ln 
          p = 2000, k = 50, K = 10, tau = 25, dynamic background (north_star (3)).
 value  : frames / device time per step (max over ranks), inputs resident in HBM;
          X (1.04 GB) is larger than L2, so no flush is needed between steps.
-         Streaming (default, --lanes 8): K batches flow through 8 lanes (own handle,
+         Streaming (default, --lanes 16): K batches flow through 16 lanes (own handle,
          CUDA stream, buffers and copy of X), so one batch's latency-bound small solve
          overlaps other batches' HBM passes -- the paper's batch decomposition of a long
          video.  `latency_ms_per_batch` reports one batch at a time (--lanes 1).
@@ -167,7 +167,7 @@ def main():
     ap.add_argument("--ref-frac", type=int, default=32)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--lanes", type=int, default=8,
+    ap.add_argument("--lanes", type=int, default=16,
                     help="batches in flight (streaming, P:573); 1 = one batch at a time")
     args = ap.parse_args()
     if args.impl == "reference":
