@@ -379,3 +379,29 @@ def test_gaussian_tensor_core_sketch(C, H, W, Hh, m, p, monkeypatch):
         assert d.max() <= PT.RTOL_Y_GAUSS, d.max()
     col = np.linalg.norm(a - b, axis=0) / np.linalg.norm(b, axis=0)
     assert col.max() <= 1e-5, col.max()
+
+
+def test_streaming_lanes_equal_sequential(C, H):
+    """The measured path: batches through cdmd.Streaming (lanes with their own handle,
+    streams, buffers; the fit on a high-priority stream) give bit-identical sketches,
+    limbs of M and masks to one batch at a time through Pipeline, at the bench size."""
+    cfg = config_by_name("c4_1080p_sparse")
+    X = video_for(cfg)
+    m, n = X.shape
+    X0 = to_dev(X)
+    vids = [X0, X0.flip(0).contiguous(), X0.roll(7, dims=0).contiguous(), X0.flip(0).roll(3, dims=0).contiguous(),
+            X0.roll(-11, dims=0).contiguous()]
+    S = C.Streaming(0, n, n, m, "sparse", cfg.p, cfg.k, cfg.K, lanes=3, seed=cfg.sensing_seed)
+    ends = S.run(vids, cfg.tau, C.BG_DYNAMIC)
+    for e in ends:
+        torch.cuda.current_stream().wait_event(e)
+    torch.cuda.synchronize()
+    P = C.Pipeline(H, n, n, m, "sparse", cfg.p, cfg.k, cfg.K, seed=cfg.sensing_seed)
+    for li, (_, _, _, pipe) in enumerate(S.lanes):
+        last = max(b for b in range(len(vids)) if b % 3 == li)
+        mask = P.run(vids[last], cfg.tau, C.BG_DYNAMIC)
+        torch.cuda.synchronize()
+        assert torch.equal(pipe.Y, P.Y), li
+        assert torch.equal(pipe.mask, mask), li
+        assert pipe.model.k_eff == P.model.k_eff and pipe.model.K_eff == P.model.K_eff
+        assert torch.equal(pipe.Phi, P.Phi), li
