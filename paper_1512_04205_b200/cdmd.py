@@ -348,9 +348,14 @@ class Streaming:
             self._next_ar += 1
             self._cv.notify_all()
 
-    def run(self, videos, tau, mode=BG_DYNAMIC, allreduce=None, start_event=None):
+    def run(self, videos, tau, mode=BG_DYNAMIC, allreduce=None, start_event=None, host_video=None,
+            host_masks=None):
         """videos: list of uint8 CUDA tensors (m, ld), one per batch.  Returns the
-        per-lane end events (record them into the caller's stream to join)."""
+        per-lane end events (record them into the caller's stream to join).
+        End to end: with `host_video` (a pinned uint8 host tensor like videos[b]) every
+        batch first copies it into its device buffer, and with `host_masks` (one pinned
+        int32 host tensor per lane, shaped like the mask) every batch copies its mask
+        back; the copies run on the lane's stream, overlapping the other lanes' work."""
         import concurrent.futures as cf
         self._next_ar = 0
         L = len(self.lanes)
@@ -363,6 +368,8 @@ class Streaming:
                     st.wait_event(start_event)
                 for b in range(li, len(videos), L):
                     X = videos[b]
+                    if host_video is not None:
+                        X.copy_(host_video, non_blocking=True)
                     pipe.sketch(X, st)
                     if allreduce is not None:
                         self._ordered_allreduce(b, allreduce, pipe.Y)
@@ -371,6 +378,8 @@ class Streaming:
                     st.wait_stream(st_fit)
                     pipe.modes(X, st)
                     pipe.foreground(X, tau, mode, st)
+                    if host_masks is not None:
+                        host_masks[li].copy_(pipe.mask, non_blocking=True)
                 ev = torch.cuda.Event(enable_timing=True)
                 ev.record(st)
                 ends[li] = ev

@@ -390,6 +390,7 @@ static cudaError_t launch_kp(const cdmd_video& v, const cdmd_model& M, const flo
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return cudaErrorInvalidValue;
   int stages = 4;
+  if (const char* e = getenv("CDMD_FG_STAGES")) { const int q = atoi(e); if (q >= 2 && q < stages) stages = q; }
   while (stages > 2 && fg_smem_bytes(KP, nfb, stages) > 226 * 1024) --stages;
   const size_t smem = fg_smem_bytes(KP, nfb, stages);
   cudaError_t e = cudaFuncSetAttribute(foreground_tc_kernel<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -13,6 +13,8 @@
 // The result is bit-identical to modes.cu's dp4a kernel (both accumulate exactly).
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "tc.cuh"
 
@@ -200,6 +202,7 @@ static cudaError_t launch_nt(const cdmd_video& v, const cdmd_model& M, float* Ph
   const size_t fixed = bbytes + 1024 + 512;
   int stages = (int)((max_smem - fixed) / TC_STAGE);
   if (stages > 8) stages = 8;
+  if (const char* e = getenv("CDMD_MODES_STAGES")) { const int q = atoi(e); if (q >= 2 && q < stages) stages = q; }
   const size_t smem = fixed + (size_t)stages * TC_STAGE;
   cudaError_t e = cudaFuncSetAttribute(modes_tc_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
