@@ -138,7 +138,8 @@ CDMD_API uint64_t cdmd_kernel_launches(void);
  * per-slab partial sketches of a pixel-sharded run SUM to the full sketch
  * (integer kinds bit-exactly).  Y (p x m, ldy >= p) is overwritten.
  * ws: device workspace of at least cdmd_sketch_workspace_bytes() bytes, 256-B
- * aligned (index lists of C).  Errors: CDMD_ERR_RANGE if p < 1 or p > n_total,
+ * aligned (index lists of C; for Gaussian C also the split-K partial sums, which are
+ * reduced in a fixed order so Y is deterministic).  Errors: CDMD_ERR_RANGE if p < 1 or p > n_total,
  * s <= 1 (sparse), m < 2; CDMD_ERR_ARG on layout violations; CDMD_ERR_WORKSPACE. */
 CDMD_API size_t cdmd_sketch_workspace_bytes(const cdmd_video* v, const cdmd_sensing* c);
 CDMD_API cdmd_status cdmd_sketch(cdmd_handle h, const cdmd_video* v, const cdmd_sensing* c,

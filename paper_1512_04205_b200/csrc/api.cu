@@ -154,9 +154,15 @@ void cdmd_destroy(cdmd_handle h) {
 }
 
 // ------------------------------------------------------------------- sketch
+static size_t sketch_ws_bytes(const cdmd_video* v, const SensingPlan& P) {
+  size_t b = al256(sensing_ws_bytes(P));
+  if (P.kind == CDMD_GAUSSIAN) b += al256(sizeof(float) * (size_t)gaussian_part_floats(*v, P.p));
+  return b;
+}
+
 size_t cdmd_sketch_workspace_bytes(const cdmd_video* v, const cdmd_sensing* c) {
   if (!v || !c || check_sensing(v->n_total, c) != CDMD_OK) return 0;
-  return sensing_ws_bytes(make_plan(v->n_total, c));
+  return sketch_ws_bytes(v, make_plan(v->n_total, c));
 }
 
 cdmd_status cdmd_sketch(cdmd_handle h, const cdmd_video* v, const cdmd_sensing* c, void* Y,
@@ -168,7 +174,7 @@ cdmd_status cdmd_sketch(cdmd_handle h, const cdmd_video* v, const cdmd_sensing* 
   if ((s = check_sensing(v->n_total, c)) != CDMD_OK) return s;
   if (ldy < c->p) return CDMD_ERR_ARG;
   const SensingPlan P = make_plan(v->n_total, c);
-  const size_t need = sensing_ws_bytes(P);
+  const size_t need = sketch_ws_bytes(v, P);
   if (ws_bytes < need || (need > 256 && !ws)) return CDMD_ERR_WORKSPACE;
   if (ws && (reinterpret_cast<uintptr_t>(ws) & 255) != 0) return CDMD_ERR_ARG;
   cudaError_t e = cudaSuccess;
@@ -192,7 +198,8 @@ cdmd_status cdmd_sketch(cdmd_handle h, const cdmd_video* v, const cdmd_sensing* 
       e = launch_sketch_rademacher(*v, P, (int32_t*)Y, ldy, st);
       break;
     case CDMD_GAUSSIAN:
-      e = launch_sketch_gaussian(*v, P, h->gauss_table, (float*)Y, ldy, st);
+      e = launch_sketch_gaussian(*v, P, h->gauss_table, (float*)Y, ldy,
+                                 (float*)((char*)ws + al256(sensing_ws_bytes(P))), st);
       break;
   }
   return cuda_status(e);

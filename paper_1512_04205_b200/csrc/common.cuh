@@ -95,8 +95,11 @@ cudaError_t launch_sketch_sparse(const cdmd_video& v, const SensingPlan& P, cons
                                  const int32_t* counts, int32_t* Y, int64_t ldy, cudaStream_t st);
 cudaError_t launch_sketch_rademacher(const cdmd_video& v, const SensingPlan& P, int32_t* Y,
                                      int64_t ldy, cudaStream_t st);
+// Gaussian: split-K partial sums go to `part` (gaussian_part_floats(v, p) floats of
+// the sketch workspace) and are reduced in a fixed order (deterministic Y)
+int64_t gaussian_part_floats(const cdmd_video& v, int64_t p);
 cudaError_t launch_sketch_gaussian(const cdmd_video& v, const SensingPlan& P, const uint16_t* table,
-                                   float* Y, int64_t ldy, cudaStream_t st);
+                                   float* Y, int64_t ldy, float* part, cudaStream_t st);
 
 cudaError_t launch_modes_simt(const cdmd_video& v, const cdmd_model& M, float* Phi, int64_t ldphi,
                               cudaStream_t st);

@@ -240,13 +240,48 @@ __global__ void __launch_bounds__(256) sketch_gaussian_simt_kernel(
 }
 
 bool sketch_gaussian_tc_supported(const cdmd_video& v);
-cudaError_t launch_sketch_gaussian_tc(const cdmd_video& v, const SensingPlan& P, const uint16_t* table, float* Y,
-                                      int64_t ldy, cudaStream_t st);
+int gaussian_tc_splits(const cdmd_video& v, int64_t p);
+cudaError_t launch_sketch_gaussian_tc(const cdmd_video& v, const SensingPlan& P, const uint16_t* table, float* part,
+                                      int* splits_out, cudaStream_t st);
+bool sketch_gaussian_tc2_supported(const cdmd_video& v);
+int gaussian_tc2_splits(const cdmd_video& v, int64_t p);
+cudaError_t launch_sketch_gaussian_tc2(const cdmd_video& v, const SensingPlan& P, const uint16_t* table, float* part,
+                                       int* splits_out, cudaStream_t st);
+
+// Y = sum over the split-K partial sums, in split order, in fp64 (deterministic)
+__global__ void __launch_bounds__(256) split_reduce_kernel(const float* __restrict__ part, int splits, int64_t p,
+                                                           int64_t m, float* __restrict__ Y, int64_t ldy) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= p * m) return;
+  const int64_t r = idx % p, t = idx / p;
+  double s = 0.0;
+  for (int q = 0; q < splits; ++q) s += (double)part[((int64_t)q * m + t) * p + r];
+  Y[r + t * ldy] = (float)s;
+}
+
+int64_t gaussian_part_floats(const cdmd_video& v, int64_t p) {
+  const int s1 = gaussian_tc_splits(v, p), s2 = gaussian_tc2_splits(v, p);
+  return (int64_t)(s1 > s2 ? s1 : s2) * v.m * p;
+}
 
 cudaError_t launch_sketch_gaussian(const cdmd_video& v, const SensingPlan& P, const uint16_t* table,
-                                   float* Y, int64_t ldy, cudaStream_t st) {
-  if (sketch_gaussian_tc_supported(v) && !getenv("CDMD_SIMT_SKETCH"))
-    return launch_sketch_gaussian_tc(v, P, table, Y, ldy, st);
+                                   float* Y, int64_t ldy, float* part, cudaStream_t st) {
+  if (!getenv("CDMD_SIMT_SKETCH") && part) {
+    // CTA pairs (sketch_tc2.cu) by default; CDMD_GAUSS_1CTA selects the single-CTA kernel
+    int splits = 0;
+    cudaError_t e = cudaErrorNotSupported;
+    if (sketch_gaussian_tc2_supported(v) && !getenv("CDMD_GAUSS_1CTA"))
+      e = launch_sketch_gaussian_tc2(v, P, table, part, &splits, st);
+    else if (sketch_gaussian_tc_supported(v))
+      e = launch_sketch_gaussian_tc(v, P, table, part, &splits, st);
+    if (e != cudaErrorNotSupported) {
+      if (e != cudaSuccess) return e;
+      const int64_t total = P.p * v.m;
+      note_launch();
+      split_reduce_kernel<<<(unsigned)ceil_div(total, 256), 256, 0, st>>>(part, splits, P.p, v.m, Y, ldy);
+      return cudaGetLastError();
+    }
+  }
   dim3 grid((unsigned)ceil_div(P.p, 64), (unsigned)ceil_div(v.m, 64));
   note_launch();
   sketch_gaussian_simt_kernel<<<grid, 256, 0, st>>>(v.X, v.ld, v.pix0, v.n_local, v.m, P.p, P.k0,

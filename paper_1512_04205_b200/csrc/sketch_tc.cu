@@ -248,7 +248,7 @@ constexpr int GS_THREADS = 32 * (2 + GS_GEN_WARPS + GS_CVT_WARPS);
 __global__ void __launch_bounds__(GS_THREADS, 1) sketch_gaussian_tc_kernel(
     const __grid_constant__ CUtensorMap mapX, int64_t pix0, int64_t n_local, int64_t m, int64_t p,
     uint32_t k0, uint32_t k1, const uint16_t* __restrict__ table_bf16, int npad, int nchunks_total,
-    int chunks_per_split, int xbox, float* __restrict__ Y, int64_t ldy) {
+    int chunks_per_split, int xbox, float* __restrict__ part) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];   // 1024-B aligned: swizzle atoms
   uint8_t* smem = smem_raw;
   const int BST = npad * GS_BK * 2;                     // bytes of a B stage (fp16)
@@ -406,7 +406,7 @@ __global__ void __launch_bounds__(GS_THREADS, 1) sketch_gaussian_tc_kernel(
         if (ry < p && nch > 0) {
 #pragma unroll
           for (int t = 0; t < 16; ++t)
-            if (c0 + t < m) atomicAdd(Y + ry + (int64_t)(c0 + t) * ldy, fmaf(128.0f, rowsum, __uint_as_float(v[t])));
+            if (c0 + t < m) part[((int64_t)blockIdx.y * m + c0 + t) * p + ry] = fmaf(128.0f, rowsum, __uint_as_float(v[t]));
         }
       }
     }
@@ -512,8 +512,21 @@ __global__ void __launch_bounds__(GS_THREADS, 1) sketch_gaussian_tc_kernel(
 
 bool sketch_gaussian_tc_supported(const cdmd_video& v) { return v.m + 1 <= 512 && (v.ld % 16) == 0 && sk_encode_fn() != nullptr; }
 
-cudaError_t launch_sketch_gaussian_tc(const cdmd_video& v, const SensingPlan& P, const uint16_t* table, float* Y,
-                                      int64_t ldy, cudaStream_t st) {
+int gaussian_tc_splits(const cdmd_video& v, int64_t p) {
+  const int nrb = (int)ceil_div(p, GS_BM);
+  const int nchunks = (int)ceil_div(v.n_local, GS_BK);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int splits = sms / nrb;   // one CTA per SM: a single wave
+  if (splits > nchunks) splits = nchunks;
+  if (splits < 1) splits = 1;
+  return (int)ceil_div(nchunks, ceil_div(nchunks, splits));
+}
+
+// part: splits x m x p fp32 partial sums (reduced by the caller)
+cudaError_t launch_sketch_gaussian_tc(const cdmd_video& v, const SensingPlan& P, const uint16_t* table, float* part,
+                                      int* splits_out, cudaStream_t st) {
   const int npad = (int)round_up(v.m + 1, 16);     // frames + the row of ones
   const int nrb = (int)ceil_div(P.p, GS_BM);
   const int nchunks = (int)ceil_div(v.n_local, GS_BK);
@@ -544,12 +557,11 @@ cudaError_t launch_sketch_gaussian_tc(const cdmd_video& v, const SensingPlan& P,
   const size_t smem = 1024 + 2 * (size_t)GS_A + 2 * (size_t)npad * GS_BK * 2 + (size_t)GS_XS * npad * GS_XK + 65536 + 512;
   cudaError_t e = cudaFuncSetAttribute(sketch_gaussian_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  e = cudaMemsetAsync(Y, 0, sizeof(float) * (size_t)ldy * v.m, st);
-  if (e != cudaSuccess) return e;
+  *splits_out = splits;
   dim3 grid((unsigned)nrb, (unsigned)splits);
   note_launch();
   sketch_gaussian_tc_kernel<<<grid, GS_THREADS, smem, st>>>(mapX, v.pix0, v.n_local, v.m, P.p, P.k0, P.k1, table, npad,
-                                                            nchunks, cps, xbox, Y, ldy);
+                                                            nchunks, cps, xbox, part);
   return cudaGetLastError();
 }
 

@@ -405,3 +405,26 @@ def test_streaming_lanes_equal_sequential(C, H):
         assert torch.equal(pipe.mask, mask), li
         assert pipe.model.k_eff == P.model.k_eff and pipe.model.K_eff == P.model.K_eff
         assert torch.equal(pipe.Phi, P.Phi), li
+
+
+def test_gaussian_sketch_deterministic_full_size(C, H, monkeypatch):
+    """Split-K partial sums are reduced in a fixed order: the 1080p Gaussian sketch is
+    bit-identical from run to run (a race between the CTA pair's producers and the
+    leader's MMAs would show up here), for the paired and the single-CTA kernels."""
+    cfg = config_by_name("c4_1080p_gaussian")
+    X = video_for(cfg)
+    m, n = X.shape
+    Xd = to_dev(X)
+    P = C.Pipeline(H, n, n, m, "gaussian", cfg.p, cfg.k, cfg.K)
+    ys = []
+    for single in (False, True):
+        if single:
+            monkeypatch.setenv("CDMD_GAUSS_1CTA", "1")
+        runs = [P.sketch(Xd).clone() for _ in range(3)]
+        torch.cuda.synchronize()
+        for r in runs[1:]:
+            assert torch.equal(r, runs[0]), single
+        ys.append(runs[0].double())
+    # the two kernels differ only in the split-K summation order
+    d = torch.linalg.norm(ys[0] - ys[1], dim=1) / torch.linalg.norm(ys[1], dim=1)
+    assert float(d.max()) <= PT.RTOL_Y_GAUSS
