@@ -76,7 +76,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G2_THREADS, 1) sketc
   uint64_t* tfull = xempty + G2_XS;
   uint64_t* lfullA = tfull + 1;                 // peer: its A half written (relayed to the leader)
   uint64_t* lfullB = lfullA + G2_S;             // peer: its B half written (relayed to the leader)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(lfullB + G2_S);
+  uint64_t* pfull = lfullB + G2_S;              // leader: the peer's A and B halves written (relay)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pfull + G2_S);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t crank = tc::cluster_ctarank();   // 0 = leader
@@ -91,8 +92,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G2_THREADS, 1) sketc
   if (warp == 0 && lane == 0) {
     for (int b = 0; b < G2_S; ++b) {
       // leader: its own producer warps + one relayed arrival from the peer
-      tc::mbar_init(&afull[b], G2_GEN + 1);
-      tc::mbar_init(&bfull[b], G2_CVT + 1);
+      tc::mbar_init(&afull[b], G2_GEN);
+      tc::mbar_init(&bfull[b], G2_CVT);
+      tc::mbar_init(&pfull[b], 1);
       tc::mbar_init(&sempty[b], 1);
       tc::mbar_init(&lfullA[b], G2_GEN);
       tc::mbar_init(&lfullB[b], G2_CVT);
@@ -123,6 +125,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G2_THREADS, 1) sketc
         const uint32_t ph = (uint32_t)(i / G2_S) & 1u;
         tc::mbar_wait(&afull[st], ph);
         tc::mbar_wait(&bfull[st], ph);
+        tc::mbar_wait(&pfull[st], ph);
         tc::fence_after();
         for (int h = 0; h < (N1 > 0 ? 2 : 1); ++h) {
           const int nn = h ? N1 : N0;
@@ -139,14 +142,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G2_THREADS, 1) sketc
       tc::mma2_commit_multicast(tfull, 0x3);
     } else if (lane == 0) {  // --------- peer: relay its stage readiness to the leader (one
       //                                  cluster-scope release per stage and operand)
-      const uint32_t af = tc::mapa(tc::smem_u32(afull), 0), bf = tc::mapa(tc::smem_u32(bfull), 0);
+      const uint32_t pf = tc::mapa(tc::smem_u32(pfull), 0);
       for (int i = 0; i < nch; ++i) {
         const int st = i % G2_S;
         const uint32_t ph = (uint32_t)(i / G2_S) & 1u;
         tc::mbar_wait(&lfullA[st], ph);
-        tc::mbar_arrive_cluster(af + 8u * (uint32_t)st);
         tc::mbar_wait(&lfullB[st], ph);
-        tc::mbar_arrive_cluster(bf + 8u * (uint32_t)st);
+        tc::mbar_arrive_cluster(pf + 8u * (uint32_t)st);   // one cluster-scope release per stage
       }
     }
   } else if (warp == wtma) {
@@ -351,7 +353,7 @@ cudaError_t launch_sketch_gaussian_tc2(const cdmd_video& v, const SensingPlan& P
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return cudaErrorInvalidValue;
   const size_t brows = (size_t)(N0 + N1) / 2;
-  const size_t smem = 1024 + (size_t)G2_S * (G2_A + brows * G2_BK * 2) + (size_t)G2_XS * brows * G2_XK + 65536 + 512;
+  const size_t smem = 1024 + (size_t)G2_S * (G2_A + brows * G2_BK * 2) + (size_t)G2_XS * brows * G2_XK + 65536 + 768;
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
   cudaError_t e = cudaFuncSetAttribute(sketch_gaussian_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
