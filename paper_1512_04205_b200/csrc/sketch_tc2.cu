@@ -28,10 +28,15 @@ constexpr int G2_BK = 32;                  // pixels per stage (64-B fp16 rows, 
 constexpr int G2_A = G2_BM * G2_BK * 2;    // bytes of an A stage (8 KB)
 constexpr int G2_XK = 64;                  // pixels per uint8 X stage (64-B TMA rows)
 constexpr int G2_XS = 2;                   // X stages
+#ifndef G2_GRP_DEF
+#define G2_GRP_DEF 2
+#endif
+constexpr int G2_GRP = G2_GRP_DEF;         // stages per producer->MMA hand-off
 #ifndef G2_S_DEF
-#define G2_S_DEF 5
+#define G2_S_DEF 4
 #endif
 constexpr int G2_S = G2_S_DEF;             // A/B stages
+constexpr int G2_NG = G2_S / G2_GRP;       // hand-off groups in flight
 constexpr int G2_GEN = 8;                  // generator warps
 constexpr int G2_CVT = 8;                  // converter warps
 constexpr int G2_THREADS = 32 * (2 + G2_GEN + G2_CVT);
@@ -122,11 +127,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G2_THREADS, 1) sketc
       const uint32_t aBase = tc::smem_u32(sA), bBase = tc::smem_u32(sB);
       for (int i = 0; i < nch; ++i) {
         const int st = i % G2_S;
-        const uint32_t ph = (uint32_t)(i / G2_S) & 1u;
-        tc::mbar_wait(&afull[st], ph);
-        tc::mbar_wait(&bfull[st], ph);
-        tc::mbar_wait(&pfull[st], ph);
-        tc::fence_after();
+        const int gs = (i / G2_GRP) % G2_NG;
+        const uint32_t ph = (uint32_t)(i / (G2_GRP * G2_NG)) & 1u;
+        if (i % G2_GRP == 0) {   // a group of G2_GRP stages is handed over at once
+          tc::mbar_wait(&afull[gs], ph);
+          tc::mbar_wait(&bfull[gs], ph);
+          tc::mbar_wait(&pfull[gs], ph);
+          tc::fence_after();
+        }
         for (int h = 0; h < (N1 > 0 ? 2 : 1); ++h) {
           const int nn = h ? N1 : N0;
           const uint32_t idesc = tc::idesc_f16(2 * G2_BM, nn, false, false, false, false);
@@ -137,18 +145,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G2_THREADS, 1) sketc
             tc::mma2_f16(tmem_base + (uint32_t)(256 * h), ad, bd, idesc, (i | kk) != 0);
           }
         }
-        tc::mma2_commit_multicast(&sempty[st], 0x3);
+        if (i % G2_GRP == G2_GRP - 1 || i == nch - 1) tc::mma2_commit_multicast(&sempty[gs], 0x3);
       }
       tc::mma2_commit_multicast(tfull, 0x3);
     } else if (lane == 0) {  // --------- peer: relay its stage readiness to the leader (one
       //                                  cluster-scope release per stage and operand)
       const uint32_t pf = tc::mapa(tc::smem_u32(pfull), 0);
-      for (int i = 0; i < nch; ++i) {
-        const int st = i % G2_S;
-        const uint32_t ph = (uint32_t)(i / G2_S) & 1u;
-        tc::mbar_wait(&lfullA[st], ph);
-        tc::mbar_wait(&lfullB[st], ph);
-        tc::mbar_arrive_cluster(pf + 8u * (uint32_t)st);   // one cluster-scope release per stage
+      for (int gi = 0; gi * G2_GRP < nch; ++gi) {
+        const int gs = gi % G2_NG;
+        const uint32_t ph = (uint32_t)(gi / G2_NG) & 1u;
+        tc::mbar_wait(&lfullA[gs], ph);
+        tc::mbar_wait(&lfullB[gs], ph);
+        tc::mbar_arrive_cluster(pf + 8u * (uint32_t)gs);   // one cluster-scope release per group
       }
     }
   } else if (warp == wtma) {
@@ -175,7 +183,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G2_THREADS, 1) sketc
     const uint32_t ctr0 = (uint32_t)(pix0 >> 3) + (uint32_t)(c_begin * (G2_BK / 8) + q0);
     for (int i = 0; i < nch; ++i) {
       const int st = i % G2_S;
-      const uint32_t ph = (uint32_t)(i / G2_S) & 1u;
+      const int gs = (i / G2_GRP) % G2_NG;
+      const uint32_t ph = (uint32_t)(i / (G2_GRP * G2_NG)) & 1u;
+      const bool gend = i % G2_GRP == G2_GRP - 1 || i == nch - 1;
       uint32_t h2[NQ][4];
 #pragma unroll
       for (int c = 0; c < NQ; ++c) {
@@ -194,16 +204,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G2_THREADS, 1) sketc
           h2[c][q] = (e0 | (e1 << 16)) ^ sg;
         }
       }
-      tc::mbar_wait(&sempty[st], ph ^ 1u);
+      if (i % G2_GRP == 0) tc::mbar_wait(&sempty[gs], ph ^ 1u);
 #pragma unroll
       for (int c = 0; c < NQ; ++c) {
         const int q8 = q0 + c * (G2_GEN / 4);
         *reinterpret_cast<uint4*>(sA + st * G2_A + rr * 64 + ((q8 ^ swz) << 4)) =
             make_uint4(h2[c][0], h2[c][1], h2[c][2], h2[c][3]);
       }
-      tc::fence_proxy_async();
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(crank == 0 ? &afull[st] : &lfullA[st]);
+      if (gend) {
+        tc::fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(crank == 0 ? &afull[gs] : &lfullA[gs]);
+      }
     }
     if (warp <= 4) {  // epilogue: TMEM lane = row of C, column t = frame, column m = sum_i c_ri
       tc::mbar_wait(tfull, 0);
@@ -241,7 +253,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G2_THREADS, 1) sketc
     brow[1] = h0r + fl;
     for (int i = 0; i < nch; ++i) {
       const int st = i % G2_S;
-      const uint32_t ph = (uint32_t)(i / G2_S) & 1u;
+      const int gs = (i / G2_GRP) % G2_NG;
+      const uint32_t ph = (uint32_t)(i / (G2_GRP * G2_NG)) & 1u;
+      const bool gend = i % G2_GRP == G2_GRP - 1 || i == nch - 1;
       const int xi = i >> 1, xs = xi % G2_XS;
       if ((i & 1) == 0) tc::mbar_wait(&xfull[xs], (uint32_t)(xi / G2_XS) & 1u);
       const uint8_t* xt = sX + (size_t)xs * XST + G2_BK * (i & 1) + 16 * hf;
@@ -281,7 +295,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G2_THREADS, 1) sketc
           }
         }
       }
-      tc::mbar_wait(&sempty[st], ph ^ 1u);
+      if (i % G2_GRP == 0) tc::mbar_wait(&sempty[gs], ph ^ 1u);
       uint8_t* bst = sB + (size_t)st * BST;
 #pragma unroll
       for (int u = 0; u < 2; ++u) {
@@ -295,7 +309,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G2_THREADS, 1) sketc
       __syncwarp();
       if (lane == 0) {
         if ((i & 1) || i == nch - 1) tc::mbar_arrive(&xempty[xs]);
-        tc::mbar_arrive(crank == 0 ? &bfull[st] : &lfullB[st]);
+        if (gend) tc::mbar_arrive(crank == 0 ? &bfull[gs] : &lfullB[gs]);
       }
     }
   }
