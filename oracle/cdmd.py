@@ -5,7 +5,9 @@ numpy.linalg (LAPACK) is used only for the small SVD / eig / lstsq steps.
 
 Steps, in the paper's order and notation:
   fit()        Alg. 1 steps 1, 4, 6, 7 + Remark 3 OMP
-               + omega = log(lambda)/dt (P:153-157)
+               + omega = log(lambda)/dt; the target rank fixed, or
+               (rank="gd") chosen by the Gavish-Donoho optimal hard threshold
+               (Remark 2; evaluation settings P:573) via optimal_rank()
   modes()      Alg. 1 step 8, Eq. cDMDModes  Phi = X' V S^-1 W
   background() Eq. DMDTerms (P:185-193): L = Re sum_{p in S} b_p phi_p lambda_p^{t-1}
                (dynamic) or x_BG = Re Phi beta (static)
@@ -115,7 +117,25 @@ def omp(D, y, K, stop_rtol=OMP_STOP_RTOL, tie_rtol=TIE_RTOL):
     return S, beta
 
 
-def fit(Yfull, k, K, dt=1.0, rank_rtol=RANK_RTOL):
+def omega_beta(beta):
+    """Gavish-Donoho unknown-noise coefficient omega(beta) ~ 0.56 b^3 - 0.95 b^2 + 1.82 b + 1.43
+    (the cubic approximation of the cited work; SPEC optimal_rank)."""
+    return 0.56 * beta ** 3 - 0.95 * beta ** 2 + 1.82 * beta + 1.43
+
+
+def optimal_rank(s, rows, cols):
+    """Remark 2: number of singular values above tau = omega(beta) median(s),
+    beta = min(rows, cols) / max(rows, cols); s = ALL singular values of the rows x cols
+    matrix.  At least 1."""
+    s = np.asarray(s, dtype=np.float64)
+    if s.size == 0:
+        raise ValueError("empty singular-value vector")
+    beta = min(rows, cols) / max(rows, cols)
+    tau = omega_beta(beta) * np.median(s)
+    return max(int(np.count_nonzero(s > tau)), 1)
+
+
+def fit(Yfull, k, K, dt=1.0, rank_rtol=RANK_RTOL, rank="fixed"):
     """cDMD small solve from the full sketch Y_full = C D (p x m).
 
     Y = Y_full[:, :m-1], Y' = Y_full[:, 1:] (Eq. FullData; reading R2).
@@ -129,6 +149,10 @@ def fit(Yfull, k, K, dt=1.0, rank_rtol=RANK_RTOL):
     Y, Yp = Yfull[:, :m - 1], Yfull[:, 1:]
     U, s, Vh = np.linalg.svd(Y, full_matrices=False)
     k = min(k, len(s))
+    if rank == "gd":      # Remark 2: k = optimal hard-threshold rank, at most k
+        k = min(k, optimal_rank(s, p, m - 1))
+    elif rank != "fixed":
+        raise ValueError(rank)
     U, s, V = U[:, :k], s[:k], Vh[:k].T
     keep = s > rank_rtol * s[0] if s.size and s[0] > 0 else np.zeros(k, dtype=bool)
     k_eff = int(np.count_nonzero(keep))
