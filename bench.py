@@ -164,6 +164,8 @@ def main():
     ap.add_argument("--impl", default="cdmd", choices=["cdmd", "reference"])
     ap.add_argument("--config", default="c4_1080p_sparse")
     ap.add_argument("--bg", default="dynamic", choices=["dynamic", "static"])
+    ap.add_argument("--rank", default="fixed", choices=["fixed", "gd"],
+                    help="target rank: the config's k, or Gavish-Donoho (Remark 2, P:361) with k as the cap")
     ap.add_argument("--ref-frac", type=int, default=32)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -194,7 +196,7 @@ def main():
     Xd = torch.zeros((m, ld), dtype=torch.uint8, device="cuda")
     Xd[:, :nl] = torch.from_numpy(X_host).cuda()
     H = C.Handle(local)
-    P = C.Pipeline(H, n, nl, m, cfg.kind, cfg.p, cfg.k, cfg.K, seed=cfg.sensing_seed, pix0=pix0)
+    P = C.Pipeline(H, n, nl, m, cfg.kind, cfg.p, cfg.k, cfg.K, seed=cfg.sensing_seed, pix0=pix0, rank=args.rank)
     mode = C.BG_DYNAMIC if args.bg == "dynamic" else C.BG_STATIC
     stream = torch.cuda.current_stream()
     ev = {s: [] for s in ("sketch", "allreduce", "fit", "modes", "foreground")}
@@ -254,7 +256,7 @@ def main():
     if args.lanes > 1:
         # K batches through `lanes` concurrent lanes; each lane reads its own copy of X
         S = C.Streaming(local, n, nl, m, cfg.kind, cfg.p, cfg.k, cfg.K, lanes=args.lanes,
-                        seed=cfg.sensing_seed, pix0=pix0)
+                        seed=cfg.sensing_seed, pix0=pix0, rank=args.rank)
         Xs = [Xd] + [Xd.clone() for _ in range(args.lanes - 1)]
         ar = (lambda Y: dist.all_reduce(Y, op=dist.ReduceOp.SUM)) if world > 1 else None
 
@@ -389,7 +391,7 @@ def main():
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8",
             "data": "synthetic",
             "config": {"workload": cfg.name, "video": f"{cfg.width}x{cfg.height}x{m}", "sensing": cfg.kind,
-                       "p": cfg.p, "k": cfg.k, "K": cfg.K, "tau": cfg.tau, "background": args.bg,
+                       "p": cfg.p, "k": cfg.k, "K": cfg.K, "tau": cfg.tau, "background": args.bg, "rank": args.rank,
                        "parallelism": f"pixel-rows x{world}", "l2": "inputs larger than L2 (X = %.2f GB)" % (n * m / 1e9),
                        "k_eff": ke, "K_eff": P.model.K_eff, "n_coef": nc},
             "stage_ms": {s: round(v, 4) for s, v in stage_ms.items()},

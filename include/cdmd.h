@@ -152,10 +152,16 @@ CDMD_API cdmd_status cdmd_sketch(cdmd_handle h, const cdmd_video* v, const cdmd_
  * cuSOLVER), M = V S^-1 W (P:346 without X'), Remark 3 OMP on Phi_Y = Y' M
  * against y_1 (Gram form of Rubinstein et al.), omega =
  * log(lambda)/dt, the background coefficient table, and the
- * fixed-point limbs of M for cdmd_modes.  BLOCKING: returns after the model is
- * complete.  Errors: CDMD_ERR_RANGE if k < 1, k > min(p, m-1), K < 1 or
- * K > k; CDMD_ERR_NUMERIC if the eigensolvers fail or every sigma is dropped
- * (model->info holds the solver info). */
+ * fixed-point limbs of M for cdmd_modes.  Target rank: k > 0 fixes it (the
+ * configs); k < 0 chooses it by the Gavish-Donoho optimal hard threshold (Remark 2,
+ * P:361; the paper's evaluation settings): sigma_j > omega(beta) median(sigma)
+ * over all min(p, m-1) singular values of Y, omega(b) = 0.56 b^3 - 0.95 b^2 + 1.82 b
+ * + 1.43, b = min(p, m-1) / max(p, m-1), at most -k and at least 1; the result is
+ * model->k_eff.  BLOCKING: returns after the model is complete.  Errors:
+ * CDMD_ERR_RANGE if |k| < 1, |k| > min(p, m-1), K < 1 or K > |k|;
+ * CDMD_ERR_UNSUPPORTED for k < 0 when m - 1 > 510 (that size's eigensolver returns
+ * only the k largest eigenvalues); CDMD_ERR_NUMERIC if the eigensolvers fail or
+ * every sigma is dropped (model->info holds the solver info). */
 CDMD_API size_t cdmd_model_bytes(int k, int K, int64_t m);
 CDMD_API cdmd_status cdmd_model_bind(cdmd_model* model, void* dev_buf, size_t bytes, int k, int K, int64_t m);
 CDMD_API size_t cdmd_fit_workspace_bytes(cdmd_handle h, int64_t p, int64_t m, int k);

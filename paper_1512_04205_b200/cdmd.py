@@ -262,7 +262,11 @@ class Pipeline:
     five-call hot path sketch -> [all-reduce] -> fit -> modes -> foreground."""
 
     def __init__(self, handle, n_total, n_local, m, kind, p, k, K, s=0.0, seed=0, pix0=0,
-                 device="cuda", dt=1.0):
+                 device="cuda", dt=1.0, rank="fixed"):
+        """rank="fixed": target rank k; rank="gd": Gavish-Donoho rank, at most k (Remark 2)."""
+        if rank not in ("fixed", "gd"):
+            raise ValueError(rank)
+        self.rank = rank
         self.h = handle
         self.kind = KINDS[kind] if isinstance(kind, str) else int(kind)
         self.n_total, self.n_local, self.m, self.p, self.k, self.K = n_total, n_local, m, p, k, K
@@ -285,7 +289,8 @@ class Pipeline:
         return self.Y
 
     def fit(self, stream=None):
-        cdmd_fit(self.h, self.Y, self.kind, self.p, self.m, self.k, self.K, self.model, self.ws_fit,
+        k = -self.k if self.rank == "gd" else self.k
+        cdmd_fit(self.h, self.Y, self.kind, self.p, self.m, k, self.K, self.model, self.ws_fit,
                  self.dt, stream)
         return self.model
 
@@ -323,7 +328,8 @@ class Streaming:
     With torch.distributed initialised, the per-batch all-reduces are issued in batch
     order on every rank (a ticket lock), so collectives match across ranks."""
 
-    def __init__(self, device, n_total, n_local, m, kind, p, k, K, lanes=4, s=0.0, seed=0, pix0=0, dt=1.0):
+    def __init__(self, device, n_total, n_local, m, kind, p, k, K, lanes=4, s=0.0, seed=0, pix0=0, dt=1.0,
+                 rank="fixed"):
         import threading
         self.lanes = []
         lo, hi = torch.cuda.Stream.priority_range()
@@ -336,7 +342,7 @@ class Streaming:
             st_fit = torch.cuda.Stream(device=device, priority=hi)
             with torch.cuda.stream(st):
                 pipe = Pipeline(h, n_total, n_local, m, kind, p, k, K, s=s, seed=seed, pix0=pix0,
-                                device=f"cuda:{device}", dt=dt)
+                                device=f"cuda:{device}", dt=dt, rank=rank)
             self.lanes.append((h, st, st_fit, pipe))
         self._cv = threading.Condition()
         self._next_ar = 0

@@ -252,8 +252,9 @@ cdmd_status cdmd_fit(cdmd_handle h, const void* Y, int64_t ldy, int32_t kind, in
   if (!h || !Y || !model || !ws) return CDMD_ERR_ARG;
   if (kind < CDMD_SPIXEL || kind > CDMD_GAUSSIAN) return CDMD_ERR_ARG;
   if (m < 2 || p < 1) return CDMD_ERR_RANGE;
-  if (k < 1 || k > p || k > m - 1 || k > model->k) return CDMD_ERR_RANGE;  // P:355 "p >= k"
-  if (K < 1 || K > k || K > model->K) return CDMD_ERR_RANGE;
+  const int kmax = k < 0 ? -k : k;   // k < 0: Gavish-Donoho rank, at most -k (Remark 2)
+  if (kmax < 1 || kmax > p || kmax > m - 1 || kmax > model->k) return CDMD_ERR_RANGE;  // P:355 "p >= k"
+  if (K < 1 || K > kmax || K > model->K) return CDMD_ERR_RANGE;
   if (ldy < p || !(dt > 0.0)) return CDMD_ERR_ARG;
   if (model->m != m) return CDMD_ERR_ARG;
   if ((reinterpret_cast<uintptr_t>(ws) & 255) != 0) return CDMD_ERR_ARG;

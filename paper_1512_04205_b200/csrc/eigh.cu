@@ -317,12 +317,17 @@ __device__ __forceinline__ void eh_sturm_multi(int n, const double* __restrict__
 // One warp per wanted eigenvalue: 128-point multisection (7 bits per round; four
 // points per lane) on Sturm counts.  The (r+1)-th largest eigenvalue (ascending
 // index n-1-r) goes to lam[k-1-r].
+// Blocks k and k + 1 (when med_cnt > 0) compute the eigenvalues of descending rank
+// (med_cnt - 1) / 2 and med_cnt / 2 into med[0], med[1]: the median of the med_cnt
+// largest eigenvalues (Gavish-Donoho rank, Remark 2).
 __global__ void __launch_bounds__(32) eh_bisect_kernel(int n, int k, const double* __restrict__ d,
                                                        const double* __restrict__ e2,
                                                        const double* __restrict__ bounds,
-                                                       double* __restrict__ lam) {
-  const int r = blockIdx.x, lane = threadIdx.x;
-  if (r >= k) return;
+                                                       double* __restrict__ lam, int med_cnt,
+                                                       double* __restrict__ med) {
+  const int r0 = blockIdx.x, lane = threadIdx.x;
+  if (r0 >= k + (med_cnt > 0 ? 2 : 0)) return;
+  const int r = r0 < k ? r0 : (r0 == k ? (med_cnt - 1) / 2 : med_cnt / 2);
   const int idx = n - 1 - r;
   double lo = bounds[0], hi = bounds[1];
   const double pivmin = bounds[3];
@@ -347,7 +352,10 @@ __global__ void __launch_bounds__(32) eh_bisect_kernel(int n, int k, const doubl
     lo = nlo;
     hi = nhi;
   }
-  if (lane == 0) lam[k - 1 - r] = 0.5 * (lo + hi);
+  if (lane == 0) {
+    if (r0 < k) lam[k - 1 - r] = 0.5 * (lo + hi);
+    else med[r0 - k] = 0.5 * (lo + hi);
+  }
 }
 
 // Inverse iteration on T - lambda I (LU with partial pivoting), one warp per group
@@ -553,8 +561,9 @@ size_t eh_work_doubles(int n, int k) {
 // G (n x n, ld ldg) -> lam[k] (ascending: the k largest), Zout (n x k column-major, ld n).
 void eh_prof_read(unsigned long long* out) { cudaMemcpyFromSymbol(out, g_eh_prof, sizeof(unsigned long long) * 8); }
 
+// med_cnt > 0: also the median of the med_cnt largest eigenvalues into med[0..1]
 cudaError_t launch_eh(int n, int k, const double* G, int64_t ldg, double* lam, double* Zout, double* work,
-                      int* info, cudaStream_t st) {
+                      int* info, int med_cnt, double* med, cudaStream_t st) {
   double* V = work;
   double* d = V + (size_t)n * n;
   double* e = d + n;
@@ -571,7 +580,7 @@ cudaError_t launch_eh(int n, int k, const double* G, int64_t ldg, double* lam, d
   note_launch();
   eh_prep_kernel<<<1, 256, 0, st>>>(n, d, e, e2, bounds);
   note_launch();
-  eh_bisect_kernel<<<k, 32, 0, st>>>(n, k, d, e2, bounds, lam);
+  eh_bisect_kernel<<<k + (med_cnt > 0 ? 2 : 0), 32, 0, st>>>(n, k, d, e2, bounds, lam, med_cnt, med);
   note_launch();
   const size_t smem2 = sizeof(double) * 5 * (size_t)n + (size_t)n + 16;
   err = cudaFuncSetAttribute(eh_invit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);

@@ -45,7 +45,7 @@ bool eh_supported(int n, int k);
 void eh_prof_read(unsigned long long* out);
 size_t eh_work_doubles(int n, int k);
 cudaError_t launch_eh(int n, int k, const double* G, int64_t ldg, double* lam, double* Zout, double* work,
-                      int* info, cudaStream_t st);
+                      int* info, int med_cnt, double* med, cudaStream_t st);
 
 // symmetric eigensolver: the 8-CTA cluster solver (eigh.cu, default for n1 <= 510),
 // CDMD_SYEV=d -> cuSOLVER syevd, CDMD_SYEV=dx -> cuSOLVER syevdx
@@ -143,9 +143,13 @@ __global__ void to_f64_kernel(const T* __restrict__ Y, int64_t ldy, int64_t p, i
 
 // sigma_j = sqrt(w), descending; V = matching eigenvectors; k_eff.  Eigen-pairs
 // are ascending in (w, A); the largest sits at index `top`.
+// gd_omega > 0: also keep only sigma_j > gd_omega * median(sigma) (Gavish-Donoho optimal
+// hard threshold, Remark 2), the median of the med_cnt largest eigenvalues'
+// square roots taken from med[0..1] (or, med == nullptr, from the full ascending w)
 __global__ void select_topk_kernel(const double* __restrict__ A, const double* __restrict__ w,
                                    int64_t n1, int64_t top, int k, double* __restrict__ V,
-                                   double* __restrict__ sigma, int* __restrict__ dinfo) {
+                                   double* __restrict__ sigma, int* __restrict__ dinfo, double gd_omega,
+                                   int med_cnt, const double* __restrict__ med) {
   const int c = blockIdx.x;  // output column
   const int64_t src = top - c;
   const double s0 = sqrt(fmax(w[top], 0.0));
@@ -154,9 +158,18 @@ __global__ void select_topk_kernel(const double* __restrict__ A, const double* _
     const double s = sqrt(fmax(w[src], 0.0));
     sigma[c] = s;
     if (c == 0) {
+      double thr = RANK_RTOL * s0;
+      if (gd_omega > 0.0) {
+        double ma, mb;   // eigenvalues of descending ranks (cnt-1)/2 and cnt/2
+        if (med) { ma = med[0]; mb = med[1]; }
+        else { ma = w[n1 - 1 - (med_cnt - 1) / 2]; mb = w[n1 - 1 - med_cnt / 2]; }
+        const double msig = 0.5 * (sqrt(fmax(ma, 0.0)) + sqrt(fmax(mb, 0.0)));
+        thr = fmax(thr, gd_omega * msig);
+      }
       int ke = 0;
       for (int j = 0; j < k; ++j)
-        if (sqrt(fmax(w[top - j], 0.0)) > RANK_RTOL * s0) ++ke; else break;
+        if (sqrt(fmax(w[top - j], 0.0)) > thr) ++ke; else break;
+      if (gd_omega > 0.0 && ke == 0 && s0 > 0.0) ke = 1;   // at least one (the rule's floor)
       dinfo[INFO_K_EFF] = ke;
     }
   }
@@ -538,6 +551,9 @@ struct FitProf {
 cdmd_status fit_impl(cdmd_handle h, const void* Y, int64_t ldy, int kind, int64_t p, int64_t m,
                      int k, int K, double dt, cdmd_model* model, void* ws, size_t ws_bytes,
                      cudaStream_t st) {
+  // k < 0: the Gavish-Donoho optimal hard-threshold rank (Remark 2), at most -k
+  const bool gd = k < 0;
+  if (gd) k = -k;
   FitWs W{};
   cdmd_status s0 = layout_ws(h, p, m, k, (char*)ws, &W);
   if (s0 != CDMD_OK) return s0;
@@ -574,10 +590,16 @@ cdmd_status fit_impl(cdmd_handle h, const void* Y, int64_t ldy, int kind, int64_
   if (h->host_ws.size() < hneed + 16) h->host_ws.resize(hneed + 16);
   int64_t top = n1 - 1;
   const int smode = syev_mode((int)n1, k);
+  // the median singular value runs over all min(p, m-1) singular values of Y
+  const int med_cnt = gd ? (int)(p < n1 ? p : n1) : 0;
+  const double beta = (double)(p < n1 ? p : n1) / (double)(p < n1 ? n1 : p);
+  const double gd_omega = gd ? 0.56 * beta * beta * beta - 0.95 * beta * beta + 1.82 * beta + 1.43 : 0.0;
+  double* med = W.ehw + eh_work_doubles((int)n1, k) - 8;   // two doubles of the eigh workspace slack
+  if (gd && smode == 2) return CDMD_ERR_UNSUPPORTED;      // syevdx computes only the k largest
   if (smode == 0) {
     // cluster tridiagonalisation + bisection + inverse iteration; k largest pairs
     // written ascending into (W.w, W.A) like syevdx
-    CU(launch_eh((int)n1, k, W.G, m, W.w, W.A, W.ehw, W.dinfo + 8, st));
+    CU(launch_eh((int)n1, k, W.G, m, W.w, W.A, W.ehw, W.dinfo + 8, med_cnt, med, st));
     top = k - 1;
   } else if (smode == 2) {
     // only the k largest eigenpairs (1-based indices n1-k+1 .. n1, ascending)
@@ -599,7 +621,8 @@ cdmd_status fit_impl(cdmd_handle h, const void* Y, int64_t ldy, int kind, int64_
   }
   prof.mark("syevd");
   note_launch();
-  select_topk_kernel<<<k, 128, 0, st>>>(W.A, W.w, n1, top, k, W.V, model->sigma, W.dinfo);
+  select_topk_kernel<<<k, 128, 0, st>>>(W.A, W.w, n1, top, k, W.V, model->sigma, W.dinfo, gd_omega, med_cnt,
+                                        smode == 0 ? med : nullptr);
   CU(cudaGetLastError());
   CU(cudaMemcpyAsync(h->host_info, W.dinfo, sizeof(int) * 16, cudaMemcpyDeviceToHost, st));
   CU(cudaStreamSynchronize(st));

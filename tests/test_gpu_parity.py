@@ -41,10 +41,10 @@ def to_dev(X, ld=None):
     return buf
 
 
-def gpu_run(C, H, X, kind, p, k, K, tau, s=0.0, seed=0, modes_simt=False, ld=None):
+def gpu_run(C, H, X, kind, p, k, K, tau, s=0.0, seed=0, modes_simt=False, ld=None, rank="fixed"):
     m, n = X.shape
     Xd = to_dev(X, ld)
-    P = C.Pipeline(H, n, n, m, kind, p, k, K, s=s, seed=seed)
+    P = C.Pipeline(H, n, n, m, kind, p, k, K, s=s, seed=seed, rank=rank)
     Y = P.sketch(Xd).cpu().numpy().T.copy()          # p x m
     P.fit()
     mh = C.model_to_host(P.model)
@@ -59,9 +59,9 @@ def gpu_run(C, H, X, kind, p, k, K, tau, s=0.0, seed=0, modes_simt=False, ld=Non
     return out
 
 
-def oracle_run(X, kind, p, k, K, tau, s=None, seed=0):
+def oracle_run(X, kind, p, k, K, tau, s=None, seed=0, rank="fixed"):
     Y = OS.sketch(X, KIND[kind], p, seed, s=s)
-    model = OD.fit(Y, k, K)
+    model = OD.fit(Y, k, K, rank=rank)
     Phi = OD.modes(X, model["M"])
     Ld = OD.background_dynamic(Phi, model)          # n x m
     Ls = OD.background_static(Phi, model)           # n
@@ -428,3 +428,25 @@ def test_gaussian_sketch_deterministic_full_size(C, H, monkeypatch):
     # the two kernels differ only in the split-K summation order
     d = torch.linalg.norm(ys[0] - ys[1], dim=1) / torch.linalg.norm(ys[1], dim=1)
     assert float(d.max()) <= PT.RTOL_Y_GAUSS
+
+
+@pytest.mark.parametrize("case", ["c1", "ragged_sparse", "rademacher_small", "c2"])
+def test_pipeline_parity_gavish_donoho(C, H, case):
+    """Automatic target rank (Remark 2): the device's Gavish-Donoho rank
+    (median singular value by bisection on the tridiagonal form) equals the oracle's,
+    and the rest of the path keeps parity at that rank."""
+    if case == "c2":
+        cfg = config_by_name("c2_320x240_spixel")
+        X, kind, p, k, K, tau = video_for(cfg), cfg.kind, cfg.p, cfg.k, cfg.K, cfg.tau
+    else:
+        name, shape, kind, p, k, K, tau = next(c for c in CASES if c[0] == case)
+        if shape is None:
+            X = video_for(config_by_name("c1_32x24_sparse"))
+        else:
+            W, Hh, m, noise, rects = shape
+            X = make_video(W, Hh, m, seed=zlib.crc32(name.encode()) % 1000, noise=noise, n_rects=rects)
+    g = gpu_run(C, H, X, kind, p, k, K, tau, rank="gd")
+    o = oracle_run(X, kind, p, k, K, tau, rank="gd")
+    assert g["model"]["k_eff"] == o["model"]["k_eff"]
+    assert 1 <= o["model"]["k_eff"] <= k
+    check_all(g, o, kind, tau)
