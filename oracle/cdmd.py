@@ -12,6 +12,7 @@ Steps, in the paper's order and notation:
   background() Eq. DMDTerms (P:185-193): L = Re sum_{p in S} b_p phi_p lambda_p^{t-1}
                (dynamic) or x_BG = Re Phi beta (static)
   mask()       Eq. thres: 1 iff |x_jt - xhat_j| > tau
+  median3()    the 3x3 median post-filter of the mask (Fig. 7)
 
 Readings of silent / garbled passages are listed in DESIGN.md §4 (R1..R20) and
 cited inline as "reading Rn".
@@ -214,6 +215,26 @@ def mask(X, L, tau):
     L = np.asarray(L, dtype=np.float64)
     Lt = L[None, :] if L.ndim == 1 else L.T
     return np.abs(Xf - Lt) > tau
+
+
+def median3(Mb, width, height):
+    """3x3 spatial median of each frame's binary mask (the "in addition median filtered
+    foreground mask" of Fig. 7; SPEC median3).  On a binary image the median of
+    the 9 values is the majority: bit = 1 iff at least 5 of the 3x3 neighbourhood are
+    set.  Outside the image counts as 0 (zero padding, reading R22).
+    Mb: bool (m, n) with n = width * height, pixel j = y * width + x.  Returns bool (m, n)."""
+    Mb = np.asarray(Mb, dtype=bool)
+    m, n = Mb.shape
+    if n != width * height:
+        raise ValueError("mask is not whole frames")
+    F = Mb.reshape(m, height, width).astype(np.int32)
+    P = np.zeros((m, height + 2, width + 2), dtype=np.int32)
+    P[:, 1:-1, 1:-1] = F
+    cnt = np.zeros_like(F)
+    for dy in range(3):
+        for dx in range(3):
+            cnt += P[:, dy:dy + height, dx:dx + width]
+    return (cnt >= 5).reshape(m, n)
 
 
 def pack_mask(Mb):
