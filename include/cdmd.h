@@ -195,6 +195,18 @@ CDMD_API cdmd_status cdmd_foreground(cdmd_handle h, const cdmd_video* v, const c
                             const float* Phi, int64_t ldphi, int32_t mode, float tau,
                             uint32_t* mask, int64_t ldw, cdmd_stream st);
 
+/* ------------------------------------------------------------ median post-filter
+ * The "in addition median filtered foreground mask" (Fig. 7): a 3x3 spatial
+ * median of every frame's mask (on a binary image: bit = 1 iff >= 5 of the 3x3
+ * neighbourhood are set), zero outside the frame (reading R22).  mask and
+ * out: m frames of ldw uint32 words (bit j % 32 of word j / 32, pixel j = y width + x)
+ * covering WHOLE frames (n = width * height pixels, ldw >= ceil(n / 32)); out must
+ * not alias mask.  A pixel-row-sharded run needs the neighbouring image rows, so
+ * call it on gathered whole frames.  Errors: CDMD_ERR_ARG on null pointers, aliasing
+ * or ldw too small; CDMD_ERR_RANGE if width, height or m < 1. */
+CDMD_API cdmd_status cdmd_mask_median3(const uint32_t* mask, int64_t ldw, int64_t width, int64_t height,
+                                       int64_t m, uint32_t* out, cdmd_stream st);
+
 /* ------------------------------------------------ test hooks (same contract)
  * Export what the device generates so tests can compare it bit for bit with the
  * oracle's definitions. */

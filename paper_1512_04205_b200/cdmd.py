@@ -58,7 +58,7 @@ SYMBOLS = ["cdmd_create", "cdmd_destroy", "cdmd_status_str", "cdmd_version", "cd
            "cdmd_sketch_workspace_bytes", "cdmd_sketch", "cdmd_model_bytes", "cdmd_model_bind",
            "cdmd_fit_workspace_bytes", "cdmd_fit", "cdmd_modes", "cdmd_background",
            "cdmd_foreground", "cdmd_philox", "cdmd_gaussian_table", "cdmd_sparse_cap",
-           "cdmd_sensing_rows", "cdmd_modes_simt", "cdmd_eig"]
+           "cdmd_sensing_rows", "cdmd_modes_simt", "cdmd_eig", "cdmd_mask_median3"]
 
 
 def _load():
@@ -83,6 +83,7 @@ def _load():
         "cdmd_modes_simt": (i32, [vp, V, M, vp, i64, vp]),
         "cdmd_background": (i32, [vp, vp, i64, i64, M, i32, i64, i64, vp, i64, vp]),
         "cdmd_foreground": (i32, [vp, V, M, vp, i64, i32, ctypes.c_float, vp, i64, vp]),
+        "cdmd_mask_median3": (i32, [vp, i64, i64, i64, i64, vp, vp]),
         "cdmd_philox": (i32, [vp, ctypes.c_uint32, ctypes.c_uint32, vp, i64, vp]),
         "cdmd_gaussian_table": (i32, [vp, vp, vp]),
         "cdmd_sparse_cap": (i64, [i64, i64, dbl]),
@@ -199,6 +200,12 @@ def cdmd_foreground(h, v, model, Phi, mode, tau, mask, stream=None):
                                                    _stream(stream)))
 
 
+def cdmd_mask_median3(mask, width, height, out, stream=None):
+    """3x3 median post-filter (Fig. 7) of a (m, ldw) packed mask of whole frames."""
+    _check("cdmd_mask_median3", _lib.cdmd_mask_median3(_ptr(mask), mask.stride(0), int(width), int(height),
+                                                       mask.shape[0], _ptr(out), _stream(stream)))
+
+
 def cdmd_philox(ctr, k0, k1, out, stream=None):
     _check("cdmd_philox", _lib.cdmd_philox(_ptr(ctr), k0, k1, _ptr(out), ctr.numel() // 4, _stream(stream)))
 
@@ -303,6 +310,14 @@ class Pipeline:
         v = video(X, self.n_total, self.pix0, self.n_local)
         cdmd_foreground(self.h, v, self.model, self.Phi, mode, tau, self.mask, stream)
         return self.mask
+
+    def median3(self, width, height, stream=None):
+        """3x3 median post-filter of the last mask (whole frames: n_local = width * height)."""
+        if width * height != self.n_local:
+            raise ValueError("median3 needs whole frames in this pipeline's slab")
+        out = torch.empty_like(self.mask)
+        cdmd_mask_median3(self.mask, width, height, out, stream)
+        return out
 
     def background(self, mode=BG_DYNAMIC, t0=0, nt=None, stream=None):
         nt = self.m - t0 if nt is None else nt

@@ -313,6 +313,18 @@ cdmd_status cdmd_foreground(cdmd_handle h, const cdmd_video* v, const cdmd_model
   return cuda_status(launch_foreground(*v, *M, Phi, ldphi, mode, tau, mask, ldw, h->sched + 1, (cudaStream_t)st));
 }
 
+cdmd_status cdmd_mask_median3(const uint32_t* mask, int64_t ldw, int64_t width, int64_t height, int64_t m,
+                              uint32_t* out, cdmd_stream st) {
+  if (!mask || !out) return CDMD_ERR_ARG;
+  if (width < 1 || height < 1 || m < 1 || m > 65535) return CDMD_ERR_RANGE;
+  const int64_t nw = ceil_div(width * height, 32);
+  if (ldw < nw) return CDMD_ERR_ARG;
+  const char *a0 = (const char*)mask, *a1 = a0 + sizeof(uint32_t) * ldw * m;
+  const char *b0 = (const char*)out, *b1 = b0 + sizeof(uint32_t) * ldw * m;
+  if (a0 < b1 && b0 < a1) return CDMD_ERR_ARG;   // aliasing
+  return cuda_status(launch_mask_median3(mask, ldw, width, height, m, out, (cudaStream_t)st));
+}
+
 // --------------------------------------------------------------- test hooks
 cdmd_status cdmd_philox(const uint32_t* ctr, uint32_t k0, uint32_t k1, uint32_t* out, int64_t count,
                         cdmd_stream st) {

@@ -450,3 +450,38 @@ def test_pipeline_parity_gavish_donoho(C, H, case):
     assert g["model"]["k_eff"] == o["model"]["k_eff"]
     assert 1 <= o["model"]["k_eff"] <= k
     check_all(g, o, kind, tau)
+
+
+@pytest.mark.parametrize("W,Hh,m,dens", [(37, 23, 5, 0.35), (64, 16, 3, 0.5), (720, 480, 4, 0.1), (5, 3, 2, 0.6),
+                                         (33, 1, 2, 0.5), (1, 40, 2, 0.5)])
+def test_mask_median3_bit_exact(C, W, Hh, m, dens):
+    """3x3 median post-filter (Fig. 7): bit-exact against the oracle on random
+    masks (widths that are not multiples of 32 straddle words across image rows)."""
+    rng = np.random.default_rng(W * 1000 + Hh)
+    n = W * Hh
+    M = rng.random((m, n)) < dens
+    ldw = (n + 31) // 32 + 3
+    packed = np.zeros((m, ldw), dtype=np.uint32)
+    packed[:, :(n + 31) // 32] = OD.pack_mask(M)
+    dev = torch.from_numpy(packed.view(np.int32)).cuda()
+    out = torch.full_like(dev, -1)
+    C.cdmd_mask_median3(dev, W, Hh, out)
+    got = OD.unpack_mask(out.cpu().numpy().view(np.uint32)[:, :(n + 31) // 32], n)
+    assert np.array_equal(got, OD.median3(M, W, Hh))
+
+
+def test_mask_median3_on_the_bench_mask(C, H):
+    """The filter applied to the 1080p dynamic-background mask the bench produces."""
+    cfg = config_by_name("c4_1080p_sparse")
+    X = video_for(cfg)
+    m, n = X.shape
+    Xd = to_dev(X)
+    P = C.Pipeline(H, n, n, m, "sparse", cfg.p, cfg.k, cfg.K)
+    P.run(Xd, cfg.tau, C.BG_DYNAMIC)
+    filt = P.median3(cfg.width, cfg.height)
+    torch.cuda.synchronize()
+    raw = OD.unpack_mask(P.mask.cpu().numpy().view(np.uint32), n)
+    got = OD.unpack_mask(filt.cpu().numpy().view(np.uint32), n)
+    ref = OD.median3(raw, cfg.width, cfg.height)
+    assert np.array_equal(got, ref)
+    assert got.sum() <= raw.sum() + raw.size // 100    # the filter mostly removes isolated noise bits
