@@ -1,77 +1,107 @@
 // median3.cu — 3x3 median post-filter of the bit-packed foreground mask (Fig. 7,
-// P:582; reading R22).  One thread per output word: the nine shifted
-// 32-pixel neighbour words (rows y-1, y, y+1; columns x-1, x, x+1) are assembled
-// with funnel shifts from the packed rows, the bits that would wrap across an image
-// row are cleared, and a bit-sliced carry-save adder tree gives "at least 5 of 9"
-// for all 32 pixels at once.
+// P:582; reading R22).  Per output word the nine shifted 32-pixel neighbour
+// words (rows y-1, y, y+1; columns x-1, x, x+1) are assembled with funnel shifts from
+// the packed rows, the bits that would wrap across an image row are cleared, and a
+// bit-sliced carry-save adder tree gives "at least 5 of 9" for all 32 pixels at once.
 #include "common.cuh"
 
 namespace cdmd {
 
 namespace {
 
-// 32 mask bits starting at pixel s of one frame (pixels outside [0, n) read as 0)
-__device__ __forceinline__ uint32_t bits32(const uint32_t* __restrict__ f, int64_t s, int64_t n, int64_t nw) {
-  if (s + 32 <= 0 || s >= n) return 0u;
-  const int64_t q = s >> 5;                     // floor division (s may be negative)
-  const int r = (int)(s & 31);
-  const uint32_t lo = (q >= 0 && q < nw) ? __ldg(f + q) : 0u;
-  const uint32_t hi = (q + 1 >= 0 && q + 1 < nw) ? __ldg(f + q + 1) : 0u;
-  uint32_t v = (uint32_t)((((uint64_t)hi << 32) | lo) >> r);
-  if (s < 0) v &= ~0u << (uint32_t)(-s);        // pixels before 0
-  const int64_t past = s + 32 - n;              // pixels at or beyond n
-  if (past > 0) v &= past >= 32 ? 0u : (~0u >> (uint32_t)past);
-  return v;
-}
-
 __device__ __forceinline__ void fa(uint32_t a, uint32_t b, uint32_t c, uint32_t& s, uint32_t& co) {
   s = a ^ b ^ c;
   co = (a & b) | (a & c) | (b & c);
 }
 
+#ifndef MW_DEF
+#define MW_DEF 8
+#endif
+constexpr int MW = MW_DEF;  // output words per thread (consecutive pixels of one frame)
+
 }  // namespace
 
+// Each thread produces MW consecutive output words.  For image row offset dy the
+// neighbour windows start at pixel j0 + dy W - 1 + {0, 1, 2}: the same bit offset r_dy
+// for every word of the thread (and every thread), so three words per row slide along
+// and each new output word costs one load per row plus funnel shifts.  32-bit pixel
+// indices (whole frames of < 2^31 pixels).
 __global__ void __launch_bounds__(256) mask_median3_kernel(const uint32_t* __restrict__ in, int64_t ldw,
-                                                           int64_t W, int64_t H, uint32_t* __restrict__ out) {
-  const int64_t n = W * H, nw = (n + 31) >> 5;
-  const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (w >= nw) return;
+                                                           int W, int H, uint32_t* __restrict__ out) {
+  const int n = W * H, nw = (n + 31) >> 5;
+  const int w0 = (blockIdx.x * blockDim.x + threadIdx.x) * MW;
+  if (w0 >= nw) return;
   const int64_t t = blockIdx.y;
   const uint32_t* f = in + t * ldw;
-  const int64_t j0 = w << 5;
-  // bits whose pixel is in column 0 (no left neighbour) or column W-1 (no right one)
-  uint32_t first = 0u, last = 0u;
-  for (int64_t i = (W - j0 % W) % W; i < 32; i += W) first |= 1u << i;
-  for (int64_t i = (W - 1 - j0 % W + W) % W; i < 32; i += W) last |= 1u << i;
-  uint32_t x[9];
+  const uint32_t lastmask = (n & 31) ? ((1u << (n & 31)) - 1u) : ~0u;   // valid bits of word nw - 1
+  auto word = [&](int q) -> uint32_t {
+    if (q < 0 || q >= nw) return 0u;
+    const uint32_t v = __ldg(f + q);
+    return q == nw - 1 ? v & lastmask : v;
+  };
+  // per row: bit offset r and the three words a (q), b (q+1), c (q+2) of the L window
+  int q[3];
+  uint32_t r[3], wa[3], wb[3], wc[3];
 #pragma unroll
-  for (int dy = -1; dy <= 1; ++dy) {
-    const int64_t s = j0 + dy * W;
-    x[3 * (dy + 1) + 0] = bits32(f, s - 1, n, nw) & ~first;   // left neighbours
-    x[3 * (dy + 1) + 1] = bits32(f, s, n, nw);
-    x[3 * (dy + 1) + 2] = bits32(f, s + 1, n, nw) & ~last;    // right neighbours
+  for (int d = 0; d < 3; ++d) {
+    const int s = (w0 << 5) + (d - 1) * W - 1;     // may be negative
+    q[d] = s >> 5;
+    r[d] = (uint32_t)s & 31u;
+    wa[d] = word(q[d]);
+    wb[d] = word(q[d] + 1);
+    wc[d] = word(q[d] + 2);
   }
-  // count of the nine bits per position: CSA tree -> (b3 b2 b1 b0), majority = count >= 5
-  uint32_t s1, c1, s2, c2, s3, c3, s4, c4, s5, c5;
-  fa(x[0], x[1], x[2], s1, c1);
-  fa(x[3], x[4], x[5], s2, c2);
-  fa(x[6], x[7], x[8], s3, c3);
-  fa(s1, s2, s3, s4, c4);        // weight 1: s4; weight 2: c1 c2 c3 c4
-  fa(c1, c2, c3, s5, c5);        // weight 2: s5 (+ c4); weight 4: c5
-  const uint32_t b1 = s5 ^ c4, c6 = s5 & c4;     // weight 2 total bit; carry to weight 4
-  const uint32_t b2 = c5 ^ c6, b3 = c5 & c6;     // weight 4 bit; weight 8 bit
-  uint32_t r = b3 | (b2 & (b1 | s4));
-  const int64_t tail = n - j0;                   // pixels of this word inside the frame
-  if (tail < 32) r &= (1u << tail) - 1u;
-  out[t * ldw + w] = r;
+  int x0 = (w0 << 5) % W;                          // column of the word's first pixel
+  const int wend = w0 + MW < nw ? w0 + MW : nw;
+  for (int w = w0; w < wend; ++w) {
+    uint32_t first = 0u, last = 0u;                // pixels in column 0 / column W-1
+    if (W >= 32) {                                 // at most one of each per word
+      const int i0 = x0 == 0 ? 0 : W - x0, i1 = W - 1 - x0;
+      if (i0 < 32) first = 1u << i0;
+      if (i1 < 32) last = 1u << i1;
+    } else {
+      for (int i = (W - x0) % W; i < 32; i += W) first |= 1u << i;
+      for (int i = (2 * W - 1 - x0) % W; i < 32; i += W) last |= 1u << i;
+    }
+    uint32_t x[9];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const uint32_t rr = r[d];
+      const uint32_t L = __funnelshift_r(wa[d], wb[d], rr);
+      const uint32_t Cc = rr == 31u ? wb[d] : __funnelshift_r(wa[d], wb[d], rr + 1u);
+      const uint32_t R = rr >= 30u ? __funnelshift_r(wb[d], wc[d], rr - 30u) : __funnelshift_r(wa[d], wb[d], rr + 2u);
+      x[3 * d + 0] = L & ~first;
+      x[3 * d + 1] = Cc;
+      x[3 * d + 2] = R & ~last;
+      // slide to the next output word
+      wa[d] = wb[d];
+      wb[d] = wc[d];
+      wc[d] = word(q[d] + 3 + (w - w0));
+    }
+    // count of the nine bits per position: CSA tree -> (b3 b2 b1 b0), majority = count >= 5
+    uint32_t s1, c1, s2, c2, s3, c3, s4, c4, s5, c5;
+    fa(x[0], x[1], x[2], s1, c1);
+    fa(x[3], x[4], x[5], s2, c2);
+    fa(x[6], x[7], x[8], s3, c3);
+    fa(s1, s2, s3, s4, c4);        // weight 1: s4; weight 2: c1 c2 c3 c4
+    fa(c1, c2, c3, s5, c5);        // weight 2: s5 (+ c4); weight 4: c5
+    const uint32_t b1 = s5 ^ c4, c6 = s5 & c4;     // weight 2 total bit; carry to weight 4
+    const uint32_t b2 = c5 ^ c6, b3 = c5 & c6;     // weight 4 bit; weight 8 bit
+    uint32_t res = b3 | (b2 & (b1 | s4));
+    if (w == nw - 1) res &= lastmask;
+    out[t * ldw + w] = res;
+    x0 += 32;
+    while (x0 >= W) x0 -= W;
+  }
 }
 
 cudaError_t launch_mask_median3(const uint32_t* in, int64_t ldw, int64_t W, int64_t H, int64_t m, uint32_t* out,
                                 cudaStream_t st) {
+  if (W * H >= ((int64_t)1 << 31)) return cudaErrorInvalidValue;
   const int64_t nw = (W * H + 31) >> 5;
-  dim3 grid((unsigned)ceil_div(nw, 256), (unsigned)m);
+  dim3 grid((unsigned)ceil_div(ceil_div(nw, MW), 256), (unsigned)m);
   note_launch();
-  mask_median3_kernel<<<grid, 256, 0, st>>>(in, ldw, W, H, out);
+  mask_median3_kernel<<<grid, 256, 0, st>>>(in, ldw, (int)W, (int)H, out);
   return cudaGetLastError();
 }
 
