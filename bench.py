@@ -318,9 +318,14 @@ def main():
     if os.path.exists(tp) and cfg.name == "c4_1080p_sparse" and world == 1 and mode:
         traffic = json.load(open(tp)).get(dom)
     sk_kernel = {"sparse": "sketch_sparse_kernel", "spixel": "sketch_spixel_kernel",
-                 "rademacher": "sketch_rademacher_tc_kernel", "gaussian": "sketch_gaussian_tc_kernel"}[cfg.kind]
-    roof = {"kernel": {"sketch": sk_kernel, "modes": "modes_tc_kernel",
-                       "foreground": "foreground_tc_kernel" if mode else "foreground_static_kernel"}[dom],
+                 "rademacher": "sketch_rademacher_tc_kernel",
+                 "gaussian": "sketch_gaussian_tc_kernel" if os.environ.get("CDMD_GAUSS_1CTA")
+                 else "sketch_gaussian_tc2_kernel"}[cfg.kind]
+    vq = C.video(Xd, n, pix0, nl)
+    md_kernel = "modes_tc_kernel" if C.cdmd_modes_path(P.model) == 1 else "modes_simt_kernel"
+    fg_kernel = {2: "foreground_tc_kernel", 1: "foreground_dynamic_kernel", 0: "foreground_static_kernel"}[
+        C.cdmd_foreground_path(vq, P.model, mode)]
+    roof = {"kernel": {"sketch": sk_kernel, "modes": md_kernel, "foreground": fg_kernel}[dom],
             "bound": bound, "achieved": round(achieved, 1), "peak": peak, "unit": unit,
             "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
             ("algorithmic_flops_per_launch" if bound == "tensor" else "algorithmic_bytes_per_launch"): algo[dom],

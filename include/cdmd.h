@@ -195,6 +195,13 @@ CDMD_API cdmd_status cdmd_foreground(cdmd_handle h, const cdmd_video* v, const c
                             const float* Phi, int64_t ldphi, int32_t mode, float tau,
                             uint32_t* mask, int64_t ldw, cdmd_stream st);
 
+/* Which kernel a call would run (diagnostics for reports): cdmd_modes -> 1 the
+ * tcgen05 kernel, 0 the CUDA-core (dp4a) kernel (k up to 64 and m up to 512 fit the
+ * tensor-core kernel's SMEM-resident limbs); cdmd_foreground -> 2 tcgen05 dynamic,
+ * 1 CUDA-core dynamic, 0 static.  Negative on invalid arguments. */
+CDMD_API int32_t cdmd_modes_path(const cdmd_model* model);
+CDMD_API int32_t cdmd_foreground_path(const cdmd_video* v, const cdmd_model* model, int32_t mode);
+
 /* ------------------------------------------------------------ median post-filter
  * The "in addition median filtered foreground mask" (Fig. 7): a 3x3 spatial
  * median of every frame's mask (on a binary image: bit = 1 iff >= 5 of the 3x3

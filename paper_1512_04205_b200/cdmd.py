@@ -58,7 +58,8 @@ SYMBOLS = ["cdmd_create", "cdmd_destroy", "cdmd_status_str", "cdmd_version", "cd
            "cdmd_sketch_workspace_bytes", "cdmd_sketch", "cdmd_model_bytes", "cdmd_model_bind",
            "cdmd_fit_workspace_bytes", "cdmd_fit", "cdmd_modes", "cdmd_background",
            "cdmd_foreground", "cdmd_philox", "cdmd_gaussian_table", "cdmd_sparse_cap",
-           "cdmd_sensing_rows", "cdmd_modes_simt", "cdmd_eig", "cdmd_mask_median3"]
+           "cdmd_sensing_rows", "cdmd_modes_simt", "cdmd_eig", "cdmd_mask_median3",
+           "cdmd_modes_path", "cdmd_foreground_path"]
 
 
 def _load():
@@ -84,6 +85,8 @@ def _load():
         "cdmd_background": (i32, [vp, vp, i64, i64, M, i32, i64, i64, vp, i64, vp]),
         "cdmd_foreground": (i32, [vp, V, M, vp, i64, i32, ctypes.c_float, vp, i64, vp]),
         "cdmd_mask_median3": (i32, [vp, i64, i64, i64, i64, vp, vp]),
+        "cdmd_modes_path": (i32, [M]),
+        "cdmd_foreground_path": (i32, [V, M, i32]),
         "cdmd_philox": (i32, [vp, ctypes.c_uint32, ctypes.c_uint32, vp, i64, vp]),
         "cdmd_gaussian_table": (i32, [vp, vp, vp]),
         "cdmd_sparse_cap": (i64, [i64, i64, dbl]),
@@ -198,6 +201,16 @@ def cdmd_foreground(h, v, model, Phi, mode, tau, mask, stream=None):
     _check("cdmd_foreground", _lib.cdmd_foreground(h.h, ctypes.byref(v), ctypes.byref(model), _ptr(Phi),
                                                    Phi.stride(0), mode, float(tau), _ptr(mask), mask.stride(0),
                                                    _stream(stream)))
+
+
+def cdmd_modes_path(model):
+    """1: tcgen05 modes kernel, 0: CUDA-core fallback."""
+    return int(_lib.cdmd_modes_path(ctypes.byref(model)))
+
+
+def cdmd_foreground_path(v, model, mode):
+    """2: tcgen05 dynamic, 1: CUDA-core dynamic, 0: static."""
+    return int(_lib.cdmd_foreground_path(ctypes.byref(v), ctypes.byref(model), int(mode)))
 
 
 def cdmd_mask_median3(mask, width, height, out, stream=None):

@@ -313,6 +313,18 @@ cdmd_status cdmd_foreground(cdmd_handle h, const cdmd_video* v, const cdmd_model
   return cuda_status(launch_foreground(*v, *M, Phi, ldphi, mode, tau, mask, ldw, h->sched + 1, (cudaStream_t)st));
 }
 
+int32_t cdmd_modes_path(const cdmd_model* M) {
+  if (!M || M->k < 1) return -1;
+  return modes_tc_supported(*M) ? 1 : 0;
+}
+
+int32_t cdmd_foreground_path(const cdmd_video* v, const cdmd_model* M, int32_t mode) {
+  if (!v || !M) return -1;
+  if (mode == CDMD_BG_STATIC) return 0;
+  if (mode != CDMD_BG_DYNAMIC) return -1;
+  return foreground_tc_supported(*v, *M) ? 2 : 1;
+}
+
 cdmd_status cdmd_mask_median3(const uint32_t* mask, int64_t ldw, int64_t width, int64_t height, int64_t m,
                               uint32_t* out, cdmd_stream st) {
   if (!mask || !out) return CDMD_ERR_ARG;

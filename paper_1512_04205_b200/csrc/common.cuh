@@ -117,4 +117,7 @@ cudaError_t launch_foreground(const cdmd_video& v, const cdmd_model& M, const fl
 cudaError_t launch_mask_median3(const uint32_t* in, int64_t ldw, int64_t W, int64_t H, int64_t m, uint32_t* out,
                                 cudaStream_t st);
 
+bool modes_tc_supported(const cdmd_model& M);
+bool foreground_tc_supported(const cdmd_video& v, const cdmd_model& M);
+
 }  // namespace cdmd
