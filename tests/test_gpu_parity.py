@@ -485,3 +485,41 @@ def test_mask_median3_on_the_bench_mask(C, H):
     ref = OD.median3(raw, cfg.width, cfg.height)
     assert np.array_equal(got, ref)
     assert got.sum() <= raw.sum() + raw.size // 100    # the filter mostly removes isolated noise bits
+
+
+def test_c5_4k_full_size_sampled(C, H):
+    """BASELINE's 4K configuration (3840x2160, 1000 frames, sparse p = 4000, k = 100) on
+    one GPU: exact integer sketch, fit parity (m - 1 = 999: the cuSOLVER syevdx path;
+    k = 100: the device eig), modes and mask on sampled pixels incl. the ragged tail
+    (k = 100 and m = 1000 take the CUDA-core modes / dynamic-foreground kernels)."""
+    cfg = config_by_name("c5_4k_sparse")
+    X = video_for(cfg)
+    m, n = X.shape
+    Xd = to_dev(X)
+    P = C.Pipeline(H, n, n, m, "sparse", cfg.p, cfg.k, cfg.K)
+    Yg = P.sketch(Xd).cpu().numpy().T.astype(np.int64)
+    Yo = OS.sketch(X, OS.SPARSE, cfg.p, 0)
+    assert np.array_equal(Yg, Yo)
+    P.fit()
+    gm = C.model_to_host(P.model)
+    om = OD.fit(Yo, cfg.k, cfg.K)
+    assert gm["k_eff"] == om["k_eff"]
+    perm, err = PT.match_eigs(gm["lam"], om["lam"])
+    assert err <= PT.RTOL_EIG
+    assert PT.supports_equal_mod_conj(gm["support"], gm["pair"], perm, om["support"], om["pair"])
+    Phi = P.modes(Xd)
+    mask = P.foreground(Xd, cfg.tau, C.BG_DYNAMIC).cpu().numpy().view(np.uint32)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(5)
+    pix = np.unique(np.concatenate([rng.choice(n, 2048, replace=False), np.arange(n - 40, n)]))
+    Po = X[1:, pix].T.astype(np.float64) @ om["M"]
+    Pg = PT.unfold(Phi.cpu().numpy()[:, pix], gm["pair"])
+    for i in range(gm["k_eff"]):
+        j = perm[i]
+        if PT.well_separated(om["lam"], j):
+            assert PT.phase_aligned_rel(Pg[:, i], Po[:, j]) <= PT.RTOL_PHI
+    Ld = OD.background_dynamic(Po, om)
+    res = np.abs(X[:, pix].astype(np.float64) - Ld.T)
+    mg = OD.unpack_mask(mask, n)[:, pix]
+    frac, band, nd = PT.mask_agreement(mg, res > cfg.tau, res, cfg.tau)
+    assert frac >= PT.MASK_AGREE and band, (frac, nd)
