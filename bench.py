@@ -171,6 +171,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--lanes", type=int, default=16,
                     help="batches in flight (streaming, P:573); 1 = one batch at a time")
+    ap.add_argument("--fit-sms", type=int, default=0,
+                    help="streaming: SMs reserved for the small solves (green-context partition; 0 = shared)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -256,7 +258,7 @@ def main():
     if args.lanes > 1:
         # K batches through `lanes` concurrent lanes; each lane reads its own copy of X
         S = C.Streaming(local, n, nl, m, cfg.kind, cfg.p, cfg.k, cfg.K, lanes=args.lanes,
-                        seed=cfg.sensing_seed, pix0=pix0, rank=args.rank)
+                        seed=cfg.sensing_seed, pix0=pix0, rank=args.rank, fit_sms=args.fit_sms)
         Xs = [Xd] + [Xd.clone() for _ in range(args.lanes - 1)]
         ar = (lambda Y: dist.all_reduce(Y, op=dist.ReduceOp.SUM)) if world > 1 else None
 
@@ -286,7 +288,7 @@ def main():
             dist.all_reduce(ts, op=dist.ReduceOp.MAX)
         ms_max = float(ts.item())
         value = m / (ms_max * 1e-3)
-        streaming = {"lanes": args.lanes, "ms_per_batch": round(ms_max, 4),
+        streaming = {"lanes": args.lanes, "ms_per_batch": round(ms_max, 4), "sm_partition": S.sms,
                      "note": "batches pipelined across lanes (own handle, stream, buffers, copy of X)"}
 
     # roofline of the dominant kernel: HBM-bound passes (algorithmic bytes per launch) and,

@@ -130,6 +130,21 @@ CDMD_API const char* cdmd_version(void);
  * Diagnostics: bench.py reports the difference across its timed region.          */
 CDMD_API uint64_t cdmd_kernel_launches(void);
 
+/* Spatial SM partition for streaming many batches ("decomposed in consecutive
+ * batches"): splits device `device`'s SMs once per process into two green contexts —
+ * `fit_sms` SMs (rounded up to the hardware granularity: multiples of 8) reserved for
+ * the small solves, the rest for the full-resolution passes — and creates
+ * `n_streams` non-blocking streams in each: pass_streams[i] (for cdmd_sketch,
+ * cdmd_modes, cdmd_foreground) and fit_streams[i] (for cdmd_fit).  The streams are
+ * plain cudaStream_t handles owned by the library for the life of the process.
+ * sms[0] / sms[1] receive the SM counts of the solve / pass partitions.  Afterwards the
+ * persistent kernels size their grids to sms[1] CTAs on every stream.
+ * Errors: CDMD_ERR_ARG (bad pointers or counts, or a partition already exists),
+ * CDMD_ERR_RANGE (nothing left for the passes), CDMD_ERR_UNSUPPORTED (driver
+ * without green contexts), CDMD_ERR_CUDA.                                        */
+CDMD_API cdmd_status cdmd_sm_partition(int device, int fit_sms, int n_streams, void** pass_streams,
+                                       void** fit_streams, int* sms);
+
 /* ------------------------------------------------------------------- sketch
  * Y_full = C D (Alg. 1 step 3; Eq. P:286-288), C generated on the fly from
  * Philox4x32-10 and never materialised (single pixel = Feistel

@@ -59,7 +59,7 @@ SYMBOLS = ["cdmd_create", "cdmd_destroy", "cdmd_status_str", "cdmd_version", "cd
            "cdmd_fit_workspace_bytes", "cdmd_fit", "cdmd_modes", "cdmd_background",
            "cdmd_foreground", "cdmd_philox", "cdmd_gaussian_table", "cdmd_sparse_cap",
            "cdmd_sensing_rows", "cdmd_modes_simt", "cdmd_eig", "cdmd_mask_median3",
-           "cdmd_modes_path", "cdmd_foreground_path"]
+           "cdmd_modes_path", "cdmd_foreground_path", "cdmd_sm_partition"]
 
 
 def _load():
@@ -85,6 +85,8 @@ def _load():
         "cdmd_background": (i32, [vp, vp, i64, i64, M, i32, i64, i64, vp, i64, vp]),
         "cdmd_foreground": (i32, [vp, V, M, vp, i64, i32, ctypes.c_float, vp, i64, vp]),
         "cdmd_mask_median3": (i32, [vp, i64, i64, i64, i64, vp, vp]),
+        "cdmd_sm_partition": (i32, [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(vp),
+                                    ctypes.POINTER(vp), ctypes.POINTER(ctypes.c_int)]),
         "cdmd_modes_path": (i32, [M]),
         "cdmd_foreground_path": (i32, [V, M, i32]),
         "cdmd_philox": (i32, [vp, ctypes.c_uint32, ctypes.c_uint32, vp, i64, vp]),
@@ -232,6 +234,28 @@ def cdmd_kernel_launches():
     return int(lib().cdmd_kernel_launches())
 
 
+_PARTITION = {}
+
+
+def cdmd_sm_partition(device, fit_sms, n_streams):
+    """Split the device's SMs (green contexts) into a solve partition of >= fit_sms SMs
+    and a pass partition (the rest), once per process.  Returns (pass_streams,
+    fit_streams, (solve_sms, pass_sms)) with the streams as torch ExternalStreams."""
+    if device in _PARTITION:
+        ps, fs, sms = _PARTITION[device]
+        if len(ps) < n_streams:
+            raise RuntimeError(f"SM partition on device {device} has {len(ps)} streams, {n_streams} requested")
+        return ps[:n_streams], fs[:n_streams], sms
+    vp = ctypes.c_void_p
+    ps, fs, sms = (vp * n_streams)(), (vp * n_streams)(), (ctypes.c_int * 2)()
+    _check("cdmd_sm_partition", lib().cdmd_sm_partition(device, fit_sms, n_streams, ps, fs, sms))
+    dev = torch.device("cuda", device)
+    out = ([torch.cuda.ExternalStream(ps[i], device=dev) for i in range(n_streams)],
+           [torch.cuda.ExternalStream(fs[i], device=dev) for i in range(n_streams)], (sms[0], sms[1]))
+    _PARTITION[device] = out
+    return out
+
+
 def cdmd_sparse_cap(n_total, p, s=0.0):
     return _lib.cdmd_sparse_cap(n_total, p, float(s or 0.0))
 
@@ -357,17 +381,25 @@ class Streaming:
     order on every rank (a ticket lock), so collectives match across ranks."""
 
     def __init__(self, device, n_total, n_local, m, kind, p, k, K, lanes=4, s=0.0, seed=0, pix0=0, dt=1.0,
-                 rank="fixed"):
+                 rank="fixed", fit_sms=0):
         import threading
         self.lanes = []
         lo, hi = torch.cuda.Stream.priority_range()
-        for _ in range(lanes):
+        self.sms = None
+        if fit_sms > 0:
+            # spatial partition (cdmd_sm_partition): the solves get SMs of their own
+            # instead of queueing behind the persistent full-resolution passes
+            pst, fst, self.sms = cdmd_sm_partition(device, fit_sms, lanes)
+        for li in range(lanes):
             h = Handle(device)
-            st = torch.cuda.Stream(device=device)
-            # the small solve runs on a high-priority stream of its own: its kernels (the
-            # 8-CTA tridiagonalisation cluster above all) get SMs ahead of the next
-            # lane's full-resolution pass instead of waiting behind it
-            st_fit = torch.cuda.Stream(device=device, priority=hi)
+            if fit_sms > 0:
+                st, st_fit = pst[li], fst[li]
+            else:
+                st = torch.cuda.Stream(device=device)
+                # the small solve runs on a high-priority stream of its own: its kernels
+                # (the 8-CTA tridiagonalisation cluster above all) get SMs ahead of the
+                # next lane's full-resolution pass instead of waiting behind it
+                st_fit = torch.cuda.Stream(device=device, priority=hi)
             with torch.cuda.stream(st):
                 pipe = Pipeline(h, n_total, n_local, m, kind, p, k, K, s=s, seed=seed, pix0=pix0,
                                 device=f"cuda:{device}", dt=dt, rank=rank)

@@ -20,7 +20,8 @@ int persistent_ctas(int sms) {
     reserve = e ? atoi(e) : 0;
     if (reserve < 0) reserve = 0;
   }
-  const int g = sms - reserve;
+  int g = sms - reserve;
+  if (g_persist_limit > 0 && g > g_persist_limit) g = g_persist_limit;   // cdmd_sm_partition
   return g < 1 ? 1 : g;
 }
 

@@ -23,6 +23,7 @@ inline void note_launch() { launch_counter().fetch_add(1, std::memory_order_rela
 // CTAs of the persistent full-resolution kernels (modes, foreground): all SMs, or
 // fewer with CDMD_PERSIST_RESERVE=R (R SMs left to other streams' small solves)
 int persistent_ctas(int sms);
+extern int g_persist_limit;   // set by cdmd_sm_partition (partition.cu)
 
 
 // ---------------------------------------------------------------- Philox4x32-10

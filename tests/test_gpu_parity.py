@@ -6,6 +6,7 @@ seconds that still span several tiles and ragged tails, plus the bench's full
 1080p configuration checked exactly (integer sketch) or on sampled outputs.
 """
 
+import os
 import zlib
 
 import numpy as np
@@ -523,3 +524,46 @@ def test_c5_4k_full_size_sampled(C, H):
     mg = OD.unpack_mask(mask, n)[:, pix]
     frac, band, nd = PT.mask_agreement(mg, res > cfg.tau, res, cfg.tau)
     assert frac >= PT.MASK_AGREE and band, (frac, nd)
+
+
+_PARTITION_SCRIPT = r"""
+import sys, torch
+sys.path.insert(0, sys.argv[1])
+from paper_1512_04205_b200 import cdmd as C
+from synth.scene import config_by_name, video_for
+cfg = config_by_name("c4_1080p_sparse")
+X = video_for(cfg)
+m, n = X.shape
+ld = ((n + 15) // 16) * 16
+X0 = torch.zeros((m, ld), dtype=torch.uint8, device="cuda")
+X0[:, :n] = torch.from_numpy(X).cuda()
+vids = [X0, X0.flip(0).contiguous(), X0.roll(5, dims=0).contiguous(), X0.roll(-9, dims=0).contiguous()]
+S = C.Streaming(0, n, n, m, "sparse", cfg.p, cfg.k, cfg.K, lanes=2, seed=cfg.sensing_seed, fit_sms=32)
+assert S.sms[0] >= 32 and S.sms[0] + S.sms[1] == torch.cuda.get_device_properties(0).multi_processor_count, S.sms
+ends = S.run(vids, cfg.tau, C.BG_DYNAMIC)
+for e in ends:
+    torch.cuda.current_stream().wait_event(e)
+torch.cuda.synchronize()
+H = C.Handle(0)
+P = C.Pipeline(H, n, n, m, "sparse", cfg.p, cfg.k, cfg.K, seed=cfg.sensing_seed)
+for li, (_, _, _, pipe) in enumerate(S.lanes):
+    mask = P.run(vids[2 + li], cfg.tau, C.BG_DYNAMIC)
+    torch.cuda.synchronize()
+    assert torch.equal(pipe.Y, P.Y) and torch.equal(pipe.Phi, P.Phi) and torch.equal(pipe.mask, mask), li
+print("partition ok", S.sms)
+"""
+
+
+def test_streaming_sm_partition_equal_sequential(tmp_path):
+    """cdmd_sm_partition (green contexts: SMs reserved for the small solves, persistent
+    grids sized to the rest) changes scheduling only: lanes on the partition streams
+    give bit-identical sketches, modes and masks to Pipeline.  Run in a subprocess: the
+    partition is process-wide."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "partition_check.py"
+    script.write_text(_PARTITION_SCRIPT)
+    r = subprocess.run([sys.executable, str(script), root], cwd=root, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+    assert "partition ok" in r.stdout

@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--config", default="c4_1080p_sparse")
     ap.add_argument("--lanes", type=int, default=8)
     ap.add_argument("--batches", type=int, default=48)
+    ap.add_argument("--fit-sms", type=int, default=0)
     a = ap.parse_args()
     cfg = config_by_name(a.config)
     X = video_for(cfg)
@@ -31,7 +32,8 @@ def main():
     ld = ((n + 15) // 16) * 16
     Xd = torch.zeros((m, ld), dtype=torch.uint8, device="cuda")
     Xd[:, :n] = torch.from_numpy(X).cuda()
-    S = C.Streaming(0, n, n, m, cfg.kind, cfg.p, cfg.k, cfg.K, lanes=a.lanes, seed=cfg.sensing_seed)
+    S = C.Streaming(0, n, n, m, cfg.kind, cfg.p, cfg.k, cfg.K, lanes=a.lanes, seed=cfg.sensing_seed,
+                    fit_sms=a.fit_sms)
     Xs = [Xd] + [Xd.clone() for _ in range(a.lanes - 1)]
     ev = {}
 
