@@ -324,7 +324,7 @@ def main():
                  "gaussian": "sketch_gaussian_tc_kernel" if os.environ.get("CDMD_GAUSS_1CTA")
                  else "sketch_gaussian_tc2_kernel"}[cfg.kind]
     vq = C.video(Xd, n, pix0, nl)
-    md_kernel = "modes_tc_kernel" if C.cdmd_modes_path(P.model) == 1 else "modes_simt_kernel"
+    md_kernel = {1: "modes_tc_kernel", 2: "modes_tc_mc_kernel"}.get(C.cdmd_modes_path(P.model), "modes_simt_kernel")
     fg_kernel = {2: "foreground_tc_kernel", 1: "foreground_dynamic_kernel", 0: "foreground_static_kernel"}[
         C.cdmd_foreground_path(vq, P.model, mode)]
     roof = {"kernel": {"sketch": sk_kernel, "modes": md_kernel, "foreground": fg_kernel}[dom],

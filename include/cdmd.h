@@ -211,8 +211,9 @@ CDMD_API cdmd_status cdmd_foreground(cdmd_handle h, const cdmd_video* v, const c
                             uint32_t* mask, int64_t ldw, cdmd_stream st);
 
 /* Which kernel a call would run (diagnostics for reports): cdmd_modes -> 1 the
- * tcgen05 kernel, 0 the CUDA-core (dp4a) kernel (k up to 64 and m up to 512 fit the
- * tensor-core kernel's SMEM-resident limbs); cdmd_foreground -> 2 tcgen05 dynamic,
+ * tcgen05 kernel (kpad <= 64, m up to 512: SMEM-resident limbs), 2 the 4-CTA cluster
+ * tcgen05 kernel (64 < kpad <= 128, m up to ~1500: X' tiles multicast to four CTAs
+ * that own 32 columns each), 0 the CUDA-core (dp4a) kernel; cdmd_foreground -> 2 tcgen05 dynamic,
  * 1 CUDA-core dynamic, 0 static.  Negative on invalid arguments. */
 CDMD_API int32_t cdmd_modes_path(const cdmd_model* model);
 CDMD_API int32_t cdmd_foreground_path(const cdmd_video* v, const cdmd_model* model, int32_t mode);

@@ -316,7 +316,8 @@ cdmd_status cdmd_foreground(cdmd_handle h, const cdmd_video* v, const cdmd_model
 
 int32_t cdmd_modes_path(const cdmd_model* M) {
   if (!M || M->k < 1) return -1;
-  return modes_tc_supported(*M) ? 1 : 0;
+  if (!modes_tc_supported(*M)) return 0;
+  return (M->kpad > 64 && !getenv("CDMD_MODES_NO_MC")) ? 2 : 1;
 }
 
 int32_t cdmd_foreground_path(const cdmd_video* v, const cdmd_model* M, int32_t mode) {

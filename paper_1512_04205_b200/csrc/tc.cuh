@@ -153,6 +153,24 @@ __device__ __forceinline__ void mma2_commit_multicast(uint64_t* bar, uint16_t ma
                : "memory");
 }
 
+// TMA 2-D load of a box into the same shared offset of every CTA in `mask`, each
+// CTA's mbarrier at `bar`'s offset receiving complete_tx for the bytes it got
+__device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* map, uint64_t* bar, int32_t c0,
+                                               int32_t c1, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "h"(mask)
+      : "memory");
+}
+// single-CTA MMAs: arrive on the mbarrier at this offset in every CTA of `mask`
+__device__ __forceinline__ void mma_commit_multicast(uint64_t* bar, uint16_t mask) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                   smem_u32(bar)),
+               "h"(mask)
+               : "memory");
+}
+
 // ------------------------------------------------- dynamic persistent tile schedule
 // A persistent CTA claims tiles from a global counter instead of a fixed stride, so
 // a CTA that starts late (its SM still held by another stream's kernel) just claims

@@ -212,6 +212,21 @@ def test_modes_tensor_core_equals_simt(C, H):
     assert torch.equal(a, b)
 
 
+def test_modes_cluster_kernel_equals_simt(C, H):
+    """k_eff > 64: the 4-CTA cluster kernel (X' multicast, 32 columns per CTA, the
+    last group partly past k_eff) is bit-identical to the dp4a kernel; ragged n and m."""
+    X = make_video(333, 120, 161, seed=5, noise=2.0, n_rects=2)
+    m, n = X.shape
+    Xd = to_dev(X)
+    P = C.Pipeline(H, n, n, m, "sparse", 300, 100, 6)
+    P.sketch(Xd)
+    P.fit()
+    assert P.model.k_eff > 64 and C.cdmd_modes_path(P.model) == 2
+    a = P.modes(Xd).clone()
+    b = P.modes(Xd, simt=True).clone()
+    assert torch.equal(a, b)
+
+
 def test_sketch_slabs_sum_to_full(C, H):
     X = make_video(256, 90, 20, seed=8, noise=2.0, n_rects=1)
     m, n = X.shape
