@@ -378,7 +378,10 @@ class Streaming:
     batch (cdmd_fit, which blocks its own host thread) overlaps the HBM-bound passes
     and solves of the others.  Each batch runs the same five calls as Pipeline.run.
     With torch.distributed initialised, the per-batch all-reduces are issued in batch
-    order on every rank (a ticket lock), so collectives match across ranks."""
+    order on every rank (a ticket lock), so collectives match across ranks.
+    Each lane uses two streams: set CUDA_DEVICE_MAX_CONNECTIONS (up to 32) to at least
+    2 x lanes before CUDA initialises, or streams share the default 8 hardware queues
+    and a lane's waiting solve stalls other lanes' work (bench.py sets 32)."""
 
     def __init__(self, device, n_total, n_local, m, kind, p, k, K, lanes=4, s=0.0, seed=0, pix0=0, dt=1.0,
                  rank="fixed", fit_sms=0):

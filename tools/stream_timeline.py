@@ -10,6 +10,7 @@ import os
 import sys
 
 import numpy as np
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")   # as bench.py
 import torch
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
