@@ -295,6 +295,8 @@ def main():
         ms_max = float(ts.item())
         value = m / (ms_max * 1e-3)
         streaming = {"lanes": args.lanes, "ms_per_batch": round(ms_max, 4), "sm_partition": S.sms,
+                     "fits": "sharded: batch b solved on rank b mod N, model broadcast" if S.shard_fit
+                     else "every rank",
                      "note": "batches pipelined across lanes (own handle, stream, buffers, copy of X)"}
 
     # roofline of the dominant kernel: HBM-bound passes (algorithmic bytes per launch) and,

@@ -338,6 +338,17 @@ class Pipeline:
                  self.dt, stream)
         return self.model
 
+    def adopt_model(self):
+        """After model_buf was overwritten with a model fitted elsewhere (the sharded
+        streaming fits: a broadcast from the owning rank), refresh the host-side fields
+        from the model's device status words (k_eff, K_eff, n_coef).  Synchronises with
+        the current stream."""
+        M = self.model
+        off = M.dev_info - self.model_buf.data_ptr()
+        d = self.model_buf[off:off + 16].view(torch.int32).cpu().tolist()
+        M.k_eff, M.K_eff, M.n_coef, M.info, M.dt = d[0], d[1], d[2], 0, self.dt
+        return M
+
     def modes(self, X, stream=None, simt=False):
         v = video(X, self.n_total, self.pix0, self.n_local)
         cdmd_modes(self.h, v, self.model, self.Phi, stream, simt=simt)
@@ -384,9 +395,21 @@ class Streaming:
     and a lane's waiting solve stalls other lanes' work (bench.py sets 32)."""
 
     def __init__(self, device, n_total, n_local, m, kind, p, k, K, lanes=4, s=0.0, seed=0, pix0=0, dt=1.0,
-                 rank="fixed", fit_sms=0):
+                 rank="fixed", fit_sms=0, shard_fit=True):
+        """shard_fit (torch.distributed with world > 1): batch b's small solve runs only
+        on rank b mod world, which broadcasts the fitted model (one buffer) to the
+        others, instead of every rank repeating every solve.  Creating the Streaming
+        object is then collective (it makes a second process group)."""
         import threading
         self.lanes = []
+        self.world, self.grank, self.coll = 1, 0, None
+        import torch.distributed as dist
+        if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+            from .dist import OrderedCollectives
+            self.world, self.grank = dist.get_world_size(), dist.get_rank()
+            bc = dist.new_group(backend=dist.get_backend()) if shard_fit else None
+            self.coll = OrderedCollectives(None, bc)
+        self.shard_fit = shard_fit and self.world > 1
         lo, hi = torch.cuda.Stream.priority_range()
         self.sms = None
         if fit_sms > 0:
@@ -427,6 +450,8 @@ class Streaming:
         back; the copies run on the lane's stream, overlapping the other lanes' work."""
         import concurrent.futures as cf
         self._next_ar = 0
+        if self.coll is not None:
+            self.coll.reset()
         L = len(self.lanes)
         ends = [None] * L
 
@@ -442,9 +467,21 @@ class Streaming:
                     pipe.sketch(X, st)
                     if allreduce is not None:
                         self._ordered_allreduce(b, allreduce, pipe.Y)
-                    st_fit.wait_stream(st)
-                    pipe.fit(st_fit)
-                    st.wait_stream(st_fit)
+                    owner = b % self.world
+                    err = None
+                    if not self.shard_fit or owner == self.grank:
+                        st_fit.wait_stream(st)
+                        try:
+                            pipe.fit(st_fit)
+                        except Exception as e:   # still take part in the broadcast below
+                            err = e
+                        st.wait_stream(st_fit)
+                    if self.shard_fit:
+                        self.coll.broadcast(b, pipe.model_buf, owner)
+                        if owner != self.grank:
+                            pipe.adopt_model()
+                    if err is not None:
+                        raise err
                     pipe.modes(X, st)
                     pipe.foreground(X, tau, mode, st)
                     if host_masks is not None:

@@ -85,3 +85,59 @@ def test_slab_generation_is_consistent():
         parts = [make_video(200, 70, 6, seed=5, noise=2.0, n_rects=2, pix0=p0, n_local=nl)
                  for p0, nl in (slab(n, world, r) for r in range(world))]
         assert np.array_equal(np.concatenate(parts, axis=1), X)
+
+
+def _ordered_worker(rank, world, port, out):
+    import random
+    import threading
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1512_04205_b200.dist import OrderedCollectives, fit_owner
+        coll = OrderedCollectives(None, dist.new_group(backend="gloo"))
+        nb, lanes = 12, 5
+        res = {}
+        rng = random.Random(rank)
+
+        def lane(li):
+            for b in range(li, nb, lanes):
+                y = torch.full((7,), float(rank + 1) * (b + 1))
+                coll.allreduce(b, y)                     # sum over ranks: (1 + 2) (b + 1)
+                owner = fit_owner(b, world)
+                model = torch.full((5,), 1000.0 * b + owner) if rank == owner else torch.zeros(5)
+                coll.broadcast(b, model, owner)          # every rank gets the owner's "model"
+                res[b] = (y.tolist(), model.tolist())
+                threading.Event().wait(rng.random() * 0.01)
+
+        ts = [threading.Thread(target=lane, args=(li,)) for li in rng.sample(range(lanes), lanes)]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join(timeout=120)
+        out.put((rank, res))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_ordered_collectives_sharded_fits_two_ranks():
+    """Streaming's batch-ordered collectives (dist.OrderedCollectives): lanes reach
+    their all-reduce and model broadcast in any order on each rank; tickets issue them
+    in batch order on two communicators, and each batch's model comes from its owner
+    rank (b mod world)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_ordered_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p_ in ps:
+        p_.start()
+    got = dict(q.get(timeout=180) for _ in range(2))
+    for p_ in ps:
+        p_.join(timeout=60)
+        assert p_.exitcode == 0
+    for rank in (0, 1):
+        res = got[rank]
+        assert sorted(res) == list(range(12))
+        for b, (y, model) in res.items():
+            assert y == [3.0 * (b + 1)] * 7
+            assert model == [1000.0 * b + (b % 2)] * 5

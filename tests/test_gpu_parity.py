@@ -582,3 +582,60 @@ def test_streaming_sm_partition_equal_sequential(tmp_path):
     r = subprocess.run([sys.executable, str(script), root], cwd=root, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
     assert "partition ok" in r.stdout
+
+
+_SHARDED_FIT_SCRIPT = r"""
+import os, sys, torch
+import torch.distributed as dist
+sys.path.insert(0, sys.argv[1])
+rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+dist.init_process_group("gloo", rank=rank, world_size=world)
+from paper_1512_04205_b200 import cdmd as C
+from paper_1512_04205_b200.dist import slab
+from synth.scene import make_video
+W, H, m, p, k, K, tau = 640, 360, 120, 600, 20, 6, 25.0
+n = W * H
+pix0, nl = slab(n, world, rank)
+Xs = make_video(W, H, m, seed=11, noise=2.0, n_rects=2, pix0=pix0, n_local=nl)
+ld = ((nl + 15) // 16) * 16
+X0 = torch.zeros((m, ld), dtype=torch.uint8, device="cuda")
+X0[:, :nl] = torch.from_numpy(Xs).cuda()
+vids = [X0, X0.flip(0).contiguous(), X0.roll(5, dims=0).contiguous(), X0.roll(-9, dims=0).contiguous(),
+        X0.roll(17, dims=0).contiguous()]
+ar = lambda Y: dist.all_reduce(Y, op=dist.ReduceOp.SUM)
+out = {}
+for shard in (True, False):
+    S = C.Streaming(0, n, nl, m, "sparse", p, k, K, lanes=2, pix0=pix0, shard_fit=shard)
+    assert S.shard_fit == shard
+    ends = S.run(vids, tau, C.BG_DYNAMIC, allreduce=ar)
+    for e in ends:
+        torch.cuda.current_stream().wait_event(e)
+    torch.cuda.synchronize()
+    out[shard] = [(pipe.Y.clone(), pipe.Phi.clone(), pipe.mask.clone(), pipe.model.k_eff, pipe.model.K_eff,
+                   pipe.model.n_coef) for (_, _, _, pipe) in S.lanes]
+for a, b in zip(out[True], out[False]):
+    assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1]) and torch.equal(a[2], b[2]), rank
+    assert a[3:] == b[3:], (a[3:], b[3:])
+dist.barrier()
+dist.destroy_process_group()
+sys.stdout.write(f"sharded ok {rank}\n")   # one write: lines of the two ranks do not interleave
+sys.stdout.flush()
+"""
+
+
+def test_streaming_sharded_fits_equal_replicated(tmp_path):
+    """Two ranks (gloo, both on cuda:0: host-mediated collectives, no kernel waits on
+    another rank's): with sharded fits each batch is solved on rank b mod 2 and its
+    model broadcast; sketches, modes, masks and model sizes equal the replicated-fit
+    run bit for bit on both ranks."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "sharded_check.py"
+    script.write_text(_SHARDED_FIT_SCRIPT)
+    port = 29500 + (os.getpid() % 1000)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(script), root]
+    r = subprocess.run(cmd, cwd=root, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+    assert "sharded ok 0" in r.stdout and "sharded ok 1" in r.stdout
