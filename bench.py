@@ -193,9 +193,17 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # CDMD_DIST_BACKEND=gloo (with more ranks than GPUs: ranks share devices) is only for
+    # exercising the multi-rank code path on a one-GPU box; its numbers mean nothing
+    backend = os.environ.get("CDMD_DIST_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     cfg = config_by_name(args.config)
     n, m = cfg.n, cfg.m
     pix0, nl = slab(n, world, rank)
