@@ -177,6 +177,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--lanes", type=int, default=24,
                     help="batches in flight (streaming, P:573); 1 = one batch at a time")
+    ap.add_argument("--replicated-fits", action="store_true",
+                    help="N > 1 streaming: every rank solves every batch (north_star's redundant solve) "
+                         "instead of rank b mod N solving batch b and broadcasting the model")
     ap.add_argument("--fit-sms", type=int, default=0,
                     help="streaming: SMs reserved for the small solves (green-context partition; 0 = shared)")
     args = ap.parse_args()
@@ -272,7 +275,8 @@ def main():
     if args.lanes > 1:
         # K batches through `lanes` concurrent lanes; each lane reads its own copy of X
         S = C.Streaming(local, n, nl, m, cfg.kind, cfg.p, cfg.k, cfg.K, lanes=args.lanes,
-                        seed=cfg.sensing_seed, pix0=pix0, rank=args.rank, fit_sms=args.fit_sms)
+                        seed=cfg.sensing_seed, pix0=pix0, rank=args.rank, fit_sms=args.fit_sms,
+                        shard_fit=not args.replicated_fits)
         Xs = [Xd] + [Xd.clone() for _ in range(args.lanes - 1)]
         ar = (lambda Y: dist.all_reduce(Y, op=dist.ReduceOp.SUM)) if world > 1 else None
 
