@@ -295,36 +295,32 @@ __global__ void __launch_bounds__(32 * (2 + FG_EPI_WARPS), 1) foreground_tc_kern
         const uint8_t* xs = sX + (size_t)stage * FG_XSTAGE;
         const uint32_t ta = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(tb * FG_BN);
         const int64_t t = (int64_t)fb * FG_BM + r;
-        // this warp's bytes of the unit first: the X stage goes back to the TMA producer
-        // before the mask arithmetic (more of the stage ring in flight)
-        uint32_t xw[FG_PW / 32][8];
+        uint32_t words[FG_PW / 32];
 #pragma unroll
         for (int w = 0; w < FG_PW / 32; ++w) {
           const int j0 = sl * FG_PW + 32 * w;       // pixel offset in the tile
+          uint32_t L[32];
+          tc::tmem_ld16(ta + j0, *reinterpret_cast<uint32_t(*)[16]>(&L[0]));
+          tc::tmem_ld16(ta + j0 + 16, *reinterpret_cast<uint32_t(*)[16]>(&L[16]));
           // pixels j0..j0+31 of frame r: box j0/128, 16-B chunks c, c+1 XOR-swizzled by r%8
           const uint8_t* row = xs + (j0 >> 7) * (FG_XSTAGE / 2) + r * 128;
           const int c = (j0 & 127) >> 4;
           const uint4 a = *reinterpret_cast<const uint4*>(row + (((c) ^ (r & 7)) << 4));
           const uint4 b = *reinterpret_cast<const uint4*>(row + (((c + 1) ^ (r & 7)) << 4));
-          xw[w][0] = a.x; xw[w][1] = a.y; xw[w][2] = a.z; xw[w][3] = a.w;
-          xw[w][4] = b.x; xw[w][5] = b.y; xw[w][6] = b.z; xw[w][7] = b.w;
-        }
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(&xempty[stage]);
-        if (++stage == stages) { stage = 0; phase ^= 1u; }
-        uint32_t words[FG_PW / 32];
-#pragma unroll
-        for (int w = 0; w < FG_PW / 32; ++w) {
-          const int j0 = sl * FG_PW + 32 * w;
-          uint32_t L[32];
-          tc::tmem_ld16(ta + j0, *reinterpret_cast<uint32_t(*)[16]>(&L[0]));
-          tc::tmem_ld16(ta + j0 + 16, *reinterpret_cast<uint32_t(*)[16]>(&L[16]));
+          const uint32_t xw[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
           tc::tmem_ld_wait();
-          words[w] = (dbg & 1) ? 0u : mask32(xw[w], L, tau);
+          words[w] = (dbg & 1) ? 0u : mask32(xw, L, tau);
         }
+        // the stage goes back only after the words are built: the shared loads have
+        // then completed (handing it back right after issuing them raced with the
+        // producer's next TMA write into the stage -- rare mask errors under load)
         tc::fence_before();
         __syncwarp();
-        if (lane == 0) tc::mbar_arrive(&tempty[tb]);
+        if (lane == 0) {
+          tc::mbar_arrive(&tempty[tb]);
+          tc::mbar_arrive(&xempty[stage]);
+        }
+        if (++stage == stages) { stage = 0; phase ^= 1u; }
         const int64_t w0 = ((int64_t)tile * FG_BN + sl * FG_PW) >> 5;   // first mask word
         if (t < m) {
           uint32_t* dst = mask + t * ldw + w0;
