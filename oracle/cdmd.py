@@ -136,7 +136,14 @@ def optimal_rank(s, rows, cols):
     return max(int(np.count_nonzero(s > tau)), 1)
 
 
-def fit(Yfull, k, K, dt=1.0, rank_rtol=RANK_RTOL, rank="fixed"):
+def select_background(omega, eps, cap=32):
+    """Background modes by frequency (modes with |omega_p| ~ 0 model the
+    slowly varying background): the columns j with |omega_j| < eps, in index order,
+    at most `cap` (the device's support limit)."""
+    return [j for j in range(len(omega)) if abs(omega[j]) < eps][:cap]
+
+
+def fit(Yfull, k, K, dt=1.0, rank_rtol=RANK_RTOL, rank="fixed", omega_eps=None):
     """cDMD small solve from the full sketch Y_full = C D (p x m).
 
     Y = Y_full[:, :m-1], Y' = Y_full[:, 1:] (Eq. FullData; reading R2).
@@ -144,6 +151,8 @@ def fit(Yfull, k, K, dt=1.0, rank_rtol=RANK_RTOL, rank="fixed"):
     A~ = U* Y' V S^-1 (P:342, P:303-309); step 7 eig (P:344, P:310-314);
     Phi_Y = Y' V S^-1 W (P:315-317); Remark 3: beta = omp(Phi_Y, y1) (P:369);
     omega = log(lambda)/dt (principal branch, reading R15).
+    omega_eps: select the background by |omega| < omega_eps (select_background)
+    instead of OMP, beta = least squares of y1 on those compressed modes.
     """
     Yfull = np.asarray(Yfull, dtype=np.float64)
     p, m = Yfull.shape
@@ -165,8 +174,13 @@ def fit(Yfull, k, K, dt=1.0, rank_rtol=RANK_RTOL, rank="fixed"):
     M = V @ np.diag(1.0 / s) @ W                       # V S^-1 W, (m-1) x k
     PhiY = Yp @ M                                      # compressed modes, p x k
     y1 = Y[:, 0]                                       # first compressed frame
-    support, beta = omp(PhiY, y1, K)
     omega = np.log(lam) / dt
+    if omega_eps is None:
+        support, beta = omp(PhiY, y1, K)
+    else:
+        support = select_background(omega, omega_eps)
+        beta = (np.linalg.lstsq(PhiY[:, support].astype(np.complex128), y1.astype(np.complex128), rcond=None)[0]
+                if support else np.zeros(0, dtype=np.complex128))
     return dict(k=k, k_eff=k_eff, sigma=s, V=V, U=U, Atilde=Atilde, lam=lam, W=W,
                 pair=pair, M=M, PhiY=PhiY, support=list(support), beta=beta,
                 omega=omega, dt=dt, m=m, p=p)
