@@ -130,6 +130,15 @@ CDMD_API const char* cdmd_version(void);
  * Diagnostics: bench.py reports the difference across its timed region.          */
 CDMD_API uint64_t cdmd_kernel_launches(void);
 
+/* Background selection of later cdmd_fit calls on this handle.  omega_eps = 0 (the
+ * default): Remark 3's OMP picks at most K modes.  omega_eps > 0: the
+ * background is the set of modes with |omega_p| = |log(lambda_p)| / dt < omega_eps
+ * ("background modes have |omega_p| ~ 0"), in mode order, at most 32 (K is
+ * then ignored), with amplitudes the least-squares fit of the first compressed frame
+ * on those modes (the same solve OMP ends with).  Errors: CDMD_ERR_ARG (null
+ * handle), CDMD_ERR_RANGE (negative or non-finite omega_eps).                     */
+CDMD_API cdmd_status cdmd_set_background_selection(cdmd_handle h, double omega_eps);
+
 /* Spatial SM partition for streaming many batches ("decomposed in consecutive
  * batches"): splits device `device`'s SMs once per process into two green contexts —
  * `fit_sms` SMs (rounded up to the hardware granularity: multiples of 8) reserved for

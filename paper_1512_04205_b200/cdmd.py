@@ -59,7 +59,8 @@ SYMBOLS = ["cdmd_create", "cdmd_destroy", "cdmd_status_str", "cdmd_version", "cd
            "cdmd_fit_workspace_bytes", "cdmd_fit", "cdmd_modes", "cdmd_background",
            "cdmd_foreground", "cdmd_philox", "cdmd_gaussian_table", "cdmd_sparse_cap",
            "cdmd_sensing_rows", "cdmd_modes_simt", "cdmd_eig", "cdmd_mask_median3",
-           "cdmd_modes_path", "cdmd_foreground_path", "cdmd_sm_partition"]
+           "cdmd_modes_path", "cdmd_foreground_path", "cdmd_sm_partition",
+           "cdmd_set_background_selection"]
 
 
 def _load():
@@ -85,6 +86,7 @@ def _load():
         "cdmd_background": (i32, [vp, vp, i64, i64, M, i32, i64, i64, vp, i64, vp]),
         "cdmd_foreground": (i32, [vp, V, M, vp, i64, i32, ctypes.c_float, vp, i64, vp]),
         "cdmd_mask_median3": (i32, [vp, i64, i64, i64, i64, vp, vp]),
+        "cdmd_set_background_selection": (i32, [vp, dbl]),
         "cdmd_sm_partition": (i32, [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(vp),
                                     ctypes.POINTER(vp), ctypes.POINTER(ctypes.c_int)]),
         "cdmd_modes_path": (i32, [M]),
@@ -306,11 +308,13 @@ class Pipeline:
     five-call hot path sketch -> [all-reduce] -> fit -> modes -> foreground."""
 
     def __init__(self, handle, n_total, n_local, m, kind, p, k, K, s=0.0, seed=0, pix0=0,
-                 device="cuda", dt=1.0, rank="fixed"):
-        """rank="fixed": target rank k; rank="gd": Gavish-Donoho rank, at most k (Remark 2)."""
+                 device="cuda", dt=1.0, rank="fixed", omega_eps=0.0):
+        """rank="fixed": target rank k; rank="gd": Gavish-Donoho rank, at most k (Remark 2).
+        omega_eps > 0: background = modes with |omega| < omega_eps instead of OMP."""
         if rank not in ("fixed", "gd"):
             raise ValueError(rank)
         self.rank = rank
+        self.omega_eps = float(omega_eps)
         self.h = handle
         self.kind = KINDS[kind] if isinstance(kind, str) else int(kind)
         self.n_total, self.n_local, self.m, self.p, self.k, self.K = n_total, n_local, m, p, k, K
@@ -334,6 +338,7 @@ class Pipeline:
 
     def fit(self, stream=None):
         k = -self.k if self.rank == "gd" else self.k
+        _check("cdmd_set_background_selection", _lib.cdmd_set_background_selection(self.h.h, self.omega_eps))
         cdmd_fit(self.h, self.Y, self.kind, self.p, self.m, k, self.K, self.model, self.ws_fit,
                  self.dt, stream)
         return self.model

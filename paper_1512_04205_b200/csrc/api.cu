@@ -100,6 +100,13 @@ const char* cdmd_version(void) { return "cdmd-b200 0.1 (sm_100a)"; }
 
 uint64_t cdmd_kernel_launches(void) { return cdmd::launch_counter().load(std::memory_order_relaxed); }
 
+cdmd_status cdmd_set_background_selection(cdmd_handle h, double omega_eps) {
+  if (!h) return CDMD_ERR_ARG;
+  if (!(omega_eps >= 0.0) || !isfinite(omega_eps)) return CDMD_ERR_RANGE;
+  h->omega_eps = omega_eps;
+  return CDMD_OK;
+}
+
 const char* cdmd_status_str(cdmd_status s) {
   switch (s) {
     case CDMD_OK: return "ok";

@@ -298,7 +298,7 @@ __global__ void __launch_bounds__(256) omp_kernel(
     int k, int K, int64_t m, const double* __restrict__ Gf, const double* __restrict__ cf,
     const double* __restrict__ G, const int32_t* __restrict__ pair, const double* __restrict__ lam,
     double* __restrict__ beta_out, int32_t* __restrict__ support_out, float* __restrict__ coef,
-    int32_t* __restrict__ coef_col, int* __restrict__ dinfo) {
+    int32_t* __restrict__ coef_col, int* __restrict__ dinfo, double omega_eps, double dt) {
   __shared__ double sc[512];
   __shared__ double red[256];
   __shared__ int redi[256];
@@ -317,12 +317,26 @@ __global__ void __launch_bounds__(256) omp_kernel(
     mode_rep(pair, j, ra, rb, sg);
     alpha[j] = {cf[ra], -sg * cf[rb]};
   }
-  if (tid == 0) { nS_sh = 0; stop_sh = 0; }
+  // frequency selection: the columns with |omega| = |log lambda| / dt < omega_eps,
+  // in index order, at most 32; each is added as a forced "OMP step" (same least squares)
+  __shared__ int T[32];
+  __shared__ int nT_sh;
+  if (tid == 0) {
+    nS_sh = 0; stop_sh = 0; nT_sh = 0;
+    if (omega_eps > 0.0) {
+      for (int j = 0; j < k && nT_sh < 32; ++j) {
+        const double lr = lam[2 * j], li = lam[2 * j + 1];
+        const double om = hypot(log(hypot(lr, li)), atan2(li, lr)) / dt;
+        if (om < omega_eps) T[nT_sh++] = j;
+      }
+    }
+  }
   __syncthreads();
-  const int Kmax = K < k ? K : k;
+  const bool by_freq = omega_eps > 0.0;
+  const int Kmax = by_freq ? nT_sh : (K < k ? K : k);
   for (int it = 0; it < Kmax; ++it) {
     const int nS = nS_sh;
-    if (tid == 0) {
+    if (tid == 0 && !by_freq) {
       double rn2 = y1n2;
       for (int s = 0; s < nS; ++s) {
         const cplx t = cconjmul(alpha[S[s]], beta[s]);
@@ -368,8 +382,8 @@ __global__ void __launch_bounds__(256) omp_kernel(
       __syncthreads();
     }
     if (tid == 0) {
-      const int js = redi[0];
-      if (!(bmax > 0.0) || !isfinite(bmax) || js >= k || nS >= 32) {
+      const int js = by_freq ? T[it] : redi[0];
+      if ((!by_freq && (!(bmax > 0.0) || !isfinite(bmax))) || js >= k || nS >= 32) {
         stop_sh = 1;
       } else {
         S[nS] = js;
@@ -681,7 +695,7 @@ cdmd_status fit_impl(cdmd_handle h, const void* Y, int64_t ldy, int kind, int64_
   prof.mark("canon+M+gram");
   note_launch();
   omp_kernel<<<1, 256, 0, st>>>(ke, K, m, W.Gf, W.cf, W.G, model->pair, model->lambda, model->beta,
-                                model->support, model->coef, model->coef_col, W.dinfo);
+                                model->support, model->coef, model->coef_col, W.dinfo, h->omega_eps, dt);
   CU(cudaGetLastError());
   prof.mark("omp+coef");
   note_launch();

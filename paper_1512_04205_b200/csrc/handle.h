@@ -17,6 +17,7 @@ struct cdmd_handle_s {
   int32_t* host_info = nullptr;      // pinned, 16 words for fit read-back
   int* sched = nullptr;              // device, tile counters of the persistent kernels (0 modes, 1 foreground)
   std::vector<char> host_ws;         // cuSOLVER host workspace (fit only)
+  double omega_eps = 0.0;            // > 0: background by |omega| < omega_eps, else OMP
 };
 
 namespace cdmd {

@@ -42,10 +42,10 @@ def to_dev(X, ld=None):
     return buf
 
 
-def gpu_run(C, H, X, kind, p, k, K, tau, s=0.0, seed=0, modes_simt=False, ld=None, rank="fixed"):
+def gpu_run(C, H, X, kind, p, k, K, tau, s=0.0, seed=0, modes_simt=False, ld=None, rank="fixed", omega_eps=0.0):
     m, n = X.shape
     Xd = to_dev(X, ld)
-    P = C.Pipeline(H, n, n, m, kind, p, k, K, s=s, seed=seed, rank=rank)
+    P = C.Pipeline(H, n, n, m, kind, p, k, K, s=s, seed=seed, rank=rank, omega_eps=omega_eps)
     Y = P.sketch(Xd).cpu().numpy().T.copy()          # p x m
     P.fit()
     mh = C.model_to_host(P.model)
@@ -60,9 +60,9 @@ def gpu_run(C, H, X, kind, p, k, K, tau, s=0.0, seed=0, modes_simt=False, ld=Non
     return out
 
 
-def oracle_run(X, kind, p, k, K, tau, s=None, seed=0, rank="fixed"):
-    Y = OS.sketch(X, KIND[kind], p, seed, s=s)
-    model = OD.fit(Y, k, K, rank=rank)
+def oracle_run(X, kind, p, k, K, tau, s=None, seed=0, rank="fixed", omega_eps=None, Y=None):
+    Y = OS.sketch(X, KIND[kind], p, seed, s=s) if Y is None else Y
+    model = OD.fit(Y, k, K, rank=rank, omega_eps=omega_eps)
     Phi = OD.modes(X, model["M"])
     Ld = OD.background_dynamic(Phi, model)          # n x m
     Ls = OD.background_static(Phi, model)           # n
@@ -465,6 +465,40 @@ def test_pipeline_parity_gavish_donoho(C, H, case):
     o = oracle_run(X, kind, p, k, K, tau, rank="gd")
     assert g["model"]["k_eff"] == o["model"]["k_eff"]
     assert 1 <= o["model"]["k_eff"] <= k
+    check_all(g, o, kind, tau)
+
+
+def _omega_gap_eps(omega, want):
+    """A threshold between |omega| values with a clear gap, selecting about `want`
+    modes (never splitting equal |omega|, e.g. a conjugate pair)."""
+    a = np.sort(np.abs(omega))
+    for i in list(range(want - 1, len(a) - 1)) + list(range(want - 2, -1, -1)):
+        if a[i + 1] - a[i] > 1e-2 * max(1.0, a[i + 1]):
+            return 0.5 * (a[i] + a[i + 1])
+    pytest.skip("no clear |omega| gap")
+
+
+@pytest.mark.parametrize("case,want", [("c1", 1), ("ragged_sparse", 3), ("c2", 2)])
+def test_pipeline_parity_frequency_background(C, H, case, want):
+    """Background by frequency (|omega| < eps instead of OMP): the device selects
+    the same modes as the oracle and the amplitudes, backgrounds and masks keep parity.
+    eps sits in a clear gap of the oracle's |omega| (a threshold decision: both sides
+    see the same gap)."""
+    if case == "c2":
+        cfg = config_by_name("c2_320x240_spixel")
+        X, kind, p, k, K, tau = video_for(cfg), cfg.kind, cfg.p, cfg.k, cfg.K, cfg.tau
+    elif case == "c1":
+        cfg = config_by_name("c1_32x24_sparse")
+        X, kind, p, k, K, tau = video_for(cfg), cfg.kind, cfg.p, cfg.k, cfg.K, cfg.tau
+    else:
+        name, shape, kind, p, k, K, tau = next(c for c in CASES if c[0] == case)
+        W, Hh, m, noise, rects = shape
+        X = make_video(W, Hh, m, seed=zlib.crc32(name.encode()) % 1000, noise=noise, n_rects=rects)
+    Y = OS.sketch(X, KIND[kind], p, 0)
+    eps = _omega_gap_eps(OD.fit(Y, k, K)["omega"], want)
+    g = gpu_run(C, H, X, kind, p, k, K, tau, omega_eps=eps)
+    o = oracle_run(X, kind, p, k, K, tau, omega_eps=eps, Y=Y)
+    assert len(o["model"]["support"]) >= 1
     check_all(g, o, kind, tau)
 
 
