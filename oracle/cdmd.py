@@ -9,6 +9,7 @@ Steps, in the paper's order and notation:
                (rank="gd") chosen by the Gavish-Donoho optimal hard threshold
                (Remark 2; evaluation settings P:573) via optimal_rank()
   modes()      Alg. 1 step 8, Eq. cDMDModes  Phi = X' V S^-1 W
+  amplitudes() Alg. 1 step 9, b = lstsq(Phi, x_1) on the full-state modes
   background() Eq. DMDTerms (P:185-193): L = Re sum_{p in S} b_p phi_p lambda_p^{t-1}
                (dynamic) or x_BG = Re Phi beta (static)
   mask()       Eq. thres: 1 iff |x_jt - xhat_j| > tau
@@ -202,6 +203,14 @@ def modes(X, M):
     """
     Xp = np.asarray(X[1:], dtype=np.float64)           # (m-1, n)
     return Xp.T @ M                                    # (n, k)
+
+
+def amplitudes(X, Phi):
+    """b = lstsq(Phi, x_1) (Alg. 1 step 9: "Compute amplitudes using x_1 as
+    initial condition"), complex128 (k,).  X uint8 (m, n) frame-major, x_1 = frame 1
+    (P:71); Phi (n, k) complex as returned by modes()."""
+    x1 = np.asarray(X[0], dtype=np.float64).astype(np.complex128)
+    return np.linalg.lstsq(np.asarray(Phi, dtype=np.complex128), x1, rcond=None)[0]
 
 
 def background_static(Phi, model):
