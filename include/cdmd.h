@@ -219,6 +219,32 @@ CDMD_API cdmd_status cdmd_foreground(cdmd_handle h, const cdmd_video* v, const c
                             const float* Phi, int64_t ldphi, int32_t mode, float tau,
                             uint32_t* mask, int64_t ldw, cdmd_stream st);
 
+/* --------------------------------------------------------------- amplitudes
+ * Full-state amplitudes b = lstsq(Phi, x_1) (Alg. 1 step 9: "compute
+ * amplitudes using x_1 as initial condition"; the paper's alternative to the OMP
+ * amplitudes of Remark 3, which cdmd_fit computes on the compressed modes).  Two
+ * phases so a pixel-row-sharded run exchanges only k_eff (k_eff + 1) doubles:
+ *
+ * cdmd_amplitudes_gram: G = [F^T F | F^T x_1] over this slab, F = the folded Phi
+ *   of cdmd_modes (n_local x k_eff, ldphi), x_1 = frame 1 of the slab (v->X).  G:
+ *   device, k_eff x (k_eff + 1) doubles, column-major, ld k_eff, overwritten.  fp64
+ *   accumulation of exact fp32 products, fixed-order reduction (deterministic).
+ *   ws: device, >= cdmd_amplitudes_workspace_bytes(h, k_eff) bytes.  Sum G over the
+ *   slabs (e.g. an all-reduce) before the solve.
+ * cdmd_amplitudes_solve: Cholesky of F^T F (fp64, one CTA), then b: device,
+ *   2 k_eff doubles (re, im) in the mode order of the model; conjugate pairs get
+ *   conjugate amplitudes.  A column of F dependent on earlier ones (pivot^2 <=
+ *   1e-12 (F^T F)_jj) gets c_j = 0 (a least-squares solution, not lstsq's minimum-
+ *   norm one; reading R24); dropped (device int32, may be NULL) receives
+ *   how many.  Errors: CDMD_ERR_ARG on null pointers, ldphi < n_local or a model
+ *   cdmd_fit has not filled; CDMD_ERR_RANGE if k_eff > 128; CDMD_ERR_WORKSPACE. */
+CDMD_API size_t cdmd_amplitudes_workspace_bytes(cdmd_handle h, int k);
+CDMD_API cdmd_status cdmd_amplitudes_gram(cdmd_handle h, const cdmd_video* v, const cdmd_model* model,
+                                          const float* Phi, int64_t ldphi, double* G, void* ws,
+                                          size_t ws_bytes, cdmd_stream st);
+CDMD_API cdmd_status cdmd_amplitudes_solve(cdmd_handle h, const cdmd_model* model, const double* G,
+                                           double* b, int32_t* dropped, cdmd_stream st);
+
 /* Which kernel a call would run (diagnostics for reports): cdmd_modes -> 1 the
  * tcgen05 kernel (kpad <= 64, m up to 512: SMEM-resident limbs), 2 the 4-CTA cluster
  * tcgen05 kernel (64 < kpad <= 128, m up to ~1500: X' tiles multicast to four CTAs

@@ -57,6 +57,7 @@ class Model(ctypes.Structure):
 SYMBOLS = ["cdmd_create", "cdmd_destroy", "cdmd_status_str", "cdmd_version", "cdmd_kernel_launches",
            "cdmd_sketch_workspace_bytes", "cdmd_sketch", "cdmd_model_bytes", "cdmd_model_bind",
            "cdmd_fit_workspace_bytes", "cdmd_fit", "cdmd_modes", "cdmd_background",
+           "cdmd_amplitudes_workspace_bytes", "cdmd_amplitudes_gram", "cdmd_amplitudes_solve",
            "cdmd_foreground", "cdmd_philox", "cdmd_gaussian_table", "cdmd_sparse_cap",
            "cdmd_sensing_rows", "cdmd_modes_simt", "cdmd_eig", "cdmd_mask_median3",
            "cdmd_modes_path", "cdmd_foreground_path", "cdmd_sm_partition",
@@ -96,6 +97,9 @@ def _load():
         "cdmd_sparse_cap": (i64, [i64, i64, dbl]),
         "cdmd_sensing_rows": (i32, [vp, i64, S, vp, vp, vp]),
         "cdmd_eig": (i32, [vp, ctypes.c_int, vp, vp, vp, vp]),
+        "cdmd_amplitudes_workspace_bytes": (sz, [vp, ctypes.c_int]),
+        "cdmd_amplitudes_gram": (i32, [vp, V, M, vp, i64, vp, vp, sz, vp]),
+        "cdmd_amplitudes_solve": (i32, [vp, M, vp, vp, vp, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -205,6 +209,23 @@ def cdmd_foreground(h, v, model, Phi, mode, tau, mask, stream=None):
     _check("cdmd_foreground", _lib.cdmd_foreground(h.h, ctypes.byref(v), ctypes.byref(model), _ptr(Phi),
                                                    Phi.stride(0), mode, float(tau), _ptr(mask), mask.stride(0),
                                                    _stream(stream)))
+
+
+def cdmd_amplitudes_workspace_bytes(h, k):
+    return int(_lib.cdmd_amplitudes_workspace_bytes(h.h, int(k)))
+
+
+def cdmd_amplitudes_gram(h, v, model, Phi, G, ws, stream=None):
+    """G: (k_eff + 1, k_eff) float64 CUDA tensor (column-major k_eff x (k_eff + 1))."""
+    _check("cdmd_amplitudes_gram", _lib.cdmd_amplitudes_gram(h.h, ctypes.byref(v), ctypes.byref(model), _ptr(Phi),
+                                                             Phi.stride(0), _ptr(G), _ptr(ws), ws.numel(),
+                                                             _stream(stream)))
+
+
+def cdmd_amplitudes_solve(h, model, G, b, dropped=None, stream=None):
+    """b: (k_eff, 2) float64 CUDA tensor (re, im); dropped: optional int32 CUDA scalar."""
+    _check("cdmd_amplitudes_solve", _lib.cdmd_amplitudes_solve(h.h, ctypes.byref(model), _ptr(G), _ptr(b),
+                                                               _ptr(dropped), _stream(stream)))
 
 
 def cdmd_modes_path(model):
@@ -371,6 +392,23 @@ class Pipeline:
         out = torch.empty_like(self.mask)
         cdmd_mask_median3(self.mask, width, height, out, stream)
         return out
+
+    def amplitudes(self, X, allreduce=None, stream=None):
+        """b = lstsq(Phi, x_1) (Alg. 1 step 9) from the modes of the last
+        modes() call: slab Gram [F^T F | F^T x_1] -> [allreduce(G), summing over the
+        pixel slabs] -> fp64 Cholesky solve.  Returns (b (k_eff,) complex128 CUDA
+        tensor, dropped (int32 CUDA scalar: dependent columns given c_j = 0))."""
+        v = video(X, self.n_total, self.pix0, self.n_local)
+        ke = self.model.k_eff
+        ws = _empty_bytes(cdmd_amplitudes_workspace_bytes(self.h, ke), self.Phi.device)
+        G = torch.empty((ke + 1, ke), dtype=torch.float64, device=self.Phi.device)
+        cdmd_amplitudes_gram(self.h, v, self.model, self.Phi, G, ws, stream)
+        if allreduce is not None:
+            allreduce(G)
+        b = torch.empty((ke, 2), dtype=torch.float64, device=self.Phi.device)
+        dropped = torch.zeros((), dtype=torch.int32, device=self.Phi.device)
+        cdmd_amplitudes_solve(self.h, self.model, G, b, dropped, stream)
+        return torch.view_as_complex(b), dropped
 
     def background(self, mode=BG_DYNAMIC, t0=0, nt=None, stream=None):
         nt = self.m - t0 if nt is None else nt

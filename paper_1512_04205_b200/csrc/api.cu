@@ -321,6 +321,34 @@ cdmd_status cdmd_foreground(cdmd_handle h, const cdmd_video* v, const cdmd_model
   return cuda_status(launch_foreground(*v, *M, Phi, ldphi, mode, tau, mask, ldw, h->sched + 1, (cudaStream_t)st));
 }
 
+// --------------------------------------------------------------- amplitudes
+size_t cdmd_amplitudes_workspace_bytes(cdmd_handle h, int k) {
+  if (!h || k < 1 || k > 128) return 0;
+  return al256(amp_gram_ws_bytes(h->sm_count, k));
+}
+
+cdmd_status cdmd_amplitudes_gram(cdmd_handle h, const cdmd_video* v, const cdmd_model* M,
+                                 const float* Phi, int64_t ldphi, double* G, void* ws,
+                                 size_t ws_bytes, cdmd_stream st) {
+  if (!h || !Phi || !G || !ws) return CDMD_ERR_ARG;
+  cdmd_status s = check_video(v);
+  if (s != CDMD_OK) return s;
+  if ((s = check_model(M, v->m)) != CDMD_OK) return s;
+  if (M->k_eff > 128) return CDMD_ERR_RANGE;
+  if (ldphi < v->n_local) return CDMD_ERR_ARG;
+  if (ws_bytes < amp_gram_ws_bytes(h->sm_count, M->k_eff)) return CDMD_ERR_WORKSPACE;
+  return cuda_status(launch_amp_gram(h->sm_count, Phi, ldphi, v->X, v->n_local, M->k_eff,
+                                     static_cast<double*>(ws), G, (cudaStream_t)st));
+}
+
+cdmd_status cdmd_amplitudes_solve(cdmd_handle h, const cdmd_model* M, const double* G, double* b,
+                                  int32_t* dropped, cdmd_stream st) {
+  if (!h || !G || !b || !M || !M->pair) return CDMD_ERR_ARG;
+  if (M->k_eff < 1 || M->k_eff > M->k) return CDMD_ERR_ARG;
+  if (M->k_eff > 128) return CDMD_ERR_RANGE;
+  return cuda_status(launch_amp_solve(G, M->k_eff, M->pair, b, dropped, (cudaStream_t)st));
+}
+
 int32_t cdmd_modes_path(const cdmd_model* M) {
   if (!M || M->k < 1) return -1;
   if (!modes_tc_supported(*M)) return 0;

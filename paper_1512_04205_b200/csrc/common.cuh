@@ -108,6 +108,11 @@ cudaError_t launch_modes_simt(const cdmd_video& v, const cdmd_model& M, float* P
 cudaError_t launch_modes_tc(const cdmd_video& v, const cdmd_model& M, float* Phi, int64_t ldphi,
                             int* tile_counter, cudaStream_t st);
 
+size_t amp_gram_ws_bytes(int sms, int k);
+cudaError_t launch_amp_gram(int sms, const float* Phi, int64_t ldphi, const uint8_t* x1, int64_t n_local,
+                            int k, double* ws, double* G, cudaStream_t st);
+cudaError_t launch_amp_solve(const double* G, int k, const int32_t* pair, double* b, int32_t* dropped,
+                             cudaStream_t st);
 cudaError_t launch_background(const float* Phi, int64_t ldphi, int64_t n_local, const cdmd_model& M,
                               int mode, int64_t t0, int64_t nt, float* L, int64_t ldl,
                               cudaStream_t st);

@@ -673,3 +673,89 @@ def test_streaming_sharded_fits_equal_replicated(tmp_path):
     r = subprocess.run(cmd, cwd=root, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
     assert "sharded ok 0" in r.stdout and "sharded ok 1" in r.stdout
+
+
+# ------------------------------------------- amplitudes b = lstsq(Phi, x_1)
+AMP_CASES = [
+    # name, (W, H, m, noise, rects) or None (C1), kind, p, k
+    ("c1", None, "sparse", 50, 10),
+    ("ragged_sparse", (100, 37, 33, 2.0, 1), "sparse", 120, 12),
+    ("rademacher_small", (180, 120, 60, 2.0, 2), "rademacher", 300, 20),
+    ("k50_ragged", (333, 101, 77, 2.0, 2), "sparse", 200, 50),
+    ("k100", (256, 160, 150, 2.0, 2), "sparse", 400, 100),
+]
+
+
+@pytest.mark.parametrize("case", AMP_CASES, ids=[c[0] for c in AMP_CASES])
+def test_amplitudes_parity(C, H, case):
+    name, shape, kind, p, k = case
+    if shape is None:
+        X = video_for(config_by_name("c1_32x24_sparse"))
+    else:
+        W, Hh, m, noise, rects = shape
+        X = make_video(W, Hh, m, seed=zlib.crc32(name.encode()) % 1000, noise=noise, n_rects=rects)
+    m, n = X.shape
+    K = min(2, k)
+    Xd = to_dev(X)
+    P = C.Pipeline(H, n, n, m, kind, p, k, K)
+    P.sketch(Xd)
+    P.fit()
+    F = P.modes(Xd)
+    b, dropped = P.amplitudes(Xd)
+    torch.cuda.synchronize()
+    mh = C.model_to_host(P.model)
+    b = b.cpu().numpy()
+    assert int(dropped.item()) == 0
+    # (1) step 9 alone: the oracle's lstsq on the GPU's own modes (same input) -> tight
+    Phi_g = PT.unfold(F.cpu().numpy(), mh["pair"])
+    b_o = OD.amplitudes(X, Phi_g)
+    cond = np.linalg.cond(Phi_g)
+    err1 = np.linalg.norm(b - b_o) / np.linalg.norm(b_o)
+    assert err1 <= 1e-12 * cond * cond + 1e-9, (err1, cond)
+    for j in np.nonzero(mh["pair"] == 1)[0]:
+        assert b[j + 1] == np.conj(b[j])
+    # (2) end to end against the oracle's modes: per-mode contributions b_j phi_j
+    # (invariant to each mode's phase normalisation) and the reconstruction of x_1
+    o = OD.fit(OS.sketch(X, KIND[kind], p, 0), k, K)
+    Phi_o = OD.modes(X, o["M"])
+    bo = OD.amplitudes(X, Phi_o)
+    perm, werr = PT.match_eigs(mh["lam"], o["lam"])
+    assert werr <= PT.RTOL_EIG
+    x1 = np.linalg.norm(X[0].astype(np.float64))
+    rec_g = (Phi_g @ b).real
+    rec_o = (Phi_o @ bo).real
+    assert np.linalg.norm(rec_g - rec_o) <= 1e-4 * x1, np.linalg.norm(rec_g - rec_o) / x1
+    worst = 0.0
+    for i, j in enumerate(perm):
+        if PT.well_separated(o["lam"], j, 1e-3):
+            worst = max(worst, np.linalg.norm(b[i] * Phi_g[:, i] - bo[j] * Phi_o[:, j]) / x1)
+    print(f"{name}: k_eff={mh['lam'].size} cond={cond:.3g} step9_rel={err1:.2e} contrib={worst:.2e}")
+    assert worst <= PT.RTOL_PHI   # b_j phi_j inherits the north_star modes tolerance
+
+
+def test_amplitudes_slabs_sum_to_full(C, H):
+    # pixel-row sharding: Gram partials of two slabs sum to the whole-video Gram
+    X = make_video(320, 120, 60, seed=11, noise=2.0, n_rects=2)
+    m, n = X.shape
+    Xd = to_dev(X)
+    P = C.Pipeline(H, n, n, m, "sparse", 200, 16, 4)
+    P.sketch(Xd)
+    P.fit()
+    F = P.modes(Xd)
+    ke = P.model.k_eff
+    ws = torch.empty(C.cdmd_amplitudes_workspace_bytes(H, ke), dtype=torch.uint8, device="cuda")
+    G = torch.empty((ke + 1, ke), dtype=torch.float64, device="cuda")
+    C.cdmd_amplitudes_gram(H, C.video(Xd, n, 0, n), P.model, P.Phi, G, ws)
+    n1 = 128 * 97
+    Gs = torch.zeros_like(G)
+    for pix0, nl in ((0, n1), (n1, n - n1)):
+        Gp = torch.empty_like(G)
+        C.cdmd_amplitudes_gram(H, C.video(Xd[:, pix0:], n, pix0, nl), P.model, P.Phi[:, pix0:], Gp, ws)
+        Gs += Gp
+    torch.cuda.synchronize()
+    G, Gs = G.cpu().numpy(), Gs.cpu().numpy()
+    assert np.max(np.abs(G - Gs)) <= 1e-12 * np.max(np.abs(G))
+    # and the Gram itself equals the fp64 product of the (exact) fp32 modes
+    Ff = F.cpu().numpy().astype(np.float64)
+    ref = np.concatenate([Ff @ Ff.T, Ff @ X[0].astype(np.float64)[:, None]], 1)   # k x (k+1)
+    assert np.max(np.abs(G.T - ref)) <= 1e-12 * np.max(np.abs(ref))
