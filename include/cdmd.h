@@ -227,8 +227,9 @@ CDMD_API cdmd_status cdmd_foreground(cdmd_handle h, const cdmd_video* v, const c
  *
  * cdmd_amplitudes_gram: G = [F^T F | F^T x_1] over this slab, F = the folded Phi
  *   of cdmd_modes (n_local x k_eff, ldphi), x_1 = frame 1 of the slab (v->X).  G:
- *   device, k_eff x (k_eff + 1) doubles, column-major, ld k_eff, overwritten.  fp64
- *   accumulation of exact fp32 products, fixed-order reduction (deterministic).
+ *   device, k_eff x (k_eff + 1) doubles, column-major, ld k_eff, overwritten.  fp32
+ *   sums within 128-pixel tiles, fp64 across tiles, fixed-order reduction
+ *   (deterministic).
  *   ws: device, >= cdmd_amplitudes_workspace_bytes(h, k_eff) bytes.  Sum G over the
  *   slabs (e.g. an all-reduce) before the solve.
  * cdmd_amplitudes_solve: Cholesky of F^T F (fp64, one CTA), then b: device,

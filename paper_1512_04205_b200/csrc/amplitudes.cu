@@ -7,8 +7,9 @@
 // (pair), because phi_j b_j + conj(phi_j b_j) = 2 (F_j Re b_j - F_{j+1} Im b_j).
 //
 // Two phases so a pixel-row-sharded run only exchanges k (k + 1) doubles:
-//   gram : G = [F^T F | F^T x_1] of the slab (HBM pass over Phi, fp64 accumulation of
-//          exact fp32 x fp32 products, fixed-order block reduction: deterministic);
+//   gram : G = [F^T F | F^T x_1] of the slab (one pass over Phi; register-blocked fp32
+//          FMAs within a 128-pixel tile, fp64 across tiles; fixed-order reduction of
+//          the per-CTA partials: deterministic);
 //   solve: Cholesky of F^T F in fp64 on one CTA, two triangular solves, unfold to b.
 // The caller sums G over slabs (all-reduce) between the two calls.
 #include "handle.h"
@@ -16,8 +17,7 @@
 namespace cdmd {
 namespace {
 
-constexpr int kAmpThreads = 512;
-constexpr int kAmpTile = 64;  // pixels per shared-memory tile
+constexpr int kAmpTile = 128;  // pixels per shared-memory tile
 
 __host__ __device__ inline int amp_entries(int k) { return k * (k + 1) / 2 + k; }
 
@@ -31,48 +31,121 @@ __device__ inline void amp_entry(int e, int k, int& i, int& j) {
   j = r + (e - base);
 }
 
-template <int NQ>
-__global__ void __launch_bounds__(kAmpThreads)
+// Shared row stride: 16-byte aligned and = 4 (mod 8) words (4-way store conflicts at worst).
+__host__ __device__ inline int amp_ldc(int nb) { return (4 * nb) % 8 == 0 ? 4 * nb + 4 : 4 * nb + 8; }
+
+// Row-major offset of entry (i, j), i <= j, in the list above.
+__host__ __device__ inline int amp_entry_index(int i, int j, int k) {
+  return i * (k + 1) - i * (i - 1) / 2 + (j - i);
+}
+
+__device__ inline void cp_async4(float* dst, const float* src, bool valid) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(d), "l"(src), "r"(valid ? 4 : 0)
+               : "memory");
+}
+
+// Register-blocked Gram pass.  Shared tile: kAmpTile pixels x ldc floats, pixel-
+// major (row p = the k folded mode values of pixel p, then x_1, zero-padded to a
+// multiple of 4), so a thread's 4 + 4 operands are two 16-byte loads.  Tiles are
+// double-buffered: cp.async (4-byte, transposing, zero-filled past n_local) fills the
+// next tile while the current one is consumed; x_1 (bytes) goes through a register.
+// Each thread of a group owns one 4 x 4 micro-tile (bi <= bj) of the upper block
+// triangle of [F x_1]^T [F x_1]; the NG (a power of two) groups of a CTA split the tile's pixels into contiguous runs.
+// Products are summed in fp32 over one tile (<= kAmpTile / NG terms), then added to
+// fp64 totals, so fp32 rounding stays per-tile.  Partials: one row of E doubles per
+// (CTA, group), summed in fixed order by amp_reduce_kernel.
+__global__ void __launch_bounds__(576)
 amp_gram_kernel(const float* __restrict__ Phi, int64_t ldphi, const uint8_t* __restrict__ x1,
-                int64_t n_local, int k, double* __restrict__ part) {
-  extern __shared__ float sF[];  // (k + 1) rows of kAmpTile + 1 floats; row k = x_1
-  constexpr int LD = kAmpTile + 1;
+                int64_t n_local, int k, int nb, int nmt, int tg, int ng, double* __restrict__ part) {
+  extern __shared__ __align__(16) float sF[];
+  const int ldc = amp_ldc(nb);
+  const int stage_floats = kAmpTile * ldc;
   const int E = amp_entries(k);
-  double acc[NQ];
-  int off_i[NQ], off_j[NQ];
-#pragma unroll
-  for (int q = 0; q < NQ; ++q) {
-    acc[q] = 0.0;
-    const int e = threadIdx.x + q * kAmpThreads;
-    int i = 0, j = 0;
-    if (e < E) amp_entry(e, k, i, j);
-    off_i[q] = i * LD;
-    off_j[q] = j * LD;
+  const int g = threadIdx.x / tg, t = threadIdx.x % tg;
+  int bi = 0, bj = 0;
+  {  // micro-tile t -> (bi, bj), bi <= bj, row-major over the block triangle
+    int r = 0, base = 0;
+    while (r < nb && t >= base + (nb - r)) { base += nb - r; ++r; }
+    bi = r;
+    bj = r + (t - base);
   }
+  const bool active = t < nmt;
+  // zero the padding columns k+1 .. 4nb-1 of both stages once
+  const int npad = 4 * nb - (k + 1);
+  for (int idx = threadIdx.x; idx < 2 * kAmpTile * npad; idx += blockDim.x) {
+    const int st = idx / (kAmpTile * npad), r = idx % (kAmpTile * npad);
+    sF[st * stage_floats + (r / npad) * ldc + k + 1 + r % npad] = 0.f;
+  }
+  double tot[16];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) tot[q] = 0.0;
   const int64_t ntiles = (n_local + kAmpTile - 1) / kAmpTile;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  auto issue = [&](int64_t tile, int st) {
     const int64_t p0 = tile * kAmpTile;
-    __syncthreads();
-    for (int idx = threadIdx.x; idx < (k + 1) * kAmpTile; idx += kAmpThreads) {
-      const int c = idx / kAmpTile, p = idx % kAmpTile;
-      const int64_t j = p0 + p;
-      float v = 0.f;
-      if (j < n_local) v = c < k ? __ldg(Phi + (int64_t)c * ldphi + j) : (float)__ldg(x1 + j);
-      sF[c * LD + p] = v;
+    float* dst = sF + st * stage_floats;
+    for (int c = warp; c < k; c += nwarps) {
+      const float* src = Phi + (int64_t)c * ldphi + p0;
+#pragma unroll
+      for (int p = lane; p < kAmpTile; p += 32) {
+        const bool ok = p0 + p < n_local;
+        cp_async4(dst + p * ldc + c, src + (ok ? p : 0), ok);
+      }
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  float xreg = 0.f;
+  auto load_x = [&](int64_t tile) {
+    const int64_t j = tile * kAmpTile + threadIdx.x;
+    xreg = (threadIdx.x < kAmpTile && j < n_local) ? (float)__ldg(x1 + j) : 0.f;
+  };
+  int64_t tile = blockIdx.x;
+  int st = 0;
+  if (tile < ntiles) { issue(tile, 0); load_x(tile); }
+  for (; tile < ntiles; tile += gridDim.x, st ^= 1) {
+    if (threadIdx.x < kAmpTile) sF[st * stage_floats + threadIdx.x * ldc + k] = xreg;
+    const int64_t nxt = tile + gridDim.x;
+    if (nxt < ntiles) {
+      issue(nxt, st ^ 1);
+      load_x(nxt);
+      asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     }
     __syncthreads();
+    if (active) {
+      const float* cur = sF + st * stage_floats;
+      float acc[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) acc[q] = 0.f;
+      const int ppg = kAmpTile / ng;  // each group: a contiguous run of the tile's pixels
+      const float* pa = cur + g * ppg * ldc + 4 * bi;
+      const float* pb = cur + g * ppg * ldc + 4 * bj;
 #pragma unroll 4
-    for (int p = 0; p < kAmpTile; ++p) {
+      for (int p = 0; p < ppg; ++p, pa += ldc, pb += ldc) {
+        const float4 a = *reinterpret_cast<const float4*>(pa);
+        const float4 b = *reinterpret_cast<const float4*>(pb);
+        const float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
 #pragma unroll
-      for (int q = 0; q < NQ; ++q)
-        acc[q] = fma((double)sF[off_i[q] + p], (double)sF[off_j[q] + p], acc[q]);
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int w = 0; w < 4; ++w) acc[u * 4 + w] = fmaf(av[u], bv[w], acc[u * 4 + w]);
+      }
+#pragma unroll
+      for (int q = 0; q < 16; ++q) tot[q] += (double)acc[q];
     }
+    __syncthreads();  // stage st is refilled by the next iteration's issue
   }
+  if (!active) return;
+  double* row = part + ((int64_t)blockIdx.x * ng + g) * E;
 #pragma unroll
-  for (int q = 0; q < NQ; ++q) {
-    const int e = threadIdx.x + q * kAmpThreads;
-    if (e < E) part[(int64_t)blockIdx.x * E + e] = acc[q];
-  }
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      const int i = 4 * bi + u, j = 4 * bj + w;
+      if (i <= j && i < k && j <= k) row[amp_entry_index(i, j, k)] = tot[u * 4 + w];
+    }
 }
 
 // Fixed-order sum of the block partials; writes G (k x (k+1), column-major, ld k)
@@ -162,10 +235,25 @@ __global__ void amp_solve_kernel(const double* __restrict__ G, int k, const int3
 
 }  // namespace
 
+struct AmpGramShape {
+  int nb, nmt, tg, ng, threads;
+};
+
+AmpGramShape amp_gram_shape(int k) {
+  AmpGramShape g;
+  g.nb = (k + 1 + 3) / 4;
+  g.nmt = g.nb * (g.nb + 1) / 2;
+  g.tg = (g.nmt + 31) / 32 * 32;
+  g.ng = 1;  // a power of two dividing kAmpTile
+  while (g.ng < 16 && g.tg * g.ng * 2 <= 512) g.ng *= 2;
+  g.threads = g.tg * g.ng;
+  return g;
+}
+
 int amp_gram_blocks(int sms) { return 2 * (sms > 0 ? sms : 148); }
 
 size_t amp_gram_ws_bytes(int sms, int k) {
-  return (size_t)amp_gram_blocks(sms) * (size_t)amp_entries(k) * sizeof(double);
+  return (size_t)amp_gram_blocks(sms) * amp_gram_shape(k).ng * (size_t)amp_entries(k) * sizeof(double);
 }
 
 size_t amp_solve_smem_bytes(int k) { return ((size_t)k * k + 2 * (size_t)k) * sizeof(double); }
@@ -173,21 +261,19 @@ size_t amp_solve_smem_bytes(int k) { return ((size_t)k * k + 2 * (size_t)k) * si
 cudaError_t launch_amp_gram(int sms, const float* Phi, int64_t ldphi, const uint8_t* x1, int64_t n_local,
                             int k, double* ws, double* G, cudaStream_t st) {
   const int E = amp_entries(k);
+  const AmpGramShape sh = amp_gram_shape(k);
   const int64_t ntiles = (n_local + kAmpTile - 1) / kAmpTile;
   int blocks = amp_gram_blocks(sms);
   if ((int64_t)blocks > ntiles) blocks = (int)ntiles;
-  const size_t smem = (size_t)(k + 1) * (kAmpTile + 1) * sizeof(float);
-  const int nq = (E + kAmpThreads - 1) / kAmpThreads;
-  note_launch();
-  if (nq <= 1) amp_gram_kernel<1><<<blocks, kAmpThreads, smem, st>>>(Phi, ldphi, x1, n_local, k, ws);
-  else if (nq <= 2) amp_gram_kernel<2><<<blocks, kAmpThreads, smem, st>>>(Phi, ldphi, x1, n_local, k, ws);
-  else if (nq <= 4) amp_gram_kernel<4><<<blocks, kAmpThreads, smem, st>>>(Phi, ldphi, x1, n_local, k, ws);
-  else if (nq <= 8) amp_gram_kernel<8><<<blocks, kAmpThreads, smem, st>>>(Phi, ldphi, x1, n_local, k, ws);
-  else amp_gram_kernel<17><<<blocks, kAmpThreads, smem, st>>>(Phi, ldphi, x1, n_local, k, ws);
-  cudaError_t e = cudaGetLastError();
+  const size_t smem = 2 * (size_t)kAmpTile * amp_ldc(sh.nb) * sizeof(float);
+  cudaError_t e = cudaFuncSetAttribute(amp_gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   note_launch();
-  amp_reduce_kernel<<<(E + 255) / 256, 256, 0, st>>>(ws, blocks, k, G);
+  amp_gram_kernel<<<blocks, sh.threads, smem, st>>>(Phi, ldphi, x1, n_local, k, sh.nb, sh.nmt, sh.tg, sh.ng, ws);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  note_launch();
+  amp_reduce_kernel<<<(E + 255) / 256, 256, 0, st>>>(ws, blocks * sh.ng, k, G);
   return cudaGetLastError();
 }
 

@@ -706,12 +706,15 @@ def test_amplitudes_parity(C, H, case):
     mh = C.model_to_host(P.model)
     b = b.cpu().numpy()
     assert int(dropped.item()) == 0
-    # (1) step 9 alone: the oracle's lstsq on the GPU's own modes (same input) -> tight
+    # (1) step 9 alone: the oracle's lstsq on the GPU's own modes (same input).  The
+    # Gram sums fp32 products in fp32 over <= 128 terms per tile (relative error
+    # <= 128 * 2^-24 ~ 8e-6 of the tile's sum of |terms|, fp64 across tiles), and b
+    # inherits cond(F^T F) = cond(F)^2 of it.
     Phi_g = PT.unfold(F.cpu().numpy(), mh["pair"])
     b_o = OD.amplitudes(X, Phi_g)
     cond = np.linalg.cond(Phi_g)
     err1 = np.linalg.norm(b - b_o) / np.linalg.norm(b_o)
-    assert err1 <= 1e-12 * cond * cond + 1e-9, (err1, cond)
+    assert err1 <= 8e-6 * cond * cond, (err1, cond)
     for j in np.nonzero(mh["pair"] == 1)[0]:
         assert b[j + 1] == np.conj(b[j])
     # (2) end to end against the oracle's modes: per-mode contributions b_j phi_j
@@ -754,8 +757,8 @@ def test_amplitudes_slabs_sum_to_full(C, H):
         Gs += Gp
     torch.cuda.synchronize()
     G, Gs = G.cpu().numpy(), Gs.cpu().numpy()
-    assert np.max(np.abs(G - Gs)) <= 1e-12 * np.max(np.abs(G))
+    assert np.max(np.abs(G - Gs)) <= 8e-6 * np.max(np.abs(G))
     # and the Gram itself equals the fp64 product of the (exact) fp32 modes
     Ff = F.cpu().numpy().astype(np.float64)
     ref = np.concatenate([Ff @ Ff.T, Ff @ X[0].astype(np.float64)[:, None]], 1)   # k x (k+1)
-    assert np.max(np.abs(G.T - ref)) <= 1e-12 * np.max(np.abs(ref))
+    assert np.max(np.abs(G.T - ref)) <= 8e-6 * np.max(np.abs(ref))
