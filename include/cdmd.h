@@ -236,7 +236,7 @@ CDMD_API cdmd_status cdmd_foreground(cdmd_handle h, const cdmd_video* v, const c
  *   2 k_eff doubles (re, im) in the mode order of the model; conjugate pairs get
  *   conjugate amplitudes.  A column of F dependent on earlier ones (pivot^2 <=
  *   1e-12 (F^T F)_jj) gets c_j = 0 (a least-squares solution, not lstsq's minimum-
- *   norm one; reading R24); dropped (device int32, may be NULL) receives
+ *   norm one; reading R23); dropped (device int32, may be NULL) receives
  *   how many.  Errors: CDMD_ERR_ARG on null pointers, ldphi < n_local or a model
  *   cdmd_fit has not filled; CDMD_ERR_RANGE if k_eff > 128; CDMD_ERR_WORKSPACE. */
 CDMD_API size_t cdmd_amplitudes_workspace_bytes(cdmd_handle h, int k);

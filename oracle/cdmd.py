@@ -9,7 +9,8 @@ Steps, in the paper's order and notation:
                (rank="gd") chosen by the Gavish-Donoho optimal hard threshold
                (Remark 2; evaluation settings P:573) via optimal_rank()
   modes()      Alg. 1 step 8, Eq. cDMDModes  Phi = X' V S^-1 W
-  amplitudes() Alg. 1 step 9, b = lstsq(Phi, x_1) on the full-state modes
+  amplitudes() Alg. 1 step 9, b = lstsq(Phi, x_1) on the full-state modes,
+               pinned in tests/test_oracle_amplitudes.py
   background() Eq. DMDTerms (P:185-193): L = Re sum_{p in S} b_p phi_p lambda_p^{t-1}
                (dynamic) or x_BG = Re Phi beta (static)
   mask()       Eq. thres: 1 iff |x_jt - xhat_j| > tau

@@ -167,7 +167,7 @@ __global__ void amp_reduce_kernel(const double* __restrict__ part, int nblocks, 
 // L^T c = y, then unfold c to the complex amplitudes.  A pivot d^2 <= kAmpPivotRtol *
 // (F^T F)_jj (column j dependent on the earlier ones to ~1e-6 in norm, below the fp32
 // resolution of Phi) drops column j: c_j = 0, still a least-squares solution
-// (reading R24).
+// (reading R23).
 constexpr double kAmpPivotRtol = 1e-12;
 
 __global__ void amp_solve_kernel(const double* __restrict__ G, int k, const int32_t* __restrict__ pair,
