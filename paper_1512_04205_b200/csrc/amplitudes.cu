@@ -55,7 +55,8 @@ __device__ inline void cp_async4(float* dst, const float* src, bool valid) {
 // Products are summed in fp32 over one tile (<= kAmpTile / NG terms), then added to
 // fp64 totals, so fp32 rounding stays per-tile.  Partials: one row of E doubles per
 // (CTA, group), summed in fixed order by amp_reduce_kernel.
-__global__ void __launch_bounds__(576)
+template <int MAXT, int MINB>
+__global__ void __launch_bounds__(MAXT, MINB)
 amp_gram_kernel(const float* __restrict__ Phi, int64_t ldphi, const uint8_t* __restrict__ x1,
                 int64_t n_local, int k, int nb, int nmt, int tg, int ng, double* __restrict__ part) {
   extern __shared__ __align__(16) float sF[];
@@ -266,10 +267,13 @@ cudaError_t launch_amp_gram(int sms, const float* Phi, int64_t ldphi, const uint
   int blocks = amp_gram_blocks(sms);
   if ((int64_t)blocks > ntiles) blocks = (int)ntiles;
   const size_t smem = 2 * (size_t)kAmpTile * amp_ldc(sh.nb) * sizeof(float);
-  cudaError_t e = cudaFuncSetAttribute(amp_gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  // <= 384 threads (k <= 62): two resident CTAs per SM (registers capped at 85) hide more latency
+  const bool two = sh.threads <= 384;
+  auto kern = two ? amp_gram_kernel<384, 2> : amp_gram_kernel<576, 1>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   note_launch();
-  amp_gram_kernel<<<blocks, sh.threads, smem, st>>>(Phi, ldphi, x1, n_local, k, sh.nb, sh.nmt, sh.tg, sh.ng, ws);
+  kern<<<blocks, sh.threads, smem, st>>>(Phi, ldphi, x1, n_local, k, sh.nb, sh.nmt, sh.tg, sh.ng, ws);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   note_launch();
