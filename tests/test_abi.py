@@ -84,6 +84,11 @@ def test_host_side_validation_and_sizes(libpath):
     assert lib.cdmd_sketch_workspace_bytes(ctypes.byref(v), ctypes.byref(bad)) == 0   # p > n
     # null handle -> invalid argument, no launch
     assert lib.cdmd_sketch(None, ctypes.byref(v), ctypes.byref(c), None, 2000, None, 0, None) == 1
+    # amplitudes (Alg. 1 step 9): host-side validation only, nothing launched
+    assert lib.cdmd_amplitudes_workspace_bytes(None, 50) == 0
+    assert lib.cdmd_amplitudes_gram(None, ctypes.byref(v), ctypes.byref(M), None, 2073600, None, None, 0,
+                                    None) == 1
+    assert lib.cdmd_amplitudes_solve(None, ctypes.byref(M), None, None, None, None) == 1
 
 
 def test_struct_layouts_match_c():

@@ -749,6 +749,8 @@ def test_amplitudes_slabs_sum_to_full(C, H):
     ws = torch.empty(C.cdmd_amplitudes_workspace_bytes(H, ke), dtype=torch.uint8, device="cuda")
     G = torch.empty((ke + 1, ke), dtype=torch.float64, device="cuda")
     C.cdmd_amplitudes_gram(H, C.video(Xd, n, 0, n), P.model, P.Phi, G, ws)
+    with pytest.raises(C.CdmdError):   # CDMD_ERR_WORKSPACE, reported before any launch
+        C.cdmd_amplitudes_gram(H, C.video(Xd, n, 0, n), P.model, P.Phi, G, ws[:256])
     n1 = 128 * 97
     Gs = torch.zeros_like(G)
     for pix0, nl in ((0, n1), (n1, n - n1)):
