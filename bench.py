@@ -354,6 +354,47 @@ def main():
             "launch_ms": round(stage_ms[dom], 4),
             "stage_roofline": {s: round(stage_roof(s)[0] / stage_roof(s)[1], 4) for s in algo}}
 
+    # Alg. 1 step 9 full-state amplitudes b = lstsq(Phi, x_1): measured on the
+    # modes of the last step, after (and outside) the timed region -- the step's
+    # background amplitudes are Remark 3's OMP ones, so this is a reported extra.
+    # Phi (n_local x k_eff fp32) is larger than L2 at the bench sizes.
+    amplitudes = None
+    if ke <= 128:
+        va = C.video(Xd, n, pix0, nl)
+        ws_a = torch.empty(max(C.cdmd_amplitudes_workspace_bytes(P.h, ke), 256), dtype=torch.uint8, device="cuda")
+        Ga = torch.empty((ke + 1, ke), dtype=torch.float64, device="cuda")
+        ba = torch.empty((ke, 2), dtype=torch.float64, device="cuda")
+
+        def amp_once(marks=None):
+            if marks:
+                marks[0].record(stream)
+            C.cdmd_amplitudes_gram(P.h, va, P.model, P.Phi, Ga, ws_a, stream)
+            if marks:
+                marks[1].record(stream)
+            if world > 1:
+                dist.all_reduce(Ga, op=dist.ReduceOp.SUM)
+            if marks:
+                marks[2].record(stream)
+            C.cdmd_amplitudes_solve(P.h, P.model, Ga, ba, None, stream)
+            if marks:
+                marks[3].record(stream)
+
+        for _ in range(3):
+            amp_once()
+        torch.cuda.synchronize()
+        reps, tg_, ts_ = 10, 0.0, 0.0
+        for _ in range(reps):
+            mk = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+            amp_once(mk)
+            torch.cuda.synchronize()
+            tg_ += mk[0].elapsed_time(mk[1]) / reps
+            ts_ += mk[2].elapsed_time(mk[3]) / reps
+        abytes = 4 * nl * ke + nl
+        amplitudes = {"step": "Alg. 1 step 9, b = lstsq(Phi, x_1), not in the timed step",
+                      "gram_kernel": "amp_gram_kernel", "gram_ms": round(tg_, 4), "solve_ms": round(ts_, 4),
+                      "algorithmic_bytes_per_launch": abytes,
+                      "gram_frac_hbm": round(abytes / (tg_ * 1e-3) / 1e9 / hbm, 4)}
+
     # e2e: host (pinned) video in, mask out, through the same public calls -- through the
     # streaming lanes when they are in use (each batch's H2D copy and mask read-back run
     # on its lane's stream and overlap other batches' work), else one batch at a time
@@ -425,6 +466,7 @@ def main():
             "latency_ms_per_batch": round(latency_ms, 4),
             "streaming": streaming,
             "roofline": roof,
+            "amplitudes": amplitudes,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,   # libcdmd kernels launched in the timed region (cdmd_kernel_launches)
