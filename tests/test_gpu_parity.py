@@ -764,3 +764,26 @@ def test_amplitudes_slabs_sum_to_full(C, H):
     Ff = F.cpu().numpy().astype(np.float64)
     ref = np.concatenate([Ff @ Ff.T, Ff @ X[0].astype(np.float64)[:, None]], 1)   # k x (k+1)
     assert np.max(np.abs(G.T - ref)) <= 8e-6 * np.max(np.abs(ref))
+
+
+def test_amplitudes_c4_full_size(C, H):
+    """Step 9 at the bench configuration (1080p x 500, k = 50), in the launch
+    configuration bench.py times: device b vs the oracle's lstsq on the same modes."""
+    cfg = config_by_name("c4_1080p_sparse")
+    X = video_for(cfg)
+    m, n = X.shape
+    Xd = to_dev(X)
+    P = C.Pipeline(H, n, n, m, "sparse", cfg.p, cfg.k, cfg.K)
+    P.sketch(Xd)
+    P.fit()
+    F = P.modes(Xd)
+    b, dropped = P.amplitudes(Xd)
+    torch.cuda.synchronize()
+    assert int(dropped.item()) == 0
+    pair = C.model_to_host(P.model)["pair"]
+    Phi_g = PT.unfold(F.cpu().numpy(), pair)
+    del F
+    b_o = OD.amplitudes(X, Phi_g)
+    cond = np.linalg.cond(Phi_g)
+    err = np.linalg.norm(b.cpu().numpy() - b_o) / np.linalg.norm(b_o)
+    assert err <= 8e-6 * cond * cond, (err, cond)
