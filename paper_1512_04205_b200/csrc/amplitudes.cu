@@ -246,12 +246,12 @@ AmpGramShape amp_gram_shape(int k) {
   g.nmt = g.nb * (g.nb + 1) / 2;
   g.tg = (g.nmt + 31) / 32 * 32;
   g.ng = 1;  // a power of two dividing kAmpTile
-  while (g.ng < 16 && g.tg * g.ng * 2 <= 512) g.ng *= 2;
+  while (g.ng < 16 && g.tg * g.ng * 2 <= 256) g.ng *= 2;
   g.threads = g.tg * g.ng;
   return g;
 }
 
-int amp_gram_blocks(int sms) { return 2 * (sms > 0 ? sms : 148); }
+int amp_gram_blocks(int sms) { return 3 * (sms > 0 ? sms : 148); }
 
 size_t amp_gram_ws_bytes(int sms, int k) {
   return (size_t)amp_gram_blocks(sms) * amp_gram_shape(k).ng * (size_t)amp_entries(k) * sizeof(double);
@@ -267,9 +267,10 @@ cudaError_t launch_amp_gram(int sms, const float* Phi, int64_t ldphi, const uint
   int blocks = amp_gram_blocks(sms);
   if ((int64_t)blocks > ntiles) blocks = (int)ntiles;
   const size_t smem = 2 * (size_t)kAmpTile * amp_ldc(sh.nb) * sizeof(float);
-  // <= 384 threads (k <= 62): two resident CTAs per SM (registers capped at 85) hide more latency
-  const bool two = sh.threads <= 384;
-  auto kern = two ? amp_gram_kernel<384, 2> : amp_gram_kernel<576, 1>;
+  // <= 192 threads (k <= 62): three resident CTAs per SM (measured: 2 x 384 threads 0.41 ms,
+  // 3 x 192 0.38 ms, 4 x 192 on 64-pixel tiles 0.39 ms at c4)
+  const bool two = sh.threads <= 192;
+  auto kern = two ? amp_gram_kernel<192, 3> : amp_gram_kernel<576, 1>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   note_launch();
