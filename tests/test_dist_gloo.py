@@ -141,3 +141,54 @@ def test_ordered_collectives_sharded_fits_two_ranks():
         for b, (y, model) in res.items():
             assert y == [3.0 * (b + 1)] * 7
             assert model == [1000.0 * b + (b % 2)] * 5
+
+
+def _amp_worker(rank, world, port, out):
+    # Alg. 1 step 9 sharded by pixel rows: each rank forms its slab's normal
+    # equations [Phi_s^H Phi_s | Phi_s^H x_1,s], one all-reduce sums them, every rank
+    # solves (the protocol of cdmd_amplitudes_gram -> all-reduce -> cdmd_amplitudes_solve)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import cdmd as D
+        from oracle import sensing as S
+        from synth.scene import make_video
+        W, H, m, p, k = 48, 40, 12, 30, 6
+        n = W * H
+        pix0, nl = slab(n, world, rank)
+        Xs = make_video(W, H, m, seed=3, noise=2.0, n_rects=1, pix0=pix0, n_local=nl)
+        Y = torch.from_numpy(np.ascontiguousarray(S.sketch(Xs, 1, p, seed=7, n_total=n, pix0=pix0)))
+        allreduce_sum(Y)
+        model = D.fit(Y.numpy(), k, 2)
+        Phi_s = D.modes(Xs, model["M"])                               # nl x k complex
+        G = np.concatenate([Phi_s.conj().T @ Phi_s, Phi_s.conj().T @ Xs[0].astype(np.float64)[:, None]], 1)
+        t = torch.view_as_real(torch.from_numpy(np.ascontiguousarray(G))).contiguous()
+        allreduce_sum(t)
+        Gs = torch.view_as_complex(t).numpy()
+        b = np.linalg.solve(Gs[:, :-1], Gs[:, -1])
+        out.put((rank, b))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_amplitudes_equal_single_rank_lstsq():
+    from oracle import cdmd as D
+    from oracle import sensing as S
+    from synth.scene import make_video
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_amp_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p_ in ps:
+        p_.start()
+    got = dict(q.get(timeout=120) for _ in range(2))
+    for p_ in ps:
+        p_.join(timeout=60)
+        assert p_.exitcode == 0
+    X = make_video(48, 40, 12, seed=3, noise=2.0, n_rects=1)
+    model = D.fit(S.sketch(X, 1, 30, seed=7), 6, 2)
+    want = D.amplitudes(X, D.modes(X, model["M"]))
+    for r in (0, 1):
+        assert np.max(np.abs(got[r] - want)) <= 1e-8 * np.max(np.abs(want))
+    assert np.array_equal(got[0], got[1])    # every rank solves the same summed system
