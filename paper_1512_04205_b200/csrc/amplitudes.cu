@@ -86,12 +86,22 @@ amp_gram_kernel(const float* __restrict__ Phi, int64_t ldphi, const uint8_t* __r
   auto issue = [&](int64_t tile, int st) {
     const int64_t p0 = tile * kAmpTile;
     float* dst = sF + st * stage_floats;
-    for (int c = warp; c < k; c += nwarps) {
-      const float* src = Phi + (int64_t)c * ldphi + p0;
+    if (p0 + kAmpTile <= n_local) {  // full tile: no bounds tests, pointer strides only
+      const float* src = Phi + (int64_t)warp * ldphi + p0 + lane;
+      float* d = dst + lane * ldc + warp;
+      const int64_t sstep = (int64_t)nwarps * ldphi;
+      for (int c = warp; c < k; c += nwarps, src += sstep, d += nwarps) {
 #pragma unroll
-      for (int p = lane; p < kAmpTile; p += 32) {
-        const bool ok = p0 + p < n_local;
-        cp_async4(dst + p * ldc + c, src + (ok ? p : 0), ok);
+        for (int j = 0; j < kAmpTile / 32; ++j) cp_async4(d + j * 32 * ldc, src + j * 32, true);
+      }
+    } else {
+      for (int c = warp; c < k; c += nwarps) {
+        const float* src = Phi + (int64_t)c * ldphi + p0;
+#pragma unroll
+        for (int p = lane; p < kAmpTile; p += 32) {
+          const bool ok = p0 + p < n_local;
+          cp_async4(dst + p * ldc + c, src + (ok ? p : 0), ok);
+        }
       }
     }
     asm volatile("cp.async.commit_group;\n" ::: "memory");
