@@ -787,3 +787,23 @@ def test_amplitudes_c4_full_size(C, H):
     cond = np.linalg.cond(Phi_g)
     err = np.linalg.norm(b.cpu().numpy() - b_o) / np.linalg.norm(b_o)
     assert err <= 8e-6 * cond * cond, (err, cond)
+
+
+def test_amplitudes_static_video_single_mode(C, H):
+    """Degenerate case: a constant video has one mode (lambda = 1, k_eff = 1) and
+    b phi reproduces the frame exactly (up to fp32 Phi)."""
+    rng = np.random.default_rng(2)
+    n, m = 128 * 5 + 37, 20
+    frame = rng.integers(0, 256, size=n, dtype=np.uint8)
+    X = np.tile(frame, (m, 1))
+    Xd = to_dev(X)
+    P = C.Pipeline(H, n, n, m, "sparse", 30, 5, 3, s=5.0)
+    P.sketch(Xd)
+    P.fit()
+    assert P.model.k_eff == 1
+    F = P.modes(Xd)
+    b, dropped = P.amplitudes(Xd)
+    torch.cuda.synchronize()
+    assert int(dropped.item()) == 0
+    rec = (F.cpu().numpy().astype(np.float64)[0] * b.cpu().numpy()[0]).real
+    assert np.max(np.abs(rec - frame)) <= 1e-4 * 255
