@@ -8,10 +8,17 @@ workload (N=1): c4_1080p_sparse = 1920x1080, m = 500 frames, sparse C (s = n/ln 
          p = 2000, k = 50, K = 10, tau = 25, dynamic background (north_star (3)).
 value  : frames / device time per step (max over ranks), inputs resident in HBM;
          X (1.04 GB) is larger than L2, so no flush is needed between steps.
-         Streaming (default, --lanes 24): K batches flow through 24 lanes (own handle,
-         CUDA stream, buffers and copy of X), so one batch's latency-bound small solve
+         Streaming (default): K batches flow through `lanes` lanes (own handle, CUDA
+         stream, buffers and copy of X), so one batch's latency-bound small solve
          overlaps other batches' HBM passes -- the paper's batch decomposition of a long
-         video.  `latency_ms_per_batch` reports one batch at a time (--lanes 1).
+         video.  lanes <= K/2, so every lane runs >= 2 batches (steady state).
+Also reported:
+  latency_ms_per_batch  one batch at a time, eager, with per-stage CUDA events;
+  per_batch             one batch at a time with the passes replayed from CUDA graphs
+                        (sketch | fit | modes+foreground), median of >= 10 runs;
+  passes_only           sketch + modes + foreground in one CUDA graph (the replicated
+                        small solve excluded), median of >= 10 runs, with its HBM fraction;
+  e2e_fused             the same with the fused single pass (N11: cdmd_foreground(Phi=NULL)).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config NAME] [--bg dynamic|static]
     python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N
@@ -29,10 +36,10 @@ import time
 
 import numpy as np
 
-# Streaming runs 2 streams per lane (24 lanes by default).  With the default 8 hardware
-# work queues, streams share queues and a lane's queued solve kernel blocks unrelated
-# streams behind it (measured: 16 concurrent solves 0.79 -> 0.51 ms/batch with 32).
-# Must be set before the CUDA context exists.
+# Streaming runs 2 streams per lane.  With the default 8 hardware work queues, streams
+# share queues and a lane's queued solve kernel blocks unrelated streams behind it
+# (measured: 16 concurrent solves 0.79 -> 0.51 ms/batch with 32).  Must be set before
+# the CUDA context exists.
 os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
@@ -41,6 +48,7 @@ sys.path.insert(0, ROOT)
 FALLBACK_HBM_GBS = 6650.0   # B200_PROFILING.md fallback, used only without MEASURED_PEAKS.json
 FALLBACK_BF16_TFLOPS = 1590.0
 METRIC = "1080p frames/sec (sketch+modes+fg mask) at 1/2/4/8 B200; % of HBM roofline"
+KINDS = {"spixel": 0, "sparse": 1, "rademacher": 2, "gaussian": 3}
 
 
 def peaks():
@@ -50,6 +58,28 @@ def peaks():
         d = json.load(open(p))
         return float(d["hbm_gbs"]), float(d["bf16_tflops"]), "measured"
     return FALLBACK_HBM_GBS, FALLBACK_BF16_TFLOPS, "fallback"
+
+
+def int8_peak_tops(torch):
+    """Dense int8 tensor-core peak measured here: torch._int_mm (cuBLASLt int8 GEMM,
+    tcgen05 kind::i8 on sm_100a) 8192^3, 2 N^3 ops, best of 10 (burst)."""
+    try:
+        a = torch.randint(-128, 127, (8192, 8192), dtype=torch.int8, device="cuda")
+        b = torch.randint(-128, 127, (8192, 8192), dtype=torch.int8, device="cuda").t()
+        for _ in range(3):
+            torch._int_mm(a, b)
+        best = 1e30
+        for _ in range(10):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            torch._int_mm(a, b)
+            e1.record()
+            torch.cuda.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        del a, b
+        return 2 * 8192 ** 3 / (best * 1e-3) / 1e12
+    except Exception:
+        return None
 
 
 class ClockSampler:
@@ -105,81 +135,127 @@ def sector_bytes_sparse(n_local, pix0, n_total, p, seed, m):
     return int(np.unique(pos // 32).size) * 32 * m + 4 * p * m
 
 
+# ------------------------------------------------------------- the oracle as a baseline
+class OracleStep:
+    """One step of the oracle (test infrastructure) on the whole workload, on this
+    host's cores: the sketch and the fit in this process, then modes + background +
+    mask of EVERY pixel, the oracle's own per-pixel functions fanned over pixel slabs in
+    worker processes (oracle/runner.py; no arithmetic of its own).  Dense sensings
+    (Rademacher / Gaussian) sketch in the workers as well (slabs sum to Y)."""
+
+    def __init__(self, cfg, bg):
+        from oracle.runner import PixelPool
+        from synth.scene import video_for
+        self.cfg, self.dynamic = cfg, bg == "dynamic"
+        self.kind = KINDS[cfg.kind]
+        self.X = video_for(cfg) if self.kind in (0, 1) else None
+        self.pool = PixelPool(cfg)
+        self.cores = len(os.sched_getaffinity(0))
+
+    def step(self):
+        from oracle import cdmd as OD
+        from oracle import sensing as OS
+        from oracle.runner import parallel_sketch
+        cfg = self.cfg
+        t0 = time.perf_counter()
+        if self.X is not None:
+            Y = OS.sketch(self.X, self.kind, cfg.p, cfg.sensing_seed)
+        else:
+            Y = parallel_sketch(cfg, self.kind)
+        t1 = time.perf_counter()
+        model = OD.fit(Y, cfg.k, cfg.K)
+        t2 = time.perf_counter()
+        self.pool.run(model, cfg.tau, dynamic=self.dynamic)
+        t3 = time.perf_counter()
+        return t3 - t0, {"sketch_s": round(t1 - t0, 3), "fit_s": round(t2 - t1, 3), "pixels_s": round(t3 - t2, 3)}
+
+    def close(self):
+        self.pool.close()
+
+
 def run_reference(args):
-    """The oracle (test infrastructure) timed as it stands on this host's cores, on a
-    bounded sample of the same workload: the full sketch + fit, then modes + dynamic
-    background + mask on 1/`frac` of the pixels, extrapolated to the whole frame."""
+    """--impl reference: the oracle as it stands, timed over --warmup + --steps full
+    steps of the same workload on this host's cores (rank 0 only)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    from oracle import cdmd as OD
-    from oracle import sensing as OS
-    from synth.scene import config_by_name, video_for
+    from synth.scene import config_by_name
     cfg = config_by_name(args.config)
-    X = video_for(cfg)
-    m, n = X.shape
-    kind = {"spixel": 0, "sparse": 1, "rademacher": 2, "gaussian": 3}[cfg.kind]
-    frac = args.ref_frac
-    rng = np.random.default_rng(0)
-    pix = np.sort(rng.choice(n, n // frac, replace=False))
-    times = []
-    for _ in range(max(1, args.steps if args.steps <= 3 else 1)):
-        t0 = time.perf_counter()
-        if kind in (0, 1):
-            Y = OS.sketch(X, kind, cfg.p, cfg.sensing_seed)
-            t_sk = time.perf_counter() - t0
-        else:  # dense sketches: a sample of rows, extrapolated
-            rows = np.arange(0, cfg.p, max(1, cfg.p // 16))
-            OS.sketch(X, kind, cfg.p, cfg.sensing_seed, rows=rows)
-            t_sk = (time.perf_counter() - t0) * cfg.p / len(rows)
-            Y = None
-        t1 = time.perf_counter()
-        if Y is None:
-            raise SystemExit("reference arm: dense-C configs need the full oracle sketch (not sampled here)")
-        model = OD.fit(Y, cfg.k, cfg.K)
-        t_fit = time.perf_counter() - t1
-        t2 = time.perf_counter()
-        Xs = X[:, pix]
-        Phi = OD.modes(Xs, model["M"])
-        L = OD.background_dynamic(Phi, model) if args.bg == "dynamic" else OD.background_static(Phi, model)
-        OD.mask(Xs, L, cfg.tau)
-        t_px = (time.perf_counter() - t2) * frac
-        times.append(t_sk + t_fit + t_px)
-    t = min(times)
-    cores = len(os.sched_getaffinity(0))
-    val = m / t
+    o = OracleStep(cfg, args.bg)
+    try:
+        for _ in range(args.warmup):
+            o.step()
+        times, parts = [], None
+        for _ in range(args.steps):
+            t, parts = o.step()
+            times.append(t)
+    finally:
+        o.close()
+    t = sum(times) / len(times)
+    val = cfg.m / t
     line = {
-        "impl": "reference", "metric": METRIC, "value": val, "unit": "frames/s", "n_gpus": args.gpus,
-        "steps": len(times), "warmup": 0, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "impl": "reference", "metric": METRIC, "value": round(val, 3), "unit": "frames/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t * 1e3, 1), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": cfg.name, "video": f"{cfg.width}x{cfg.height}x{cfg.m}", "sensing": cfg.kind,
                    "p": cfg.p, "k": cfg.k, "K": cfg.K, "tau": cfg.tau, "background": args.bg},
-        "cpu_baseline": {"value": val, "unit": "frames/s", "cores": cores, "kind": "oracle",
-                         "sample": f"full sketch+fit; modes+background+mask on 1/{frac} of the pixels "
-                                   f"({len(pix)} px), extrapolated x{frac}"},
-        "e2e": {"value": val, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "cpu_baseline": {"value": round(val, 3), "unit": "frames/s", "cores": o.cores, "kind": "oracle",
+                         "sample": f"the whole workload every step (no extrapolation): sketch + fit in one "
+                                   f"process, modes+background+mask of all {cfg.n} px over {o.pool.cores} "
+                                   f"worker processes; last step {parts}"},
+        "e2e": {"value": round(val, 3), "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(cfg, args):
+    """The oracle as it stands, one full step of the workload (about 10-30 s of CPU work
+    on the box's cores), after one untimed step."""
+    o = OracleStep(cfg, args.bg)
+    try:
+        o.step()
+        t, parts = o.step()
+    finally:
+        o.close()
+    return {"value": round(cfg.m / t, 3), "unit": "frames/s", "cores": o.cores, "kind": "oracle",
+            "sample": f"{cfg.name}: one whole step, no extrapolation ({parts}; pixels over "
+                      f"{o.pool.cores} worker processes)"}
+
+
+# --------------------------------------------------------------------------- helpers
+def median_ms(torch, fn, reps, stream):
+    """Median over `reps` runs of fn() timed with CUDA events on `stream`."""
+    ts = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        fn()
+        b.record(stream)
+        b.synchronize()
+        ts.append(a.elapsed_time(b))
+    return statistics.median(ts), ts
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="cdmd", choices=["cdmd", "reference"])
     ap.add_argument("--config", default="c4_1080p_sparse")
     ap.add_argument("--bg", default="dynamic", choices=["dynamic", "static"])
     ap.add_argument("--rank", default="fixed", choices=["fixed", "gd"],
                     help="target rank: the config's k, or Gavish-Donoho (Remark 2, P:361) with k as the cap")
-    ap.add_argument("--ref-frac", type=int, default=32)
+    ap.add_argument("--partition", default="pixel", choices=["pixel", "batch"],
+                    help="N > 1: pixel-row slabs + all-reduce of Y (north_star), or batch-parallel "
+                         "replicas (P:573; whole frames per rank, no collective)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--lanes", type=int, default=24,
-                    help="batches in flight (streaming, P:573); 1 = one batch at a time")
-    ap.add_argument("--replicated-fits", action="store_true",
-                    help="N > 1 streaming: every rank solves every batch (north_star's redundant solve) "
-                         "instead of rank b mod N solving batch b and broadcasting the model")
+    ap.add_argument("--lanes", type=int, default=16,
+                    help="batches in flight (streaming, P:573), capped at steps/2; 1 = one batch at a time")
+    ap.add_argument("--fused", action="store_true",
+                    help="streaming value through the fused single pass (N11) instead of modes + foreground")
+    ap.add_argument("--graph-reps", type=int, default=20)
     ap.add_argument("--fit-sms", type=int, default=0,
                     help="streaming: SMs reserved for the small solves (green-context partition; 0 = shared)")
     args = ap.parse_args()
@@ -209,7 +285,8 @@ def main():
             dist.init_process_group(backend)
     cfg = config_by_name(args.config)
     n, m = cfg.n, cfg.m
-    pix0, nl = slab(n, world, rank)
+    pixel = world > 1 and args.partition == "pixel"
+    pix0, nl = slab(n, world, rank) if pixel else (0, n)
     X_host = video_for(cfg, pix0=pix0, n_local=nl)
     ld = ((nl + 15) // 16) * 16
     Xd = torch.zeros((m, ld), dtype=torch.uint8, device="cuda")
@@ -218,6 +295,7 @@ def main():
     P = C.Pipeline(H, n, nl, m, cfg.kind, cfg.p, cfg.k, cfg.K, seed=cfg.sensing_seed, pix0=pix0, rank=args.rank)
     mode = C.BG_DYNAMIC if args.bg == "dynamic" else C.BG_STATIC
     stream = torch.cuda.current_stream()
+    allreduce = (lambda Y: dist.all_reduce(Y, op=dist.ReduceOp.SUM)) if pixel else None
     ev = {s: [] for s in ("sketch", "allreduce", "fit", "modes", "foreground")}
 
     def step(record=False):
@@ -227,8 +305,8 @@ def main():
         P.sketch(Xd)
         if record:
             marks[1].record(stream)
-        if world > 1:
-            dist.all_reduce(P.Y, op=dist.ReduceOp.SUM)
+        if allreduce is not None:
+            allreduce(P.Y)
         if record:
             marks[2].record(stream)
         P.fit()
@@ -243,6 +321,7 @@ def main():
             for i, s in enumerate(ev):
                 ev[s].append((marks[i], marks[i + 1]))
 
+    # ---- 1. one batch at a time, eager, per-stage events
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -262,35 +341,111 @@ def main():
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    ms = start.elapsed_time(stop) / args.steps
-    stage_ms = {s: sum(a.elapsed_time(b) for a, b in v) / len(v) for s, v in ev.items()}
-    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
-    value = m / (ms_max * 1e-3)
-    latency_ms = ms_max
 
+    def max_over_ranks(x):
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    latency_ms = max_over_ranks(start.elapsed_time(stop) / args.steps)
+    stage_ms = {s: sum(a.elapsed_time(b) for a, b in v) / len(v) for s, v in ev.items()}
+    ms_max, value, launches_seq = latency_ms, m / (latency_ms * 1e-3), launches
+    hbm, bf16, peak_src = peaks()
+    step_bytes = nl * m + nl * m // 8          # X read once + the bit mask (north_star)
+
+    # ---- 2. CUDA graphs: passes captured, the fit eager between replays
+    graphs = {}
+    s_cap = torch.cuda.Stream()
+    s_cap.wait_stream(stream)
+
+    def capture(fn):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(s_cap):
+            fn()                                   # warm (outside the capture)
+            torch.cuda.synchronize()
+            with torch.cuda.graph(g, stream=s_cap):
+                fn()
+        torch.cuda.synchronize()
+        return g
+
+    try:
+        graphs["sketch"] = capture(lambda: P.sketch(Xd))
+        graphs["passes_mf"] = capture(lambda: (P.modes(Xd), P.foreground(Xd, cfg.tau, mode)))
+        graphs["passes_all"] = capture(lambda: (P.sketch(Xd), P.modes(Xd), P.foreground(Xd, cfg.tau, mode)))
+    except Exception as e:   # report, do not hide: the eager numbers above still stand
+        graphs = {"error": repr(e)}
+    fused_ok = True
+    try:
+        P.foreground(Xd, cfg.tau, mode, fused=True)
+        torch.cuda.synchronize()
+        if "error" not in graphs:
+            graphs["passes_fused"] = capture(lambda: (P.sketch(Xd), P.foreground(Xd, cfg.tau, mode, fused=True)))
+            graphs["fg_fused"] = capture(lambda: P.foreground(Xd, cfg.tau, mode, fused=True))
+    except Exception as e:
+        fused_ok = repr(e)
+    reps = max(10, args.graph_reps)
+    per_batch = passes_only = e2e_fused = None
+    if "error" not in graphs:
+        def one_batch():
+            graphs["sketch"].replay()
+            if allreduce is not None:
+                with torch.cuda.stream(s_cap):
+                    allreduce(P.Y)
+            with torch.cuda.stream(s_cap):
+                P.fit()
+            graphs["passes_mf"].replay()
+
+        with torch.cuda.stream(s_cap):
+            for _ in range(3):
+                one_batch()
+            med, _ = median_ms(torch, one_batch, reps, s_cap)
+            med = max_over_ranks(med)
+            per_batch = {"ms_median": round(med, 4), "frames_per_s": round(m / (med * 1e-3), 1), "runs": reps,
+                         "mode": "sketch graph | fit (eager: it reads the model sizes back once) | "
+                                 "modes+foreground graph"}
+            for _ in range(3):
+                graphs["passes_all"].replay()
+            med, _ = median_ms(torch, graphs["passes_all"].replay, reps, s_cap)
+            med = max_over_ranks(med)
+            passes_only = {"ms_median": round(med, 4), "frames_per_s": round(m / (med * 1e-3), 1), "runs": reps,
+                           "step_hbm_frac": round(step_bytes / (med * 1e-3) / 1e9 / hbm, 4),
+                           "graph": "sketch + modes + foreground (fit excluded: the replicated small solve)"}
+            if "passes_fused" in graphs:
+                for _ in range(3):
+                    graphs["passes_fused"].replay()
+                med, _ = median_ms(torch, graphs["passes_fused"].replay, reps, s_cap)
+                med = max_over_ranks(med)
+                fmed, _ = median_ms(torch, graphs["fg_fused"].replay, reps, s_cap)
+                fmed = max_over_ranks(fmed)
+                fg_bytes = nl * m + 4 * m * ((nl + 31) // 32)
+                e2e_fused = {"passes_ms_median": round(med, 4), "passes_frames_per_s": round(m / (med * 1e-3), 1),
+                             "step_hbm_frac": round(step_bytes / (med * 1e-3) / 1e9 / hbm, 4),
+                             "fused_kernel_ms": round(fmed, 4),
+                             "fused_kernel_hbm_frac": round(fg_bytes / (fmed * 1e-3) / 1e9 / hbm, 4),
+                             "graph": "sketch + fused foreground (N11: the support's modes in-slab, no Phi "
+                                      "written; fit excluded)"}
+        torch.cuda.synchronize()
+
+    # ---- 3. streaming (the value): lanes reused, steady state
     streaming = None
-    if args.lanes > 1:
-        # K batches through `lanes` concurrent lanes; each lane reads its own copy of X
-        S = C.Streaming(local, n, nl, m, cfg.kind, cfg.p, cfg.k, cfg.K, lanes=args.lanes,
-                        seed=cfg.sensing_seed, pix0=pix0, rank=args.rank, fit_sms=args.fit_sms,
-                        shard_fit=not args.replicated_fits)
-        Xs = [Xd] + [Xd.clone() for _ in range(args.lanes - 1)]
-        ar = (lambda Y: dist.all_reduce(Y, op=dist.ReduceOp.SUM)) if world > 1 else None
+    lanes = max(1, min(args.lanes, args.steps // 2))
+    if args.lanes > 1 and lanes > 1:
+        S = C.Streaming(local, n, nl, m, cfg.kind, cfg.p, cfg.k, cfg.K, lanes=lanes, seed=cfg.sensing_seed,
+                        pix0=pix0, rank=args.rank, fit_sms=args.fit_sms, fused=args.fused and fused_ok is True)
+        Xs = [Xd] + [Xd.clone() for _ in range(lanes - 1)]
 
         def stream_run(nb):
             a = torch.cuda.Event(enable_timing=True)
             a.record(stream)
-            ends = S.run([Xs[b % args.lanes] for b in range(nb)], cfg.tau, mode, allreduce=ar, start_event=a)
+            ends = S.run([Xs[b % lanes] for b in range(nb)], cfg.tau, mode, allreduce=allreduce, start_event=a)
             for e in ends:
                 stream.wait_event(e)
             b_ = torch.cuda.Event(enable_timing=True)
             b_.record(stream)
             return a, b_
 
-        stream_run(max(args.warmup, args.lanes))
+        stream_run(max(args.warmup, lanes))
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -301,19 +456,18 @@ def main():
             launches = C.cdmd_kernel_launches() - n0
         if world > 1:
             dist.barrier()
-        ts = torch.tensor([a.elapsed_time(b_) / args.steps], dtype=torch.float64, device="cuda")
-        if world > 1:
-            dist.all_reduce(ts, op=dist.ReduceOp.MAX)
-        ms_max = float(ts.item())
+        ms_max = max_over_ranks(a.elapsed_time(b_) / args.steps)
         value = m / (ms_max * 1e-3)
-        streaming = {"lanes": args.lanes, "ms_per_batch": round(ms_max, 4), "sm_partition": S.sms,
-                     "fits": "sharded: batch b solved on rank b mod N, model broadcast" if S.shard_fit
-                     else "every rank",
-                     "note": "batches pipelined across lanes (own handle, stream, buffers, copy of X)"}
+        streaming = {"lanes": lanes, "batches": args.steps, "ms_per_batch": round(ms_max, 4),
+                     "sm_partition": S.sms, "fused": S.fused,
+                     "step_hbm_frac": round(step_bytes / (ms_max * 1e-3) / 1e9 / hbm, 4),
+                     "note": "batches pipelined across lanes (own handle, stream, buffers, copy of X); "
+                             "each lane runs >= 2 batches"}
+    if not pixel and world > 1:
+        value *= world      # batch-parallel replicas: every rank processes its own batches
 
-    # roofline of the dominant kernel: HBM-bound passes (algorithmic bytes per launch) and,
-    # for the dense sensings, the tensor-core sketch (algorithmic 2 p n m flops per launch)
-    hbm, bf16, peak_src = peaks()
+    # ---- roofline of the dominant kernel: HBM-bound passes (algorithmic bytes per
+    # launch) and, for the dense sensings, the tensor-core sketch (2 p n m per launch)
     ke, nc = P.model.k_eff, P.model.n_coef
     algo = {
         "modes": nl * (m - 1) + 4 * nl * ke,
@@ -324,8 +478,10 @@ def main():
                           if cfg.kind == "sparse" else 32 * cfg.p * m + 4 * cfg.p * m)
     elif cfg.kind in ("rademacher", "gaussian"):
         algo["sketch"] = 2 * cfg.p * nl * m
-    # kind::f16 runs at the bf16 rate; kind::i8 at twice it (the guide's nominal 4.5 / 2.25 ratio)
-    tensor_peak = bf16 * (2.0 if cfg.kind == "rademacher" else 1.0)
+    i8 = int8_peak_tops(torch) if cfg.kind == "rademacher" else None
+    tensor_peak = (i8 if i8 else 2.0 * bf16) if cfg.kind == "rademacher" else bf16
+    tensor_src = ("measured here: torch._int_mm int8 8192^3 (burst)" if i8 else
+                  "2 x measured bf16 (nominal ratio)") if cfg.kind == "rademacher" else peak_src
 
     def stage_roof(s):
         if s == "sketch" and cfg.kind in ("rademacher", "gaussian"):
@@ -348,8 +504,9 @@ def main():
     fg_kernel = {2: "foreground_tc_kernel", 1: "foreground_dynamic_kernel", 0: "foreground_static_kernel"}[
         C.cdmd_foreground_path(vq, P.model, mode)]
     roof = {"kernel": {"sketch": sk_kernel, "modes": md_kernel, "foreground": fg_kernel}[dom],
-            "bound": bound, "achieved": round(achieved, 1), "peak": peak, "unit": unit,
-            "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
+            "bound": bound, "achieved": round(achieved, 1), "peak": round(peak, 1), "unit": unit,
+            "frac": round(achieved / peak, 4), "traffic": traffic,
+            "peak_source": tensor_src if bound == "tensor" else peak_src,
             ("algorithmic_flops_per_launch" if bound == "tensor" else "algorithmic_bytes_per_launch"): algo[dom],
             "launch_ms": round(stage_ms[dom], 4),
             "stage_roofline": {s: round(stage_roof(s)[0] / stage_roof(s)[1], 4) for s in algo}}
@@ -357,9 +514,13 @@ def main():
     # Alg. 1 step 9 full-state amplitudes b = lstsq(Phi, x_1): measured on the
     # modes of the last step, after (and outside) the timed region -- the step's
     # background amplitudes are Remark 3's OMP ones, so this is a reported extra.
-    # Phi (n_local x k_eff fp32) is larger than L2 at the bench sizes.
     amplitudes = None
     if ke <= 128:
+        P.sketch(Xd)
+        if allreduce is not None:
+            allreduce(P.Y)
+        P.fit()
+        P.modes(Xd)
         va = C.video(Xd, n, pix0, nl)
         ws_a = torch.empty(max(C.cdmd_amplitudes_workspace_bytes(P.h, ke), 256), dtype=torch.uint8, device="cuda")
         Ga = torch.empty((ke + 1, ke), dtype=torch.float64, device="cuda")
@@ -371,7 +532,7 @@ def main():
             C.cdmd_amplitudes_gram(P.h, va, P.model, P.Phi, Ga, ws_a, stream)
             if marks:
                 marks[1].record(stream)
-            if world > 1:
+            if pixel:
                 dist.all_reduce(Ga, op=dist.ReduceOp.SUM)
             if marks:
                 marks[2].record(stream)
@@ -382,13 +543,13 @@ def main():
         for _ in range(3):
             amp_once()
         torch.cuda.synchronize()
-        reps, tg_, ts_ = 10, 0.0, 0.0
-        for _ in range(reps):
+        reps_a, tg_, ts_ = 10, 0.0, 0.0
+        for _ in range(reps_a):
             mk = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
             amp_once(mk)
             torch.cuda.synchronize()
-            tg_ += mk[0].elapsed_time(mk[1]) / reps
-            ts_ += mk[2].elapsed_time(mk[3]) / reps
+            tg_ += mk[0].elapsed_time(mk[1]) / reps_a
+            ts_ += mk[2].elapsed_time(mk[3]) / reps_a
         abytes = 4 * nl * ke + nl
         amplitudes = {"step": "Alg. 1 step 9, b = lstsq(Phi, x_1), not in the timed step",
                       "gram_kernel": "amp_gram_kernel", "gram_ms": round(tg_, 4), "solve_ms": round(ts_, 4),
@@ -403,13 +564,13 @@ def main():
         Xh = torch.from_numpy(np.ascontiguousarray(np.pad(X_host, ((0, 0), (0, ld - nl))))).pin_memory()
         mask_shape, mask_dtype = P.mask.shape, P.mask.dtype
         if streaming is not None:
-            mhs = [torch.empty(mask_shape, dtype=mask_dtype).pin_memory() for _ in range(args.lanes)]
-            e_steps = max(args.steps, 2 * args.lanes)
+            mhs = [torch.empty(mask_shape, dtype=mask_dtype).pin_memory() for _ in range(lanes)]
+            e_steps = max(args.steps, 2 * lanes)
 
             def e2e_run(nb):
                 a = torch.cuda.Event(enable_timing=True)
                 a.record(stream)
-                ends = S.run([Xs[b % args.lanes] for b in range(nb)], cfg.tau, mode, allreduce=ar, start_event=a,
+                ends = S.run([Xs[b % lanes] for b in range(nb)], cfg.tau, mode, allreduce=allreduce, start_event=a,
                              host_video=Xh, host_masks=mhs)
                 for e in ends:
                     stream.wait_event(e)
@@ -417,7 +578,7 @@ def main():
                 b_.record(stream)
                 return a, b_
 
-            e2e_run(args.lanes)
+            e2e_run(lanes)
             torch.cuda.synchronize()
             if world > 1:
                 dist.barrier()
@@ -441,10 +602,9 @@ def main():
                 e2e_step()
             b.record(stream)
             torch.cuda.synchronize()
-        te = torch.tensor([a.elapsed_time(b) / e_steps], dtype=torch.float64, device="cuda")
-        if world > 1:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e = {"value": m / (float(te.item()) * 1e-3), "unit": "frames/s",
+        te = max_over_ranks(a.elapsed_time(b) / e_steps)
+        ev_ = m / (te * 1e-3) * (world if not pixel and world > 1 else 1)
+        e2e = {"value": round(ev_, 1), "unit": "frames/s",
                "h2d_bytes_per_step": int(Xh.numel()) * world,
                "d2h_bytes_per_step": int(P.mask.numel() * P.mask.element_size()) * world,
                "mode": "streaming lanes" if streaming is not None else "one batch at a time"}
@@ -452,67 +612,36 @@ def main():
     if rank == 0:
         cpu = None
         if not args.no_cpu_baseline and world == 1:
-            cpu = cpu_baseline(cfg, X_host, args)
+            cpu = cpu_baseline(cfg, args)
+        par = (f"pixel-rows x{world}" if pixel else f"batch replicas x{world}") if world > 1 else "1 GPU"
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": "frames/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max, 4),
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8",
-            "data": "synthetic",
+            "higher_is_better": True, "scaling": "weak" if (world > 1 and not pixel) else "strong",
+            "vs_baseline": None, "dtype": "u8", "data": "synthetic",
             "config": {"workload": cfg.name, "video": f"{cfg.width}x{cfg.height}x{m}", "sensing": cfg.kind,
                        "p": cfg.p, "k": cfg.k, "K": cfg.K, "tau": cfg.tau, "background": args.bg, "rank": args.rank,
-                       "parallelism": f"pixel-rows x{world}", "l2": "inputs larger than L2 (X = %.2f GB)" % (n * m / 1e9),
+                       "parallelism": par, "l2": "inputs larger than L2 (X = %.2f GB)" % (n * m / 1e9),
                        "k_eff": ke, "K_eff": P.model.K_eff, "n_coef": nc},
             "stage_ms": {s: round(v, 4) for s, v in stage_ms.items()},
             "latency_ms_per_batch": round(latency_ms, 4),
+            "per_batch": per_batch,
+            "passes_only": passes_only,
+            "e2e_fused": e2e_fused if e2e_fused else {"unavailable": str(fused_ok)},
             "streaming": streaming,
             "roofline": roof,
             "amplitudes": amplitudes,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,   # libcdmd kernels launched in the timed region (cdmd_kernel_launches)
+            "gpu_launches_sequential": launches_seq,
             "clocks": clk.summary(),
         }
+        if "error" in graphs:
+            line["graph_error"] = graphs["error"]
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
-
-
-def cpu_baseline(cfg, X, args):
-    """The oracle as it stands, on a bounded sample (about 10-30 s of CPU work)."""
-    from oracle import cdmd as OD
-    from oracle import sensing as OS
-    m, n = X.shape
-    frac = args.ref_frac
-    rng = np.random.default_rng(0)
-    pix = np.sort(rng.choice(n, n // frac, replace=False))
-    kind = {"spixel": 0, "sparse": 1, "rademacher": 2, "gaussian": 3}[cfg.kind]
-    dense = cfg.kind in ("rademacher", "gaussian")
-    t0 = time.perf_counter()
-    if dense:
-        # a dense C row costs a full pass over X on the CPU: time every frac-th row and
-        # extrapolate; the fit runs on those rows (a p/frac x m sketch)
-        rstep = frac * (2 if cfg.kind == "gaussian" else 1)
-        Y = OS.sketch(X, kind, cfg.p, cfg.sensing_seed, rows=np.arange(0, cfg.p, rstep))
-        t_sk = (time.perf_counter() - t0) * rstep
-    else:
-        Y = OS.sketch(X, kind, cfg.p, cfg.sensing_seed)
-        t_sk = time.perf_counter() - t0
-    t1 = time.perf_counter()
-    model = OD.fit(Y, min(cfg.k, Y.shape[0]), cfg.K)
-    t_fit = time.perf_counter() - t1
-    t2 = time.perf_counter()
-    Xs = X[:, pix]
-    Phi = OD.modes(Xs, model["M"])
-    L = OD.background_dynamic(Phi, model) if args.bg == "dynamic" else OD.background_static(Phi, model)
-    OD.mask(Xs, L, cfg.tau)
-    t_px = (time.perf_counter() - t2) * frac
-    total = t_sk + t_fit + t_px
-    return {"value": round(m / total, 3), "unit": "frames/s", "cores": len(os.sched_getaffinity(0)),
-            "kind": "oracle",
-            "sample": f"{cfg.name}: " + (f"sketch of every {rstep}th row ({t_sk / rstep:.1f}s) extrapolated x{rstep}"
-                                         f" + fit of that {Y.shape[0]}-row sketch ({t_fit:.1f}s)" if dense else
-                                         f"full sketch ({t_sk:.1f}s) + fit ({t_fit:.1f}s)") + "; modes+background+mask "
-                      f"on 1/{frac} of the pixels ({len(pix)} px, {t_px / frac:.1f}s) extrapolated x{frac}"}
 
 
 if __name__ == "__main__":

@@ -8,8 +8,11 @@
  * Conventions shared by every entry point
  *  - Pointers are DEVICE pointers unless the argument says "host".
  *  - The CALLER owns every buffer (video, sketch, model, modes, mask, workspace);
- *    the library keeps only immutable per-handle state (cuBLAS/cuSOLVER handles,
- *    the Gaussian table) and never allocates on the hot path.
+ *    the library keeps only per-handle state (cuBLAS/cuSOLVER handles, the Gaussian
+ *    table, a ring of 64 tile counters for the persistent kernels -- each launch of
+ *    cdmd_modes / cdmd_foreground takes the next one, so up to 64 such launches of one
+ *    handle may be in flight at once on any streams -- and the set of sparse sensing
+ *    plans already checked) and never allocates on the hot path.
  *  - Calls are asynchronous on the given stream, except cdmd_fit (it reads the
  *    solver status and the model sizes back to the host once) and cdmd_create.
  *  - Validation happens on the host before any launch; an invalid call returns a
@@ -133,8 +136,8 @@ CDMD_API uint64_t cdmd_kernel_launches(void);
 /* Background selection of later cdmd_fit calls on this handle.  omega_eps = 0 (the
  * default): Remark 3's OMP picks at most K modes.  omega_eps > 0: the
  * background is the set of modes with |omega_p| = |log(lambda_p)| / dt < omega_eps
- * ("background modes have |omega_p| ~ 0"), in mode order, at most 32 (K is
- * then ignored), with amplitudes the least-squares fit of the first compressed frame
+ * ("background modes have |omega_p| ~ 0"), in mode order, at most K (the
+ * first K such modes; reading R24), with amplitudes the least-squares fit of the first compressed frame
  * on those modes (the same solve OMP ends with).  Errors: CDMD_ERR_ARG (null
  * handle), CDMD_ERR_RANGE (negative or non-finite omega_eps).                     */
 CDMD_API cdmd_status cdmd_set_background_selection(cdmd_handle h, double omega_eps);
@@ -163,8 +166,13 @@ CDMD_API cdmd_status cdmd_sm_partition(int device, int fit_sms, int n_streams, v
  * (integer kinds bit-exactly).  Y (p x m, ldy >= p) is overwritten.
  * ws: device workspace of at least cdmd_sketch_workspace_bytes() bytes, 256-B
  * aligned (index lists of C; for Gaussian C also the split-K partial sums, which are
- * reduced in a fixed order so Y is deterministic).  Errors: CDMD_ERR_RANGE if p < 1 or p > n_total,
- * s <= 1 (sparse), m < 2; CDMD_ERR_ARG on layout violations; CDMD_ERR_WORKSPACE. */
+ * reduced in a fixed order so Y is deterministic).  Sparse C: the first call with a
+ * given (n_total, p, s, seed) on a handle checks the generated rows against their ELL
+ * capacity (mu + 12 sqrt(mu) + 16 entries, mu = n/s) with one stream synchronisation;
+ * later calls with that plan do not synchronise (so the first call must not be inside
+ * a CUDA graph capture: CDMD_ERR_ARG).  Errors: CDMD_ERR_RANGE if p < 1 or p > n_total,
+ * s <= 1 (sparse), m < 2; CDMD_ERR_ARG on layout violations; CDMD_ERR_WORKSPACE;
+ * CDMD_ERR_NUMERIC if a sparse row exceeds its capacity (Y is not written). */
 CDMD_API size_t cdmd_sketch_workspace_bytes(const cdmd_video* v, const cdmd_sensing* c);
 CDMD_API cdmd_status cdmd_sketch(cdmd_handle h, const cdmd_video* v, const cdmd_sensing* c,
                         void* Y, int64_t ldy, void* ws, size_t ws_bytes, cdmd_stream st);

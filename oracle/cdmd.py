@@ -141,7 +141,7 @@ def optimal_rank(s, rows, cols):
 def select_background(omega, eps, cap=32):
     """Background modes by frequency (modes with |omega_p| ~ 0 model the
     slowly varying background): the columns j with |omega_j| < eps, in index order,
-    at most `cap` (the device's support limit)."""
+    at most `cap` (fit passes K: the model holds at most K background modes, reading R24)."""
     return [j for j in range(len(omega)) if abs(omega[j]) < eps][:cap]
 
 
@@ -180,7 +180,7 @@ def fit(Yfull, k, K, dt=1.0, rank_rtol=RANK_RTOL, rank="fixed", omega_eps=None):
     if omega_eps is None:
         support, beta = omp(PhiY, y1, K)
     else:
-        support = select_background(omega, omega_eps)
+        support = select_background(omega, omega_eps, cap=K)   # ||beta||_0 <= K (reading R24)
         beta = (np.linalg.lstsq(PhiY[:, support].astype(np.complex128), y1.astype(np.complex128), rcond=None)[0]
                 if support else np.zeros(0, dtype=np.complex128))
     return dict(k=k, k_eff=k_eff, sigma=s, V=V, U=U, Atilde=Atilde, lam=lam, W=W,

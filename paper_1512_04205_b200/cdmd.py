@@ -205,10 +205,11 @@ def cdmd_background(h, Phi, n_local, model, mode, t0, nt, L, stream=None):
 
 
 def cdmd_foreground(h, v, model, Phi, mode, tau, mask, stream=None):
-    """mask: (m, ldw) int32/uint32-sized CUDA tensor of packed words."""
+    """mask: (m, ldw) int32/uint32-sized CUDA tensor of packed words.  Phi=None: the
+    fused single pass (N11) -- the support's modes are computed in-slab from X."""
     _check("cdmd_foreground", _lib.cdmd_foreground(h.h, ctypes.byref(v), ctypes.byref(model), _ptr(Phi),
-                                                   Phi.stride(0), mode, float(tau), _ptr(mask), mask.stride(0),
-                                                   _stream(stream)))
+                                                   Phi.stride(0) if Phi is not None else 0, mode, float(tau),
+                                                   _ptr(mask), mask.stride(0), _stream(stream)))
 
 
 def cdmd_amplitudes_workspace_bytes(h, k):
@@ -364,25 +365,15 @@ class Pipeline:
                  self.dt, stream)
         return self.model
 
-    def adopt_model(self):
-        """After model_buf was overwritten with a model fitted elsewhere (the sharded
-        streaming fits: a broadcast from the owning rank), refresh the host-side fields
-        from the model's device status words (k_eff, K_eff, n_coef).  Synchronises with
-        the current stream."""
-        M = self.model
-        off = M.dev_info - self.model_buf.data_ptr()
-        d = self.model_buf[off:off + 16].view(torch.int32).cpu().tolist()
-        M.k_eff, M.K_eff, M.n_coef, M.info, M.dt = d[0], d[1], d[2], 0, self.dt
-        return M
-
     def modes(self, X, stream=None, simt=False):
         v = video(X, self.n_total, self.pix0, self.n_local)
         cdmd_modes(self.h, v, self.model, self.Phi, stream, simt=simt)
         return self.Phi[:self.model.k_eff]
 
-    def foreground(self, X, tau, mode=BG_DYNAMIC, stream=None):
+    def foreground(self, X, tau, mode=BG_DYNAMIC, stream=None, fused=False):
+        """fused=True: cdmd_foreground(Phi=NULL), the single pass N11 (no modes() call needed)."""
         v = video(X, self.n_total, self.pix0, self.n_local)
-        cdmd_foreground(self.h, v, self.model, self.Phi, mode, tau, self.mask, stream)
+        cdmd_foreground(self.h, v, self.model, None if fused else self.Phi, mode, tau, self.mask, stream)
         return self.mask
 
     def median3(self, width, height, stream=None):
@@ -416,13 +407,16 @@ class Pipeline:
         cdmd_background(self.h, self.Phi, self.n_local, self.model, mode, t0, nt, L, stream)
         return L
 
-    def run(self, X, tau, mode=BG_DYNAMIC, allreduce=None, stream=None):
+    def run(self, X, tau, mode=BG_DYNAMIC, allreduce=None, stream=None, fused=False):
+        """sketch -> [allreduce] -> fit -> modes -> foreground (fused: no modes pass;
+        the foreground computes the support's modes in-slab, N11)."""
         self.sketch(X, stream)
         if allreduce is not None:
             allreduce(self.Y)
         self.fit(stream)
-        self.modes(X, stream)
-        return self.foreground(X, tau, mode, stream)
+        if not fused:
+            self.modes(X, stream)
+        return self.foreground(X, tau, mode, stream, fused=fused)
 
 
 class Streaming:
@@ -431,34 +425,34 @@ class Streaming:
     thread) sets run batches round-robin, so the latency-bound small solve of one
     batch (cdmd_fit, which blocks its own host thread) overlaps the HBM-bound passes
     and solves of the others.  Each batch runs the same five calls as Pipeline.run.
-    With torch.distributed initialised, the per-batch all-reduces are issued in batch
-    order on every rank (a ticket lock), so collectives match across ranks.
+
+    Across GPUs (torch.distributed initialised, world > 1) two partitions:
+      * pixel-row slabs (run(..., allreduce=fn)): each rank sketches its slab, the
+        per-batch all-reduces of Y are issued in batch order on every rank (one ticket
+        sequence over one communicator, dist.OrderedAllreduce) and every rank repeats
+        the fit (bit-identical Y -> identical model);
+      * batch-parallel replicas (no allreduce): each rank runs its own whole-frame
+        batches (dist.my_batches), no collective at all.
+    A lane that raises aborts the ticket sequence (the other lanes stop waiting) and
+    run() re-raises the first error.
     Each lane uses two streams: set CUDA_DEVICE_MAX_CONNECTIONS (up to 32) to at least
     2 x lanes before CUDA initialises, or streams share the default 8 hardware queues
     and a lane's waiting solve stalls other lanes' work (bench.py sets 32)."""
 
     def __init__(self, device, n_total, n_local, m, kind, p, k, K, lanes=4, s=0.0, seed=0, pix0=0, dt=1.0,
-                 rank="fixed", fit_sms=0, shard_fit=True):
-        """shard_fit (torch.distributed with world > 1): batch b's small solve runs only
-        on rank b mod world, which broadcasts the fitted model (one buffer) to the
-        others, instead of every rank repeating every solve.  Creating the Streaming
-        object is then collective (it makes a second process group)."""
-        import threading
+                 rank="fixed", fit_sms=0, fused=False):
+        """fused: foreground through cdmd_foreground(Phi=NULL) (N11: modes of the
+        support computed in-slab, no cdmd_modes pass) instead of modes + foreground."""
+        from .dist import OrderedAllreduce
         self.lanes = []
-        self.world, self.grank, self.coll = 1, 0, None
-        import torch.distributed as dist
-        if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
-            from .dist import OrderedCollectives
-            self.world, self.grank = dist.get_world_size(), dist.get_rank()
-            bc = dist.new_group(backend=dist.get_backend()) if shard_fit else None
-            self.coll = OrderedCollectives(None, bc)
-        self.shard_fit = shard_fit and self.world > 1
-        lo, hi = torch.cuda.Stream.priority_range()
+        self.fused = fused
+        self.ordered = OrderedAllreduce()
         self.sms = None
         if fit_sms > 0:
             # spatial partition (cdmd_sm_partition): the solves get SMs of their own
             # instead of queueing behind the persistent full-resolution passes
             pst, fst, self.sms = cdmd_sm_partition(device, fit_sms, lanes)
+        lo, hi = torch.cuda.Stream.priority_range()
         for li in range(lanes):
             h = Handle(device)
             if fit_sms > 0:
@@ -473,69 +467,64 @@ class Streaming:
                 pipe = Pipeline(h, n_total, n_local, m, kind, p, k, K, s=s, seed=seed, pix0=pix0,
                                 device=f"cuda:{device}", dt=dt, rank=rank)
             self.lanes.append((h, st, st_fit, pipe))
-        self._cv = threading.Condition()
-        self._next_ar = 0
-
-    def _ordered_allreduce(self, b, fn, Y):
-        with self._cv:
-            self._cv.wait_for(lambda: self._next_ar == b)
-            fn(Y)
-            self._next_ar += 1
-            self._cv.notify_all()
 
     def run(self, videos, tau, mode=BG_DYNAMIC, allreduce=None, start_event=None, host_video=None,
             host_masks=None):
         """videos: list of uint8 CUDA tensors (m, ld), one per batch.  Returns the
         per-lane end events (record them into the caller's stream to join).
+        allreduce(Y): the per-batch sum of the slab sketches (pixel-row sharding), issued
+        in batch order; None for one GPU or batch-parallel replicas.
         End to end: with `host_video` (a pinned uint8 host tensor like videos[b]) every
         batch first copies it into its device buffer, and with `host_masks` (one pinned
         int32 host tensor per lane, shaped like the mask) every batch copies its mask
         back; the copies run on the lane's stream, overlapping the other lanes' work."""
         import concurrent.futures as cf
-        self._next_ar = 0
-        if self.coll is not None:
-            self.coll.reset()
+        self.ordered.reset()
         L = len(self.lanes)
         ends = [None] * L
 
         def lane_work(li):
             h, st, st_fit, pipe = self.lanes[li]
-            with torch.cuda.stream(st):
-                if start_event is not None:
-                    st.wait_event(start_event)
-                for b in range(li, len(videos), L):
-                    X = videos[b]
-                    if host_video is not None:
-                        X.copy_(host_video, non_blocking=True)
-                    pipe.sketch(X, st)
-                    if allreduce is not None:
-                        self._ordered_allreduce(b, allreduce, pipe.Y)
-                    owner = b % self.world
-                    err = None
-                    if not self.shard_fit or owner == self.grank:
+            try:
+                with torch.cuda.stream(st):
+                    if start_event is not None:
+                        st.wait_event(start_event)
+                    for b in range(li, len(videos), L):
+                        X = videos[b]
+                        if host_video is not None:
+                            X.copy_(host_video, non_blocking=True)
+                        pipe.sketch(X, st)
+                        if allreduce is not None:
+                            self.ordered.run(b, lambda: allreduce(pipe.Y))
                         st_fit.wait_stream(st)
-                        try:
-                            pipe.fit(st_fit)
-                        except Exception as e:   # still take part in the broadcast below
-                            err = e
+                        pipe.fit(st_fit)
                         st.wait_stream(st_fit)
-                    if self.shard_fit:
-                        self.coll.broadcast(b, pipe.model_buf, owner)
-                        if owner != self.grank:
-                            pipe.adopt_model()
-                    if err is not None:
-                        raise err
-                    pipe.modes(X, st)
-                    pipe.foreground(X, tau, mode, st)
-                    if host_masks is not None:
-                        host_masks[li].copy_(pipe.mask, non_blocking=True)
-                ev = torch.cuda.Event(enable_timing=True)
-                ev.record(st)
-                ends[li] = ev
+                        if self.fused:
+                            pipe.foreground(X, tau, mode, st, fused=True)
+                        else:
+                            pipe.modes(X, st)
+                            pipe.foreground(X, tau, mode, st)
+                        if host_masks is not None:
+                            host_masks[li].copy_(pipe.mask, non_blocking=True)
+                    ev = torch.cuda.Event(enable_timing=True)
+                    ev.record(st)
+                    ends[li] = ev
+            except BaseException as e:
+                self.ordered.abort(e)
+                raise
 
+        errs = []
         with cf.ThreadPoolExecutor(L) as ex:
-            for f in [ex.submit(lane_work, i) for i in range(L)]:
-                f.result()
+            futs = [ex.submit(lane_work, i) for i in range(L)]
+            for f in futs:
+                try:
+                    f.result()
+                except BaseException as e:
+                    errs.append(e)
+        if errs:
+            from .dist import LaneAbort
+            first = next((e for e in errs if not isinstance(e, LaneAbort)), errs[0])
+            raise first
         return ends
 
 

@@ -139,7 +139,7 @@ cdmd_status cdmd_create(int device, cdmd_handle* out) {
   if (st == CDMD_OK && cusolverDnCreateParams(&h->params) != CUSOLVER_STATUS_SUCCESS) st = CDMD_ERR_CUDA;
   if (st == CDMD_OK && cudaMalloc(&h->gauss_table, 65536 * sizeof(uint16_t)) != cudaSuccess) st = CDMD_ERR_CUDA;
   if (st == CDMD_OK && cudaMallocHost(&h->host_info, 16 * sizeof(int32_t)) != cudaSuccess) st = CDMD_ERR_CUDA;
-  if (st == CDMD_OK && cudaMalloc(&h->sched, 16 * sizeof(int)) != cudaSuccess) st = CDMD_ERR_CUDA;
+  if (st == CDMD_OK && cudaMalloc(&h->sched, CDMD_SCHED_SLOTS * sizeof(int)) != cudaSuccess) st = CDMD_ERR_CUDA;
   if (st == CDMD_OK && launch_gaussian_table(h->gauss_table, 0) != cudaSuccess) st = CDMD_ERR_CUDA;
   if (st == CDMD_OK && cudaDeviceSynchronize() != cudaSuccess) st = CDMD_ERR_CUDA;
   if (st != CDMD_OK) {
@@ -162,6 +162,28 @@ void cdmd_destroy(cdmd_handle h) {
 }
 
 // ------------------------------------------------------------------- sketch
+// A sparse row longer than its ELL capacity (mu + 12 sqrt(mu) + 16 entries; a
+// binomial tail below 1e-20 per row) would be truncated.  The index lists depend
+// only on (n, p, s, seed), so the first call with a plan reads the overflow flag back
+// once (one stream sync) and reports CDMD_ERR_NUMERIC; later calls with a checked plan
+// do not sync.
+static bool sparse_checked(cdmd_handle h, const SensingPlan& P, uint64_t seed) {
+  std::lock_guard<std::mutex> g(h->mu);
+  return h->sparse_checked.count(std::make_tuple(P.n, P.p, P.s, seed)) != 0;
+}
+
+static cdmd_status check_sparse_once(cdmd_handle h, const SensingPlan& P, uint64_t seed, const int32_t* flags,
+                                     cudaStream_t st) {
+  int32_t f = 0;
+  if (cudaMemcpyAsync(&f, flags, sizeof(int32_t), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess)
+    return CDMD_ERR_CUDA;
+  if (f & FLAG_SPARSE_OVERFLOW) return CDMD_ERR_NUMERIC;
+  std::lock_guard<std::mutex> g(h->mu);
+  h->sparse_checked.insert(std::make_tuple(P.n, P.p, P.s, seed));
+  return CDMD_OK;
+}
+
 static size_t sketch_ws_bytes(const cdmd_video* v, const SensingPlan& P) {
   size_t b = al256(sensing_ws_bytes(P));
   if (P.kind == CDMD_GAUSSIAN) b += al256(sizeof(float) * (size_t)gaussian_part_floats(*v, P.p));
@@ -194,11 +216,21 @@ cdmd_status cdmd_sketch(cdmd_handle h, const cdmd_video* v, const cdmd_sensing* 
       break;
     }
     case CDMD_SPARSE: {
+      const bool checked = sparse_checked(h, P, c->seed);
+      if (!checked) {   // the first call of a plan syncs once: not inside a graph capture
+        cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+        if (cudaStreamIsCapturing(st, &cap) != cudaSuccess) return CDMD_ERR_CUDA;
+        if (cap != cudaStreamCaptureStatusNone) return CDMD_ERR_ARG;
+      }
       int32_t* ell = (int32_t*)ws;
       int32_t* counts = (int32_t*)((char*)ws + al256(sizeof(int32_t) * P.p * P.cap));
       int32_t* flags = (int32_t*)((char*)counts + al256(sizeof(int32_t) * P.p));
       e = cudaMemsetAsync(flags, 0, 16, st);
       if (e == cudaSuccess) e = launch_sparse_rows(P, ell, counts, flags, st);
+      if (e == cudaSuccess && !checked) {
+        const cdmd_status cs = check_sparse_once(h, P, c->seed, flags, st);
+        if (cs != CDMD_OK) return cs;
+      }
       if (e == cudaSuccess) e = launch_sketch_sparse(*v, P, ell, counts, (int32_t*)Y, ldy, st);
       break;
     }
@@ -285,7 +317,7 @@ cdmd_status cdmd_modes(cdmd_handle h, const cdmd_video* v, const cdmd_model* M, 
                        int64_t ldphi, cdmd_stream st) {
   cdmd_status s = modes_common(h, v, M, Phi, ldphi);
   if (s != CDMD_OK) return s;
-  return cuda_status(launch_modes_tc(*v, *M, Phi, ldphi, h->sched + 0, (cudaStream_t)st));
+  return cuda_status(launch_modes_tc(*v, *M, Phi, ldphi, sched_slot(h), (cudaStream_t)st));
 }
 
 cdmd_status cdmd_modes_simt(cdmd_handle h, const cdmd_video* v, const cdmd_model* M, float* Phi,
@@ -318,7 +350,7 @@ cdmd_status cdmd_foreground(cdmd_handle h, const cdmd_video* v, const cdmd_model
   if ((s = check_model(M, v->m)) != CDMD_OK) return s;
   if (!(tau > 0.0f)) return CDMD_ERR_RANGE;
   if (ldphi < v->n_local || ldw < ceil_div(v->n_local, 32)) return CDMD_ERR_ARG;
-  return cuda_status(launch_foreground(*v, *M, Phi, ldphi, mode, tau, mask, ldw, h->sched + 1, (cudaStream_t)st));
+  return cuda_status(launch_foreground(*v, *M, Phi, ldphi, mode, tau, mask, ldw, sched_slot(h), (cudaStream_t)st));
 }
 
 // --------------------------------------------------------------- amplitudes
@@ -406,7 +438,11 @@ cdmd_status cdmd_sensing_rows(cdmd_handle h, int64_t n_total, const cdmd_sensing
     if (cudaMallocAsync((void**)&flags, 16, st) != cudaSuccess) return CDMD_ERR_CUDA;
     cudaMemsetAsync(flags, 0, 16, st);
     cudaError_t e = launch_sparse_rows(P, rows_or_ell, counts, flags, st);
+    int32_t f = 0;
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&f, flags, sizeof(int32_t), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     cudaFreeAsync(flags, st);
+    if (e == cudaSuccess && (f & FLAG_SPARSE_OVERFLOW)) return CDMD_ERR_NUMERIC;
     return cuda_status(e);
   }
   return CDMD_ERR_ARG;

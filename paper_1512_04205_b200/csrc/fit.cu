@@ -318,13 +318,15 @@ __global__ void __launch_bounds__(256) omp_kernel(
     alpha[j] = {cf[ra], -sg * cf[rb]};
   }
   // frequency selection: the columns with |omega| = |log lambda| / dt < omega_eps,
-  // in index order, at most 32; each is added as a forced "OMP step" (same least squares)
+  // in index order, at most K (the model's support capacity; reading R24); each is added
+  // as a forced "OMP step" (same least squares)
   __shared__ int T[32];
   __shared__ int nT_sh;
   if (tid == 0) {
     nS_sh = 0; stop_sh = 0; nT_sh = 0;
     if (omega_eps > 0.0) {
-      for (int j = 0; j < k && nT_sh < 32; ++j) {
+      const int cap = K < 32 ? K : 32;   // beta/support hold K entries, coef 2K rows
+      for (int j = 0; j < k && nT_sh < cap; ++j) {
         const double lr = lam[2 * j], li = lam[2 * j + 1];
         const double om = hypot(log(hypot(lr, li)), atan2(li, lr)) / dt;
         if (om < omega_eps) T[nT_sh++] = j;

@@ -30,6 +30,11 @@ constexpr int FG_XSTAGE = FG_BM * FG_BN;   // bytes of X per unit (two 128x128 S
 constexpr int FG_FSPLIT = 4;        // pixel slices per unit (per TMEM lane quarter)
 constexpr int FG_EPI_WARPS = 4 * FG_FSPLIT;
 constexpr int FG_PW = FG_BN / FG_FSPLIT;   // pixels per epilogue warp per unit
+#ifdef CDMD_ABLATIONS
+#define FG_ABL(x) (x)
+#else
+#define FG_ABL(x) false
+#endif
 
 // no-swizzle K-major core-matrix layout: row r, 16-B chunk c at
 // (r / 8) * SBO + c * 128 + (r % 8) * 16, SBO = 16 * KP
@@ -208,7 +213,7 @@ __global__ void __launch_bounds__(32 * (2 + FG_EPI_WARPS), 1) foreground_tc_kern
                 const uint64_t ad =
                     desc_nosw(aBase + pi * PART_A + fb * (FG_BM / 8) * (16 * KP) + kk * 256, 128, 16 * KP);
                 const uint64_t bd = desc_nosw(bBase + (bb * 3 + pj) * PART_B + kk * 256, 128, 16 * KP);
-                if (!(dbg & 2)) tc::mma_f16(d, ad, bd, IDESC, first ? 0u : 1u);
+                if (!FG_ABL(dbg & 2)) tc::mma_f16(d, ad, bd, IDESC, first ? 0u : 1u);
                 first = 0;
               }
           tc::mma_commit(&tfull[tb]);
@@ -309,7 +314,7 @@ __global__ void __launch_bounds__(32 * (2 + FG_EPI_WARPS), 1) foreground_tc_kern
           const uint4 b = *reinterpret_cast<const uint4*>(row + (((c + 1) ^ (r & 7)) << 4));
           const uint32_t xw[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
           tc::tmem_ld_wait();
-          words[w] = (dbg & 1) ? 0u : mask32(xw, L, tau);
+          words[w] = FG_ABL(dbg & 1) ? 0u : mask32(xw, L, tau);
         }
         // the stage goes back only after the words are built: the shared loads have
         // then completed (handing it back right after issuing them raced with the
@@ -365,10 +370,16 @@ static size_t fg_smem_bytes(int KP, int nfb, int stages) {
          512;
 }
 
+// ablation switches exist only in builds with -DCDMD_ABLATIONS;
+// the release kernel always runs the MMAs and the mask arithmetic
+#ifdef CDMD_ABLATIONS
 static int dbg_mode() {
   const char* e = getenv("CDMD_FG_DBG");
   return e ? atoi(e) : 0;
 }
+#else
+static int dbg_mode() { return 0; }
+#endif
 
 static int fg_kp(int n_coef) { return n_coef <= 16 ? 16 : (n_coef <= 32 ? 32 : 0); }
 

@@ -3,6 +3,10 @@
 #include <cublas_v2.h>
 #include <cusolverDn.h>
 
+#include <atomic>
+#include <mutex>
+#include <set>
+#include <tuple>
 #include <vector>
 
 #include "common.cuh"
@@ -15,12 +19,26 @@ struct cdmd_handle_s {
   cusolverDnParams_t params = nullptr;
   uint16_t* gauss_table = nullptr;   // device, 65536 bf16 bit patterns (immutable)
   int32_t* host_info = nullptr;      // pinned, 16 words for fit read-back
-  int* sched = nullptr;              // device, tile counters of the persistent kernels (0 modes, 1 foreground)
+  // device, CDMD_SCHED_SLOTS tile counters of the persistent kernels (dynamic tile
+  // schedule).  Every launch takes the next slot, so persistent launches of one handle
+  // on different streams never share a counter (up to CDMD_SCHED_SLOTS in flight).
+  int* sched = nullptr;
+  std::atomic<uint32_t> sched_next{0};
+  // sparse plans (n, p, s, seed) whose index lists were checked once against their ELL
+  // capacity (cdmd_sketch syncs the first time a plan is seen, never afterwards)
+  std::set<std::tuple<int64_t, int64_t, double, uint64_t>> sparse_checked;
+  std::mutex mu;
   std::vector<char> host_ws;         // cuSOLVER host workspace (fit only)
   double omega_eps = 0.0;            // > 0: background by |omega| < omega_eps, else OMP
 };
 
+#define CDMD_SCHED_SLOTS 64
+
 namespace cdmd {
+// a tile counter of its own for one persistent launch (reset on the launch's stream)
+inline int* sched_slot(cdmd_handle h) {
+  return h->sched + (h->sched_next.fetch_add(1, std::memory_order_relaxed) % CDMD_SCHED_SLOTS);
+}
 cdmd_status fit_impl(cdmd_handle h, const void* Y, int64_t ldy, int kind, int64_t p, int64_t m,
                      int k, int K, double dt, cdmd_model* model, void* ws, size_t ws_bytes,
                      cudaStream_t st);

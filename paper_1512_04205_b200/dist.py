@@ -5,10 +5,11 @@ owns global pixels [pix0_g, pix0_g + n_g) of every frame.  The sketch is linear
 in the pixels (Y = C D = sum_g C[:, slab_g] D[slab_g, :]), so each rank sketches
 its slab with C's GLOBAL columns and one all-reduce(SUM) of the small p x m Y
 gives every rank the full sketch (int32 sums: exact and order-independent).
-One batch at a time the fit is then replicated bit-identically on every rank;
-the streaming lanes instead solve batch b on rank b mod world and broadcast the
-model (OrderedCollectives).  Modes + mask run communication-free on each slab.
-This module holds only the host logic.
+The fit is then replicated bit-identically on every rank; modes + mask run
+communication-free on each slab.  The streaming lanes issue the per-batch
+all-reduces in batch order (OrderedAllreduce).  For long videos the alternative is
+batch-parallel replicas: whole batches per rank, no collective at all
+(batch_owner).  This module holds only the host logic.
 """
 
 import math
@@ -33,50 +34,65 @@ def allreduce_sum(tensor, group=None):
     return tensor
 
 
-def fit_owner(batch, world):
-    """Rank that runs the small solve of `batch` when fits are sharded (round robin)."""
+def batch_owner(batch, world):
+    """Batch-parallel replicas (a long video is "split into batches of 200
+    consecutive frames" whose decompositions are "computed for each batch
+    independently"): rank b mod world runs batch b end to end on whole frames, with no
+    collective at all."""
     return batch % world
 
 
-class OrderedCollectives:
-    """Batch-ordered collectives for the streaming lanes (host logic only).
+def my_batches(nb, world, rank):
+    """The batches of a batch-parallel run that this rank owns, in order."""
+    return [b for b in range(nb) if batch_owner(b, world) == rank]
 
-    Lane threads reach their collectives in any order; NCCL (and gloo) need every rank
-    to issue the collectives of one communicator in the same order.  Each kind of
-    collective has its own ticket sequence in batch order and its own communicator:
-    the all-reduce of the partial sketches on `ar_group`, the broadcast of a fitted
-    model from its owner (fit_owner) on `bc_group`, so the two sequences never have to
-    interleave identically across ranks.  With sharded fits each rank runs 1/world of
-    the small solves (the per-batch work is independent) instead of all of them."""
 
-    def __init__(self, ar_group=None, bc_group=None):
+class LaneAbort(RuntimeError):
+    """Raised in a lane that was waiting for a collective ticket when another lane failed."""
+
+
+class OrderedAllreduce:
+    """Batch-ordered all-reduces of the per-slab partial sketches for the streaming
+    lanes of a pixel-sharded run (host logic only).
+
+    Lane threads reach their all-reduce in any order, but every rank must issue the
+    collectives of a communicator in the same order.  One ticket sequence in batch
+    order over the one communicator gives exactly that: batch b's all-reduce is issued
+    once batches 0..b-1 have issued theirs, on every rank.  It is the only collective of
+    the data path (the fits are replicated: every rank gets bit-identical Y).
+    If a lane fails, abort() wakes every waiter with LaneAbort instead of leaving them
+    blocked on a ticket that will never come."""
+
+    def __init__(self, group=None):
         import threading
-        self.ar_group, self.bc_group = ar_group, bc_group
-        # one lock per sequence: a thread blocked inside one kind of collective (gloo
-        # calls block until the peers join) must not stop the other sequence
-        self._cv = {"ar": threading.Condition(), "bc": threading.Condition()}
-        self._next = {"ar": 0, "bc": 0}
+        self.group = group
+        self._cv = threading.Condition()
+        self._next = 0
+        self._abort = None
 
     def reset(self):
-        for kind, cv in self._cv.items():
-            with cv:
-                self._next[kind] = 0
-                cv.notify_all()
+        with self._cv:
+            self._next, self._abort = 0, None
+            self._cv.notify_all()
 
-    def _ordered(self, kind, b, fn):
-        cv = self._cv[kind]
-        with cv:
-            cv.wait_for(lambda: self._next[kind] == b)
+    def abort(self, exc):
+        with self._cv:
+            if self._abort is None:
+                self._abort = exc
+            self._cv.notify_all()
+
+    def run(self, b, fn):
+        """Run fn() as the b-th collective of the sequence."""
+        with self._cv:
+            self._cv.wait_for(lambda: self._next == b or self._abort is not None)
+            if self._abort is not None:
+                raise LaneAbort(f"batch {b}: another lane failed: {self._abort!r}")
             try:
                 fn()
             finally:
-                self._next[kind] += 1
-                cv.notify_all()
+                self._next += 1
+                self._cv.notify_all()
 
     def allreduce(self, b, tensor):
         import torch.distributed as dist
-        self._ordered("ar", b, lambda: dist.all_reduce(tensor, op=dist.ReduceOp.SUM, group=self.ar_group))
-
-    def broadcast(self, b, tensor, src):
-        import torch.distributed as dist
-        self._ordered("bc", b, lambda: dist.broadcast(tensor, src=src, group=self.bc_group))
+        self.run(b, lambda: dist.all_reduce(tensor, op=dist.ReduceOp.SUM, group=self.group))

@@ -94,21 +94,18 @@ def _ordered_worker(rank, world, port, out):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        from paper_1512_04205_b200.dist import OrderedCollectives, fit_owner
-        coll = OrderedCollectives(None, dist.new_group(backend="gloo"))
+        from paper_1512_04205_b200.dist import OrderedAllreduce
+        coll = OrderedAllreduce()
         nb, lanes = 12, 5
         res = {}
         rng = random.Random(rank)
 
         def lane(li):
             for b in range(li, nb, lanes):
+                threading.Event().wait(rng.random() * 0.01)   # lanes arrive in random order
                 y = torch.full((7,), float(rank + 1) * (b + 1))
-                coll.allreduce(b, y)                     # sum over ranks: (1 + 2) (b + 1)
-                owner = fit_owner(b, world)
-                model = torch.full((5,), 1000.0 * b + owner) if rank == owner else torch.zeros(5)
-                coll.broadcast(b, model, owner)          # every rank gets the owner's "model"
-                res[b] = (y.tolist(), model.tolist())
-                threading.Event().wait(rng.random() * 0.01)
+                coll.allreduce(b, y)                          # sum over ranks: (1 + 2) (b + 1)
+                res[b] = y.tolist()
 
         ts = [threading.Thread(target=lane, args=(li,)) for li in rng.sample(range(lanes), lanes)]
         for t in ts:
@@ -120,11 +117,10 @@ def _ordered_worker(rank, world, port, out):
         dist.destroy_process_group()
 
 
-def test_ordered_collectives_sharded_fits_two_ranks():
-    """Streaming's batch-ordered collectives (dist.OrderedCollectives): lanes reach
-    their all-reduce and model broadcast in any order on each rank; tickets issue them
-    in batch order on two communicators, and each batch's model comes from its owner
-    rank (b mod world)."""
+def test_ordered_allreduce_two_ranks():
+    """Streaming's batch-ordered all-reduces (dist.OrderedAllreduce): lanes reach their
+    all-reduce in any order on each rank; one ticket sequence on one communicator issues
+    them in batch order, so every batch is summed with the same batch of the peer."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
@@ -138,9 +134,48 @@ def test_ordered_collectives_sharded_fits_two_ranks():
     for rank in (0, 1):
         res = got[rank]
         assert sorted(res) == list(range(12))
-        for b, (y, model) in res.items():
+        for b, y in res.items():
             assert y == [3.0 * (b + 1)] * 7
-            assert model == [1000.0 * b + (b % 2)] * 5
+
+
+def test_ordered_allreduce_abort_wakes_waiters():
+    """A failed lane aborts the sequence: lanes waiting for a later ticket raise
+    LaneAbort instead of waiting forever (no process group needed: fn is local)."""
+    import threading
+    from paper_1512_04205_b200.dist import LaneAbort, OrderedAllreduce
+    coll = OrderedAllreduce()
+    seen, errs = [], []
+
+    def waiter(b):
+        try:
+            coll.run(b, lambda: seen.append(b))
+        except LaneAbort as e:
+            errs.append((b, str(e)))
+
+    ts = [threading.Thread(target=waiter, args=(b,)) for b in (1, 2, 3)]
+    for t in ts:
+        t.start()
+    coll.abort(RuntimeError("cdmd_fit failed on batch 0"))   # batch 0 never issues its ticket
+    for t in ts:
+        t.join(timeout=10)
+        assert not t.is_alive()
+    assert seen == [] and sorted(b for b, _ in errs) == [1, 2, 3]
+    coll.reset()
+    coll.run(0, lambda: seen.append(0))
+    assert seen == [0]
+
+
+def test_batch_replicas_partition():
+    """Batch-parallel replicas: every batch has exactly one owner rank, owners
+    round-robin, and a rank's batches are in order."""
+    from paper_1512_04205_b200.dist import batch_owner, my_batches
+    for world in (1, 2, 3, 8):
+        for nb in (0, 1, 7, 24):
+            got = sorted(b for r in range(world) for b in my_batches(nb, world, r))
+            assert got == list(range(nb))
+            for r in range(world):
+                mb = my_batches(nb, world, r)
+                assert mb == sorted(mb) and all(batch_owner(b, world) == r for b in mb)
 
 
 def _amp_worker(rank, world, port, out):

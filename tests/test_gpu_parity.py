@@ -246,25 +246,47 @@ def test_c3_rademacher_full_size_sampled_rows(C, H):
     m, n = X.shape
     P = C.Pipeline(H, n, n, m, "rademacher", cfg.p, cfg.k, cfg.K)
     Y = P.sketch(to_dev(X)).cpu().numpy().T
-    rows = [0, 1, 777, cfg.p - 1]
+    # 64 rows over every 128-row tile of the tensor-core kernel: each tile's first and
+    # last row and three random rows inside it (12 tiles at p = 1500, the last ragged)
+    rng = np.random.default_rng(3)
+    rows = set()
+    for r0 in range(0, cfg.p, 128):
+        r1 = min(cfg.p, r0 + 128)
+        rows |= {r0, r1 - 1, *rng.integers(r0, r1, 3).tolist()}
+    rows = sorted(rows)[:64] if len(rows) > 64 else sorted(rows)
+    while len(rows) < 64:
+        rows = sorted(set(rows) | {int(rng.integers(0, cfg.p))})
     want = OS.sketch(X, OS.RADEMACHER, cfg.p, 0, rows=rows)
+    assert len(rows) == 64 and {r // 128 for r in rows} == set(range((cfg.p + 127) // 128))
     assert np.array_equal(Y[rows].astype(np.int64), want)
 
 
-def test_c4_gaussian_full_size_sampled_rows(C, H):
-    cfg = config_by_name("c4_1080p_gaussian")
-    X = video_for(cfg)
-    m, n = X.shape
-    P = C.Pipeline(H, n, n, m, "gaussian", cfg.p, cfg.k, cfg.K)
-    Y = P.sketch(to_dev(X)).cpu().numpy().T.astype(np.float64)
-    rows = [0, 1999]
-    want = OS.sketch(X, OS.GAUSSIAN, cfg.p, 0, rows=rows, chunk=1 << 18)
-    d = np.linalg.norm(Y[rows] - want, axis=1) / np.linalg.norm(want, axis=1)
-    assert d.max() <= PT.RTOL_Y_GAUSS
+def _phi_columns_parity(Pg, Po, perm, lam_o, k_eff):
+    """Per-column relative error of the folded-then-unfolded device modes against the
+    oracle's, after unit-phase alignment, over well-separated eigenvalues; returns the worst."""
+    worst = 0.0
+    for i in range(k_eff):
+        j = perm[i]
+        if PT.well_separated(lam_o, j):
+            worst = max(worst, PT.phase_aligned_rel(Pg[:, i], Po[:, j]))
+    return worst
+
+
+def _full_frame_mask_parity(mask_words, n, ref_mask, band):
+    """Whole-frame mask agreement: >= 99.9 % and every disagreement inside the oracle's
+    1e-3 band around tau (band = |resid - tau| <= 1e-3, computed by the oracle)."""
+    got = OD.unpack_mask(mask_words, n)
+    dis = got != ref_mask
+    frac = 1.0 - dis.mean()
+    outside = int(np.count_nonzero(dis & ~band))
+    return frac, outside, int(dis.sum())
 
 
 def test_c4_sparse_full_size(C, H):
-    """The bench configuration, in the bench's launch configuration."""
+    """The bench configuration, in the bench's launch configuration, against the oracle
+    on EVERY pixel: exact Y, fit parity, all n rows of Phi per column, and the whole
+    1080p x 500 mask (the oracle's per-pixel steps fanned over pixel slabs)."""
+    from oracle.runner import PixelPool
     cfg = config_by_name("c4_1080p_sparse")
     X = video_for(cfg)
     m, n = X.shape
@@ -279,25 +301,69 @@ def test_c4_sparse_full_size(C, H):
     assert gm["k_eff"] == om["k_eff"]
     perm, err = PT.match_eigs(gm["lam"], om["lam"])
     assert err <= PT.RTOL_EIG
+    assert np.max(np.abs(gm["sigma"] - om["sigma"]) / om["sigma"]) <= 1e-6
     assert PT.supports_equal_mod_conj(gm["support"], gm["pair"], perm, om["support"], om["pair"])
-    Phi = P.modes(Xd)
+    Phi = P.modes(Xd).cpu().numpy()
     mask = P.foreground(Xd, cfg.tau, C.BG_DYNAMIC).cpu().numpy().view(np.uint32)
     torch.cuda.synchronize()
-    # sampled pixels: oracle Phi rows and background for 4096 random pixels + a ragged tail
-    rng = np.random.default_rng(0)
-    pix = np.unique(np.concatenate([rng.choice(n, 4096, replace=False), np.arange(n - 40, n)]))
-    Po = X[1:, pix].T.astype(np.float64) @ om["M"]                    # |pix| x k
-    Pg = PT.unfold(Phi.cpu().numpy()[:, pix], gm["pair"])
-    for i in range(gm["k_eff"]):
-        j = perm[i]
-        if PT.well_separated(om["lam"], j):
-            assert PT.phase_aligned_rel(Pg[:, i], Po[:, j]) <= PT.RTOL_PHI
-    Ld = OD.background_dynamic(Po, om)                                # |pix| x m
-    res = np.abs(X[:, pix].astype(np.float64) - Ld.T)
-    mo = res > cfg.tau
-    mg = OD.unpack_mask(mask, n)[:, pix]
-    frac, band, nd = PT.mask_agreement(mg, mo, res, cfg.tau)
-    assert frac >= PT.MASK_AGREE and band, (frac, nd)
+    del Xd
+    with PixelPool(cfg) as pool:
+        ref = pool.run(om, cfg.tau, dynamic=True, want=("Phi", "mask", "band"))
+    worst = _phi_columns_parity(PT.unfold(Phi, gm["pair"]), ref["Phi"], perm, om["lam"], gm["k_eff"])
+    assert worst <= PT.RTOL_PHI, worst
+    frac, outside, nd = _full_frame_mask_parity(mask, n, ref["mask"], ref["band"])
+    print(f"c4 sparse full frame: phi worst {worst:.2e}, mask agreement {frac:.7f} ({nd} px, {outside} outside band)")
+    assert frac >= PT.MASK_AGREE and outside == 0, (frac, nd, outside)
+
+
+def test_c4_gaussian_full_pipeline(C, H):
+    """BASELINE's 1080p Gaussian(bf16) configuration through the whole path against the
+    oracle: all 2000 rows of Y normwise per column (the oracle's sketch summed over pixel
+    slabs computed in worker processes), then
+      (a) the device fit on the device's fp32 Y against the oracle fit of that same Y:
+          sigma to 1e-6, lambda to 1e-4, supports equal;
+      (b) the Gaussian sketch's own effect, oracle fit of the oracle Y against oracle fit
+          of the device Y: |d sigma_j| <= ||dY||_2 (Weyl) and lambda to 1e-4;
+      (c) Phi (every pixel, per column) and the dynamic mask (every pixel) against the
+          oracle with the model of (a)."""
+    from oracle.runner import PixelPool, parallel_sketch
+    cfg = config_by_name("c4_1080p_gaussian")
+    X = video_for(cfg)
+    m, n = X.shape
+    Xd = to_dev(X)
+    P = C.Pipeline(H, n, n, m, "gaussian", cfg.p, cfg.k, cfg.K)
+    Yg = P.sketch(Xd).cpu().numpy().T.astype(np.float64)          # p x m
+    P.fit()
+    gm = C.model_to_host(P.model)
+    Phi = P.modes(Xd).cpu().numpy()
+    mask = P.foreground(Xd, cfg.tau, C.BG_DYNAMIC).cpu().numpy().view(np.uint32)
+    torch.cuda.synchronize()
+    del Xd
+    Yo = parallel_sketch(cfg, OS.GAUSSIAN)
+    d = np.linalg.norm(Yg - Yo, axis=0) / np.linalg.norm(Yo, axis=0)
+    assert d.max() <= PT.RTOL_Y_GAUSS, d.max()
+    # (a) the fit on identical input
+    oa = OD.fit(Yg, cfg.k, cfg.K)
+    assert gm["k_eff"] == oa["k_eff"]
+    perm, err = PT.match_eigs(gm["lam"], oa["lam"])
+    assert err <= PT.RTOL_EIG, err
+    assert np.max(np.abs(gm["sigma"] - oa["sigma"]) / oa["sigma"]) <= 1e-6
+    assert PT.supports_equal_mod_conj(gm["support"], gm["pair"], perm, oa["support"], oa["pair"])
+    # (b) what the fp32 sketch changes (perturbation bounds on the same oracle)
+    ob = OD.fit(Yo, cfg.k, cfg.K)
+    dY2 = np.linalg.norm(Yg - Yo, 2)
+    ks = min(oa["k_eff"], ob["k_eff"])
+    assert np.all(np.abs(oa["sigma"][:ks] - ob["sigma"][:ks]) <= 2 * dY2)
+    print(f"c4 gaussian: Y normwise max {d.max():.2e}, fit lambda {err:.2e}, "
+          f"oracle(Yg) vs oracle(Yo) lambda {PT.match_eigs(oa['lam'], ob['lam'])[1]:.2e}")
+    # (c) every pixel
+    with PixelPool(cfg) as pool:
+        ref = pool.run(oa, cfg.tau, dynamic=True, want=("Phi", "mask", "band"))
+    worst = _phi_columns_parity(PT.unfold(Phi, gm["pair"]), ref["Phi"], perm, oa["lam"], gm["k_eff"])
+    assert worst <= PT.RTOL_PHI, worst
+    frac, outside, nd = _full_frame_mask_parity(mask, n, ref["mask"], ref["band"])
+    print(f"c4 gaussian full frame: phi worst {worst:.2e}, mask agreement {frac:.7f} ({nd} px, {outside} outside band)")
+    assert frac >= PT.MASK_AGREE and outside == 0, (frac, nd, outside)
 
 
 def test_errors_are_reported_not_launched(C, H):
@@ -502,6 +568,71 @@ def test_pipeline_parity_frequency_background(C, H, case, want):
     check_all(g, o, kind, tau)
 
 
+def test_frequency_background_capped_at_K(C, H):
+    """More slow modes than the model's K (reading R24): the device keeps the first K of
+    them in mode order, like the oracle, and writes nothing past the model's K-sized
+    arrays (the model buffer is followed by a guard region checked unchanged)."""
+    cfg = config_by_name("c2_320x240_spixel")
+    X = video_for(cfg)
+    m, n = X.shape
+    k, K = cfg.k, 3
+    Y = OS.sketch(X, KIND[cfg.kind], cfg.p, 0)
+    om_all = OD.fit(Y, k, K)["omega"]
+    eps = float(np.max(np.abs(om_all))) + 1.0          # every mode qualifies
+    Xd = to_dev(X)
+    P = C.Pipeline(H, n, n, m, cfg.kind, cfg.p, k, K, omega_eps=eps)
+    nb = P.model_buf.numel()
+    guard = torch.full((nb + 4096,), 0x5A, dtype=torch.uint8, device="cuda")
+    guard[:nb] = P.model_buf
+    P.model_buf = guard[:nb]                              # rebind the model inside the guarded buffer
+    P.model = C.cdmd_model_bind(P.model_buf, k, K, m)
+    g = gpu_run_pipeline(C, P, Xd, X, cfg.tau)
+    torch.cuda.synchronize()
+    assert bool((guard[nb:] == 0x5A).all()), "write past the model buffer"
+    o = oracle_run(X, cfg.kind, cfg.p, k, K, cfg.tau, omega_eps=eps, Y=Y)
+    assert len(o["model"]["support"]) == K and g["model"]["K_eff"] == K
+    check_all(g, o, cfg.kind, cfg.tau)
+
+
+def gpu_run_pipeline(C, P, Xd, X, tau):
+    """gpu_run on an existing Pipeline (same outputs)."""
+    m, n = X.shape
+    Y = P.sketch(Xd).cpu().numpy().T.copy()
+    P.fit()
+    out = dict(Y=Y, model=C.model_to_host(P.model), Phi=P.modes(Xd).cpu().numpy())
+    for mode, name in ((C.BG_DYNAMIC, "dyn"), (C.BG_STATIC, "sta")):
+        out["mask_" + name] = OD.unpack_mask(P.foreground(Xd, tau, mode).cpu().numpy().view(np.uint32), n)
+        out["L_" + name] = P.background(mode).cpu().numpy()
+    return out
+
+
+def test_sparse_plan_check_refused_inside_graph_capture(C):
+    """The first sketch of a new sparse plan checks the index lists once with a stream
+    sync; inside a CUDA graph capture that is refused (CDMD_ERR_ARG) instead of silently
+    skipped, and after one eager call the same plan captures fine."""
+    H2 = C.Handle(0)
+    X = make_video(64, 48, 12, seed=2, noise=1.0, n_rects=1)
+    m, n = X.shape
+    Xd = to_dev(X)
+    P = C.Pipeline(H2, n, n, m, "sparse", 40, 4, 2, seed=77)
+    s = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with pytest.raises(C.CdmdError) as e:
+        with torch.cuda.graph(g, stream=s):
+            P.sketch(Xd, s)
+    assert e.value.code == 1
+    torch.cuda.synchronize()
+    P.sketch(Xd)
+    want = P.Y.clone()
+    P.Y.zero_()
+    g2 = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g2, stream=s):
+        P.sketch(Xd, s)
+    g2.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(P.Y, want)
+
+
 @pytest.mark.parametrize("W,Hh,m,dens", [(37, 23, 5, 0.35), (64, 16, 3, 0.5), (720, 480, 4, 0.1), (5, 3, 2, 0.6),
                                          (33, 1, 2, 0.5), (1, 40, 2, 0.5)])
 def test_mask_median3_bit_exact(C, W, Hh, m, dens):
@@ -618,10 +749,11 @@ def test_streaming_sm_partition_equal_sequential(tmp_path):
     assert "partition ok" in r.stdout
 
 
-_SHARDED_FIT_SCRIPT = r"""
-import os, sys, torch
+_SHARDED_SCRIPT = r"""
+import os, sys, numpy as np, torch
 import torch.distributed as dist
 sys.path.insert(0, sys.argv[1])
+out_dir = sys.argv[2]
 rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
 dist.init_process_group("gloo", rank=rank, world_size=world)
 from paper_1512_04205_b200 import cdmd as C
@@ -634,45 +766,72 @@ Xs = make_video(W, H, m, seed=11, noise=2.0, n_rects=2, pix0=pix0, n_local=nl)
 ld = ((nl + 15) // 16) * 16
 X0 = torch.zeros((m, ld), dtype=torch.uint8, device="cuda")
 X0[:, :nl] = torch.from_numpy(Xs).cuda()
-vids = [X0, X0.flip(0).contiguous(), X0.roll(5, dims=0).contiguous(), X0.roll(-9, dims=0).contiguous(),
-        X0.roll(17, dims=0).contiguous()]
+shifts = [0, 5, -9]                      # batch b = the video rolled by shifts[b] frames
+vids = [X0.roll(sh, dims=0).contiguous() for sh in shifts]
 ar = lambda Y: dist.all_reduce(Y, op=dist.ReduceOp.SUM)
-out = {}
-for shard in (True, False):
-    S = C.Streaming(0, n, nl, m, "sparse", p, k, K, lanes=2, pix0=pix0, shard_fit=shard)
-    assert S.shard_fit == shard
-    ends = S.run(vids, tau, C.BG_DYNAMIC, allreduce=ar)
-    for e in ends:
-        torch.cuda.current_stream().wait_event(e)
-    torch.cuda.synchronize()
-    out[shard] = [(pipe.Y.clone(), pipe.Phi.clone(), pipe.mask.clone(), pipe.model.k_eff, pipe.model.K_eff,
-                   pipe.model.n_coef) for (_, _, _, pipe) in S.lanes]
-for a, b in zip(out[True], out[False]):
-    assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1]) and torch.equal(a[2], b[2]), rank
-    assert a[3:] == b[3:], (a[3:], b[3:])
+S = C.Streaming(0, n, nl, m, "sparse", p, k, K, lanes=3, pix0=pix0)
+ends = S.run(vids, tau, C.BG_DYNAMIC, allreduce=ar)
+for e in ends:
+    torch.cuda.current_stream().wait_event(e)
+torch.cuda.synchronize()
+res = {}
+for b, (_, _, _, pipe) in enumerate(S.lanes):      # lane b ran batch b (3 lanes, 3 batches)
+    mh = C.model_to_host(pipe.model)
+    res[f"Y{b}"] = pipe.Y.cpu().numpy()
+    res[f"Phi{b}"] = pipe.Phi[:pipe.model.k_eff].cpu().numpy()
+    res[f"mask{b}"] = pipe.mask.cpu().numpy()
+    for key in ("lam", "sigma", "pair", "support"):
+        res[f"{key}{b}"] = np.asarray(mh[key])
+np.savez(os.path.join(out_dir, f"rank{rank}.npz"), pix0=pix0, nl=nl, **res)
 dist.barrier()
 dist.destroy_process_group()
-sys.stdout.write(f"sharded ok {rank}\n")   # one write: lines of the two ranks do not interleave
+sys.stdout.write(f"sharded ok {rank}\n")
 sys.stdout.flush()
 """
 
 
-def test_streaming_sharded_fits_equal_replicated(tmp_path):
-    """Two ranks (gloo, both on cuda:0: host-mediated collectives, no kernel waits on
-    another rank's): with sharded fits each batch is solved on rank b mod 2 and its
-    model broadcast; sketches, modes, masks and model sizes equal the replicated-fit
-    run bit for bit on both ranks."""
+def test_two_rank_sharded_path_equals_single_process_oracle(tmp_path):
+    """The pixel-row-sharded path through libcdmd on two ranks
+    (gloo, both on cuda:0: host-mediated all-reduces, no kernel waits on another rank's):
+    each rank sketches its slab with C's global columns, the streaming lanes all-reduce
+    Y in batch order, every rank fits, and modes + masks of the two slabs, put side by
+    side, are compared with the SINGLE-PROCESS oracle on the whole video, per batch."""
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     script = tmp_path / "sharded_check.py"
-    script.write_text(_SHARDED_FIT_SCRIPT)
+    script.write_text(_SHARDED_SCRIPT)
     port = 29500 + (os.getpid() % 1000)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
-           "--master-addr=127.0.0.1", f"--master-port={port}", str(script), root]
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(script), root, str(tmp_path)]
     r = subprocess.run(cmd, cwd=root, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
-    assert "sharded ok 0" in r.stdout and "sharded ok 1" in r.stdout
+    R = [np.load(tmp_path / f"rank{q}.npz") for q in (0, 1)]
+    W, Hh, m, p, k, K, tau = 640, 360, 120, 600, 20, 6, 25.0
+    X = make_video(W, Hh, m, seed=11, noise=2.0, n_rects=2)
+    n = X.shape[1]
+    assert int(R[0]["pix0"]) == 0 and int(R[0]["nl"]) + int(R[1]["nl"]) == n
+    for b, sh in enumerate([0, 5, -9]):
+        Xb = np.roll(X, sh, axis=0)
+        Yo = OS.sketch(Xb, OS.SPARSE, p, 0)
+        om = OD.fit(Yo, k, K)
+        Phi_o = OD.modes(Xb, om["M"])
+        L = OD.background_dynamic(Phi_o, om)
+        res = np.abs(Xb.astype(np.float64) - L.T)
+        for q in (0, 1):   # every rank holds the same all-reduced Y and the same model
+            assert np.array_equal(R[q][f"Y{b}"].T.astype(np.int64), Yo), (b, q)
+            assert list(R[q][f"pair{b}"]) == list(R[0][f"pair{b}"])
+            assert np.array_equal(R[q][f"lam{b}"], R[0][f"lam{b}"])
+        lam_g = R[0][f"lam{b}"]
+        perm, err = PT.match_eigs(lam_g, om["lam"])
+        assert err <= PT.RTOL_EIG and len(lam_g) == om["k_eff"]
+        assert PT.supports_equal_mod_conj(list(R[0][f"support{b}"]), R[0][f"pair{b}"], perm, om["support"], om["pair"])
+        Phi_g = np.concatenate([R[q][f"Phi{b}"][:, :int(R[q]["nl"])] for q in (0, 1)], axis=1)
+        worst = _phi_columns_parity(PT.unfold(Phi_g, R[0][f"pair{b}"]), Phi_o, perm, om["lam"], len(lam_g))
+        assert worst <= PT.RTOL_PHI, (b, worst)
+        mg = np.concatenate([OD.unpack_mask(R[q][f"mask{b}"].view(np.uint32), int(R[q]["nl"])) for q in (0, 1)], axis=1)
+        frac, band, nd = PT.mask_agreement(mg, res > tau, res, tau)
+        assert frac >= PT.MASK_AGREE and band, (b, frac, nd)
 
 
 # ------------------------------------------- amplitudes b = lstsq(Phi, x_1) (P:348)
@@ -706,15 +865,13 @@ def test_amplitudes_parity(C, H, case):
     mh = C.model_to_host(P.model)
     b = b.cpu().numpy()
     assert int(dropped.item()) == 0
-    # (1) step 9 alone: the oracle's lstsq on the GPU's own modes (same input).  The
-    # Gram sums fp32 products in fp32 over <= 128 terms per tile (relative error
-    # <= 128 * 2^-24 ~ 8e-6 of the tile's sum of |terms|, fp64 across tiles), and b
-    # inherits cond(F^T F) = cond(F)^2 of it.
+    # (1) step 9 alone: the oracle's lstsq on the GPU's own modes (same input), within
+    # north_star's 1e-4 relative for fp32-level quantities
     Phi_g = PT.unfold(F.cpu().numpy(), mh["pair"])
     b_o = OD.amplitudes(X, Phi_g)
     cond = np.linalg.cond(Phi_g)
     err1 = np.linalg.norm(b - b_o) / np.linalg.norm(b_o)
-    assert err1 <= 8e-6 * cond * cond, (err1, cond)
+    assert err1 <= PT.RTOL_PHI, (err1, cond)
     for j in np.nonzero(mh["pair"] == 1)[0]:
         assert b[j + 1] == np.conj(b[j])
     # (2) end to end against the oracle's modes: per-mode contributions b_j phi_j
@@ -780,13 +937,29 @@ def test_amplitudes_c4_full_size(C, H):
     b, dropped = P.amplitudes(Xd)
     torch.cuda.synchronize()
     assert int(dropped.item()) == 0
-    pair = C.model_to_host(P.model)["pair"]
-    Phi_g = PT.unfold(F.cpu().numpy(), pair)
+    mh = C.model_to_host(P.model)
+    Phi_g = PT.unfold(F.cpu().numpy(), mh["pair"])
     del F
+    b = b.cpu().numpy()
     b_o = OD.amplitudes(X, Phi_g)
-    cond = np.linalg.cond(Phi_g)
-    err = np.linalg.norm(b.cpu().numpy() - b_o) / np.linalg.norm(b_o)
-    assert err <= 8e-6 * cond * cond, (err, cond)
+    err = np.linalg.norm(b - b_o) / np.linalg.norm(b_o)
+    assert err <= PT.RTOL_PHI, err
+    # end to end: per-mode contributions b_j phi_j against the oracle's own modes and
+    # amplitudes (full frame, the oracle's modes fanned over pixel slabs)
+    from oracle.runner import PixelPool
+    o = OD.fit(OS.sketch(X, OS.SPARSE, cfg.p, 0), cfg.k, cfg.K)
+    with PixelPool(cfg) as pool:
+        Phi_o = pool.run(o, cfg.tau, want=("Phi",))["Phi"]
+    bo = OD.amplitudes(X, Phi_o)
+    perm, werr = PT.match_eigs(mh["lam"], o["lam"])
+    assert werr <= PT.RTOL_EIG
+    x1 = np.linalg.norm(X[0].astype(np.float64))
+    worst = 0.0
+    for i, j in enumerate(perm):
+        if PT.well_separated(o["lam"], j, 1e-3):
+            worst = max(worst, np.linalg.norm(b[i] * Phi_g[:, i] - bo[j] * Phi_o[:, j]) / x1)
+    print(f"c4 amplitudes: step9_rel={err:.2e} contrib={worst:.2e}")
+    assert worst <= PT.RTOL_PHI
 
 
 def test_amplitudes_static_video_single_mode(C, H):
@@ -807,3 +980,24 @@ def test_amplitudes_static_video_single_mode(C, H):
     assert int(dropped.item()) == 0
     rec = (F.cpu().numpy().astype(np.float64)[0] * b.cpu().numpy()[0]).real
     assert np.max(np.abs(rec - frame)) <= 1e-4 * 255
+
+
+@pytest.mark.parametrize("tool,cases", [("memcheck", ["c1", "ragged_sparse", "ragged_spixel", "rademacher", "gaussian"]),
+                                        ("synccheck", ["c1", "ragged_sparse", "gaussian"]),
+                                        ("initcheck", ["c1", "ragged_sparse"]),
+                                        ("racecheck", ["c1"])])
+def test_compute_sanitizer(tool, cases):
+    """compute-sanitizer over libcdmd's own kernels (kernel names in namespace cdmd; the
+    cuBLAS kernels of the fit are library code) on C1 and the ragged cases: no errors."""
+    import shutil
+    import subprocess
+    import sys
+    cs = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
+    if not os.path.exists(cs):
+        pytest.skip("compute-sanitizer not installed")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [cs, "--tool", tool, "--kernel-regex", "kns=cdmd", "--error-exitcode", "9",
+           sys.executable, os.path.join(root, "tools", "sanitize_cases.py"), *cases]
+    r = subprocess.run(cmd, cwd=root, capture_output=True, text=True, timeout=900)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0 and "cases ok" in out and "ERROR SUMMARY: 0 errors" in out, out[-6000:]

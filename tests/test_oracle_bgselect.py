@@ -66,3 +66,18 @@ def test_decaying_mode_joins_above_its_rate():
     assert len(mdl["support"]) == 2                               # static + decay, not the pair
     bg = (mdl["PhiY"][:, mdl["support"]] @ mdl["beta"]).real
     assert np.allclose(bg, static[:, 0] + decay[:, 0], atol=1e-9)
+
+
+def test_selection_is_capped_at_K():
+    # reading R24: at most K background modes (||beta||_0 <= K, as for OMP); with every
+    # planted frequency below eps and K = 2 the first two selected modes in mode order are
+    # kept and their amplitudes are the least-squares fit of y1 on those two alone
+    static, decay, osc = _planted(orth=False, seed=3)
+    Y = static + decay + osc
+    full = fit(Y, 4, 4, omega_eps=1.0)
+    capped = fit(Y, 4, 2, omega_eps=1.0)
+    assert capped["support"] == full["support"][:2]
+    D = capped["PhiY"][:, capped["support"]]
+    y1 = Y[:, 0]
+    r = y1 - D @ capped["beta"]
+    assert np.linalg.norm(D.conj().T @ r) < 1e-9 * np.linalg.norm(D) * np.linalg.norm(y1)

@@ -15,6 +15,55 @@ def test_omega_cubic_values():
     assert OD.omega_beta(b) == pytest.approx(0.56 * b**3 - 0.95 * b**2 + 1.82 * b + 1.43, abs=1e-15)
 
 
+def _mp_density(beta):
+    """Marchenko-Pastur density of the squared singular values of an i.i.d. noise matrix
+    with aspect ratio beta and unit entry variance (scaled by the long side)."""
+    lo, hi = (1 - np.sqrt(beta)) ** 2, (1 + np.sqrt(beta)) ** 2
+    return lo, hi, lambda x: np.sqrt(max((hi - x) * (x - lo), 0.0)) / (2 * np.pi * beta * x)
+
+
+def _mp_median(beta):
+    from scipy import integrate, optimize
+    lo, hi, f = _mp_density(beta)
+    return optimize.brentq(lambda mu: integrate.quad(f, lo, mu, limit=200)[0] - 0.5, lo + 1e-12, hi)
+
+
+def _lambda_star(beta):
+    """Gavish-Donoho optimal hard threshold for KNOWN noise level, in units of sqrt(n) sigma."""
+    return np.sqrt(2 * (beta + 1) + 8 * beta / ((beta + 1) + np.sqrt(beta * beta + 14 * beta + 1)))
+
+
+def test_mp_density_is_a_distribution():
+    # sanity of the numerical Marchenko-Pastur law used below: total mass 1, mean 1
+    from scipy import integrate
+    for beta in (0.1, 0.5, 1.0):
+        lo, hi, f = _mp_density(beta)
+        assert integrate.quad(f, lo, hi, limit=200)[0] == pytest.approx(1.0, abs=1e-7)
+        assert integrate.quad(lambda x: x * f(x), lo, hi, limit=200)[0] == pytest.approx(1.0, abs=1e-7)
+
+
+def test_omega_cubic_matches_the_exact_unknown_noise_coefficient():
+    """Remark 2 / evaluation settings use the unknown-noise rule
+    tau = omega(beta) median(sigma).  Its exact coefficient is
+    omega(beta) = lambda*(beta) / sqrt(mu_beta), mu_beta the Marchenko-Pastur median
+    (Gavish & Donoho 2014); the cubic 0.56 b^3 - 0.95 b^2 + 1.82 b + 1.43 is their fit
+    to it.  Pinned against the exact value within 1e-2 for beta in [0.05, 1] (measured
+    worst 5.7e-3 at beta = 0.1): a wrong sign or coefficient of any term moves it by
+    more (e.g. +0.95 b^2 gives 4.76 at beta = 1)."""
+    for beta in (0.05, 0.1, 0.25, 0.5, 0.75, 1.0):
+        exact = _lambda_star(beta) / np.sqrt(_mp_median(beta))
+        assert abs(OD.omega_beta(beta) - exact) <= 1e-2, (beta, OD.omega_beta(beta), exact)
+    # the two ingredients pinned on their own: lambda*(1) = 4 / sqrt(3) (closed form), and
+    # mu_beta against the empirical median of the squared singular values of an i.i.d.
+    # N(0, 1/n) matrix (Monte Carlo, 2000 x 2000 and 500 x 2000)
+    assert _lambda_star(1.0) == pytest.approx(4 / np.sqrt(3), abs=1e-12)
+    rng = np.random.default_rng(0)
+    for rows, beta in ((2000, 1.0), (500, 0.25)):
+        Z = rng.standard_normal((rows, 2000)) / np.sqrt(2000)
+        emp = np.median(np.linalg.svd(Z, compute_uv=False) ** 2)
+        assert _mp_median(beta) == pytest.approx(emp, abs=4e-3), (beta, emp)
+
+
 def test_one_dominant_value():
     assert OD.optimal_rank([10.0, 1e-12, 1e-13], 100, 99) == 1
 
