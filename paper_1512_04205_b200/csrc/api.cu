@@ -343,13 +343,18 @@ cdmd_status cdmd_background(cdmd_handle h, const float* Phi, int64_t ldphi, int6
 cdmd_status cdmd_foreground(cdmd_handle h, const cdmd_video* v, const cdmd_model* M,
                             const float* Phi, int64_t ldphi, int32_t mode, float tau,
                             uint32_t* mask, int64_t ldw, cdmd_stream st) {
-  if (!h || !mask || !Phi) return CDMD_ERR_ARG;
+  if (!h || !mask) return CDMD_ERR_ARG;
   if (mode != CDMD_BG_STATIC && mode != CDMD_BG_DYNAMIC) return CDMD_ERR_ARG;
   cdmd_status s = check_video(v);
   if (s != CDMD_OK) return s;
   if ((s = check_model(M, v->m)) != CDMD_OK) return s;
   if (!(tau > 0.0f)) return CDMD_ERR_RANGE;
-  if (ldphi < v->n_local || ldw < ceil_div(v->n_local, 32)) return CDMD_ERR_ARG;
+  if (ldw < ceil_div(v->n_local, 32)) return CDMD_ERR_ARG;
+  if (!Phi) {   // N11: the support's modes computed in-slab from X (fused_tc.cu)
+    if (!fused_supported(*v, *M, mode)) return CDMD_ERR_UNSUPPORTED;
+    return cuda_status(launch_fused_fg(*v, *M, tau, mask, ldw, sched_slot(h), (cudaStream_t)st));
+  }
+  if (ldphi < v->n_local) return CDMD_ERR_ARG;
   return cuda_status(launch_foreground(*v, *M, Phi, ldphi, mode, tau, mask, ldw, sched_slot(h), (cudaStream_t)st));
 }
 

@@ -27,9 +27,8 @@ namespace cdmd {
 constexpr int FG_BN = 256;          // pixels per tile (UMMA N, TMEM columns per buffer)
 constexpr int FG_BM = 128;          // frames per unit (UMMA M, TMEM lanes)
 constexpr int FG_XSTAGE = FG_BM * FG_BN;   // bytes of X per unit (two 128x128 SW128 boxes)
-constexpr int FG_FSPLIT = 4;        // pixel slices per unit (per TMEM lane quarter)
-constexpr int FG_EPI_WARPS = 4 * FG_FSPLIT;
-constexpr int FG_PW = FG_BN / FG_FSPLIT;   // pixels per epilogue warp per unit
+// epilogue warps EW (template): 4 TMEM lane quarters x EW/4 pixel slices of 1024/EW
+// pixels; each thread builds 1024/EW/32 mask words per unit
 #ifdef CDMD_ABLATIONS
 #define FG_ABL(x) (x)
 #else
@@ -105,13 +104,16 @@ __device__ __forceinline__ uint32_t mask32(const uint32_t (&xw)[8], const uint32
   return ~word;
 }
 
-template <int KP>
-__global__ void __launch_bounds__(32 * (2 + FG_EPI_WARPS), 1) foreground_tc_kernel(
+template <int KP, int EW>
+__global__ void __launch_bounds__(32 * (2 + EW), 1) foreground_tc_kernel(
     const __grid_constant__ CUtensorMap mapX, int64_t n_local, int64_t m, int nfb,
     const float* __restrict__ Phi, int64_t ldphi, const float* __restrict__ coef,
     const int32_t* __restrict__ coef_col, int n_coef, float tau, uint32_t* __restrict__ mask,
     int64_t ldw, int num_tiles, int stages, int dbg, int* __restrict__ tile_counter) {
   constexpr int PART_B = FG_BN * KP * 2;  // bytes of one split part of Phi_F (B)
+  constexpr int FG_EPI_WARPS = EW;
+  constexpr int FG_PW = FG_BN / (EW / 4);  // pixels per epilogue warp per unit
+  constexpr int NW = FG_PW / 32;           // mask words per thread per unit
   extern __shared__ __align__(1024) uint8_t smem_raw[];   // 1024-B aligned: SWIZZLE_128B atoms
   uint8_t* smem = smem_raw;                                  // (keeps the shared address space visible)
   const int mA = nfb * FG_BM;
@@ -234,8 +236,8 @@ __global__ void __launch_bounds__(32 * (2 + FG_EPI_WARPS), 1) foreground_tc_kern
     // (consecutive threads own consecutive pixels: coalesced) and split into smem
     // when its buffer is free.
     const int br = etid & (FG_BN - 1);
-    const int bfh = etid >> 8;                    // which half of the KP columns
-    constexpr int BH = KP / 2;
+    const int bfh = etid >> 8;                    // which part of the KP columns
+    constexpr int BH = KP * FG_BN / (32 * EW);    // columns of Phi_F per thread
     float pv[BH];
     auto load_phi = [&](int tile) {
       const int64_t j = (int64_t)tile * FG_BN + br;
@@ -300,13 +302,17 @@ __global__ void __launch_bounds__(32 * (2 + FG_EPI_WARPS), 1) foreground_tc_kern
         const uint8_t* xs = sX + (size_t)stage * FG_XSTAGE;
         const uint32_t ta = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(tb * FG_BN);
         const int64_t t = (int64_t)fb * FG_BM + r;
-        uint32_t words[FG_PW / 32];
+        uint32_t words[NW];
+        // TMEM loads of word w + 1 in flight while word w is built (tcgen05.wait::ld
+        // waits for all of this thread's loads, so it is issued before the arithmetic)
+        uint32_t La[32], Lb[32];
+        tc::tmem_ld16(ta + sl * FG_PW, *reinterpret_cast<uint32_t(*)[16]>(&La[0]));
+        tc::tmem_ld16(ta + sl * FG_PW + 16, *reinterpret_cast<uint32_t(*)[16]>(&La[16]));
 #pragma unroll
-        for (int w = 0; w < FG_PW / 32; ++w) {
+        for (int w = 0; w < NW; ++w) {
           const int j0 = sl * FG_PW + 32 * w;       // pixel offset in the tile
-          uint32_t L[32];
-          tc::tmem_ld16(ta + j0, *reinterpret_cast<uint32_t(*)[16]>(&L[0]));
-          tc::tmem_ld16(ta + j0 + 16, *reinterpret_cast<uint32_t(*)[16]>(&L[16]));
+          uint32_t (&L)[32] = (w & 1) ? Lb : La;
+          uint32_t (&Ln)[32] = (w & 1) ? La : Lb;
           // pixels j0..j0+31 of frame r: box j0/128, 16-B chunks c, c+1 XOR-swizzled by r%8
           const uint8_t* row = xs + (j0 >> 7) * (FG_XSTAGE / 2) + r * 128;
           const int c = (j0 & 127) >> 4;
@@ -314,6 +320,10 @@ __global__ void __launch_bounds__(32 * (2 + FG_EPI_WARPS), 1) foreground_tc_kern
           const uint4 b = *reinterpret_cast<const uint4*>(row + (((c + 1) ^ (r & 7)) << 4));
           const uint32_t xw[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
           tc::tmem_ld_wait();
+          if (w + 1 < NW) {
+            tc::tmem_ld16(ta + j0 + 32, *reinterpret_cast<uint32_t(*)[16]>(&Ln[0]));
+            tc::tmem_ld16(ta + j0 + 48, *reinterpret_cast<uint32_t(*)[16]>(&Ln[16]));
+          }
           words[w] = FG_ABL(dbg & 1) ? 0u : mask32(xw, L, tau);
         }
         // the stage goes back only after the words are built: the shared loads have
@@ -329,15 +339,12 @@ __global__ void __launch_bounds__(32 * (2 + FG_EPI_WARPS), 1) foreground_tc_kern
         const int64_t w0 = ((int64_t)tile * FG_BN + sl * FG_PW) >> 5;   // first mask word
         if (t < m) {
           uint32_t* dst = mask + t * ldw + w0;
-          if (32 * (w0 + 1) < n_local) {          // both words hold pixels of the slab
-            if ((ldw & 1) == 0) {
-              *reinterpret_cast<uint2*>(dst) = make_uint2(words[0], words[1]);
-            } else {
-              dst[0] = words[0];
-              dst[1] = words[1];
-            }
-          } else if (32 * w0 < n_local) {
-            dst[0] = words[0];
+          if (32 * (w0 + NW) <= n_local + 31 && 32 * (w0 + NW - 1) < n_local && (ldw & 3) == 0 && NW == 4) {
+            *reinterpret_cast<uint4*>(dst) = make_uint4(words[0], words[1 % NW], words[2 % NW], words[3 % NW]);
+          } else {
+#pragma unroll
+            for (int w = 0; w < NW; ++w)
+              if (32 * (w0 + w) < n_local) dst[w] = words[w];
           }
         }
       }
@@ -390,7 +397,7 @@ bool foreground_tc_supported(const cdmd_video& v, const cdmd_model& M) {
   return fg_smem_bytes(KP, nfb, 2) <= 226 * 1024 && (v.ld % 16) == 0;   // 1 KB: static smem
 }
 
-template <int KP>
+template <int KP, int EW>
 static cudaError_t launch_kp(const cdmd_video& v, const cdmd_model& M, const float* Phi, int64_t ldphi,
                              float tau, uint32_t* mask, int64_t ldw, int* tile_counter, cudaStream_t st) {
   const int nfb = (int)ceil_div(v.m, FG_BM);
@@ -408,7 +415,7 @@ static cudaError_t launch_kp(const cdmd_video& v, const cdmd_model& M, const flo
   if (const char* e = getenv("CDMD_FG_STAGES")) { const int q = atoi(e); if (q >= 2 && q <= 4) stages = q; }
   while (stages > 2 && fg_smem_bytes(KP, nfb, stages) > 226 * 1024) --stages;
   const size_t smem = fg_smem_bytes(KP, nfb, stages);
-  cudaError_t e = cudaFuncSetAttribute(foreground_tc_kernel<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = cudaFuncSetAttribute(foreground_tc_kernel<KP, EW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -419,7 +426,7 @@ static cudaError_t launch_kp(const cdmd_video& v, const cdmd_model& M, const flo
   e = cudaMemsetAsync(tile_counter, 0, sizeof(int), st);
   if (e != cudaSuccess) return e;
   note_launch();
-  foreground_tc_kernel<KP><<<grid, 32 * (2 + FG_EPI_WARPS), smem, st>>>(
+  foreground_tc_kernel<KP, EW><<<grid, 32 * (2 + EW), smem, st>>>(
       mapX, v.n_local, v.m, nfb, Phi, ldphi, M.coef, M.coef_col, M.n_coef, tau, mask, ldw, num_tiles, stages, dbg_mode(),
       tile_counter);
   return cudaGetLastError();
@@ -427,8 +434,16 @@ static cudaError_t launch_kp(const cdmd_video& v, const cdmd_model& M, const flo
 
 cudaError_t launch_foreground_tc(const cdmd_video& v, const cdmd_model& M, const float* Phi, int64_t ldphi,
                                  float tau, uint32_t* mask, int64_t ldw, int* tile_counter, cudaStream_t st) {
-  if (fg_kp(M.n_coef) == 16) return launch_kp<16>(v, M, Phi, ldphi, tau, mask, ldw, tile_counter, st);
-  return launch_kp<32>(v, M, Phi, ldphi, tau, mask, ldw, tile_counter, st);
+  static int ew = -1;
+  if (ew < 0) {   // epilogue warps (CDMD_FG_EW = 8 or 16; measured in DESIGN.md §5.4)
+    const char* e = getenv("CDMD_FG_EW");
+    ew = (e && atoi(e) == 16) ? 16 : 8;
+  }
+  if (fg_kp(M.n_coef) == 16)
+    return ew == 16 ? launch_kp<16, 16>(v, M, Phi, ldphi, tau, mask, ldw, tile_counter, st)
+                    : launch_kp<16, 8>(v, M, Phi, ldphi, tau, mask, ldw, tile_counter, st);
+  return ew == 16 ? launch_kp<32, 16>(v, M, Phi, ldphi, tau, mask, ldw, tile_counter, st)
+                  : launch_kp<32, 8>(v, M, Phi, ldphi, tau, mask, ldw, tile_counter, st);
 }
 
 }  // namespace cdmd

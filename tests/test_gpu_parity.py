@@ -55,9 +55,23 @@ def gpu_run(C, H, X, kind, p, k, K, tau, s=0.0, seed=0, modes_simt=False, ld=Non
         Wd = P.foreground(Xd, tau, mode).cpu().numpy().view(np.uint32)
         out["mask_" + name] = OD.unpack_mask(Wd, n)
         out["L_" + name] = P.background(mode).cpu().numpy()   # (m, n) frame-major
+    fused = fused_mask(C, P, Xd, tau)
+    if fused is not None:
+        out["mask_fus"] = OD.unpack_mask(fused, n)
     torch.cuda.synchronize()
     out["P"], out["Xd"] = P, Xd
     return out
+
+
+def fused_mask(C, P, Xd, tau):
+    """The fused single pass N11 (cdmd_foreground with Phi = NULL): packed mask words, or
+    None where it is not supported (CDMD_ERR_UNSUPPORTED: n_coef > 16 or m > 512)."""
+    try:
+        return P.foreground(Xd, tau, C.BG_DYNAMIC, fused=True).cpu().numpy().view(np.uint32).copy()
+    except C.CdmdError as e:
+        if e.code == 6:
+            return None
+        raise
 
 
 def oracle_run(X, kind, p, k, K, tau, s=None, seed=0, rank="fixed", omega_eps=None, Y=None):
@@ -102,9 +116,11 @@ def check_all(g, o, kind, tau):
     scale = max(1.0, np.abs(o["L_dyn"]).max())
     assert np.abs(g["L_dyn"] - o["L_dyn"]).max() <= 1e-4 * scale
     assert np.abs(g["L_sta"][0] - o["L_sta"]).max() <= 1e-4 * scale
-    # masks
-    for name in ("dyn", "sta"):
-        frac, band, nd = PT.mask_agreement(g["mask_" + name], o["mask_" + name], o["res_" + name], tau)
+    # masks (the fused single pass against the oracle's dynamic mask)
+    for name, ref in (("dyn", "dyn"), ("sta", "sta"), ("fus", "dyn")):
+        if "mask_" + name not in g:
+            continue
+        frac, band, nd = PT.mask_agreement(g["mask_" + name], o["mask_" + ref], o["res_" + ref], tau)
         assert frac >= PT.MASK_AGREE and band, (name, frac, nd)
 
 
@@ -313,6 +329,16 @@ def test_c4_sparse_full_size(C, H):
     assert worst <= PT.RTOL_PHI, worst
     frac, outside, nd = _full_frame_mask_parity(mask, n, ref["mask"], ref["band"])
     print(f"c4 sparse full frame: phi worst {worst:.2e}, mask agreement {frac:.7f} ({nd} px, {outside} outside band)")
+    assert frac >= PT.MASK_AGREE and outside == 0, (frac, nd, outside)
+    # N11: the fused single pass (no cdmd_modes call) on the same model, every pixel
+    Xd = to_dev(X)
+    fm = fused_mask(C, P, Xd, cfg.tau)
+    torch.cuda.synchronize()
+    assert fm is not None, "fused path unsupported at the bench configuration"
+    frac, outside, nd = _full_frame_mask_parity(fm, n, ref["mask"], ref["band"])
+    same = float((fm == mask).mean())
+    print(f"c4 sparse fused: mask agreement {frac:.7f} ({nd} px, {outside} outside band), "
+          f"words equal to the two-pass mask {same:.7f}")
     assert frac >= PT.MASK_AGREE and outside == 0, (frac, nd, outside)
 
 
@@ -982,22 +1008,101 @@ def test_amplitudes_static_video_single_mode(C, H):
     assert np.max(np.abs(rec - frame)) <= 1e-4 * 255
 
 
-@pytest.mark.parametrize("tool,cases", [("memcheck", ["c1", "ragged_sparse", "ragged_spixel", "rademacher", "gaussian"]),
-                                        ("synccheck", ["c1", "ragged_sparse", "gaussian"]),
-                                        ("initcheck", ["c1", "ragged_sparse"]),
-                                        ("racecheck", ["c1"])])
-def test_compute_sanitizer(tool, cases):
-    """compute-sanitizer over libcdmd's own kernels (kernel names in namespace cdmd; the
-    cuBLAS kernels of the fit are library code) on C1 and the ragged cases: no errors."""
-    import shutil
-    import subprocess
-    import sys
-    cs = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
-    if not os.path.exists(cs):
-        pytest.skip("compute-sanitizer not installed")
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    cmd = [cs, "--tool", tool, "--kernel-regex", "kns=cdmd", "--error-exitcode", "9",
-           sys.executable, os.path.join(root, "tools", "sanitize_cases.py"), *cases]
-    r = subprocess.run(cmd, cwd=root, capture_output=True, text=True, timeout=900)
-    out = r.stdout + r.stderr
-    assert r.returncode == 0 and "cases ok" in out and "ERROR SUMMARY: 0 errors" in out, out[-6000:]
+GUARD = 4096
+_CANARY = 0xA5
+
+
+def _guarded(shape, dtype):
+    """A tensor in the middle of a buffer with GUARD canary bytes on both sides."""
+    nb = int(np.prod(shape)) * torch.tensor([], dtype=dtype).element_size()
+    buf = torch.full((nb + 2 * GUARD,), _CANARY, dtype=torch.uint8, device="cuda")
+    return buf, buf[GUARD:GUARD + nb].view(dtype).view(shape)
+
+
+def _guards_intact(buf):
+    return bool((buf[:GUARD] == _CANARY).all()) and bool((buf[-GUARD:] == _CANARY).all())
+
+
+@pytest.mark.parametrize("case", ["c1", "ragged_sparse", "ragged_spixel", "rademacher", "gaussian"])
+def test_no_out_of_bounds_writes(C, H, case):
+    """compute-sanitizer is closed on this GPU pool, so out-of-bounds WRITES are caught
+    with canaries instead: every caller buffer of every entry point (Y, sketch and fit
+    workspaces, the model, Phi, L, the masks of all three foreground paths, the
+    amplitudes Gram / b) sits between 4 KB guard regions of 0xA5 that must be intact
+    after the whole path ran; small and ragged cases (n not a multiple of 128, odd m)."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location(
+        "sanitize_cases", os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                       "tools", "sanitize_cases.py"))
+    sc = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(sc)
+    mk, kind, p, k, K = sc.CASES[case]
+    X = mk()
+    m, n = X.shape
+    Xd = to_dev(X)
+    P = C.Pipeline(H, n, n, m, kind, p, k, K)
+    bufs = {}
+
+    def swap(name, attr, shape, dtype):
+        b, t = _guarded(shape, dtype)
+        bufs[name] = b
+        setattr(P, attr, t)
+
+    swap("Y", "Y", tuple(P.Y.shape), P.Y.dtype)
+    swap("ws_sketch", "ws_sketch", tuple(P.ws_sketch.shape), torch.uint8)
+    swap("ws_fit", "ws_fit", tuple(P.ws_fit.shape), torch.uint8)
+    swap("model", "model_buf", (P.model_buf.numel(),), torch.uint8)
+    # the model must start 256-B aligned: the guard (4096) keeps the alignment
+    P.model = C.cdmd_model_bind(P.model_buf, k, K, m)
+    swap("Phi", "Phi", tuple(P.Phi.shape), torch.float32)
+    swap("mask", "mask", tuple(P.mask.shape), torch.int32)
+    P.run(Xd, 25.0, C.BG_DYNAMIC)
+    P.foreground(Xd, 25.0, C.BG_STATIC)
+    fused_mask(C, P, Xd, 25.0)
+    bL, L = _guarded((m, n), torch.float32)
+    C.cdmd_background(H, P.Phi, n, P.model, C.BG_DYNAMIC, 0, m, L)
+    ke = P.model.k_eff
+    bG, G = _guarded((ke + 1, ke), torch.float64)
+    bw, ws = _guarded((C.cdmd_amplitudes_workspace_bytes(H, ke),), torch.uint8)
+    bb, b = _guarded((ke, 2), torch.float64)
+    C.cdmd_amplitudes_gram(H, C.video(Xd, n, 0, n), P.model, P.Phi, G, ws)
+    C.cdmd_amplitudes_solve(H, P.model, G, b)
+    torch.cuda.synchronize()
+    bufs.update(L=bL, G=bG, amp_ws=bw, b=bb)
+    bad = [name for name, buf in bufs.items() if not _guards_intact(buf)]
+    assert not bad, f"guard regions overwritten: {bad}"
+
+
+def test_repeatable_under_concurrency(C, H):
+    """A race in the persistent kernels' tile schedule or stage hand-offs shows up as
+    run-to-run differences: at the bench size, modes, the two-pass mask and the fused
+    mask are bit-identical over 12 repetitions, half of them issued from three streams
+    at once (different CTA start times and tile claims)."""
+    cfg = config_by_name("c4_1080p_sparse")
+    X = video_for(cfg)
+    m, n = X.shape
+    Xd = to_dev(X)
+    pipes = [C.Pipeline(H, n, n, m, "sparse", cfg.p, cfg.k, cfg.K) for _ in range(3)]
+    P0 = pipes[0]
+    P0.run(Xd, cfg.tau, C.BG_DYNAMIC)
+    ref = (P0.Phi.clone(), P0.mask.clone())
+    ref_f = P0.foreground(Xd, cfg.tau, C.BG_DYNAMIC, fused=True).clone()
+    for Pq in pipes[1:]:
+        Pq.sketch(Xd)
+        Pq.fit()
+    streams = [torch.cuda.Stream() for _ in range(3)]
+    torch.cuda.synchronize()
+    for rep in range(6):
+        for Pq, st in zip(pipes, streams):
+            with torch.cuda.stream(st):
+                Pq.modes(Xd, st)
+                Pq.foreground(Xd, cfg.tau, C.BG_DYNAMIC, st)
+        torch.cuda.synchronize()
+        for Pq in pipes:
+            assert torch.equal(Pq.Phi, ref[0]) and torch.equal(Pq.mask, ref[1]), rep
+        for Pq, st in zip(pipes, streams):
+            with torch.cuda.stream(st):
+                Pq.foreground(Xd, cfg.tau, C.BG_DYNAMIC, st, fused=True)
+        torch.cuda.synchronize()
+        for Pq in pipes:
+            assert torch.equal(Pq.mask, ref_f), rep
