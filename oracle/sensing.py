@@ -26,6 +26,13 @@ DESIGN.md §3 (they are ours, the paper fixes only the distributions):
   Gaussian     : c_ri = T[u16], u16 = 16-bit half (i mod 8) of
                  Philox(ctr=(i // 8, r, 0, 4)) (w0 low half is slot 0, w0 high
                  half slot 1, ...), T[j] = bf16_RNE(Phi^-1((j + 1/2) / 2^16))
+  SRFT         : C = R F D, realified (reading R25): p/2
+                 frequencies f_r = pi'(r) (the Feistel bijection of single pixel with
+                 tag 5), phases phi_i = 16-bit half (i mod 8) of Philox(ctr=(i // 8, 0,
+                 0, 6)) (D = exp(2 pi i phi / 2^16), uniform on the 2^16-th roots of
+                 unity); entry phase index q_ri = (phi_i - floor(2^16 ((f_r i) mod n) / n))
+                 mod 2^16; row r < p/2: fp16_RNE(cos(2 pi q / 2^16)) (Re), row p/2 + r:
+                 fp16_RNE(sin(2 pi q / 2^16)) (Im)
 
 Key = (seed & 0xffffffff, seed >> 32).  Columns are indexed by the GLOBAL pixel
 index, so slabs of a pixel-sharded video sum to the full sketch.
@@ -41,9 +48,10 @@ from scipy.special import ndtri
 
 from .philox import philox4x32_10, seed_key
 
-SPIXEL, SPARSE, RADEMACHER, GAUSSIAN = 0, 1, 2, 3
-KIND_NAMES = {SPIXEL: "spixel", SPARSE: "sparse", RADEMACHER: "rademacher", GAUSSIAN: "gaussian"}
-TAG = {SPIXEL: 1, SPARSE: 2, RADEMACHER: 3, GAUSSIAN: 4}
+SPIXEL, SPARSE, RADEMACHER, GAUSSIAN, SRFT = 0, 1, 2, 3, 4
+KIND_NAMES = {SPIXEL: "spixel", SPARSE: "sparse", RADEMACHER: "rademacher", GAUSSIAN: "gaussian", SRFT: "srft"}
+TAG = {SPIXEL: 1, SPARSE: 2, RADEMACHER: 3, GAUSSIAN: 4, SRFT: 5}
+TAG_SRFT_PHASE = 6
 FEISTEL_ROUNDS = 6
 
 
@@ -58,14 +66,25 @@ def _feistel_halfbits(n):
     return (bits + 1) // 2
 
 
-def _feistel_encrypt(x, h, k0, k1):
+def _feistel_encrypt(x, h, k0, k1, tag=TAG[SPIXEL]):
     mask = np.uint64((1 << h) - 1)
     L = x >> np.uint64(h)
     R = x & mask
     for i in range(FEISTEL_ROUNDS):
-        f = philox4x32_10(R, i, 0, TAG[SPIXEL], k0, k1)[0] & mask
+        f = philox4x32_10(R, i, 0, tag, k0, k1)[0] & mask
         L, R = R, L ^ f
     return (L << np.uint64(h)) | R
+
+
+def _feistel_perm(n, p, seed, tag):
+    k0, k1 = seed_key(seed)
+    h = _feistel_halfbits(n)
+    out = np.arange(p, dtype=np.uint64)
+    todo = np.ones(p, dtype=bool)
+    while todo.any():
+        out[todo] = _feistel_encrypt(out[todo], h, k0, k1, tag)
+        todo = out >= np.uint64(n)
+    return out.astype(np.int64)
 
 
 def spixel_rows(n, p, seed):
@@ -167,6 +186,53 @@ def gaussian_block(rows, cols, seed):
     return _GT[u16.astype(np.int64)]
 
 
+# ------------------------------------------------------------------------- SRFT
+def srft_freqs(n, nf, seed):
+    """R of C = R F D: nf distinct frequencies of [0, n), drawn without
+    replacement through the Feistel bijection (tag 5)."""
+    return _feistel_perm(n, nf, seed, TAG[SRFT])
+
+
+def srft_phases(cols, seed):
+    """D: phase indices phi_i in [0, 2^16) of the unit-circle diagonal,
+    d_i = exp(2 pi i phi_i / 2^16): the 16-bit half (i mod 8) of Philox(i // 8, 0, 0, 6)."""
+    k0, k1 = seed_key(seed)
+    cols = np.asarray(cols, dtype=np.uint64)
+    w = philox4x32_10(cols >> np.uint64(3), 0, 0, TAG_SRFT_PHASE, k0, k1)
+    slot = cols & np.uint64(7)
+    word = np.choose((slot >> np.uint64(1)).astype(np.int64), w)
+    return ((word >> (np.uint64(16) * (slot & np.uint64(1)))) & np.uint64(0xFFFF)).astype(np.int64)
+
+
+def srft_table():
+    """(cos, sin) of 2 pi j / 2^16, j = 0 .. 65535, rounded to fp16 (RNE), as fp64."""
+    j = np.arange(65536, dtype=np.float64)
+    ang = 2.0 * np.pi * j / 65536.0
+    return np.cos(ang).astype(np.float16).astype(np.float64), np.sin(ang).astype(np.float16).astype(np.float64)
+
+
+_ST = None
+
+
+def srft_block(rows, cols, seed, n, p):
+    """Dense rows of the realified SRFT (reading R25): C[r] = Re(R F D)[r] for r < p/2,
+    Im(R F D)[r - p/2] for r >= p/2, with F(f, i) = exp(-2 pi i f i / n) (the
+    "/m" of the garbled formula read as /n) and the phase quantised to 2^-16 turn."""
+    global _ST
+    if _ST is None:
+        _ST = srft_table()
+    if p % 2:
+        raise ValueError("SRFT needs an even p (p/2 complex measurements)")
+    rows = np.asarray(rows, dtype=np.int64)
+    cols = np.asarray(cols, dtype=np.int64)
+    f = srft_freqs(n, p // 2, seed)[rows % (p // 2)][:, None]           # frequency of each row
+    a = (f * cols[None, :]) % n                                         # (f i) mod n, < 2^23
+    b = (a * 65536) // n                                                # floor(2^16 a / n)
+    q = (srft_phases(cols, seed)[None, :] - b) % 65536
+    re = (rows < p // 2)[:, None]
+    return np.where(re, _ST[0][q], _ST[1][q])
+
+
 # ------------------------------------------------------------------ dense C
 def dense_C(kind, n, p, seed, s=None, rows=None):
     """Materialise C (or the given rows of it) — only for tiny n (brute-force pins)."""
@@ -188,6 +254,8 @@ def dense_C(kind, n, p, seed, s=None, rows=None):
         return rademacher_block(rows, np.arange(n), seed).astype(np.int64)
     if kind == GAUSSIAN:
         return gaussian_block(rows, np.arange(n), seed)
+    if kind == SRFT:
+        return srft_block(rows, np.arange(n), seed, n, p)
     raise ValueError(kind)
 
 
@@ -218,8 +286,12 @@ def sketch(X, kind, p, seed, s=None, n_total=None, pix0=0, rows=None, chunk=1 <<
             sel = (pos >= pix0) & (pos < pix0 + n_local)
             Y[a] = (X[:, pos[sel] - pix0].astype(np.int64) * sg[sel].astype(np.int64)).sum(axis=1)
         return Y
-    if kind in (RADEMACHER, GAUSSIAN):
-        block = rademacher_block if kind == RADEMACHER else gaussian_block
+    if kind in (RADEMACHER, GAUSSIAN, SRFT):
+        if kind == SRFT:
+            def block(r, c, sd):
+                return srft_block(r, c, sd, n, p)
+        else:
+            block = rademacher_block if kind == RADEMACHER else gaussian_block
         acc_t = np.int64 if kind == RADEMACHER else np.float64
         Y = np.zeros((len(rows), m), dtype=acc_t)
         for c0 in range(0, n_local, chunk):

@@ -158,6 +158,10 @@ void cdmd_destroy(cdmd_handle h) {
   if (h->gauss_table) cudaFree(h->gauss_table);
   if (h->host_info) cudaFreeHost(h->host_info);
   if (h->sched) cudaFree(h->sched);
+  for (auto& kv : h->sparse_csc) {
+    cudaFree(kv.second.pos);
+    cudaFree(kv.second.rs);
+  }
   delete h;
 }
 
@@ -225,13 +229,24 @@ cdmd_status cdmd_sketch(cdmd_handle h, const cdmd_video* v, const cdmd_sensing* 
       int32_t* ell = (int32_t*)ws;
       int32_t* counts = (int32_t*)((char*)ws + al256(sizeof(int32_t) * P.p * P.cap));
       int32_t* flags = (int32_t*)((char*)counts + al256(sizeof(int32_t) * P.p));
-      e = cudaMemsetAsync(flags, 0, 16, st);
-      if (e == cudaSuccess) e = launch_sparse_rows(P, ell, counts, flags, st);
-      if (e == cudaSuccess && !checked) {
-        const cdmd_status cs = check_sparse_once(h, P, c->seed, flags, st);
-        if (cs != CDMD_OK) return cs;
+      const bool sorted = sketch_sparse_sorted_supported(P.p) && !getenv("CDMD_SPARSE_ELL");
+      const SparseCsc* csc = nullptr;
+      if (sorted && checked) {   // the cached pixel-sorted C: no per-call index generation
+        csc = sparse_csc_get(h, P, c->seed, nullptr, nullptr, st, &e);
       }
-      if (e == cudaSuccess) e = launch_sketch_sparse(*v, P, ell, counts, (int32_t*)Y, ldy, st);
+      if (!csc) {
+        e = cudaMemsetAsync(flags, 0, 16, st);
+        if (e == cudaSuccess) e = launch_sparse_rows(P, ell, counts, flags, st);
+        if (e == cudaSuccess && !checked) {
+          const cdmd_status cs = check_sparse_once(h, P, c->seed, flags, st);
+          if (cs != CDMD_OK) return cs;
+        }
+        if (e == cudaSuccess && sorted) csc = sparse_csc_get(h, P, c->seed, ell, counts, st, &e);
+      }
+      if (e == cudaSuccess) {
+        if (csc) e = launch_sketch_sparse_sorted(*v, P, csc->pos, csc->rs, csc->nent, (int32_t*)Y, ldy, st);
+        else e = launch_sketch_sparse(*v, P, ell, counts, (int32_t*)Y, ldy, st);
+      }
       break;
     }
     case CDMD_RADEMACHER:

@@ -22,7 +22,7 @@
 // X is read from HBM once; the full Phi is never written (Alg. 1's Phi output is
 // cdmd_modes' job).  The X stages of a tile stay resident from phase A to the mask,
 // two tiles in flight (8 stages of 16 KB at m <= 512).  Warp roles: 0 TMA producer,
-// 1 TMEM owner + MMA issuer (A of tile i, then B of tile i-1), 4-7 convert, 8-15 mask.
+// 1 TMEM owner + MMA issuer (A of tile i, then B of tile i-1), 2-5 convert, 6-13 mask.
 #include <cuda_bf16.h>
 #include <cudaTypedefs.h>
 
@@ -39,8 +39,8 @@ constexpr int FU_NA = CDMD_LIMBS * FU_NC;  // phase A N
 constexpr int FU_MASK_WARPS = 8;         // 4 TMEM lane quarters x 2 slices of 64 pixels
 constexpr int FU_PW = FU_BM / (FU_MASK_WARPS / 4);   // pixels per mask warp
 constexpr int FU_NW = FU_PW / 32;          // mask words per thread per stage
-constexpr int FU_CONV_WARP0 = 4;           // warps 4..7: TMEM lane quarters 0..3
-constexpr int FU_MASK_WARP0 = 8;
+constexpr int FU_CONV_WARP0 = 2;           // warps 2..5: TMEM lane quarters 2, 3, 0, 1
+constexpr int FU_MASK_WARP0 = 6;           // warps 6..13: quarters (warp % 4) x 2 pixel slices
 constexpr int FU_THREADS = 32 * (FU_MASK_WARP0 + FU_MASK_WARPS);
 constexpr int FU_MAX_FB = 4;               // m <= 512
 
@@ -249,7 +249,7 @@ __global__ void __launch_bounds__(FU_THREADS, 1) fused_fg_kernel(
       }
       if (ti >= 1) issue_b(ti - 1);
     }
-  } else if (warp < FU_MASK_WARP0) {  // ---------------------------------- convert
+  } else if (warp < FU_MASK_WARP0) {  // ------------------------------ convert (2..5)
     const int q = warp & 3;
     const int row = q * 32 + lane;              // pixel of the tile (TMEM lane)
     for (int ti = 0;; ++ti) {

@@ -4,12 +4,22 @@
 #include <cusolverDn.h>
 
 #include <atomic>
+#include <map>
 #include <mutex>
 #include <set>
 #include <tuple>
 #include <vector>
 
 #include "common.cuh"
+
+namespace cdmd {
+// pixel-sorted entries of a sparse C (sparse_csc.cu): pos ascending, rs = row << 1 | negative
+struct SparseCsc {
+  int32_t* pos = nullptr;
+  int32_t* rs = nullptr;
+  int nent = 0;
+};
+}  // namespace cdmd
 
 struct cdmd_handle_s {
   int device = 0;
@@ -27,6 +37,7 @@ struct cdmd_handle_s {
   // sparse plans (n, p, s, seed) whose index lists were checked once against their ELL
   // capacity (cdmd_sketch syncs the first time a plan is seen, never afterwards)
   std::set<std::tuple<int64_t, int64_t, double, uint64_t>> sparse_checked;
+  std::map<std::tuple<int64_t, int64_t, double, uint64_t>, cdmd::SparseCsc> sparse_csc;   // plan -> sorted C
   std::mutex mu;
   std::vector<char> host_ws;         // cuSOLVER host workspace (fit only)
   double omega_eps = 0.0;            // > 0: background by |omega| < omega_eps, else OMP
@@ -39,6 +50,11 @@ namespace cdmd {
 inline int* sched_slot(cdmd_handle h) {
   return h->sched + (h->sched_next.fetch_add(1, std::memory_order_relaxed) % CDMD_SCHED_SLOTS);
 }
+const SparseCsc* sparse_csc_get(cdmd_handle h, const SensingPlan& P, uint64_t seed, const int32_t* ell,
+                                const int32_t* counts, cudaStream_t st, cudaError_t* err);
+bool sketch_sparse_sorted_supported(int64_t p);
+cudaError_t launch_sketch_sparse_sorted(const cdmd_video& v, const SensingPlan& P, const int32_t* pos,
+                                        const int32_t* rs, int nent, int32_t* Y, int64_t ldy, cudaStream_t st);
 cdmd_status fit_impl(cdmd_handle h, const void* Y, int64_t ldy, int kind, int64_t p, int64_t m,
                      int k, int K, double dt, cdmd_model* model, void* ws, size_t ws_bytes,
                      cudaStream_t st);

@@ -89,6 +89,103 @@ cudaError_t launch_sketch_sparse(const cdmd_video& v, const SensingPlan& P, cons
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------- sparse, pixel-sorted
+// The same sum Y[r, t] = sum_e sign_e D[pos_e, t], reorganised so that X is read once
+// per touched 32-B sector and frame in address order: the (pos, row, sign) entries of
+// C are sorted by pixel once per sensing plan (cached by the handle, sparse_csc_build),
+// a CTA owns SK_TF frames and walks the whole sorted list for them, scattering
+// sign * x into its frames' column of Y kept in shared memory (int32 atomics: exact
+// and order-independent), then writes those columns of Y.  No global atomics.
+constexpr int SK_TF = 4;        // frames per CTA
+constexpr int SK_T = 512;
+
+__global__ void __launch_bounds__(SK_T) sketch_sparse_sorted_kernel(
+    const uint8_t* __restrict__ X, int64_t ld, int64_t pix0, int64_t n_local, int64_t m, int64_t p,
+    const int32_t* __restrict__ pos, const int32_t* __restrict__ rs, int nent, int32_t* __restrict__ Y,
+    int64_t ldy) {
+  extern __shared__ int32_t ys[];                 // [p][SK_TF]
+  __shared__ int range[2];
+  const int64_t t0 = (int64_t)blockIdx.x * SK_TF;
+  const int nt = (int)(m - t0 < SK_TF ? m - t0 : SK_TF);
+  for (int64_t i = threadIdx.x; i < p * SK_TF; i += SK_T) ys[i] = 0;
+  if (threadIdx.x < 2) {   // entries of this slab: [first pos >= pix0, first pos >= pix0 + n_local)
+    const int64_t key = threadIdx.x == 0 ? pix0 : pix0 + n_local;
+    int lo = 0, hi = nent;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if ((int64_t)pos[mid] < key) lo = mid + 1; else hi = mid;
+    }
+    range[threadIdx.x] = lo;
+  }
+  __syncthreads();
+  const int e0 = range[0], e1 = range[1];
+  const uint8_t* __restrict__ xt = X + t0 * ld - pix0;
+  int e = e0 + (int)threadIdx.x;
+  // two entries per iteration: 2 x SK_TF independent gathers in flight per thread
+  for (; e + SK_T < e1; e += 2 * SK_T) {
+    const int64_t pa = pos[e], pb = pos[e + SK_T];
+    const int ra = rs[e], rb = rs[e + SK_T];
+    int va[SK_TF], vb[SK_TF];
+#pragma unroll
+    for (int tt = 0; tt < SK_TF; ++tt) {
+      va[tt] = tt < nt ? (int)__ldg(xt + tt * ld + pa) : 0;
+      vb[tt] = tt < nt ? (int)__ldg(xt + tt * ld + pb) : 0;
+    }
+#pragma unroll
+    for (int tt = 0; tt < SK_TF; ++tt) {
+      atomicAdd(&ys[(ra >> 1) * SK_TF + tt], (ra & 1) ? -va[tt] : va[tt]);
+      atomicAdd(&ys[(rb >> 1) * SK_TF + tt], (rb & 1) ? -vb[tt] : vb[tt]);
+    }
+  }
+  for (; e < e1; e += SK_T) {
+    const int64_t pa = pos[e];
+    const int ra = rs[e];
+#pragma unroll
+    for (int tt = 0; tt < SK_TF; ++tt) {
+      const int v = tt < nt ? (int)__ldg(xt + tt * ld + pa) : 0;
+      atomicAdd(&ys[(ra >> 1) * SK_TF + tt], (ra & 1) ? -v : v);
+    }
+  }
+  __syncthreads();
+  for (int tt = 0; tt < nt; ++tt)
+    for (int64_t r = threadIdx.x; r < p; r += SK_T) Y[r + (t0 + tt) * ldy] = ys[r * SK_TF + tt];
+}
+
+bool sketch_sparse_sorted_supported(int64_t p) { return (size_t)p * SK_TF * sizeof(int32_t) <= 160 * 1024; }
+
+cudaError_t launch_sketch_sparse_sorted(const cdmd_video& v, const SensingPlan& P, const int32_t* pos,
+                                        const int32_t* rs, int nent, int32_t* Y, int64_t ldy, cudaStream_t st) {
+  const size_t smem = (size_t)P.p * SK_TF * sizeof(int32_t);
+  cudaError_t e = cudaFuncSetAttribute(sketch_sparse_sorted_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  note_launch();
+  sketch_sparse_sorted_kernel<<<(unsigned)ceil_div(v.m, SK_TF), SK_T, smem, st>>>(v.X, v.ld, v.pix0, v.n_local, v.m,
+                                                                                 P.p, pos, rs, nent, Y, ldy);
+  return cudaGetLastError();
+}
+
+// ELL rows -> (key = pos or 0xFFFFFF for an unused slot, value = row << 1 | negative)
+__global__ void sparse_ell_to_pairs_kernel(const int32_t* __restrict__ ell, const int32_t* __restrict__ counts,
+                                           int64_t p, int64_t cap, int32_t* __restrict__ key,
+                                           int32_t* __restrict__ val) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= p * cap) return;
+  const int64_t r = i / cap, c = i % cap;
+  const int32_t en = ell[i];
+  const bool used = c < counts[r];
+  key[i] = used ? (en >> 1) : 0xFFFFFF;
+  val[i] = used ? (int32_t)((r << 1) | (en & 1)) : 0;
+}
+
+cudaError_t launch_sparse_ell_to_pairs(const SensingPlan& P, const int32_t* ell, const int32_t* counts, int32_t* key,
+                                       int32_t* val, cudaStream_t st) {
+  const int64_t N = P.p * P.cap;
+  note_launch();
+  sparse_ell_to_pairs_kernel<<<(unsigned)ceil_div(N, 256), 256, 0, st>>>(ell, counts, P.p, P.cap, key, val);
+  return cudaGetLastError();
+}
+
 // -------------------------------------------------------- Rademacher (SIMT)
 // Block tile: 64 rows of C x 64 frames; K loop over 128-pixel chunks aligned to
 // the global 128-pixel grid (pix0 % 128 == 0), so one Philox call yields the

@@ -256,6 +256,30 @@ def test_sketch_slabs_sum_to_full(C, H):
         assert torch.equal(acc, full.Y)
 
 
+@pytest.mark.parametrize("W,Hh,m,p,slabs", [(1920, 1080, 500, 2000, 1), (333, 101, 77, 200, 1), (640, 360, 30, 600, 3)])
+def test_sparse_sorted_sketch_equals_ell(C, H, W, Hh, m, p, slabs, monkeypatch):
+    """The pixel-sorted sparse sketch (C sorted by pixel once per plan, cached by the
+    handle; a CTA per 4 frames scattering into Y in shared memory) is bit-identical to the
+    row-wise ELL gather kernel, on whole frames and on pixel slabs (pix0 > 0)."""
+    X = make_video(W, Hh, m, seed=W + m, noise=2.0, n_rects=2)
+    n = X.shape[1]
+    from paper_1512_04205_b200.dist import slab
+    for q in range(slabs):
+        p0, nl = slab(n, slabs, q)
+        Xd = to_dev(X[:, p0:p0 + nl])
+        P = C.Pipeline(H, n, nl, m, "sparse", p, 8, 2, pix0=p0, seed=q + 3)
+        a = P.sketch(Xd).clone()
+        a2 = P.sketch(Xd).clone()                 # second call: the cached sorted C
+        monkeypatch.setenv("CDMD_SPARSE_ELL", "1")
+        b = P.sketch(Xd).clone()
+        monkeypatch.delenv("CDMD_SPARSE_ELL")
+        torch.cuda.synchronize()
+        assert torch.equal(a, b) and torch.equal(a2, b), (q, p0, nl)
+        if W < 1000:
+            want = OS.sketch(X[:, p0:p0 + nl], OS.SPARSE, p, q + 3, n_total=n, pix0=p0)
+            assert np.array_equal(a.cpu().numpy().T.astype(np.int64), want)
+
+
 def test_c3_rademacher_full_size_sampled_rows(C, H):
     cfg = config_by_name("c3_720x480_rademacher")
     X = video_for(cfg)
