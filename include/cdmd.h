@@ -25,7 +25,8 @@
  *    of a pixel-sharded run holds the slab of global pixels [pix0, pix0+n_local).
  *    X must be 16-byte aligned, ld >= n_local and ld % 16 == 0, pix0 % 128 == 0.
  *  - Sketch Y_full = C D: p x m, column-major, Y[r + t*ldy]; int32 for
- *    CDMD_SPIXEL / CDMD_SPARSE / CDMD_RADEMACHER (exact), float for CDMD_GAUSSIAN.
+ *    CDMD_SPIXEL / CDMD_SPARSE / CDMD_RADEMACHER (exact), float for CDMD_GAUSSIAN and
+ *    CDMD_SRFT (rows 0 .. p/2-1 = Re, p/2 .. p-1 = Im of the complex measurements).
  *    Y = first m-1 columns, Y' = last m-1 columns (Eq. FullData, reading R2).
  *  - Modes Phi (Eq. cDMDModes): complex n x k with columns in conjugate
  *    pairs, stored FOLDED as k_eff real float columns, Phi[j + c*ldphi]:
@@ -68,7 +69,10 @@ typedef enum {
   CDMD_SPIXEL = 0,     /* C = R, p rows of I_n without replacement            */
   CDMD_SPARSE = 1,     /* +-1 w.p. 1/(2s) each, 0 otherwise                    */
   CDMD_RADEMACHER = 2, /* +-1 (Bernoulli; the s = 1 case of P:386-393)              */
-  CDMD_GAUSSIAN = 3    /* N(0,1) rounded to bf16 (reading R7)                       */
+  CDMD_GAUSSIAN = 3,   /* N(0,1) rounded to bf16 (reading R7)                       */
+  CDMD_SRFT = 4        /* subsampled random Fourier transform C = R F D, realified:
+                          p (even) real rows = Re and Im of p/2 complex measurements; phases
+                          quantised to 2^-16 turn, entries fp16 (reading R25)             */
 } cdmd_measure;
 
 typedef enum {
@@ -163,7 +167,9 @@ CDMD_API cdmd_status cdmd_sm_partition(int device, int fit_sms, int n_streams, v
  * permutation rows; sparse = geometric-gap rows; Rademacher = bits; Gaussian =
  * bf16 inverse-CDF table).  Columns of C are indexed by the GLOBAL pixel, so the
  * per-slab partial sketches of a pixel-sharded run SUM to the full sketch
- * (integer kinds bit-exactly).  Y (p x m, ldy >= p) is overwritten.
+ * (integer kinds bit-exactly).  Y (p x m, ldy >= p) is overwritten.  SRFT: p even,
+ * 2 <= p <= 2 n_total, m + 1 <= 512 (the tensor-core kernel), else CDMD_ERR_RANGE /
+ * CDMD_ERR_UNSUPPORTED.
  * ws: device workspace of at least cdmd_sketch_workspace_bytes() bytes, 256-B
  * aligned (index lists of C; for Gaussian C also the split-K partial sums, which are
  * reduced in a fixed order so Y is deterministic).  Sparse C: the first call with a
@@ -282,8 +288,12 @@ CDMD_API cdmd_status cdmd_philox(const uint32_t* ctr, uint32_t k0, uint32_t k1, 
                         int64_t count, cdmd_stream st);
 /* out: device uint16 [65536] bf16 bit patterns of the Gaussian table. */
 CDMD_API cdmd_status cdmd_gaussian_table(cdmd_handle h, uint16_t* out, cdmd_stream st);
-/* Single pixel: rows (device int32 [p]).  Sparse: device int32 [p*cap] ELL of
- * (pos << 1 | negative) and int32 counts [p]; cap from cdmd_sparse_cap(). */
+/* out: device uint16 [16385] fp16 bit patterns of the SRFT quarter wave
+ * Q[r] = fp16_RNE(cos(2 pi r / 2^16)), r = 0 .. 2^14 (reading R25). */
+CDMD_API cdmd_status cdmd_srft_table(cdmd_handle h, uint16_t* out, cdmd_stream st);
+/* Single pixel: rows (device int32 [p]).  SRFT: the p/2 frequencies of R (device int32
+ * [p/2]).  Sparse: device int32 [p*cap] ELL of (pos << 1 | negative) and int32 counts
+ * [p]; cap from cdmd_sparse_cap(). */
 CDMD_API int64_t cdmd_sparse_cap(int64_t n_total, int64_t p, double s);
 CDMD_API cdmd_status cdmd_sensing_rows(cdmd_handle h, int64_t n_total, const cdmd_sensing* c,
                               int32_t* rows_or_ell, int32_t* counts, cdmd_stream st);

@@ -205,10 +205,17 @@ def srft_phases(cols, seed):
 
 
 def srft_table():
-    """(cos, sin) of 2 pi j / 2^16, j = 0 .. 65535, rounded to fp16 (RNE), as fp64."""
-    j = np.arange(65536, dtype=np.float64)
-    ang = 2.0 * np.pi * j / 65536.0
-    return np.cos(ang).astype(np.float16).astype(np.float64), np.sin(ang).astype(np.float16).astype(np.float64)
+    """(cos, sin) of 2 pi j / 2^16, j = 0 .. 65535, as fp16 (RNE) values in fp64, built
+    from the quarter wave Q[r] = fp16(cos(2 pi r / 2^16)), r = 0 .. 2^14, by the exact
+    symmetries cos(pi/2 qd + t) = (Q[r], -Q[2^14 - r], -Q[r], Q[2^14 - r]) for quadrant
+    qd = 0..3 (t = 2 pi r / 2^16), and sin(x) = cos(x - pi/2)."""
+    r = np.arange(16385, dtype=np.float64)
+    Q = np.cos(2.0 * np.pi * r / 65536.0).astype(np.float16).astype(np.float64)
+    j = np.arange(65536)
+    qd, rr = j >> 14, j & 16383
+    idx = np.where(qd & 1, 16384 - rr, rr)
+    cos = np.where((qd == 1) | (qd == 2), -Q[idx], Q[idx])
+    return cos, cos[(j - 16384) % 65536]
 
 
 _ST = None

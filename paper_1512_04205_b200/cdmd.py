@@ -18,8 +18,8 @@ import torch
 
 from .build import LIB
 
-SPIXEL, SPARSE, RADEMACHER, GAUSSIAN = 0, 1, 2, 3
-KINDS = {"spixel": SPIXEL, "sparse": SPARSE, "rademacher": RADEMACHER, "gaussian": GAUSSIAN}
+SPIXEL, SPARSE, RADEMACHER, GAUSSIAN, SRFT = 0, 1, 2, 3, 4
+KINDS = {"spixel": SPIXEL, "sparse": SPARSE, "rademacher": RADEMACHER, "gaussian": GAUSSIAN, "srft": SRFT}
 BG_STATIC, BG_DYNAMIC = 0, 1
 STATUS = {0: "ok", 1: "invalid argument", 2: "argument out of range", 3: "numerical failure",
           4: "CUDA error", 5: "workspace too small", 6: "unsupported device (needs sm_100a)"}
@@ -58,7 +58,7 @@ SYMBOLS = ["cdmd_create", "cdmd_destroy", "cdmd_status_str", "cdmd_version", "cd
            "cdmd_sketch_workspace_bytes", "cdmd_sketch", "cdmd_model_bytes", "cdmd_model_bind",
            "cdmd_fit_workspace_bytes", "cdmd_fit", "cdmd_modes", "cdmd_background",
            "cdmd_amplitudes_workspace_bytes", "cdmd_amplitudes_gram", "cdmd_amplitudes_solve",
-           "cdmd_foreground", "cdmd_philox", "cdmd_gaussian_table", "cdmd_sparse_cap",
+           "cdmd_foreground", "cdmd_philox", "cdmd_gaussian_table", "cdmd_srft_table", "cdmd_sparse_cap",
            "cdmd_sensing_rows", "cdmd_modes_simt", "cdmd_eig", "cdmd_mask_median3",
            "cdmd_modes_path", "cdmd_foreground_path", "cdmd_sm_partition",
            "cdmd_set_background_selection"]
@@ -94,6 +94,7 @@ def _load():
         "cdmd_foreground_path": (i32, [V, M, i32]),
         "cdmd_philox": (i32, [vp, ctypes.c_uint32, ctypes.c_uint32, vp, i64, vp]),
         "cdmd_gaussian_table": (i32, [vp, vp, vp]),
+        "cdmd_srft_table": (i32, [vp, vp, vp]),
         "cdmd_sparse_cap": (i64, [i64, i64, dbl]),
         "cdmd_sensing_rows": (i32, [vp, i64, S, vp, vp, vp]),
         "cdmd_eig": (i32, [vp, ctypes.c_int, vp, vp, vp, vp]),
@@ -253,6 +254,10 @@ def cdmd_gaussian_table(h, out, stream=None):
     _check("cdmd_gaussian_table", _lib.cdmd_gaussian_table(h.h, _ptr(out), _stream(stream)))
 
 
+def cdmd_srft_table(h, out, stream=None):
+    _check("cdmd_srft_table", _lib.cdmd_srft_table(h.h, _ptr(out), _stream(stream)))
+
+
 def cdmd_kernel_launches():
     """libcdmd kernel launches issued by this process so far (cuBLAS/cuSOLVER excluded)."""
     return int(lib().cdmd_kernel_launches())
@@ -342,7 +347,7 @@ class Pipeline:
         self.n_total, self.n_local, self.m, self.p, self.k, self.K = n_total, n_local, m, p, k, K
         self.pix0, self.dt = pix0, dt
         self.c = sensing(self.kind, p, s, seed)
-        ydt = torch.float32 if self.kind == GAUSSIAN else torch.int32
+        ydt = torch.float32 if self.kind in (GAUSSIAN, SRFT) else torch.int32
         self.Y = torch.empty((m, p), dtype=ydt, device=device)          # column-major p x m
         probe = Video(0, n_total, pix0, n_local, m, ((n_local + 15) // 16) * 16)
         self.ws_sketch = _empty_bytes(cdmd_sketch_workspace_bytes(probe, self.c), device)

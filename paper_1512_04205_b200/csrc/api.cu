@@ -50,7 +50,11 @@ cdmd_status check_video(const cdmd_video* v) {
 
 cdmd_status check_sensing(int64_t n_total, const cdmd_sensing* c) {
   if (!c) return CDMD_ERR_ARG;
-  if (c->kind < CDMD_SPIXEL || c->kind > CDMD_GAUSSIAN) return CDMD_ERR_ARG;
+  if (c->kind < CDMD_SPIXEL || c->kind > CDMD_SRFT) return CDMD_ERR_ARG;
+  if (c->kind == CDMD_SRFT) {   // p real rows = Re, Im of p/2 distinct frequencies
+    if (c->p < 2 || (c->p & 1) || c->p > 2 * n_total) return CDMD_ERR_RANGE;
+    return CDMD_OK;
+  }
   if (c->p < 1 || c->p > n_total) return CDMD_ERR_RANGE;
   if (c->kind == CDMD_SPARSE && c->s > 0 && c->s <= 1.0) return CDMD_ERR_RANGE;
   if (c->kind == CDMD_SPARSE && c->s <= 0 && n_total < 3) return CDMD_ERR_RANGE;  // n/ln n > 1
@@ -141,6 +145,8 @@ cdmd_status cdmd_create(int device, cdmd_handle* out) {
   if (st == CDMD_OK && cudaMallocHost(&h->host_info, 16 * sizeof(int32_t)) != cudaSuccess) st = CDMD_ERR_CUDA;
   if (st == CDMD_OK && cudaMalloc(&h->sched, CDMD_SCHED_SLOTS * sizeof(int)) != cudaSuccess) st = CDMD_ERR_CUDA;
   if (st == CDMD_OK && launch_gaussian_table(h->gauss_table, 0) != cudaSuccess) st = CDMD_ERR_CUDA;
+  if (st == CDMD_OK && cudaMalloc(&h->srft_table, 16385 * sizeof(uint16_t)) != cudaSuccess) st = CDMD_ERR_CUDA;
+  if (st == CDMD_OK && launch_srft_table(h->srft_table, 0) != cudaSuccess) st = CDMD_ERR_CUDA;
   if (st == CDMD_OK && cudaDeviceSynchronize() != cudaSuccess) st = CDMD_ERR_CUDA;
   if (st != CDMD_OK) {
     cdmd_destroy(h);
@@ -156,6 +162,7 @@ void cdmd_destroy(cdmd_handle h) {
   if (h->solver) cusolverDnDestroy(h->solver);
   if (h->blas) cublasDestroy(h->blas);
   if (h->gauss_table) cudaFree(h->gauss_table);
+  if (h->srft_table) cudaFree(h->srft_table);
   if (h->host_info) cudaFreeHost(h->host_info);
   if (h->sched) cudaFree(h->sched);
   for (auto& kv : h->sparse_csc) {
@@ -190,7 +197,7 @@ static cdmd_status check_sparse_once(cdmd_handle h, const SensingPlan& P, uint64
 
 static size_t sketch_ws_bytes(const cdmd_video* v, const SensingPlan& P) {
   size_t b = al256(sensing_ws_bytes(P));
-  if (P.kind == CDMD_GAUSSIAN) b += al256(sizeof(float) * (size_t)gaussian_part_floats(*v, P.p));
+  if (P.kind == CDMD_GAUSSIAN || P.kind == CDMD_SRFT) b += al256(sizeof(float) * (size_t)gaussian_part_floats(*v, P.p));
   return b;
 }
 
@@ -256,6 +263,15 @@ cdmd_status cdmd_sketch(cdmd_handle h, const cdmd_video* v, const cdmd_sensing* 
       e = launch_sketch_gaussian(*v, P, h->gauss_table, (float*)Y, ldy,
                                  (float*)((char*)ws + al256(sensing_ws_bytes(P))), st);
       break;
+    case CDMD_SRFT: {
+      if (!sketch_srft_supported(*v)) return CDMD_ERR_UNSUPPORTED;
+      int32_t* freqs = (int32_t*)ws;
+      e = launch_srft_freqs(P, freqs, st);
+      if (e == cudaSuccess)
+        e = launch_sketch_srft(*v, P, freqs, h->srft_table, (float*)Y, ldy,
+                               (float*)((char*)ws + al256(sensing_ws_bytes(P))), st);
+      break;
+    }
   }
   return cuda_status(e);
 }
@@ -305,7 +321,7 @@ cdmd_status cdmd_fit(cdmd_handle h, const void* Y, int64_t ldy, int32_t kind, in
                      int k, int K, double dt, cdmd_model* model, void* ws, size_t ws_bytes,
                      cdmd_stream st) {
   if (!h || !Y || !model || !ws) return CDMD_ERR_ARG;
-  if (kind < CDMD_SPIXEL || kind > CDMD_GAUSSIAN) return CDMD_ERR_ARG;
+  if (kind < CDMD_SPIXEL || kind > CDMD_SRFT) return CDMD_ERR_ARG;
   if (m < 2 || p < 1) return CDMD_ERR_RANGE;
   const int kmax = k < 0 ? -k : k;   // k < 0: Gavish-Donoho rank, at most -k (Remark 2)
   if (kmax < 1 || kmax > p || kmax > m - 1 || kmax > model->k) return CDMD_ERR_RANGE;  // P:355 "p >= k"
@@ -439,6 +455,12 @@ cdmd_status cdmd_gaussian_table(cdmd_handle h, uint16_t* out, cdmd_stream st) {
                                      cudaMemcpyDeviceToDevice, (cudaStream_t)st));
 }
 
+cdmd_status cdmd_srft_table(cdmd_handle h, uint16_t* out, cdmd_stream st) {
+  if (!h || !out) return CDMD_ERR_ARG;
+  return cuda_status(cudaMemcpyAsync(out, h->srft_table, 16385 * sizeof(uint16_t), cudaMemcpyDeviceToDevice,
+                                     (cudaStream_t)st));
+}
+
 int64_t cdmd_sparse_cap(int64_t n_total, int64_t p, double s) {
   cdmd_sensing c{CDMD_SPARSE, p, s, 0};
   return make_plan(n_total, &c).cap;
@@ -452,6 +474,7 @@ cdmd_status cdmd_sensing_rows(cdmd_handle h, int64_t n_total, const cdmd_sensing
   if (s != CDMD_OK) return s;
   const SensingPlan P = make_plan(n_total, c);
   if (P.kind == CDMD_SPIXEL) return cuda_status(launch_spixel_rows(P, rows_or_ell, st));
+  if (P.kind == CDMD_SRFT) return cuda_status(launch_srft_freqs(P, rows_or_ell, st));
   if (P.kind == CDMD_SPARSE) {
     if (!counts) return CDMD_ERR_ARG;
     int32_t* flags = nullptr;

@@ -54,7 +54,8 @@ __device__ __forceinline__ float combine_limbs(uint32_t a0, uint32_t a1, uint32_
 }
 
 // Philox counter word c3 tags the use of the stream.
-enum : uint32_t { TAG_SPIXEL = 1, TAG_SPARSE = 2, TAG_RADEMACHER = 3, TAG_GAUSSIAN = 4 };
+enum : uint32_t { TAG_SPIXEL = 1, TAG_SPARSE = 2, TAG_RADEMACHER = 3, TAG_GAUSSIAN = 4, TAG_SRFT = 5,
+                  TAG_SRFT_PHASE = 6 };
 
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 __host__ __device__ inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
@@ -84,6 +85,12 @@ size_t sensing_ws_bytes(const SensingPlan& P);
 
 // launchers (return cudaGetLastError())
 cudaError_t launch_spixel_rows(const SensingPlan& P, int32_t* rows, cudaStream_t st);
+// SRFT: the p/2 frequencies of R (the Feistel bijection with tag TAG_SRFT)
+cudaError_t launch_srft_freqs(const SensingPlan& P, int32_t* freqs, cudaStream_t st);
+cudaError_t launch_srft_table(uint16_t* table, cudaStream_t st);
+cudaError_t launch_sketch_srft(const cdmd_video& v, const SensingPlan& P, const int32_t* freqs,
+                               const uint16_t* table, float* Y, int64_t ldy, float* part, cudaStream_t st);
+bool sketch_srft_supported(const cdmd_video& v);
 cudaError_t launch_sparse_rows(const SensingPlan& P, int32_t* ell, int32_t* counts,
                                int32_t* flags, cudaStream_t st);
 cudaError_t launch_gaussian_table(uint16_t* table, cudaStream_t st);

@@ -695,6 +695,9 @@ __global__ void __launch_bounds__(32) hqr_eig_kernel(int nn, const double* __res
 //
 // hqrv_kernel: A (k x k column-major) -> W (wr, wi pairs as hqr2), H0 (the Hessenberg
 // form, row-major k x k) and Q (row-major k x k) for hinvit_kernel.
+__device__ unsigned long long g_hqr_prof[8];   // orthes, ortran, deflation search, m search, bulge steps, iterations, steps
+void hqr_prof_read(unsigned long long* out) { cudaMemcpyFromSymbol(out, g_hqr_prof, sizeof(unsigned long long) * 8); }
+
 __global__ void __launch_bounds__(32) hqrv_kernel(int nn, const double* __restrict__ A, double* __restrict__ W,
                                                  double* __restrict__ H0, double* __restrict__ Qout,
                                                  int* __restrict__ info) {
@@ -715,6 +718,9 @@ __global__ void __launch_bounds__(32) hqrv_kernel(int nn, const double* __restri
     Vx(i, j) = (i == j) ? 1.0 : 0.0;
   }
   wp.sync();
+  unsigned long long pr[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  unsigned long long tq = clock64();
+#define HQ_TICK(k) do { const unsigned long long t_ = clock64(); pr[k] += t_ - tq; tq = t_; } while (0)
   const int low = 0, high = nn - 1;
   // ------------------------------------------------ orthes (Hessenberg)
   for (int m = low + 1; m <= high - 1; ++m) {
@@ -759,6 +765,7 @@ __global__ void __launch_bounds__(32) hqrv_kernel(int nn, const double* __restri
       wp.sync();
     }
   }
+  HQ_TICK(0);
   // ortran: Q explicitly
   for (int m = high - 1; m >= low + 1; --m) {
     if (Hx(m, m - 1) != 0.0) {
@@ -790,14 +797,26 @@ __global__ void __launch_bounds__(32) hqrv_kernel(int nn, const double* __restri
     for (int j = (i > 0 ? i - 1 : 0); j < nn; ++j) norm += fabs(Hx(i, j));
   norm = wp.sum(norm);
   int iter = 0, total_iter = 0, fail = 0;
+  HQ_TICK(1);
   while (n >= low) {
-    int l = n;
-    while (l > low) {
-      s = fabs(Hx(l - 1, l - 1)) + fabs(Hx(l, l));
-      if (s == 0.0) s = norm;
-      if (fabs(Hx(l, l - 1)) < eps * s) break;
-      l--;
+    // deflation search, 32 candidates per round: the largest l in (low, n] with a
+    // negligible subdiagonal H(l, l-1) (the sequential scan's first hit), else low
+    int l = low;
+    for (int base = n; base > low; base -= 32) {
+      const int cand = base - lane;
+      bool hit = false;
+      if (cand > low) {
+        double sl = fabs(Hx(cand - 1, cand - 1)) + fabs(Hx(cand, cand));
+        if (sl == 0.0) sl = norm;
+        hit = fabs(Hx(cand, cand - 1)) < eps * sl;
+      }
+      const unsigned bal = __ballot_sync(0xffffffffu, hit);
+      if (bal) {
+        l = base - (__ffs(bal) - 1);
+        break;
+      }
     }
+    HQ_TICK(2);
     if (l == n) {  // one root
       if (lane == 0) {
         d[n] = Hx(n, n) + exshift;
@@ -865,20 +884,34 @@ __global__ void __launch_bounds__(32) hqrv_kernel(int nn, const double* __restri
         fail = 1;
         break;
       }
-      int m = n - 2;   // (p, q, r) carried multiplied by H(m+1, m): no divisions
-      while (m >= l) {
-        z = Hx(m, m);
-        r = x - z;
-        s = y - z;
-        const double h = Hx(m + 1, m);
-        p = (r * s - w) + Hx(m, m + 1) * h;
-        q = (Hx(m + 1, m + 1) - z - r - s) * h;
-        r = Hx(m + 2, m + 1) * h;
-        if (m == l) break;
-        if (fabs(Hx(m, m - 1)) * (fabs(q) + fabs(r)) <
-            eps * (fabs(p) * (fabs(Hx(m - 1, m - 1)) + fabs(z) + fabs(Hx(m + 1, m + 1)))))
+      pr[5]++;
+      // start of the bulge, 32 candidates per round: the largest m in [l, n-2] where two
+      // consecutive small subdiagonals allow splitting (or m = l), with its (p, q, r)
+      // carried multiplied by H(m+1, m) (no divisions), as the sequential scan
+      int m = l;
+      for (int base = n - 2; base >= l; base -= 32) {
+        const int cand = base - lane;
+        bool hit = false;
+        double pp = 0.0, qq = 0.0, rr = 0.0;
+        if (cand >= l) {
+          const double zz = Hx(cand, cand);
+          const double r_ = x - zz, s_ = y - zz;
+          const double h = Hx(cand + 1, cand);
+          pp = (r_ * s_ - w) + Hx(cand, cand + 1) * h;
+          qq = (Hx(cand + 1, cand + 1) - zz - r_ - s_) * h;
+          rr = Hx(cand + 2, cand + 1) * h;
+          hit = (cand == l) || (fabs(Hx(cand, cand - 1)) * (fabs(qq) + fabs(rr)) <
+                                eps * (fabs(pp) * (fabs(Hx(cand - 1, cand - 1)) + fabs(zz) + fabs(Hx(cand + 1, cand + 1)))));
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, hit);
+        if (bal) {
+          const int src = __ffs(bal) - 1;
+          m = base - src;
+          p = __shfl_sync(0xffffffffu, pp, src);
+          q = __shfl_sync(0xffffffffu, qq, src);
+          r = __shfl_sync(0xffffffffu, rr, src);
           break;
-        m--;
+        }
       }
       {
         const double sc = fabs(p) + fabs(q) + fabs(r);
@@ -889,12 +922,14 @@ __global__ void __launch_bounds__(32) hqrv_kernel(int nn, const double* __restri
           r *= isc;
         }
       }
+      HQ_TICK(3);
       wp.sync();
       for (int i = m + 2 + lane; i <= n; i += 32) {
         Hx(i, i - 2) = 0.0;
         if (i > m + 2) Hx(i, i - 3) = 0.0;
       }
       wp.sync();
+      pr[6] += n - m;
       for (int kk = m; kk <= n - 1; ++kk) {  // double QR step on the active block l..n
         const bool notlast = (kk != n - 1);
         if (kk != m) {
@@ -958,9 +993,13 @@ __global__ void __launch_bounds__(32) hqrv_kernel(int nn, const double* __restri
           wp.sync();
         }
       }
+      HQ_TICK(4);
     }
   }
   wp.sync();
+  if (lane == 0)
+    for (int k2 = 0; k2 < 7; ++k2) g_hqr_prof[k2] = pr[k2];
+#undef HQ_TICK
   if (fail) {
     if (lane == 0) *info = 1;
     return;

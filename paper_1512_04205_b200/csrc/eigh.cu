@@ -12,6 +12,7 @@
 // It uses 8 SMs for the O(n^3) phase, so several batches' fits overlap (streaming).
 #include <cooperative_groups.h>
 #include <math.h>
+#include <stdio.h>
 #include <stdlib.h>
 
 #include "common.cuh"
@@ -260,223 +261,6 @@ __global__ void __cluster_dims__(EH_CL, 1, 1) __launch_bounds__(EH_T, 1)
   if (rank == ((n - 1) % EH_CL) && tid == 0) d[n - 1] = Aloc[eh_off(rank, (n - 1) / EH_CL) + (n - 1)];
 }
 
-// ---------------------------------------------------------------------------------
-// Register-resident tridiagonalisation on ONE 16-CTA cluster (n <= 512).
-// The FULL symmetric matrix lives in registers: row l on CTA l % 16 (slot s = l / 16),
-// each row spread over a half-warp, thread g holding A[l][g + 16 t], t < 32 (64 regs).
-// Per column j two cluster exchanges, both bulk DSMEM copies (cp.async.bulk
-// shared::cluster) that signal the receivers' mbarriers:
-//   1. the owner of row j (= column j below the diagonal, by symmetry) stages the row
-//      with its squared norm and broadcasts it; every CTA forms the Householder vector;
-//   2. every CTA computes p = tau A v on its own rows (row dots: no column partials,
-//      since both triangles are stored) and broadcasts its slot-major p values and the
-//      partial p.v; every CTA then forms w and applies A -= v w^T + w v^T to its rows.
-// Same reflectors and outputs as eh_tridiag_kernel (LAPACK dsytd2 lower order).
-constexpr int E16_CL = 16;
-constexpr int E16_T = 512;
-constexpr int E16_NMAX = 512;
-constexpr int E16_TPR = 32;            // elements per thread per row (t < 32)
-constexpr int E16_PST = 34;            // staged p: 32 slot values, kp, pad
-
-__device__ __forceinline__ void e16_bulk_s2s(uint32_t dst_cluster, uint32_t src_cta, uint32_t bytes,
-                                             uint32_t mbar_cluster) {
-  asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   dst_cluster),
-               "r"(src_cta), "r"(bytes), "r"(mbar_cluster)
-               : "memory");
-}
-
-// the owner of row c stages it (entries c .. n-1 as they stand: the diagonal d[c] and the
-// column below it, |x[c+2:]|^2 at index n) and broadcasts the staged row into every CTA's xbuf[c & 1]
-__device__ __forceinline__ void e16_send_row(int c, int n, int npad, int rank, int slot, int g, int tid,
-                                             const double (&a)[E16_TPR], double* stage_x, uint32_t s_stx,
-                                             uint32_t s_xbuf, uint32_t s_xbar) {
-  if (slot == c / E16_CL && rank == c % E16_CL) {
-    double part = 0.0;
-#pragma unroll
-    for (int t = 0; t < E16_TPR; ++t) {
-      const int i = g + 16 * t;
-      if (i >= c && i < n) {   // i = c: the diagonal d[c], final from here on
-        stage_x[i] = a[t];
-        if (i > c + 1) part += a[t] * a[t];
-      }
-    }
-#pragma unroll
-    for (int o = 8; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);   // within the half-warp
-    if (g == 0) stage_x[n] = part;
-  }
-  __syncthreads();
-  if (rank == c % E16_CL && tid == 0) {
-    tc::fence_proxy_async();   // the staged row (generic writes) -> bulk copy (async proxy)
-    const int b = c & 1;
-    for (int r = 0; r < E16_CL; ++r)
-      e16_bulk_s2s(tc::mapa(s_xbuf + 8u * (uint32_t)(b * (E16_NMAX + 2)), r), s_stx, 8u * (uint32_t)npad,
-                   tc::mapa(s_xbar + 8u * (uint32_t)b, r));
-  }
-}
-
-__global__ void __launch_bounds__(E16_T, 1)
-    e16_tridiag_kernel(int n, const double* __restrict__ G, int64_t ldg, double* __restrict__ d,
-                       double* __restrict__ e, double* __restrict__ tau_out, double* __restrict__ V) {
-  cg::cluster_group cluster = cg::this_cluster();
-  const int rank = (int)cluster.block_rank();
-  const int tid = threadIdx.x, lane = tid & 31;
-  const int slot = tid >> 4;                 // row slot of this half-warp
-  const int g = tid & 15;                    // element phase: columns g + 16 t
-  const int l = rank + E16_CL * slot;        // global row of this thread
-  const bool has_row = l < n;
-  const int npad = (n + 1 + 1) & ~1;         // staged row: n values + |x|^2, 16-B multiple
-  __shared__ __align__(16) double xbuf[2][E16_NMAX + 2];
-  __shared__ __align__(16) double pbuf[2][E16_CL][E16_PST];
-  __shared__ __align__(16) double stage_x[E16_NMAX + 2];
-  __shared__ __align__(16) double stage_p[2][E16_PST];   // by column parity: a copy may still read the other
-  __shared__ double vsh[E16_NMAX], wsh[E16_NMAX];
-  __shared__ double red[16];
-  __shared__ __align__(8) uint64_t xbar[2], pbar[2];
-  double a[E16_TPR];
-#pragma unroll
-  for (int t = 0; t < E16_TPR; ++t) {
-    const int i = g + 16 * t;
-    a[t] = (has_row && i < n) ? G[i + (int64_t)l * ldg] : 0.0;   // A[l][i] = G[i][l] (symmetric)
-  }
-  if (tid == 0) {
-    for (int q = 0; q < 2; ++q) {
-      tc::mbar_init(&xbar[q], 1);
-      tc::mbar_init(&pbar[q], 1);
-    }
-    tc::fence_mbar_init();
-  }
-  __syncthreads();
-  cluster.sync();
-  const uint32_t s_xbuf = tc::smem_u32(&xbuf[0][0]), s_pbuf = tc::smem_u32(&pbuf[0][0][0]);
-  const uint32_t s_xbar = tc::smem_u32(&xbar[0]), s_pbar = tc::smem_u32(&pbar[0]);
-  const uint32_t s_stx = tc::smem_u32(stage_x), s_stp = tc::smem_u32(&stage_p[0][0]);
-
-  e16_send_row(0, n, npad, rank, slot, g, tid, a, stage_x, s_stx, s_xbuf, s_xbar);
-  for (int j = 0; j < n - 1; ++j) {
-    const int b = j & 1;
-    const uint32_t par = (uint32_t)(j >> 1) & 1u;
-    if (tid == 0) tc::mbar_arrive_expect_tx(&xbar[b], 8u * (uint32_t)npad);
-    tc::mbar_wait(&xbar[b], par);
-    const double* x = xbuf[b];
-    // Householder reflector H = I - tau v v^T zeroing x[j+2:] (dlarfg), on every CTA
-    const double alpha = x[j + 1];
-    const double xnorm = sqrt(x[n]);
-    double beta = alpha, tau = 0.0, scal = 0.0;
-    if (xnorm != 0.0) {
-      beta = -copysign(hypot(alpha, xnorm), alpha);
-      tau = (beta - alpha) / beta;
-      scal = 1.0 / (alpha - beta);
-    }
-    for (int i = j + 1 + tid; i < n; i += E16_T) vsh[i] = (i == j + 1) ? 1.0 : x[i] * scal;
-    if (rank == 0 && tid == 0) {
-      e[j] = beta;
-      tau_out[j] = tau;
-    }
-    if (rank == 0 && tid == 0) d[j] = x[j];
-    __syncthreads();
-    if (rank == 0 && tau != 0.0)
-      for (int i = j + 1 + tid; i < n; i += E16_T) V[i + (int64_t)j * n] = vsh[i];
-    // p_l = tau sum_{i > j} A[l][i] v_i on own rows; partial p.v
-    double acc = 0.0;
-    const bool act = has_row && l > j;
-#pragma unroll
-    for (int t = 0; t < E16_TPR; ++t) {
-      const int i = g + 16 * t;
-      if (act && i > j && i < n) acc = fma(a[t], vsh[i], acc);
-    }
-#pragma unroll
-    for (int o = 8; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    const double pl = act ? tau * acc : 0.0;
-    double kp = (g == 0 && act) ? pl * vsh[l] : 0.0;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) kp += __shfl_xor_sync(0xffffffffu, kp, o);
-    if (g == 0) stage_p[b][slot] = pl;
-    if (lane == 0) red[tid >> 5] = kp;
-    __syncthreads();
-    if (tid == 0) {
-      double s = 0.0;
-      for (int q = 0; q < E16_T / 32; ++q) s += red[q];
-      stage_p[b][32] = s;
-      stage_p[b][33] = 0.0;
-      tc::fence_proxy_async();
-      for (int r = 0; r < E16_CL; ++r)
-        e16_bulk_s2s(tc::mapa(s_pbuf + 8u * (uint32_t)((b * E16_CL + rank) * E16_PST), r), s_stp + 8u * E16_PST * b,
-                     8u * E16_PST,
-                     tc::mapa(s_pbar + 8u * (uint32_t)b, r));
-      tc::mbar_arrive_expect_tx(&pbar[b], 8u * E16_PST * E16_CL);
-    }
-    tc::mbar_wait(&pbar[b], par);
-    // w = p - (tau/2)(p.v) v
-    double pv = 0.0;
-#pragma unroll
-    for (int r = 0; r < E16_CL; ++r) pv += pbuf[b][r][32];
-    const double K = -0.5 * tau * pv;
-    for (int i = j + 1 + tid; i < n; i += E16_T) wsh[i] = pbuf[b][i % E16_CL][i / E16_CL] + K * vsh[i];
-    __syncthreads();
-    // A -= v w^T + w v^T on own rows (both triangles)
-    if (act) {
-      const double vl = vsh[l], wl = wsh[l];
-#pragma unroll
-      for (int t = 0; t < E16_TPR; ++t) {
-        const int i = g + 16 * t;
-        if (i > j && i < n) a[t] -= vl * wsh[i] + wl * vsh[i];
-      }
-    }
-    if (j + 1 < n - 1) e16_send_row(j + 1, n, npad, rank, slot, g, tid, a, stage_x, s_stx, s_xbuf, s_xbar);
-  }
-  if (rank == (n - 1) % E16_CL && slot == (n - 1) / E16_CL) {
-#pragma unroll
-    for (int t = 0; t < E16_TPR; ++t)
-      if (g + 16 * t == n - 1) stage_x[n - 1] = a[t];
-  }
-  __syncthreads();
-  if (rank == (n - 1) % E16_CL && tid == 0) d[n - 1] = stage_x[n - 1];
-  cluster.sync();   // no CTA leaves while a peer may still copy into it
-}
-
-static bool e16_ok(int n) {
-  static int ok = -1;
-  if (ok < 0) {
-    ok = 0;
-    const char* env = getenv("CDMD_EH8");
-    if (!env && cudaFuncSetAttribute(e16_tridiag_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
-                    cudaSuccess) {
-      cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3(E16_CL, 1, 1);
-      cfg.blockDim = dim3(E16_T, 1, 1);
-      cudaLaunchAttribute at;
-      at.id = cudaLaunchAttributeClusterDimension;
-      at.val.clusterDim.x = E16_CL;
-      at.val.clusterDim.y = 1;
-      at.val.clusterDim.z = 1;
-      cfg.attrs = &at;
-      cfg.numAttrs = 1;
-      int clusters = 0;
-      if (cudaOccupancyMaxActiveClusters(&clusters, e16_tridiag_kernel, &cfg) == cudaSuccess && clusters >= 1) ok = 1;
-    }
-    cudaGetLastError();
-  }
-  return ok == 1 && n >= 3 && n <= E16_NMAX;
-}
-
-static cudaError_t launch_e16(int n, const double* G, int64_t ldg, double* d, double* e, double* tau, double* V,
-                              cudaStream_t st) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(E16_CL, 1, 1);
-  cfg.blockDim = dim3(E16_T, 1, 1);
-  cfg.stream = st;
-  cudaLaunchAttribute at;
-  at.id = cudaLaunchAttributeClusterDimension;
-  at.val.clusterDim.x = E16_CL;
-  at.val.clusterDim.y = 1;
-  at.val.clusterDim.z = 1;
-  cfg.attrs = &at;
-  cfg.numAttrs = 1;
-  note_launch();
-  return cudaLaunchKernelEx(&cfg, e16_tridiag_kernel, n, G, ldg, d, e, tau, V);
-}
-
 // Gershgorin bounds, ||T||, pivmin and e^2 (one block)
 __global__ void eh_prep_kernel(int n, const double* __restrict__ d, const double* __restrict__ e,
                                double* __restrict__ e2, double* __restrict__ bounds) {
@@ -523,6 +307,19 @@ __device__ __forceinline__ double eh_pow2_norm(double a) {   // 2^-e with |a| 2^
   const int ex = (int)((bits >> 52) & 0x7ff);
   return __longlong_as_double((long long)(2046 - ex) << 52);
 }
+__device__ __forceinline__ void eh_sturm_step(double di, double ei, const double (&x)[EH_NP], double pivmin,
+                                              double (&p0)[EH_NP], double (&p1)[EH_NP], int (&cnt)[EH_NP]) {
+#pragma unroll
+  for (int u = 0; u < EH_NP; ++u) {
+    double pn = fma(di - x[u], p1[u], -ei * p0[u]);
+    if (fabs(pn) < pivmin * fabs(p1[u])) pn = -pivmin * p1[u];   // ratio clamp
+    cnt[u] += ((__double_as_longlong(pn) ^ __double_as_longlong(p1[u])) < 0) ? 1 : 0;
+    p0[u] = p1[u];
+    p1[u] = pn;
+  }
+}
+// d, e2 in shared memory (uniform across the warp: broadcast loads); the steps come in
+// groups of 8 whose operands are loaded before the group, off the dependent chain
 __device__ __forceinline__ void eh_sturm_multi(int n, const double* __restrict__ d, const double* __restrict__ e2,
                                                const double (&x)[EH_NP], double pivmin, int (&cnt)[EH_NP]) {
   double p0[EH_NP], p1[EH_NP];   // p_{i-1}, p_i
@@ -534,25 +331,24 @@ __device__ __forceinline__ void eh_sturm_multi(int n, const double* __restrict__
     p1[u] = q;
     cnt[u] = q < 0 ? 1 : 0;
   }
-  for (int i = 1; i < n; ++i) {
-    const double di = d[i], ei = e2[i - 1];
+  int i = 1;
+  for (; i + 8 <= n; i += 8) {
+    double dv[8], ev[8];
 #pragma unroll
-    for (int u = 0; u < EH_NP; ++u) {
-      double pn = fma(di - x[u], p1[u], -ei * p0[u]);
-      if (fabs(pn) < pivmin * fabs(p1[u])) pn = -pivmin * p1[u];   // ratio clamp
-      cnt[u] += ((__double_as_longlong(pn) ^ __double_as_longlong(p1[u])) < 0) ? 1 : 0;
-      p0[u] = p1[u];
-      p1[u] = pn;
+    for (int s = 0; s < 8; ++s) {
+      dv[s] = d[i + s];
+      ev[s] = e2[i + s - 1];
     }
-    if ((i & 7) == 7) {
 #pragma unroll
-      for (int u = 0; u < EH_NP; ++u) {
-        const double sc = eh_pow2_norm(fabs(p1[u]) > fabs(p0[u]) ? p1[u] : p0[u]);
-        p0[u] *= sc;
-        p1[u] *= sc;
-      }
+    for (int s = 0; s < 8; ++s) eh_sturm_step(dv[s], ev[s], x, pivmin, p0, p1, cnt);
+#pragma unroll
+    for (int u = 0; u < EH_NP; ++u) {   // rescale by a power of two every 8 steps
+      const double sc = eh_pow2_norm(fabs(p1[u]) > fabs(p0[u]) ? p1[u] : p0[u]);
+      p0[u] *= sc;
+      p1[u] *= sc;
     }
   }
+  for (; i < n; ++i) eh_sturm_step(d[i], e2[i - 1], x, pivmin, p0, p1, cnt);
 }
 
 // One warp per wanted eigenvalue: 128-point multisection (7 bits per round; four
@@ -561,13 +357,21 @@ __device__ __forceinline__ void eh_sturm_multi(int n, const double* __restrict__
 // Blocks k and k + 1 (when med_cnt > 0) compute the eigenvalues of descending rank
 // (med_cnt - 1) / 2 and med_cnt / 2 into med[0], med[1]: the median of the med_cnt
 // largest eigenvalues (Gavish-Donoho rank, Remark 2).
-__global__ void __launch_bounds__(32) eh_bisect_kernel(int n, int k, const double* __restrict__ d,
-                                                       const double* __restrict__ e2,
+__global__ void __launch_bounds__(32) eh_bisect_kernel(int n, int k, const double* d,
+                                                       const double* e2,
                                                        const double* __restrict__ bounds,
                                                        double* __restrict__ lam, int med_cnt,
                                                        double* __restrict__ med) {
   const int r0 = blockIdx.x, lane = threadIdx.x;
   if (r0 >= k + (med_cnt > 0 ? 2 : 0)) return;
+  extern __shared__ double bsm[];     // d[n], e2[n]
+  for (int i = lane; i < n; i += 32) {
+    bsm[i] = d[i];
+    bsm[n + i] = e2[i];
+  }
+  __syncwarp();
+  d = bsm;
+  e2 = bsm + n;
   const int r = r0 < k ? r0 : (r0 == k ? (med_cnt - 1) / 2 : med_cnt / 2);
   const int idx = n - 1 - r;
   double lo = bounds[0], hi = bounds[1];
@@ -811,9 +615,13 @@ cudaError_t launch_eh(int n, int k, const double* G, int64_t ldg, double* lam, d
   double* tau = e + n;
   double* wk = tau + n;
   cudaError_t err;
-  if (e16_ok(n)) {   // register-resident 16-CTA cluster (default where it can be scheduled)
-    if ((err = launch_e16(n, G, ldg, d, e, tau, V, st)) != cudaSuccess) return err;
-  } else {
+  // CDMD_PROFILE_FIT: CUDA events between the solver's kernels, printed to stderr
+  const bool prof = getenv("CDMD_PROFILE_FIT") != nullptr;
+  cudaEvent_t ev[6];
+  if (prof) for (int i = 0; i < 6; ++i) { cudaEventCreate(&ev[i]); }
+  auto mark = [&](int i) { if (prof) cudaEventRecord(ev[i], st); };
+  mark(0);
+  {
     const size_t smem = eh_tridiag_smem(n);
     err = cudaFuncSetAttribute(eh_tridiag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (err != cudaSuccess) return err;
@@ -821,19 +629,32 @@ cudaError_t launch_eh(int n, int k, const double* G, int64_t ldg, double* lam, d
     eh_tridiag_kernel<<<EH_CL, EH_T, smem, st>>>(n, G, ldg, d, e, tau, V);
     if ((err = cudaGetLastError()) != cudaSuccess) return err;
   }
+  mark(1);
   double* e2 = wk;
   double* bounds = e2 + n;
   note_launch();
   eh_prep_kernel<<<1, 256, 0, st>>>(n, d, e, e2, bounds);
   note_launch();
-  eh_bisect_kernel<<<k + (med_cnt > 0 ? 2 : 0), 32, 0, st>>>(n, k, d, e2, bounds, lam, med_cnt, med);
+  eh_bisect_kernel<<<k + (med_cnt > 0 ? 2 : 0), 32, sizeof(double) * 2 * (size_t)n, st>>>(n, k, d, e2, bounds, lam,
+                                                                                          med_cnt, med);
+  mark(2);
   note_launch();
   const size_t smem2 = sizeof(double) * 5 * (size_t)n + (size_t)n + 16;
   err = cudaFuncSetAttribute(eh_invit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
   if (err != cudaSuccess) return err;
   eh_invit_kernel<<<(unsigned)k, 32, smem2, st>>>(n, k, d, e, bounds, lam, Zout, info);
+  mark(3);
   note_launch();
   eh_backtransform_kernel<<<(unsigned)ceil_div(k, 4), 128, 0, st>>>(n, k, V, tau, Zout);
+  mark(4);
+  if (prof) {
+    cudaEventSynchronize(ev[4]);
+    float t[4];
+    for (int i = 0; i < 4; ++i) cudaEventElapsedTime(&t[i], ev[i], ev[i + 1]);
+    fprintf(stderr, "[cdmd_eh] tridiag %.3f  bisect %.3f  invit %.3f  backtransform %.3f ms\n", t[0], t[1], t[2],
+            t[3]);
+    for (int i = 0; i < 6; ++i) cudaEventDestroy(ev[i]);
+  }
   return cudaGetLastError();
 }
 

@@ -43,6 +43,7 @@ struct FitWs {
 size_t hqr_smem_bytes(int k);
 bool eh_supported(int n, int k);
 void eh_prof_read(unsigned long long* out);
+void hqr_prof_read(unsigned long long* out);
 size_t eh_work_doubles(int n, int k);
 cudaError_t launch_eh(int n, int k, const double* G, int64_t ldg, double* lam, double* Zout, double* work,
                       int* info, int med_cnt, double* med, cudaStream_t st);
@@ -587,7 +588,7 @@ cdmd_status fit_impl(cdmd_handle h, const void* Y, int64_t ldy, int kind, int64_
   {
     const int64_t N = p * m;
     note_launch();
-    if (kind == CDMD_GAUSSIAN)
+    if (kind == CDMD_GAUSSIAN || kind == CDMD_SRFT)
       to_f64_kernel<float><<<(unsigned)ceil_div(N, 256), 256, 0, st>>>((const float*)Y, ldy, p, m, W.Yd);
     else
       to_f64_kernel<int32_t><<<(unsigned)ceil_div(N, 256), 256, 0, st>>>((const int32_t*)Y, ldy, p, m, W.Yd);
@@ -709,11 +710,11 @@ cdmd_status fit_impl(cdmd_handle h, const void* Y, int64_t ldy, int kind, int64_
   CU(cudaStreamSynchronize(st));
   prof.mark("quant+sync");
   prof.report();
-  if (prof.on && syev_mode((int)n1, k) == 0) {
+  if (prof.on) {
     unsigned long long t[8];
-    eh_prof_read(t);
-    fprintf(stderr, "[cdmd_eh] load %llu  a %llu  sync %llu  c %llu  d %llu  e %llu (cycles, CTA 0)\n", t[0], t[1],
-            t[2], t[3], t[4], t[5]);
+    hqr_prof_read(t);
+    fprintf(stderr, "[cdmd_hqr] orthes %llu  ortran %llu  deflation %llu  m-search %llu  bulges %llu  iters %llu  steps %llu (cycles)\n",
+            t[0], t[1], t[2], t[3], t[4], t[5], t[6]);
   }
   model->K_eff = h->host_info[INFO_K_SEL];
   model->n_coef = h->host_info[INFO_N_COEF];

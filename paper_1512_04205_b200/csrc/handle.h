@@ -28,6 +28,7 @@ struct cdmd_handle_s {
   cusolverDnHandle_t solver = nullptr;
   cusolverDnParams_t params = nullptr;
   uint16_t* gauss_table = nullptr;   // device, 65536 bf16 bit patterns (immutable)
+  uint16_t* srft_table = nullptr;    // device, 16385 fp16 bit patterns of the SRFT quarter wave (immutable)
   int32_t* host_info = nullptr;      // pinned, 16 words for fit read-back
   // device, CDMD_SCHED_SLOTS tile counters of the persistent kernels (dynamic tile
   // schedule).  Every launch takes the next slot, so persistent launches of one handle

@@ -3,6 +3,7 @@
 // materialised: single pixel and sparse C become index lists (p and ~p ln n
 // entries), Rademacher and Gaussian entries are regenerated inside the sketch
 // kernels.  Cost is O(p) / O(p ln n) threads of Philox work per call.
+#include <cuda_fp16.h>
 #include <math.h>
 
 #include "common.cuh"
@@ -31,6 +32,7 @@ SensingPlan make_plan(int64_t n_total, const cdmd_sensing* c) {
 size_t sensing_ws_bytes(const SensingPlan& P) {
   auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
   if (P.kind == CDMD_SPIXEL) return al(sizeof(int32_t) * P.p);
+  if (P.kind == CDMD_SRFT) return al(sizeof(int32_t) * (P.p / 2 + 1));
   if (P.kind == CDMD_SPARSE)
     return al(sizeof(int32_t) * P.p * P.cap) + al(sizeof(int32_t) * P.p) + al(16);
   return 256;
@@ -42,7 +44,7 @@ size_t sensing_ws_bytes(const SensingPlan& P) {
 // restricted to [0, n) by cycle walking.  Distinct rows = sampling without
 // replacement.
 __global__ void spixel_rows_kernel(int64_t n, int64_t p, int h, uint32_t k0, uint32_t k1,
-                                   int32_t* __restrict__ rows) {
+                                   int32_t* __restrict__ rows, uint32_t tag) {
   const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= p) return;
   const uint64_t mask = (1ull << h) - 1ull;
@@ -51,7 +53,7 @@ __global__ void spixel_rows_kernel(int64_t n, int64_t p, int h, uint32_t k0, uin
     uint64_t L = x >> h, R = x & mask;
 #pragma unroll 1
     for (uint32_t i = 0; i < 6; ++i) {
-      const uint64_t f = (uint64_t)philox(make_uint4((uint32_t)R, i, 0u, TAG_SPIXEL), k0, k1).x & mask;
+      const uint64_t f = (uint64_t)philox(make_uint4((uint32_t)R, i, 0u, tag), k0, k1).x & mask;
       const uint64_t nl = R;
       R = L ^ f;
       L = nl;
@@ -64,7 +66,30 @@ __global__ void spixel_rows_kernel(int64_t n, int64_t p, int h, uint32_t k0, uin
 cudaError_t launch_spixel_rows(const SensingPlan& P, int32_t* rows, cudaStream_t st) {
   const int T = 128;
   note_launch();
-  spixel_rows_kernel<<<(unsigned)ceil_div(P.p, T), T, 0, st>>>(P.n, P.p, P.h, P.k0, P.k1, rows);
+  spixel_rows_kernel<<<(unsigned)ceil_div(P.p, T), T, 0, st>>>(P.n, P.p, P.h, P.k0, P.k1, rows, TAG_SPIXEL);
+  return cudaGetLastError();
+}
+
+// SRFT (reading R25): R = p/2 distinct frequencies, the same Feistel
+// bijection with its own tag
+cudaError_t launch_srft_freqs(const SensingPlan& P, int32_t* freqs, cudaStream_t st) {
+  const int T = 128;
+  const int64_t nf = P.p / 2;
+  note_launch();
+  spixel_rows_kernel<<<(unsigned)ceil_div(nf, T), T, 0, st>>>(P.n, nf, P.h, P.k0, P.k1, freqs, TAG_SRFT);
+  return cudaGetLastError();
+}
+
+// Q[r] = fp16_RNE(cos(2 pi r / 2^16)), r = 0 .. 2^14 (fp64 cos, one rounding)
+__global__ void srft_table_kernel(uint16_t* __restrict__ table) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r > 16384) return;
+  table[r] = __half_as_ushort(__double2half(cos(2.0 * 3.141592653589793238 * (double)r / 65536.0)));
+}
+
+cudaError_t launch_srft_table(uint16_t* table, cudaStream_t st) {
+  note_launch();
+  srft_table_kernel<<<(16385 + 255) / 256, 256, 0, st>>>(table);
   return cudaGetLastError();
 }
 

@@ -356,6 +356,24 @@ __global__ void __launch_bounds__(256) split_reduce_kernel(const float* __restri
   Y[r + t * ldy] = (float)s;
 }
 
+cudaError_t launch_sketch_tc2(const cdmd_video& v, const SensingPlan& P, const uint16_t* table, float* part,
+                              int* splits_out, const int32_t* freqs, cudaStream_t st);
+
+bool sketch_srft_supported(const cdmd_video& v) { return sketch_gaussian_tc2_supported(v); }
+
+// SRFT (reading R25): the Gaussian pair kernel with the SRFT generator, then the same
+// fixed-order split reduction
+cudaError_t launch_sketch_srft(const cdmd_video& v, const SensingPlan& P, const int32_t* freqs,
+                               const uint16_t* table, float* Y, int64_t ldy, float* part, cudaStream_t st) {
+  int splits = 0;
+  cudaError_t e = launch_sketch_tc2(v, P, table, part, &splits, freqs, st);
+  if (e != cudaSuccess) return e;
+  const int64_t total = P.p * v.m;
+  note_launch();
+  split_reduce_kernel<<<(unsigned)ceil_div(total, 256), 256, 0, st>>>(part, splits, P.p, v.m, Y, ldy);
+  return cudaGetLastError();
+}
+
 int64_t gaussian_part_floats(const cdmd_video& v, int64_t p) {
   const int s1 = gaussian_tc_splits(v, p), s2 = gaussian_tc2_splits(v, p);
   return (int64_t)(s1 > s2 ? s1 : s2) * v.m * p;

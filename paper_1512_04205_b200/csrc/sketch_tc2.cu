@@ -58,10 +58,20 @@ PFN_cuTensorMapEncodeTiled_v12000 g2_encode_fn() {
 // npad: frames + the row of ones, rounded up to 32.  MMA h (h = 0, 1) covers frames
 // [256 h, 256 h + N_h), N_0 = min(256, npad), N_1 = npad - N_0; CTA r of the pair holds
 // frames 256 h + r N_h / 2 + [0, N_h / 2) of it (B rows: h = 0 first, then h = 1).
+// SRFT (template SR = true, reading R25): the same pipeline with another generator.
+// A CTA's 128 rows of C are the Re (rows 0..63) and Im (rows 64..127) parts of 64
+// frequencies f of R; a generator thread owns one frequency and one 8-pixel chunk of
+// every 32-pixel stage and writes both rows.  Entry phase index q = phi_i - b_i (mod
+// 2^16) with b_i = floor(2^16 ((f i) mod n) / n) advanced by an exact integer
+// recurrence (b += floor(2^16 f / n), rem += 2^16 f mod n, carry at n), phi_i from
+// Philox(i / 8, 0, 0, TAG_SRFT_PHASE); the values come from the fp16 quarter-wave
+// table in shared memory.
+template <bool SR>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G2_THREADS, 1) sketch_gaussian_tc2_kernel(
     const __grid_constant__ CUtensorMap mapX0, const __grid_constant__ CUtensorMap mapX1, int64_t pix0,
     int64_t n_local, int64_t m, int64_t p, uint32_t k0, uint32_t k1, const uint16_t* __restrict__ table_bf16,
-    int npad, int nchunks_total, int chunks_per_split, float* __restrict__ part) {
+    int npad, int nchunks_total, int chunks_per_split, float* __restrict__ part, int64_t n_total,
+    const int32_t* __restrict__ freqs) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw;
   const int N0 = npad < 256 ? npad : 256, N1 = npad - N0;
@@ -90,9 +100,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G2_THREADS, 1) sketc
   const int c_begin = blockIdx.y * chunks_per_split;
   const int c_end = min(nchunks_total, c_begin + chunks_per_split);
   const int nch = c_end - c_begin;
-  for (int j = threadIdx.x; j < 32768; j += blockDim.x) {   // positive half of T as fp16 bits
-    const float v = __uint_as_float((uint32_t)table_bf16[32768 + j] << 16);
-    htab[j] = __half_as_ushort(__float2half_rn(v));         // exact: 8 significant bits
+  if (SR) {
+    for (int j = threadIdx.x; j <= 16384; j += blockDim.x) htab[j] = table_bf16[j];   // fp16 quarter wave
+  } else {
+    for (int j = threadIdx.x; j < 32768; j += blockDim.x) {   // positive half of T as fp16 bits
+      const float v = __uint_as_float((uint32_t)table_bf16[32768 + j] << 16);
+      htab[j] = __half_as_ushort(__float2half_rn(v));         // exact: 8 significant bits
+    }
   }
   if (warp == 0 && lane == 0) {
     for (int b = 0; b < G2_S; ++b) {
@@ -171,6 +185,82 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G2_THREADS, 1) sketc
         uint8_t* dst = sX + (size_t)xs * XST;
         tc::tma_load_2d(dst, &mapX0, &xfull[xs], px, (int)crank * h0r);
         if (h1r) tc::tma_load_2d(dst + (size_t)h0r * G2_XK, &mapX1, &xfull[xs], px, 256 + (int)crank * h1r);
+      }
+    }
+  } else if (warp <= G2_GEN && SR) {  // ------------------- SRFT generators, then epilogue
+    const int g = threadIdx.x - 32;
+    const int fr = g & 63, cq = g >> 6;         // frequency of the CTA, 8-pixel chunk of a stage
+    const int64_t nf = p / 2;
+    const int64_t fi = (int64_t)blockIdx.x * 64 + fr;
+    const bool fok = fi < nf;
+    const uint64_t n = (uint64_t)n_total;
+    const uint64_t f = fok ? (uint64_t)freqs[fi] : 0ull;
+    const uint32_t Qf = (uint32_t)((65536ull * f) / n), Rf = (uint32_t)((65536ull * f) % n);
+    const uint32_t Q24 = (uint32_t)((65536ull * 24ull * f) / n), R24 = (uint32_t)((65536ull * 24ull * f) % n);
+    const uint32_t nn = (uint32_t)n;
+    const uint64_t P0 = (uint64_t)pix0 + (uint64_t)c_begin * G2_BK + 8ull * cq;
+    const uint64_t a0 = (f * P0) % n;
+    uint32_t b = (uint32_t)((65536ull * a0) / n), rem = (uint32_t)((65536ull * a0) % n);
+    const int swzr = (fr >> 1) & 3, swzi = ((64 + fr) >> 1) & 3;
+    auto cosq = [&](uint32_t q) -> uint32_t {   // fp16 bits of cos(2 pi q / 2^16)
+      const uint32_t qd = (q >> 14) & 3u, r = q & 16383u;
+      const uint32_t idx = (qd & 1u) ? 16384u - r : r;
+      return (uint32_t)htab[idx] ^ ((((qd + 1u) >> 1) & 1u) << 15);
+    };
+    for (int i = 0; i < nch; ++i) {
+      const int st = i % G2_S;
+      const int gs = (i / G2_GRP) % G2_NG;
+      const uint32_t ph = (uint32_t)(i / (G2_GRP * G2_NG)) & 1u;
+      const bool gend = i % G2_GRP == G2_GRP - 1 || i == nch - 1;
+      const uint64_t Pc = (uint64_t)pix0 + (uint64_t)(c_begin + i) * G2_BK + 8ull * cq;   // multiple of 8
+      const uint4 w = philox(make_uint4((uint32_t)(Pc >> 3), 0u, 0u, TAG_SRFT_PHASE), k0, k1);
+      const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+      uint32_t re[4], im[4];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const uint32_t phi = (ws[u >> 1] >> (16 * (u & 1))) & 0xFFFFu;
+        const uint32_t q = (phi - b) & 0xFFFFu;
+        const uint32_t c = fok ? cosq(q) : 0u, sn = fok ? cosq((q - 16384u) & 0xFFFFu) : 0u;
+        if (u & 1) { re[u >> 1] |= c << 16; im[u >> 1] |= sn << 16; }
+        else { re[u >> 1] = c; im[u >> 1] = sn; }
+        b += Qf;                      // i -> i + 1
+        rem += Rf;
+        if (rem >= nn) { rem -= nn; ++b; }
+      }
+      b += Q24;                       // i + 8 -> i + 32: this thread's chunk of the next stage
+      rem += R24;
+      if (rem >= nn) { rem -= nn; ++b; }
+      if (i % G2_GRP == 0) tc::mbar_wait(&sempty[gs], ph ^ 1u);
+      *reinterpret_cast<uint4*>(sA + st * G2_A + fr * 64 + ((cq ^ swzr) << 4)) = make_uint4(re[0], re[1], re[2], re[3]);
+      *reinterpret_cast<uint4*>(sA + st * G2_A + (64 + fr) * 64 + ((cq ^ swzi) << 4)) =
+          make_uint4(im[0], im[1], im[2], im[3]);
+      if (gend) {
+        tc::fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(crank == 0 ? &afull[gs] : &lfullA[gs]);
+      }
+    }
+    if (warp <= 4) {  // epilogue: TMEM lane = row of the tile (Re 0..63, Im 64..127)
+      tc::mbar_wait(tfull, 0);
+      tc::fence_after();
+      const int q = warp & 3;
+      const int rr = q * 32 + lane;
+      const int64_t fq = (int64_t)blockIdx.x * 64 + (rr & 63);
+      const int64_t ry = rr < 64 ? fq : nf + fq;
+      const uint32_t ta = tmem_base + ((uint32_t)(q * 32) << 16);
+      uint32_t rs[16];
+      tc::tmem_ld16(ta + (uint32_t)(m & ~15), rs);
+      tc::tmem_ld_wait();
+      const float rowsum = __uint_as_float(rs[m & 15]);
+      for (int c0 = 0; c0 < (int)m; c0 += 16) {
+        uint32_t v[16];
+        tc::tmem_ld16(ta + c0, v);
+        tc::tmem_ld_wait();
+        if (fq < nf && nch > 0) {
+#pragma unroll
+          for (int t = 0; t < 16; ++t)
+            if (c0 + t < m) part[((int64_t)blockIdx.y * m + c0 + t) * p + ry] = fmaf(128.0f, rowsum, __uint_as_float(v[t]));
+        }
       }
     }
   } else if (warp <= G2_GEN) {  // ---------------------------- C generators, then epilogue
@@ -339,8 +429,9 @@ int gaussian_tc2_splits(const cdmd_video& v, int64_t p) {
 }
 
 // part: splits x m x p fp32 partial sums (reduced by the caller)
-cudaError_t launch_sketch_gaussian_tc2(const cdmd_video& v, const SensingPlan& P, const uint16_t* table, float* part,
-                                       int* splits_out, cudaStream_t st) {
+cudaError_t launch_sketch_tc2(const cdmd_video& v, const SensingPlan& P, const uint16_t* table, float* part,
+                              int* splits_out, const int32_t* freqs, cudaStream_t st) {
+  const bool sr = P.kind == CDMD_SRFT;
   const int npad = (int)round_up(v.m + 1, 32);     // frames + the row of ones
   const int N0 = npad < 256 ? npad : 256, N1 = npad - N0;
   const int npairs = (int)ceil_div(P.p, 2 * G2_BM);
@@ -369,14 +460,20 @@ cudaError_t launch_sketch_gaussian_tc2(const cdmd_video& v, const SensingPlan& P
   const size_t brows = (size_t)(N0 + N1) / 2;
   const size_t smem = 1024 + (size_t)G2_S * (G2_A + brows * G2_BK * 2) + (size_t)G2_XS * brows * G2_XK + 65536 + 768;
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
-  cudaError_t e = cudaFuncSetAttribute(sketch_gaussian_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  auto kern = sr ? sketch_gaussian_tc2_kernel<true> : sketch_gaussian_tc2_kernel<false>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   *splits_out = splits;
   dim3 grid((unsigned)(2 * npairs), (unsigned)splits);
   note_launch();
-  sketch_gaussian_tc2_kernel<<<grid, G2_THREADS, smem, st>>>(mapX0, mapX1, v.pix0, v.n_local, v.m, P.p, P.k0, P.k1,
-                                                             table, npad, nchunks, cps, part);
+  kern<<<grid, G2_THREADS, smem, st>>>(mapX0, mapX1, v.pix0, v.n_local, v.m, P.p, P.k0, P.k1, table, npad, nchunks,
+                                       cps, part, P.n, freqs);
   return cudaGetLastError();
+}
+
+cudaError_t launch_sketch_gaussian_tc2(const cdmd_video& v, const SensingPlan& P, const uint16_t* table, float* part,
+                                       int* splits_out, cudaStream_t st) {
+  return launch_sketch_tc2(v, P, table, part, splits_out, nullptr, st);
 }
 
 }  // namespace cdmd

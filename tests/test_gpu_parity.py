@@ -20,7 +20,7 @@ import parity as PT  # tests/parity.py (tests/ is on sys.path under pytest)
 
 pytestmark = pytest.mark.gpu
 
-KIND = {"spixel": 0, "sparse": 1, "rademacher": 2, "gaussian": 3}
+KIND = {"spixel": 0, "sparse": 1, "rademacher": 2, "gaussian": 3, "srft": 4}
 
 
 @pytest.fixture(scope="module")
@@ -88,7 +88,7 @@ def oracle_run(X, kind, p, k, K, tau, s=None, seed=0, rank="fixed", omega_eps=No
 
 def check_all(g, o, kind, tau):
     # sketch
-    if kind == "gaussian":
+    if kind in ("gaussian", "srft"):
         d = np.linalg.norm(g["Y"] - o["Y"], axis=0) / np.linalg.norm(o["Y"], axis=0)
         assert d.max() <= PT.RTOL_Y_GAUSS, d.max()
     else:
@@ -191,6 +191,8 @@ CASES = [
     ("ragged_spixel", (97, 61, 45, 2.0, 2), "spixel", 400, 15, 6, 25.0),
     ("rademacher_small", (180, 120, 60, 2.0, 2), "rademacher", 300, 20, 6, 25.0),
     ("gaussian_small", (160, 100, 50, 2.0, 1), "gaussian", 256, 16, 6, 25.0),
+    ("srft_small", (160, 100, 50, 2.0, 1), "srft", 256, 16, 6, 25.0),
+    ("srft_ragged", (97, 61, 45, 2.0, 2), "srft", 202, 15, 6, 25.0),
 ]
 
 
@@ -278,6 +280,41 @@ def test_sparse_sorted_sketch_equals_ell(C, H, W, Hh, m, p, slabs, monkeypatch):
         if W < 1000:
             want = OS.sketch(X[:, p0:p0 + nl], OS.SPARSE, p, q + 3, n_total=n, pix0=p0)
             assert np.array_equal(a.cpu().numpy().T.astype(np.int64), want)
+
+
+def test_srft_table_and_frequencies_bit_exact(C, H):
+    """SRFT (reading R25): the device's fp16 quarter-wave table and the frequencies of R
+    equal the oracle's bit for bit."""
+    out = torch.zeros(16385, dtype=torch.int16, device="cuda")
+    C.cdmd_srft_table(H, out)
+    got = out.cpu().numpy().view(np.float16).astype(np.float64)
+    r = np.arange(16385, dtype=np.float64)
+    want = np.cos(2.0 * np.pi * r / 65536.0).astype(np.float16).astype(np.float64)
+    assert np.array_equal(got, want)
+    for n, p, seed in [(768, 200, 3), (2073600, 2000, 0), (97 * 61, 202, 0), (1000, 2000, 5)]:
+        fr = torch.zeros(p // 2, dtype=torch.int32, device="cuda")
+        C.cdmd_sensing_rows(H, n, C.sensing("srft", p, 0, seed), fr)
+        assert np.array_equal(fr.cpu().numpy().astype(np.int64), OS.srft_freqs(n, p // 2, seed))
+
+
+@pytest.mark.parametrize("W,Hh,m,p,slabs", [(160, 100, 50, 256, 1), (333, 101, 77, 202, 2), (720, 480, 300, 1500, 1)])
+def test_srft_sketch_normwise(C, H, W, Hh, m, p, slabs):
+    """The SRFT sketch on fp16 tensor cores (exact fp16 x fp16 products, fp32 sums) against
+    the oracle's fp64 product with the same C, per column normwise <= 1e-4, on whole
+    frames and on pixel slabs whose partial sketches add up."""
+    X = make_video(W, Hh, m, seed=W + p, noise=2.0, n_rects=2)
+    n = X.shape[1]
+    from paper_1512_04205_b200.dist import slab
+    acc = None
+    for q in range(slabs):
+        p0, nl = slab(n, slabs, q)
+        P = C.Pipeline(H, n, nl, m, "srft", p, 8, 2, pix0=p0)
+        Y = P.sketch(to_dev(X[:, p0:p0 + nl])).cpu().numpy().T.astype(np.float64)
+        acc = Y if acc is None else acc + Y
+    rows = np.arange(p) if W < 700 else np.r_[0:8, p // 2:p // 2 + 8, p - 4:p]
+    want = OS.sketch(X, OS.SRFT, p, 0, rows=rows)
+    d = np.linalg.norm(acc[rows] - want, axis=0) / np.linalg.norm(want, axis=0)
+    assert d.max() <= PT.RTOL_Y_GAUSS, d.max()
 
 
 def test_c3_rademacher_full_size_sampled_rows(C, H):
