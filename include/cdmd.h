@@ -197,9 +197,9 @@ CDMD_API cdmd_status cdmd_sketch(cdmd_handle h, const cdmd_video* v, const cdmd_
  * + 1.43, b = min(p, m-1) / max(p, m-1), at most -k and at least 1; the result is
  * model->k_eff.  BLOCKING: returns after the model is complete.  Errors:
  * CDMD_ERR_RANGE if |k| < 1, |k| > min(p, m-1), K < 1 or K > |k|;
- * CDMD_ERR_UNSUPPORTED for k < 0 when m - 1 > 510 (that size's eigensolver returns
- * only the k largest eigenvalues); CDMD_ERR_NUMERIC if the eigensolvers fail or
- * every sigma is dropped (model->info holds the solver info). */
+ * CDMD_ERR_NUMERIC if the eigensolvers fail or every sigma is dropped (model->info
+ * holds the solver info).  m - 1 > 510: the symmetric eigensolve is cuSOLVER's
+ * (syevdx for the k largest; syevd, every eigenvalue, for k < 0). */
 CDMD_API size_t cdmd_model_bytes(int k, int K, int64_t m);
 CDMD_API cdmd_status cdmd_model_bind(cdmd_model* model, void* dev_buf, size_t bytes, int k, int K, int64_t m);
 CDMD_API size_t cdmd_fit_workspace_bytes(cdmd_handle h, int64_t p, int64_t m, int k);

@@ -383,7 +383,7 @@ cdmd_status cdmd_foreground(cdmd_handle h, const cdmd_video* v, const cdmd_model
   if (ldw < ceil_div(v->n_local, 32)) return CDMD_ERR_ARG;
   if (!Phi) {   // N11: the support's modes computed in-slab from X (fused_tc.cu)
     if (!fused_supported(*v, *M, mode)) return CDMD_ERR_UNSUPPORTED;
-    return cuda_status(launch_fused_fg(*v, *M, tau, mask, ldw, sched_slot(h), (cudaStream_t)st));
+    return cuda_status(launch_fused_fg(*v, *M, mode, tau, mask, ldw, sched_slot(h), (cudaStream_t)st));
   }
   if (ldphi < v->n_local) return CDMD_ERR_ARG;
   return cuda_status(launch_foreground(*v, *M, Phi, ldphi, mode, tau, mask, ldw, sched_slot(h), (cudaStream_t)st));

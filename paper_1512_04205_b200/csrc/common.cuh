@@ -127,10 +127,10 @@ cudaError_t launch_foreground(const cdmd_video& v, const cdmd_model& M, const fl
                               int64_t ldphi, int mode, float tau, uint32_t* mask, int64_t ldw,
                               int* tile_counter, cudaStream_t st);
 
-// N11 fused single pass (fused_tc.cu): dynamic background, n_coef <= 16, m <= 512
+// N11 fused single pass (fused_tc.cu): dynamic or static background, n_coef <= 16, m <= 512
 bool fused_supported(const cdmd_video& v, const cdmd_model& M, int mode);
-cudaError_t launch_fused_fg(const cdmd_video& v, const cdmd_model& M, float tau, uint32_t* mask, int64_t ldw,
-                            int* tile_counter, cudaStream_t st);
+cudaError_t launch_fused_fg(const cdmd_video& v, const cdmd_model& M, int mode, float tau, uint32_t* mask,
+                            int64_t ldw, int* tile_counter, cudaStream_t st);
 
 cudaError_t launch_mask_median3(const uint32_t* in, int64_t ldw, int64_t W, int64_t H, int64_t m, uint32_t* out,
                                 cudaStream_t st);

@@ -745,17 +745,31 @@ __global__ void __launch_bounds__(32) hqrv_kernel(int nn, const double* __restri
       wp.sync();
       const double ih = 1.0 / h;
       for (int j = m + lane; j < nn; j += 32) {   // H = (I - u u'/h) H
-        double f = 0.0;
-        for (int i = high; i >= m; --i) f += ort[i] * Hx(i, j);
-        f *= ih;
-        for (int i = m; i <= high; ++i) Hx(i, j) -= f * ort[i];
+        double f0 = 0.0, f1 = 0.0, f2 = 0.0, f3 = 0.0;   // four chains: the dot is latency-bound
+        int i = high;
+        for (; i - 3 >= m; i -= 4) {
+          f0 += ort[i] * Hx(i, j);
+          f1 += ort[i - 1] * Hx(i - 1, j);
+          f2 += ort[i - 2] * Hx(i - 2, j);
+          f3 += ort[i - 3] * Hx(i - 3, j);
+        }
+        for (; i >= m; --i) f0 += ort[i] * Hx(i, j);
+        const double f = ((f0 + f1) + (f2 + f3)) * ih;
+        for (int i2 = m; i2 <= high; ++i2) Hx(i2, j) -= f * ort[i2];
       }
       wp.sync();
       for (int i = lane; i <= high; i += 32) {   // H = H (I - u u'/h)
-        double f = 0.0;
-        for (int j = high; j >= m; --j) f += ort[j] * Hx(i, j);
-        f *= ih;
-        for (int j = m; j <= high; ++j) Hx(i, j) -= f * ort[j];
+        double f0 = 0.0, f1 = 0.0, f2 = 0.0, f3 = 0.0;
+        int j = high;
+        for (; j - 3 >= m; j -= 4) {
+          f0 += ort[j] * Hx(i, j);
+          f1 += ort[j - 1] * Hx(i, j - 1);
+          f2 += ort[j - 2] * Hx(i, j - 2);
+          f3 += ort[j - 3] * Hx(i, j - 3);
+        }
+        for (; j >= m; --j) f0 += ort[j] * Hx(i, j);
+        const double f = ((f0 + f1) + (f2 + f3)) * ih;
+        for (int j2 = m; j2 <= high; ++j2) Hx(i, j2) -= f * ort[j2];
       }
       wp.sync();
       if (lane == 0) {
@@ -772,10 +786,17 @@ __global__ void __launch_bounds__(32) hqrv_kernel(int nn, const double* __restri
       for (int i = m + 1 + lane; i <= high; i += 32) ort[i] = Hx(i, m - 1);
       wp.sync();
       for (int j = m + lane; j <= high; j += 32) {
-        double g = 0.0;
-        for (int i = m; i <= high; ++i) g += ort[i] * Vx(i, j);
-        g = (g / ort[m]) / Hx(m, m - 1);
-        for (int i = m; i <= high; ++i) Vx(i, j) += g * ort[i];
+        double g0 = 0.0, g1 = 0.0, g2 = 0.0, g3 = 0.0;
+        int i = m;
+        for (; i + 3 <= high; i += 4) {
+          g0 += ort[i] * Vx(i, j);
+          g1 += ort[i + 1] * Vx(i + 1, j);
+          g2 += ort[i + 2] * Vx(i + 2, j);
+          g3 += ort[i + 3] * Vx(i + 3, j);
+        }
+        for (; i <= high; ++i) g0 += ort[i] * Vx(i, j);
+        const double g = (((g0 + g1) + (g2 + g3)) / ort[m]) / Hx(m, m - 1);
+        for (int i2 = m; i2 <= high; ++i2) Vx(i2, j) += g * ort[i2];
       }
       wp.sync();
     }
@@ -960,9 +981,10 @@ __global__ void __launch_bounds__(32) hqrv_kernel(int nn, const double* __restri
             newsub = -Hx(kk, kk - 1);
             setsub = true;
           }
-          wp.sync();
+          // H(kk, kk-1) is touched by no other update of this step (rows kk.. / columns
+          // kk..kk+2 below): no barrier around its store, the step's later barriers order it
+          wp.sync();   // every lane has read H(kk, kk-1) above
           if (setsub && lane == 0) Hx(kk, kk - 1) = newsub;
-          wp.sync();
           p = p + s;
           const double is = rcp_nr(s), ip = rcp_nr(p);
           x = p * is;

@@ -357,19 +357,20 @@ __device__ __forceinline__ void eh_sturm_multi(int n, const double* __restrict__
 // Blocks k and k + 1 (when med_cnt > 0) compute the eigenvalues of descending rank
 // (med_cnt - 1) / 2 and med_cnt / 2 into med[0], med[1]: the median of the med_cnt
 // largest eigenvalues (Gavish-Donoho rank, Remark 2).
-__global__ void __launch_bounds__(32) eh_bisect_kernel(int n, int k, const double* d,
-                                                       const double* e2,
-                                                       const double* __restrict__ bounds,
-                                                       double* __restrict__ lam, int med_cnt,
-                                                       double* __restrict__ med) {
-  const int r0 = blockIdx.x, lane = threadIdx.x;
+constexpr int EH_BW = 8;   // warps per eigenvalue: 32 EH_BW EH_NP points per multisection round
+__global__ void __launch_bounds__(32 * EH_BW) eh_bisect_kernel(int n, int k, const double* d, const double* e2,
+                                                               const double* __restrict__ bounds,
+                                                               double* __restrict__ lam, int med_cnt,
+                                                               double* __restrict__ med) {
+  const int r0 = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (r0 >= k + (med_cnt > 0 ? 2 : 0)) return;
   extern __shared__ double bsm[];     // d[n], e2[n]
-  for (int i = lane; i < n; i += 32) {
+  __shared__ int wsum[2][EH_BW];
+  for (int i = tid; i < n; i += 32 * EH_BW) {
     bsm[i] = d[i];
     bsm[n + i] = e2[i];
   }
-  __syncwarp();
+  __syncthreads();
   d = bsm;
   e2 = bsm + n;
   const int r = r0 < k ? r0 : (r0 == k ? (med_cnt - 1) / 2 : med_cnt / 2);
@@ -377,27 +378,32 @@ __global__ void __launch_bounds__(32) eh_bisect_kernel(int n, int k, const doubl
   double lo = bounds[0], hi = bounds[1];
   const double pivmin = bounds[3];
   const double eps = 2.220446049250313e-16;
-  constexpr int NPT = 32 * EH_NP;   // points per round, at lo + (hi - lo) t / (NPT + 1)
+  constexpr int NPT = 32 * EH_BW * EH_NP;   // points per round, at lo + (hi - lo) t / (NPT + 1)
   for (int round = 0; round < 40; ++round) {
-    if (hi - lo <= 2.0 * eps * fmax(fabs(lo), fabs(hi)) + pivmin) break;
+    if (hi - lo <= 2.0 * eps * fmax(fabs(lo), fabs(hi)) + pivmin) break;   // uniform across the CTA
     double x[EH_NP];
     int c[EH_NP];
 #pragma unroll
-    for (int u = 0; u < EH_NP; ++u) x[u] = lo + (hi - lo) * (double)(EH_NP * lane + u + 1) / (double)(NPT + 1);
+    for (int u = 0; u < EH_NP; ++u) x[u] = lo + (hi - lo) * (double)(EH_NP * tid + u + 1) / (double)(NPT + 1);
     eh_sturm_multi(n, d, e2, x, pivmin, c);
     // points with count <= idx lie below the eigenvalue; counts are monotone in the
-    // point index, so the number below is the total over lanes and chains
+    // point index, so the number below is the total over threads and chains
     int nbl = 0;
 #pragma unroll
     for (int u = 0; u < EH_NP; ++u) nbl += c[u] <= idx ? 1 : 0;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) nbl += __shfl_xor_sync(0xffffffffu, nbl, o);
+    if (lane == 0) wsum[round & 1][warp] = nbl;
+    __syncthreads();
+    nbl = 0;
+#pragma unroll
+    for (int w = 0; w < EH_BW; ++w) nbl += wsum[round & 1][w];
     const double nlo = nbl > 0 ? lo + (hi - lo) * (double)nbl / (double)(NPT + 1) : lo;
     const double nhi = nbl < NPT ? lo + (hi - lo) * (double)(nbl + 1) / (double)(NPT + 1) : hi;
     lo = nlo;
     hi = nhi;
   }
-  if (lane == 0) {
+  if (tid == 0) {
     if (r0 < k) lam[k - 1 - r] = 0.5 * (lo + hi);
     else med[r0 - k] = 0.5 * (lo + hi);
   }
@@ -635,8 +641,8 @@ cudaError_t launch_eh(int n, int k, const double* G, int64_t ldg, double* lam, d
   note_launch();
   eh_prep_kernel<<<1, 256, 0, st>>>(n, d, e, e2, bounds);
   note_launch();
-  eh_bisect_kernel<<<k + (med_cnt > 0 ? 2 : 0), 32, sizeof(double) * 2 * (size_t)n, st>>>(n, k, d, e2, bounds, lam,
-                                                                                          med_cnt, med);
+  eh_bisect_kernel<<<k + (med_cnt > 0 ? 2 : 0), 32 * EH_BW, sizeof(double) * 2 * (size_t)n, st>>>(
+      n, k, d, e2, bounds, lam, med_cnt, med);
   mark(2);
   note_launch();
   const size_t smem2 = sizeof(double) * 5 * (size_t)n + (size_t)n + 16;

@@ -606,13 +606,15 @@ cdmd_status fit_impl(cdmd_handle h, const void* Y, int64_t ldy, int kind, int64_
   size_t hneed = W.sy_host_bytes > W.ge_host_bytes ? W.sy_host_bytes : W.ge_host_bytes;
   if (h->host_ws.size() < hneed + 16) h->host_ws.resize(hneed + 16);
   int64_t top = n1 - 1;
-  const int smode = syev_mode((int)n1, k);
+  // Gavish-Donoho needs every singular value of Y (the median): beyond the cluster
+  // solver's size (n1 > 510, C5) it takes cuSOLVER's full syevd instead of syevdx
+  int smode = syev_mode((int)n1, k);
+  if (gd && smode == 2) smode = 1;
   // the median singular value runs over all min(p, m-1) singular values of Y
   const int med_cnt = gd ? (int)(p < n1 ? p : n1) : 0;
   const double beta = (double)(p < n1 ? p : n1) / (double)(p < n1 ? n1 : p);
   const double gd_omega = gd ? 0.56 * beta * beta * beta - 0.95 * beta * beta + 1.82 * beta + 1.43 : 0.0;
   double* med = W.ehw + eh_work_doubles((int)n1, k) - 8;   // two doubles of the eigh workspace slack
-  if (gd && smode == 2) return CDMD_ERR_UNSUPPORTED;      // syevdx computes only the k largest
   if (smode == 0) {
     // cluster tridiagonalisation + bisection + inverse iteration; k largest pairs
     // written ascending into (W.w, W.A) like syevdx

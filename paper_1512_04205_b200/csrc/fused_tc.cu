@@ -22,7 +22,8 @@
 // X is read from HBM once; the full Phi is never written (Alg. 1's Phi output is
 // cdmd_modes' job).  The X stages of a tile stay resident from phase A to the mask,
 // two tiles in flight (8 stages of 16 KB at m <= 512).  Warp roles: 0 TMA producer,
-// 1 TMEM owner + MMA issuer (A of tile i, then B of tile i-1), 2-5 convert, 6-13 mask.
+// 1 TMEM owner + phase A issuer, 2-5 convert, 6-13 mask, 14 phase B issuer; the
+// producer starts loading while the other warps build the resident operands.
 #include <cuda_bf16.h>
 #include <cudaTypedefs.h>
 
@@ -41,7 +42,8 @@ constexpr int FU_PW = FU_BM / (FU_MASK_WARPS / 4);   // pixels per mask warp
 constexpr int FU_NW = FU_PW / 32;          // mask words per thread per stage
 constexpr int FU_CONV_WARP0 = 2;           // warps 2..5: TMEM lane quarters 2, 3, 0, 1
 constexpr int FU_MASK_WARP0 = 6;           // warps 6..13: quarters (warp % 4) x 2 pixel slices
-constexpr int FU_THREADS = 32 * (FU_MASK_WARP0 + FU_MASK_WARPS);
+constexpr int FU_BWARP = FU_MASK_WARP0 + FU_MASK_WARPS;   // phase B issuer (warp 14)
+constexpr int FU_THREADS = 32 * (FU_BWARP + 1);
 constexpr int FU_MAX_FB = 4;               // m <= 512
 
 __device__ __forceinline__ uint32_t fu_km_off(int r, int c, int KP) {
@@ -95,6 +97,16 @@ __device__ __forceinline__ uint32_t fu_mask32(const uint32_t (&xw)[8], const uin
   return ~word;
 }
 
+// STATIC (template ST): no phase B; the convert warps reduce Phi_F of each
+// pixel to its static background L = sum_f Phi_F[f] c_f(1) (the fmaf order of
+// foreground.cu's static kernel) and the integer bounds x > floor(L + tau), x <
+// ceil(L - tau) (bytes, plus an "always" bit); the mask warps compare four pixels per
+// byte-SIMD instruction against them.
+__device__ __forceinline__ uint32_t fu_movemask4(uint32_t v) {  // bytes 0x00/0xFF -> 4 bits
+  return ((v & 0x01010101u) * 0x10204080u) >> 28;
+}
+
+template <bool ST>
 __global__ void __launch_bounds__(FU_THREADS, 1) fused_fg_kernel(
     const __grid_constant__ CUtensorMap mapX, int64_t n_local, int64_t m, int nfb, int64_t mpad, int kpad,
     const int8_t* __restrict__ Mq, const double* __restrict__ Mq_scale, const float* __restrict__ coef,
@@ -121,40 +133,13 @@ __global__ void __launch_bounds__(FU_THREADS, 1) fused_fg_kernel(
   __shared__ int tq_id[tc::TQ_N];
   __shared__ uint64_t tq_bar[2 * tc::TQ_N];
   __shared__ float sScale[FU_NC];
+  __shared__ float sC0[FU_NC];                              // ST: c_f(1)
+  __shared__ __align__(16) uint8_t sHi[2][FU_BM], sLo[2][FU_BM];   // ST: per-pixel byte bounds, by tile parity
+  __shared__ uint32_t sAlw[2][FU_BM / 32];                  // ST: pixels outside [0, 255] +- tau: always set
+  __shared__ uint64_t bnd_full[2], bnd_empty[2];
   const tc::TileQueue tq{tq_id, tq_bar, tq_bar + tc::TQ_N};
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-  // ---- resident operands: Mq' (shifted limbs of the support columns) and H (+ constant)
-  for (int f = threadIdx.x; f < FU_NC; f += blockDim.x)
-    sScale[f] = f < n_coef ? (float)Mq_scale[coef_col[f]] : 0.f;
-  const int nchunks = FU_NA * nfb * 8;          // 16-B chunks of Mq'
-  for (int q = threadIdx.x; q < nchunks; q += blockDim.x) {
-    const int row = q / (nfb * 8), rest = q % (nfb * 8);
-    const int kb = rest >> 3, c = rest & 7;
-    const int l = row / FU_NC, f = row % FU_NC;
-    const int8_t* src = (f < n_coef) ? Mq + ((int64_t)l * kpad + coef_col[f]) * mpad : nullptr;
-    uint32_t w[4] = {0u, 0u, 0u, 0u};
-#pragma unroll
-    for (int b = 0; b < 16; ++b) {
-      const int64_t t = (int64_t)kb * FU_BK + c * 16 + b;    // frame of X (X' frame t - 1)
-      const uint32_t v = (src && t >= 1 && t <= m - 1) ? (uint32_t)(uint8_t)__ldg(src + t - 1) : 0u;
-      w[b >> 2] |= v << (8 * (b & 3));
-    }
-    *reinterpret_cast<uint4*>(sQ + (size_t)kb * FU_NA * FU_BK + row * 128 + ((c ^ (row & 7)) << 4)) =
-        make_uint4(w[0], w[1], w[2], w[3]);
-  }
-  for (int idx = threadIdx.x; idx < mA * FU_NC; idx += blockDim.x) {
-    const int t = idx / FU_NC, f = idx % FU_NC;
-    const float v = (t < m && f < n_coef) ? coef[(int64_t)f * m + t] : 0.f;
-    const __nv_bfloat16 a = __float2bfloat16_rn(v);
-    const float r1 = v - __bfloat162float(a);
-    const __nv_bfloat16 b = __float2bfloat16_rn(r1);
-    const __nv_bfloat16 c = __float2bfloat16_rn(r1 - __bfloat162float(b));
-    const uint32_t off = fu_km_off(t, f >> 3, FU_NC) + (f & 7) * 2;
-    *reinterpret_cast<__nv_bfloat16*>(sH + off) = a;
-    *reinterpret_cast<__nv_bfloat16*>(sH + PART_A + off) = b;
-    *reinterpret_cast<__nv_bfloat16*>(sH + 2 * PART_A + off) = c;
-  }
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < stages; ++s) {
       tc::mbar_init(&xfull[s], 1);
@@ -168,16 +153,58 @@ __global__ void __launch_bounds__(FU_THREADS, 1) fused_fg_kernel(
     }
     tc::mbar_init(pfull, 4);
     tc::mbar_init(pempty, 1);
-    tc::tq_init(tq, 1 + 4 + FU_MASK_WARPS);
+    for (int b = 0; b < 2; ++b) {
+      tc::mbar_init(&bnd_full[b], 4);
+      tc::mbar_init(&bnd_empty[b], FU_MASK_WARPS);
+    }
+    tc::tq_init(tq, (ST ? 1 : 2) + 4 + FU_MASK_WARPS);   // A issuer, [B issuer,] convert, mask
     tc::fence_mbar_init();
     tc::tma_prefetch(&mapX);
   }
   if (warp == 1) tc::tmem_alloc(tmem_slot, 512);
-  tc::fence_proxy_async();   // generic-proxy smem writes (Mq', H) -> async proxy (MMA)
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // the TMA producer starts right away; every other warp builds the resident operands
+  // (the shifted limbs Mq' and the split H) and meets the others at named barrier 1
+  if (warp != 0) {
+    const int ntb = blockDim.x - 32, t0 = threadIdx.x - 32;
+    for (int f = t0; f < FU_NC; f += ntb) {
+      sScale[f] = f < n_coef ? (float)Mq_scale[coef_col[f]] : 0.f;
+      sC0[f] = f < n_coef ? coef[(int64_t)f * m] : 0.f;
+    }
+    const int nchunks = FU_NA * nfb * 8;          // 16-B chunks of Mq'
+    for (int q = t0; q < nchunks; q += ntb) {
+      const int row = q / (nfb * 8), rest = q % (nfb * 8);
+      const int kb = rest >> 3, c = rest & 7;
+      const int l = row / FU_NC, f = row % FU_NC;
+      const int8_t* src = (f < n_coef) ? Mq + ((int64_t)l * kpad + coef_col[f]) * mpad : nullptr;
+      uint32_t w[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+      for (int b = 0; b < 16; ++b) {
+        const int64_t t = (int64_t)kb * FU_BK + c * 16 + b;    // frame of X (X' frame t - 1)
+        const uint32_t v = (src && t >= 1 && t <= m - 1) ? (uint32_t)(uint8_t)__ldg(src + t - 1) : 0u;
+        w[b >> 2] |= v << (8 * (b & 3));
+      }
+      *reinterpret_cast<uint4*>(sQ + (size_t)kb * FU_NA * FU_BK + row * 128 + ((c ^ (row & 7)) << 4)) =
+          make_uint4(w[0], w[1], w[2], w[3]);
+    }
+    for (int idx = t0; idx < (ST ? 0 : mA * FU_NC); idx += ntb) {
+      const int t = idx / FU_NC, f = idx % FU_NC;
+      const float v = (t < m && f < n_coef) ? coef[(int64_t)f * m + t] : 0.f;
+      const __nv_bfloat16 a = __float2bfloat16_rn(v);
+      const float r1 = v - __bfloat162float(a);
+      const __nv_bfloat16 b = __float2bfloat16_rn(r1);
+      const __nv_bfloat16 c = __float2bfloat16_rn(r1 - __bfloat162float(b));
+      const uint32_t off = fu_km_off(t, f >> 3, FU_NC) + (f & 7) * 2;
+      *reinterpret_cast<__nv_bfloat16*>(sH + off) = a;
+      *reinterpret_cast<__nv_bfloat16*>(sH + PART_A + off) = b;
+      *reinterpret_cast<__nv_bfloat16*>(sH + 2 * PART_A + off) = c;
+    }
+    tc::fence_proxy_async();   // generic-proxy smem writes (Mq', H) -> async proxy (MMA)
+    asm volatile("bar.sync 1, %0;" ::"r"(ntb) : "memory");
+  }
   // TMEM columns: phase A accumulators [0, 64) and [64, 128); phase B [128, 256), [256, 384)
 
   if (warp == 0) {
@@ -198,14 +225,37 @@ __global__ void __launch_bounds__(FU_THREADS, 1) fused_fg_kernel(
   } else if (warp == 1) {
     if (lane == 0) {  // --------------------------------------------- MMA issuer
       constexpr uint32_t IDA = tc::idesc_i8(FU_BM, FU_NA, false, true, true, false);
-      constexpr uint32_t IDB = tc::idesc_f16(FU_BK, FU_BM, true, true, false, false);
-      const uint32_t xBase = tc::smem_u32(sX), qBase = tc::smem_u32(sQ), hBase = tc::smem_u32(sH),
-                     pBase = tc::smem_u32(sP);
+      const uint32_t xBase = tc::smem_u32(sX), qBase = tc::smem_u32(sQ);
       int stage = 0;
       uint32_t phase = 0;
+      for (int ti = 0;; ++ti) {   // phase A only: phase B has an issuer of its own
+        if (tc::tq_take(tq, ti) < 0) break;
+        const int ab = ti & 1;
+        tc::mbar_wait(&aempty[ab], ((uint32_t)(ti >> 1) & 1u) ^ 1u);
+        tc::fence_after();
+        const uint32_t d = tmem_base + (uint32_t)(ab * FU_NA);
+        for (int fb = 0; fb < nfb; ++fb) {
+          tc::mbar_wait(&xfull[stage], phase);
+          tc::fence_after();
+#pragma unroll
+          for (int kk = 0; kk < FU_BK / 32; ++kk) {
+            const uint64_t ad = tc::smem_desc_sw128(xBase + stage * FU_STAGE + kk * 32 * 128, FU_STAGE, 1024);
+            const uint64_t bd = tc::smem_desc_sw128(qBase + fb * FU_NA * FU_BK + kk * 32, 0, 1024);
+            tc::mma_i8(d, ad, bd, IDA, (fb | kk) != 0);
+          }
+          if (++stage == stages) { stage = 0; phase ^= 1u; }
+        }
+        tc::mma_commit(&afull[ab]);
+      }
+    }
+  } else if (warp == FU_BWARP) {
+    if (lane == 0 && !ST) {  // ------------------------------------ phase B issuer
+      constexpr uint32_t IDB = tc::idesc_f16(FU_BK, FU_BM, true, true, false, false);
+      const uint32_t hBase = tc::smem_u32(sH), pBase = tc::smem_u32(sP);
       int itB = 0;
-      auto issue_b = [&](int u) {   // phase B of the u-th tile of this CTA
-        tc::mbar_wait(pfull, (uint32_t)u & 1u);
+      for (int u = 0;; ++u) {
+        if (tc::tq_take(tq, u) < 0) break;
+        tc::mbar_wait(pfull, (uint32_t)u & 1u);   // Phi_F of tile u split into sP
         tc::fence_after();
         for (int fb = 0; fb < nfb; ++fb, ++itB) {
           const int bb = itB & 1;
@@ -225,29 +275,7 @@ __global__ void __launch_bounds__(FU_THREADS, 1) fused_fg_kernel(
           tc::mma_commit(&bfull[bb]);
         }
         tc::mma_commit(pempty);
-      };
-      int ti = 0;
-      for (;; ++ti) {
-        if (tc::tq_take(tq, ti) < 0) break;
-        const int ab = ti & 1;
-        tc::mbar_wait(&aempty[ab], ((uint32_t)(ti >> 1) & 1u) ^ 1u);
-        tc::fence_after();
-        const uint32_t d = tmem_base + (uint32_t)(ab * FU_NA);
-        for (int fb = 0; fb < nfb; ++fb) {
-          tc::mbar_wait(&xfull[stage], phase);
-          tc::fence_after();
-#pragma unroll
-          for (int kk = 0; kk < FU_BK / 32; ++kk) {
-            const uint64_t ad = tc::smem_desc_sw128(xBase + stage * FU_STAGE + kk * 32 * 128, FU_STAGE, 1024);
-            const uint64_t bd = tc::smem_desc_sw128(qBase + fb * FU_NA * FU_BK + kk * 32, 0, 1024);
-            tc::mma_i8(d, ad, bd, IDA, (fb | kk) != 0);
-          }
-          if (++stage == stages) { stage = 0; phase ^= 1u; }
-        }
-        tc::mma_commit(&afull[ab]);
-        if (ti >= 1) issue_b(ti - 1);
       }
-      if (ti >= 1) issue_b(ti - 1);
     }
   } else if (warp < FU_MASK_WARP0) {  // ------------------------------ convert (2..5)
     const int q = warp & 3;
@@ -260,6 +288,7 @@ __global__ void __launch_bounds__(FU_THREADS, 1) fused_fg_kernel(
       tc::fence_after();
       const uint32_t ta = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(ab * FU_NA);
       uint32_t h0[8], h1[8], h2[8];
+      float phif[FU_NC];
 #pragma unroll
       for (int half = 0; half < 2; ++half) {   // columns 8 half .. 8 half + 7
         uint32_t r0[8], r1[8], r2[8], r3[8];
@@ -273,6 +302,8 @@ __global__ void __launch_bounds__(FU_THREADS, 1) fused_fg_kernel(
           const int f = 8 * half + g;
           const float v0 = combine_limbs(r0[g], r1[g], r2[g], r3[g], sScale[f]);
           const float v1 = combine_limbs(r0[g + 1], r1[g + 1], r2[g + 1], r3[g + 1], sScale[f + 1]);
+          phif[f] = v0;
+          phif[f + 1] = v1;
           const __nv_bfloat162 a = __floats2bfloat162_rn(v0, v1);
           const float2 af = __bfloat1622float2(a);
           const float e0 = v0 - af.x, e1 = v1 - af.y;
@@ -287,6 +318,24 @@ __global__ void __launch_bounds__(FU_THREADS, 1) fused_fg_kernel(
       tc::fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&aempty[ab]);
+      if (ST) {   // static background and integer bounds of pixel `row`
+        float L = 0.f;
+#pragma unroll
+        for (int f = 0; f < FU_NC; ++f)
+          if (f < n_coef) L = fmaf(phif[f], sC0[f], L);   // the static kernel's order
+        const int bb = ti & 1;
+        tc::mbar_wait(&bnd_empty[bb], ((uint32_t)(ti >> 1) & 1u) ^ 1u);
+        const float fh = floorf(L + tau), fl = ceilf(L - tau);
+        const int64_t j = (int64_t)tile * FU_BM + row;
+        const bool alw = j < n_local && (fh < 0.f || fl > 255.f);
+        sHi[bb][row] = (uint8_t)fminf(fmaxf(fh, 0.f), 255.f);
+        sLo[bb][row] = (uint8_t)fminf(fmaxf(fl, 0.f), 255.f);
+        const uint32_t bal = __ballot_sync(0xffffffffu, alw);
+        if (lane == 0) sAlw[bb][q] = bal;
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&bnd_full[bb]);
+        continue;
+      }
       tc::mbar_wait(pempty, ((uint32_t)ti & 1u) ^ 1u);   // phase B of the previous tile is done with sP
 #pragma unroll
       for (int c8 = 0; c8 < 2; ++c8) {
@@ -301,7 +350,7 @@ __global__ void __launch_bounds__(FU_THREADS, 1) fused_fg_kernel(
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(pfull);
     }
-  } else {  // -------------------------------------------------------------- mask
+  } else if (warp < FU_BWARP) {  // ---------------------------------------- mask
     const int mw = warp - FU_MASK_WARP0;
     const int q = warp & 3;                // TMEM lane quarter: frames 32q .. 32q + 31 of a stage
     const int sl = mw >> 2;                // pixels [FU_PW sl, FU_PW (sl + 1)) of the tile
@@ -316,6 +365,56 @@ __global__ void __launch_bounds__(FU_THREADS, 1) fused_fg_kernel(
       const int tile = tc::tq_take_warp(tq, ti);
       if (tile < 0) break;
       const int64_t w0 = ((int64_t)tile * FU_BM + sl * FU_PW) >> 5;   // this thread's first mask word
+      if (ST) {   // ------------------------------ static: byte bounds, all frames of the tile
+        const int tb = ti & 1;
+        tc::mbar_wait(&bnd_full[tb], (uint32_t)(ti >> 1) & 1u);
+        uint32_t hiw[FU_NW][8], low[FU_NW][8], alw[FU_NW], valid[FU_NW];
+#pragma unroll
+        for (int w = 0; w < FU_NW; ++w) {
+          const int p0 = sl * FU_PW + 32 * w;
+          const uint4 h0 = *reinterpret_cast<const uint4*>(&sHi[tb][p0]);
+          const uint4 h1 = *reinterpret_cast<const uint4*>(&sHi[tb][p0 + 16]);
+          const uint4 l0 = *reinterpret_cast<const uint4*>(&sLo[tb][p0]);
+          const uint4 l1 = *reinterpret_cast<const uint4*>(&sLo[tb][p0 + 16]);
+          hiw[w][0] = h0.x; hiw[w][1] = h0.y; hiw[w][2] = h0.z; hiw[w][3] = h0.w;
+          hiw[w][4] = h1.x; hiw[w][5] = h1.y; hiw[w][6] = h1.z; hiw[w][7] = h1.w;
+          low[w][0] = l0.x; low[w][1] = l0.y; low[w][2] = l0.z; low[w][3] = l0.w;
+          low[w][4] = l1.x; low[w][5] = l1.y; low[w][6] = l1.z; low[w][7] = l1.w;
+          alw[w] = sAlw[tb][p0 >> 5];
+          const int64_t j0 = 32 * (w0 + w);
+          valid[w] = (j0 + 32 <= n_local) ? 0xffffffffu : (j0 < n_local ? ((1u << (n_local - j0)) - 1u) : 0u);
+        }
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&bnd_empty[tb]);
+        for (int fb = 0; fb < nfb; ++fb) {
+          tc::mbar_wait(&xfull[stage], phase);
+          const uint8_t* rowp = sX + (size_t)stage * FU_STAGE + r * 128;
+          uint32_t words[FU_NW];
+#pragma unroll
+          for (int w = 0; w < FU_NW; ++w) {
+            const int c = (sl * FU_PW + 32 * w) >> 4;
+            const uint4 a = *reinterpret_cast<const uint4*>(rowp + ((c ^ (r & 7)) << 4));
+            const uint4 b = *reinterpret_cast<const uint4*>(rowp + (((c + 1) ^ (r & 7)) << 4));
+            const uint32_t xw[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+            uint32_t word = alw[w];
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+              word |= fu_movemask4(__vcmpgtu4(xw[u], hiw[w][u]) | __vcmpltu4(xw[u], low[w][u])) << (4 * u);
+            words[w] = word & valid[w];
+          }
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive(&xempty[stage]);
+          if (++stage == stages) { stage = 0; phase ^= 1u; }
+          const int64_t t = (int64_t)fb * FU_BK + r;
+          if (t < m) {
+            uint32_t* dst = mask + t * ldw + w0;
+#pragma unroll
+            for (int w = 0; w < FU_NW; ++w)
+              if (32 * (w0 + w) < n_local) dst[w] = words[w];
+          }
+        }
+        continue;
+      }
       for (int fb = 0; fb < nfb; ++fb, ++itB) {
         const int bb = itB & 1;
         tc::mbar_wait(&bfull[bb], (uint32_t)(itB >> 1) & 1u);
@@ -396,15 +495,16 @@ static int fu_stages(int nfb) {
 }
 
 bool fused_supported(const cdmd_video& v, const cdmd_model& M, int mode) {
-  if (mode != CDMD_BG_DYNAMIC) return false;
+  if (mode != CDMD_BG_DYNAMIC && mode != CDMD_BG_STATIC) return false;
   if (M.n_coef < 1 || M.n_coef > FU_NC || !fu_encode_fn()) return false;
   const int nfb = (int)ceil_div(v.m, FU_BK);
   if (nfb > FU_MAX_FB || M.mpad > (int64_t)nfb * FU_BK) return false;
   return fu_smem_bytes(nfb, fu_stages(nfb)) <= 225 * 1024 && fu_stages(nfb) >= nfb + 1 && (v.ld % 16) == 0;
 }
 
-cudaError_t launch_fused_fg(const cdmd_video& v, const cdmd_model& M, float tau, uint32_t* mask, int64_t ldw,
-                            int* tile_counter, cudaStream_t st) {
+cudaError_t launch_fused_fg(const cdmd_video& v, const cdmd_model& M, int mode, float tau, uint32_t* mask,
+                            int64_t ldw, int* tile_counter, cudaStream_t st) {
+  auto kern = mode == CDMD_BG_STATIC ? fused_fg_kernel<true> : fused_fg_kernel<false>;
   const int nfb = (int)ceil_div(v.m, FU_BK);
   CUtensorMap mapX;
   cuuint64_t dims[2] = {(cuuint64_t)v.n_local, (cuuint64_t)v.m};
@@ -417,7 +517,7 @@ cudaError_t launch_fused_fg(const cdmd_video& v, const cdmd_model& M, float tau,
     return cudaErrorInvalidValue;
   const int stages = fu_stages(nfb);
   const size_t smem = fu_smem_bytes(nfb, stages);
-  cudaError_t e = cudaFuncSetAttribute(fused_fg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -428,7 +528,7 @@ cudaError_t launch_fused_fg(const cdmd_video& v, const cdmd_model& M, float tau,
   e = cudaMemsetAsync(tile_counter, 0, sizeof(int), st);
   if (e != cudaSuccess) return e;
   note_launch();
-  fused_fg_kernel<<<grid, FU_THREADS, smem, st>>>(mapX, v.n_local, v.m, nfb, M.mpad, M.kpad, M.Mq, M.Mq_scale,
+  kern<<<grid, FU_THREADS, smem, st>>>(mapX, v.n_local, v.m, nfb, M.mpad, M.kpad, M.Mq, M.Mq_scale,
                                                   M.coef, M.coef_col, M.n_coef, tau, mask, ldw, num_tiles, stages,
                                                   tile_counter);
   return cudaGetLastError();

@@ -599,7 +599,7 @@ def test_gaussian_sketch_deterministic_full_size(C, H, monkeypatch):
     assert float(d.max()) <= PT.RTOL_Y_GAUSS
 
 
-@pytest.mark.parametrize("case", ["c1", "ragged_sparse", "rademacher_small", "c2"])
+@pytest.mark.parametrize("case", ["c1", "ragged_sparse", "rademacher_small", "c2", "long_m"])
 def test_pipeline_parity_gavish_donoho(C, H, case):
     """Automatic target rank (Remark 2): the device's Gavish-Donoho rank
     (median singular value by bisection on the tridiagonal form) equals the oracle's,
@@ -607,6 +607,8 @@ def test_pipeline_parity_gavish_donoho(C, H, case):
     if case == "c2":
         cfg = config_by_name("c2_320x240_spixel")
         X, kind, p, k, K, tau = video_for(cfg), cfg.kind, cfg.p, cfg.k, cfg.K, cfg.tau
+    elif case == "long_m":   # m - 1 = 599 > 510: the full cuSOLVER syevd path of the GD rank
+        X, kind, p, k, K, tau = make_video(200, 96, 600, seed=21, noise=2.0, n_rects=1), "sparse", 800, 30, 6, 25.0
     else:
         name, shape, kind, p, k, K, tau = next(c for c in CASES if c[0] == case)
         if shape is None:
@@ -1167,3 +1169,28 @@ def test_repeatable_under_concurrency(C, H):
         torch.cuda.synchronize()
         for Pq in pipes:
             assert torch.equal(Pq.mask, ref_f), rep
+
+
+@pytest.mark.parametrize("partition", ["pixel", "batch"])
+def test_bench_two_ranks_runs(partition, tmp_path):
+    """bench.py under torchrun with two ranks sharing cuda:0 over gloo (the multi-rank
+    code path of the pixel-row split -- slab sketches + batch-ordered all-reduce -- and
+    of batch-parallel replicas -- no collective); one JSON line from rank 0."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    port = 29600 + (os.getpid() % 1000) + (7 if partition == "batch" else 0)
+    env = dict(os.environ, CDMD_DIST_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.join(root, "bench.py"), "--gpus", "2",
+           "--steps", "4", "--warmup", "3", "--lanes", "2", "--no-cpu-baseline", "--no-e2e", "--graph-reps", "10",
+           "--partition", partition, "--config", "c2_320x240_spixel"]
+    r = subprocess.run(cmd, cwd=root, capture_output=True, text=True, timeout=900, env=env)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0
+    assert d["scaling"] == ("weak" if partition == "batch" else "strong")
+    assert d["config"]["parallelism"].startswith("pixel-rows" if partition == "pixel" else "batch replicas")

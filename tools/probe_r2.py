@@ -39,6 +39,10 @@ def probe_fused(H):
         torch.cuda.synchronize()
         same = float((P.mask == ref).float().mean())
         say(f"  words equal to the two-pass mask: {same:.7f}")
+        ref_s = P.foreground(Xd, 25.0, C.BG_STATIC).clone()
+        P.foreground(Xd, 25.0, C.BG_STATIC, fused=True)
+        torch.cuda.synchronize()
+        say(f"  static: words equal to the two-pass static mask: {float((P.mask == ref_s).float().mean()):.7f}")
         if W == 1920:
             ts = []
             for _ in range(10):
@@ -57,6 +61,15 @@ def probe_fused(H):
                 b.synchronize()
                 t2.append(a.elapsed_time(b))
             say(f"  fused {np.median(ts):.4f} ms, two-pass foreground {np.median(t2):.4f} ms")
+            ts = []
+            for _ in range(10):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record()
+                P.foreground(Xd, 25.0, C.BG_STATIC, fused=True)
+                b.record()
+                b.synchronize()
+                ts.append(a.elapsed_time(b))
+            say(f"  fused static {np.median(ts):.4f} ms")
 
 
 def probe_fit(H):
