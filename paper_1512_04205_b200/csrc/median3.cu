@@ -3,6 +3,8 @@
 // words (rows y-1, y, y+1; columns x-1, x, x+1) are assembled with funnel shifts from
 // the packed rows, the bits that would wrap across an image row are cleared, and a
 // bit-sliced carry-save adder tree gives "at least 5 of 9" for all 32 pixels at once.
+#include <stdlib.h>
+
 #include "common.cuh"
 
 namespace cdmd {
@@ -14,10 +16,6 @@ __device__ __forceinline__ void fa(uint32_t a, uint32_t b, uint32_t c, uint32_t&
   co = (a & b) | (a & c) | (b & c);
 }
 
-#ifndef MW_DEF
-#define MW_DEF 8
-#endif
-constexpr int MW = MW_DEF;  // output words per thread (consecutive pixels of one frame)
 
 }  // namespace
 
@@ -26,6 +24,7 @@ constexpr int MW = MW_DEF;  // output words per thread (consecutive pixels of on
 // for every word of the thread (and every thread), so three words per row slide along
 // and each new output word costs one load per row plus funnel shifts.  32-bit pixel
 // indices (whole frames of < 2^31 pixels).
+template <int MW>   // output words per thread (consecutive pixels of one frame)
 __global__ void __launch_bounds__(256) mask_median3_kernel(const uint32_t* __restrict__ in, int64_t ldw,
                                                            int W, int H, uint32_t* __restrict__ out) {
   const int n = W * H, nw = (n + 31) >> 5;
@@ -39,21 +38,23 @@ __global__ void __launch_bounds__(256) mask_median3_kernel(const uint32_t* __res
     const uint32_t v = __ldg(f + q);
     return q == nw - 1 ? v & lastmask : v;
   };
-  // per row: bit offset r and the three words a (q), b (q+1), c (q+2) of the L window
+  // per row: bit offset r; every word the thread's MW outputs need (MW + 2 per row) is
+  // loaded up front, so all 3 (MW + 2) loads are in flight at once
   int q[3];
-  uint32_t r[3], wa[3], wb[3], wc[3];
+  uint32_t r[3], v[3][MW + 2];
 #pragma unroll
   for (int d = 0; d < 3; ++d) {
     const int s = (w0 << 5) + (d - 1) * W - 1;     // may be negative
     q[d] = s >> 5;
     r[d] = (uint32_t)s & 31u;
-    wa[d] = word(q[d]);
-    wb[d] = word(q[d] + 1);
-    wc[d] = word(q[d] + 2);
+#pragma unroll
+    for (int u = 0; u < MW + 2; ++u) v[d][u] = word(q[d] + u);
   }
   int x0 = (w0 << 5) % W;                          // column of the word's first pixel
-  const int wend = w0 + MW < nw ? w0 + MW : nw;
-  for (int w = w0; w < wend; ++w) {
+#pragma unroll
+  for (int u = 0; u < MW; ++u) {
+    const int w = w0 + u;
+    if (w >= nw) break;
     uint32_t first = 0u, last = 0u;                // pixels in column 0 / column W-1
     if (W >= 32) {                                 // at most one of each per word
       const int i0 = x0 == 0 ? 0 : W - x0, i1 = W - 1 - x0;
@@ -67,16 +68,13 @@ __global__ void __launch_bounds__(256) mask_median3_kernel(const uint32_t* __res
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
       const uint32_t rr = r[d];
-      const uint32_t L = __funnelshift_r(wa[d], wb[d], rr);
-      const uint32_t Cc = rr == 31u ? wb[d] : __funnelshift_r(wa[d], wb[d], rr + 1u);
-      const uint32_t R = rr >= 30u ? __funnelshift_r(wb[d], wc[d], rr - 30u) : __funnelshift_r(wa[d], wb[d], rr + 2u);
+      const uint32_t wa = v[d][u], wb = v[d][u + 1], wc = v[d][u + 2];
+      const uint32_t L = __funnelshift_r(wa, wb, rr);
+      const uint32_t Cc = rr == 31u ? wb : __funnelshift_r(wa, wb, rr + 1u);
+      const uint32_t R = rr >= 30u ? __funnelshift_r(wb, wc, rr - 30u) : __funnelshift_r(wa, wb, rr + 2u);
       x[3 * d + 0] = L & ~first;
       x[3 * d + 1] = Cc;
       x[3 * d + 2] = R & ~last;
-      // slide to the next output word
-      wa[d] = wb[d];
-      wb[d] = wc[d];
-      wc[d] = word(q[d] + 3 + (w - w0));
     }
     // count of the nine bits per position: CSA tree -> (b3 b2 b1 b0), majority = count >= 5
     uint32_t s1, c1, s2, c2, s3, c3, s4, c4, s5, c5;
@@ -99,9 +97,20 @@ cudaError_t launch_mask_median3(const uint32_t* in, int64_t ldw, int64_t W, int6
                                 cudaStream_t st) {
   if (W * H >= ((int64_t)1 << 31)) return cudaErrorInvalidValue;
   const int64_t nw = (W * H + 31) >> 5;
-  dim3 grid((unsigned)ceil_div(ceil_div(nw, MW), 256), (unsigned)m);
+  static int mw = -1;   // words per thread (CDMD_MEDIAN_MW: 1, 2, 4 or 8)
+  if (mw < 0) {
+    const char* e = getenv("CDMD_MEDIAN_MW");
+    mw = e ? atoi(e) : 2;
+    if (mw != 1 && mw != 2 && mw != 4 && mw != 8) mw = 2;
+  }
+  dim3 grid((unsigned)ceil_div(ceil_div(nw, mw), 256), (unsigned)m);
   note_launch();
-  mask_median3_kernel<<<grid, 256, 0, st>>>(in, ldw, (int)W, (int)H, out);
+  switch (mw) {
+    case 1: mask_median3_kernel<1><<<grid, 256, 0, st>>>(in, ldw, (int)W, (int)H, out); break;
+    case 4: mask_median3_kernel<4><<<grid, 256, 0, st>>>(in, ldw, (int)W, (int)H, out); break;
+    case 8: mask_median3_kernel<8><<<grid, 256, 0, st>>>(in, ldw, (int)W, (int)H, out); break;
+    default: mask_median3_kernel<2><<<grid, 256, 0, st>>>(in, ldw, (int)W, (int)H, out); break;
+  }
   return cudaGetLastError();
 }
 
