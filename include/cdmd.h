@@ -268,6 +268,24 @@ CDMD_API cdmd_status cdmd_amplitudes_solve(cdmd_handle h, const cdmd_model* mode
 CDMD_API int32_t cdmd_modes_path(const cdmd_model* model);
 CDMD_API int32_t cdmd_foreground_path(const cdmd_video* v, const cdmd_model* model, int32_t mode);
 
+/* ------------------------------------------- foreground with the median fused
+ * The fused single pass (cdmd_foreground with Phi = NULL, N11) with the 3x3 median
+ * post-filter of Fig. 7 (as cdmd_mask_median3, zero outside the frame) folded into
+ * the same kernel: tiles are 128-pixel chunks of image rows; once every tile of image
+ * rows y-1, y, y+1 has written its raw mask words, the CTA that completes them filters
+ * row y for all m frames.  Whole frames only: v->pix0 == 0, v->n_local == v->n_total
+ * == width * height, width % 32 == 0.
+ * raw: the unfiltered mask (m frames of ldw words, as cdmd_foreground writes it);
+ * out: the filtered mask (same layout, must not alias raw); ws: device, >=
+ * cdmd_foreground_median3_ws_bytes(width, height) bytes (row counters).
+ * Errors: CDMD_ERR_ARG (null / aliasing / layout), CDMD_ERR_RANGE (tau <= 0),
+ * CDMD_ERR_UNSUPPORTED (width % 32 != 0, or the fused pass unsupported: n_coef > 16 or
+ * m > 512), CDMD_ERR_WORKSPACE. */
+CDMD_API size_t cdmd_foreground_median3_ws_bytes(int64_t width, int64_t height);
+CDMD_API cdmd_status cdmd_foreground_median3(cdmd_handle h, const cdmd_video* v, const cdmd_model* model,
+                                             int32_t mode, float tau, int64_t width, int64_t height, uint32_t* raw,
+                                             uint32_t* out, int64_t ldw, void* ws, size_t ws_bytes, cdmd_stream st);
+
 /* ------------------------------------------------------------ median post-filter
  * The "in addition median filtered foreground mask" (Fig. 7): a 3x3 spatial
  * median of every frame's mask (on a binary image: bit = 1 iff >= 5 of the 3x3

@@ -61,7 +61,7 @@ SYMBOLS = ["cdmd_create", "cdmd_destroy", "cdmd_status_str", "cdmd_version", "cd
            "cdmd_foreground", "cdmd_philox", "cdmd_gaussian_table", "cdmd_srft_table", "cdmd_sparse_cap",
            "cdmd_sensing_rows", "cdmd_modes_simt", "cdmd_eig", "cdmd_mask_median3",
            "cdmd_modes_path", "cdmd_foreground_path", "cdmd_sm_partition",
-           "cdmd_set_background_selection"]
+           "cdmd_set_background_selection", "cdmd_foreground_median3", "cdmd_foreground_median3_ws_bytes"]
 
 
 def _load():
@@ -87,6 +87,8 @@ def _load():
         "cdmd_background": (i32, [vp, vp, i64, i64, M, i32, i64, i64, vp, i64, vp]),
         "cdmd_foreground": (i32, [vp, V, M, vp, i64, i32, ctypes.c_float, vp, i64, vp]),
         "cdmd_mask_median3": (i32, [vp, i64, i64, i64, i64, vp, vp]),
+        "cdmd_foreground_median3_ws_bytes": (sz, [i64, i64]),
+        "cdmd_foreground_median3": (i32, [vp, V, M, i32, ctypes.c_float, i64, i64, vp, vp, i64, vp, sz, vp]),
         "cdmd_set_background_selection": (i32, [vp, dbl]),
         "cdmd_sm_partition": (i32, [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(vp),
                                     ctypes.POINTER(vp), ctypes.POINTER(ctypes.c_int)]),
@@ -211,6 +213,14 @@ def cdmd_foreground(h, v, model, Phi, mode, tau, mask, stream=None):
     _check("cdmd_foreground", _lib.cdmd_foreground(h.h, ctypes.byref(v), ctypes.byref(model), _ptr(Phi),
                                                    Phi.stride(0) if Phi is not None else 0, mode, float(tau),
                                                    _ptr(mask), mask.stride(0), _stream(stream)))
+
+
+def cdmd_foreground_median3(h, v, model, mode, tau, width, height, raw, out, ws, stream=None):
+    """Fused pass (N11) with the 3x3 median post-filter folded in: raw and filtered
+    (m, ldw) masks of whole frames (width % 32 == 0); ws: >= cdmd_foreground_median3_ws_bytes."""
+    _check("cdmd_foreground_median3", _lib.cdmd_foreground_median3(
+        h.h, ctypes.byref(v), ctypes.byref(model), int(mode), float(tau), int(width), int(height), _ptr(raw),
+        _ptr(out), raw.stride(0), _ptr(ws), ws.numel() * ws.element_size(), _stream(stream)))
 
 
 def cdmd_amplitudes_workspace_bytes(h, k):
@@ -380,6 +390,20 @@ class Pipeline:
         v = video(X, self.n_total, self.pix0, self.n_local)
         cdmd_foreground(self.h, v, self.model, None if fused else self.Phi, mode, tau, self.mask, stream)
         return self.mask
+
+    def foreground_median3(self, X, tau, width, height, mode=BG_DYNAMIC, stream=None):
+        """The fused pass with the 3x3 median folded in (whole frames, width % 32 == 0).
+        Returns (raw mask, filtered mask); self.mask holds the raw one."""
+        if width * height != self.n_local or self.pix0 != 0:
+            raise ValueError("the fused median needs whole frames in this pipeline's slab")
+        v = video(X, self.n_total, self.pix0, self.n_local)
+        if getattr(self, "_med_out", None) is None:
+            self._med_out = torch.empty_like(self.mask)
+            self._med_ws = _empty_bytes(_lib.cdmd_foreground_median3_ws_bytes(int(width), int(height)),
+                                        self.mask.device)
+        cdmd_foreground_median3(self.h, v, self.model, mode, tau, width, height, self.mask, self._med_out,
+                                self._med_ws, stream)
+        return self.mask, self._med_out
 
     def median3(self, width, height, stream=None):
         """3x3 median post-filter of the last mask (whole frames: n_local = width * height)."""

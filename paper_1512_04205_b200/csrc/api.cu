@@ -430,6 +430,32 @@ int32_t cdmd_foreground_path(const cdmd_video* v, const cdmd_model* M, int32_t m
   return foreground_tc_supported(*v, *M) ? 2 : 1;
 }
 
+size_t cdmd_foreground_median3_ws_bytes(int64_t width, int64_t height) {
+  if (width < 1 || height < 1) return 0;
+  return al256(sizeof(int) * ((size_t)height + 1));   // a completion counter per image row + the row queue
+}
+
+cdmd_status cdmd_foreground_median3(cdmd_handle h, const cdmd_video* v, const cdmd_model* M, int32_t mode, float tau,
+                                    int64_t width, int64_t height, uint32_t* raw, uint32_t* out, int64_t ldw, void* ws,
+                                    size_t ws_bytes, cdmd_stream st) {
+  if (!h || !raw || !out || !ws) return CDMD_ERR_ARG;
+  if (mode != CDMD_BG_STATIC && mode != CDMD_BG_DYNAMIC) return CDMD_ERR_ARG;
+  cdmd_status s = check_video(v);
+  if (s != CDMD_OK) return s;
+  if ((s = check_model(M, v->m)) != CDMD_OK) return s;
+  if (!(tau > 0.0f)) return CDMD_ERR_RANGE;
+  if (width < 1 || height < 1 || width * height != v->n_total || v->pix0 != 0 || v->n_local != v->n_total)
+    return CDMD_ERR_ARG;
+  if (ldw < ceil_div(v->n_local, 32)) return CDMD_ERR_ARG;
+  const char *a0 = (const char*)raw, *a1 = a0 + sizeof(uint32_t) * ldw * v->m;
+  const char *b0 = (const char*)out, *b1 = b0 + sizeof(uint32_t) * ldw * v->m;
+  if (a0 < b1 && b0 < a1) return CDMD_ERR_ARG;   // aliasing
+  if (ws_bytes < cdmd_foreground_median3_ws_bytes(width, height)) return CDMD_ERR_WORKSPACE;
+  if ((width % 32) != 0 || width > (int64_t)1 << 24 || !fused_supported(*v, *M, mode)) return CDMD_ERR_UNSUPPORTED;
+  return cuda_status(launch_fused_fg_median(*v, *M, mode, tau, raw, ldw, sched_slot(h), (int)width, (int)height, out,
+                                            (int*)ws, (cudaStream_t)st));
+}
+
 cdmd_status cdmd_mask_median3(const uint32_t* mask, int64_t ldw, int64_t width, int64_t height, int64_t m,
                               uint32_t* out, cdmd_stream st) {
   if (!mask || !out) return CDMD_ERR_ARG;

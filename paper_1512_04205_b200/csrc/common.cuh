@@ -131,6 +131,10 @@ cudaError_t launch_foreground(const cdmd_video& v, const cdmd_model& M, const fl
 bool fused_supported(const cdmd_video& v, const cdmd_model& M, int mode);
 cudaError_t launch_fused_fg(const cdmd_video& v, const cdmd_model& M, int mode, float tau, uint32_t* mask,
                             int64_t ldw, int* tile_counter, cudaStream_t st);
+// ... with the 3x3 median fused (whole frames, imgW % 32 == 0): raw mask -> mask, filtered -> medout
+cudaError_t launch_fused_fg_median(const cdmd_video& v, const cdmd_model& M, int mode, float tau, uint32_t* mask,
+                                   int64_t ldw, int* tile_counter, int imgW, int imgH, uint32_t* medout, int* medcnt,
+                                   cudaStream_t st);
 
 cudaError_t launch_mask_median3(const uint32_t* in, int64_t ldw, int64_t W, int64_t H, int64_t m, uint32_t* out,
                                 cudaStream_t st);

@@ -27,6 +27,8 @@
 #include <cuda_bf16.h>
 #include <cudaTypedefs.h>
 
+#include <stdlib.h>
+
 #include "common.cuh"
 #include "tc.cuh"
 
@@ -97,6 +99,106 @@ __device__ __forceinline__ uint32_t fu_mask32(const uint32_t (&xw)[8], const uin
   return ~word;
 }
 
+// ---- the fused 3x3 median post-filter (Fig. 7; reading R22: 3x3, zero padding)
+// (a) After the 8 mask warps wrote a tile's raw mask words, the tile counts towards its
+//     image rows y-1, y, y+1 (release atomics after a barrier: the CTA's words first).
+// (b) Once a CTA's tiles are exhausted, its convert, mask and phase-B warps filter
+//     (image row, 32-frame block) tasks claimed from a second counter in row order: each
+//     waits (acquire) until the rows y-1, y, y+1 of its row are complete, then consecutive threads take
+//     8-word runs of one frame row (all 30 loads of a run in flight), the neighbour bits by
+//     one-bit shifts across adjacent words (zero outside the frame), and the bit-sliced
+//     carry-save count "at least 5 of 9", as median3.cu.  Rows are filtered while other
+//     CTAs still process tiles.
+__device__ __forceinline__ void fu_fa(uint32_t a, uint32_t b, uint32_t c, uint32_t& s, uint32_t& co) {
+  s = a ^ b ^ c;
+  co = (a & b) | (a & c) | (b & c);
+}
+
+__device__ __forceinline__ void fu_count_tile(int tile, int H, int ncw, int* cnt, int mw, int lane) {
+  asm volatile("bar.sync 2, 256;" ::: "memory");   // every mask thread's raw words of the tile are written
+  if (mw == 0 && lane < 3) {
+    const int yy = tile / ncw + lane - 1;
+    if (yy >= 0 && yy < H)
+      asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(cnt + yy) : "memory");
+  }
+}
+
+// phase (b): nthr threads (tid 0 .. nthr-1) of warps 2..14, named barrier 3
+__device__ __noinline__ void fu_median_rows(int64_t m, int64_t ldw, int W, int H, int ncw, const uint32_t* raw,
+                                            uint32_t* out, int* cnt, int* rowq, int tid, int nthr, int& rowsh) {
+  const int nwr = W >> 5;                          // words per image row
+  constexpr int MT = 8;                            // output words per run
+  const int tpr = (nwr + MT - 1) / MT;             // runs per frame row
+  constexpr int FBT = 32;                          // frames per task
+  const int nfbt = (int)((m + FBT - 1) / FBT);
+  for (;;) {
+    if (tid == 0) {
+      const int task = atomicAdd(rowq, 1);         // tasks in row order: (row, frame block)
+      const int Y = task / nfbt;
+      rowsh = task;
+      if (Y < H) {   // wait until rows Y-1, Y, Y+1 are complete
+        for (int d = -1; d <= 1; ++d) {
+          const int yy = Y + d;
+          if (yy < 0 || yy >= H) continue;
+          const int need = ncw * ((yy > 0) + 1 + (yy < H - 1));
+          int c;
+          for (;;) {
+            asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(c) : "l"(cnt + yy) : "memory");
+            if (c >= need) break;
+            __nanosleep(256);
+          }
+        }
+      }
+    }
+    asm volatile("bar.sync 3, %0;" ::"r"(nthr) : "memory");
+    const int task = rowsh;
+    asm volatile("bar.sync 3, %0;" ::"r"(nthr) : "memory");
+    const int Y = task / nfbt;
+    if (Y >= H) break;
+    const int t0 = (task - Y * nfbt) * FBT;
+    const int nt = (int)(m - t0 < FBT ? m - t0 : FBT);
+    const int total = nt * tpr;
+    for (int idx = tid; idx < total; idx += nthr) {
+      const int t = t0 + idx / tpr, w0 = (idx % tpr) * MT;
+      const uint32_t* rt = raw + (int64_t)t * ldw;
+      uint32_t v[3][MT + 2];   // words w0 - 1 .. w0 + MT of rows Y-1, Y, Y+1
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        const int yy = Y + d - 1;
+        const bool rowok = yy >= 0 && yy < H;
+        const uint32_t* rw = rt + (int64_t)(rowok ? yy : 0) * nwr;
+#pragma unroll
+        for (int u = 0; u < MT + 2; ++u) {
+          const int w = w0 + u - 1;
+          v[d][u] = (rowok && w >= 0 && w < nwr) ? __ldcg(rw + w) : 0u;
+        }
+      }
+      uint32_t* ot = out + (int64_t)t * ldw + (int64_t)Y * nwr;
+#pragma unroll
+      for (int u = 0; u < MT; ++u) {
+        if (w0 + u >= nwr) break;
+        uint32_t x[9];
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          const uint32_t a = v[d][u], b = v[d][u + 1], c = v[d][u + 2];
+          x[3 * d + 0] = (b << 1) | (a >> 31);   // pixel x - 1
+          x[3 * d + 1] = b;
+          x[3 * d + 2] = (b >> 1) | (c << 31);   // pixel x + 1
+        }
+        uint32_t s1, c1, s2, c2, s3, c3, s4, c4, s5, c5;
+        fu_fa(x[0], x[1], x[2], s1, c1);
+        fu_fa(x[3], x[4], x[5], s2, c2);
+        fu_fa(x[6], x[7], x[8], s3, c3);
+        fu_fa(s1, s2, s3, s4, c4);
+        fu_fa(c1, c2, c3, s5, c5);
+        const uint32_t b1 = s5 ^ c4, c6 = s5 & c4;
+        const uint32_t b2 = c5 ^ c6, b3 = c5 & c6;
+        ot[w0 + u] = b3 | (b2 & (b1 | s4));
+      }
+    }
+  }
+}
+
 // STATIC (template ST): no phase B; the convert warps reduce Phi_F of each
 // pixel to its static background L = sum_f Phi_F[f] c_f(1) (the fmaf order of
 // foreground.cu's static kernel) and the integer bounds x > floor(L + tau), x <
@@ -111,7 +213,12 @@ __global__ void __launch_bounds__(FU_THREADS, 1) fused_fg_kernel(
     const __grid_constant__ CUtensorMap mapX, int64_t n_local, int64_t m, int nfb, int64_t mpad, int kpad,
     const int8_t* __restrict__ Mq, const double* __restrict__ Mq_scale, const float* __restrict__ coef,
     const int32_t* __restrict__ coef_col, int n_coef, float tau, uint32_t* __restrict__ mask, int64_t ldw,
-    int num_tiles, int stages, int* __restrict__ tile_counter) {
+    int num_tiles, int stages, int* __restrict__ tile_counter, int imgW, int imgH, int ncw,
+    uint32_t* __restrict__ medout, int* __restrict__ medcnt) {
+  // imgW > 0: the 3x3 median post-filter is fused (Fig. 7): tile = (image row y,
+  // 128-pixel chunk c) of whole frames (imgW % 32 == 0), the raw mask goes to `mask`
+  // (workspace) and the filtered one to `medout`; a tile's median is computed by the
+  // CTA that completes the last of its (up to) nine neighbour tiles (counters medcnt).
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw;
   const int mA = nfb * FU_BK;
@@ -137,8 +244,17 @@ __global__ void __launch_bounds__(FU_THREADS, 1) fused_fg_kernel(
   __shared__ __align__(16) uint8_t sHi[2][FU_BM], sLo[2][FU_BM];   // ST: per-pixel byte bounds, by tile parity
   __shared__ uint32_t sAlw[2][FU_BM / 32];                  // ST: pixels outside [0, 255] +- tau: always set
   __shared__ uint64_t bnd_full[2], bnd_empty[2];
+  __shared__ int rowsh;                                     // median: the row being filtered
   const tc::TileQueue tq{tq_id, tq_bar, tq_bar + tc::TQ_N};
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // first pixel and length of a tile
+  auto tile_base = [&](int tile) -> int64_t {
+    return imgW > 0 ? (int64_t)(tile / ncw) * imgW + (int64_t)(tile % ncw) * FU_BM : (int64_t)tile * FU_BM;
+  };
+  auto tile_len = [&](int tile) -> int {
+    const int64_t rest = imgW > 0 ? (int64_t)imgW - (int64_t)(tile % ncw) * FU_BM : n_local - (int64_t)tile * FU_BM;
+    return rest < FU_BM ? (int)rest : FU_BM;
+  };
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < stages; ++s) {
@@ -217,7 +333,7 @@ __global__ void __launch_bounds__(FU_THREADS, 1) fused_fg_kernel(
         for (int fb = 0; fb < nfb; ++fb) {
           tc::mbar_wait(&xempty[stage], phase ^ 1u);
           tc::mbar_arrive_expect_tx(&xfull[stage], FU_STAGE);
-          tc::tma_load_2d(sX + (size_t)stage * FU_STAGE, &mapX, &xfull[stage], tile * FU_BM, fb * FU_BK);
+          tc::tma_load_2d(sX + (size_t)stage * FU_STAGE, &mapX, &xfull[stage], (int32_t)tile_base(tile), fb * FU_BK);
           if (++stage == stages) { stage = 0; phase ^= 1u; }
         }
       }
@@ -326,8 +442,7 @@ __global__ void __launch_bounds__(FU_THREADS, 1) fused_fg_kernel(
         const int bb = ti & 1;
         tc::mbar_wait(&bnd_empty[bb], ((uint32_t)(ti >> 1) & 1u) ^ 1u);
         const float fh = floorf(L + tau), fl = ceilf(L - tau);
-        const int64_t j = (int64_t)tile * FU_BM + row;
-        const bool alw = j < n_local && (fh < 0.f || fl > 255.f);
+        const bool alw = row < tile_len(tile) && (fh < 0.f || fl > 255.f);
         sHi[bb][row] = (uint8_t)fminf(fmaxf(fh, 0.f), 255.f);
         sLo[bb][row] = (uint8_t)fminf(fmaxf(fl, 0.f), 255.f);
         const uint32_t bal = __ballot_sync(0xffffffffu, alw);
@@ -364,7 +479,8 @@ __global__ void __launch_bounds__(FU_THREADS, 1) fused_fg_kernel(
     for (int ti = 0;; ++ti) {
       const int tile = tc::tq_take_warp(tq, ti);
       if (tile < 0) break;
-      const int64_t w0 = ((int64_t)tile * FU_BM + sl * FU_PW) >> 5;   // this thread's first mask word
+      const int64_t w0 = (tile_base(tile) + sl * FU_PW) >> 5;   // this thread's first mask word
+      const int tlen = tile_len(tile);                             // pixels of the tile (multiple of 32 unless ragged)
       if (ST) {   // ------------------------------ static: byte bounds, all frames of the tile
         const int tb = ti & 1;
         tc::mbar_wait(&bnd_full[tb], (uint32_t)(ti >> 1) & 1u);
@@ -381,8 +497,7 @@ __global__ void __launch_bounds__(FU_THREADS, 1) fused_fg_kernel(
           low[w][0] = l0.x; low[w][1] = l0.y; low[w][2] = l0.z; low[w][3] = l0.w;
           low[w][4] = l1.x; low[w][5] = l1.y; low[w][6] = l1.z; low[w][7] = l1.w;
           alw[w] = sAlw[tb][p0 >> 5];
-          const int64_t j0 = 32 * (w0 + w);
-          valid[w] = (j0 + 32 <= n_local) ? 0xffffffffu : (j0 < n_local ? ((1u << (n_local - j0)) - 1u) : 0u);
+          valid[w] = (p0 + 32 <= tlen) ? 0xffffffffu : (p0 < tlen ? ((1u << (tlen - p0)) - 1u) : 0u);
         }
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&bnd_empty[tb]);
@@ -410,9 +525,10 @@ __global__ void __launch_bounds__(FU_THREADS, 1) fused_fg_kernel(
             uint32_t* dst = mask + t * ldw + w0;
 #pragma unroll
             for (int w = 0; w < FU_NW; ++w)
-              if (32 * (w0 + w) < n_local) dst[w] = words[w];
+              if (sl * FU_PW + 32 * w < tlen) dst[w] = words[w];
           }
         }
+        if (imgW > 0) fu_count_tile(tile, imgH, ncw, medcnt, mw, lane);
         continue;
       }
       for (int fb = 0; fb < nfb; ++fb, ++itB) {
@@ -451,17 +567,22 @@ __global__ void __launch_bounds__(FU_THREADS, 1) fused_fg_kernel(
         const int64_t t = (int64_t)fb * FU_BK + r;
         if (t < m) {
           uint32_t* dst = mask + t * ldw + w0;
-          if (FU_NW == 2 && (ldw & 1) == 0 && 32 * (w0 + 1) < n_local) {
+          if (FU_NW == 2 && ((ldw | w0) & 1) == 0 && sl * FU_PW + 32 < tlen) {   // 8-B aligned pair
             *reinterpret_cast<uint2*>(dst) = make_uint2(words[0], words[FU_NW - 1]);
           } else {
 #pragma unroll
             for (int w = 0; w < FU_NW; ++w)
-              if (32 * (w0 + w) < n_local) dst[w] = words[w];
+              if (sl * FU_PW + 32 * w < tlen) dst[w] = words[w];
           }
         }
       }
+      if (imgW > 0) fu_count_tile(tile, imgH, ncw, medcnt, mw, lane);
     }
   }
+  // phase (b): warps 2 .. FU_BWARP filter whole image rows (median fused)
+  if (imgW > 0 && warp >= 2)
+    fu_median_rows(m, ldw, imgW, imgH, ncw, mask, medout, medcnt, medcnt + imgH, threadIdx.x - 64,
+                   blockDim.x - 64, rowsh);
   __syncthreads();
   if (warp == 1) {
     tc::fence_after();
@@ -504,6 +625,12 @@ bool fused_supported(const cdmd_video& v, const cdmd_model& M, int mode) {
 
 cudaError_t launch_fused_fg(const cdmd_video& v, const cdmd_model& M, int mode, float tau, uint32_t* mask,
                             int64_t ldw, int* tile_counter, cudaStream_t st) {
+  return launch_fused_fg_median(v, M, mode, tau, mask, ldw, tile_counter, 0, 0, nullptr, nullptr, st);
+}
+
+cudaError_t launch_fused_fg_median(const cdmd_video& v, const cdmd_model& M, int mode, float tau, uint32_t* mask,
+                                   int64_t ldw, int* tile_counter, int imgW, int imgH, uint32_t* medout, int* medcnt,
+                                   cudaStream_t st) {
   auto kern = mode == CDMD_BG_STATIC ? fused_fg_kernel<true> : fused_fg_kernel<false>;
   const int nfb = (int)ceil_div(v.m, FU_BK);
   CUtensorMap mapX;
@@ -522,15 +649,17 @@ cudaError_t launch_fused_fg(const cdmd_video& v, const cdmd_model& M, int mode, 
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int num_tiles = (int)ceil_div(v.n_local, FU_BM);
+  const int ncw = imgW > 0 ? (int)ceil_div(imgW, FU_BM) : 0;
+  const int num_tiles = imgW > 0 ? imgH * ncw : (int)ceil_div(v.n_local, FU_BM);
   const int pc = persistent_ctas(sms);
   const int grid = num_tiles < pc ? num_tiles : pc;
   e = cudaMemsetAsync(tile_counter, 0, sizeof(int), st);
+  if (e == cudaSuccess && imgW > 0) e = cudaMemsetAsync(medcnt, 0, sizeof(int) * ((size_t)imgH + 1), st);
   if (e != cudaSuccess) return e;
   note_launch();
   kern<<<grid, FU_THREADS, smem, st>>>(mapX, v.n_local, v.m, nfb, M.mpad, M.kpad, M.Mq, M.Mq_scale,
                                                   M.coef, M.coef_col, M.n_coef, tau, mask, ldw, num_tiles, stages,
-                                                  tile_counter);
+                                                  tile_counter, imgW, imgH, ncw, medout, medcnt);
   return cudaGetLastError();
 }
 

@@ -100,16 +100,16 @@ cudaError_t launch_mask_median3(const uint32_t* in, int64_t ldw, int64_t W, int6
   static int mw = -1;   // words per thread (CDMD_MEDIAN_MW: 1, 2, 4 or 8)
   if (mw < 0) {
     const char* e = getenv("CDMD_MEDIAN_MW");
-    mw = e ? atoi(e) : 2;
-    if (mw != 1 && mw != 2 && mw != 4 && mw != 8) mw = 2;
+    mw = e ? atoi(e) : 8;   // measured at 1080p x 500: 1 / 2 / 4 / 8 -> 0.29 / 0.22 / 0.171 / 0.167 ms
+    if (mw != 1 && mw != 2 && mw != 4 && mw != 8) mw = 8;
   }
   dim3 grid((unsigned)ceil_div(ceil_div(nw, mw), 256), (unsigned)m);
   note_launch();
   switch (mw) {
     case 1: mask_median3_kernel<1><<<grid, 256, 0, st>>>(in, ldw, (int)W, (int)H, out); break;
     case 4: mask_median3_kernel<4><<<grid, 256, 0, st>>>(in, ldw, (int)W, (int)H, out); break;
-    case 8: mask_median3_kernel<8><<<grid, 256, 0, st>>>(in, ldw, (int)W, (int)H, out); break;
-    default: mask_median3_kernel<2><<<grid, 256, 0, st>>>(in, ldw, (int)W, (int)H, out); break;
+    case 2: mask_median3_kernel<2><<<grid, 256, 0, st>>>(in, ldw, (int)W, (int)H, out); break;
+    default: mask_median3_kernel<8><<<grid, 256, 0, st>>>(in, ldw, (int)W, (int)H, out); break;
   }
   return cudaGetLastError();
 }

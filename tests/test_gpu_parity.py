@@ -1194,3 +1194,38 @@ def test_bench_two_ranks_runs(partition, tmp_path):
     assert d["n_gpus"] == 2 and d["value"] > 0
     assert d["scaling"] == ("weak" if partition == "batch" else "strong")
     assert d["config"]["parallelism"].startswith("pixel-rows" if partition == "pixel" else "batch replicas")
+
+
+@pytest.mark.parametrize("W,Hh,m,p,k,K,mode", [(64, 48, 40, 120, 10, 3, "dyn"), (320, 240, 200, 1000, 20, 10, "dyn"),
+                                                (320, 240, 200, 1000, 20, 10, "sta"), (96, 33, 77, 200, 12, 4, "dyn"),
+                                                (1920, 1080, 500, 2000, 50, 10, "dyn")])
+def test_fused_median_bit_exact(C, H, W, Hh, m, p, k, K, mode):
+    """The 3x3 median folded into the fused pass (Fig. 7): the filtered mask equals
+    the oracle's median3 of the raw mask bit for bit (every frame, every pixel, the image
+    borders zero-padded), and the raw mask equals the fused pass's own mask."""
+    X = make_video(W, Hh, m, seed=W + Hh, noise=2.0, n_rects=2)
+    n = W * Hh
+    Xd = to_dev(X)
+    P = C.Pipeline(H, n, n, m, "sparse", p, k, K)
+    P.sketch(Xd)
+    P.fit()
+    md = C.BG_DYNAMIC if mode == "dyn" else C.BG_STATIC
+    plain = P.foreground(Xd, 25.0, md, fused=True).clone()
+    raw, out = P.foreground_median3(Xd, 25.0, W, Hh, md)
+    torch.cuda.synchronize()
+    assert torch.equal(raw, plain)
+    rawb = OD.unpack_mask(raw.cpu().numpy().view(np.uint32), n)
+    got = OD.unpack_mask(out.cpu().numpy().view(np.uint32), n)
+    assert np.array_equal(got, OD.median3(rawb, W, Hh))
+
+
+def test_fused_median_needs_word_aligned_rows(C, H):
+    X = make_video(100, 37, 33, seed=5, noise=2.0, n_rects=1)   # width 100: rows not word-aligned
+    n = X.shape[1]
+    P = C.Pipeline(H, n, n, 33, "sparse", 120, 12, 5)
+    Xd = to_dev(X)
+    P.sketch(Xd)
+    P.fit()
+    with pytest.raises(C.CdmdError) as e:
+        P.foreground_median3(Xd, 25.0, 100, 37)
+    assert e.value.code == 6

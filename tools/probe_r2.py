@@ -70,6 +70,15 @@ def probe_fused(H):
                 b.synchronize()
                 ts.append(a.elapsed_time(b))
             say(f"  fused static {np.median(ts):.4f} ms")
+            ts = []
+            for _ in range(10):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record()
+                P.foreground_median3(Xd, 25.0, W, Hh, C.BG_DYNAMIC)
+                b.record()
+                b.synchronize()
+                ts.append(a.elapsed_time(b))
+            say(f"  fused + median {np.median(ts):.4f} ms")
 
 
 def probe_fit(H):
