@@ -48,7 +48,7 @@ sys.path.insert(0, ROOT)
 FALLBACK_HBM_GBS = 6650.0   # B200_PROFILING.md fallback, used only without MEASURED_PEAKS.json
 FALLBACK_BF16_TFLOPS = 1590.0
 METRIC = "1080p frames/sec (sketch+modes+fg mask) at 1/2/4/8 B200; % of HBM roofline"
-KINDS = {"spixel": 0, "sparse": 1, "rademacher": 2, "gaussian": 3}
+KINDS = {"spixel": 0, "sparse": 1, "rademacher": 2, "gaussian": 3, "srft": 4}
 
 
 def peaks():
@@ -463,6 +463,20 @@ def main():
                      "step_hbm_frac": round(step_bytes / (ms_max * 1e-3) / 1e9 / hbm, 4),
                      "note": "batches pipelined across lanes (own handle, stream, buffers, copy of X); "
                              "each lane runs >= 2 batches"}
+        # the same lanes through the fused single pass (N11: no cdmd_modes; the support's
+        # modes in-slab) -- the E2E-fused variant of SURVEY.md §8(d), reported alongside
+        if fused_ok is True and not args.fused:
+            S.fused = True
+            stream_run(max(args.warmup, lanes))
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+            a2, b2 = stream_run(args.steps)
+            torch.cuda.synchronize()
+            S.fused = False
+            msf = max_over_ranks(a2.elapsed_time(b2) / args.steps)
+            streaming["fused_ms_per_batch"] = round(msf, 4)
+            streaming["fused_frames_per_s"] = round(m / (msf * 1e-3) * (world if not pixel and world > 1 else 1), 1)
     if not pixel and world > 1:
         value *= world      # batch-parallel replicas: every rank processes its own batches
 
