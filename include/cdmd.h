@@ -136,6 +136,12 @@ CDMD_API const char* cdmd_version(void);
  * all streams; cuBLAS / cuSOLVER launches inside cdmd_fit are not counted).
  * Diagnostics: bench.py reports the difference across its timed region.          */
 CDMD_API uint64_t cdmd_kernel_launches(void);
+/* Eigensolver diagnostics of handle h (cdmd_fit step 4): *runs = fits whose k
+ * largest Gram eigenpairs were computed by Lanczos (lanczos.cu),
+ * *fallbacks = those of them whose Ritz pairs failed the residual test
+ * |beta_{J-1} s_{J-1,i}| <= 1e-9 (theta_i - theta_{k+1}) and were recomputed by the
+ * Householder solver.  Either pointer may be NULL.  Errors: CDMD_ERR_ARG (null h).   */
+CDMD_API cdmd_status cdmd_eigensolver_stats(cdmd_handle h, uint64_t* runs, uint64_t* fallbacks);
 
 /* Background selection of later cdmd_fit calls on this handle.  omega_eps = 0 (the
  * default): Remark 3's OMP picks at most K modes.  omega_eps > 0: the
@@ -198,8 +204,12 @@ CDMD_API cdmd_status cdmd_sketch(cdmd_handle h, const cdmd_video* v, const cdmd_
  * model->k_eff.  BLOCKING: returns after the model is complete.  Errors:
  * CDMD_ERR_RANGE if |k| < 1, |k| > min(p, m-1), K < 1 or K > |k|;
  * CDMD_ERR_NUMERIC if the eigensolvers fail or every sigma is dropped (model->info
- * holds the solver info).  m - 1 > 510: the symmetric eigensolve is cuSOLVER's
- * (syevdx for the k largest; syevd, every eigenvalue, for k < 0). */
+ * holds the solver info).  Symmetric eigensolve (the k largest pairs of Y^T Y): by
+ * Lanczos with full reorthogonalisation on one 16-CTA cluster (m - 1 <= 512,
+ * 2.5 k + 9 <= 144), accepted only if every Ritz pair passes the residual test (see
+ * cdmd_eigensolver_stats), else by the 8-CTA Householder solver (m - 1 <= 510; also for
+ * k < 0, which needs every eigenvalue), else cuSOLVER's (syevdx for the k largest;
+ * syevd for k < 0). */
 CDMD_API size_t cdmd_model_bytes(int k, int K, int64_t m);
 CDMD_API cdmd_status cdmd_model_bind(cdmd_model* model, void* dev_buf, size_t bytes, int k, int K, int64_t m);
 CDMD_API size_t cdmd_fit_workspace_bytes(cdmd_handle h, int64_t p, int64_t m, int k);

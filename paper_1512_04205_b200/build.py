@@ -12,7 +12,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "lib", "libcdmd.so")
-SOURCES = ["api.cu", "sensing.cu", "sketch.cu", "fit.cu", "modes.cu", "modes_tc.cu", "foreground.cu", "foreground_tc.cu", "eig.cu", "eigh.cu", "sketch_tc.cu", "sketch_tc2.cu", "median3.cu", "partition.cu", "amplitudes.cu", "fused_tc.cu", "sparse_csc.cu"]
+SOURCES = ["api.cu", "sensing.cu", "sketch.cu", "fit.cu", "modes.cu", "modes_tc.cu", "foreground.cu", "foreground_tc.cu", "eig.cu", "eigh.cu", "sketch_tc.cu", "sketch_tc2.cu", "median3.cu", "partition.cu", "amplitudes.cu", "fused_tc.cu", "sparse_csc.cu", "lanczos.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

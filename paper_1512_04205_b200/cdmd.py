@@ -55,6 +55,7 @@ class Model(ctypes.Structure):
 
 
 SYMBOLS = ["cdmd_create", "cdmd_destroy", "cdmd_status_str", "cdmd_version", "cdmd_kernel_launches",
+           "cdmd_eigensolver_stats",
            "cdmd_sketch_workspace_bytes", "cdmd_sketch", "cdmd_model_bytes", "cdmd_model_bind",
            "cdmd_fit_workspace_bytes", "cdmd_fit", "cdmd_modes", "cdmd_background",
            "cdmd_amplitudes_workspace_bytes", "cdmd_amplitudes_gram", "cdmd_amplitudes_solve",
@@ -76,6 +77,8 @@ def _load():
         "cdmd_status_str": (ctypes.c_char_p, [i32]),
         "cdmd_version": (ctypes.c_char_p, []),
         "cdmd_kernel_launches": (ctypes.c_uint64, []),
+        "cdmd_eigensolver_stats": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_uint64),
+                                                  ctypes.POINTER(ctypes.c_uint64)]),
         "cdmd_sketch_workspace_bytes": (sz, [V, S]),
         "cdmd_sketch": (i32, [vp, V, S, vp, i64, vp, sz, vp]),
         "cdmd_model_bytes": (sz, [ctypes.c_int, ctypes.c_int, i64]),
@@ -271,6 +274,14 @@ def cdmd_srft_table(h, out, stream=None):
 def cdmd_kernel_launches():
     """libcdmd kernel launches issued by this process so far (cuBLAS/cuSOLVER excluded)."""
     return int(lib().cdmd_kernel_launches())
+
+
+def cdmd_eigensolver_stats(h):
+    """(runs, fallbacks): fits on handle h whose eigenpairs came from Lanczos, and how many
+    of them failed the residual test and were recomputed by the Householder solver."""
+    runs, fb = ctypes.c_uint64(0), ctypes.c_uint64(0)
+    _check("cdmd_eigensolver_stats", _lib.cdmd_eigensolver_stats(h.h, ctypes.byref(runs), ctypes.byref(fb)))
+    return int(runs.value), int(fb.value)
 
 
 _PARTITION = {}

@@ -281,7 +281,7 @@ cudaError_t launch_amp_gram(int sms, const float* Phi, int64_t ldphi, const uint
   // 3 x 192 0.38 ms, 4 x 192 on 64-pixel tiles 0.39 ms at c4)
   const bool two = sh.threads <= 192;
   auto kern = two ? amp_gram_kernel<192, 3> : amp_gram_kernel<576, 1>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = smem_optin(reinterpret_cast<const void*>(kern));
   if (e != cudaSuccess) return e;
   note_launch();
   kern<<<blocks, sh.threads, smem, st>>>(Phi, ldphi, x1, n_local, k, sh.nb, sh.nmt, sh.tg, sh.ng, ws);
@@ -295,8 +295,7 @@ cudaError_t launch_amp_gram(int sms, const float* Phi, int64_t ldphi, const uint
 cudaError_t launch_amp_solve(const double* G, int k, const int32_t* pair, double* b, int32_t* dropped,
                              cudaStream_t st) {
   const size_t smem = amp_solve_smem_bytes(k);
-  cudaError_t e = cudaFuncSetAttribute(amp_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
+  cudaError_t e = smem_optin(reinterpret_cast<const void*>(amp_solve_kernel));
   if (e != cudaSuccess) return e;
   note_launch();
   amp_solve_kernel<<<1, 256, smem, st>>>(G, k, pair, b, dropped);

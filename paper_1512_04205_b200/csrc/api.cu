@@ -10,6 +10,25 @@
 
 #include "handle.h"
 
+namespace cdmd {
+cudaError_t smem_optin(const void* kern) {
+  static std::mutex mu;
+  static std::set<std::pair<int, const void*>> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> g(mu);
+  if (done.count({dev, kern})) return cudaSuccess;
+  cudaFuncAttributes a;
+  if ((e = cudaFuncGetAttributes(&a, kern)) != cudaSuccess) return e;
+  int optin = 0;
+  if ((e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev)) != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)a.sharedSizeBytes);
+  if (e == cudaSuccess) done.insert({dev, kern});
+  return e;
+}
+}  // namespace cdmd
+
 using namespace cdmd;
 
 namespace cdmd {
@@ -102,7 +121,15 @@ extern "C" {
 
 const char* cdmd_version(void) { return "cdmd-b200 0.1 (sm_100a)"; }
 
+
 uint64_t cdmd_kernel_launches(void) { return cdmd::launch_counter().load(std::memory_order_relaxed); }
+
+cdmd_status cdmd_eigensolver_stats(cdmd_handle h, uint64_t* runs, uint64_t* fallbacks) {
+  if (!h) return CDMD_ERR_ARG;
+  if (runs) *runs = h->lz_runs.load();
+  if (fallbacks) *fallbacks = h->lz_fallbacks.load();
+  return CDMD_OK;
+}
 
 cdmd_status cdmd_set_background_selection(cdmd_handle h, double omega_eps) {
   if (!h) return CDMD_ERR_ARG;

@@ -20,6 +20,11 @@ inline std::atomic<uint64_t>& launch_counter() {
 }
 inline void note_launch() { launch_counter().fetch_add(1, std::memory_order_relaxed); }
 
+// Opt kernel `kern` into the device's whole shared memory per block (minus its static
+// shared memory), once per (device, kernel).  The attribute is per function: setting it
+// to each launch's own size would let one host thread lower it under another's launch.
+cudaError_t smem_optin(const void* kern);
+
 // CTAs of the persistent full-resolution kernels (modes, foreground): all SMs, or
 // fewer with CDMD_PERSIST_RESERVE=R (R SMs left to other streams' small solves)
 int persistent_ctas(int sms);

@@ -1179,13 +1179,13 @@ cudaError_t launch_hqr_eig(int k, const double* A, double* W, double* VR, int* i
     double* H0 = scratch;
     double* Q = scratch + (size_t)k * k;
     const size_t smem = hqr_smem_bytes(k);
-    cudaError_t e = cudaFuncSetAttribute(hqrv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = smem_optin(reinterpret_cast<const void*>(hqrv_kernel));
     if (e != cudaSuccess) return e;
     note_launch();
     hqrv_kernel<<<1, 32, smem, st>>>(k, A, W, H0, Q, info);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     const size_t smem2 = hinvit_smem(k);
-    e = cudaFuncSetAttribute(hinvit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
+    e = smem_optin(reinterpret_cast<const void*>(hinvit_kernel));
     if (e != cudaSuccess) return e;
     note_launch();
     hinvit_kernel<<<(unsigned)k, 32, smem2, st>>>(k, W, H0, Q, VR);
@@ -1193,7 +1193,7 @@ cudaError_t launch_hqr_eig(int k, const double* A, double* W, double* VR, int* i
   }
   const int par3 = hqr_smem_par3(k) <= 226 * 1024;
   const size_t smem = par3 ? hqr_smem_par3(k) : hqr_smem_bytes(k);
-  cudaError_t e = cudaFuncSetAttribute(hqr_eig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = smem_optin(reinterpret_cast<const void*>(hqr_eig_kernel));
   if (e != cudaSuccess) return e;
   note_launch();
   hqr_eig_kernel<<<1, 32, smem, st>>>(k, A, W, VR, info, par3);

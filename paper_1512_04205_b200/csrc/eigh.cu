@@ -606,7 +606,7 @@ size_t eh_tridiag_smem(int n) {
 bool eh_supported(int n, int k) { return n >= 3 && n <= EH_NMAX && k <= 256 && eh_tridiag_smem(n) <= 227 * 1024; }
 
 size_t eh_work_doubles(int n, int k) {
-  return (size_t)n * n + 3 * (size_t)n + (size_t)n * k + 64;
+  return (size_t)n * n + 7 * (size_t)n + (size_t)n * k + 128;
 }
 
 // G (n x n, ld ldg) -> lam[k] (ascending: the k largest), Zout (n x k column-major, ld n).
@@ -629,7 +629,7 @@ cudaError_t launch_eh(int n, int k, const double* G, int64_t ldg, double* lam, d
   mark(0);
   {
     const size_t smem = eh_tridiag_smem(n);
-    err = cudaFuncSetAttribute(eh_tridiag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    err = smem_optin(reinterpret_cast<const void*>(eh_tridiag_kernel));
     if (err != cudaSuccess) return err;
     note_launch();
     eh_tridiag_kernel<<<EH_CL, EH_T, smem, st>>>(n, G, ldg, d, e, tau, V);
@@ -646,7 +646,7 @@ cudaError_t launch_eh(int n, int k, const double* G, int64_t ldg, double* lam, d
   mark(2);
   note_launch();
   const size_t smem2 = sizeof(double) * 5 * (size_t)n + (size_t)n + 16;
-  err = cudaFuncSetAttribute(eh_invit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
+  err = smem_optin(reinterpret_cast<const void*>(eh_invit_kernel));
   if (err != cudaSuccess) return err;
   eh_invit_kernel<<<(unsigned)k, 32, smem2, st>>>(n, k, d, e, bounds, lam, Zout, info);
   mark(3);
@@ -662,6 +662,68 @@ cudaError_t launch_eh(int n, int k, const double* G, int64_t ldg, double* lam, d
     for (int i = 0; i < 6; ++i) cudaEventDestroy(ev[i]);
   }
   return cudaGetLastError();
+}
+
+// Lanczos variant (lanczos.cu): the same outputs as launch_eh (k largest pairs ascending
+// in lam, Zout) from a Krylov space of J = lz_steps(n, k) << n; *flag = 0 when every Ritz
+// pair passed the residual test, else the caller reruns launch_eh.  The returned error
+// is cudaErrorNotSupported when this device cannot co-schedule the 16-CTA cluster.
+bool lz_supported(int n, int k);
+int lz_steps(int n, int k);
+void lz_prof_read(unsigned long long* out);
+cudaError_t launch_lz(int n, int J, const double* G, int64_t ldg, double* alpha, double* beta, double* Q, int* jdone,
+                      cudaStream_t st);
+cudaError_t launch_lz_check(int J, int k, const double* beta, const double* lam1, const double* S, const int* jdone,
+                            int* flag, cudaStream_t st);
+cudaError_t launch_lz_ritz(int n, int J, int k, const double* Q, const double* S, const double* lam1, double* lam,
+                           double* Z, cudaStream_t st);
+
+cudaError_t launch_eh_lz(int n, int k, const double* G, int64_t ldg, double* lam, double* Zout, double* work,
+                         int* info, int* flag, cudaStream_t st) {
+  const int J = lz_steps(n, k);
+  // work: Q (n x J) | alpha, beta, e2 (J each) | bounds (8) | lam1 (k + 1) | S (J x (k + 1)) | jdone
+  double* Q = work;
+  double* al = Q + (size_t)n * J;
+  double* be = al + J;
+  double* e2 = be + J;
+  double* bounds = e2 + J;
+  double* lam1 = bounds + 8;
+  double* S = lam1 + (k + 1);
+  int* jdone = reinterpret_cast<int*>(S + (size_t)J * (k + 1));
+  cudaError_t err;
+  const bool prof = getenv("CDMD_PROFILE_FIT") != nullptr;
+  cudaEvent_t ev[4];
+  if (prof) for (int i = 0; i < 4; ++i) cudaEventCreate(&ev[i]);
+  auto mark = [&](int i) { if (prof) cudaEventRecord(ev[i], st); };
+  mark(0);
+  if ((err = launch_lz(n, J, G, ldg, al, be, Q, jdone, st)) != cudaSuccess) return err;
+  mark(1);
+  note_launch();
+  eh_prep_kernel<<<1, 256, 0, st>>>(J, al, be, e2, bounds);
+  note_launch();
+  eh_bisect_kernel<<<k + 1, 32 * EH_BW, sizeof(double) * 2 * (size_t)J, st>>>(J, k + 1, al, e2, bounds, lam1, 0,
+                                                                               nullptr);
+  const size_t smem2 = sizeof(double) * 5 * (size_t)J + (size_t)J + 16;
+  note_launch();
+  eh_invit_kernel<<<(unsigned)(k + 1), 32, smem2, st>>>(J, k + 1, al, be, bounds, lam1, S, info);
+  if ((err = cudaGetLastError()) != cudaSuccess) return err;
+  mark(2);
+  if ((err = launch_lz_check(J, k, be, lam1, S, jdone, flag, st)) != cudaSuccess) return err;
+  if ((err = launch_lz_ritz(n, J, k, Q, S, lam1, lam, Zout, st)) != cudaSuccess) return err;
+  mark(3);
+  if (prof) {
+    cudaEventSynchronize(ev[3]);
+    float t[3];
+    for (int i = 0; i < 3; ++i) cudaEventElapsedTime(&t[i], ev[i], ev[i + 1]);
+    fprintf(stderr, "[cdmd_lz] J %d  lanczos %.3f  tridiag eig %.3f  ritz %.3f ms\n", J, t[0], t[1], t[2]);
+    unsigned long long pc[12];
+    lz_prof_read(pc);
+    if (pc[0])   // built with -DCDMD_LZ_PROF
+      fprintf(stderr, "[cdmd_lz] cycles/step: matvec %llu sendA %llu h1 %llu z1 %llu sendB %llu h2 %llu z2 %llu xQ %llu\n",
+              pc[0] / J, pc[1] / J, pc[2] / J, pc[3] / J, pc[4] / J, pc[5] / J, pc[6] / J, pc[7] / J);
+    for (int i = 0; i < 4; ++i) cudaEventDestroy(ev[i]);
+  }
+  return cudaSuccess;
 }
 
 }  // namespace cdmd

@@ -48,12 +48,19 @@ size_t eh_work_doubles(int n, int k);
 cudaError_t launch_eh(int n, int k, const double* G, int64_t ldg, double* lam, double* Zout, double* work,
                       int* info, int med_cnt, double* med, cudaStream_t st);
 
-// symmetric eigensolver: the 8-CTA cluster solver (eigh.cu, default for n1 <= 510),
+bool lz_supported(int n, int k);
+cudaError_t launch_eh_lz(int n, int k, const double* G, int64_t ldg, double* lam, double* Zout, double* work,
+                         int* info, int* flag, cudaStream_t st);
+
+// symmetric eigensolver: Lanczos on a 16-CTA cluster (lanczos.cu, default where it fits;
+// its residual test falls back to the next), the 8-CTA Householder cluster solver
+// (eigh.cu, n1 <= 510), else cuSOLVER syevdx.  CDMD_SYEV=h -> Householder cluster solver,
 // CDMD_SYEV=d -> cuSOLVER syevd, CDMD_SYEV=dx -> cuSOLVER syevdx
 static int syev_mode(int n1, int k) {
   const char* e = getenv("CDMD_SYEV");
   if (e && e[0] == 'd' && e[1] == 0) return 1;
   if (e && e[0] == 'd' && e[1] == 'x') return 2;
+  if (!(e && e[0] == 'h') && lz_supported(n1, k)) return 3;
   return eh_supported(n1, k) ? 0 : 2;
 }
 cudaError_t launch_hqr_eig(int k, const double* A, double* W, double* VR, int* info, double* scratch,
@@ -560,9 +567,15 @@ struct FitProf {
   do {                                                    \
     if ((x) != CUBLAS_STATUS_SUCCESS) return CDMD_ERR_CUDA; \
   } while (0)
-#define CU(x)                                 \
-  do {                                        \
-    if ((x) != cudaSuccess) return CDMD_ERR_CUDA; \
+// CDMD_DEBUG=1: name the failing call and the CUDA error on stderr
+#define CU(x)                                                                               \
+  do {                                                                                      \
+    const cudaError_t e_ = (x);                                                             \
+    if (e_ != cudaSuccess) {                                                                \
+      if (getenv("CDMD_DEBUG")) fprintf(stderr, "[cdmd_fit] %s:%d %s: %s\n", __FILE__, __LINE__, #x, \
+                                        cudaGetErrorString(e_));                            \
+      return CDMD_ERR_CUDA;                                                                 \
+    }                                                                                       \
   } while (0)
 
 cdmd_status fit_impl(cdmd_handle h, const void* Y, int64_t ldy, int kind, int64_t p, int64_t m,
@@ -610,16 +623,29 @@ cdmd_status fit_impl(cdmd_handle h, const void* Y, int64_t ldy, int kind, int64_
   // solver's size (n1 > 510, C5) it takes cuSOLVER's full syevd instead of syevdx
   int smode = syev_mode((int)n1, k);
   if (gd && smode == 2) smode = 1;
+  if (gd && smode == 3) smode = eh_supported((int)n1, k) ? 0 : 1;   // the median needs every eigenvalue
   // the median singular value runs over all min(p, m-1) singular values of Y
   const int med_cnt = gd ? (int)(p < n1 ? p : n1) : 0;
   const double beta = (double)(p < n1 ? p : n1) / (double)(p < n1 ? n1 : p);
   const double gd_omega = gd ? 0.56 * beta * beta * beta - 0.95 * beta * beta + 1.82 * beta + 1.43 : 0.0;
   double* med = W.ehw + eh_work_doubles((int)n1, k) - 8;   // two doubles of the eigh workspace slack
+  if (smode == 3) {
+    // Lanczos: k largest pairs written ascending into (W.w, W.A); dinfo[10] = not converged
+    cudaError_t le = launch_eh_lz((int)n1, k, W.G, m, W.w, W.A, W.ehw, W.dinfo + 8, W.dinfo + 10, st);
+    if (le == cudaErrorNotSupported) {
+      (void)cudaGetLastError();
+      smode = eh_supported((int)n1, k) ? 0 : 2;
+    } else {
+      CU(le);
+    }
+    top = k - 1;
+  }
   if (smode == 0) {
     // cluster tridiagonalisation + bisection + inverse iteration; k largest pairs
     // written ascending into (W.w, W.A) like syevdx
     CU(launch_eh((int)n1, k, W.G, m, W.w, W.A, W.ehw, W.dinfo + 8, med_cnt, med, st));
     top = k - 1;
+  } else if (smode == 3) {
   } else if (smode == 2) {
     // only the k largest eigenpairs (1-based indices n1-k+1 .. n1, ascending)
     int64_t meig = 0;
@@ -645,6 +671,31 @@ cdmd_status fit_impl(cdmd_handle h, const void* Y, int64_t ldy, int kind, int64_
   CU(cudaGetLastError());
   CU(cudaMemcpyAsync(h->host_info, W.dinfo, sizeof(int) * 16, cudaMemcpyDeviceToHost, st));
   CU(cudaStreamSynchronize(st));
+  if (smode == 3) h->lz_runs.fetch_add(1);
+  if (smode == 3 && h->host_info[10] != 0) {
+    // a Ritz pair failed the residual test: the Householder solver decides
+    h->lz_fallbacks.fetch_add(1);
+    if (eh_supported((int)n1, k)) {
+      CU(launch_eh((int)n1, k, W.G, m, W.w, W.A, W.ehw, W.dinfo + 8, 0, nullptr, st));
+    } else {
+      CU(cudaMemcpy2DAsync(W.A, sizeof(double) * n1, W.G, sizeof(double) * m, sizeof(double) * n1, n1,
+                           cudaMemcpyDeviceToDevice, st));
+      int64_t meig = 0;
+      double vl = 0.0, vu = 0.0;
+      if (cusolverDnXsyevdx(h->solver, h->params, CUSOLVER_EIG_MODE_VECTOR, CUSOLVER_EIG_RANGE_I,
+                            CUBLAS_FILL_MODE_LOWER, n1, CUDA_R_64F, W.A, n1, &vl, &vu, n1 - k + 1, n1, &meig,
+                            CUDA_R_64F, W.w, CUDA_R_64F, W.sy_dev, W.sy_dev_bytes,
+                            W.sy_host_bytes ? h->host_ws.data() : nullptr, W.sy_host_bytes,
+                            W.dinfo + 8) != CUSOLVER_STATUS_SUCCESS)
+        return CDMD_ERR_CUDA;
+    }
+    note_launch();
+    select_topk_kernel<<<k, 128, 0, st>>>(W.A, W.w, n1, top, k, W.V, model->sigma, W.dinfo, gd_omega, med_cnt,
+                                          nullptr);
+    CU(cudaGetLastError());
+    CU(cudaMemcpyAsync(h->host_info, W.dinfo, sizeof(int) * 16, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+  }
   prof.mark("select+sync");
   if (h->host_info[8] != 0) {
     model->info = h->host_info[8];

@@ -415,7 +415,7 @@ static cudaError_t launch_kp(const cdmd_video& v, const cdmd_model& M, const flo
   if (const char* e = getenv("CDMD_FG_STAGES")) { const int q = atoi(e); if (q >= 2 && q <= 4) stages = q; }
   while (stages > 2 && fg_smem_bytes(KP, nfb, stages) > 226 * 1024) --stages;
   const size_t smem = fg_smem_bytes(KP, nfb, stages);
-  cudaError_t e = cudaFuncSetAttribute(foreground_tc_kernel<KP, EW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = smem_optin(reinterpret_cast<const void*>(foreground_tc_kernel<KP, EW>));
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);

@@ -644,7 +644,7 @@ cudaError_t launch_fused_fg_median(const cdmd_video& v, const cdmd_model& M, int
     return cudaErrorInvalidValue;
   const int stages = fu_stages(nfb);
   const size_t smem = fu_smem_bytes(nfb, stages);
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = smem_optin(reinterpret_cast<const void*>(kern));
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);

@@ -42,6 +42,8 @@ struct cdmd_handle_s {
   std::mutex mu;
   std::vector<char> host_ws;         // cuSOLVER host workspace (fit only)
   double omega_eps = 0.0;            // > 0: background by |omega| < omega_eps, else OMP
+  std::atomic<uint64_t> lz_runs{0};       // cdmd_fit calls whose eigenpairs came from Lanczos
+  std::atomic<uint64_t> lz_fallbacks{0};  // ... of which failed the residual test (Householder reran)
 };
 
 #define CDMD_SCHED_SLOTS 64

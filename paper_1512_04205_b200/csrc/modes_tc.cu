@@ -351,7 +351,7 @@ static cudaError_t launch_nt(const cdmd_video& v, const cdmd_model& M, float* Ph
   if (stages > 8) stages = 8;
   if (const char* e = getenv("CDMD_MODES_STAGES")) { const int q = atoi(e); if (q >= 2 && q < stages) stages = q; }
   const size_t smem = fixed + (size_t)stages * TC_STAGE;
-  cudaError_t e = cudaFuncSetAttribute(modes_tc_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = smem_optin(reinterpret_cast<const void*>(modes_tc_kernel<NT>));
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -386,7 +386,7 @@ static cudaError_t launch_mc(const cdmd_video& v, const cdmd_model& M, float* Ph
   if (stages > 8) stages = 8;
   if (const char* e = getenv("CDMD_MODES_STAGES")) { const int q = atoi(e); if (q >= 2 && q < stages) stages = q; }
   const size_t smem = fixed + (size_t)stages * TC_STAGE;
-  cudaError_t e = cudaFuncSetAttribute(modes_tc_mc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = smem_optin(reinterpret_cast<const void*>(modes_tc_mc_kernel));
   if (e != cudaSuccess) return e;
   const int num_tiles = (int)ceil_div(v.n_local, TC_BM);
   cudaLaunchConfig_t cfg = {};

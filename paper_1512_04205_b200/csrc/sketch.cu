@@ -156,8 +156,7 @@ bool sketch_sparse_sorted_supported(int64_t p) { return (size_t)p * SK_TF * size
 cudaError_t launch_sketch_sparse_sorted(const cdmd_video& v, const SensingPlan& P, const int32_t* pos,
                                         const int32_t* rs, int nent, int32_t* Y, int64_t ldy, cudaStream_t st) {
   const size_t smem = (size_t)P.p * SK_TF * sizeof(int32_t);
-  cudaError_t e = cudaFuncSetAttribute(sketch_sparse_sorted_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
+  cudaError_t e = smem_optin(reinterpret_cast<const void*>(sketch_sparse_sorted_kernel));
   if (e != cudaSuccess) return e;
   note_launch();
   sketch_sparse_sorted_kernel<<<(unsigned)ceil_div(v.m, SK_TF), SK_T, smem, st>>>(v.X, v.ld, v.pix0, v.n_local, v.m,

@@ -198,8 +198,7 @@ cudaError_t launch_sketch_rademacher_tc(const cdmd_video& v, const SensingPlan& 
   auto smem_of = [&](int s) { return (size_t)1024 + (size_t)s * (xst + SK_CST) + 512; };
   while (stages > 2 && smem_of(stages) > 110 * 1024) --stages;  // two CTAs per SM
   const size_t smem = smem_of(stages);
-  cudaError_t e = cudaFuncSetAttribute(sketch_rademacher_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
+  cudaError_t e = smem_optin(reinterpret_cast<const void*>(sketch_rademacher_tc_kernel));
   if (e != cudaSuccess) return e;
   e = cudaMemsetAsync(Y, 0, sizeof(int32_t) * (size_t)ldy * v.m, st);
   if (e != cudaSuccess) return e;
@@ -555,7 +554,7 @@ cudaError_t launch_sketch_gaussian_tc(const cdmd_video& v, const SensingPlan& P,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return cudaErrorInvalidValue;
   const size_t smem = 1024 + 2 * (size_t)GS_A + 2 * (size_t)npad * GS_BK * 2 + (size_t)GS_XS * npad * GS_XK + 65536 + 512;
-  cudaError_t e = cudaFuncSetAttribute(sketch_gaussian_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = smem_optin(reinterpret_cast<const void*>(sketch_gaussian_tc_kernel));
   if (e != cudaSuccess) return e;
   *splits_out = splits;
   dim3 grid((unsigned)nrb, (unsigned)splits);

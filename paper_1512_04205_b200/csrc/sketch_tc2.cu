@@ -461,7 +461,7 @@ cudaError_t launch_sketch_tc2(const cdmd_video& v, const SensingPlan& P, const u
   const size_t smem = 1024 + (size_t)G2_S * (G2_A + brows * G2_BK * 2) + (size_t)G2_XS * brows * G2_XK + 65536 + 768;
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
   auto kern = sr ? sketch_gaussian_tc2_kernel<true> : sketch_gaussian_tc2_kernel<false>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = smem_optin(reinterpret_cast<const void*>(kern));
   if (e != cudaSuccess) return e;
   *splits_out = splits;
   dim3 grid((unsigned)(2 * npairs), (unsigned)splits);

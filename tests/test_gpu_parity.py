@@ -1229,3 +1229,62 @@ def test_fused_median_needs_word_aligned_rows(C, H):
     with pytest.raises(C.CdmdError) as e:
         P.foreground_median3(Xd, 25.0, 100, 37)
     assert e.value.code == 6
+
+
+@pytest.mark.parametrize("name", ["c2_320x240_spixel", "c4_1080p_sparse"])
+def test_lanczos_eigensolver_matches_oracle_and_householder(C, H, name, monkeypatch):
+    """Step 4's k largest Gram eigenpairs by Lanczos (lanczos.cu) pass the residual test
+    on the paper-shaped sketches (no Householder fallback), agree with the oracle's
+    eigendecomposition (sigma to 1e-6, lambda to RTOL_EIG), and give the same model as
+    the Householder cluster solver (CDMD_SYEV=h) up to rounding."""
+    cfg = config_by_name(name)
+    X = video_for(cfg)
+    m, n = X.shape
+    Xd = to_dev(X)
+    kind = {"sparse": OS.SPARSE, "spixel": OS.SPIXEL}[cfg.kind]
+    Yo = OS.sketch(X, kind, cfg.p, cfg.sensing_seed)
+    om = OD.fit(Yo, cfg.k, cfg.K)
+    models = {}
+    for solver in ("lz", "h"):
+        if solver == "h":
+            monkeypatch.setenv("CDMD_SYEV", "h")
+        else:
+            monkeypatch.delenv("CDMD_SYEV", raising=False)
+        runs0, fb0 = C.cdmd_eigensolver_stats(H)
+        P = C.Pipeline(H, n, n, m, cfg.kind, cfg.p, cfg.k, cfg.K, seed=cfg.sensing_seed)
+        P.sketch(Xd)
+        P.fit()
+        torch.cuda.synchronize()
+        runs1, fb1 = C.cdmd_eigensolver_stats(H)
+        if solver == "lz":
+            assert (runs1 - runs0, fb1 - fb0) == (1, 0), (runs1 - runs0, fb1 - fb0)
+        else:
+            assert runs1 == runs0
+        models[solver] = C.model_to_host(P.model)
+    for gm in models.values():
+        assert gm["k_eff"] == om["k_eff"]
+        perm, err = PT.match_eigs(gm["lam"], om["lam"])
+        assert err <= PT.RTOL_EIG, err
+        assert np.max(np.abs(gm["sigma"] - om["sigma"]) / om["sigma"]) <= 1e-6
+        assert PT.supports_equal_mod_conj(gm["support"], gm["pair"], perm, om["support"], om["pair"])
+    a, b = models["lz"], models["h"]
+    assert np.max(np.abs(a["sigma"] - b["sigma"]) / b["sigma"]) <= 1e-10
+    perm, err = PT.match_eigs(a["lam"], b["lam"])
+    assert err <= 1e-8, err
+
+
+def test_lanczos_falls_back_on_an_invariant_subspace(C, H):
+    """A rank-one Gram (a constant video): the Krylov space closes after one step, the
+    residual test refuses it, and the Householder solver gives k_eff = 1."""
+    rng = np.random.default_rng(5)
+    n, m = 4096 + 77, 40
+    X = np.tile(rng.integers(0, 256, size=n, dtype=np.uint8), (m, 1))
+    Xd = to_dev(X)
+    runs0, fb0 = C.cdmd_eigensolver_stats(H)
+    P = C.Pipeline(H, n, n, m, "sparse", 60, 10, 3, s=5.0)
+    P.sketch(Xd)
+    P.fit()
+    torch.cuda.synchronize()
+    runs1, fb1 = C.cdmd_eigensolver_stats(H)
+    assert (runs1 - runs0, fb1 - fb0) == (1, 1)
+    assert P.model.k_eff == 1
