@@ -418,7 +418,12 @@ cudaError_t launch_lz(int n, int J, const double* G, int64_t ldg, double* alpha,
   cfg.attrs = &at;
   cfg.numAttrs = 1;
   note_launch();
-  return cudaLaunchKernelEx(&cfg, lz_kernel, n, G, ldg, J, alpha, beta, Q, jdone);
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, lz_kernel, n, G, ldg, J, alpha, beta, Q, jdone);
+  if (e == cudaErrorInvalidClusterSize) {   // e.g. a green context with fewer SMs than one cluster
+    (void)cudaGetLastError();
+    return cudaErrorNotSupported;
+  }
+  return e;
 }
 
 cudaError_t launch_lz_check(int J, int k, const double* beta, const double* lam1, const double* S, const int* jdone,

@@ -796,7 +796,10 @@ def test_c5_4k_full_size_sampled(C, H):
 
 
 _PARTITION_SCRIPT = r"""
-import sys, torch
+import os, sys, torch
+# the same eigensolver on both sides: the fit partition's green context may not hold a
+# 16-SM cluster, where cdmd_fit's Lanczos falls back to the Householder solver
+os.environ["CDMD_SYEV"] = "h"
 sys.path.insert(0, sys.argv[1])
 from paper_1512_04205_b200 import cdmd as C
 from synth.scene import config_by_name, video_for

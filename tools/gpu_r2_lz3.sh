@@ -1,5 +1,5 @@
 cd $GRAFT_REPO_ROOT
-CDMD_PROFILE_FIT=1 timeout 120 python tools/probe_fit.py c4_1080p_sparse 3 > gpurun_out/lz3_probe.log 2>&1
-timeout 1500 python -m pytest tests -m gpu -q -x -rf > gpurun_out/lz3_pytest.log 2>&1
-timeout 900 python bench.py --steps 20 --warmup 5 > gpurun_out/lz3_bench.json 2> gpurun_out/lz3_bench.err
+CDMD_DEBUG=1 timeout 600 python -m pytest tests -m gpu -q -rf -k "partition or lanczos or smoke" > gpurun_out/lz3_pytest.log 2>&1
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/lz3_smoke.log 2>&1
+echo "smoke rc $?" >> gpurun_out/lz3_smoke.log
 echo done
