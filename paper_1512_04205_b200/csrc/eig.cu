@@ -696,118 +696,157 @@ __global__ void __launch_bounds__(32) hqr_eig_kernel(int nn, const double* __res
 // hqrv_kernel: A (k x k column-major) -> W (wr, wi pairs as hqr2), H0 (the Hessenberg
 // form, row-major k x k) and Q (row-major k x k) for hinvit_kernel.
 __device__ unsigned long long g_hqr_prof[8];   // orthes, ortran, deflation search, m search, bulge steps, iterations, steps
-void hqr_prof_read(unsigned long long* out) { cudaMemcpyFromSymbol(out, g_hqr_prof, sizeof(unsigned long long) * 8); }
+__device__ unsigned long long g_hqr_prof2[4];  // CDMD_HQR_PROF2: bulge step = scalar chain, row update, column update
+void hqr_prof_read(unsigned long long* out) {
+  cudaMemcpyFromSymbol(out, g_hqr_prof, sizeof(unsigned long long) * 8);
+  cudaMemcpyFromSymbol(out + 8, g_hqr_prof2, sizeof(unsigned long long) * 4);
+}
 
-__global__ void __launch_bounds__(32) hqrv_kernel(int nn, const double* __restrict__ A, double* __restrict__ W,
-                                                 double* __restrict__ H0, double* __restrict__ Qout,
-                                                 int* __restrict__ info) {
+constexpr int HQ_WARPS = 8;   // warps of hqrv_kernel: all reduce to Hessenberg form, warp 0 runs hqr
+
+__global__ void __launch_bounds__(32 * HQ_WARPS, 1) hqrv_kernel(int nn, const double* __restrict__ A,
+                                                            double* __restrict__ W, double* __restrict__ H0,
+                                                            double* __restrict__ Qout, int* __restrict__ info) {
   extern __shared__ double sm[];
   const int ld = nn + 1;
   double* H = sm;                 // nn x ld, row-major
   double* V = H + nn * ld;        // Q, row-major
-  double* ort = V + nn * ld;      // nn
+  const int vsz = nn * ld > 3 * ld + 80 ? nn * ld : 3 * ld + 80;
+  double* ort = V + vsz;          // nn
   double* d = ort + nn;           // nn real parts
   double* e = d + nn;             // nn imaginary parts
   const Warp wp{(int)(threadIdx.x & 31)};
-  const int lane = wp.lane;
+  const int lane = wp.lane, warp = (int)(threadIdx.x >> 5), tid = (int)threadIdx.x;
+  constexpr int NT = 32 * HQ_WARPS;
 #define Hx(i, j) H[(i) * ld + (j)]
 #define Vx(i, j) V[(i) * ld + (j)]
-  for (int idx = lane; idx < nn * nn; idx += 32) {
+  for (int idx = tid; idx < nn * nn; idx += NT) {
     const int i = idx % nn, j = idx / nn;  // A column-major
     Hx(i, j) = A[idx];
     Vx(i, j) = (i == j) ? 1.0 : 0.0;
   }
-  wp.sync();
+  // the padding column and the bulge step's scratch block hold zeros (finite: the step
+  // multiplies them by zero coefficients)
+  for (int i = tid; i < nn; i += NT) Hx(i, nn) = 0.0;
+  __syncthreads();
   unsigned long long pr[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   unsigned long long tq = clock64();
 #define HQ_TICK(k) do { const unsigned long long t_ = clock64(); pr[k] += t_ - tq; tq = t_; } while (0)
   const int low = 0, high = nn - 1;
-  // ------------------------------------------------ orthes (Hessenberg)
+  // ------------------------------------------------ orthes (Hessenberg), all warps.
+  // Thread t = (c, g): c = t % 64 a column (left update) or row (right update), g = t / 64
+  // one of four interleaved slices of the dot product; the four partials meet in part[]
+  // and every thread of the column/row then updates its slice.
+  double* part = e + nn;          // [4][64] partial dots (e's tail of the shared block)
+  double* scr = V;                // 3 x ld + 80 (V's storage once Q is copied out): where the
+                                  // bulge step's idle lanes load and store
+  const int tc_ = tid & 63, tg = tid >> 6;
   for (int m = low + 1; m <= high - 1; ++m) {
+    // the reflector from column m - 1 (every warp redundantly: no barrier for the scalars)
     double scale = 0.0;
     for (int i = m + lane; i <= high; i += 32) scale += fabs(Hx(i, m - 1));
     scale = wp.sum(scale);
-    if (scale != 0.0) {
-      double h = 0.0;
-      const double isc = 1.0 / scale;
-      for (int i = m + lane; i <= high; i += 32) {
-        const double o = Hx(i, m - 1) * isc;
-        ort[i] = o;
-        h += o * o;
-      }
-      h = wp.sum(h);
-      wp.sync();
-      const double om = ort[m];
-      const double g = om > 0 ? -sqrt(h) : sqrt(h);
-      h = h - om * g;
-      wp.sync();
-      if (lane == 0) ort[m] = om - g;
-      wp.sync();
-      const double ih = 1.0 / h;
-      for (int j = m + lane; j < nn; j += 32) {   // H = (I - u u'/h) H
-        double f0 = 0.0, f1 = 0.0, f2 = 0.0, f3 = 0.0;   // four chains: the dot is latency-bound
-        int i = high;
-        for (; i - 3 >= m; i -= 4) {
-          f0 += ort[i] * Hx(i, j);
-          f1 += ort[i - 1] * Hx(i - 1, j);
-          f2 += ort[i - 2] * Hx(i - 2, j);
-          f3 += ort[i - 3] * Hx(i - 3, j);
-        }
-        for (; i >= m; --i) f0 += ort[i] * Hx(i, j);
-        const double f = ((f0 + f1) + (f2 + f3)) * ih;
-        for (int i2 = m; i2 <= high; ++i2) Hx(i2, j) -= f * ort[i2];
-      }
-      wp.sync();
-      for (int i = lane; i <= high; i += 32) {   // H = H (I - u u'/h)
-        double f0 = 0.0, f1 = 0.0, f2 = 0.0, f3 = 0.0;
-        int j = high;
-        for (; j - 3 >= m; j -= 4) {
-          f0 += ort[j] * Hx(i, j);
-          f1 += ort[j - 1] * Hx(i, j - 1);
-          f2 += ort[j - 2] * Hx(i, j - 2);
-          f3 += ort[j - 3] * Hx(i, j - 3);
-        }
-        for (; j >= m; --j) f0 += ort[j] * Hx(i, j);
-        const double f = ((f0 + f1) + (f2 + f3)) * ih;
-        for (int j2 = m; j2 <= high; ++j2) Hx(i, j2) -= f * ort[j2];
-      }
-      wp.sync();
-      if (lane == 0) {
-        ort[m] = scale * ort[m];
-        Hx(m, m - 1) = scale * g;
-      }
-      wp.sync();
+    if (scale == 0.0) continue;   // uniform across the CTA
+    const double isc = 1.0 / scale;
+    double h = 0.0;
+    for (int i = m + lane; i <= high; i += 32) {
+      const double o = Hx(i, m - 1) * isc;
+      h += o * o;
     }
+    h = wp.sum(h);
+    const double om = Hx(m, m - 1) * isc;
+    const double g = om > 0 ? -sqrt(h) : sqrt(h);
+    h = h - om * g;
+    const double ih = 1.0 / h;
+    __syncthreads();   // every warp has read column m - 1
+    if (tid <= high - m) ort[m + tid] = tid == 0 ? om - g : Hx(m + tid, m - 1) * isc;
+    __syncthreads();
+    // H = (I - u u'/h) H: f_j = u' H(:, j), j = m .. nn-1
+    for (int j0 = m; j0 < nn; j0 += 64) {
+      const int j = j0 + tc_;
+      double f0 = 0.0, f1 = 0.0;
+      if (j < nn) {
+        int i = m + tg;
+        for (; i + 4 <= high; i += 8) {
+          f0 = fma(ort[i], Hx(i, j), f0);
+          f1 = fma(ort[i + 4], Hx(i + 4, j), f1);
+        }
+        if (i <= high) f0 = fma(ort[i], Hx(i, j), f0);
+        part[tg * 64 + tc_] = f0 + f1;
+      }
+      __syncthreads();
+      if (j < nn) {
+        const double f = ((part[tc_] + part[64 + tc_]) + (part[128 + tc_] + part[192 + tc_])) * ih;
+        for (int i = m + tg; i <= high; i += 4) Hx(i, j) -= f * ort[i];
+      }
+      __syncthreads();
+    }
+    // H = H (I - u u'/h): g_i = H(i, :) u, i = 0 .. high
+    for (int i0 = 0; i0 <= high; i0 += 64) {
+      const int i = i0 + tc_;
+      double f0 = 0.0, f1 = 0.0;
+      if (i <= high) {
+        int j = m + tg;
+        for (; j + 4 <= high; j += 8) {
+          f0 = fma(ort[j], Hx(i, j), f0);
+          f1 = fma(ort[j + 4], Hx(i, j + 4), f1);
+        }
+        if (j <= high) f0 = fma(ort[j], Hx(i, j), f0);
+        part[tg * 64 + tc_] = f0 + f1;
+      }
+      __syncthreads();
+      if (i <= high) {
+        const double f = ((part[tc_] + part[64 + tc_]) + (part[128 + tc_] + part[192 + tc_])) * ih;
+        for (int j = m + tg; j <= high; j += 4) Hx(i, j) -= f * ort[j];
+      }
+      __syncthreads();
+    }
+    if (tid == 0) {
+      ort[m] = scale * ort[m];
+      Hx(m, m - 1) = scale * g;
+    }
+    __syncthreads();
   }
   HQ_TICK(0);
-  // ortran: Q explicitly
+  // ortran: Q explicitly, V(:, j) += g_j u with g_j = u' V(:, j) / (u_m H(m, m-1)),
+  // the same (column, slice) thread map
   for (int m = high - 1; m >= low + 1; --m) {
-    if (Hx(m, m - 1) != 0.0) {
-      for (int i = m + 1 + lane; i <= high; i += 32) ort[i] = Hx(i, m - 1);
-      wp.sync();
-      for (int j = m + lane; j <= high; j += 32) {
-        double g0 = 0.0, g1 = 0.0, g2 = 0.0, g3 = 0.0;
-        int i = m;
-        for (; i + 3 <= high; i += 4) {
-          g0 += ort[i] * Vx(i, j);
-          g1 += ort[i + 1] * Vx(i + 1, j);
-          g2 += ort[i + 2] * Vx(i + 2, j);
-          g3 += ort[i + 3] * Vx(i + 3, j);
+    const double hm = Hx(m, m - 1);
+    if (hm == 0.0) continue;   // uniform
+    if (tid >= 1 && tid <= high - m) ort[m + tid] = Hx(m + tid, m - 1);
+    __syncthreads();
+    const double iom = 1.0 / (ort[m] * hm);
+    for (int j0 = m; j0 <= high; j0 += 64) {
+      const int j = j0 + tc_;
+      double f0 = 0.0, f1 = 0.0;
+      if (j <= high) {
+        int i = m + tg;
+        for (; i + 4 <= high; i += 8) {
+          f0 = fma(ort[i], Vx(i, j), f0);
+          f1 = fma(ort[i + 4], Vx(i + 4, j), f1);
         }
-        for (; i <= high; ++i) g0 += ort[i] * Vx(i, j);
-        const double g = (((g0 + g1) + (g2 + g3)) / ort[m]) / Hx(m, m - 1);
-        for (int i2 = m; i2 <= high; ++i2) Vx(i2, j) += g * ort[i2];
+        if (i <= high) f0 = fma(ort[i], Vx(i, j), f0);
+        part[tg * 64 + tc_] = f0 + f1;
       }
-      wp.sync();
+      __syncthreads();
+      if (j <= high) {
+        const double f = ((part[tc_] + part[64 + tc_]) + (part[128 + tc_] + part[192 + tc_])) * iom;
+        for (int i = m + tg; i <= high; i += 4) Vx(i, j) += f * ort[i];
+      }
+      __syncthreads();
     }
   }
   // the Hessenberg form and Q for the inverse iteration (below-subdiagonal entries are
   // orthes' workspace: zero them in the copy)
-  for (int idx = lane; idx < nn * nn; idx += 32) {
+  for (int idx = tid; idx < nn * nn; idx += NT) {
     const int i = idx / nn, j = idx % nn;
     H0[idx] = (i > j + 1) ? 0.0 : Hx(i, j);
     Qout[idx] = Vx(i, j);
   }
+  __syncthreads();   // Q copied out: V's storage becomes the scratch block
+  for (int i = tid; i < 3 * ld + 80; i += NT) scr[i] = 0.0;
+  __syncthreads();
+  if (warp != 0) return;   // hqr below is one warp's: no CTA barrier after this point
   // ------------------------------------------------------- hqr (values only)
   int n = nn - 1;
   const double eps = 0x1p-52;
@@ -818,6 +857,9 @@ __global__ void __launch_bounds__(32) hqrv_kernel(int nn, const double* __restri
     for (int j = (i > 0 ? i - 1 : 0); j < nn; ++j) norm += fabs(Hx(i, j));
   norm = wp.sum(norm);
   int iter = 0, total_iter = 0, fail = 0;
+#ifdef CDMD_HQR_PROF2
+  unsigned long long pb[3] = {0, 0, 0};
+#endif
   HQ_TICK(1);
   while (n >= low) {
     // deflation search, 32 candidates per round: the largest l in (low, n] with a
@@ -951,12 +993,60 @@ __global__ void __launch_bounds__(32) hqrv_kernel(int nn, const double* __restri
       }
       wp.sync();
       pr[6] += n - m;
+#ifdef CDMD_HQR_PROF2
+      unsigned long long tb_prev = clock64();
+#endif
+      // Each step splits into the 3 x 3 block B = H(kk..kk+2, kk..kk+2) and row kk+3 of
+      // columns kk..kk+2, which every lane updates redundantly in registers (they hold the
+      // next step's p, q, r: no shuffle or shared-memory round trip on the chain), and the
+      // rest -- rows kk..kk+2 of columns kk+3..n, columns kk..kk+2 of rows l..kk-1 -- one
+      // column / row per lane slot.  Every operand is loaded at the top of the step, before
+      // the reflector is known.  Idle lanes and the absent row / column kk+2 of the last
+      // step (r = z = 0) use the scratch block: scr[0..2] stays zero, scr[4..6] is the
+      // column-update dummy, scr[8 + lane + {0, ld, 2 ld}] the row-update dummies.
+      double* const Z0 = scr;
+      double* const CD = scr + 4;
+      bool nreg = false;
+      double pn = 0.0, qn = 0.0, rn = 0.0;
       for (int kk = m; kk <= n - 1; ++kk) {  // double QR step on the active block l..n
         const bool notlast = (kk != n - 1);
+        // ---- operands (independent of this step's reflector)
+        double* bp[3][3];
+#pragma unroll
+        for (int t = 0; t < 3; ++t)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) bp[t][c] = (notlast || (t < 2 && c < 2)) ? &Hx(kk + t, kk + c) : Z0;
+        double B[3][3];
+#pragma unroll
+        for (int t = 0; t < 3; ++t)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) B[t][c] = *bp[t][c];
+        const bool has3 = kk + 3 <= n;
+        const double* r3l = has3 ? &Hx(kk + 3, kk) : Z0;
+        double* r3s = has3 ? &Hx(kk + 3, kk) : CD;
+        double r30 = r3l[0], r31 = r3l[1], r32 = notlast ? r3l[2] : 0.0;
+        const int j0 = kk + 3 + lane, j1 = j0 + 32;
+        double* rb0 = j0 <= n ? &Hx(kk, j0) : scr + 8 + lane;
+        double* rb1 = j1 <= n ? &Hx(kk, j1) : scr + 40 + lane;
+        double u0 = rb0[0], u1 = rb0[ld], u2 = rb0[2 * ld];
+        double w0 = rb1[0], w1 = rb1[ld], w2 = rb1[2 * ld];
+        const int i0 = l + lane, i1 = i0 + 32;
+        double* cb0 = i0 <= kk - 1 ? &Hx(i0, kk) : CD;
+        double* cb1 = i1 <= kk - 1 ? &Hx(i1, kk) : CD;
+        double g00 = cb0[0], g01 = cb0[1], g02 = cb0[2];
+        double g10 = cb1[0], g11 = cb1[1], g12 = cb1[2];
+        // ---- the reflector
         if (kk != m) {
-          p = Hx(kk, kk - 1);
-          q = Hx(kk + 1, kk - 1);
-          r = notlast ? Hx(kk + 2, kk - 1) : 0.0;
+          if (nreg) {
+            p = pn;
+            q = qn;
+            r = notlast ? rn : 0.0;
+          } else {
+            p = Hx(kk, kk - 1);
+            q = Hx(kk + 1, kk - 1);
+            r = notlast ? Hx(kk + 2, kk - 1) : 0.0;
+          }
+          nreg = false;
           x = fabs(p) + fabs(q) + fabs(r);
           if (x == 0.0) continue;
           if (x < 1e-140 || x > 1e140) {
@@ -968,59 +1058,137 @@ __global__ void __launch_bounds__(32) hqrv_kernel(int nn, const double* __restri
             x = 1.0;
           }
         }
+        nreg = false;
         const double ss = p * p + q * q + r * r;
-        s = ss > 0.0 ? ss * rsqrt_nr(ss) : 0.0;
-        if (p < 0) s = -s;
-        if (s != 0) {
-          double newsub = 0.0;
-          bool setsub = false;
-          if (kk != m) {
-            newsub = -s * x;
-            setsub = true;
-          } else if (l != m) {
-            newsub = -Hx(kk, kk - 1);
-            setsub = true;
-          }
-          // H(kk, kk-1) is touched by no other update of this step (rows kk.. / columns
-          // kk..kk+2 below): no barrier around its store, the step's later barriers order it
-          wp.sync();   // every lane has read H(kk, kk-1) above
-          if (setsub && lane == 0) Hx(kk, kk - 1) = newsub;
-          p = p + s;
-          const double is = rcp_nr(s), ip = rcp_nr(p);
-          x = p * is;
-          y = q * is;
-          z = r * is;
-          q = q * ip;
-          r = r * ip;
-          for (int j = kk + lane; j <= n; j += 32) {  // rows kk..kk+2, columns kk..n
-            double pp = Hx(kk, j) + q * Hx(kk + 1, j);
-            if (notlast) {
-              pp = pp + r * Hx(kk + 2, j);
-              Hx(kk + 2, j) = Hx(kk + 2, j) - pp * z;
-            }
-            Hx(kk, j) = Hx(kk, j) - pp * x;
-            Hx(kk + 1, j) = Hx(kk + 1, j) - pp * y;
-          }
-          wp.sync();
-          const int imax = n < kk + 3 ? n : kk + 3;
-          for (int i = l + lane; i <= imax; i += 32) {  // columns kk..kk+2, rows l..imax
-            double pp = x * Hx(i, kk) + y * Hx(i, kk + 1);
-            if (notlast) {
-              pp = pp + z * Hx(i, kk + 2);
-              Hx(i, kk + 2) = Hx(i, kk + 2) - pp * r;
-            }
-            Hx(i, kk) = Hx(i, kk) - pp;
-            Hx(i, kk + 1) = Hx(i, kk + 1) - pp * q;
-          }
-          wp.sync();
+        const double rs = ss > 0.0 ? rsqrt_nr(ss) : 0.0;
+        s = ss * rs;
+        double is = rs;   // 1 / s
+        if (p < 0) {
+          s = -s;
+          is = -is;
         }
+        if (s == 0) continue;
+        if (kk != m) {
+          Hx(kk, kk - 1) = -s * x;   // every lane the same value; read by no lane this step
+        } else if (l != m) {
+          const double hs = Hx(kk, kk - 1);
+          wp.sync();
+          Hx(kk, kk - 1) = -hs;
+        }
+#ifdef CDMD_HQR_PROF2
+        unsigned long long tb0 = clock64();
+#endif
+        p = p + s;
+        const double ip = rcp_nr(p);
+        x = p * is;
+        y = q * is;
+        z = r * is;
+        q = q * ip;
+        r = r * ip;
+        // ---- block and row kk+3 (every lane): rows from the left, then columns from the right
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const double pp = fma(r, B[2][c], fma(q, B[1][c], B[0][c]));
+          B[0][c] -= pp * x;
+          B[1][c] -= pp * y;
+          B[2][c] -= pp * z;
+        }
+#pragma unroll
+        for (int t = 0; t < 3; ++t) {
+          const double pp = fma(z, B[t][2], fma(y, B[t][1], x * B[t][0]));
+          B[t][0] -= pp;
+          B[t][1] -= pp * q;
+          B[t][2] -= pp * r;
+        }
+        {
+          const double pp = fma(z, r32, fma(y, r31, x * r30));
+          r30 -= pp;
+          r31 -= pp * q;
+          r32 -= pp * r;
+        }
+        // ---- the rest, a column / row per lane slot
+        {
+          const double pu = fma(r, u2, fma(q, u1, u0));
+          const double pw = fma(r, w2, fma(q, w1, w0));
+          u0 -= pu * x;
+          u1 -= pu * y;
+          u2 -= pu * z;
+          w0 -= pw * x;
+          w1 -= pw * y;
+          w2 -= pw * z;
+          const double pg = fma(z, g02, fma(y, g01, x * g00));
+          const double ph = fma(z, g12, fma(y, g11, x * g10));
+          g00 -= pg;
+          g01 -= pg * q;
+          g02 -= pg * r;
+          g10 -= ph;
+          g11 -= ph * q;
+          g12 -= ph * r;
+        }
+#ifdef CDMD_HQR_PROF2
+        unsigned long long tb1 = clock64();
+#endif
+#pragma unroll
+        for (int t = 0; t < 3; ++t)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) *bp[t][c] = B[t][c];
+        r3s[0] = r30;
+        r3s[1] = r31;
+        if (notlast) r3s[2] = r32;
+        rb0[0] = u0;
+        rb0[ld] = u1;
+        rb0[2 * ld] = u2;
+        rb1[0] = w0;
+        rb1[ld] = w1;
+        rb1[2 * ld] = w2;
+        cb0[0] = g00;
+        cb0[1] = g01;
+        cb0[2] = g02;
+        cb1[0] = g10;
+        cb1[1] = g11;
+        cb1[2] = g12;
+        // slots beyond two (n > 64): plain loops
+        for (int j = j1 + 32; j <= n; j += 32) {
+          double pp = Hx(kk, j) + q * Hx(kk + 1, j);
+          if (notlast) {
+            pp = pp + r * Hx(kk + 2, j);
+            Hx(kk + 2, j) = Hx(kk + 2, j) - pp * z;
+          }
+          Hx(kk, j) = Hx(kk, j) - pp * x;
+          Hx(kk + 1, j) = Hx(kk + 1, j) - pp * y;
+        }
+        for (int i = i1 + 32; i <= kk - 1; i += 32) {
+          double pp = x * Hx(i, kk) + y * Hx(i, kk + 1);
+          if (notlast) {
+            pp = pp + z * Hx(i, kk + 2);
+            Hx(i, kk + 2) = Hx(i, kk + 2) - pp * r;
+          }
+          Hx(i, kk) = Hx(i, kk) - pp;
+          Hx(i, kk + 1) = Hx(i, kk + 1) - pp * q;
+        }
+        pn = B[1][0];
+        qn = B[2][0];
+        rn = r30;
+        nreg = true;
+        wp.sync();
+#ifdef CDMD_HQR_PROF2
+        unsigned long long tb2 = clock64();
+        pb[0] += tb0 - tb_prev;
+        pb[1] += tb1 - tb0;
+        pb[2] += tb2 - tb1;
+        tb_prev = tb2;
+#endif
       }
       HQ_TICK(4);
     }
   }
   wp.sync();
-  if (lane == 0)
+  if (lane == 0) {
     for (int k2 = 0; k2 < 7; ++k2) g_hqr_prof[k2] = pr[k2];
+#ifdef CDMD_HQR_PROF2
+    for (int k2 = 0; k2 < 3; ++k2) g_hqr_prof2[k2] = pb[k2];
+#endif
+  }
 #undef HQ_TICK
   if (fail) {
     if (lane == 0) *info = 1;
@@ -1167,7 +1335,12 @@ __global__ void __launch_bounds__(32) hinvit_kernel(int nn, const double* __rest
   }
 }
 
-size_t hqr_smem_bytes(int k) { return sizeof(double) * ((size_t)2 * k * (k + 1) + 3 * (size_t)k); }
+// hqrv: H | V (at least the bulge step's 3 (k+1) + 64 scratch) | ort, d, e | part[256]
+static size_t hqr_vsz(int k) {
+  const size_t a = (size_t)k * (k + 1), b = 3 * ((size_t)k + 1) + 80;
+  return a > b ? a : b;
+}
+size_t hqr_smem_bytes(int k) { return sizeof(double) * ((size_t)k * (k + 1) + hqr_vsz(k) + 3 * (size_t)k + 256); }
 static size_t hqr_smem_par3(int k) { return hqr_smem_bytes(k) + sizeof(double) * 64 * (size_t)k; }
 
 static size_t hinvit_smem(int k) { return sizeof(double) * ((size_t)2 * k * (k + 1) + 4 * (size_t)k) + k + 16; }
@@ -1182,7 +1355,7 @@ cudaError_t launch_hqr_eig(int k, const double* A, double* W, double* VR, int* i
     cudaError_t e = smem_optin(reinterpret_cast<const void*>(hqrv_kernel));
     if (e != cudaSuccess) return e;
     note_launch();
-    hqrv_kernel<<<1, 32, smem, st>>>(k, A, W, H0, Q, info);
+    hqrv_kernel<<<1, 32 * HQ_WARPS, smem, st>>>(k, A, W, H0, Q, info);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     const size_t smem2 = hinvit_smem(k);
     e = smem_optin(reinterpret_cast<const void*>(hinvit_kernel));

@@ -261,18 +261,41 @@ __global__ void __cluster_dims__(EH_CL, 1, 1) __launch_bounds__(EH_T, 1)
   if (rank == ((n - 1) % EH_CL) && tid == 0) d[n - 1] = Aloc[eh_off(rank, (n - 1) / EH_CL) + (n - 1)];
 }
 
-// Gershgorin bounds, ||T||, pivmin and e^2 (one block)
+// Gershgorin bounds, ||T||, pivmin and e^2 (one block; min / max reductions over the
+// threads, exact in any order)
 __global__ void eh_prep_kernel(int n, const double* __restrict__ d, const double* __restrict__ e,
                                double* __restrict__ e2, double* __restrict__ bounds) {
-  for (int i = threadIdx.x; i < n; i += blockDim.x) e2[i] = i < n - 1 ? e[i] * e[i] : 0.0;
+  __shared__ double rgl[32], rgu[32], rtn[32], rem[32];
+  double gl = INFINITY, gu = -INFINITY, tn = 0.0, emax2 = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const double ei = i < n - 1 ? e[i] : 0.0;
+    e2[i] = ei * ei;
+    const double r = (i > 0 ? fabs(e[i - 1]) : 0.0) + fabs(ei);
+    gl = fmin(gl, d[i] - r);
+    gu = fmax(gu, d[i] + r);
+    tn = fmax(tn, fabs(d[i]) + r);
+    emax2 = fmax(emax2, ei * ei);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    gl = fmin(gl, __shfl_xor_sync(0xffffffffu, gl, o));
+    gu = fmax(gu, __shfl_xor_sync(0xffffffffu, gu, o));
+    tn = fmax(tn, __shfl_xor_sync(0xffffffffu, tn, o));
+    emax2 = fmax(emax2, __shfl_xor_sync(0xffffffffu, emax2, o));
+  }
+  const int w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    rgl[w] = gl;
+    rgu[w] = gu;
+    rtn[w] = tn;
+    rem[w] = emax2;
+  }
+  __syncthreads();
   if (threadIdx.x == 0) {
-    double gl = d[0], gu = d[0], tn = 0.0, emax2 = 0.0;
-    for (int i = 0; i < n; ++i) {
-      const double r = (i > 0 ? fabs(e[i - 1]) : 0.0) + (i < n - 1 ? fabs(e[i]) : 0.0);
-      gl = fmin(gl, d[i] - r);
-      gu = fmax(gu, d[i] + r);
-      tn = fmax(tn, fabs(d[i]) + r);
-      if (i < n - 1) emax2 = fmax(emax2, e[i] * e[i]);
+    for (int v = 1; v < nw; ++v) {
+      gl = fmin(gl, rgl[v]);
+      gu = fmax(gu, rgu[v]);
+      tn = fmax(tn, rtn[v]);
+      emax2 = fmax(emax2, rem[v]);
     }
     const double pivmin = fmax(2.2250738585072014e-308 * fmax(emax2, 1.0), 1e-300);
     const double pad = 2.0 * 2.220446049250313e-16 * tn * n + 2.0 * pivmin;
@@ -426,8 +449,17 @@ __global__ void __launch_bounds__(32) eh_invit_kernel(int n, int k, const double
   double* u2 = u1 + n;
   double* lm = u2 + n;
   double* z = lm + n;
-  uint8_t* pv = reinterpret_cast<uint8_t*>(z + n);   // rows i, i+1 swapped
+  double* ds = z + n;             // d, e staged: lane 0's LU reads them on a serial chain
+  double* es = ds + n;
+  uint8_t* pv = reinterpret_cast<uint8_t*>(es + n);   // rows i, i+1 swapped
   const int lane = threadIdx.x;
+  for (int i = lane; i < n; i += 32) {
+    ds[i] = d[i];
+    es[i] = e[i];
+  }
+  __syncwarp();
+  d = ds;
+  e = es;
   const double tnorm = bounds[2];
   const double eps = 2.220446049250313e-16;
   // group c of the descending order r = 0 .. k-1 (q = k-1-r): [r0, r1)
@@ -645,7 +677,7 @@ cudaError_t launch_eh(int n, int k, const double* G, int64_t ldg, double* lam, d
       n, k, d, e2, bounds, lam, med_cnt, med);
   mark(2);
   note_launch();
-  const size_t smem2 = sizeof(double) * 5 * (size_t)n + (size_t)n + 16;
+  const size_t smem2 = sizeof(double) * 7 * (size_t)n + (size_t)n + 16;
   err = smem_optin(reinterpret_cast<const void*>(eh_invit_kernel));
   if (err != cudaSuccess) return err;
   eh_invit_kernel<<<(unsigned)k, 32, smem2, st>>>(n, k, d, e, bounds, lam, Zout, info);
@@ -692,18 +724,20 @@ cudaError_t launch_eh_lz(int n, int k, const double* G, int64_t ldg, double* lam
   int* jdone = reinterpret_cast<int*>(S + (size_t)J * (k + 1));
   cudaError_t err;
   const bool prof = getenv("CDMD_PROFILE_FIT") != nullptr;
-  cudaEvent_t ev[4];
-  if (prof) for (int i = 0; i < 4; ++i) cudaEventCreate(&ev[i]);
+  cudaEvent_t ev[6];
+  if (prof) for (int i = 0; i < 6; ++i) cudaEventCreate(&ev[i]);
   auto mark = [&](int i) { if (prof) cudaEventRecord(ev[i], st); };
   mark(0);
   if ((err = launch_lz(n, J, G, ldg, al, be, Q, jdone, st)) != cudaSuccess) return err;
   mark(1);
   note_launch();
   eh_prep_kernel<<<1, 256, 0, st>>>(J, al, be, e2, bounds);
+  mark(4);
   note_launch();
   eh_bisect_kernel<<<k + 1, 32 * EH_BW, sizeof(double) * 2 * (size_t)J, st>>>(J, k + 1, al, e2, bounds, lam1, 0,
                                                                                nullptr);
-  const size_t smem2 = sizeof(double) * 5 * (size_t)J + (size_t)J + 16;
+  mark(5);
+  const size_t smem2 = sizeof(double) * 7 * (size_t)J + (size_t)J + 16;
   note_launch();
   eh_invit_kernel<<<(unsigned)(k + 1), 32, smem2, st>>>(J, k + 1, al, be, bounds, lam1, S, info);
   if ((err = cudaGetLastError()) != cudaSuccess) return err;
@@ -715,13 +749,17 @@ cudaError_t launch_eh_lz(int n, int k, const double* G, int64_t ldg, double* lam
     cudaEventSynchronize(ev[3]);
     float t[3];
     for (int i = 0; i < 3; ++i) cudaEventElapsedTime(&t[i], ev[i], ev[i + 1]);
-    fprintf(stderr, "[cdmd_lz] J %d  lanczos %.3f  tridiag eig %.3f  ritz %.3f ms\n", J, t[0], t[1], t[2]);
+    float tp = 0.f, tb = 0.f;
+    cudaEventElapsedTime(&tp, ev[1], ev[4]);
+    cudaEventElapsedTime(&tb, ev[4], ev[5]);
+    fprintf(stderr, "[cdmd_lz] J %d  lanczos %.3f  tridiag eig %.3f (prep %.3f bisect %.3f)  ritz %.3f ms\n", J, t[0],
+            t[1], tp, tb, t[2]);
     unsigned long long pc[12];
     lz_prof_read(pc);
     if (pc[0])   // built with -DCDMD_LZ_PROF
       fprintf(stderr, "[cdmd_lz] cycles/step: matvec %llu sendA %llu h1 %llu z1 %llu sendB %llu h2 %llu z2 %llu xQ %llu\n",
               pc[0] / J, pc[1] / J, pc[2] / J, pc[3] / J, pc[4] / J, pc[5] / J, pc[6] / J, pc[7] / J);
-    for (int i = 0; i < 4; ++i) cudaEventDestroy(ev[i]);
+    for (int i = 0; i < 6; ++i) cudaEventDestroy(ev[i]);
   }
   return cudaSuccess;
 }

@@ -302,11 +302,34 @@ __device__ __forceinline__ cplx gram_c(const double* Gf, int k, const int32_t* p
 
 // OMP (Remark 3 P:363-369) in Gram form + background coefficient table.
 // One block.  corr_j = phi_j^H r = alpha_j - sum_{s in S} <phi_j, phi_s> beta_s.
+__device__ unsigned long long g_omp_prof[4];   // cycles: staging, selection, outputs, coefficient table
 __global__ void __launch_bounds__(256) omp_kernel(
-    int k, int K, int64_t m, const double* __restrict__ Gf, const double* __restrict__ cf,
-    const double* __restrict__ G, const int32_t* __restrict__ pair, const double* __restrict__ lam,
+    int k, int K, int64_t m, const double* __restrict__ Gf_g, const double* __restrict__ cf,
+    const double* __restrict__ G, const int32_t* __restrict__ pair_g, const double* __restrict__ lam_g,
     double* __restrict__ beta_out, int32_t* __restrict__ support_out, float* __restrict__ coef,
-    int32_t* __restrict__ coef_col, int* __restrict__ dinfo, double omega_eps, double dt) {
+    int32_t* __restrict__ coef_col, int* __restrict__ dinfo, double omega_eps, double dt, int staged) {
+  // staged: Gf (k x k), lambda (2k) and the pairing (k) copied to shared memory first --
+  // the selection loop and the Cholesky read them one element at a time on serial chains
+  extern __shared__ double omp_dyn[];
+  const unsigned long long tp0 = clock64();
+  const double* Gf = Gf_g;
+  const double* lam = lam_g;
+  const int32_t* pair = pair_g;
+  cplx* Gc = nullptr;   // staged: the complex Gram <phi_i, phi_j> of the modes, k x k
+  if (staged) {
+    Gc = reinterpret_cast<cplx*>(omp_dyn);
+    double* ls = omp_dyn + 2 * (size_t)k * k;
+    int32_t* ps = reinterpret_cast<int32_t*>(ls + 2 * k);
+    for (int i = threadIdx.x; i < 2 * k; i += blockDim.x) ls[i] = lam_g[i];
+    for (int i = threadIdx.x; i < k; i += blockDim.x) ps[i] = pair_g[i];
+    __syncthreads();
+    lam = ls;
+    pair = ps;
+    for (int idx = threadIdx.x; idx < k * k; idx += blockDim.x) Gc[idx] = gram_c(Gf_g, k, pair, idx / k, idx % k);
+    __syncthreads();
+  }
+  auto gram = [&](int i, int j) -> cplx { return Gc ? Gc[i * k + j] : gram_c(Gf, k, pair, i, j); };
+  const unsigned long long tp1 = clock64();
   __shared__ double sc[512];
   __shared__ double red[256];
   __shared__ int redi[256];
@@ -360,12 +383,12 @@ __global__ void __launch_bounds__(256) omp_kernel(
     for (int j = tid; j < k; j += blockDim.x) {
       bool in = false;
       for (int s = 0; s < nS; ++s) in |= (S[s] == j);
-      const cplx gjj = gram_c(Gf, k, pair, j, j);
+      const cplx gjj = gram(j, j);
       double score = -1.0;
       if (!in && gjj.r > 0.0) {
         cplx c = alpha[j];
         for (int s = 0; s < nS; ++s) {
-          const cplx g = gram_c(Gf, k, pair, j, S[s]);
+          const cplx g = gram(j, S[s]);
           const cplx t = cmul(g, beta[s]);
           c.r -= t.r; c.i -= t.i;
         }
@@ -398,11 +421,12 @@ __global__ void __launch_bounds__(256) omp_kernel(
       } else {
         S[nS] = js;
         const int n = nS + 1;
-        // complex Cholesky of Gc[S,S] (Hermitian positive definite), from scratch
+        // complex Cholesky of Gc[S,S] (Hermitian positive definite): rows 0..n-2 are the
+        // previous iteration's factor (the same support), only row n-1 is new
         bool ok = true;
-        for (int a = 0; a < n && ok; ++a) {
+        for (int a = n - 1; a < n && ok; ++a) {
           for (int b = 0; b <= a; ++b) {
-            cplx s = gram_c(Gf, k, pair, S[a], S[b]);  // <phi_a, phi_b>: row a, col b
+            cplx s = gram(S[a], S[b]);  // <phi_a, phi_b>: row a, col b
             for (int q = 0; q < b; ++q) {
               const cplx t = cmul(Lc[a * 32 + q], cplx{Lc[b * 32 + q].r, -Lc[b * 32 + q].i});
               s.r -= t.r; s.i -= t.i;
@@ -448,6 +472,7 @@ __global__ void __launch_bounds__(256) omp_kernel(
     if (stop_sh) break;
   }
   __syncthreads();
+  const unsigned long long tp2 = clock64();
   const int nS = nS_sh;
   // outputs + used fold columns (sorted, unique)
   if (tid == 0) {
@@ -478,30 +503,56 @@ __global__ void __launch_bounds__(256) omp_kernel(
     dinfo[INFO_N_COEF] = nF;
   }
   __syncthreads();
+  const unsigned long long tp3 = clock64();
   const int nF = nF_sh;
   // coef[f][t] = sum over support modes touching fold column F[f] of
   //   Re(beta lambda^t) (the f_ra part) or -sg Im(beta lambda^t) (the f_rb part)
-  for (int64_t idx = tid; idx < (int64_t)nF * m; idx += blockDim.x) {
-    const int f = (int)(idx / m);
-    const int64_t t = idx % m;
-    double acc = 0.0;
+  // (per frame t: beta_s lambda_s^t of each support mode once, then the fold columns'
+  // sums in support order)
+  __shared__ double llog[32], larg_s[32];
+  __shared__ int sra[32], srb[32];
+  __shared__ double ssg[32];
+  if (tid < nS) {
+    const double lr = lam[2 * S[tid]], li = lam[2 * S[tid] + 1];
+    llog[tid] = log(hypot(lr, li));
+    larg_s[tid] = atan2(li, lr);
+    int ra, rb;
+    double sg;
+    mode_rep(pair, S[tid], ra, rb, sg);
+    sra[tid] = ra;
+    srb[tid] = rb;
+    ssg[tid] = sg;
+  }
+  __syncthreads();
+  for (int64_t t = tid; t < m; t += blockDim.x) {
+    cplx cs_[32];
     for (int s = 0; s < nS; ++s) {
-      int ra, rb;
-      double sg;
-      mode_rep(pair, S[s], ra, rb, sg);
-      if (ra != F[f] && !(sg != 0.0 && rb == F[f])) continue;
-      const double lr = lam[2 * S[s]], li = lam[2 * S[s] + 1];
-      const double lmod = hypot(lr, li), larg = atan2(li, lr);
-      const double mag = exp((double)t * log(lmod));
+      const double mag = exp((double)t * llog[s]);
       double sn, cs;
-      sincos((double)t * larg, &sn, &cs);
-      const cplx c = cmul(beta[s], cplx{mag * cs, mag * sn});
-      if (ra == F[f]) acc += c.r;
-      if (sg != 0.0 && rb == F[f]) acc += -sg * c.i;
+      sincos((double)t * larg_s[s], &sn, &cs);
+      cs_[s] = cmul(beta[s], cplx{mag * cs, mag * sn});
     }
-    coef[f * m + t] = (float)acc;
+    for (int f = 0; f < nF; ++f) {
+      double acc = 0.0;
+      for (int s = 0; s < nS; ++s) {
+        const int ra = sra[s], rb = srb[s];
+        const double sg = ssg[s];
+        if (ra != F[f] && !(sg != 0.0 && rb == F[f])) continue;
+        if (ra == F[f]) acc += cs_[s].r;
+        if (sg != 0.0 && rb == F[f]) acc += -sg * cs_[s].i;
+      }
+      coef[f * m + t] = (float)acc;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    g_omp_prof[0] = tp1 - tp0;
+    g_omp_prof[1] = tp2 - tp1;
+    g_omp_prof[2] = tp3 - tp2;
+    g_omp_prof[3] = clock64() - tp3;
   }
 }
+void omp_prof_read(unsigned long long* out) { cudaMemcpyFromSymbol(out, g_omp_prof, sizeof(unsigned long long) * 4); }
 
 // int8 limbs of M: Q = rint(M / s_c * 126 * 128^(L-1)),
 // balanced base-128 digits, Mq[(l*kpad + c) * mpad + t]; scale = s_c / (126 128^(L-1)).
@@ -750,8 +801,14 @@ cdmd_status fit_impl(cdmd_handle h, const void* Y, int64_t ldy, int kind, int64_
                  W.cf, 1));
   prof.mark("canon+M+gram");
   note_launch();
-  omp_kernel<<<1, 256, 0, st>>>(ke, K, m, W.Gf, W.cf, W.G, model->pair, model->lambda, model->beta,
-                                model->support, model->coef, model->coef_col, W.dinfo, h->omega_eps, dt);
+  {
+    const size_t osm = sizeof(double) * (2 * (size_t)ke * ke + 2 * (size_t)ke) + sizeof(int32_t) * (size_t)ke + 16;
+    const int staged = osm <= 160 * 1024;
+    if (staged) CU(smem_optin(reinterpret_cast<const void*>(omp_kernel)));
+    omp_kernel<<<1, 256, staged ? osm : 0, st>>>(ke, K, m, W.Gf, W.cf, W.G, model->pair, model->lambda,
+                                                 model->beta, model->support, model->coef, model->coef_col,
+                                                 W.dinfo, h->omega_eps, dt, staged);
+  }
   CU(cudaGetLastError());
   prof.mark("omp+coef");
   note_launch();
@@ -764,10 +821,17 @@ cdmd_status fit_impl(cdmd_handle h, const void* Y, int64_t ldy, int kind, int64_
   prof.mark("quant+sync");
   prof.report();
   if (prof.on) {
-    unsigned long long t[8];
+    unsigned long long t[12];
     hqr_prof_read(t);
     fprintf(stderr, "[cdmd_hqr] orthes %llu  ortran %llu  deflation %llu  m-search %llu  bulges %llu  iters %llu  steps %llu (cycles)\n",
             t[0], t[1], t[2], t[3], t[4], t[5], t[6]);
+    unsigned long long o[4];
+    omp_prof_read(o);
+    fprintf(stderr, "[cdmd_omp] staging %llu  selection %llu  outputs %llu  coef table %llu (cycles)\n", o[0], o[1],
+            o[2], o[3]);
+    if (t[8] && t[6])   // built with -DCDMD_HQR_PROF2
+      fprintf(stderr, "[cdmd_hqr] per bulge step: chain %llu  row update %llu  column update %llu (cycles)\n",
+              t[8] / t[6], t[9] / t[6], t[10] / t[6]);
   }
   model->K_eff = h->host_info[INFO_K_SEL];
   model->n_coef = h->host_info[INFO_N_COEF];
