@@ -30,12 +30,6 @@ namespace cdmd {
 
 constexpr int LZ_CL = 16;       // CTAs per cluster
 constexpr int LZ_T = 512;       // threads per CTA
-constexpr int LZ_R = 32;        // rows per CTA (row l on CTA l % 16, slot l / 16)
-constexpr int LZ_NMAX = LZ_CL * LZ_R;
-constexpr int LZ_JMAX = 144;    // Krylov dimension cap (k <= 54 at J = 2.5 k + 9)
-constexpr int LZ_HS = LZ_JMAX + 2;   // partial-sum row: JMAX values, ||z||^2 partial, pad
-
-
 // per-phase cycle totals of CTA 0's thread 0 (built with -DCDMD_LZ_PROF; printed by
 // launch_eh_lz under CDMD_PROFILE_FIT)
 __device__ unsigned long long g_lz_prof[12];
@@ -64,46 +58,65 @@ __device__ __forceinline__ void lz_st_async(uint32_t cluster_addr, double v, uin
 // entries c < count owned by CTA t (c % 16 == t)
 __device__ __forceinline__ int lz_owned(int count, int t) { return count > t ? (count - 1 - t) / LZ_CL + 1 : 0; }
 
-constexpr int LZ_NS = LZ_JMAX / LZ_CL + 1;   // slots per owner: entries c = 16 slot + owner, c <= JMAX
-constexpr int LZ_AS = LZ_NS + 1;             // gathered row: the owner's slots and its sum of squares
+// The two variants: SMALL (n <= 512: 32 rows per CTA, the rows of G in registers, 32
+// doubles per thread, kept in the exchange order of q) and BIG (n <= 1024: 64 rows per
+// CTA, the rows of G streamed from L2 every step -- 8 MB of G stay L2-resident -- against
+// q reassembled in natural order in shared memory).
+template <bool BIG>
+struct LzCfg {
+  static constexpr int R = BIG ? 64 : 32;      // rows per CTA (row l on CTA l % 16, slot l / 16)
+  static constexpr int NMAX = LZ_CL * R;       // 512 / 1024
+  static constexpr int JM = BIG ? 288 : 144;   // Krylov dimension cap (2.5 k + 9 <= JM)
+  static constexpr int NS = JM / LZ_CL + 1;    // slots per owner: entries c = 16 slot + owner, c <= JM
+  static constexpr int AS = NS + 1;            // gathered row: the owner's slots and its sum of squares
+  static constexpr int QLD = BIG ? R + 1 : R;  // row stride of qp (padded: conflict-free reassembly)
+  static constexpr int RH = R / 32;            // rows per half-warp
+};
 
-// dynamic shared memory: Qs[32][JMAX] | rsA[16][NS] | agA[16][AS] | rsB[16][NS] | agB[16][AS] |
-// qp[16][32] | zsh[32] | bars[5].  The CTA's 32 rows of G live in registers (32 doubles per
-// thread).  The two projections h1 = Q^T z, h2 = Q^T z1 are cluster all-reduces done as
-// reduce-scatter + all-gather with st.async (entry c is summed by CTA c % 16, from the
-// 16 partials it receives in rs*, then sent to every CTA's ag*): a few hundred bytes per
-// CTA per hop instead of every partial vector to every CTA.  qp is the current basis
-// vector in the exchange's order, qp[32 r + s] = q_j[r + 16 s] (CTA r's slot s) -- the
-// order the register copy of G is kept in.  Barriers: RS_A, AG_A, RS_B, AG_B, Q, each
+// dynamic shared memory: Qs[R][JM] | rsA[16][NS] | agA[16][AS] | rsB[16][NS] | agB[16][AS] |
+// qp[16][QLD] | qn[NMAX] (BIG) | zsh[R] | bars[5].  The two projections h1 = Q^T z,
+// h2 = Q^T z1 are cluster all-reduces done as reduce-scatter + all-gather with st.async
+// (entry c is summed by CTA c % 16, from the 16 partials it receives in rs*, then sent to
+// every CTA's ag*): a few hundred bytes per CTA per hop instead of every partial vector to
+// every CTA.  qp holds q_j in the exchange's order, qp[QLD r + s] = q_j[r + 16 s] (CTA r's
+// slot s) -- SMALL keeps its register copy of G in that order; BIG reassembles q_j in
+// natural order (qn) for the streamed rows.  Barriers: RS_A, AG_A, RS_B, AG_B, Q, each
 // completing once per step (parity j & 1); B carries ||z1||^2 as entry nc.
-size_t lz_smem_bytes(int) {
-  return sizeof(double) * ((size_t)LZ_R * LZ_JMAX + 2 * (size_t)LZ_CL * (LZ_NS + LZ_AS) + (size_t)LZ_CL * LZ_R + LZ_R) +
+template <bool BIG>
+size_t lz_smem_bytes_t() {
+  using C = LzCfg<BIG>;
+  return sizeof(double) * ((size_t)C::R * C::JM + 2 * (size_t)LZ_CL * (C::NS + C::AS) + (size_t)LZ_CL * C::QLD +
+                           (BIG ? (size_t)C::NMAX : 0) + C::R) +
          64;
 }
 
+template <bool BIG>
 __global__ void __launch_bounds__(LZ_T, 1)
     lz_kernel(int n, const double* __restrict__ G, int64_t ldg, int J, double* __restrict__ alpha,
               double* __restrict__ beta, double* __restrict__ Qout, int* __restrict__ jdone) {
+  using C = LzCfg<BIG>;
+  constexpr int R = C::R, JM = C::JM, NS = C::NS, AS = C::AS, QLD = C::QLD;
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = (int)cluster.block_rank();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   extern __shared__ __align__(16) double lsm[];
-  double* Qs = lsm;                                   // [32][JMAX] local rows of the basis
-  double* rsA = Qs + (size_t)LZ_R * LZ_JMAX;          // [16 senders][NS] partials of my entries
-  double* agA = rsA + LZ_CL * LZ_NS;                  // [16 owners][AS] h1, gathered
-  double* rsB = agA + LZ_CL * LZ_AS;
-  double* agB = rsB + LZ_CL * LZ_NS;                  // h2 and ||z1||^2 (entry nc), sums of squares
-  double* qp = agB + LZ_CL * LZ_AS;                   // [16][32] q_j, exchange order
-  double* zsh = qp + LZ_CL * LZ_R;                    // [32]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(zsh + LZ_R);   // RS_A, AG_A, RS_B, AG_B, Q
+  double* Qs = lsm;                                   // [R][JM] local rows of the basis
+  double* rsA = Qs + (size_t)R * JM;                  // [16 senders][NS] partials of my entries
+  double* agA = rsA + LZ_CL * NS;                     // [16 owners][AS] h1, gathered
+  double* rsB = agA + LZ_CL * AS;
+  double* agB = rsB + LZ_CL * NS;                     // h2 and ||z1||^2 (entry nc), sums of squares
+  double* qp = agB + LZ_CL * AS;                      // [16][QLD] q_j, exchange order
+  double* qn = qp + LZ_CL * QLD;                      // BIG: [NMAX] q_j, natural order
+  double* zsh = qn + (BIG ? C::NMAX : 0);             // [R]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(zsh + R);   // RS_A, AG_A, RS_B, AG_B, Q
   __shared__ double red2[LZ_T / 32];
   const uint32_t s_rsA = tc::smem_u32(rsA), s_agA = tc::smem_u32(agA), s_rsB = tc::smem_u32(rsB);
   const uint32_t s_agB = tc::smem_u32(agB), s_qp = tc::smem_u32(qp), s_bar = tc::smem_u32(bars);
-  const int s_row = warp * 2 + (lane >> 4), g = lane & 15;   // half-warp per local row
-  // row l = rank + 16 s_row of G (symmetric: row l = column l), in qp's order:
+  const int s_row = warp * 2 + (lane >> 4), g = lane & 15;   // half-warp per local row (+ 32 rr)
+  // SMALL: row l = rank + 16 s_row of G (symmetric: row l = column l) in qp's order,
   // greg[2t + e] = G[l][t + 16 (2g + e)]
-  double greg[32];
-  {
+  double greg[BIG ? 1 : 32];
+  if (!BIG) {
     const int l = rank + LZ_CL * s_row;
 #pragma unroll
     for (int t = 0; t < 16; ++t)
@@ -113,29 +126,38 @@ __global__ void __launch_bounds__(LZ_T, 1)
         greg[2 * t + e] = (l < n && i < n) ? __ldg(G + i + (int64_t)l * ldg) : 0.0;
       }
   }
-  for (int idx = tid; idx < LZ_R * LZ_JMAX; idx += LZ_T) Qs[idx] = 0.0;
+  // BIG: double2 loads of the streamed rows when every row starts 16-B aligned
+  const bool al2 = BIG && ((ldg & 1) == 0) && ((reinterpret_cast<uintptr_t>(G) & 15) == 0);
+  for (int idx = tid; idx < R * JM; idx += LZ_T) Qs[idx] = 0.0;
   // q_0: a fixed pseudo-random unit vector (identical on every CTA, no exchange)
   {
-    const int l = (tid >> 5) + LZ_CL * (tid & 31);   // qp position tid
-    double v = 0.0;
-    if (l < n) {
-      const uint4 w = philox(make_uint4((uint32_t)l, 0u, 0u, 0x4C5Au), 0x1234567u, 0x89ABCDEu);
-      v = ((double)w.x + 0.5) * 0x1p-32 - 0.5;
+    double nq = 0.0;
+    for (int P = tid; P < C::NMAX; P += LZ_T) {
+      const int l = BIG ? P : (P >> 5) + LZ_CL * (P & 31);   // SMALL: qp position P
+      double v = 0.0;
+      if (l < n) {
+        const uint4 w = philox(make_uint4((uint32_t)l, 0u, 0u, 0x4C5Au), 0x1234567u, 0x89ABCDEu);
+        v = ((double)w.x + 0.5) * 0x1p-32 - 0.5;
+      }
+      nq = fma(v, v, nq);
+      if (BIG) qn[P] = v; else qp[P] = v;
     }
-    double nq = v * v;
     for (int o = 16; o > 0; o >>= 1) nq += __shfl_xor_sync(0xffffffffu, nq, o);
     if (lane == 0) red2[warp] = nq;
     __syncthreads();
     double nq2 = 0.0;
     for (int w = 0; w < LZ_T / 32; ++w) nq2 += red2[w];
-    qp[tid] = v / sqrt(nq2);
+    const double inq = 1.0 / sqrt(nq2);
+    for (int P = tid; P < C::NMAX; P += LZ_T) {
+      if (BIG) qn[P] *= inq; else qp[P] *= inq;
+    }
   }
   if (tid == 0) {
     for (int q = 0; q < 5; ++q) tc::mbar_init(&bars[q], 1);
     tc::fence_mbar_init();
   }
   __syncthreads();
-  if (tid < LZ_R) Qs[tid * LZ_JMAX + 0] = qp[rank * LZ_R + tid];
+  if (tid < R) Qs[tid * JM + 0] = BIG ? qn[rank + LZ_CL * tid] : qp[rank * QLD + tid];
   cluster.sync();
   int jend = J;
 #ifdef CDMD_LZ_PROF
@@ -147,8 +169,8 @@ __global__ void __launch_bounds__(LZ_T, 1)
   for (int j = 0; j < J; ++j) {
     const uint32_t par = (uint32_t)j & 1u;
     const int nc = j + 1, ncb = nc + 1;   // basis columns 0..j; B's entries (h2, ||z1||^2)
-    // (1) z = G q_j on the local rows (registers x broadcast shared loads)
-    {
+    // (1) z = G q_j on the local rows
+    if (!BIG) {   // registers x broadcast shared loads
       double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
 #pragma unroll
       for (int t = 0; t < 16; t += 2) {
@@ -163,13 +185,53 @@ __global__ void __launch_bounds__(LZ_T, 1)
 #pragma unroll
       for (int o = 8; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
       if (g == 0) zsh[s_row] = a;
+    } else {      // two streamed rows per half-warp (L2-resident G)
+      const int l0 = rank + LZ_CL * s_row, l1 = l0 + LZ_CL * 32;
+      const double* r0 = G + (int64_t)(l0 < n ? l0 : 0) * ldg;
+      const double* r1 = G + (int64_t)(l1 < n ? l1 : 0) * ldg;
+      double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+      if (al2) {
+        const int n2 = n & ~1;
+#pragma unroll 4
+        for (int i = 2 * g; i < n2; i += 32) {
+          const double2 q = *reinterpret_cast<const double2*>(qn + i);
+          const double2 x0 = __ldg(reinterpret_cast<const double2*>(r0 + i));
+          const double2 x1 = __ldg(reinterpret_cast<const double2*>(r1 + i));
+          a0 = fma(x0.x, q.x, a0);
+          a1 = fma(x0.y, q.y, a1);
+          b0 = fma(x1.x, q.x, b0);
+          b1 = fma(x1.y, q.y, b1);
+        }
+        if ((n & 1) && g == 0) {
+          a0 = fma(__ldg(r0 + n - 1), qn[n - 1], a0);
+          b0 = fma(__ldg(r1 + n - 1), qn[n - 1], b0);
+        }
+      } else {
+#pragma unroll 4
+        for (int i = g; i < n; i += 16) {
+          const double q = qn[i];
+          a0 = fma(__ldg(r0 + i), q, a0);
+          b0 = fma(__ldg(r1 + i), q, b0);
+        }
+      }
+      double a = a0 + a1, b = b0 + b1;
+#pragma unroll
+      for (int o = 8; o > 0; o >>= 1) {
+        a += __shfl_xor_sync(0xffffffffu, a, o);
+        b += __shfl_xor_sync(0xffffffffu, b, o);
+      }
+      if (g == 0) {
+        zsh[s_row] = l0 < n ? a : 0.0;
+        zsh[s_row + 32] = l1 < n ? b : 0.0;
+      }
     }
-    if (tid == 0) {   // this step's expected bytes (each barrier's previous phase is complete)
-      tc::mbar_arrive_expect_tx(&bars[0], 8u * LZ_CL * lz_owned(nc, rank));
-      tc::mbar_arrive_expect_tx(&bars[1], 8u * nc);
-      tc::mbar_arrive_expect_tx(&bars[2], 8u * LZ_CL * lz_owned(ncb, rank));
-      tc::mbar_arrive_expect_tx(&bars[3], 8u * (ncb + LZ_CL));
-      tc::mbar_arrive_expect_tx(&bars[4], 8u * LZ_CL * LZ_R);
+    if (tid < 5) {   // this step's expected bytes (each barrier's previous phase is complete)
+      const uint32_t bytes = tid == 0   ? 8u * LZ_CL * lz_owned(nc, rank)
+                             : tid == 1 ? 8u * nc
+                             : tid == 2 ? 8u * LZ_CL * lz_owned(ncb, rank)
+                             : tid == 3 ? 8u * (ncb + LZ_CL)
+                                        : 8u * LZ_CL * R;
+      tc::mbar_arrive_expect_tx(&bars[tid], bytes);
     }
     __syncthreads();
     LZ_TICK(0);
@@ -177,14 +239,14 @@ __global__ void __launch_bounds__(LZ_T, 1)
     if (tid < nc) {
       double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
 #pragma unroll
-      for (int s = 0; s < LZ_R; s += 4) {
-        a0 = fma(Qs[s * LZ_JMAX + tid], zsh[s], a0);
-        a1 = fma(Qs[(s + 1) * LZ_JMAX + tid], zsh[s + 1], a1);
-        a2 = fma(Qs[(s + 2) * LZ_JMAX + tid], zsh[s + 2], a2);
-        a3 = fma(Qs[(s + 3) * LZ_JMAX + tid], zsh[s + 3], a3);
+      for (int s = 0; s < R; s += 4) {
+        a0 = fma(Qs[s * JM + tid], zsh[s], a0);
+        a1 = fma(Qs[(s + 1) * JM + tid], zsh[s + 1], a1);
+        a2 = fma(Qs[(s + 2) * JM + tid], zsh[s + 2], a2);
+        a3 = fma(Qs[(s + 3) * JM + tid], zsh[s + 3], a3);
       }
       const uint32_t o = (uint32_t)(tid & (LZ_CL - 1));
-      lz_st_async(tc::mapa(s_rsA + 8u * (uint32_t)(rank * LZ_NS + tid / LZ_CL), o), (a0 + a1) + (a2 + a3),
+      lz_st_async(tc::mapa(s_rsA + 8u * (uint32_t)(rank * NS + tid / LZ_CL), o), (a0 + a1) + (a2 + a3),
                   tc::mapa(s_bar, o));
     }
     LZ_TICK(1);
@@ -192,17 +254,17 @@ __global__ void __launch_bounds__(LZ_T, 1)
     if (warp == 0) {
       tc::mbar_wait(&bars[0], par);
       const int c = LZ_CL * lane + rank;
-      if (lane < LZ_NS && c < nc) {
+      if (lane < NS && c < nc) {
         double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
 #pragma unroll
         for (int r = 0; r < LZ_CL; r += 4) {
-          a0 += rsA[r * LZ_NS + lane];
-          a1 += rsA[(r + 1) * LZ_NS + lane];
-          a2 += rsA[(r + 2) * LZ_NS + lane];
-          a3 += rsA[(r + 3) * LZ_NS + lane];
+          a0 += rsA[r * NS + lane];
+          a1 += rsA[(r + 1) * NS + lane];
+          a2 += rsA[(r + 2) * NS + lane];
+          a3 += rsA[(r + 3) * NS + lane];
         }
         const double v = (a0 + a1) + (a2 + a3);
-        const uint32_t off = 8u * (uint32_t)(rank * LZ_AS + lane);
+        const uint32_t off = 8u * (uint32_t)(rank * AS + lane);
 #pragma unroll 4
         for (int t = 0; t < LZ_CL; ++t) lz_st_async(tc::mapa(s_agA + off, t), v, tc::mapa(s_bar + 8u, t));
       }
@@ -211,22 +273,28 @@ __global__ void __launch_bounds__(LZ_T, 1)
     LZ_TICK(2);
     // (4) z1 = z - Q h1 on the local rows (h1_c = agA[(c % 16) AS + c / 16]), local ||z1||^2
     {
-      const double* qr = Qs + s_row * LZ_JMAX;
-      const double* hg = agA + g * LZ_AS;
-      double a = 0.0, b = 0.0;
-      int i = 0;
-      for (; LZ_CL * (i + 1) + g < nc; i += 2) {
-        a = fma(qr[LZ_CL * i + g], hg[i], a);
-        b = fma(qr[LZ_CL * (i + 1) + g], hg[i + 1], b);
-      }
-      if (LZ_CL * i + g < nc) a = fma(qr[LZ_CL * i + g], hg[i], a);
-      a += b;
+      const double* hg = agA + g * AS;
+      double sq = 0.0;
 #pragma unroll
-      for (int o = 8; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-      const double z1 = zsh[s_row] - a;
-      double sq = z1 * z1;
-      sq += __shfl_xor_sync(0xffffffffu, sq, 16);   // the warp's two rows
-      if (g == 0) zsh[s_row] = z1;
+      for (int rr = 0; rr < C::RH; ++rr) {
+        const int s = s_row + 32 * rr;
+        const double* qr = Qs + s * JM;
+        double a = 0.0, b = 0.0;
+        int i = 0;
+        for (; LZ_CL * (i + 1) + g < nc; i += 2) {
+          a = fma(qr[LZ_CL * i + g], hg[i], a);
+          b = fma(qr[LZ_CL * (i + 1) + g], hg[i + 1], b);
+        }
+        if (LZ_CL * i + g < nc) a = fma(qr[LZ_CL * i + g], hg[i], a);
+        a += b;
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+        const double z1 = zsh[s] - a;
+        sq = fma(z1, z1, sq);
+        __syncwarp();
+        if (g == 0) zsh[s] = z1;
+      }
+      sq += __shfl_xor_sync(0xffffffffu, sq, 16);   // the warp's rows
       if (lane == 0) red2[warp] = sq;
     }
     __syncthreads();
@@ -237,11 +305,11 @@ __global__ void __launch_bounds__(LZ_T, 1)
       if (tid < nc) {
         double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
 #pragma unroll
-        for (int s = 0; s < LZ_R; s += 4) {
-          a0 = fma(Qs[s * LZ_JMAX + tid], zsh[s], a0);
-          a1 = fma(Qs[(s + 1) * LZ_JMAX + tid], zsh[s + 1], a1);
-          a2 = fma(Qs[(s + 2) * LZ_JMAX + tid], zsh[s + 2], a2);
-          a3 = fma(Qs[(s + 3) * LZ_JMAX + tid], zsh[s + 3], a3);
+        for (int s = 0; s < R; s += 4) {
+          a0 = fma(Qs[s * JM + tid], zsh[s], a0);
+          a1 = fma(Qs[(s + 1) * JM + tid], zsh[s + 1], a1);
+          a2 = fma(Qs[(s + 2) * JM + tid], zsh[s + 2], a2);
+          a3 = fma(Qs[(s + 3) * JM + tid], zsh[s + 3], a3);
         }
         v = (a0 + a1) + (a2 + a3);
       } else {
@@ -254,7 +322,7 @@ __global__ void __launch_bounds__(LZ_T, 1)
         v = a0 + a1;
       }
       const uint32_t o = (uint32_t)(tid & (LZ_CL - 1));
-      lz_st_async(tc::mapa(s_rsB + 8u * (uint32_t)(rank * LZ_NS + tid / LZ_CL), o), v, tc::mapa(s_bar + 16u, o));
+      lz_st_async(tc::mapa(s_rsB + 8u * (uint32_t)(rank * NS + tid / LZ_CL), o), v, tc::mapa(s_bar + 16u, o));
     }
     LZ_TICK(4);
     // (6) owners: sums, and the sum of squares of my h2 entries (not of the norm entry)
@@ -262,58 +330,61 @@ __global__ void __launch_bounds__(LZ_T, 1)
       tc::mbar_wait(&bars[2], par);
       const int c = LZ_CL * lane + rank;
       double v = 0.0;
-      if (lane < LZ_NS && c < ncb) {
+      if (lane < NS && c < ncb) {
         double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
 #pragma unroll
         for (int r = 0; r < LZ_CL; r += 4) {
-          a0 += rsB[r * LZ_NS + lane];
-          a1 += rsB[(r + 1) * LZ_NS + lane];
-          a2 += rsB[(r + 2) * LZ_NS + lane];
-          a3 += rsB[(r + 3) * LZ_NS + lane];
+          a0 += rsB[r * NS + lane];
+          a1 += rsB[(r + 1) * NS + lane];
+          a2 += rsB[(r + 2) * NS + lane];
+          a3 += rsB[(r + 3) * NS + lane];
         }
         v = (a0 + a1) + (a2 + a3);
-        const uint32_t off = 8u * (uint32_t)(rank * LZ_AS + lane);
+        const uint32_t off = 8u * (uint32_t)(rank * AS + lane);
 #pragma unroll 4
         for (int t = 0; t < LZ_CL; ++t) lz_st_async(tc::mapa(s_agB + off, t), v, tc::mapa(s_bar + 24u, t));
       }
-      double sq = c < nc && lane < LZ_NS ? v * v : 0.0;
+      double sq = c < nc && lane < NS ? v * v : 0.0;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
       if (lane < LZ_CL)
-        lz_st_async(tc::mapa(s_agB + 8u * (uint32_t)(rank * LZ_AS + LZ_NS), lane), sq,
-                    tc::mapa(s_bar + 24u, lane));
+        lz_st_async(tc::mapa(s_agB + 8u * (uint32_t)(rank * AS + NS), lane), sq, tc::mapa(s_bar + 24u, lane));
     }
     tc::mbar_wait(&bars[3], par);
     LZ_TICK(5);
     // (7) z2 = z1 - Q h2; alpha_j, beta_j; q_{j+1} = z2 / beta_j.  ||h2||^2 is the 16 owners'
     // sums of squares added by a 16-lane butterfly: bitwise identical in every lane and CTA.
-    double nh2 = agB[(lane & 15) * LZ_AS + LZ_NS];
+    double nh2 = agB[(lane & 15) * AS + NS];
 #pragma unroll
     for (int o = 8; o > 0; o >>= 1) nh2 += __shfl_xor_sync(0xffffffffu, nh2, o);
-    const double nz1 = agB[(nc & (LZ_CL - 1)) * LZ_AS + nc / LZ_CL];
+    const double nz1 = agB[(nc & (LZ_CL - 1)) * AS + nc / LZ_CL];
     const double b2 = nz1 - nh2;
     const double bj = b2 > 0.0 ? sqrt(b2) : 0.0;
-    const double aj = agA[(j & (LZ_CL - 1)) * LZ_AS + j / LZ_CL] + agB[(j & (LZ_CL - 1)) * LZ_AS + j / LZ_CL];
+    const double aj = agA[(j & (LZ_CL - 1)) * AS + j / LZ_CL] + agB[(j & (LZ_CL - 1)) * AS + j / LZ_CL];
     const bool stop = !(bj > 1e-13 * fabs(aj) + 1e-300) || j + 1 == J;   // invariant subspace / last step
     const double ib = stop ? 0.0 : 1.0 / bj;
     {
-      const double* qr = Qs + s_row * LZ_JMAX;
-      const double* hg = agB + g * LZ_AS;
-      double a = 0.0, b = 0.0;
-      int i = 0;
-      for (; LZ_CL * (i + 1) + g < nc; i += 2) {
-        a = fma(qr[LZ_CL * i + g], hg[i], a);
-        b = fma(qr[LZ_CL * (i + 1) + g], hg[i + 1], b);
-      }
-      if (LZ_CL * i + g < nc) a = fma(qr[LZ_CL * i + g], hg[i], a);
-      a += b;
+      const double* hg = agB + g * AS;
 #pragma unroll
-      for (int o = 8; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-      const double qv = (zsh[s_row] - a) * ib;   // the same in all 16 lanes of the half-warp
-      if (!stop) {
-        // lane g sends the row to CTA g
-        lz_st_async(tc::mapa(s_qp + 8u * (uint32_t)(rank * LZ_R + s_row), g), qv, tc::mapa(s_bar + 32u, g));
-        if (g == 0) Qs[s_row * LZ_JMAX + j + 1] = qv;
+      for (int rr = 0; rr < C::RH; ++rr) {
+        const int s = s_row + 32 * rr;
+        const double* qr = Qs + s * JM;
+        double a = 0.0, b = 0.0;
+        int i = 0;
+        for (; LZ_CL * (i + 1) + g < nc; i += 2) {
+          a = fma(qr[LZ_CL * i + g], hg[i], a);
+          b = fma(qr[LZ_CL * (i + 1) + g], hg[i + 1], b);
+        }
+        if (LZ_CL * i + g < nc) a = fma(qr[LZ_CL * i + g], hg[i], a);
+        a += b;
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+        const double qv = (zsh[s] - a) * ib;   // the same in all 16 lanes of the half-warp
+        if (!stop) {
+          // lane g sends the row to CTA g
+          lz_st_async(tc::mapa(s_qp + 8u * (uint32_t)(rank * QLD + s), g), qv, tc::mapa(s_bar + 32u, g));
+          if (g == 0) Qs[s * JM + j + 1] = qv;
+        }
       }
     }
     if (rank == 0 && tid == 0) {
@@ -328,13 +399,17 @@ __global__ void __launch_bounds__(LZ_T, 1)
     }
     LZ_TICK(6);
     tc::mbar_wait(&bars[4], par);
+    if (BIG) {   // q_{j+1} in natural order for the streamed rows
+      for (int i = tid; i < C::NMAX; i += LZ_T) qn[i] = i < n ? qp[(i & (LZ_CL - 1)) * QLD + i / LZ_CL] : 0.0;
+      __syncthreads();
+    }
     LZ_TICK(7);
   }
   // the basis, n x jend column-major
   __syncthreads();
-  for (int idx = tid; idx < LZ_R * jend; idx += LZ_T) {
+  for (int idx = tid; idx < R * jend; idx += LZ_T) {
     const int s = idx / jend, c = idx % jend, l = rank + LZ_CL * s;
-    if (l < n) Qout[l + (int64_t)c * n] = Qs[s * LZ_JMAX + c];
+    if (l < n) Qout[l + (int64_t)c * n] = Qs[s * JM + c];
   }
   if (rank == 0 && tid == 0) {
     *jdone = jend;
@@ -364,13 +439,14 @@ __global__ void lz_check_kernel(int J, int k, const double* __restrict__ beta, c
   *flag = bad;
 }
 
-// 1 when this device co-schedules the 16-CTA cluster at the full shared-memory size
+// 1 when this device co-schedules the variant's 16-CTA cluster at its shared-memory size
+template <bool BIG>
 static int lz_cluster_ok() {
   static int ok = -1;
   if (ok >= 0) return ok;
-  const size_t smem = lz_smem_bytes(LZ_NMAX);
-  cudaError_t e = cudaFuncSetAttribute(lz_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-  if (e == cudaSuccess) e = smem_optin(reinterpret_cast<const void*>(lz_kernel));
+  const size_t smem = lz_smem_bytes_t<BIG>();
+  cudaError_t e = cudaFuncSetAttribute(lz_kernel<BIG>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  if (e == cudaSuccess) e = smem_optin(reinterpret_cast<const void*>(lz_kernel<BIG>));
   int nc = 0;
   if (e == cudaSuccess) {
     cudaLaunchConfig_t cfg = {};
@@ -384,31 +460,37 @@ static int lz_cluster_ok() {
     at.val.clusterDim.z = 1;
     cfg.attrs = &at;
     cfg.numAttrs = 1;
-    e = cudaOccupancyMaxActiveClusters(&nc, lz_kernel, &cfg);
+    e = cudaOccupancyMaxActiveClusters(&nc, lz_kernel<BIG>, &cfg);
   }
   if (e != cudaSuccess) (void)cudaGetLastError();
   ok = (e == cudaSuccess && nc > 0) ? 1 : 0;
   return ok;
 }
 
-bool lz_supported(int n, int k) {
-  if (n < 8 || n > LZ_NMAX || k < 1 || k + 1 > n || 5 * k / 2 + 9 > LZ_JMAX) return false;
-  if (lz_smem_bytes(n) > 227 * 1024) return false;
-  return lz_cluster_ok() == 1;
-}
+static bool lz_big(int n) { return n > LzCfg<false>::NMAX; }
 
 int lz_steps(int n, int k) {
   const int J = 5 * k / 2 + 9;
   return J < n ? J : n;
 }
 
-cudaError_t launch_lz(int n, int J, const double* G, int64_t ldg, double* alpha, double* beta, double* Q, int* jdone,
-                      cudaStream_t st) {
-  if (lz_cluster_ok() != 1) return cudaErrorNotSupported;   // also sets the function attributes
+bool lz_supported(int n, int k) {
+  if (n < 8 || n > LzCfg<true>::NMAX || k < 1 || k + 1 > n) return false;
+  if (lz_big(n)) return lz_steps(n, k) <= LzCfg<true>::JM && lz_cluster_ok<true>() == 1;
+  return lz_steps(n, k) <= LzCfg<false>::JM && lz_cluster_ok<false>() == 1;
+}
+
+// Krylov dimension cap of the variant that serves n (workspace sizing)
+int lz_jmax(int n) { return lz_big(n) ? LzCfg<true>::JM : LzCfg<false>::JM; }
+
+template <bool BIG>
+static cudaError_t launch_lz_t(int n, int J, const double* G, int64_t ldg, double* alpha, double* beta, double* Q,
+                               int* jdone, cudaStream_t st) {
+  if (lz_cluster_ok<BIG>() != 1) return cudaErrorNotSupported;   // also sets the function attributes
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(LZ_CL, 1, 1);
   cfg.blockDim = dim3(LZ_T, 1, 1);
-  cfg.dynamicSmemBytes = lz_smem_bytes(n);
+  cfg.dynamicSmemBytes = lz_smem_bytes_t<BIG>();
   cfg.stream = st;
   cudaLaunchAttribute at;
   at.id = cudaLaunchAttributeClusterDimension;
@@ -418,12 +500,18 @@ cudaError_t launch_lz(int n, int J, const double* G, int64_t ldg, double* alpha,
   cfg.attrs = &at;
   cfg.numAttrs = 1;
   note_launch();
-  const cudaError_t e = cudaLaunchKernelEx(&cfg, lz_kernel, n, G, ldg, J, alpha, beta, Q, jdone);
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, lz_kernel<BIG>, n, G, ldg, J, alpha, beta, Q, jdone);
   if (e == cudaErrorInvalidClusterSize) {   // e.g. a green context with fewer SMs than one cluster
     (void)cudaGetLastError();
     return cudaErrorNotSupported;
   }
   return e;
+}
+
+cudaError_t launch_lz(int n, int J, const double* G, int64_t ldg, double* alpha, double* beta, double* Q, int* jdone,
+                      cudaStream_t st) {
+  return lz_big(n) ? launch_lz_t<true>(n, J, G, ldg, alpha, beta, Q, jdone, st)
+                   : launch_lz_t<false>(n, J, G, ldg, alpha, beta, Q, jdone, st);
 }
 
 cudaError_t launch_lz_check(int J, int k, const double* beta, const double* lam1, const double* S, const int* jdone,

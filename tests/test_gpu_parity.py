@@ -759,9 +759,10 @@ def test_mask_median3_on_the_bench_mask(C, H):
 
 def test_c5_4k_full_size_sampled(C, H):
     """BASELINE's 4K configuration (3840x2160, 1000 frames, sparse p = 4000, k = 100) on
-    one GPU: exact integer sketch, fit parity (m - 1 = 999: the cuSOLVER syevdx path;
-    k = 100: the device eig), modes and mask on sampled pixels incl. the ragged tail
-    (k = 100 and m = 1000 take the CUDA-core modes / dynamic-foreground kernels)."""
+    one GPU: exact integer sketch, fit parity (m - 1 = 999: the streamed-G Lanczos variant,
+    no fallback; k = 100: the device eig), sigma to 1e-6, modes and mask on sampled pixels
+    incl. the ragged tail (k = 100 and m = 1000 take the CUDA-core modes /
+    dynamic-foreground kernels)."""
     cfg = config_by_name("c5_4k_sparse")
     X = video_for(cfg)
     m, n = X.shape
@@ -770,12 +771,16 @@ def test_c5_4k_full_size_sampled(C, H):
     Yg = P.sketch(Xd).cpu().numpy().T.astype(np.int64)
     Yo = OS.sketch(X, OS.SPARSE, cfg.p, 0)
     assert np.array_equal(Yg, Yo)
+    runs0, fb0 = C.cdmd_eigensolver_stats(H)
     P.fit()
+    runs1, fb1 = C.cdmd_eigensolver_stats(H)
+    assert (runs1 - runs0, fb1 - fb0) == (1, 0), (runs1 - runs0, fb1 - fb0)
     gm = C.model_to_host(P.model)
     om = OD.fit(Yo, cfg.k, cfg.K)
     assert gm["k_eff"] == om["k_eff"]
     perm, err = PT.match_eigs(gm["lam"], om["lam"])
     assert err <= PT.RTOL_EIG
+    assert np.max(np.abs(gm["sigma"] - om["sigma"]) / om["sigma"]) <= 1e-6
     assert PT.supports_equal_mod_conj(gm["support"], gm["pair"], perm, om["support"], om["pair"])
     Phi = P.modes(Xd)
     mask = P.foreground(Xd, cfg.tau, C.BG_DYNAMIC).cpu().numpy().view(np.uint32)
