@@ -1209,11 +1209,17 @@ __global__ void __launch_bounds__(32 * HQ_WARPS, 1) hqrv_kernel(int nn, const do
 // adjacent rows (Hessenberg), a first solve U x = eps3 (EISPACK invit), one more
 // inverse-iteration step, then v = Q x.  VR column j = Re v (and j+1 = Im v for a
 // pair); canonicalize_kernel normalises and phases it.
-__global__ void __launch_bounds__(32) hinvit_kernel(int nn, const double* __restrict__ W,
-                                                   const double* __restrict__ H0, const double* __restrict__ Q,
-                                                   double* __restrict__ VR) {
-  extern __shared__ double sm[];
-  const int j = blockIdx.x, lane = threadIdx.x;
+constexpr int HI_WARPS = 4;   // eigenvalues per CTA of hinvit_kernel (a warp each, own shared slice)
+
+__global__ void __launch_bounds__(32 * HI_WARPS) hinvit_kernel(int nn, const double* __restrict__ W,
+                                                              const double* __restrict__ H0,
+                                                              const double* __restrict__ Q,
+                                                              double* __restrict__ VR, size_t warp_doubles) {
+  extern __shared__ double smv[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int j = blockIdx.x * (int)(blockDim.x >> 5) + wid;
+  if (j >= nn) return;
+  double* sm = smv + (size_t)wid * warp_doubles;
   const double wr = W[2 * j], wi = W[2 * j + 1];
   if (wi < 0.0) return;   // second member of a pair
   const bool cx = wi != 0.0;
@@ -1357,11 +1363,18 @@ cudaError_t launch_hqr_eig(int k, const double* A, double* W, double* VR, int* i
     note_launch();
     hqrv_kernel<<<1, 32 * HQ_WARPS, smem, st>>>(k, A, W, H0, Q, info);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    const size_t smem2 = hinvit_smem(k);
+    // a warp per eigenvalue, HI_WARPS to a CTA when their shared slices fit (fewer SMs held
+    // while the streaming lanes' passes run)
+    const size_t wd = (hinvit_smem(k) + 15) / 8;
+    const int per = sizeof(double) * wd * HI_WARPS <= 200 * 1024 ? HI_WARPS : 1;
     e = smem_optin(reinterpret_cast<const void*>(hinvit_kernel));
     if (e != cudaSuccess) return e;
     note_launch();
-    hinvit_kernel<<<(unsigned)k, 32, smem2, st>>>(k, W, H0, Q, VR);
+    if (per == HI_WARPS)
+      hinvit_kernel<<<(unsigned)ceil_div(k, HI_WARPS), 32 * HI_WARPS, sizeof(double) * wd * HI_WARPS, st>>>(k, W, H0, Q,
+                                                                                                        VR, wd);
+    else
+      hinvit_kernel<<<(unsigned)k, 32, sizeof(double) * wd, st>>>(k, W, H0, Q, VR, wd);
     return cudaGetLastError();
   }
   const int par3 = hqr_smem_par3(k) <= 226 * 1024;

@@ -380,20 +380,24 @@ __device__ __forceinline__ void eh_sturm_multi(int n, const double* __restrict__
 // Blocks k and k + 1 (when med_cnt > 0) compute the eigenvalues of descending rank
 // (med_cnt - 1) / 2 and med_cnt / 2 into med[0], med[1]: the median of the med_cnt
 // largest eigenvalues (Gavish-Donoho rank, Remark 2).
-constexpr int EH_BW = 8;   // warps per eigenvalue: 32 EH_BW EH_NP points per multisection round
+constexpr int EH_BW = 8;   // warps per CTA; BW of them per eigenvalue (8 / BW eigenvalues per CTA)
+template <int BW>
 __global__ void __launch_bounds__(32 * EH_BW) eh_bisect_kernel(int n, int k, const double* d, const double* e2,
                                                                const double* __restrict__ bounds,
                                                                double* __restrict__ lam, int med_cnt,
                                                                double* __restrict__ med) {
-  const int r0 = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (r0 >= k + (med_cnt > 0 ? 2 : 0)) return;
+  constexpr int NG = EH_BW / BW;   // eigenvalues per CTA
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gi = warp / BW, gt = tid - gi * 32 * BW;   // group, thread within the group
+  const int r0 = blockIdx.x * NG + gi;
   extern __shared__ double bsm[];     // d[n], e2[n]
-  __shared__ int wsum[2][EH_BW];
+  __shared__ int wsum[NG][2][BW];
   for (int i = tid; i < n; i += 32 * EH_BW) {
     bsm[i] = d[i];
     bsm[n + i] = e2[i];
   }
   __syncthreads();
+  if (r0 >= k + (med_cnt > 0 ? 2 : 0)) return;   // a whole group (named barriers below)
   d = bsm;
   e2 = bsm + n;
   const int r = r0 < k ? r0 : (r0 == k ? (med_cnt - 1) / 2 : med_cnt / 2);
@@ -401,13 +405,13 @@ __global__ void __launch_bounds__(32 * EH_BW) eh_bisect_kernel(int n, int k, con
   double lo = bounds[0], hi = bounds[1];
   const double pivmin = bounds[3];
   const double eps = 2.220446049250313e-16;
-  constexpr int NPT = 32 * EH_BW * EH_NP;   // points per round, at lo + (hi - lo) t / (NPT + 1)
-  for (int round = 0; round < 40; ++round) {
-    if (hi - lo <= 2.0 * eps * fmax(fabs(lo), fabs(hi)) + pivmin) break;   // uniform across the CTA
+  constexpr int NPT = 32 * BW * EH_NP;   // points per round, at lo + (hi - lo) t / (NPT + 1)
+  for (int round = 0; round < 60; ++round) {
+    if (hi - lo <= 2.0 * eps * fmax(fabs(lo), fabs(hi)) + pivmin) break;   // uniform across the group
     double x[EH_NP];
     int c[EH_NP];
 #pragma unroll
-    for (int u = 0; u < EH_NP; ++u) x[u] = lo + (hi - lo) * (double)(EH_NP * tid + u + 1) / (double)(NPT + 1);
+    for (int u = 0; u < EH_NP; ++u) x[u] = lo + (hi - lo) * (double)(EH_NP * gt + u + 1) / (double)(NPT + 1);
     eh_sturm_multi(n, d, e2, x, pivmin, c);
     // points with count <= idx lie below the eigenvalue; counts are monotone in the
     // point index, so the number below is the total over threads and chains
@@ -416,17 +420,18 @@ __global__ void __launch_bounds__(32 * EH_BW) eh_bisect_kernel(int n, int k, con
     for (int u = 0; u < EH_NP; ++u) nbl += c[u] <= idx ? 1 : 0;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) nbl += __shfl_xor_sync(0xffffffffu, nbl, o);
-    if (lane == 0) wsum[round & 1][warp] = nbl;
-    __syncthreads();
+    if (lane == 0) wsum[gi][round & 1][warp - gi * BW] = nbl;
+    if (BW > 1) asm volatile("bar.sync %0, %1;" ::"r"(1 + gi), "r"(32 * BW) : "memory");
+    else __syncwarp();
     nbl = 0;
 #pragma unroll
-    for (int w = 0; w < EH_BW; ++w) nbl += wsum[round & 1][w];
+    for (int w = 0; w < BW; ++w) nbl += wsum[gi][round & 1][w];
     const double nlo = nbl > 0 ? lo + (hi - lo) * (double)nbl / (double)(NPT + 1) : lo;
     const double nhi = nbl < NPT ? lo + (hi - lo) * (double)(nbl + 1) / (double)(NPT + 1) : hi;
     lo = nlo;
     hi = nhi;
   }
-  if (tid == 0) {
+  if (gt == 0) {
     if (r0 < k) lam[k - 1 - r] = 0.5 * (lo + hi);
     else med[r0 - k] = 0.5 * (lo + hi);
   }
@@ -435,7 +440,7 @@ __global__ void __launch_bounds__(32 * EH_BW) eh_bisect_kernel(int n, int k, con
 // Inverse iteration on T - lambda I (LU with partial pivoting), one warp per group
 // of eigenvalues closer than 1e-7 ||T|| (re-orthogonalised with modified Gram-Schmidt,
 // as LAPACK dstein does for clusters).  lam ascending (k largest); Z[:, q] <-> lam[q].
-__global__ void __launch_bounds__(32) eh_invit_kernel(int n, int k, const double* __restrict__ d,
+__global__ void __launch_bounds__(128) eh_invit_kernel(int n, int k, const double* __restrict__ d,
                                                       const double* __restrict__ e,
                                                       const double* __restrict__ bounds,
                                                       const double* __restrict__ lam, double* __restrict__ Z,
@@ -443,7 +448,9 @@ __global__ void __launch_bounds__(32) eh_invit_kernel(int n, int k, const double
   // one warp (CTA) per group of (numerically) equal eigenvalues; the LU factors and
   // the iterate live in shared memory.  Lane 0 runs the two sequential recurrences
   // (multiplying by stored reciprocal pivots); the lanes share the vector operations.
-  extern __shared__ double ism[];
+  extern __shared__ double ismv[];
+  const int wid = threadIdx.x >> 5;
+  double* ism = ismv + (size_t)wid * (7 * (size_t)n + (n + 7) / 8 + 2);   // this warp's slice
   double* ui = ism;               // 1 / pivot
   double* u1 = ui + n;
   double* u2 = u1 + n;
@@ -452,7 +459,8 @@ __global__ void __launch_bounds__(32) eh_invit_kernel(int n, int k, const double
   double* ds = z + n;             // d, e staged: lane 0's LU reads them on a serial chain
   double* es = ds + n;
   uint8_t* pv = reinterpret_cast<uint8_t*>(es + n);   // rows i, i+1 swapped
-  const int lane = threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int grp = blockIdx.x * (int)(blockDim.x >> 5) + wid;   // this warp's group of eigenvalues
   for (int i = lane; i < n; i += 32) {
     ds[i] = d[i];
     es[i] = e[i];
@@ -466,13 +474,13 @@ __global__ void __launch_bounds__(32) eh_invit_kernel(int n, int k, const double
   int g = -1, r0 = 0, r1 = 0;
   for (int r = 0; r < k; ++r) {
     if (r == 0 || fabs(lam[k - r] - lam[k - 1 - r]) > 1e-7 * tnorm) {
-      if (g == (int)blockIdx.x) break;
+      if (g == grp) break;
       ++g;
       r0 = r;
     }
     r1 = r + 1;
   }
-  if (g != (int)blockIdx.x) return;
+  if (g != grp) return;
   auto warp_sum = [&](double v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -569,7 +577,7 @@ __global__ void __launch_bounds__(32) eh_invit_kernel(int n, int k, const double
     for (int i = lane; i < n; i += 32) Z[i + (int64_t)q * n] = sg * z[i];
     __syncwarp();
   }
-  if (blockIdx.x == 0 && lane == 0) *info = 0;
+  if (grp == 0 && lane == 0) *info = 0;
 }
 
 // Z <- Q Z, Q = H_0 H_1 ... H_{n-3} (applied last to first): one warp per column of
@@ -629,6 +637,10 @@ __global__ void __launch_bounds__(128) eh_backtransform_kernel(int n, int k, con
   }
 }
 
+// eh_invit_kernel: EH_IW warps per CTA, a group of eigenvalues each, with their own slice
+constexpr int EH_IW = 4;
+static size_t eh_invit_smem(int n) { return sizeof(double) * EH_IW * (7 * (size_t)n + (n + 7) / 8 + 2); }
+
 size_t eh_tridiag_smem(int n) {
   const int64_t stride = (n + EH_CL - 1) / EH_CL + 1;
   return sizeof(double) * ((size_t)eh_asz_max(n) + 6 * (size_t)n + 2 * EH_CL * stride + 4 * EH_CL + stride + 40 +
@@ -673,14 +685,14 @@ cudaError_t launch_eh(int n, int k, const double* G, int64_t ldg, double* lam, d
   note_launch();
   eh_prep_kernel<<<1, 256, 0, st>>>(n, d, e, e2, bounds);
   note_launch();
-  eh_bisect_kernel<<<k + (med_cnt > 0 ? 2 : 0), 32 * EH_BW, sizeof(double) * 2 * (size_t)n, st>>>(
+  eh_bisect_kernel<EH_BW><<<k + (med_cnt > 0 ? 2 : 0), 32 * EH_BW, sizeof(double) * 2 * (size_t)n, st>>>(
       n, k, d, e2, bounds, lam, med_cnt, med);
   mark(2);
   note_launch();
-  const size_t smem2 = sizeof(double) * 7 * (size_t)n + (size_t)n + 16;
   err = smem_optin(reinterpret_cast<const void*>(eh_invit_kernel));
   if (err != cudaSuccess) return err;
-  eh_invit_kernel<<<(unsigned)k, 32, smem2, st>>>(n, k, d, e, bounds, lam, Zout, info);
+  eh_invit_kernel<<<(unsigned)ceil_div(k, EH_IW), 32 * EH_IW, eh_invit_smem(n), st>>>(n, k, d, e, bounds, lam, Zout,
+                                                                                      info);
   mark(3);
   note_launch();
   eh_backtransform_kernel<<<(unsigned)ceil_div(k, 4), 128, 0, st>>>(n, k, V, tau, Zout);
@@ -734,12 +746,15 @@ cudaError_t launch_eh_lz(int n, int k, const double* G, int64_t ldg, double* lam
   eh_prep_kernel<<<1, 256, 0, st>>>(J, al, be, e2, bounds);
   mark(4);
   note_launch();
-  eh_bisect_kernel<<<k + 1, 32 * EH_BW, sizeof(double) * 2 * (size_t)J, st>>>(J, k + 1, al, e2, bounds, lam1, 0,
-                                                                               nullptr);
+  // the Krylov tridiagonal is short: two warps per eigenvalue, four eigenvalues per CTA
+  // (a quarter of the SMs held while the streaming lanes' passes run)
+  eh_bisect_kernel<2><<<(unsigned)ceil_div(k + 1, EH_BW / 2), 32 * EH_BW, sizeof(double) * 2 * (size_t)J, st>>>(
+      J, k + 1, al, e2, bounds, lam1, 0, nullptr);
   mark(5);
-  const size_t smem2 = sizeof(double) * 7 * (size_t)J + (size_t)J + 16;
+  if ((err = smem_optin(reinterpret_cast<const void*>(eh_invit_kernel))) != cudaSuccess) return err;
   note_launch();
-  eh_invit_kernel<<<(unsigned)(k + 1), 32, smem2, st>>>(J, k + 1, al, be, bounds, lam1, S, info);
+  eh_invit_kernel<<<(unsigned)ceil_div(k + 1, EH_IW), 32 * EH_IW, eh_invit_smem(J), st>>>(J, k + 1, al, be, bounds,
+                                                                                          lam1, S, info);
   if ((err = cudaGetLastError()) != cudaSuccess) return err;
   mark(2);
   if ((err = launch_lz_check(J, k, be, lam1, S, jdone, flag, st)) != cudaSuccess) return err;

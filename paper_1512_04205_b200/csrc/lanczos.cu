@@ -18,6 +18,7 @@
 // Lanczos residual |beta_{J-1}| |s_{J-1,i}| = ||G v_i - theta_i v_i|| decides whether the
 // Ritz pairs are converged (relative to the gap to theta_k); if not, cdmd_fit falls back
 // to the Householder solver.
+#include <atomic>
 #include <cooperative_groups.h>
 #include <math.h>
 
@@ -442,8 +443,12 @@ __global__ void lz_check_kernel(int J, int k, const double* __restrict__ beta, c
 // 1 when this device co-schedules the variant's 16-CTA cluster at its shared-memory size
 template <bool BIG>
 static int lz_cluster_ok() {
-  static int ok = -1;
-  if (ok >= 0) return ok;
+  static std::atomic<int> okd[64];   // per device: 0 unknown, 1 yes, 2 no
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 0;
+  const int known = okd[dev].load();
+  if (known) return known == 1 ? 1 : 0;
+  int ok;
   const size_t smem = lz_smem_bytes_t<BIG>();
   cudaError_t e = cudaFuncSetAttribute(lz_kernel<BIG>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   if (e == cudaSuccess) e = smem_optin(reinterpret_cast<const void*>(lz_kernel<BIG>));
@@ -464,6 +469,7 @@ static int lz_cluster_ok() {
   }
   if (e != cudaSuccess) (void)cudaGetLastError();
   ok = (e == cudaSuccess && nc > 0) ? 1 : 0;
+  okd[dev].store(ok ? 1 : 2);
   return ok;
 }
 

@@ -143,9 +143,28 @@ def probe_sparse(H):
         say(f"  {name}: {np.median(ts):.4f} ms")
 
 
+def probe_gauss(H):
+    cfg = config_by_name("c4_1080p_gaussian")
+    X = video_for(cfg)
+    m, n = X.shape
+    Xd = dev(X)
+    P = C.Pipeline(H, n, n, m, "gaussian", cfg.p, cfg.k, cfg.K)
+    P.sketch(Xd)
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        P.sketch(Xd)
+        e1.record()
+        e1.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    say(f"gaussian sketch {np.median(ts):.4f} ms")
+
+
 if __name__ == "__main__":
     H = C.Handle(0)
     what = sys.argv[1:] or ["fused", "fit", "sparse"]
     for w in what:
-        {"fused": probe_fused, "fit": probe_fit, "sparse": probe_sparse}[w](H)
+        {"fused": probe_fused, "fit": probe_fit, "sparse": probe_sparse, "gauss": probe_gauss}[w](H)
     say("probe done")
