@@ -746,9 +746,9 @@ cudaError_t launch_eh_lz(int n, int k, const double* G, int64_t ldg, double* lam
   eh_prep_kernel<<<1, 256, 0, st>>>(J, al, be, e2, bounds);
   mark(4);
   note_launch();
-  // the Krylov tridiagonal is short: two warps per eigenvalue, four eigenvalues per CTA
-  // (a quarter of the SMs held while the streaming lanes' passes run)
-  eh_bisect_kernel<2><<<(unsigned)ceil_div(k + 1, EH_BW / 2), 32 * EH_BW, sizeof(double) * 2 * (size_t)J, st>>>(
+  // eight warps per eigenvalue (lowest latency; packing four eigenvalues to a CTA with
+  // eh_bisect_kernel<2> holds a quarter of the SMs but measured +30 us and no streaming gain)
+  eh_bisect_kernel<EH_BW><<<(unsigned)(k + 1), 32 * EH_BW, sizeof(double) * 2 * (size_t)J, st>>>(
       J, k + 1, al, e2, bounds, lam1, 0, nullptr);
   mark(5);
   if ((err = smem_optin(reinterpret_cast<const void*>(eh_invit_kernel))) != cudaSuccess) return err;
