@@ -1296,3 +1296,33 @@ def test_lanczos_falls_back_on_an_invariant_subspace(C, H):
     runs1, fb1 = C.cdmd_eigensolver_stats(H)
     assert (runs1 - runs0, fb1 - fb0) == (1, 1)
     assert P.model.k_eff == 1
+
+
+@pytest.mark.parametrize("p,m,k,decay,seed", [(200, 60, 10, 0.8, 0), (600, 200, 40, 0.93, 1), (1500, 513, 30, 0.9, 2),
+                                              (1500, 514, 30, 0.9, 3), (2000, 800, 54, 0.95, 4),
+                                              (900, 300, 40, 1.0, 5)])
+def test_fit_eigensolver_sizes_match_oracle(C, H, p, m, k, decay, seed):
+    """cdmd_fit on planted sketches across the eigensolvers' size limits (Lanczos SMALL up
+    to m - 1 = 512, BIG beyond; a flat spectrum (decay 1) whose Ritz pairs may fail the
+    residual test and fall back): sigma, lambda and k_eff equal the oracle's whichever
+    path ran, and Lanczos was attempted where the sizes allow it."""
+    rng = np.random.default_rng(100 + seed)
+    r = min(p, m)
+    U, _ = np.linalg.qr(rng.standard_normal((p, r)))
+    V, _ = np.linalg.qr(rng.standard_normal((m, r)))
+    s = 1e4 * decay ** np.arange(r) * (1.0 + 0.1 * rng.random(r))
+    Yf = ((U * s) @ V.T + rng.standard_normal((p, m))).astype(np.float32)
+    P = C.Pipeline(H, 1024, 1024, m, "gaussian", p, k, min(5, k))
+    P.Y.copy_(torch.from_numpy(np.ascontiguousarray(Yf.T)).cuda())
+    runs0, fb0 = C.cdmd_eigensolver_stats(H)
+    P.fit()
+    torch.cuda.synchronize()
+    runs1, fb1 = C.cdmd_eigensolver_stats(H)
+    assert runs1 - runs0 == 1, "Lanczos not attempted"
+    gm = C.model_to_host(P.model)
+    om = OD.fit(Yf.astype(np.float64), k, min(5, k))
+    assert gm["k_eff"] == om["k_eff"]
+    assert np.max(np.abs(gm["sigma"] - om["sigma"]) / om["sigma"]) <= 1e-6
+    perm, err = PT.match_eigs(gm["lam"], om["lam"])
+    assert err <= PT.RTOL_EIG, err
+    print(f"p={p} m={m} k={k} decay={decay}: fallback {fb1 - fb0}")
