@@ -1,3 +1,5 @@
+# GPU-box script (run via gpurun from the repo root): GPU suite, bench and reference arm,
+# the launch list and ncu --set full captures of the full-resolution passes (r2f_*).
 cd $GRAFT_REPO_ROOT
 timeout 1500 python -m pytest tests -m gpu -q -rf --durations=20 > gpurun_out/r2f_pytest.log 2>&1
 timeout 900 python bench.py --steps 20 --warmup 5 > gpurun_out/r2f_bench.json 2> gpurun_out/r2f_bench.err
