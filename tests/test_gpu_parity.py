@@ -1326,3 +1326,32 @@ def test_fit_eigensolver_sizes_match_oracle(C, H, p, m, k, decay, seed):
     perm, err = PT.match_eigs(gm["lam"], om["lam"])
     assert err <= PT.RTOL_EIG, err
     print(f"p={p} m={m} k={k} decay={decay}: fallback {fb1 - fb0}")
+
+
+@pytest.mark.parametrize("p,m,k", [(60, 9, 2), (300, 40, 38), (1200, 513, 54), (1200, 513, 55), (3000, 1025, 60)])
+def test_fit_eigensolver_edges(C, H, p, m, k):
+    """Edge sizes of the eigensolver dispatch: the smallest Lanczos system (m - 1 = 8), a
+    Krylov space as large as the matrix (J = m - 1), the k cap of the SMALL variant
+    (2.5 k + 9 <= 144: k = 54 Lanczos, k = 55 Householder), and m - 1 = 1024 (BIG's
+    limit).  sigma, lambda, k_eff equal the oracle's whichever solver ran."""
+    rng = np.random.default_rng(7 + m + k)
+    r = min(p, m)
+    U, _ = np.linalg.qr(rng.standard_normal((p, r)))
+    V, _ = np.linalg.qr(rng.standard_normal((m, r)))
+    s = 1e4 * 0.9 ** np.arange(r) * (1.0 + 0.1 * rng.random(r))
+    Yf = ((U * s) @ V.T + 0.1 * rng.standard_normal((p, m))).astype(np.float32)
+    P = C.Pipeline(H, 1024, 1024, m, "gaussian", p, k, min(3, k))
+    P.Y.copy_(torch.from_numpy(np.ascontiguousarray(Yf.T)).cuda())
+    runs0, _ = C.cdmd_eigensolver_stats(H)
+    P.fit()
+    torch.cuda.synchronize()
+    runs1, _ = C.cdmd_eigensolver_stats(H)
+    expect_lz = (m - 1 >= 8) and (m - 1 <= 1024) and (k + 1 <= m - 1) and \
+        (min(5 * k // 2 + 9, m - 1) <= (144 if m - 1 <= 512 else 288))
+    assert (runs1 - runs0 == 1) == expect_lz, (runs1 - runs0, expect_lz)
+    gm = C.model_to_host(P.model)
+    om = OD.fit(Yf.astype(np.float64), k, min(3, k))
+    assert gm["k_eff"] == om["k_eff"]
+    assert np.max(np.abs(gm["sigma"] - om["sigma"]) / om["sigma"]) <= 1e-6
+    perm, err = PT.match_eigs(gm["lam"], om["lam"])
+    assert err <= PT.RTOL_EIG, err
