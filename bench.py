@@ -14,8 +14,10 @@ value  : frames / device time per step (max over ranks), inputs resident in HBM;
          video.  lanes <= K/2, so every lane runs >= 2 batches (steady state).
 Also reported:
   latency_ms_per_batch  one batch at a time, eager, with per-stage CUDA events;
-  per_batch             one batch at a time with the passes replayed from CUDA graphs
-                        (sketch | fit | modes+foreground), median of >= 10 runs;
+  per_batch             one batch at a time, the whole step (sketch + fit + modes +
+                        foreground) replayed from ONE CUDA graph (cdmd_fit reads nothing back
+                        under capture; the replays' self-check flag is verified), median of
+                        >= 10 runs; eager_fit_ms_median: the same with the fit eager;
   passes_only           sketch + modes + foreground in one CUDA graph (the replicated
                         small solve excluded), median of >= 10 runs, with its HBM fraction;
   e2e_fused             the same with the fused single pass (N11: cdmd_foreground(Phi=NULL)).
@@ -375,6 +377,12 @@ def main():
         graphs["passes_all"] = capture(lambda: (P.sketch(Xd), P.modes(Xd), P.foreground(Xd, cfg.tau, mode)))
     except Exception as e:   # report, do not hide: the eager numbers above still stand
         graphs = {"error": repr(e)}
+    step_graph_err = None
+    if "error" not in graphs and allreduce is None:
+        try:   # the whole step in one graph: cdmd_fit has no host read-back under capture
+            graphs["step"] = capture(lambda: (P.sketch(Xd), P.fit(), P.modes(Xd), P.foreground(Xd, cfg.tau, mode)))
+        except Exception as e:
+            step_graph_err = repr(e)
     fused_ok = True
     try:
         P.foreground(Xd, cfg.tau, mode, fused=True)
@@ -404,6 +412,20 @@ def main():
             per_batch = {"ms_median": round(med, 4), "frames_per_s": round(m / (med * 1e-3), 1), "runs": reps,
                          "mode": "sketch graph | fit (eager: it reads the model sizes back once) | "
                                  "modes+foreground graph"}
+            if "step" in graphs:
+                for _ in range(3):
+                    graphs["step"].replay()
+                gmed, _ = median_ms(torch, graphs["step"].replay, reps, s_cap)
+                torch.cuda.synchronize()
+                if not P.graph_stale():   # the replays' self-check (sizes as captured, no fallback)
+                    gmed = max_over_ranks(gmed)
+                    per_batch = {"ms_median": round(gmed, 4), "frames_per_s": round(m / (gmed * 1e-3), 1),
+                                 "runs": reps, "mode": "one CUDA graph: sketch + fit + modes + foreground",
+                                 "eager_fit_ms_median": per_batch["ms_median"]}
+                else:
+                    per_batch["step_graph"] = "stale: a replay disagreed with the captured sizes"
+            elif step_graph_err:
+                per_batch["step_graph"] = step_graph_err
             for _ in range(3):
                 graphs["passes_all"].replay()
             med, _ = median_ms(torch, graphs["passes_all"].replay, reps, s_cap)

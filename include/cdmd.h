@@ -209,7 +209,14 @@ CDMD_API cdmd_status cdmd_sketch(cdmd_handle h, const cdmd_video* v, const cdmd_
  * 2.5 k + 9 <= 144), accepted only if every Ritz pair passes the residual test (see
  * cdmd_eigensolver_stats), else by the 8-CTA Householder solver (m - 1 <= 510; also for
  * k < 0, which needs every eigenvalue), else cuSOLVER's (syevdx for the k largest;
- * syevd for k < 0). */
+ * syevd for k < 0).
+ * Under stream capture (a CUDA graph of a whole step) cdmd_fit reads nothing back to the
+ * host: it keeps the model's sizes from the previous eager fit of the same (p, m, k, K)
+ * (k_eff, K_eff, n_coef; CDMD_ERR_UNSUPPORTED if there was none, for k < 0, or when a
+ * cuSOLVER path would be needed) and runs no eigensolver fallback; every replay re-checks
+ * itself and sets bit 16 (FLAG_GRAPH_STALE) of model->dev_info[3] when this run's sizes
+ * differ, the Lanczos residual test failed or a solver reported an error -- then refit
+ * eagerly and recapture. */
 CDMD_API size_t cdmd_model_bytes(int k, int K, int64_t m);
 CDMD_API cdmd_status cdmd_model_bind(cdmd_model* model, void* dev_buf, size_t bytes, int k, int K, int64_t m);
 CDMD_API size_t cdmd_fit_workspace_bytes(cdmd_handle h, int64_t p, int64_t m, int k);

@@ -384,6 +384,15 @@ class Pipeline:
         cdmd_sketch(self.h, v, self.c, self.Y, self.ws_sketch, stream)
         return self.Y
 
+    def graph_stale(self):
+        """After a replay of a captured step: True when the run disagreed with the sizes the
+        graph was captured with (k_eff, K_eff, n_coef, an eigensolver fallback or error) --
+        refit eagerly and recapture.  One 32-byte device-to-host read."""
+        base = self.model_buf.data_ptr()
+        off = self.model.dev_info - base
+        flags = int(self.model_buf[off + 12:off + 16].view(torch.int32).item())   # dev_info[INFO_FLAGS]
+        return bool(flags & 16)
+
     def fit(self, stream=None):
         k = -self.k if self.rank == "gd" else self.k
         _check("cdmd_set_background_selection", _lib.cdmd_set_background_selection(self.h.h, self.omega_eps))

@@ -356,7 +356,10 @@ cdmd_status cdmd_fit(cdmd_handle h, const void* Y, int64_t ldy, int32_t kind, in
   if (ldy < p || !(dt > 0.0)) return CDMD_ERR_ARG;
   if (model->m != m) return CDMD_ERR_ARG;
   if ((reinterpret_cast<uintptr_t>(ws) & 255) != 0) return CDMD_ERR_ARG;
-  model->k_eff = model->K_eff = model->n_coef = model->info = 0;
+  cudaStreamCaptureStatus cst = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing((cudaStream_t)st, &cst) != cudaSuccess) return CDMD_ERR_CUDA;
+  // under capture the model keeps the sizes of its previous (eager) fit: the graph assumes them
+  if (cst == cudaStreamCaptureStatusNone) model->k_eff = model->K_eff = model->n_coef = model->info = 0;
   return fit_impl(h, Y, ldy, kind, p, m, k, K, dt, model, ws, ws_bytes, (cudaStream_t)st);
 }
 

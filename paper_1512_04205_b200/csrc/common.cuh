@@ -67,7 +67,7 @@ __host__ __device__ inline int64_t round_up(int64_t a, int64_t b) { return ceil_
 
 // dev_info words written by kernels (read back by cdmd_fit)
 enum { INFO_K_EFF = 0, INFO_K_SEL = 1, INFO_N_COEF = 2, INFO_FLAGS = 3 };
-enum { FLAG_SPARSE_OVERFLOW = 1, FLAG_NONFINITE = 2, FLAG_EIG_PAIRING = 4 };
+enum { FLAG_SPARSE_OVERFLOW = 1, FLAG_NONFINITE = 2, FLAG_EIG_PAIRING = 4, FLAG_OMP_CHOL = 8, FLAG_GRAPH_STALE = 16 };
 
 }  // namespace cdmd
 

@@ -666,7 +666,9 @@ cudaError_t launch_eh(int n, int k, const double* G, int64_t ldg, double* lam, d
   double* wk = tau + n;
   cudaError_t err;
   // CDMD_PROFILE_FIT: CUDA events between the solver's kernels, printed to stderr
-  const bool prof = getenv("CDMD_PROFILE_FIT") != nullptr;
+  cudaStreamCaptureStatus cst_ = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(st, &cst_);
+  const bool prof = cst_ == cudaStreamCaptureStatusNone && getenv("CDMD_PROFILE_FIT") != nullptr;
   cudaEvent_t ev[6];
   if (prof) for (int i = 0; i < 6; ++i) { cudaEventCreate(&ev[i]); }
   auto mark = [&](int i) { if (prof) cudaEventRecord(ev[i], st); };
@@ -735,7 +737,9 @@ cudaError_t launch_eh_lz(int n, int k, const double* G, int64_t ldg, double* lam
   double* S = lam1 + (k + 1);
   int* jdone = reinterpret_cast<int*>(S + (size_t)J * (k + 1));
   cudaError_t err;
-  const bool prof = getenv("CDMD_PROFILE_FIT") != nullptr;
+  cudaStreamCaptureStatus cst_ = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(st, &cst_);
+  const bool prof = cst_ == cudaStreamCaptureStatusNone && getenv("CDMD_PROFILE_FIT") != nullptr;
   cudaEvent_t ev[6];
   if (prof) for (int i = 0; i < 6; ++i) cudaEventCreate(&ev[i]);
   auto mark = [&](int i) { if (prof) cudaEventRecord(ev[i], st); };

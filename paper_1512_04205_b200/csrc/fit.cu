@@ -98,37 +98,49 @@ static cdmd_status layout_ws(cdmd_handle h, int64_t p, int64_t m, int k, char* b
   W->cf = (double*)take(sizeof(double) * k);
   W->dinfo = (int*)take(sizeof(int) * 16);
   W->ehw = (double*)take(sizeof(double) * eh_work_doubles((int)n1, k));
-  // solver workspaces (queried with the final dimensions)
-  size_t d = 0, hb = 0;
-  if (cusolverDnXsyevd_bufferSize(h->solver, h->params, CUSOLVER_EIG_MODE_VECTOR,
-                                  CUBLAS_FILL_MODE_LOWER, n1, CUDA_R_64F, W->A, n1, CUDA_R_64F,
-                                  W->w, CUDA_R_64F, &d, &hb) != CUSOLVER_STATUS_SUCCESS)
-    return CDMD_ERR_CUDA;
+  // solver workspaces (queried with the final dimensions, once per handle and shape)
+  std::array<size_t, 4> sz{};
+  bool have = false;
   {
-    size_t d2 = 0, hb2 = 0;
-    int64_t meig = 0;
-    double vl = 0.0, vu = 0.0;
-    if (cusolverDnXsyevdx_bufferSize(h->solver, h->params, CUSOLVER_EIG_MODE_VECTOR, CUSOLVER_EIG_RANGE_I,
-                                     CUBLAS_FILL_MODE_LOWER, n1, CUDA_R_64F, W->A, n1, &vl, &vu,
-                                     n1 - k + 1, n1, &meig, CUDA_R_64F, W->w, CUDA_R_64F, &d2,
-                                     &hb2) != CUSOLVER_STATUS_SUCCESS)
-      return CDMD_ERR_CUDA;
-    if (d2 > d) d = d2;
-    if (hb2 > hb) hb = hb2;
+    std::lock_guard<std::mutex> g(h->mu);
+    auto it = h->fit_ws_sizes.find({p, m, k});
+    if (it != h->fit_ws_sizes.end()) {
+      sz = it->second;
+      have = true;
+    }
   }
-  W->sy_dev_bytes = d;
-  W->sy_host_bytes = hb;
-  W->sy_dev = take(d + 16);
-  d = 0;
-  hb = 0;
-  if (cusolverDnXgeev_bufferSize(h->solver, h->params, CUSOLVER_EIG_MODE_NOVECTOR,
-                                 CUSOLVER_EIG_MODE_VECTOR, k, CUDA_R_64F, W->B, k, CUDA_C_64F,
-                                 W->Wc, CUDA_R_64F, nullptr, k, CUDA_R_64F, W->VR, k, CUDA_R_64F,
-                                 &d, &hb) != CUSOLVER_STATUS_SUCCESS)
-    return CDMD_ERR_CUDA;
-  W->ge_dev_bytes = d;
-  W->ge_host_bytes = hb;
-  W->ge_dev = take(d + 16);
+  if (!have) {   // (not under stream capture: cdmd_fit_workspace_bytes or an eager fit fills the cache)
+    size_t d = 0, hb = 0;
+    if (cusolverDnXsyevd_bufferSize(h->solver, h->params, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n1,
+                                    CUDA_R_64F, W->A, n1, CUDA_R_64F, W->w, CUDA_R_64F, &d,
+                                    &hb) != CUSOLVER_STATUS_SUCCESS)
+      return CDMD_ERR_CUDA;
+    {
+      size_t d2 = 0, hb2 = 0;
+      int64_t meig = 0;
+      double vl = 0.0, vu = 0.0;
+      if (cusolverDnXsyevdx_bufferSize(h->solver, h->params, CUSOLVER_EIG_MODE_VECTOR, CUSOLVER_EIG_RANGE_I,
+                                       CUBLAS_FILL_MODE_LOWER, n1, CUDA_R_64F, W->A, n1, &vl, &vu, n1 - k + 1, n1,
+                                       &meig, CUDA_R_64F, W->w, CUDA_R_64F, &d2, &hb2) != CUSOLVER_STATUS_SUCCESS)
+        return CDMD_ERR_CUDA;
+      if (d2 > d) d = d2;
+      if (hb2 > hb) hb = hb2;
+    }
+    size_t gd = 0, ghb = 0;
+    if (cusolverDnXgeev_bufferSize(h->solver, h->params, CUSOLVER_EIG_MODE_NOVECTOR, CUSOLVER_EIG_MODE_VECTOR, k,
+                                   CUDA_R_64F, W->B, k, CUDA_C_64F, W->Wc, CUDA_R_64F, nullptr, k, CUDA_R_64F, W->VR,
+                                   k, CUDA_R_64F, &gd, &ghb) != CUSOLVER_STATUS_SUCCESS)
+      return CDMD_ERR_CUDA;
+    sz = {d, hb, gd, ghb};
+    std::lock_guard<std::mutex> g(h->mu);
+    h->fit_ws_sizes[{p, m, k}] = sz;
+  }
+  W->sy_dev_bytes = sz[0];
+  W->sy_host_bytes = sz[1];
+  W->sy_dev = take(sz[0] + 16);
+  W->ge_dev_bytes = sz[2];
+  W->ge_host_bytes = sz[3];
+  W->ge_dev = take(sz[2] + 16);
   W->total = off;
   return CDMD_OK;
 }
@@ -614,9 +626,14 @@ struct FitProf {
   }
 };
 
-#define BL(x)                                             \
-  do {                                                    \
-    if ((x) != CUBLAS_STATUS_SUCCESS) return CDMD_ERR_CUDA; \
+#define BL(x)                                                                                   \
+  do {                                                                                          \
+    const cublasStatus_t b_ = (x);                                                              \
+    if (b_ != CUBLAS_STATUS_SUCCESS) {                                                          \
+      if (getenv("CDMD_DEBUG")) fprintf(stderr, "[cdmd_fit] %s:%d %s: cuBLAS status %d\n", __FILE__, __LINE__, #x, \
+                                        (int)b_);                                               \
+      return CDMD_ERR_CUDA;                                                                     \
+    }                                                                                           \
   } while (0)
 // CDMD_DEBUG=1: name the failing call and the CUDA error on stderr
 #define CU(x)                                                                               \
@@ -629,6 +646,14 @@ struct FitProf {
     }                                                                                       \
   } while (0)
 
+// graph capture: the sizes a replay assumes (the previous eager fit's) against this run's
+__global__ void graph_check_kernel(int* __restrict__ dinfo, int ke, int K_sel, int n_coef) {
+  if (threadIdx.x != 0) return;
+  const bool bad = dinfo[INFO_K_EFF] != ke || dinfo[INFO_K_SEL] != K_sel || dinfo[INFO_N_COEF] != n_coef ||
+                   dinfo[8] != 0 || dinfo[9] != 0 || dinfo[10] != 0;
+  if (bad) dinfo[INFO_FLAGS] |= FLAG_GRAPH_STALE;
+}
+
 cdmd_status fit_impl(cdmd_handle h, const void* Y, int64_t ldy, int kind, int64_t p, int64_t m,
                      int k, int K, double dt, cdmd_model* model, void* ws, size_t ws_bytes,
                      cudaStream_t st) {
@@ -640,8 +665,15 @@ cdmd_status fit_impl(cdmd_handle h, const void* Y, int64_t ldy, int kind, int64_
   if (s0 != CDMD_OK) return s0;
   if (ws_bytes < W.total) return CDMD_ERR_WORKSPACE;
   const int64_t n1 = m - 1;
+  // Stream capture (a CUDA graph of the whole step): no host read-backs -- the sizes come
+  // from the previous eager fit of this model, and the graph_check kernel flags a replay
+  // whose run disagrees (dev_info[INFO_FLAGS] & FLAG_GRAPH_STALE) so the caller refits eagerly
+  cudaStreamCaptureStatus cst = cudaStreamCaptureStatusNone;
+  CU(cudaStreamIsCapturing(st, &cst));
+  const bool cap = cst != cudaStreamCaptureStatusNone;
+  if (cap && (gd || model->k_eff < 1)) return CDMD_ERR_UNSUPPORTED;
   FitProf prof;
-  prof.on = getenv("CDMD_PROFILE_FIT") != nullptr;
+  prof.on = !cap && getenv("CDMD_PROFILE_FIT") != nullptr;
   prof.st = st;
   prof.mark("start");
   BL(cublasSetStream(h->blas, st));
@@ -680,6 +712,7 @@ cdmd_status fit_impl(cdmd_handle h, const void* Y, int64_t ldy, int kind, int64_
   const double beta = (double)(p < n1 ? p : n1) / (double)(p < n1 ? n1 : p);
   const double gd_omega = gd ? 0.56 * beta * beta * beta - 0.95 * beta * beta + 1.82 * beta + 1.43 : 0.0;
   double* med = W.ehw + eh_work_doubles((int)n1, k) - 8;   // two doubles of the eigh workspace slack
+  if (cap && smode != 0 && smode != 3) return CDMD_ERR_UNSUPPORTED;   // cuSOLVER's host workspaces
   if (smode == 3) {
     // Lanczos: k largest pairs written ascending into (W.w, W.A); dinfo[10] = not converged
     cudaError_t le = launch_eh_lz((int)n1, k, W.G, m, W.w, W.A, W.ehw, W.dinfo + 8, W.dinfo + 10, st);
@@ -720,10 +753,12 @@ cdmd_status fit_impl(cdmd_handle h, const void* Y, int64_t ldy, int kind, int64_
   select_topk_kernel<<<k, 128, 0, st>>>(W.A, W.w, n1, top, k, W.V, model->sigma, W.dinfo, gd_omega, med_cnt,
                                         smode == 0 ? med : nullptr);
   CU(cudaGetLastError());
-  CU(cudaMemcpyAsync(h->host_info, W.dinfo, sizeof(int) * 16, cudaMemcpyDeviceToHost, st));
-  CU(cudaStreamSynchronize(st));
-  if (smode == 3) h->lz_runs.fetch_add(1);
-  if (smode == 3 && h->host_info[10] != 0) {
+  if (!cap) {
+    CU(cudaMemcpyAsync(h->host_info, W.dinfo, sizeof(int) * 16, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+  }
+  if (smode == 3 && !cap) h->lz_runs.fetch_add(1);
+  if (smode == 3 && !cap && h->host_info[10] != 0) {
     // a Ritz pair failed the residual test: the Householder solver decides
     h->lz_fallbacks.fetch_add(1);
     if (eh_supported((int)n1, k)) {
@@ -748,11 +783,11 @@ cdmd_status fit_impl(cdmd_handle h, const void* Y, int64_t ldy, int kind, int64_
     CU(cudaStreamSynchronize(st));
   }
   prof.mark("select+sync");
-  if (h->host_info[8] != 0) {
+  if (!cap && h->host_info[8] != 0) {
     model->info = h->host_info[8];
     return CDMD_ERR_NUMERIC;
   }
-  const int ke = h->host_info[INFO_K_EFF];
+  const int ke = cap ? model->k_eff : h->host_info[INFO_K_EFF];
   model->k_eff = ke;
   if (ke < 1) return CDMD_ERR_NUMERIC;
   // A~ = S^-1 V^T (Y^T Y') V S^-1, Y^T Y' = G[0:m-1, 1:m] = G + m (ld m)
@@ -769,6 +804,8 @@ cdmd_status fit_impl(cdmd_handle h, const void* Y, int64_t ldy, int kind, int64_
   // cuSOLVER's hybrid geev for k > 118 or with CDMD_GEEV=cusolver.
   if (use_device_eig(ke)) {
     CU(launch_hqr_eig(ke, W.B, W.Wc, W.VR, W.dinfo + 9, W.Es, st));
+  } else if (cap) {
+    return CDMD_ERR_UNSUPPORTED;   // cuSOLVER geev's host workspace
   } else {
     size_t d = 0, hb = 0;
     if (cusolverDnXgeev_bufferSize(h->solver, h->params, CUSOLVER_EIG_MODE_NOVECTOR,
@@ -815,6 +852,13 @@ cdmd_status fit_impl(cdmd_handle h, const void* Y, int64_t ldy, int kind, int64_
   quantize_kernel<<<model->kpad, 256, 0, st>>>(model->Mfold, n1, ke, model->kpad, model->mpad,
                                                model->Mq, model->Mq_scale);
   CU(cudaGetLastError());
+  if (cap) {   // a replay checks itself against the sizes it was captured with
+    note_launch();
+    graph_check_kernel<<<1, 32, 0, st>>>(W.dinfo, ke, model->K_eff, model->n_coef);
+    CU(cudaGetLastError());
+    CU(cudaMemcpyAsync(model->dev_info, W.dinfo, sizeof(int32_t) * 8, cudaMemcpyDeviceToDevice, st));
+    return CDMD_OK;
+  }
   CU(cudaMemcpyAsync(model->dev_info, W.dinfo, sizeof(int32_t) * 8, cudaMemcpyDeviceToDevice, st));
   CU(cudaMemcpyAsync(h->host_info, W.dinfo, sizeof(int) * 16, cudaMemcpyDeviceToHost, st));
   CU(cudaStreamSynchronize(st));

@@ -5,6 +5,7 @@
 
 #include <atomic>
 #include <map>
+#include <array>
 #include <mutex>
 #include <set>
 #include <tuple>
@@ -42,6 +43,9 @@ struct cdmd_handle_s {
   std::mutex mu;
   std::vector<char> host_ws;         // cuSOLVER host workspace (fit only)
   double omega_eps = 0.0;            // > 0: background by |omega| < omega_eps, else OMP
+  // cuSOLVER workspace sizes per (p, m, k) (sy_dev, sy_host, ge_dev, ge_host): queried once,
+  // so a fit under stream capture needs no cuSOLVER call
+  std::map<std::tuple<int64_t, int64_t, int>, std::array<size_t, 4>> fit_ws_sizes;
   std::atomic<uint64_t> lz_runs{0};       // cdmd_fit calls whose eigenpairs came from Lanczos
   std::atomic<uint64_t> lz_fallbacks{0};  // ... of which failed the residual test (Householder reran)
 };

@@ -1355,3 +1355,42 @@ def test_fit_eigensolver_edges(C, H, p, m, k):
     assert np.max(np.abs(gm["sigma"] - om["sigma"]) / om["sigma"]) <= 1e-6
     perm, err = PT.match_eigs(gm["lam"], om["lam"])
     assert err <= PT.RTOL_EIG, err
+
+
+def test_whole_step_cuda_graph(C, H):
+    """The step sketch -> fit -> modes -> foreground captured in ONE CUDA graph (cdmd_fit
+    without host read-backs under stream capture) replays bit-identically to the eager
+    step, and its self-check flag stays clear; a Gavish-Donoho fit refuses capture."""
+    cfg = config_by_name("c2_320x240_spixel")
+    X = video_for(cfg)
+    m, n = X.shape
+    Xd = to_dev(X)
+    P = C.Pipeline(H, n, n, m, cfg.kind, cfg.p, cfg.k, cfg.K, seed=cfg.sensing_seed)
+    mask_e = P.run(Xd, cfg.tau, C.BG_DYNAMIC).clone()
+    phi_e = P.Phi.clone()
+    torch.cuda.synchronize()
+    s = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        P.run(Xd, cfg.tau, C.BG_DYNAMIC)   # warm the capture stream's handles
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=s):
+            P.sketch(Xd)
+            P.fit()
+            P.modes(Xd)
+            P.foreground(Xd, cfg.tau, C.BG_DYNAMIC)
+    P.mask.zero_()
+    P.Phi.zero_()
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    assert not P.graph_stale()
+    assert torch.equal(P.mask, mask_e)
+    assert torch.equal(P.Phi, phi_e)
+    Pg = C.Pipeline(H, n, n, m, cfg.kind, cfg.p, cfg.k, cfg.K, seed=cfg.sensing_seed, rank="gd")
+    Pg.run(Xd, cfg.tau, C.BG_DYNAMIC)
+    torch.cuda.synchronize()
+    g2 = torch.cuda.CUDAGraph()
+    with pytest.raises(C.CdmdError):
+        with torch.cuda.graph(g2, stream=s):
+            Pg.fit()
