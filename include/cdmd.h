@@ -213,7 +213,9 @@ CDMD_API cdmd_status cdmd_sketch(cdmd_handle h, const cdmd_video* v, const cdmd_
  * Under stream capture (a CUDA graph of a whole step) cdmd_fit reads nothing back to the
  * host: it keeps the model's sizes from the previous eager fit of the same (p, m, k, K)
  * (k_eff, K_eff, n_coef; CDMD_ERR_UNSUPPORTED if there was none, for k < 0, or when a
- * cuSOLVER path would be needed) and runs no eigensolver fallback; every replay re-checks
+ * cuSOLVER path would be needed), takes the symmetric solver the last eager fit of that
+ * shape ended with (Lanczos, or Householder after a fallback) and runs no fallback of its
+ * own; every replay re-checks
  * itself and sets bit 16 (FLAG_GRAPH_STALE) of model->dev_info[3] when this run's sizes
  * differ, the Lanczos residual test failed or a solver reported an error -- then refit
  * eagerly and recapture. */

@@ -712,6 +712,10 @@ cdmd_status fit_impl(cdmd_handle h, const void* Y, int64_t ldy, int kind, int64_
   const double beta = (double)(p < n1 ? p : n1) / (double)(p < n1 ? n1 : p);
   const double gd_omega = gd ? 0.56 * beta * beta * beta - 0.95 * beta * beta + 1.82 * beta + 1.43 : 0.0;
   double* med = W.ehw + eh_work_doubles((int)n1, k) - 8;   // two doubles of the eigh workspace slack
+  if (cap && smode == 3) {   // mirror the eager path: Householder where Lanczos last fell back
+    std::lock_guard<std::mutex> g(h->mu);
+    if (h->lz_fell_back.count({n1, k})) smode = eh_supported((int)n1, k) ? 0 : 2;
+  }
   if (cap && smode != 0 && smode != 3) return CDMD_ERR_UNSUPPORTED;   // cuSOLVER's host workspaces
   if (smode == 3) {
     // Lanczos: k largest pairs written ascending into (W.w, W.A); dinfo[10] = not converged
@@ -757,7 +761,12 @@ cdmd_status fit_impl(cdmd_handle h, const void* Y, int64_t ldy, int kind, int64_
     CU(cudaMemcpyAsync(h->host_info, W.dinfo, sizeof(int) * 16, cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
   }
-  if (smode == 3 && !cap) h->lz_runs.fetch_add(1);
+  if (smode == 3 && !cap) {
+    h->lz_runs.fetch_add(1);
+    std::lock_guard<std::mutex> g(h->mu);
+    if (h->host_info[10] != 0) h->lz_fell_back.insert({n1, k});
+    else h->lz_fell_back.erase({n1, k});
+  }
   if (smode == 3 && !cap && h->host_info[10] != 0) {
     // a Ritz pair failed the residual test: the Householder solver decides
     h->lz_fallbacks.fetch_add(1);

@@ -46,6 +46,9 @@ struct cdmd_handle_s {
   // cuSOLVER workspace sizes per (p, m, k) (sy_dev, sy_host, ge_dev, ge_host): queried once,
   // so a fit under stream capture needs no cuSOLVER call
   std::map<std::tuple<int64_t, int64_t, int>, std::array<size_t, 4>> fit_ws_sizes;
+  // (m - 1, k) shapes whose last eager fit fell back from Lanczos: a fit captured into a
+  // graph for them takes the Householder solver directly, as the eager fit ended up doing
+  std::set<std::pair<int64_t, int>> lz_fell_back;
   std::atomic<uint64_t> lz_runs{0};       // cdmd_fit calls whose eigenpairs came from Lanczos
   std::atomic<uint64_t> lz_fallbacks{0};  // ... of which failed the residual test (Householder reran)
 };
