@@ -54,7 +54,15 @@ def report(path):
             "dram__throughput.avg.pct_of_peak_sustained_elapsed", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
             "sm__pipe_tc_cycles_active.avg.pct_of_peak_sustained_elapsed", "sm__inst_executed_pipe_tc.sum",
             "smsp__inst_executed.sum", "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
-            "sm__warps_active.avg.pct_of_peak_sustained_active", "lts__t_sector_hit_rate.pct"]
+            "sm__warps_active.avg.pct_of_peak_sustained_active", "lts__t_sector_hit_rate.pct",
+            # shared-memory bandwidth (the Gaussian sketch's bound)
+            "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
+            "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+            "l1tex__data_pipe_tc_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+            "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum",
+            "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum",
+            "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_st.sum",
+            "smsp__inst_executed_op_shared_ld.sum"]
     units = rows[1]
     for r in rows[2:]:
         print("kernel:", r[h.index("Kernel Name")][:140])

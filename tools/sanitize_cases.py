@@ -46,6 +46,7 @@ def run(name):
     P.amplitudes(Xd)
     if name == "c1":
         P.median3(32, 24)
+        P.foreground_median3(Xd, 25.0, 32, 24)
     torch.cuda.synchronize()
     print(name, "k_eff", P.model.k_eff, "K_eff", P.model.K_eff, flush=True)
 
