@@ -30,6 +30,9 @@ def cuda_home():
 def _stale():
     if not os.path.exists(LIB):
         return True
+    stamp = os.path.join(HERE, "lib", "obj", "flags")   # the library was built with other extra flags
+    if (open(stamp).read() if os.path.exists(stamp) else "") != os.environ.get("CDMD_EXTRA_NVCC", ""):
+        return True
     t = os.path.getmtime(LIB)
     deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [os.path.join(ROOT, "include", "cdmd.h"), __file__]
     return any(os.path.getmtime(d) > t for d in deps)
