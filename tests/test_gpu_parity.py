@@ -338,6 +338,47 @@ def test_c3_rademacher_full_size_sampled_rows(C, H):
     assert np.array_equal(Y[rows].astype(np.int64), want)
 
 
+def test_c3_rademacher_full_pipeline(C, H):
+    """BASELINE's C3 (720x480x300, Rademacher p = 1500, k = 30) through the whole path
+    against the oracle: ALL 1500 rows of Y bit-exact (the oracle's slab sketches summed,
+    computed in worker processes), the fit (sigma 1e-6, lambda 1e-4, supports), Phi on
+    every pixel per column and the dynamic mask on every pixel."""
+    from oracle.runner import PixelPool, parallel_sketch
+    cfg = config_by_name("c3_720x480_rademacher")
+    X = video_for(cfg)
+    m, n = X.shape
+    Xd = to_dev(X)
+    P = C.Pipeline(H, n, n, m, "rademacher", cfg.p, cfg.k, cfg.K)
+    Yg = P.sketch(Xd).cpu().numpy().T.astype(np.int64)
+    P.fit()
+    gm = C.model_to_host(P.model)
+    Phi = P.modes(Xd).cpu().numpy()
+    mask = P.foreground(Xd, cfg.tau, C.BG_DYNAMIC).cpu().numpy().view(np.uint32)
+    torch.cuda.synchronize()
+    del Xd
+    Yo = parallel_sketch(cfg, OS.RADEMACHER)
+    assert np.array_equal(Yg, Yo)
+    om = OD.fit(Yo, cfg.k, cfg.K)
+    assert gm["k_eff"] == om["k_eff"]
+    perm, err = PT.match_eigs(gm["lam"], om["lam"])
+    assert err <= PT.RTOL_EIG, err
+    assert np.max(np.abs(gm["sigma"] - om["sigma"]) / om["sigma"]) <= 1e-6
+    assert PT.supports_equal_mod_conj(gm["support"], gm["pair"], perm, om["support"], om["pair"])
+    with PixelPool(cfg) as pool:
+        ref = pool.run(om, cfg.tau, dynamic=True, want=("Phi", "mask", "band"))
+    worst = _phi_columns_parity(PT.unfold(Phi, gm["pair"]), ref["Phi"], perm, om["lam"], gm["k_eff"])
+    assert worst <= PT.RTOL_PHI, worst
+    frac, outside, nd = _full_frame_mask_parity(mask, n, ref["mask"], ref["band"])
+    print(f"c3 rademacher full: phi worst {worst:.2e}, mask agreement {frac:.7f} ({nd} px, {outside} outside band)")
+    assert frac >= PT.MASK_AGREE and outside == 0, (frac, nd, outside)
+    fm = fused_mask(C, P, to_dev(X), cfg.tau)   # N11 on the same model, when the support fits it
+    torch.cuda.synchronize()
+    if fm is not None:
+        frac, outside, nd = _full_frame_mask_parity(fm, n, ref["mask"], ref["band"])
+        print(f"c3 rademacher fused: mask agreement {frac:.7f} ({nd} px, {outside} outside band)")
+        assert frac >= PT.MASK_AGREE and outside == 0, (frac, nd, outside)
+
+
 def _phi_columns_parity(Pg, Po, perm, lam_o, k_eff):
     """Per-column relative error of the folded-then-unfolded device modes against the
     oracle's, after unit-phase alignment, over well-separated eigenvalues; returns the worst."""
