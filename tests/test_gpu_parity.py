@@ -763,15 +763,19 @@ def test_sparse_plan_check_refused_inside_graph_capture(C):
     assert torch.equal(P.Y, want)
 
 
-@pytest.mark.parametrize("W,Hh,m,dens", [(37, 23, 5, 0.35), (64, 16, 3, 0.5), (720, 480, 4, 0.1), (5, 3, 2, 0.6),
-                                         (33, 1, 2, 0.5), (1, 40, 2, 0.5)])
-def test_mask_median3_bit_exact(C, W, Hh, m, dens):
+@pytest.mark.parametrize("W,Hh,m,dens,pad", [(37, 23, 5, 0.35, 3), (64, 16, 3, 0.5, 3), (720, 480, 4, 0.1, 3),
+                                             (5, 3, 2, 0.6, 3), (33, 1, 2, 0.5, 3), (1, 40, 2, 0.5, 3),
+                                             # word-aligned rows (W % 128 == 0, ldw % 4 == 0): the vectorised kernel
+                                             (256, 37, 5, 0.4, 4), (128, 1, 3, 0.5, 0), (384, 2, 2, 0.55, 0),
+                                             (1920, 9, 3, 0.2, 0), (512, 64, 2, 0.9, 8)])
+def test_mask_median3_bit_exact(C, W, Hh, m, dens, pad):
     """3x3 median post-filter (Fig. 7): bit-exact against the oracle on random
-    masks (widths that are not multiples of 32 straddle words across image rows)."""
+    masks (widths that are not multiples of 32 straddle words across image rows; widths
+    that are multiples of 128 take the vectorised word-aligned kernel)."""
     rng = np.random.default_rng(W * 1000 + Hh)
     n = W * Hh
     M = rng.random((m, n)) < dens
-    ldw = (n + 31) // 32 + 3
+    ldw = (n + 31) // 32 + pad
     packed = np.zeros((m, ldw), dtype=np.uint32)
     packed[:, :(n + 31) // 32] = OD.pack_mask(M)
     dev = torch.from_numpy(packed.view(np.int32)).cuda()

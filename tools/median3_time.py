@@ -1,5 +1,5 @@
 import torch, sys
-sys.path.insert(0, '/root/repo')
+sys.path.insert(0, '.')
 from paper_1512_04205_b200 import cdmd as C
 W, H, m = 1920, 1080, 500
 n = W * H
