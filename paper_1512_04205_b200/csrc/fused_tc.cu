@@ -199,6 +199,98 @@ __device__ __noinline__ void fu_median_rows(int64_t m, int64_t ldw, int W, int H
   }
 }
 
+// phase (b) for word-aligned rows (W % 128 == 0, 16-B aligned masks, ldw % 4 == 0): tasks
+// are bands of FU_MB image rows over ALL frames (one task per CTA at 1080p), so the
+// claim / wait / barrier overhead is paid ~once per CTA; within a band a thread takes
+// (4-word group g, frame t) items and slides a three-row window down the band's rows,
+// one coalesced 16-B load per row, the side words from the neighbouring lanes (as
+// median3.cu's word-aligned kernel; the words across an image-row boundary are zero).
+constexpr int FU_MB = 8;
+__device__ __noinline__ void fu_median_bands(int64_t m, int64_t ldw, int W, int H, int ncw, const uint32_t* raw,
+                                             uint32_t* out, int* cnt, int* rowq, int tid, int nthr, int& rowsh) {
+  const int nwr = W >> 5, G = nwr >> 2;
+  const int nb = (H + FU_MB - 1) / FU_MB;
+  const int lane = tid & 31;
+  for (;;) {
+    if (tid == 0) {
+      const int b = atomicAdd(rowq, 1);
+      rowsh = b;
+      if (b < nb) {   // wait until every row of the band (and so its neighbours) is complete
+        for (int yy = b * FU_MB; yy < min(H, (b + 1) * FU_MB); ++yy) {
+          const int need = ncw * ((yy > 0) + 1 + (yy < H - 1));
+          int c;
+          for (;;) {
+            asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(c) : "l"(cnt + yy) : "memory");
+            if (c >= need) break;
+            __nanosleep(256);
+          }
+        }
+      }
+    }
+    asm volatile("bar.sync 3, %0;" ::"r"(nthr) : "memory");
+    const int b = rowsh;
+    asm volatile("bar.sync 3, %0;" ::"r"(nthr) : "memory");
+    if (b >= nb) break;
+    const int y0 = b * FU_MB;
+    const int64_t items = (int64_t)G * m;
+    for (int64_t i0 = 0; i0 < items; i0 += nthr) {       // warp-uniform trip count (shuffles)
+      const int64_t it = i0 + tid;
+      const bool act = it < items;
+      const int g = act ? (int)(it % G) : 0;
+      const int64_t t = act ? it / G : 0;
+      const uint32_t* f = raw + t * ldw;
+      uint32_t* o = out + t * ldw;
+      auto load_row = [&](int y, uint32_t (&c)[4], uint32_t& lw, uint32_t& rw) {
+        const bool ok = act && y >= 0 && y < H;
+        const int64_t q = (int64_t)y * nwr + 4 * g;
+        uint4 v = make_uint4(0u, 0u, 0u, 0u);
+        if (ok) v = __ldcg(reinterpret_cast<const uint4*>(f + q));
+        c[0] = v.x; c[1] = v.y; c[2] = v.z; c[3] = v.w;
+        lw = __shfl_up_sync(0xffffffffu, v.w, 1);
+        rw = __shfl_down_sync(0xffffffffu, v.x, 1);
+        if (lane == 0) lw = (ok && g > 0) ? __ldcg(f + q - 1) : 0u;
+        if (lane == 31) rw = (ok && g < G - 1) ? __ldcg(f + q + 4) : 0u;
+      };
+      // all FU_MB + 2 rows in flight at once: one CTA per SM runs this trailing phase, so
+      // the loads of a thread are what hides the L2 latency
+      uint32_t c[FU_MB + 2][4], lw[FU_MB + 2], rw[FU_MB + 2];
+#pragma unroll
+      for (int i = 0; i < FU_MB + 2; ++i) load_row(y0 - 1 + i, c[i], lw[i], rw[i]);
+#pragma unroll
+      for (int i = 0; i < FU_MB; ++i) {
+        const int y = y0 + i;
+        if (act && y < H) {
+          uint32_t res[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            uint32_t x[9];
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+              const int rr = i + d;
+              const uint32_t cc = c[rr][u];
+              const uint32_t l = (u == 0) ? (g == 0 ? 0u : lw[rr]) : c[rr][u - 1];
+              const uint32_t r = (u == 3) ? (g == G - 1 ? 0u : rw[rr]) : c[rr][u + 1];
+              x[3 * d + 0] = (cc << 1) | (l >> 31);
+              x[3 * d + 1] = cc;
+              x[3 * d + 2] = (cc >> 1) | (r << 31);
+            }
+            uint32_t s1, c1, s2, c2, s3, c3, s4, c4, s5, c5;
+            fu_fa(x[0], x[1], x[2], s1, c1);
+            fu_fa(x[3], x[4], x[5], s2, c2);
+            fu_fa(x[6], x[7], x[8], s3, c3);
+            fu_fa(s1, s2, s3, s4, c4);
+            fu_fa(c1, c2, c3, s5, c5);
+            const uint32_t b1 = s5 ^ c4, c6 = s5 & c4;
+            const uint32_t b2 = c5 ^ c6, b3 = c5 & c6;
+            res[u] = b3 | (b2 & (b1 | s4));
+          }
+          *reinterpret_cast<uint4*>(o + (int64_t)y * nwr + 4 * g) = make_uint4(res[0], res[1], res[2], res[3]);
+        }
+      }
+    }
+  }
+}
+
 // STATIC (template ST): no phase B; the convert warps reduce Phi_F of each
 // pixel to its static background L = sum_f Phi_F[f] c_f(1) (the fmaf order of
 // foreground.cu's static kernel) and the integer bounds x > floor(L + tau), x <
@@ -581,7 +673,11 @@ __global__ void __launch_bounds__(FU_THREADS, 1) fused_fg_kernel(
   }
   // phase (b): warps 2 .. FU_BWARP filter whole image rows (median fused)
   if (imgW > 0 && warp >= 2)
-    fu_median_rows(m, ldw, imgW, imgH, ncw, mask, medout, medcnt, medcnt + imgH, threadIdx.x - 64,
+    if (imgW % 128 == 0 && ldw % 4 == 0 && ((reinterpret_cast<uintptr_t>(mask) | reinterpret_cast<uintptr_t>(medout)) & 15) == 0)
+      fu_median_bands(m, ldw, imgW, imgH, ncw, mask, medout, medcnt, medcnt + imgH, threadIdx.x - 64,
+                      blockDim.x - 64, rowsh);
+    else
+      fu_median_rows(m, ldw, imgW, imgH, ncw, mask, medout, medcnt, medcnt + imgH, threadIdx.x - 64,
                    blockDim.x - 64, rowsh);
   __syncthreads();
   if (warp == 1) {

@@ -1251,6 +1251,8 @@ def test_bench_two_ranks_runs(partition, tmp_path):
 
 @pytest.mark.parametrize("W,Hh,m,p,k,K,mode", [(64, 48, 40, 120, 10, 3, "dyn"), (320, 240, 200, 1000, 20, 10, "dyn"),
                                                 (320, 240, 200, 1000, 20, 10, "sta"), (96, 33, 77, 200, 12, 4, "dyn"),
+                                                # W % 128 == 0: the banded median phase (H not a multiple of 8)
+                                                (256, 45, 60, 300, 12, 4, "dyn"), (384, 19, 33, 300, 12, 4, "sta"),
                                                 (1920, 1080, 500, 2000, 50, 10, "dyn")])
 def test_fused_median_bit_exact(C, H, W, Hh, m, p, k, K, mode):
     """The 3x3 median folded into the fused pass (Fig. 7): the filtered mask equals
