@@ -67,6 +67,22 @@ __device__ __forceinline__ double rsqrt_nr(double x) {
   y = y * fma(-h * y, y, 1.5);
   return y * fma(-h * y, y, 1.5);
 }
+// The same to full precision in fewer dependent steps (the Francis step's scalar chain):
+// one third-order correction from the hardware approximation (relative error e0 ~ 2^-22
+// -> ~e0^3): reciprocal r (1 + e + e^2), e = 1 - x r; reciprocal square root
+// y (1 + e/2 + 3 e^2 / 8), e = 1 - x y^2.
+__device__ __forceinline__ double rcp_hc(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  const double e = fma(-x, r, 1.0);
+  return fma(r, fma(e, e, e), r);
+}
+__device__ __forceinline__ double rsqrt_hc(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double e = fma(-x, y * y, 1.0);
+  return fma(y * e, fma(e, 0.375, 0.5), y);
+}
 
 }  // namespace
 
@@ -1047,27 +1063,26 @@ __global__ void __launch_bounds__(32 * HQ_WARPS, 1) hqrv_kernel(int nn, const do
             r = notlast ? Hx(kk + 2, kk - 1) : 0.0;
           }
           nreg = false;
-          x = fabs(p) + fabs(q) + fabs(r);
-          if (x == 0.0) continue;
-          if (x < 1e-140 || x > 1e140) {
-            const double ix = 1.0 / x;
-            p = p * ix;
-            q = q * ix;
-            r = r * ix;
-          } else {
-            x = 1.0;
-          }
         }
         nreg = false;
-        const double ss = p * p + q * q + r * r;
-        const double rs = ss > 0.0 ? rsqrt_nr(ss) : 0.0;
-        s = ss * rs;
-        double is = rs;   // 1 / s
-        if (p < 0) {
-          s = -s;
-          is = -is;
+        // EISPACK scales (p, q, r) by |p| + |q| + |r|; the scaling only matters near under- or
+        // overflow, so the range test is taken on p^2 + q^2 + r^2 (needed anyway) and the
+        // abs-sum stays off the step's dependent chain (x = 1 otherwise, as before)
+        double ss = p * p + q * q + r * r;
+        x = 1.0;
+        if (kk != m && !(ss >= 1e-280 && ss <= 1e280)) {
+          x = fabs(p) + fabs(q) + fabs(r);
+          if (x == 0.0) continue;
+          const double ix = 1.0 / x;
+          p = p * ix;
+          q = q * ix;
+          r = r * ix;
+          ss = p * p + q * q + r * r;
         }
-        if (s == 0) continue;
+        if (ss == 0.0) continue;
+        double is = rsqrt_hc(ss);   // 1 / s, s = sign(p) ||(p, q, r)||
+        if (p < 0) is = -is;
+        s = ss * is;
         if (kk != m) {
           Hx(kk, kk - 1) = -s * x;   // every lane the same value; read by no lane this step
         } else if (l != m) {
@@ -1078,8 +1093,8 @@ __global__ void __launch_bounds__(32 * HQ_WARPS, 1) hqrv_kernel(int nn, const do
 #ifdef CDMD_HQR_PROF2
         unsigned long long tb0 = clock64();
 #endif
-        p = p + s;
-        const double ip = rcp_nr(p);
+        p = fma(ss, is, p);   // p + s
+        const double ip = rcp_hc(p);
         x = p * is;
         y = q * is;
         z = r * is;
