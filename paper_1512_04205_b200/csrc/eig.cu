@@ -1069,6 +1069,7 @@ __global__ void __launch_bounds__(32 * HQ_WARPS, 1) hqrv_kernel(int nn, const do
         // overflow, so the range test is taken on p^2 + q^2 + r^2 (needed anyway) and the
         // abs-sum stays off the step's dependent chain (x = 1 otherwise, as before)
         double ss = p * p + q * q + r * r;
+        double is = rsqrt_hc(ss);   // 1 / s, s = sign(p) ||(p, q, r)|| (issued before the range test)
         x = 1.0;
         if (kk != m && !(ss >= 1e-280 && ss <= 1e280)) {
           x = fabs(p) + fabs(q) + fabs(r);
@@ -1078,9 +1079,9 @@ __global__ void __launch_bounds__(32 * HQ_WARPS, 1) hqrv_kernel(int nn, const do
           q = q * ix;
           r = r * ix;
           ss = p * p + q * q + r * r;
+          is = rsqrt_hc(ss);
         }
         if (ss == 0.0) continue;
-        double is = rsqrt_hc(ss);   // 1 / s, s = sign(p) ||(p, q, r)||
         if (p < 0) is = -is;
         s = ss * is;
         if (kk != m) {
