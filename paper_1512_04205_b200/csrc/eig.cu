@@ -1071,17 +1071,19 @@ __global__ void __launch_bounds__(32 * HQ_WARPS, 1) hqrv_kernel(int nn, const do
         double ss = p * p + q * q + r * r;
         double is = rsqrt_hc(ss);   // 1 / s, s = sign(p) ||(p, q, r)|| (issued before the range test)
         x = 1.0;
-        if (kk != m && !(ss >= 1e-280 && ss <= 1e280)) {
-          x = fabs(p) + fabs(q) + fabs(r);
-          if (x == 0.0) continue;
-          const double ix = 1.0 / x;
-          p = p * ix;
-          q = q * ix;
-          r = r * ix;
-          ss = p * p + q * q + r * r;
-          is = rsqrt_hc(ss);
+        if (!(ss >= 1e-280 && ss <= 1e280)) {   // rare: one branch per step for every special case
+          if (kk != m) {
+            x = fabs(p) + fabs(q) + fabs(r);
+            if (x == 0.0) continue;
+            const double ix = 1.0 / x;
+            p = p * ix;
+            q = q * ix;
+            r = r * ix;
+            ss = p * p + q * q + r * r;
+            is = rsqrt_hc(ss);
+          }
+          if (ss == 0.0) continue;
         }
-        if (ss == 0.0) continue;
         if (p < 0) is = -is;
         s = ss * is;
         if (kk != m) {
@@ -1163,7 +1165,8 @@ __global__ void __launch_bounds__(32 * HQ_WARPS, 1) hqrv_kernel(int nn, const do
         cb1[0] = g10;
         cb1[1] = g11;
         cb1[2] = g12;
-        // slots beyond two (n > 64): plain loops
+        // slots beyond two (n > 64): plain loops, behind warp-uniform guards
+        if (kk + 3 + 64 <= n)
         for (int j = j1 + 32; j <= n; j += 32) {
           double pp = Hx(kk, j) + q * Hx(kk + 1, j);
           if (notlast) {
@@ -1173,6 +1176,7 @@ __global__ void __launch_bounds__(32 * HQ_WARPS, 1) hqrv_kernel(int nn, const do
           Hx(kk, j) = Hx(kk, j) - pp * x;
           Hx(kk + 1, j) = Hx(kk + 1, j) - pp * y;
         }
+        if (l + 64 <= kk - 1)
         for (int i = i1 + 32; i <= kk - 1; i += 32) {
           double pp = x * Hx(i, kk) + y * Hx(i, kk + 1);
           if (notlast) {
