@@ -1007,6 +1007,11 @@ __global__ void __launch_bounds__(32 * HQ_WARPS, 1) hqrv_kernel(int nn, const do
         Hx(i, i - 2) = 0.0;
         if (i > m + 2) Hx(i, i - 3) = 0.0;
       }
+      // EISPACK negates H(m, m-1) at the first bulge step when the bulge starts below l;
+      // it does not depend on the reflector, so it is done here, off the step loop
+      const double hneg = (l != m) ? -Hx(m, m - 1) : 0.0;
+      wp.sync();
+      if (l != m && lane == 0) Hx(m, m - 1) = hneg;
       wp.sync();
       pr[6] += n - m;
 #ifdef CDMD_HQR_PROF2
@@ -1022,8 +1027,9 @@ __global__ void __launch_bounds__(32 * HQ_WARPS, 1) hqrv_kernel(int nn, const do
       // column-update dummy, scr[8 + lane + {0, ld, 2 ld}] the row-update dummies.
       double* const Z0 = scr;
       double* const CD = scr + 4;
-      bool nreg = false;
-      double pn = 0.0, qn = 0.0, rn = 0.0;
+      // (p, q, r) of every step come from registers: the bulge start's for kk = m, the
+      // previous step's updated block otherwise, or -- after a skipped step -- column kk of H
+      double pn = p, qn = q, rn = r;
       for (int kk = m; kk <= n - 1; ++kk) {  // double QR step on the active block l..n
         const bool notlast = (kk != n - 1);
         // ---- operands (independent of this step's reflector)
@@ -1052,19 +1058,9 @@ __global__ void __launch_bounds__(32 * HQ_WARPS, 1) hqrv_kernel(int nn, const do
         double g00 = cb0[0], g01 = cb0[1], g02 = cb0[2];
         double g10 = cb1[0], g11 = cb1[1], g12 = cb1[2];
         // ---- the reflector
-        if (kk != m) {
-          if (nreg) {
-            p = pn;
-            q = qn;
-            r = notlast ? rn : 0.0;
-          } else {
-            p = Hx(kk, kk - 1);
-            q = Hx(kk + 1, kk - 1);
-            r = notlast ? Hx(kk + 2, kk - 1) : 0.0;
-          }
-          nreg = false;
-        }
-        nreg = false;
+        p = pn;
+        q = qn;
+        r = notlast ? rn : 0.0;
         // EISPACK scales (p, q, r) by |p| + |q| + |r|; the scaling only matters near under- or
         // overflow, so the range test is taken on p^2 + q^2 + r^2 (needed anyway) and the
         // abs-sum stays off the step's dependent chain (x = 1 otherwise, as before)
@@ -1072,9 +1068,17 @@ __global__ void __launch_bounds__(32 * HQ_WARPS, 1) hqrv_kernel(int nn, const do
         double is = rsqrt_hc(ss);   // 1 / s, s = sign(p) ||(p, q, r)|| (issued before the range test)
         x = 1.0;
         if (!(ss >= 1e-280 && ss <= 1e280)) {   // rare: one branch per step for every special case
+          // a skipped step hands the next one column kk of H as its (p, q, r)
+          auto skip_operands = [&]() {
+            if (kk + 1 <= n - 1) {
+              pn = Hx(kk + 1, kk);
+              qn = Hx(kk + 2, kk);
+              rn = (kk + 3 <= n) ? Hx(kk + 3, kk) : 0.0;
+            }
+          };
           if (kk != m) {
             x = fabs(p) + fabs(q) + fabs(r);
-            if (x == 0.0) continue;
+            if (x == 0.0) { skip_operands(); continue; }
             const double ix = 1.0 / x;
             p = p * ix;
             q = q * ix;
@@ -1082,17 +1086,11 @@ __global__ void __launch_bounds__(32 * HQ_WARPS, 1) hqrv_kernel(int nn, const do
             ss = p * p + q * q + r * r;
             is = rsqrt_hc(ss);
           }
-          if (ss == 0.0) continue;
+          if (ss == 0.0) { skip_operands(); continue; }
         }
         if (p < 0) is = -is;
         s = ss * is;
-        if (kk != m) {
-          Hx(kk, kk - 1) = -s * x;   // every lane the same value; read by no lane this step
-        } else if (l != m) {
-          const double hs = Hx(kk, kk - 1);
-          wp.sync();
-          Hx(kk, kk - 1) = -hs;
-        }
+        if (kk != m) Hx(kk, kk - 1) = -s * x;   // every lane the same value; read by no lane this step
 #ifdef CDMD_HQR_PROF2
         unsigned long long tb0 = clock64();
 #endif
@@ -1189,7 +1187,6 @@ __global__ void __launch_bounds__(32 * HQ_WARPS, 1) hqrv_kernel(int nn, const do
         pn = B[1][0];
         qn = B[2][0];
         rn = r30;
-        nreg = true;
         wp.sync();
 #ifdef CDMD_HQR_PROF2
         unsigned long long tb2 = clock64();
