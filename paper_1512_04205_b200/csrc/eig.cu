@@ -49,6 +49,21 @@ __device__ __forceinline__ void cdiv(double xr, double xi, double yr, double yi,
   }
 }
 
+// (x / y) complex through one reciprocal of |y|^2 (no division subroutine and its branches
+// on the inverse iteration's serial chain); Smith's algorithm where |y|^2 could underflow or
+// overflow.  rcp_hc is defined below.
+__device__ __forceinline__ double rcp_hc(double x);
+__device__ __forceinline__ void cdiv_fast(double xr, double xi, double yr, double yi, double& cr, double& ci) {
+  const double d = fma(yr, yr, yi * yi);
+  if (!(d >= 1e-280 && d <= 1e280)) {
+    cdiv(xr, xi, yr, yi, cr, ci);
+    return;
+  }
+  const double id = rcp_hc(d);
+  cr = fma(xr, yr, xi * yi) * id;
+  ci = fma(xi, yr, -(xr * yi)) * id;
+}
+
 // reciprocal and reciprocal square root: hardware approximation + two Newton steps
 // (about 1 ulp; the Francis step's scalar chain is latency-bound, IEEE division and
 // sqrt are several times longer)
@@ -1275,7 +1290,7 @@ __global__ void __launch_bounds__(32 * HI_WARPS) hinvit_kernel(int nn, const dou
     const double lr = swp ? ar : br, li = swp ? ai : bi;   // eliminated
     if (pr == 0.0 && pi == 0.0) pr = eps3;
     double cr, ci;   // multiplier l / p
-    cdiv(lr, li, pr, pi, cr, ci);
+    cdiv_fast(lr, li, pr, pi, cr, ci);
     __syncwarp();
     for (int c = k + lane; c < nn; c += 32) {
       double ur = Br[k * ld + c], ui = Bi[k * ld + c];
@@ -1324,7 +1339,7 @@ __global__ void __launch_bounds__(32 * HI_WARPS) hinvit_kernel(int nn, const dou
       double ur = Br[i * ld + i], ui = Bi[i * ld + i];
       if (ur == 0.0 && ui == 0.0) ur = eps3;
       double vr, vi;
-      cdiv(xr[i], xi[i], ur, ui, vr, vi);
+      cdiv_fast(xr[i], xi[i], ur, ui, vr, vi);
       __syncwarp();
       for (int r2 = lane; r2 < i; r2 += 32) {
         const double cr = Br[r2 * ld + i], ci = Bi[r2 * ld + i];
