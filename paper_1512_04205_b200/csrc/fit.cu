@@ -349,6 +349,7 @@ __global__ void __launch_bounds__(256) omp_kernel(
   __shared__ cplx alpha[512];
   __shared__ cplx beta[32];
   __shared__ cplx Lc[32 * 32];  // Cholesky factor of Gc[S,S]
+  __shared__ double Linv[32];   // 1 / its real diagonal (thread 0's serial chain multiplies)
   __shared__ int nS_sh, stop_sh;
   __shared__ int F[128];
   __shared__ int nF_sh;
@@ -445,10 +446,12 @@ __global__ void __launch_bounds__(256) omp_kernel(
             }
             if (a == b) {
               if (!(s.r > 0.0)) { ok = false; break; }
-              Lc[a * 32 + a] = {sqrt(s.r), 0.0};
+              const double dg = sqrt(s.r);
+              Lc[a * 32 + a] = {dg, 0.0};
+              Linv[a] = 1.0 / dg;
             } else {
-              const double d = Lc[b * 32 + b].r;
-              Lc[a * 32 + b] = {s.r / d, s.i / d};
+              const double id = Linv[b];
+              Lc[a * 32 + b] = {s.r * id, s.i * id};
             }
           }
         }
@@ -465,7 +468,7 @@ __global__ void __launch_bounds__(256) omp_kernel(
               const cplx t = cmul(Lc[a * 32 + q], z[q]);
               s.r -= t.r; s.i -= t.i;
             }
-            z[a] = {s.r / Lc[a * 32 + a].r, s.i / Lc[a * 32 + a].r};
+            z[a] = {s.r * Linv[a], s.i * Linv[a]};
           }
           for (int a = n - 1; a >= 0; --a) {  // L^H beta = z
             cplx s = z[a];
@@ -474,7 +477,7 @@ __global__ void __launch_bounds__(256) omp_kernel(
               const cplx t = cmul(lq, beta[q]);
               s.r -= t.r; s.i -= t.i;
             }
-            beta[a] = {s.r / Lc[a * 32 + a].r, s.i / Lc[a * 32 + a].r};
+            beta[a] = {s.r * Linv[a], s.i * Linv[a]};
           }
           nS_sh = n;
         }
