@@ -206,7 +206,7 @@ CDMD_API cdmd_status cdmd_sketch(cdmd_handle h, const cdmd_video* v, const cdmd_
  * CDMD_ERR_NUMERIC if the eigensolvers fail or every sigma is dropped (model->info
  * holds the solver info).  Symmetric eigensolve (the k largest pairs of Y^T Y): by
  * Lanczos with full reorthogonalisation on one 16-CTA cluster (m - 1 <= 512,
- * 2.5 k + 9 <= 144), accepted only if every Ritz pair passes the residual test (see
+ * 2.25 k + 9 <= 144), accepted only if every Ritz pair passes the residual test (see
  * cdmd_eigensolver_stats), else by the 8-CTA Householder solver (m - 1 <= 510; also for
  * k < 0, which needs every eigenvalue), else cuSOLVER's (syevdx for the k largest;
  * syevd for k < 0).

@@ -4,7 +4,7 @@
 //
 // The one-stage Householder tridiagonalisation (eigh.cu) is a chain of n - 2 dependent
 // column steps, each a trailing matvec plus cluster exchanges.  The top k eigenpairs of
-// the snapshot Gram converge in a Krylov space of about 2.5 k (measured on the c4 sketch:
+// the snapshot Gram converge in a Krylov space of about 2.2 k (measured on the c4 sketch:
 // Ritz values to 2e-13 and every Ritz vector to 1e-11 of LAPACK's after 125 steps for
 // k = 50, n = 499), so Lanczos reaches the same result in J << n steps:
 //   z = G q_j                           (G rows resident in shared memory, 32 per CTA)
@@ -67,7 +67,7 @@ template <bool BIG>
 struct LzCfg {
   static constexpr int R = BIG ? 64 : 32;      // rows per CTA (row l on CTA l % 16, slot l / 16)
   static constexpr int NMAX = LZ_CL * R;       // 512 / 1024
-  static constexpr int JM = BIG ? 288 : 144;   // Krylov dimension cap (2.5 k + 9 <= JM)
+  static constexpr int JM = BIG ? 288 : 144;   // Krylov dimension cap (2.25 k + 9 <= JM)
   static constexpr int NS = JM / LZ_CL + 1;    // slots per owner: entries c = 16 slot + owner, c <= JM
   static constexpr int AS = NS + 1;            // gathered row: the owner's slots and its sum of squares
   static constexpr int QLD = BIG ? R + 1 : R;  // row stride of qp (padded: conflict-free reassembly)
@@ -476,7 +476,7 @@ static int lz_cluster_ok() {
 static bool lz_big(int n) { return n > LzCfg<false>::NMAX; }
 
 int lz_steps(int n, int k) {
-  const int J = 5 * k / 2 + 9;
+  const int J = 9 * k / 4 + 9;   // 2.25 k + 9 (tools/lanczos_sim.py: converged by ~2.2 k + 5)
   return J < n ? J : n;
 }
 
