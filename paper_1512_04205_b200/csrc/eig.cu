@@ -779,7 +779,7 @@ __global__ void __launch_bounds__(32 * HQ_WARPS, 1) hqrv_kernel(int nn, const do
     for (int i = m + lane; i <= high; i += 32) scale += fabs(Hx(i, m - 1));
     scale = wp.sum(scale);
     if (scale == 0.0) continue;   // uniform across the CTA
-    const double isc = 1.0 / scale;
+    const double isc = rcp_hc(scale);
     double h = 0.0;
     for (int i = m + lane; i <= high; i += 32) {
       const double o = Hx(i, m - 1) * isc;
@@ -787,9 +787,10 @@ __global__ void __launch_bounds__(32 * HQ_WARPS, 1) hqrv_kernel(int nn, const do
     }
     h = wp.sum(h);
     const double om = Hx(m, m - 1) * isc;
-    const double g = om > 0 ? -sqrt(h) : sqrt(h);
+    const double sq = h * rsqrt_hc(h);   // h > 0: the column below the subdiagonal is not all zero
+    const double g = om > 0 ? -sq : sq;
     h = h - om * g;
-    const double ih = 1.0 / h;
+    const double ih = rcp_hc(h);
     __syncthreads();   // every warp has read column m - 1
     if (tid <= high - m) ort[m + tid] = tid == 0 ? om - g : Hx(m + tid, m - 1) * isc;
     __syncthreads();
@@ -847,7 +848,7 @@ __global__ void __launch_bounds__(32 * HQ_WARPS, 1) hqrv_kernel(int nn, const do
     if (hm == 0.0) continue;   // uniform
     if (tid >= 1 && tid <= high - m) ort[m + tid] = Hx(m + tid, m - 1);
     __syncthreads();
-    const double iom = 1.0 / (ort[m] * hm);
+    const double iom = rcp_hc(ort[m] * hm);
     for (int j0 = m; j0 <= high; j0 += 64) {
       const int j = j0 + tc_;
       double f0 = 0.0, f1 = 0.0;

@@ -208,36 +208,45 @@ __global__ void __launch_bounds__(256) canonicalize_kernel(
     double dt, double* __restrict__ lam_out, double* __restrict__ om_out, int32_t* __restrict__ pair_out,
     double* __restrict__ SW, int* __restrict__ dinfo) {
   __shared__ int ufirst[256], upair[256], ucol[256];
-  __shared__ double umod[256];
+  __shared__ int f0[256], p0[256];
+  __shared__ double m0[256], wsh[2 * 256];
   __shared__ int nu_sh;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  if (tid == 0) {
+  for (int i = tid; i < 2 * k && i < 2 * 256; i += blockDim.x) wsh[i] = Wc[i];   // staged once
+  __syncthreads();
+  if (tid == 0) {   // the units (a real eigenvalue or a conjugate pair), in eig's order
     int nu = 0, flags = 0;
     for (int j = 0; j < k && nu < 256;) {
-      const double re = Wc[2 * j], im = Wc[2 * j + 1];
+      const double re = wsh[2 * j], im = wsh[2 * j + 1];
       int pr = 0;
       if (im != 0.0) {
-        if (im > 0.0 && j + 1 < k && Wc[2 * j + 2] == re && Wc[2 * j + 3] == -im) pr = 1;
+        if (im > 0.0 && j + 1 < k && wsh[2 * j + 2] == re && wsh[2 * j + 3] == -im) pr = 1;
         else flags |= FLAG_EIG_PAIRING;
       }
-      ufirst[nu] = j; upair[nu] = pr; umod[nu] = hypot(re, pr ? im : 0.0); ++nu;
+      f0[nu] = j; p0[nu] = pr; m0[nu] = hypot(re, pr ? im : 0.0); ++nu;
       j += pr ? 2 : 1;
     }
-    // stable insertion sort by (|lambda| desc, real before pair)
-    for (int a = 1; a < nu; ++a) {
-      const int f = ufirst[a], pr = upair[a];
-      const double ka = umod[a];
-      int b = a - 1;
-      while (b >= 0 && !((umod[b] > ka) || (umod[b] == ka && upair[b] <= pr))) {
-        ufirst[b + 1] = ufirst[b]; upair[b + 1] = upair[b]; umod[b + 1] = umod[b];
-        --b;
-      }
-      ufirst[b + 1] = f; upair[b + 1] = pr; umod[b + 1] = ka;
-    }
-    int c = 0;
-    for (int u = 0; u < nu; ++u) { ucol[u] = c; c += upair[u] ? 2 : 1; }
     nu_sh = nu;
     if (flags) atomicOr(&dinfo[INFO_FLAGS], flags);
+  }
+  __syncthreads();
+  {  // stable order by (|lambda| desc, real before pair): each unit's rank counted in parallel
+    const int nu = nu_sh;
+    for (int a = tid; a < nu; a += blockDim.x) {
+      const double ka = isnan(m0[a]) ? -1.0 : m0[a];
+      const int pa = p0[a];
+      int rk = 0;
+      for (int b = 0; b < nu; ++b) {
+        const double kb = isnan(m0[b]) ? -1.0 : m0[b];
+        rk += (kb > ka || (kb == ka && (p0[b] < pa || (p0[b] == pa && b < a)))) ? 1 : 0;
+      }
+      ufirst[rk] = f0[a]; upair[rk] = pa;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int c = 0;
+    for (int u = 0; u < nu_sh; ++u) { ucol[u] = c; c += upair[u] ? 2 : 1; }
   }
   __syncthreads();
   const int nu = nu_sh;
