@@ -404,10 +404,11 @@ __global__ void __launch_bounds__(32 * EH_BW) eh_bisect_kernel(int n, int k, con
   const int idx = n - 1 - r;
   double lo = bounds[0], hi = bounds[1];
   const double pivmin = bounds[3];
-  const double eps = 2.220446049250313e-16;
   constexpr int NPT = 32 * BW * EH_NP;   // points per round, at lo + (hi - lo) t / (NPT + 1)
   for (int round = 0; round < 60; ++round) {
-    if (hi - lo <= 2.0 * eps * fmax(fabs(lo), fabs(hi)) + pivmin) break;   // uniform across the group
+    // stop at 2^-44 relative (sigma = sqrt(theta) to ~1e-14, far inside every use; the
+    // inverse iteration refines the vectors): one multisection round fewer than 2 eps at c4
+    if (hi - lo <= 0x1p-44 * fmax(fabs(lo), fabs(hi)) + pivmin) break;   // uniform across the group
     double x[EH_NP];
     int c[EH_NP];
 #pragma unroll
