@@ -306,15 +306,14 @@ __global__ void eh_prep_kernel(int n, const double* __restrict__ d, const double
   }
 }
 
-// reciprocal: hardware approximation + two Newton steps (about 1 ulp; the Sturm
-// recurrence is a chain of dependent divisions, IEEE division is several times longer)
+// reciprocal: hardware approximation + one third-order correction r (1 + e + e^2),
+// e = 1 - x r (about 1 ulp; used on serial chains -- the inverse iteration's LU --
+// where IEEE division is several times longer)
 __device__ __forceinline__ double eh_rcp(double x) {
   double r;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-  double t = fma(-x, r, 1.0);
-  r = fma(r, t, r);
-  t = fma(-x, r, 1.0);
-  return fma(r, t, r);
+  const double e = fma(-x, r, 1.0);
+  return fma(r, fma(e, e, e), r);
 }
 
 // Sturm counts at EH_NP points at once (independent chains interleave).
@@ -499,19 +498,21 @@ __global__ void __launch_bounds__(128) eh_invit_kernel(int n, int k, const doubl
         const double enext = (i + 1 < n - 1) ? e[i + 1] : 0.0;
         if (fabs(a) >= fabs(sub)) {
           const double piv = (a != 0.0) ? a : tiny;
-          const double mult = (a != 0.0) ? sub / a : 0.0;
+          const double ip = eh_rcp(piv);   // the chain multiplies by it (no division subroutine)
+          const double mult = (a != 0.0) ? sub * ip : 0.0;
           pv[i] = 0;
           lm[i] = mult;
-          ui[i] = 1.0 / piv;
+          ui[i] = ip;
           u1[i] = b;
           u2[i] = 0.0;
           a = dnext - mult * b;
           b = enext;
         } else {
-          const double mult = a / sub;
+          const double ip = eh_rcp(sub);
+          const double mult = a * ip;
           pv[i] = 1;
           lm[i] = mult;
-          ui[i] = 1.0 / sub;
+          ui[i] = ip;
           u1[i] = dnext;
           u2[i] = enext;
           a = b - mult * dnext;
