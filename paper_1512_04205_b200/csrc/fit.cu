@@ -419,25 +419,26 @@ __global__ void __launch_bounds__(256) omp_kernel(
       sc[j] = score;
       best = fmax(best, score);
     }
-    red[tid] = best;
+    // max score and the lowest index within the tie band: warp shuffles, then one value per
+    // warp (two block barriers per iteration instead of a 256-wide tree each)
+    const int nwarp = (int)(blockDim.x >> 5), wl = tid & 31, wi = tid >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) best = fmax(best, __shfl_xor_sync(0xffffffffu, best, o));
+    if (wl == 0) red[wi] = best;
     __syncthreads();
-    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
-      if (tid < o) red[tid] = fmax(red[tid], red[tid + o]);
-      __syncthreads();
-    }
-    const double bmax = red[0];
-    __syncthreads();
+    double bmax = red[0];
+    for (int w = 1; w < nwarp; ++w) bmax = fmax(bmax, red[w]);
     int cand = 1 << 30;
     for (int j = tid; j < k; j += blockDim.x)
       if (sc[j] >= bmax * (1.0 - TIE_RTOL) && j < cand) cand = j;
-    redi[tid] = cand;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) cand = min(cand, __shfl_xor_sync(0xffffffffu, cand, o));
+    if (wl == 0) redi[wi] = cand;
     __syncthreads();
-    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
-      if (tid < o) redi[tid] = min(redi[tid], redi[tid + o]);
-      __syncthreads();
-    }
     if (tid == 0) {
-      const int js = by_freq ? T[it] : redi[0];
+      int jbest = redi[0];
+      for (int w = 1; w < nwarp; ++w) jbest = min(jbest, redi[w]);
+      const int js = by_freq ? T[it] : jbest;
       if ((!by_freq && (!(bmax > 0.0) || !isfinite(bmax))) || js >= k || nS >= 32) {
         stop_sh = 1;
       } else {
