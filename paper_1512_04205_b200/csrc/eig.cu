@@ -738,7 +738,10 @@ constexpr int HQ_WARPS = 8;   // warps of hqrv_kernel: all reduce to Hessenberg 
 template <bool BIG>   // BIG: more than 64 rows (slots beyond two per lane in the bulge step)
 __global__ void __launch_bounds__(32 * HQ_WARPS, 1) hqrv_kernel(int nn, const double* __restrict__ A,
                                                             double* __restrict__ W, double* __restrict__ H0,
-                                                            double* __restrict__ Qout, int* __restrict__ info) {
+                                                            double* __restrict__ Qout, int* __restrict__ info,
+                                                            int ovl) {
+  // ovl: the shared block also holds a copy R of H after orthes and a separate scratch
+  // block, so warps 4..7 accumulate Q (ortran, from R) while warp 0 already runs hqr
   extern __shared__ double sm[];
   const int ld = nn + 1;
   double* H = sm;                 // nn x ld, row-major
@@ -841,6 +844,51 @@ __global__ void __launch_bounds__(32 * HQ_WARPS, 1) hqrv_kernel(int nn, const do
     __syncthreads();
   }
   HQ_TICK(0);
+  if (ovl) {
+    double* R = part + 256;          // nn x ld: H as orthes left it (ortran's reflectors)
+    double* scr2 = R + nn * ld;      // 3 ld + 80: hqr's scratch block
+    for (int idx = tid; idx < nn * nn; idx += NT) {
+      const int i = idx / nn, j = idx % nn;
+      const double h = Hx(i, j);
+      H0[idx] = (i > j + 1) ? 0.0 : h;
+      R[i * ld + j] = h;
+    }
+    for (int i = tid; i < 3 * ld + 80; i += NT) scr2[i] = 0.0;
+    __syncthreads();
+    if (warp >= 4) {   // ortran on 128 threads (32 columns x 4 slices), named barrier 1
+      const int t = tid - 128, tc = t & 31, ts = t >> 5;
+      for (int m = high - 1; m >= low + 1; --m) {
+        const double hm = R[m * ld + m - 1];
+        if (hm == 0.0) continue;   // uniform
+        if (t >= 1 && t <= high - m) ort[m + t] = R[(m + t) * ld + m - 1];
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        const double iom = rcp_hc(ort[m] * hm);
+        for (int j0 = m; j0 <= high; j0 += 32) {
+          const int j = j0 + tc;
+          double f0 = 0.0, f1 = 0.0;
+          if (j <= high) {
+            int i = m + ts;
+            for (; i + 4 <= high; i += 8) {
+              f0 = fma(ort[i], Vx(i, j), f0);
+              f1 = fma(ort[i + 4], Vx(i + 4, j), f1);
+            }
+            if (i <= high) f0 = fma(ort[i], Vx(i, j), f0);
+            part[ts * 32 + tc] = f0 + f1;
+          }
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          if (j <= high) {
+            const double f = ((part[tc] + part[32 + tc]) + (part[64 + tc] + part[96 + tc])) * iom;
+            for (int i = m + ts; i <= high; i += 4) Vx(i, j) += f * ort[i];
+          }
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+        }
+      }
+      for (int idx = t; idx < nn * nn; idx += 128) Qout[idx] = Vx(idx / nn, idx % nn);
+      return;
+    }
+    if (warp != 0) return;
+    scr = scr2;
+  } else {
   // ortran: Q explicitly, V(:, j) += g_j u with g_j = u' V(:, j) / (u_m H(m, m-1)),
   // the same (column, slice) thread map
   for (int m = high - 1; m >= low + 1; --m) {
@@ -880,6 +928,7 @@ __global__ void __launch_bounds__(32 * HQ_WARPS, 1) hqrv_kernel(int nn, const do
   for (int i = tid; i < 3 * ld + 80; i += NT) scr[i] = 0.0;
   __syncthreads();
   if (warp != 0) return;   // hqr below is one warp's: no CTA barrier after this point
+  }
   // ------------------------------------------------------- hqr (values only)
   int n = nn - 1;
   const double eps = 0x1p-52;
@@ -1399,8 +1448,11 @@ cudaError_t launch_hqr_eig(int k, const double* A, double* W, double* VR, int* i
     auto kern = k > 64 ? hqrv_kernel<true> : hqrv_kernel<false>;
     cudaError_t e = smem_optin(reinterpret_cast<const void*>(kern));
     if (e != cudaSuccess) return e;
+    // Q accumulated beside hqr when the copy of H and a separate scratch block fit
+    const size_t smem_ovl = smem + sizeof(double) * ((size_t)k * (k + 1) + 3 * ((size_t)k + 1) + 80);
+    const int ovl = (smem_ovl <= 226 * 1024 && !getenv("CDMD_HQR_SEQ")) ? 1 : 0;
     note_launch();
-    kern<<<1, 32 * HQ_WARPS, smem, st>>>(k, A, W, H0, Q, info);
+    kern<<<1, 32 * HQ_WARPS, ovl ? smem_ovl : smem, st>>>(k, A, W, H0, Q, info, ovl);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     // a warp per eigenvalue, HI_WARPS to a CTA when their shared slices fit (fewer SMs held
     // while the streaming lanes' passes run)
